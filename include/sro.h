@@ -1,0 +1,162 @@
+/* sro.h — C-ABI of the B200-native hot path of block-coordinate Frank-Wolfe
+ * for convex semi-relaxed optimal transport (arXiv 2103.05857).
+ *
+ * Problem (Eq. 7):
+ *     minimize_{T >= 0, T^T 1_m = b}  f(T) = <T, C> + 1/(2 lambda) ||T 1_n - a||^2
+ * over the Cartesian product of scaled simplices b_1 Delta_m x ... x b_n Delta_m
+ * (Eq. 8). Column i of T is the block t_i; its gradient is
+ * grad_i f = c_i + h with the shared vector h = (T 1_n - a)/lambda.
+ *
+ * Every entry point returns an sro_status; no exception crosses the ABI.
+ * sro_last_error(h) returns a human-readable message for the last failure.
+ * All arrays are plain pointers with explicit sizes; no torch types.
+ *
+ * Precision: SRO_FP64 evaluates C (or the colour costs) in binary64.
+ * SRO_FP32 stores / evaluates C in binary32 and promotes it to binary64 before
+ * adding h; every reduction, line search and update is binary64 in both modes.
+ * The arithmetic of every step is fixed operation by operation (DESIGN.md §3,
+ * readings R1-R22), so a run is bitwise reproducible and matches the oracle.
+ *
+ * Threading: a handle is single-writer. Distinct handles may run concurrently
+ * on distinct CUDA streams.
+ */
+#ifndef SRO_H
+#define SRO_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sro_solver* sro_handle;
+
+typedef enum {
+  SRO_OK = 0,
+  SRO_NOT_CONVERGED = 1,   /* iteration budget exhausted with gap > epsilon (not an error) */
+  SRO_ERR_INVALID_ARG = 2, /* bad pointer, size, option combination or layout */
+  SRO_ERR_DIMENSION = 3,   /* m, n out of range */
+  SRO_ERR_MARGINALS = 4,   /* a or b negative, non-finite, or not summing to 1 within 1e-12 */
+  SRO_ERR_NONFINITE = 5,   /* non-finite cost / value met; state left at the last finite iterate */
+  SRO_ERR_CAPACITY = 6,    /* a column support would exceed slab_cap; state left before that step */
+  SRO_ERR_CUDA = 7,        /* CUDA runtime error (message in sro_last_error) */
+  SRO_ERR_NCCL = 8,        /* multi-rank exchange failed */
+  SRO_ERR_OOM = 9,         /* device allocation failed */
+  SRO_ERR_STATE = 10       /* sro_solve called with a different variant/options/seed without sro_reset */
+} sro_status;
+
+/* Cost representation. C_{k,i} is the cost of moving source bin k (row, k < m)
+ * to target bin i (column, i < n).                                           */
+typedef enum {
+  SRO_COST_DENSE = 0,         /* C column-major: element (k,i) at data[i*ld + k], ld >= m */
+  SRO_COST_SQEUCLID = 1,      /* colours: C_ki = ((dx*dx + dy*dy) + dz*dz), d = x_k - y_i (BASELINE configs) */
+  SRO_COST_EUCLID = 2,        /* colours: C_ki = sqrt(...) */
+  SRO_COST_HASH_UNIFORM = 3   /* C_ki = (splitmix64(seed + (i*m + k + 1) * 0x9E3779B97F4A7C15) >> 40) * 2^-24,
+                                 iid uniform on [0,1), exact in binary32; materialised on the device
+                                 (BASELINE config [3]) */
+} sro_cost_kind;
+
+typedef enum { SRO_FP64 = 0, SRO_FP32 = 1 } sro_precision;
+
+typedef struct {
+  int32_t kind;         /* sro_cost_kind */
+  int32_t prec;         /* sro_precision: element type of data / x / y */
+  const void* data;     /* DENSE: m x n column-major, element type by prec */
+  int64_t ld;           /* DENSE: leading dimension (elements), >= m */
+  const void* x;        /* SQEUCLID/EUCLID: source colours, x[3k + d], d = 0..2 */
+  const void* y;        /* SQEUCLID/EUCLID: target colours, y[3i + d] */
+  uint64_t hash_seed;   /* HASH_UNIFORM */
+  int32_t data_on_device; /* 0: host pointers, copied at sro_create.
+                             1: device pointers, BORROWED (must outlive the handle);
+                             DENSE requires 16-byte aligned data and ld*elem % 16 == 0 */
+} sro_cost;
+
+typedef struct {
+  int32_t m, n;         /* rows (source bins), columns (target bins), each >= 1 */
+  double lambda;        /* relaxation parameter (Eq. 7), finite and > 0 */
+  int32_t slab_cap;     /* per-column support capacity (<= 31; 0 -> default 31) */
+  int32_t device;       /* CUDA device ordinal */
+  void* cuda_stream;    /* cudaStream_t to run on (NULL -> a stream owned by the handle) */
+} sro_params;
+
+typedef enum { SRO_FW = 0, SRO_BCFW = 1, SRO_BCAFW = 2, SRO_BCPFW = 3, SRO_BATCHED = 4 } sro_variant;
+typedef enum { SRO_STEP_DEC = 0, SRO_STEP_ELS = 1 } sro_step;
+typedef enum { SRO_SAMPLE_U = 0, SRO_SAMPLE_P = 1, SRO_SAMPLE_GA = 2 } sro_sampling;
+
+/* One per-step record (optional; tests compare it with the oracle's trace). */
+typedef struct {
+  int64_t k;            /* step counter before the step */
+  int32_t i;            /* column (first column of U for block steps) */
+  int32_t j;            /* LMO argmin row of column i (Eq. 9) */
+  int32_t v;            /* away / pairwise atom row (Eq. 13), -1 if none */
+  int32_t dir;          /* 0 FW direction, 1 away, 2 pairwise, 3 no-op */
+  double gamma, num, den, minval;
+} sro_trace_rec;
+
+typedef struct {
+  int32_t step;           /* sro_step */
+  int32_t sampling;       /* sro_sampling (BCFW family and batched; ignored by FW) */
+  double epsilon;         /* stop at the first gap check with g <= epsilon */
+  int32_t gap_period;     /* epochs between gap checks (>= 1) */
+  int32_t ga_M;           /* GA: global refresh of all column gaps every M*n steps (>= 1) */
+  int32_t ga_inner;       /* GA: 1 = refresh the visited column's gap each step (GAD), 0 = GAS */
+  int32_t ga_post_update; /* GA: 1 = store g_i(T^{k+1}), 0 = g_i(T^k) */
+  int32_t block_size;     /* BATCHED: columns per block B (B divides n) */
+  const int32_t* visit;   /* optional host array of explicit visits (columns, or block indices for
+                             BATCHED), length >= iters; NULL -> the sampling rule */
+  sro_trace_rec* trace;   /* optional host array receiving one record per step, length >= iters */
+} sro_options;
+
+typedef struct {
+  int64_t iters_done;     /* steps performed by this call */
+  int64_t k;              /* global step counter after the call */
+  double gap;             /* last evaluated duality gap g(T) (NaN if none) */
+  double objective;       /* f(T) at the end of the call */
+  int32_t converged;      /* 1 if a gap check met epsilon */
+  int32_t gap_checks;     /* gap evaluations in this call */
+  int64_t entries_scanned;/* cost entries read by LMO calls in this call (steps + sweeps) */
+  double device_ms;       /* device time of the call (CUDA events on the solver stream) */
+} sro_result;
+
+/* Create a solver. a: host fp64[m] (source marginal), b: host fp64[n] (target
+ * marginal), copied. cost as described above. T starts at the first-row
+ * vertex T^(0) = (b_1 e_1, ..., b_n e_1).
+ * Errors: INVALID_ARG, DIMENSION, MARGINALS, NONFINITE, OOM, CUDA. */
+sro_status sro_create(const double* a, const double* b, const sro_cost* cost, const sro_params* params,
+                      sro_handle* out);
+
+/* Run `iters` steps of `variant` (Alg. 1 / A.1-A.4, PAPER.md P:189-227,
+ * P:1765-1869; BATCHED is the super-block FW step of DESIGN.md R18),
+ * continuing from the handle's state. Gap checks at epoch boundaries
+ * and, for FW, every iteration. seed selects the sampling
+ * stream. Returns OK (converged), NOT_CONVERGED (budget spent) or an error.
+ * Two calls with iters a and b equal one call with a + b. */
+sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* opts, int64_t iters, uint64_t seed,
+                     sro_result* out);
+
+/* Duality gap g(T) (Thm 2) as sum_i g_i (Eq. 11).
+ * per_column: host fp64[n] or NULL; argmin_rows: host int32[n] or NULL. */
+sro_status sro_gap(sro_handle h, double* total, double* per_column, int32_t* argmin_rows);
+
+/* Objective f(T) (Eq. 7). */
+sro_status sro_objective(sro_handle h, double* f);
+
+/* Plan export. dense_colmajor: host fp64[m*n] or NULL. COO triplets (rows, cols,
+ * vals; host, capacity cap) may be NULL; *nnz receives the number of nonzeros
+ * (COO is written column by column, rows ascending). */
+sro_status sro_get_plan(sro_handle h, double* dense_colmajor, int32_t* rows, int32_t* cols, double* vals,
+                        int64_t cap, int64_t* nnz);
+
+/* Row sums r = T 1_n as maintained by the solver (host fp64[m]). */
+sro_status sro_get_rowsums(sro_handle h, double* r);
+
+/* Back to T^(0), k = 0; clears the variant/options/seed lock. */
+sro_status sro_reset(sro_handle h);
+
+void sro_destroy(sro_handle h);
+const char* sro_last_error(sro_handle h);
+const char* sro_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -141,7 +141,7 @@ def make_options(step=ELS, sampling=U, epsilon=1e-6, gap_period=1, ga_M=1, ga_in
 class Oracle:
     """One oracle instance (problem + plan state)."""
 
-    def __init__(self, a, b, lam, *, C=None, X=None, Y=None, cost="dense", hash_seed=0, cap=64):
+    def __init__(self, a, b, lam, *, C=None, X=None, Y=None, cost="dense", prec="f64", hash_seed=0, cap=64):
         L = _L()
         self.a = np.ascontiguousarray(a, dtype=np.float64)
         self.b = np.ascontiguousarray(b, dtype=np.float64)
@@ -149,6 +149,12 @@ class Oracle:
         self.lam = float(lam)
         self.cap = cap
         kind = {"dense": COST_DENSE, "sqeuclid": COST_SQEUCLID, "euclid": COST_EUCLID, "hash": COST_HASH}[cost]
+        if prec == "f32" and kind in (COST_SQEUCLID, COST_EUCLID):
+            kind += 3            # colours evaluated in binary32 (OR_COST_*_F32)
+            X = np.asarray(X, dtype=np.float32).astype(np.float64)
+            Y = np.asarray(Y, dtype=np.float32).astype(np.float64)
+        elif prec == "f32" and kind == COST_DENSE:
+            C = np.asarray(C, dtype=np.float32).astype(np.float64)
         Cc = Xc = Yc = None
         ld = self.m
         if kind == COST_DENSE:
@@ -156,7 +162,7 @@ class Oracle:
             Cc = np.asfortranarray(np.asarray(C, dtype=np.float64))
             assert Cc.shape == (self.m, self.n)
             Cc = Cc.T.copy()  # n x m C-order == column-major m x n
-        elif kind in (COST_SQEUCLID, COST_EUCLID):
+        elif kind != COST_HASH:
             Xc = np.ascontiguousarray(X, dtype=np.float64)
             Yc = np.ascontiguousarray(Y, dtype=np.float64)
         st = ct.c_int(0)

@@ -135,6 +135,16 @@ static double cost(const or_state* s, int32_t k, int32_t i) {
   switch (s->cost_kind) {
     case OR_COST_DENSE:
       return s->C[(int64_t)i * s->ld + k];
+    case OR_COST_SQEUCLID_F32:
+    case OR_COST_EUCLID_F32: {
+      /* binary32 colours evaluated in binary32 arithmetic, same operation
+       * order, promoted exactly to binary64 (BASELINE "fp32" configs, R10) */
+      float dx = (float)s->X[3 * (int64_t)k + 0] - (float)s->Y[3 * (int64_t)i + 0];
+      float dy = (float)s->X[3 * (int64_t)k + 1] - (float)s->Y[3 * (int64_t)i + 1];
+      float dz = (float)s->X[3 * (int64_t)k + 2] - (float)s->Y[3 * (int64_t)i + 2];
+      float d2 = ((dx * dx) + (dy * dy)) + (dz * dz);
+      return s->cost_kind == OR_COST_EUCLID_F32 ? (double)sqrtf(d2) : (double)d2;
+    }
     case OR_COST_SQEUCLID:
     case OR_COST_EUCLID: {
       double dx = s->X[3 * (int64_t)k + 0] - s->Y[3 * (int64_t)i + 0];
@@ -249,7 +259,7 @@ or_state* or_create(int32_t m, int32_t n, double lambda, const double* a, const 
                     uint64_t hash_seed, int32_t cap, int* status) {
   *status = OR_ERR_ARG;
   if (m < 1 || n < 1 || !(lambda > 0.0) || !isfinite(lambda) || cap < 1 || !a || !b) return NULL;
-  if (cost_kind < OR_COST_DENSE || cost_kind > OR_COST_HASH) return NULL;
+  if (cost_kind < OR_COST_DENSE || cost_kind > OR_COST_EUCLID_F32) return NULL;
   or_state* s = (or_state*)calloc(1, sizeof(or_state));
   if (!s) return NULL;
   s->m = m; s->n = n; s->lambda = lambda; s->cost_kind = cost_kind; s->cap = cap;
@@ -264,7 +274,7 @@ or_state* or_create(int32_t m, int32_t n, double lambda, const double* a, const 
     s->C = (double*)malloc(sizeof(double) * (size_t)m * (size_t)n);
     if (!s->C) { free_state(s); return NULL; }
     for (int32_t i = 0; i < n; i++) memcpy(s->C + (int64_t)i * m, C + (int64_t)i * ld, sizeof(double) * m);
-  } else if (cost_kind == OR_COST_SQEUCLID || cost_kind == OR_COST_EUCLID) {
+  } else if (cost_kind != OR_COST_HASH) {
     if (!X || !Y) { free_state(s); return NULL; }
     s->X = (double*)malloc(sizeof(double) * 3 * (size_t)m);
     s->Y = (double*)malloc(sizeof(double) * 3 * (size_t)n);
@@ -274,7 +284,8 @@ or_state* or_create(int32_t m, int32_t n, double lambda, const double* a, const 
   /* validation: a, b >= 0 summing to 1 within 1e-12; C finite, >= 0 */
   double sa = 0.0, sb = 0.0;
   for (int32_t k = 0; k < m; k++) { if (!(a[k] >= 0.0) || !isfinite(a[k])) { free_state(s); *status = 4; return NULL; } sa = sa + a[k]; }
-  for (int32_t i = 0; i < n; i++) { if (!(b[i] >= 0.0) || !isfinite(b[i])) { free_state(s); *status = 4; return NULL; } sb = sb + b[i]; }
+  /* b_i > 0: every block b_i Delta_m is a proper simplex (Eq. 8) */
+  for (int32_t i = 0; i < n; i++) { if (!(b[i] > 0.0) || !isfinite(b[i])) { free_state(s); *status = 4; return NULL; } sb = sb + b[i]; }
   if (fabs(sa - 1.0) > 1e-12 || fabs(sb - 1.0) > 1e-12) { free_state(s); *status = 4; return NULL; }
   if (cost_kind == OR_COST_DENSE) {
     for (int64_t q = 0; q < (int64_t)m * n; q++)

@@ -19,7 +19,8 @@ extern "C" {
 #endif
 
 enum { OR_OK = 0, OR_NOT_CONVERGED = 1, OR_ERR_ARG = 2, OR_ERR_NONFINITE = 5, OR_ERR_CAPACITY = 6, OR_ERR_STATE = 10 };
-enum { OR_COST_DENSE = 0, OR_COST_SQEUCLID = 1, OR_COST_EUCLID = 2, OR_COST_HASH = 3 };
+enum { OR_COST_DENSE = 0, OR_COST_SQEUCLID = 1, OR_COST_EUCLID = 2, OR_COST_HASH = 3,
+       OR_COST_SQEUCLID_F32 = 4, OR_COST_EUCLID_F32 = 5 };
 enum { OR_FW = 0, OR_BCFW = 1, OR_BCAFW = 2, OR_BCPFW = 3, OR_BATCHED = 4 };
 enum { OR_STEP_DEC = 0, OR_STEP_ELS = 1 };
 enum { OR_SAMPLE_U = 0, OR_SAMPLE_P = 1, OR_SAMPLE_GA = 2 };

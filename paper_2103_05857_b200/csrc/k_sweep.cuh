@@ -1,0 +1,214 @@
+// k_sweep.cuh — the column LMO sweep (Eq. 9) fused with
+// the per-column duality-gap epilogue (Eq. 11).
+//
+// For a contiguous column range [col0, col0 + L): j_p = argmin_k (C_{k,i} + h_k)
+// (lowest k on ties), minval_p, and g_p = <t_i, c_i + h> - b_i minval_p.
+//
+// Layout: C column-major (each LMO is one contiguous, 128-bit vectorised,
+// coalesced column read, BASELINE north_star), h staged per row slab in
+// shared memory and reused by every column the CTA visits. One warp owns one
+// column at a time; a CTA of 8 warps streams many columns. Rows are split in
+// slabs of at most SLAB rows (blockIdx.y); with more than one slab the
+// per-slab (min, row) partials are merged in slab order by k_lmo_merge.
+// Roofline: HBM (dense, 4 or 8 B per entry) or FP32/FP64 issue (colours).
+#pragma once
+#include "sro_device.cuh"
+
+namespace sro {
+
+constexpr int SWEEP_THREADS = 256;
+constexpr int SWEEP_WARPS = SWEEP_THREADS / 32;
+constexpr int SLAB = 8192;
+
+__device__ __forceinline__ float4 ld_stream(const float4* p) { return __ldcs(p); }
+__device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
+
+// --------------------------------------------------------------------------
+// Cost sources
+// --------------------------------------------------------------------------
+template <typename T> struct Vec;
+template <> struct Vec<float> { using type = float4; static constexpr int W = 4; };
+template <> struct Vec<double> { using type = double2; static constexpr int W = 2; };
+
+__device__ __forceinline__ void proc4(const float4& v, int k, const double* hs, double& best, int& bj) {
+  double x0 = d_add((double)v.x, hs[k]), x1 = d_add((double)v.y, hs[k + 1]);
+  double x2 = d_add((double)v.z, hs[k + 2]), x3 = d_add((double)v.w, hs[k + 3]);
+  if (x0 < best) { best = x0; bj = k; }
+  if (x1 < best) { best = x1; bj = k + 1; }
+  if (x2 < best) { best = x2; bj = k + 2; }
+  if (x3 < best) { best = x3; bj = k + 3; }
+}
+__device__ __forceinline__ void proc4(const double2& v, int k, const double* hs, double& best, int& bj) {
+  double x0 = d_add(v.x, hs[k]), x1 = d_add(v.y, hs[k + 1]);
+  if (x0 < best) { best = x0; bj = k; }
+  if (x1 < best) { best = x1; bj = k + 1; }
+}
+
+template <typename T>
+struct SrcDense {
+  const T* C;
+  int64_t ld;
+  static constexpr int SMEM_PER_ROW = 0;
+  __device__ __forceinline__ void stage(int, int, char*) const {}
+  __device__ __forceinline__ double cost(int k, int i) const { return (double)C[(int64_t)i * ld + k]; }
+  // Scan rows [row0, row0+rows) of column i; lane-strided 128-bit vectors,
+  // rows ascending within a lane. hs is the slab of h (index k - row0).
+  __device__ __forceinline__ void scan(int i, int row0, int rows, const double* hs, const char*, double& best,
+                                       int& bj) const {
+    using V = typename Vec<T>::type;
+    constexpr int W = Vec<T>::W;
+    const int lane = threadIdx.x & 31;
+    const V* p = reinterpret_cast<const V*>(C + (int64_t)i * ld + row0);
+    const int nvec = rows / W;
+    int q = lane;
+    for (; q + 96 < nvec; q += 128) {
+      V a = ld_stream(p + q), b = ld_stream(p + q + 32), c = ld_stream(p + q + 64), d = ld_stream(p + q + 96);
+      proc4(a, W * q, hs, best, bj);
+      proc4(b, W * (q + 32), hs, best, bj);
+      proc4(c, W * (q + 64), hs, best, bj);
+      proc4(d, W * (q + 96), hs, best, bj);
+    }
+    for (; q < nvec; q += 32) proc4(ld_stream(p + q), W * q, hs, best, bj);
+    const int k = nvec * W + lane;
+    if (k < rows) {
+      double x = d_add((double)C[(int64_t)i * ld + row0 + k], hs[k]);
+      if (x < best) { best = x; bj = k; }
+    }
+    // bj is slab-relative here; caller adds row0
+  }
+};
+
+template <typename T, bool EUCLID>
+struct SrcColour {
+  const T* x;   // 3m
+  const T* y;   // 3n
+  static constexpr int SMEM_PER_ROW = 3 * sizeof(T);
+  __device__ __forceinline__ void stage(int row0, int rows, char* sm) const {
+    T* xs = reinterpret_cast<T*>(sm);
+    for (int k = threadIdx.x; k < rows; k += blockDim.x) {
+      xs[k] = x[3 * (int64_t)(row0 + k)];
+      xs[rows + k] = x[3 * (int64_t)(row0 + k) + 1];
+      xs[2 * rows + k] = x[3 * (int64_t)(row0 + k) + 2];
+    }
+  }
+  __device__ __forceinline__ double cost(int k, int i) const {
+    return colour_cost<EUCLID>(x[3 * (int64_t)k], x[3 * (int64_t)k + 1], x[3 * (int64_t)k + 2], y[3 * (int64_t)i],
+                               y[3 * (int64_t)i + 1], y[3 * (int64_t)i + 2]);
+  }
+  __device__ __forceinline__ void scan(int i, int row0, int rows, const double* hs, const char* sm, double& best,
+                                       int& bj) const {
+    const T* xs = reinterpret_cast<const T*>(sm);
+    const T y0 = y[3 * (int64_t)i], y1 = y[3 * (int64_t)i + 1], y2 = y[3 * (int64_t)i + 2];
+    const int lane = threadIdx.x & 31;
+#pragma unroll 4
+    for (int k = lane; k < rows; k += 32) {
+      double c = colour_cost<EUCLID>(xs[k], xs[rows + k], xs[2 * rows + k], y0, y1, y2);
+      double v = d_add(c, hs[k]);
+      if (v < best) { best = v; bj = k; }
+    }
+  }
+};
+
+// Per-column gap epilogue (Eq. 11): lanes hold one support entry each;
+// dot = sequential sum over supp(t_i), rows ascending (R19).
+template <class Src>
+__device__ __forceinline__ double column_gap_epilogue(const Src& src, int i, double minval, const int* __restrict__ cnt,
+                                                      const int* __restrict__ srow, const double* __restrict__ sval,
+                                                      int cap, const double* __restrict__ b,
+                                                      const double* __restrict__ h) {
+  const int lane = threadIdx.x & 31;
+  const int c = cnt[i];
+  double term = 0.0;
+  if (lane < c) {
+    const int k = srow[(int64_t)i * cap + lane];
+    const double t = sval[(int64_t)i * cap + lane];
+    term = d_mul(t, d_add(src.cost(k, i), h[k]));
+  }
+  const double dot = warp_seq_sum(term, c);
+  return d_sub(dot, d_mul(b[i], minval));
+}
+
+struct SweepOut {
+  int* j;          // [L] final rows (single slab) or partial rows [nslabs*L]
+  double* minval;  // [L] or partial [nslabs*L]
+  double* g;       // [L] column gaps (single slab only)
+};
+
+// grid = (gx, nslabs). col0 = col0_dev ? *col0_dev * col0_mul : col0_host.
+template <class Src>
+__global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_sweep(Src src, int m, const double* __restrict__ h,
+                                                             const int* __restrict__ col0_dev, int col0_mul,
+                                                             int col0_host, int L, const int* __restrict__ cnt,
+                                                             const int* __restrict__ srow,
+                                                             const double* __restrict__ sval, int cap,
+                                                             const double* __restrict__ b, SweepOut out,
+                                                             const int* __restrict__ stop, int* status) {
+  if (stop && *stop) return;
+  extern __shared__ __align__(16) double sm_h[];
+  const int nslabs = gridDim.y, slab = blockIdx.y;
+  const int row0 = slab * SLAB;
+  const int rows = min(SLAB, m - row0);
+  for (int k = threadIdx.x; k < rows; k += blockDim.x) sm_h[k] = h[row0 + k];
+  char* sm_src = reinterpret_cast<char*>(sm_h + ((rows + 1) & ~1));
+  src.stage(row0, rows, sm_src);
+  __syncthreads();
+  const int col0 = col0_dev ? (*col0_dev) * col0_mul : col0_host;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int p = blockIdx.x * SWEEP_WARPS + warp; p < L; p += gridDim.x * SWEEP_WARPS) {
+    const int i = col0 + p;
+    double best = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+    int bj = 0x7fffffff;
+    src.scan(i, row0, rows, sm_h, sm_src, best, bj);
+    if (bj != 0x7fffffff) bj += row0;
+    warp_argmin(best, bj);
+    if (nslabs == 1) {
+      if (!(best < 1.0e308 && best > -1.0e308)) { if (lane == 0) set_status(status, 5); }
+      const double g = column_gap_epilogue(src, i, best, cnt, srow, sval, cap, b, h);
+      if (lane == 0) { out.j[p] = bj; out.minval[p] = best; out.g[p] = g; }
+    } else if (lane == 0) {
+      out.j[(int64_t)slab * L + p] = bj;
+      out.minval[(int64_t)slab * L + p] = best;
+    }
+  }
+}
+
+// Merge per-slab partials in slab order and apply the gap epilogue. One warp per column.
+template <class Src>
+__global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_merge(Src src, int nslabs, const double* __restrict__ h,
+                                                             const int* __restrict__ col0_dev, int col0_mul,
+                                                             int col0_host, int L, const int* __restrict__ cnt,
+                                                             const int* __restrict__ srow,
+                                                             const double* __restrict__ sval, int cap,
+                                                             const double* __restrict__ b, const int* __restrict__ pj,
+                                                             const double* __restrict__ pmin, int* out_j,
+                                                             double* out_min, double* out_g,
+                                                             const int* __restrict__ stop, int* status) {
+  if (stop && *stop) return;
+  const int col0 = col0_dev ? (*col0_dev) * col0_mul : col0_host;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int p = blockIdx.x * SWEEP_WARPS + warp; p < L; p += gridDim.x * SWEEP_WARPS) {
+    double best = __longlong_as_double(0x7ff0000000000000LL);
+    int bj = 0x7fffffff;
+    for (int s = lane; s < nslabs; s += 32) argmin_merge(best, bj, pmin[(int64_t)s * L + p], pj[(int64_t)s * L + p]);
+    warp_argmin(best, bj);
+    if (!(best < 1.0e308 && best > -1.0e308)) { if (lane == 0) set_status(status, 5); }
+    const double g = column_gap_epilogue(src, col0 + p, best, cnt, srow, sval, cap, b, h);
+    if (lane == 0) { out_j[p] = bj; out_min[p] = best; out_g[p] = g; }
+  }
+}
+
+// psum256 of x[0..L) -> *out (one CTA of 256 threads). If stop_eps is given,
+// sets *stop = (total <= eps) (FW stop check, Alg. A.1 line 4).
+__global__ void __launch_bounds__(256) k_psum256(const double* __restrict__ x, int64_t L, double* out,
+                                                 const double* __restrict__ eps, int* stop_flag,
+                                                 const int* __restrict__ stop_in) {
+  if (stop_in && *stop_in) return;
+  __shared__ double red[8];
+  double v = block_psum256(x, L, red);
+  if (threadIdx.x == 0) {
+    *out = v;
+    if (stop_flag && eps) { if (v <= *eps) *stop_flag = 1; }
+  }
+}
+
+}  // namespace sro

@@ -1,0 +1,827 @@
+// sro_api.cu — C-ABI (include/sro.h) and host runtime of the B200 hot path.
+//
+// The host side only validates arguments, owns device memory, generates the
+// column-visit order from the counter-based SplitMix64 stream (R21-R22) and
+// sequences kernels on the solver stream; every step of the method runs in
+// the kernels of k_sweep.cuh, k_bcfw.cuh and k_block.cuh.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sro.h"
+#include "k_bcfw.cuh"
+#include "k_block.cuh"
+#include "k_sweep.cuh"
+#include "sro_device.cuh"
+
+using namespace sro;
+
+namespace {
+
+struct Solver {
+  int m = 0, n = 0, cap = 31, device = 0;
+  double lambda = 1.0;
+  int kind = 0, prec = 0, borrowed = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::string err;
+  // problem
+  double *a = nullptr, *b = nullptr;
+  void* C = nullptr;     // dense (fp32 or fp64), ld elements
+  int64_t ld = 0;
+  void* x = nullptr;     // colours
+  void* y = nullptr;
+  bool owns_cost = false;
+  // state
+  double *r = nullptr, *h = nullptr;
+  int *cnt = nullptr, *srow = nullptr;
+  double* sval = nullptr;
+  long long k = 0;
+  bool configured = false;
+  int variant = -1;
+  sro_options opt{};
+  uint64_t seed = 0;
+  // GA
+  double *G = nullptr, *fen = nullptr;
+  // scratch
+  int* status = nullptr;      // device status word
+  int* steps_done = nullptr;
+  int* stop = nullptr;
+  double* scal = nullptr;     // 8 device scalars
+  double* epsd = nullptr;
+  int* visit = nullptr;
+  int64_t visit_cap = 0;
+  double* trace = nullptr;
+  int64_t trace_cap = 0;
+  int* sw_j = nullptr;        // sweep outputs, length n
+  double* sw_min = nullptr;
+  double* sw_g = nullptr;
+  int* part_j = nullptr;      // slab partials
+  double* part_min = nullptr;
+  int64_t part_cap = 0;
+  // block-step workspace
+  int64_t blk_L = 0, blk_P = 0;
+  int *pcount = nullptr, *poff = nullptr, *ptotal = nullptr, *prow = nullptr, *ppos = nullptr;
+  double *pd = nullptr, *pt = nullptr, *pdelta = nullptr;
+  int *rowcnt = nullptr, *rowstart = nullptr, *cursor = nullptr, *tmp = nullptr, *sorted = nullptr;
+  double* X = nullptr;
+  int num_sms = 148;
+};
+
+#define CUDA_TRY(s, call)                                                                  \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess) {                                                               \
+      (s)->err = std::string(#call) + ": " + cudaGetErrorString(e_);                       \
+      return e_ == cudaErrorMemoryAllocation ? SRO_ERR_OOM : SRO_ERR_CUDA;                 \
+    }                                                                                      \
+  } while (0)
+
+thread_local std::string g_create_err;
+
+template <typename T>
+cudaError_t dalloc(T** p, size_t count) {
+  return cudaMalloc((void**)p, sizeof(T) * (count ? count : 1));
+}
+
+// ---------------------------------------------------------------------------
+// Small kernels: init, validation, hash generator, objective pieces, max cost
+// ---------------------------------------------------------------------------
+__global__ void k_init_plan(const double* __restrict__ b, const double* __restrict__ a, double* r, double* h,
+                            int* cnt, int* srow, double* sval, int m, int n, int cap, double lambda) {
+  // T^(0) = (b_1 e_1, ..., b_n e_1); r_0 = sum_i b_i left to right.
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+  for (int i = tid; i < n; i += stride) {
+    cnt[i] = 1;
+    srow[(int64_t)i * cap] = 0;
+    sval[(int64_t)i * cap] = b[i];
+  }
+  for (int k = tid; k < m; k += stride) {
+    if (k == 0) {
+      double r0 = 0.0;
+      for (int i = 0; i < n; i++) r0 = d_add(r0, b[i]);
+      r[0] = r0;
+      h[0] = d_div(d_sub(r0, a[0]), lambda);
+    } else {
+      r[k] = 0.0;
+      h[k] = d_div(d_sub(0.0, a[k]), lambda);
+    }
+  }
+}
+
+template <typename T>
+__global__ void k_check_dense(const T* __restrict__ C, int64_t ld, int m, int n, int* status) {
+  const int64_t total = (int64_t)m * n;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = q / m, k = q % m;
+    const double v = (double)C[i * ld + k];
+    if (!(v >= 0.0) || !(v < 1.0e308)) set_status(status, 5);
+  }
+}
+
+template <typename T>
+__global__ void k_check_finite(const T* __restrict__ x, int64_t count, int* status) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < count; q += (int64_t)gridDim.x * blockDim.x) {
+    const double v = (double)x[q];
+    if (!(v > -1.0e308 && v < 1.0e308)) set_status(status, 5);
+  }
+}
+
+// SRO_COST_HASH_UNIFORM: C_ki = (splitmix64(seed + (i m + k + 1) GOLDEN) >> 40) 2^-24, fp32 exact.
+__global__ void k_gen_hash(float* C, int64_t ld, int m, int n, uint64_t seed) {
+  const int64_t total = (int64_t)m * n;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = q / m, k = q % m;
+    const uint64_t z = mix64(seed + ((uint64_t)q + 1) * GOLDEN);
+    C[i * ld + k] = (float)(z >> 40) * 0x1p-24f;
+  }
+}
+
+// lin_i = sum_{k in supp(t_i)} t_ki C_ki (rows ascending), one thread per column.
+template <class Src>
+__global__ void k_lin(Src src, const int* cnt, const int* srow, const double* sval, int cap, int n, double* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int e = 0; e < cnt[i]; e++) {
+      const int k = srow[(int64_t)i * cap + e];
+      acc = d_add(acc, d_mul(sval[(int64_t)i * cap + e], src.cost(k, i)));
+    }
+    out[i] = acc;
+  }
+}
+__global__ void k_pen(const double* r, const double* a, int m, double* out) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < m; k += gridDim.x * blockDim.x) {
+    const double d = d_sub(r[k], a[k]);
+    out[k] = d_mul(d, d);
+  }
+}
+__global__ void k_objective_final(const double* L, const double* pen, double lambda, double* f) {
+  *f = d_add(*L, d_div(*pen, d_mul(2.0, lambda)));
+}
+
+// max_{k,i} C_ki (order-free max): GA stored-gap initial constant (R14).
+template <class Src>
+__global__ void k_max_cost(Src src, int m, int n, unsigned long long* out) {
+  double mx = 0.0;
+  const int64_t total = (int64_t)m * n;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const double c = src.cost((int)(q % m), (int)(q / m));
+    if (c > mx) mx = c;
+  }
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(mx));  // mx >= 0
+}
+__global__ void k_ga_init(double* G, double* fen, int n, const unsigned long long* cmax_bits, double lambda) {
+  const double cinit = d_add(__longlong_as_double((long long)*cmax_bits), d_div(2.0, lambda));
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) G[i] = cinit;
+}
+
+__global__ void k_copy(const double* __restrict__ s, double* d, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) d[i] = s[i];
+}
+
+// ---------------------------------------------------------------------------
+// Host helpers: visit order (R21-R22), identical definition to the paper reading
+// ---------------------------------------------------------------------------
+int uniform_index(uint64_t x, int N) {
+  unsigned __int128 p = (unsigned __int128)(x >> 11) * (unsigned __int128)(uint32_t)N;
+  return (int)(uint64_t)(p >> 53);
+}
+void make_visits(int sampling, uint64_t seed, long long k0, int64_t count, int N, const int32_t* explicit_visit,
+                 int64_t done_offset, std::vector<int>& out) {
+  out.resize(count);
+  if (explicit_visit) {
+    for (int64_t s = 0; s < count; s++) out[s] = explicit_visit[done_offset + s];
+    return;
+  }
+  if (sampling == SRO_SAMPLE_U) {
+    for (int64_t s = 0; s < count; s++) out[s] = uniform_index(rng_u64(seed, 0, (uint64_t)(k0 + s)), N);
+    return;
+  }
+  // P: fresh Fisher-Yates permutation per epoch
+  std::vector<int> perm(N);
+  long long cur_epoch = -1;
+  for (int64_t s = 0; s < count; s++) {
+    const long long kk = k0 + s, e = kk / N;
+    if (e != cur_epoch) {
+      for (int q = 0; q < N; q++) perm[q] = q;
+      for (int q = N - 1; q >= 1; q--) {
+        const uint64_t x = rng_u64(seed, 2, (uint64_t)e * (uint64_t)N + (uint64_t)(N - 1 - q));
+        const int rr = uniform_index(x, q + 1);
+        std::swap(perm[q], perm[rr]);
+      }
+      cur_epoch = e;
+    }
+    out[s] = perm[kk % N];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Kernel dispatch over the cost source
+// ---------------------------------------------------------------------------
+template <class F>
+sro_status with_sweep_src(Solver* s, F f) {
+  if (s->kind == SRO_COST_DENSE || s->kind == SRO_COST_HASH_UNIFORM) {
+    if (s->prec == SRO_FP32) return f(SrcDense<float>{(const float*)s->C, s->ld});
+    return f(SrcDense<double>{(const double*)s->C, s->ld});
+  }
+  const bool eu = s->kind == SRO_COST_EUCLID;
+  if (s->prec == SRO_FP32) {
+    if (eu) return f(SrcColour<float, true>{(const float*)s->x, (const float*)s->y});
+    return f(SrcColour<float, false>{(const float*)s->x, (const float*)s->y});
+  }
+  if (eu) return f(SrcColour<double, true>{(const double*)s->x, (const double*)s->y});
+  return f(SrcColour<double, false>{(const double*)s->x, (const double*)s->y});
+}
+
+sro_status check_status(Solver* s) {
+  int st = 0;
+  CUDA_TRY(s, cudaMemcpyAsync(&st, s->status, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(s, cudaStreamSynchronize(s->stream));
+  if (st) {
+    s->err = st == 5 ? "non-finite value met in the LMO" : st == 6 ? "column support exceeds slab_cap" : "device error";
+    CUDA_TRY(s, cudaMemsetAsync(s->status, 0, sizeof(int), s->stream));
+    return (sro_status)st;
+  }
+  return SRO_OK;
+}
+
+// LMO sweep over [col0, col0+L) -> out_j, out_min, out_g (device arrays of length >= L).
+sro_status sweep(Solver* s, const int* col0_dev, int col0_mul, int col0_host, int L, int* out_j, double* out_min,
+                 double* out_g, const int* stop) {
+  const int nslabs = (s->m + SLAB - 1) / SLAB;
+  if (nslabs > 1 && (int64_t)nslabs * L > s->part_cap) {
+    cudaFree(s->part_j); cudaFree(s->part_min);
+    s->part_cap = (int64_t)nslabs * L;
+    CUDA_TRY(s, dalloc(&s->part_j, s->part_cap));
+    CUDA_TRY(s, dalloc(&s->part_min, s->part_cap));
+  }
+  return with_sweep_src(s, [&](auto src) -> sro_status {
+    using Src = decltype(src);
+    const int rows = s->m < SLAB ? s->m : SLAB;
+    const size_t smem = sizeof(double) * (size_t)((rows + 1) & ~1) + (size_t)Src::SMEM_PER_ROW * rows;
+    auto kern = k_lmo_sweep<Src>;
+    CUDA_TRY(s, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, SWEEP_THREADS, smem));
+    if (per_sm < 1) per_sm = 1;
+    int gx = s->num_sms * per_sm;
+    const int need = (L + SWEEP_WARPS - 1) / SWEEP_WARPS;
+    if (nslabs > 1) gx = (gx + nslabs - 1) / nslabs;
+    if (gx > need) gx = need;
+    if (gx < 1) gx = 1;
+    SweepOut o;
+    if (nslabs == 1) { o.j = out_j; o.minval = out_min; o.g = out_g; }
+    else { o.j = s->part_j; o.minval = s->part_min; o.g = nullptr; }
+    kern<<<dim3(gx, nslabs), SWEEP_THREADS, smem, s->stream>>>(src, s->m, s->h, col0_dev, col0_mul, col0_host, L,
+                                                             s->cnt, s->srow, s->sval, s->cap, s->b, o, stop,
+                                                             s->status);
+    CUDA_TRY(s, cudaGetLastError());
+    if (nslabs > 1) {
+      int gm = (L + SWEEP_WARPS - 1) / SWEEP_WARPS;
+      if (gm > s->num_sms * 8) gm = s->num_sms * 8;
+      k_lmo_merge<Src><<<gm, SWEEP_THREADS, 0, s->stream>>>(src, nslabs, s->h, col0_dev, col0_mul, col0_host, L,
+                                                            s->cnt, s->srow, s->sval, s->cap, s->b, s->part_j,
+                                                            s->part_min, out_j, out_min, out_g, stop, s->status);
+      CUDA_TRY(s, cudaGetLastError());
+    }
+    return SRO_OK;
+  });
+}
+
+// Full gap sweep: g(T) = psum256_i g_i (Thm 2 / Eq. 11) -> host.
+sro_status gap_sweep(Solver* s, double* total) {
+  sro_status st = sweep(s, nullptr, 0, 0, s->n, s->sw_j, s->sw_min, s->sw_g, nullptr);
+  if (st) return st;
+  k_psum256<<<1, 256, 0, s->stream>>>(s->sw_g, s->n, s->scal + 4, nullptr, nullptr, nullptr);
+  CUDA_TRY(s, cudaGetLastError());
+  CUDA_TRY(s, cudaMemcpyAsync(total, s->scal + 4, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+  st = check_status(s);  // synchronises
+  return st;
+}
+
+sro_status ensure_visit(Solver* s, int64_t count) {
+  if (count > s->visit_cap) {
+    cudaFree(s->visit);
+    s->visit_cap = count < 4096 ? 4096 : count;
+    CUDA_TRY(s, dalloc(&s->visit, s->visit_cap));
+  }
+  return SRO_OK;
+}
+sro_status ensure_trace(Solver* s, int64_t count) {
+  if (count > s->trace_cap) {
+    cudaFree(s->trace);
+    s->trace_cap = count;
+    CUDA_TRY(s, dalloc(&s->trace, 9 * s->trace_cap));
+  }
+  return SRO_OK;
+}
+
+void copy_trace_out(const std::vector<double>& tr, int64_t count, sro_trace_rec* out) {
+  for (int64_t s = 0; s < count; s++) {
+    const double* t = &tr[9 * s];
+    out[s].k = (int64_t)t[0];
+    out[s].i = (int32_t)t[1];
+    out[s].j = (int32_t)t[2];
+    out[s].v = (int32_t)t[3];
+    out[s].dir = (int32_t)t[4];
+    out[s].gamma = t[5];
+    out[s].num = t[6];
+    out[s].den = t[7];
+    out[s].minval = t[8];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Sequential BCFW family: persistent kernel segments
+// ---------------------------------------------------------------------------
+template <class Col, int VAR, bool GA>
+sro_status launch_bcfw(Solver* s, BcfwArgs& A, Col col, size_t smem) {
+  auto kern = k_bcfw<Col, VAR, GA>;
+  CUDA_TRY(s, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<1, BCFW_THREADS, smem, s->stream>>>(A, col);
+  CUDA_TRY(s, cudaGetLastError());
+  return SRO_OK;
+}
+
+template <int VAR, bool GA>
+sro_status bcfw_segment_var(Solver* s, BcfwArgs& A, size_t smem_base) {
+  const int m = s->m;
+  if (s->kind == SRO_COST_DENSE || s->kind == SRO_COST_HASH_UNIFORM) {
+    if (s->prec == SRO_FP32) {
+      BcDense<float, 4> c; c.C = (const float*)s->C; c.ld = s->ld; c.m = m; c.nvec = m / 4;
+      return launch_bcfw<BcDense<float, 4>, VAR, GA>(s, A, c, smem_base);
+    }
+    BcDense<double, 4> c; c.C = (const double*)s->C; c.ld = s->ld; c.m = m; c.nvec = m / 2;
+    return launch_bcfw<BcDense<double, 4>, VAR, GA>(s, A, c, smem_base);
+  }
+  const bool eu = s->kind == SRO_COST_EUCLID;
+  if (s->prec == SRO_FP32) {
+    if (eu) { BcColour<float, true> c{(const float*)s->x, nullptr, (const float*)s->y, m};
+              return launch_bcfw<BcColour<float, true>, VAR, GA>(s, A, c, smem_base); }
+    BcColour<float, false> c{(const float*)s->x, nullptr, (const float*)s->y, m};
+    return launch_bcfw<BcColour<float, false>, VAR, GA>(s, A, c, smem_base);
+  }
+  if (eu) { BcColour<double, true> c{(const double*)s->x, nullptr, (const double*)s->y, m};
+            return launch_bcfw<BcColour<double, true>, VAR, GA>(s, A, c, smem_base); }
+  BcColour<double, false> c{(const double*)s->x, nullptr, (const double*)s->y, m};
+  return launch_bcfw<BcColour<double, false>, VAR, GA>(s, A, c, smem_base);
+}
+
+sro_status bcfw_segment(Solver* s, int variant, const sro_options* o, int steps, const int* dvisit,
+                        double* dtrace) {
+  BcfwArgs A{};
+  A.m = s->m; A.n = s->n; A.cap = s->cap; A.lambda = s->lambda;
+  A.a = s->a; A.b = s->b; A.r = s->r; A.h = s->h; A.cnt = s->cnt; A.srow = s->srow; A.sval = s->sval;
+  A.visit = dvisit; A.steps = steps; A.k0 = s->k; A.step_rule = o->step;
+  A.G = s->G; A.fen = s->fen; A.ga_inner = o->ga_inner; A.ga_post = o->ga_post_update; A.seed = s->seed;
+  A.status = s->status; A.steps_done = s->steps_done; A.trace = dtrace;
+  const bool ga = o->sampling == SRO_SAMPLE_GA;
+  A.h_smem = (size_t)s->m * sizeof(double) <= 160 * 1024;
+  size_t smem = sizeof(double) * ((A.h_smem ? (size_t)((s->m + 1) & ~1) : 0) + 256 + BCFW_WARPS) +
+                sizeof(int) * (BCFW_WARPS + 4) + sizeof(double) * 2;
+  A.ga_smem = 0;
+  if (ga && smem + sizeof(double) * (2 * (size_t)s->n + 1) <= 220 * 1024) {
+    A.ga_smem = 1;
+    smem += sizeof(double) * (2 * (size_t)s->n + 1);
+  }
+  A.x_smem = 0;
+  if (variant == SRO_BCFW) return ga ? bcfw_segment_var<VAR_PLAIN, true>(s, A, smem) : bcfw_segment_var<VAR_PLAIN, false>(s, A, smem);
+  if (variant == SRO_BCAFW) return ga ? bcfw_segment_var<VAR_AWAY, true>(s, A, smem) : bcfw_segment_var<VAR_AWAY, false>(s, A, smem);
+  return ga ? bcfw_segment_var<VAR_PAIR, true>(s, A, smem) : bcfw_segment_var<VAR_PAIR, false>(s, A, smem);
+}
+
+sro_status ga_global_refresh(Solver* s) {
+  sro_status st = sweep(s, nullptr, 0, 0, s->n, s->sw_j, s->sw_min, s->G, nullptr);
+  if (st) return st;
+  k_fen_build<<<1, 32, 0, s->stream>>>(s->G, s->fen, s->n);
+  CUDA_TRY(s, cudaGetLastError());
+  return SRO_OK;
+}
+
+sro_status ga_initialise(Solver* s) {
+  unsigned long long* d_cmax = reinterpret_cast<unsigned long long*>(s->scal + 6);
+  CUDA_TRY(s, cudaMemsetAsync(d_cmax, 0, sizeof(unsigned long long), s->stream));
+  sro_status st = with_sweep_src(s, [&](auto src) -> sro_status {
+    k_max_cost<<<s->num_sms * 4, 256, 0, s->stream>>>(src, s->m, s->n, d_cmax);
+    CUDA_TRY(s, cudaGetLastError());
+    return SRO_OK;
+  });
+  if (st) return st;
+  k_ga_init<<<64, 256, 0, s->stream>>>(s->G, s->fen, s->n, d_cmax, s->lambda);
+  k_fen_build<<<1, 32, 0, s->stream>>>(s->G, s->fen, s->n);
+  CUDA_TRY(s, cudaGetLastError());
+  return SRO_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Plain step over a contiguous column set (FW / batched)
+// ---------------------------------------------------------------------------
+sro_status ensure_block_ws(Solver* s, int64_t L) {
+  const int64_t P = L * (s->cap + 1);
+  if (L <= s->blk_L && P <= s->blk_P) return SRO_OK;
+  cudaFree(s->pcount); cudaFree(s->poff); cudaFree(s->ptotal); cudaFree(s->prow); cudaFree(s->ppos);
+  cudaFree(s->pd); cudaFree(s->pt); cudaFree(s->pdelta); cudaFree(s->tmp); cudaFree(s->sorted);
+  if (!s->rowcnt) {
+    CUDA_TRY(s, dalloc(&s->rowcnt, s->m)); CUDA_TRY(s, dalloc(&s->rowstart, s->m + 1));
+    CUDA_TRY(s, dalloc(&s->cursor, s->m + 1)); CUDA_TRY(s, dalloc(&s->X, s->m));
+  }
+  s->blk_L = L; s->blk_P = P;
+  CUDA_TRY(s, dalloc(&s->pcount, L)); CUDA_TRY(s, dalloc(&s->poff, L + 1)); CUDA_TRY(s, dalloc(&s->ptotal, 1));
+  CUDA_TRY(s, dalloc(&s->prow, P)); CUDA_TRY(s, dalloc(&s->ppos, P)); CUDA_TRY(s, dalloc(&s->pd, P));
+  CUDA_TRY(s, dalloc(&s->pt, P)); CUDA_TRY(s, dalloc(&s->pdelta, P)); CUDA_TRY(s, dalloc(&s->tmp, P));
+  CUDA_TRY(s, dalloc(&s->sorted, P));
+  return SRO_OK;
+}
+
+// One plain step over [col0, col0+L). For FW (stop_check) the gap G_[n] is
+// checked against epsilon before the update (Alg. A.1 line 4).
+sro_status plain_block_step(Solver* s, const int* col0_dev, int col0_mul, int L, int step_rule, long long nprime,
+                            bool stop_check, double* trace_dev) {
+  sro_status st = ensure_block_ws(s, L);
+  if (st) return st;
+  const int* stop = stop_check ? s->stop : nullptr;
+  st = sweep(s, col0_dev, col0_mul, 0, L, s->sw_j, s->sw_min, s->sw_g, stop);
+  if (st) return st;
+  k_psum256<<<1, 256, 0, s->stream>>>(s->sw_g, L, s->scal + 0, stop_check ? s->epsd : nullptr,
+                                      stop_check ? s->stop : nullptr, nullptr);
+  BlockArgs A{};
+  A.m = s->m; A.n = s->n; A.cap = s->cap; A.lambda = s->lambda; A.a = s->a; A.b = s->b; A.r = s->r; A.h = s->h;
+  A.cnt = s->cnt; A.srow = s->srow; A.sval = s->sval; A.col0_dev = col0_dev; A.col0_mul = col0_mul; A.L = L;
+  A.j = s->sw_j; A.minval = s->sw_min; A.pcount = s->pcount; A.poff = s->poff; A.ptotal = s->ptotal;
+  A.prow = s->prow; A.ppos = s->ppos; A.pd = s->pd; A.pt = s->pt; A.pdelta = s->pdelta; A.rowcnt = s->rowcnt;
+  A.rowstart = s->rowstart; A.cursor = s->cursor; A.tmp = s->tmp; A.sorted = s->sorted; A.X = s->X;
+  A.scal = s->scal; A.stop = stop; A.status = s->status;
+  const int tpb = 256;
+  int gL = (L + tpb - 1) / tpb; if (gL > s->num_sms * 8) gL = s->num_sms * 8;
+  int gM = (s->m + tpb - 1) / tpb; if (gM > s->num_sms * 8) gM = s->num_sms * 8;
+  const int gP = s->num_sms * 8;
+  k_pairs_count<<<gL, tpb, 0, s->stream>>>(A);
+  k_scan_excl<<<1, 1024, 0, s->stream>>>(s->pcount, L, s->poff, nullptr, s->ptotal, stop, s->status);
+  CUDA_TRY(s, cudaMemsetAsync(s->rowcnt, 0, sizeof(int) * s->m, s->stream));
+  k_pairs_gen<<<gL, tpb, 0, s->stream>>>(A);
+  k_scan_excl<<<1, 1024, 0, s->stream>>>(s->rowcnt, s->m, s->rowstart, s->cursor, nullptr, stop, s->status);
+  k_place<<<gP, tpb, 0, s->stream>>>(A);
+  k_rank<<<gP, tpb, 0, s->stream>>>(A);
+  k_rowsum_dir<<<gM, tpb, 0, s->stream>>>(A);
+  k_psum256<<<1, 256, 0, s->stream>>>(s->X, s->m, s->scal + 1, nullptr, nullptr, stop);
+  const long long kk = s->k;
+  k_gamma<<<1, 32, 0, s->stream>>>(A, step_rule, kk, nprime, trace_dev);
+  k_cap_check<<<gL, tpb, 0, s->stream>>>(A);
+  k_update_cols<<<gL, tpb, 0, s->stream>>>(A);
+  k_rowsum_update<<<gM, tpb, 0, s->stream>>>(A);
+  CUDA_TRY(s, cudaGetLastError());
+  return SRO_OK;
+}
+
+bool options_equal(const sro_options& x, const sro_options& y) {
+  return x.step == y.step && x.sampling == y.sampling && x.epsilon == y.epsilon && x.gap_period == y.gap_period &&
+         x.ga_M == y.ga_M && x.ga_inner == y.ga_inner && x.ga_post_update == y.ga_post_update &&
+         x.block_size == y.block_size;
+}
+
+sro_status objective_dev(Solver* s, double* f_host) {
+  sro_status st = with_sweep_src(s, [&](auto src) -> sro_status {
+    k_lin<<<(s->n + 255) / 256, 256, 0, s->stream>>>(src, s->cnt, s->srow, s->sval, s->cap, s->n, s->sw_g);
+    CUDA_TRY(s, cudaGetLastError());
+    return SRO_OK;
+  });
+  if (st) return st;
+  k_psum256<<<1, 256, 0, s->stream>>>(s->sw_g, s->n, s->scal + 4, nullptr, nullptr, nullptr);
+  k_pen<<<(s->m + 255) / 256, 256, 0, s->stream>>>(s->r, s->a, s->m, s->sw_min);
+  k_psum256<<<1, 256, 0, s->stream>>>(s->sw_min, s->m, s->scal + 5, nullptr, nullptr, nullptr);
+  k_objective_final<<<1, 1, 0, s->stream>>>(s->scal + 4, s->scal + 5, s->lambda, s->scal + 7);
+  CUDA_TRY(s, cudaGetLastError());
+  CUDA_TRY(s, cudaMemcpyAsync(f_host, s->scal + 7, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(s, cudaStreamSynchronize(s->stream));
+  return SRO_OK;
+}
+
+sro_status do_reset(Solver* s) {
+  k_init_plan<<<s->num_sms, 256, 0, s->stream>>>(s->b, s->a, s->r, s->h, s->cnt, s->srow, s->sval, s->m, s->n, s->cap,
+                                                s->lambda);
+  CUDA_TRY(s, cudaGetLastError());
+  CUDA_TRY(s, cudaMemsetAsync(s->stop, 0, sizeof(int), s->stream));
+  s->k = 0;
+  s->configured = false;
+  return SRO_OK;
+}
+
+void free_solver(Solver* s) {
+  if (!s) return;
+  void* ptrs[] = {s->a, s->b, s->r, s->h, s->cnt, s->srow, s->sval, s->G, s->fen, s->status, s->steps_done,
+                  s->stop, s->scal, s->epsd, s->visit, s->trace, s->sw_j, s->sw_min, s->sw_g, s->part_j,
+                  s->part_min, s->pcount, s->poff, s->ptotal, s->prow, s->ppos, s->pd, s->pt, s->pdelta,
+                  s->rowcnt, s->rowstart, s->cursor, s->tmp, s->sorted, s->X};
+  for (void* p : ptrs) if (p) cudaFree(p);
+  if (s->owns_cost) { if (s->C) cudaFree(s->C); if (s->x) cudaFree(s->x); if (s->y) cudaFree(s->y); }
+  if (s->ev0) cudaEventDestroy(s->ev0);
+  if (s->ev1) cudaEventDestroy(s->ev1);
+  if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
+  delete s;
+}
+
+}  // namespace
+
+struct sro_solver : Solver {};
+
+extern "C" {
+
+const char* sro_version(void) { return "sro-b200 0.1 (sm_100a)"; }
+
+const char* sro_last_error(sro_handle h) {
+  if (!h) return g_create_err.c_str();
+  return static_cast<Solver*>(h)->err.c_str();
+}
+
+sro_status sro_create(const double* a, const double* b, const sro_cost* cost, const sro_params* p, sro_handle* out) {
+  g_create_err.clear();
+  if (!out || !a || !b || !cost || !p) { g_create_err = "null argument"; return SRO_ERR_INVALID_ARG; }
+  *out = nullptr;
+  if (p->m < 1 || p->n < 1) { g_create_err = "m, n must be >= 1"; return SRO_ERR_DIMENSION; }
+  if (!(p->lambda > 0.0) || !std::isfinite(p->lambda)) { g_create_err = "lambda must be finite and > 0"; return SRO_ERR_INVALID_ARG; }
+  const int cap = p->slab_cap == 0 ? 31 : p->slab_cap;
+  if (cap < 1 || cap > 31) { g_create_err = "slab_cap must be in [1, 31]"; return SRO_ERR_INVALID_ARG; }
+  if (cost->kind < 0 || cost->kind > 3 || cost->prec < 0 || cost->prec > 1) { g_create_err = "bad cost kind/precision"; return SRO_ERR_INVALID_ARG; }
+  // marginals: finite, a >= 0, b > 0, each summing to 1 within 1e-12
+  double sa = 0.0, sb = 0.0;
+  for (int k = 0; k < p->m; k++) { if (!(a[k] >= 0.0) || !std::isfinite(a[k])) { g_create_err = "a must be finite and >= 0"; return SRO_ERR_MARGINALS; } sa += a[k]; }
+  for (int i = 0; i < p->n; i++) { if (!(b[i] > 0.0) || !std::isfinite(b[i])) { g_create_err = "b must be finite and > 0"; return SRO_ERR_MARGINALS; } sb += b[i]; }
+  if (std::fabs(sa - 1.0) > 1e-12 || std::fabs(sb - 1.0) > 1e-12) { g_create_err = "marginals must sum to 1 within 1e-12"; return SRO_ERR_MARGINALS; }
+
+  Solver* s = new Solver();
+  s->m = p->m; s->n = p->n; s->cap = cap; s->lambda = p->lambda; s->device = p->device;
+  s->kind = cost->kind; s->prec = cost->prec; s->borrowed = cost->data_on_device;
+  if (s->kind == SRO_COST_HASH_UNIFORM) s->prec = SRO_FP32;
+  auto fail = [&](sro_status st, const std::string& msg) { g_create_err = msg.empty() ? s->err : msg; free_solver(s); return st; };
+  if (cudaSetDevice(p->device) != cudaSuccess) return fail(SRO_ERR_CUDA, "cudaSetDevice failed (no CUDA device?)");
+  cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, p->device);
+  if (p->cuda_stream) s->stream = (cudaStream_t)p->cuda_stream;
+  else { if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess) return fail(SRO_ERR_CUDA, "stream"); s->own_stream = true; }
+  cudaEventCreate(&s->ev0); cudaEventCreate(&s->ev1);
+  const int m = s->m, n = s->n;
+#define ALLOC(ptr, cnt_)                                                              \
+  if (dalloc(&(ptr), (cnt_)) != cudaSuccess) return fail(SRO_ERR_OOM, "device allocation failed");
+  ALLOC(s->a, m); ALLOC(s->b, n); ALLOC(s->r, m); ALLOC(s->h, m);
+  ALLOC(s->cnt, n); ALLOC(s->srow, (size_t)n * cap); ALLOC(s->sval, (size_t)n * cap);
+  ALLOC(s->G, n); ALLOC(s->fen, (size_t)n + 1);
+  ALLOC(s->status, 1); ALLOC(s->steps_done, 1); ALLOC(s->stop, 1); ALLOC(s->scal, 8); ALLOC(s->epsd, 1);
+  ALLOC(s->sw_j, n); ALLOC(s->sw_min, (size_t)(m > n ? m : n)); ALLOC(s->sw_g, (size_t)(m > n ? m : n));
+  cudaMemsetAsync(s->status, 0, sizeof(int), s->stream);
+  cudaMemcpyAsync(s->a, a, sizeof(double) * m, cudaMemcpyHostToDevice, s->stream);
+  cudaMemcpyAsync(s->b, b, sizeof(double) * n, cudaMemcpyHostToDevice, s->stream);
+  const size_t esz = s->prec == SRO_FP32 ? 4 : 8;
+  const int vec = 16 / (int)esz;
+  if (s->kind == SRO_COST_DENSE) {
+    if (!cost->data || cost->ld < m) return fail(SRO_ERR_INVALID_ARG, "dense cost needs data and ld >= m");
+    if (cost->data_on_device) {
+      if (((uintptr_t)cost->data % 16) != 0 || (cost->ld * (int64_t)esz) % 16 != 0)
+        return fail(SRO_ERR_INVALID_ARG, "borrowed dense cost must be 16-byte aligned with ld*elem % 16 == 0");
+      s->C = const_cast<void*>(cost->data); s->ld = cost->ld;
+    } else {
+      s->ld = ((int64_t)m + vec - 1) / vec * vec;
+      if (cudaMalloc(&s->C, esz * (size_t)s->ld * n) != cudaSuccess) return fail(SRO_ERR_OOM, "cost allocation failed");
+      s->owns_cost = true;
+      if (cudaMemcpy2DAsync(s->C, esz * s->ld, cost->data, esz * cost->ld, esz * m, n, cudaMemcpyHostToDevice, s->stream) != cudaSuccess)
+        return fail(SRO_ERR_CUDA, "cost upload failed");
+    }
+    if (s->prec == SRO_FP32) k_check_dense<float><<<s->num_sms * 4, 256, 0, s->stream>>>((const float*)s->C, s->ld, m, n, s->status);
+    else k_check_dense<double><<<s->num_sms * 4, 256, 0, s->stream>>>((const double*)s->C, s->ld, m, n, s->status);
+  } else if (s->kind == SRO_COST_HASH_UNIFORM) {
+    s->ld = ((int64_t)m + 3) / 4 * 4;
+    if (cudaMalloc(&s->C, 4 * (size_t)s->ld * n) != cudaSuccess) return fail(SRO_ERR_OOM, "cost allocation failed");
+    s->owns_cost = true;
+    k_gen_hash<<<s->num_sms * 8, 256, 0, s->stream>>>((float*)s->C, s->ld, m, n, cost->hash_seed);
+  } else {
+    if (!cost->x || !cost->y) return fail(SRO_ERR_INVALID_ARG, "colour cost needs x and y");
+    if (cost->data_on_device) { s->x = const_cast<void*>(cost->x); s->y = const_cast<void*>(cost->y); }
+    else {
+      if (cudaMalloc(&s->x, esz * 3 * (size_t)m) != cudaSuccess || cudaMalloc(&s->y, esz * 3 * (size_t)n) != cudaSuccess)
+        return fail(SRO_ERR_OOM, "colour allocation failed");
+      s->owns_cost = true;
+      cudaMemcpyAsync(s->x, cost->x, esz * 3 * (size_t)m, cudaMemcpyHostToDevice, s->stream);
+      cudaMemcpyAsync(s->y, cost->y, esz * 3 * (size_t)n, cudaMemcpyHostToDevice, s->stream);
+    }
+    if (s->prec == SRO_FP32) {
+      k_check_finite<float><<<64, 256, 0, s->stream>>>((const float*)s->x, 3LL * m, s->status);
+      k_check_finite<float><<<64, 256, 0, s->stream>>>((const float*)s->y, 3LL * n, s->status);
+    } else {
+      k_check_finite<double><<<64, 256, 0, s->stream>>>((const double*)s->x, 3LL * m, s->status);
+      k_check_finite<double><<<64, 256, 0, s->stream>>>((const double*)s->y, 3LL * n, s->status);
+    }
+  }
+  if (cudaGetLastError() != cudaSuccess) return fail(SRO_ERR_CUDA, "kernel launch failed at create");
+  int st = 0;
+  cudaMemcpyAsync(&st, s->status, sizeof(int), cudaMemcpyDeviceToHost, s->stream);
+  if (cudaStreamSynchronize(s->stream) != cudaSuccess) return fail(SRO_ERR_CUDA, "create failed");
+  if (st) return fail(SRO_ERR_NONFINITE, "cost must be finite and >= 0");
+  if (do_reset(s) != SRO_OK) return fail(SRO_ERR_CUDA, "");
+  if (cudaStreamSynchronize(s->stream) != cudaSuccess) return fail(SRO_ERR_CUDA, "init failed");
+  *out = static_cast<sro_handle>(static_cast<sro_solver*>(s));
+  return SRO_OK;
+}
+
+void sro_destroy(sro_handle h) {
+  if (!h) return;
+  Solver* s = static_cast<Solver*>(h);
+  cudaSetDevice(s->device);
+  cudaStreamSynchronize(s->stream);
+  free_solver(s);
+}
+
+sro_status sro_reset(sro_handle h) {
+  if (!h) return SRO_ERR_INVALID_ARG;
+  Solver* s = static_cast<Solver*>(h);
+  cudaSetDevice(s->device);
+  sro_status st = do_reset(s);
+  if (st) return st;
+  CUDA_TRY(s, cudaStreamSynchronize(s->stream));
+  return SRO_OK;
+}
+
+sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_t iters, uint64_t seed, sro_result* out) {
+  if (!h || !o || !out || iters < 0) return SRO_ERR_INVALID_ARG;
+  Solver* s = static_cast<Solver*>(h);
+  cudaSetDevice(s->device);
+  memset(out, 0, sizeof(*out));
+  out->gap = NAN;
+  out->objective = NAN;
+  if (variant < SRO_FW || variant > SRO_BATCHED) { s->err = "bad variant"; return SRO_ERR_INVALID_ARG; }
+  if (o->gap_period < 1) { s->err = "gap_period must be >= 1"; return SRO_ERR_INVALID_ARG; }
+  if ((variant == SRO_BCAFW || variant == SRO_BCPFW) && o->step != SRO_STEP_ELS) { s->err = "away/pairwise need the line search (Alg. A.2/A.3)"; return SRO_ERR_INVALID_ARG; }
+  if (o->sampling == SRO_SAMPLE_GA && !(variant == SRO_BCFW || variant == SRO_BCAFW || variant == SRO_BCPFW)) { s->err = "GA sampling needs a BCFW-family variant"; return SRO_ERR_INVALID_ARG; }
+  if (o->sampling == SRO_SAMPLE_GA && o->ga_M < 1) { s->err = "ga_M must be >= 1"; return SRO_ERR_INVALID_ARG; }
+  if (o->sampling < 0 || o->sampling > 2 || o->step < 0 || o->step > 1) { s->err = "bad sampling/step"; return SRO_ERR_INVALID_ARG; }
+  long long nprime;
+  if (variant == SRO_FW) nprime = 1;
+  else if (variant == SRO_BATCHED) {
+    if (o->block_size < 1 || s->n % o->block_size != 0) { s->err = "block_size must divide n"; return SRO_ERR_INVALID_ARG; }
+    nprime = s->n / o->block_size;
+  } else nprime = s->n;
+  if (s->configured) {
+    if (s->variant != variant || s->seed != seed || !options_equal(s->opt, *o)) { s->err = "solver configured differently; call sro_reset"; return SRO_ERR_STATE; }
+  }
+  const bool ga = o->sampling == SRO_SAMPLE_GA && variant != SRO_FW;
+  sro_status st = SRO_OK;
+  CUDA_TRY(s, cudaEventRecord(s->ev0, s->stream));
+  if (!s->configured) {
+    s->configured = true; s->variant = variant; s->opt = *o; s->seed = seed;
+    s->opt.visit = nullptr; s->opt.trace = nullptr;
+    if (ga) { st = ga_initialise(s); if (st) return st; }
+  }
+  CUDA_TRY(s, cudaMemcpyAsync(s->epsd, &o->epsilon, sizeof(double), cudaMemcpyHostToDevice, s->stream));
+  const int m = s->m, n = s->n;
+  int64_t done = 0;
+  const long long period = (long long)o->gap_period * nprime;
+  std::vector<int> hv;
+  std::vector<double> htr;
+  if (o->trace) { st = ensure_trace(s, iters > 0 ? iters : 1); if (st) return st; }
+
+  if (variant == SRO_FW) {
+    const int one = 0;
+    (void)one;
+    CUDA_TRY(s, cudaMemsetAsync(s->stop, 0, sizeof(int), s->stream));
+    while (done < iters) {
+      st = plain_block_step(s, nullptr, 0, n, o->step, 1, true, o->trace ? s->trace + 9 * done : nullptr);
+      if (st) return st;
+      double G = 0.0;
+      int stopped = 0;
+      CUDA_TRY(s, cudaMemcpyAsync(&G, s->scal + 0, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+      CUDA_TRY(s, cudaMemcpyAsync(&stopped, s->stop, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+      st = check_status(s);
+      if (st) return st;
+      out->gap = G; out->gap_checks++;
+      out->entries_scanned += (int64_t)m * n;
+      if (stopped) { out->converged = 1; break; }
+      s->k++; done++;
+    }
+    CUDA_TRY(s, cudaMemsetAsync(s->stop, 0, sizeof(int), s->stream));
+  } else {
+    // visit order for the whole call (U / P / explicit); GA draws on the device
+    if (!ga) {
+      make_visits(o->sampling, seed, s->k, iters, (int)nprime, o->visit, 0, hv);
+      st = ensure_visit(s, iters > 0 ? iters : 1);
+      if (st) return st;
+      if (iters > 0) CUDA_TRY(s, cudaMemcpyAsync(s->visit, hv.data(), sizeof(int) * iters, cudaMemcpyHostToDevice, s->stream));
+    }
+    const long long gaMn = ga ? (long long)o->ga_M * n : 0;
+    for (;;) {
+      if (s->k % period == 0) {
+        double g = 0.0;
+        st = gap_sweep(s, &g);
+        if (st) return st;
+        out->gap = g; out->gap_checks++;
+        out->entries_scanned += (int64_t)m * n;
+        if (g <= o->epsilon) { out->converged = 1; break; }
+      }
+      if (done >= iters) break;
+      if (variant == SRO_BATCHED) {
+        st = plain_block_step(s, s->visit + done, o->block_size, o->block_size, o->step, nprime, false,
+                              o->trace ? s->trace + 9 * done : nullptr);
+        if (st) return st;
+        st = check_status(s);
+        if (st) return st;
+        out->entries_scanned += (int64_t)m * o->block_size;
+        s->k++; done++;
+        continue;
+      }
+      long long seg = iters - done;
+      const long long to_check = period - s->k % period;
+      if (seg > to_check) seg = to_check;
+      if (ga) { const long long to_ref = gaMn - s->k % gaMn; if (seg > to_ref) seg = to_ref; }
+      st = bcfw_segment(s, variant, o, (int)seg, ga ? nullptr : s->visit + done, o->trace ? s->trace + 9 * done : nullptr);
+      if (st) return st;
+      int sd = 0;
+      CUDA_TRY(s, cudaMemcpyAsync(&sd, s->steps_done, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+      st = check_status(s);
+      s->k += sd; done += sd;
+      out->entries_scanned += (int64_t)m * sd * ((ga && o->ga_inner && o->ga_post_update) ? 2 : 1);
+      if (st) break;
+      if (ga && s->k % gaMn == 0) {
+        st = ga_global_refresh(s);
+        if (st) return st;
+        out->entries_scanned += (int64_t)m * n;
+      }
+    }
+  }
+  out->iters_done = done;
+  out->k = s->k;
+  CUDA_TRY(s, cudaEventRecord(s->ev1, s->stream));
+  if (o->trace && done > 0) {
+    htr.resize(9 * (size_t)done);
+    CUDA_TRY(s, cudaMemcpyAsync(htr.data(), s->trace, sizeof(double) * 9 * done, cudaMemcpyDeviceToHost, s->stream));
+  }
+  CUDA_TRY(s, cudaStreamSynchronize(s->stream));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, s->ev0, s->ev1);
+  out->device_ms = ms;
+  if (o->trace && done > 0) copy_trace_out(htr, done, o->trace);
+  if (st) return st;
+  double f = NAN;
+  sro_status st2 = objective_dev(s, &f);
+  if (st2) return st2;
+  out->objective = f;
+  return out->converged ? SRO_OK : SRO_NOT_CONVERGED;
+}
+
+sro_status sro_gap(sro_handle h, double* total, double* per_column, int32_t* argmin_rows) {
+  if (!h || !total) return SRO_ERR_INVALID_ARG;
+  Solver* s = static_cast<Solver*>(h);
+  cudaSetDevice(s->device);
+  sro_status st = gap_sweep(s, total);
+  if (st) return st;
+  if (per_column) CUDA_TRY(s, cudaMemcpyAsync(per_column, s->sw_g, sizeof(double) * s->n, cudaMemcpyDeviceToHost, s->stream));
+  if (argmin_rows) CUDA_TRY(s, cudaMemcpyAsync(argmin_rows, s->sw_j, sizeof(int) * s->n, cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(s, cudaStreamSynchronize(s->stream));
+  return SRO_OK;
+}
+
+sro_status sro_objective(sro_handle h, double* f) {
+  if (!h || !f) return SRO_ERR_INVALID_ARG;
+  Solver* s = static_cast<Solver*>(h);
+  cudaSetDevice(s->device);
+  return objective_dev(s, f);
+}
+
+sro_status sro_get_rowsums(sro_handle h, double* r) {
+  if (!h || !r) return SRO_ERR_INVALID_ARG;
+  Solver* s = static_cast<Solver*>(h);
+  cudaSetDevice(s->device);
+  CUDA_TRY(s, cudaMemcpyAsync(r, s->r, sizeof(double) * s->m, cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(s, cudaStreamSynchronize(s->stream));
+  return SRO_OK;
+}
+
+sro_status sro_get_plan(sro_handle h, double* dense, int32_t* rows, int32_t* cols, double* vals, int64_t cap,
+                        int64_t* nnz) {
+  if (!h) return SRO_ERR_INVALID_ARG;
+  Solver* s = static_cast<Solver*>(h);
+  cudaSetDevice(s->device);
+  std::vector<int> hc(s->n), hr((size_t)s->n * s->cap);
+  std::vector<double> hv((size_t)s->n * s->cap);
+  CUDA_TRY(s, cudaMemcpyAsync(hc.data(), s->cnt, sizeof(int) * s->n, cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(s, cudaMemcpyAsync(hr.data(), s->srow, sizeof(int) * hr.size(), cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(s, cudaMemcpyAsync(hv.data(), s->sval, sizeof(double) * hv.size(), cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(s, cudaStreamSynchronize(s->stream));
+  if (dense) memset(dense, 0, sizeof(double) * (size_t)s->m * s->n);
+  int64_t q = 0;
+  for (int i = 0; i < s->n; i++)
+    for (int e = 0; e < hc[i]; e++) {
+      const int k = hr[(size_t)i * s->cap + e];
+      const double v = hv[(size_t)i * s->cap + e];
+      if (dense) dense[(size_t)i * s->m + k] = v;
+      if (rows && cols && vals && q < cap) { rows[q] = k; cols[q] = i; vals[q] = v; }
+      q++;
+    }
+  if (nnz) *nnz = q;
+  if (rows && cols && vals && q > cap) { s->err = "COO capacity too small"; return SRO_ERR_CAPACITY; }
+  return SRO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,240 @@
+"""Thin ctypes binding of libsro.so (include/sro.h). Argument marshalling only:
+every step of the method runs in the CUDA kernels behind the C-ABI. There is
+no CPU fallback: if the library cannot be loaded, or no CUDA device is
+present, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import os
+
+import numpy as np
+
+__all__ = [
+    "load_library", "Solver", "SroError", "SRO_FW", "SRO_BCFW", "SRO_BCAFW", "SRO_BCPFW", "SRO_BATCHED",
+    "STEP_DEC", "STEP_ELS", "SAMPLE_U", "SAMPLE_P", "SAMPLE_GA", "TRACE_DTYPE", "EXPORTED_SYMBOLS",
+]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsro.so")
+
+SRO_FW, SRO_BCFW, SRO_BCAFW, SRO_BCPFW, SRO_BATCHED = 0, 1, 2, 3, 4
+STEP_DEC, STEP_ELS = 0, 1
+SAMPLE_U, SAMPLE_P, SAMPLE_GA = 0, 1, 2
+COST_KINDS = {"dense": 0, "sqeuclid": 1, "euclid": 2, "hash": 3}
+PRECS = {"f64": 0, "f32": 1}
+OK, NOT_CONVERGED = 0, 1
+EXPORTED_SYMBOLS = ("sro_create", "sro_solve", "sro_gap", "sro_objective", "sro_get_plan", "sro_get_rowsums",
+                    "sro_reset", "sro_destroy", "sro_last_error", "sro_version")
+
+_STATUS = {0: "OK", 1: "NOT_CONVERGED", 2: "ERR_INVALID_ARG", 3: "ERR_DIMENSION", 4: "ERR_MARGINALS",
+           5: "ERR_NONFINITE", 6: "ERR_CAPACITY", 7: "ERR_CUDA", 8: "ERR_NCCL", 9: "ERR_OOM", 10: "ERR_STATE"}
+
+
+class SroError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"sro status {status} ({_STATUS.get(status, '?')}): {msg}")
+        self.status = status
+
+
+class SroCost(ct.Structure):
+    _fields_ = [("kind", ct.c_int32), ("prec", ct.c_int32), ("data", ct.c_void_p), ("ld", ct.c_int64),
+                ("x", ct.c_void_p), ("y", ct.c_void_p), ("hash_seed", ct.c_uint64), ("data_on_device", ct.c_int32)]
+
+
+class SroParams(ct.Structure):
+    _fields_ = [("m", ct.c_int32), ("n", ct.c_int32), ("lambda_", ct.c_double), ("slab_cap", ct.c_int32),
+                ("device", ct.c_int32), ("cuda_stream", ct.c_void_p)]
+
+
+class SroTraceRec(ct.Structure):
+    _fields_ = [("k", ct.c_int64), ("i", ct.c_int32), ("j", ct.c_int32), ("v", ct.c_int32), ("dir", ct.c_int32),
+                ("gamma", ct.c_double), ("num", ct.c_double), ("den", ct.c_double), ("minval", ct.c_double)]
+
+
+TRACE_DTYPE = np.dtype([("k", np.int64), ("i", np.int32), ("j", np.int32), ("v", np.int32), ("dir", np.int32),
+                        ("gamma", np.float64), ("num", np.float64), ("den", np.float64), ("minval", np.float64)])
+assert TRACE_DTYPE.itemsize == ct.sizeof(SroTraceRec)
+
+
+class SroOptions(ct.Structure):
+    _fields_ = [("step", ct.c_int32), ("sampling", ct.c_int32), ("epsilon", ct.c_double),
+                ("gap_period", ct.c_int32), ("ga_M", ct.c_int32), ("ga_inner", ct.c_int32),
+                ("ga_post_update", ct.c_int32), ("block_size", ct.c_int32), ("visit", ct.c_void_p),
+                ("trace", ct.c_void_p)]
+
+
+class SroResult(ct.Structure):
+    _fields_ = [("iters_done", ct.c_int64), ("k", ct.c_int64), ("gap", ct.c_double), ("objective", ct.c_double),
+                ("converged", ct.c_int32), ("gap_checks", ct.c_int32), ("entries_scanned", ct.c_int64),
+                ("device_ms", ct.c_double)]
+
+
+_lib = None
+
+
+def load_library():
+    """Load libsro.so (built by paper_2103_05857_b200.build / __graft_entry__.build())."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise SroError(-1, f"{LIB_PATH} missing: run `python -m paper_2103_05857_b200.build`")
+        L = ct.CDLL(LIB_PATH)
+        vp, i32, i64, u64, d = ct.c_void_p, ct.c_int32, ct.c_int64, ct.c_uint64, ct.c_double
+        L.sro_create.argtypes = [vp, vp, ct.POINTER(SroCost), ct.POINTER(SroParams), ct.POINTER(vp)]
+        L.sro_create.restype = ct.c_int
+        L.sro_solve.argtypes = [vp, i32, ct.POINTER(SroOptions), i64, u64, ct.POINTER(SroResult)]
+        L.sro_solve.restype = ct.c_int
+        L.sro_gap.argtypes = [vp, ct.POINTER(d), vp, vp]
+        L.sro_gap.restype = ct.c_int
+        L.sro_objective.argtypes = [vp, ct.POINTER(d)]
+        L.sro_objective.restype = ct.c_int
+        L.sro_get_plan.argtypes = [vp, vp, vp, vp, vp, i64, ct.POINTER(i64)]
+        L.sro_get_plan.restype = ct.c_int
+        L.sro_get_rowsums.argtypes = [vp, vp]
+        L.sro_get_rowsums.restype = ct.c_int
+        L.sro_reset.argtypes = [vp]
+        L.sro_reset.restype = ct.c_int
+        L.sro_destroy.argtypes = [vp]
+        L.sro_destroy.restype = None
+        L.sro_last_error.argtypes = [vp]
+        L.sro_last_error.restype = ct.c_char_p
+        L.sro_version.argtypes = []
+        L.sro_version.restype = ct.c_char_p
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):          # torch tensor (device or host)
+        return ct.c_void_p(a.data_ptr())
+    return a.ctypes.data_as(ct.c_void_p)
+
+
+def _is_cuda(t):
+    return hasattr(t, "is_cuda") and t.is_cuda
+
+
+class Solver:
+    """One solver handle: problem (a, b, cost, lambda) + plan state on the GPU.
+
+    cost='dense': C is m x n (rows = source bins); numpy arrays are copied,
+    CUDA torch tensors are borrowed (pass C.T-contiguous, i.e. column-major).
+    cost='sqeuclid' / 'euclid': X (m x 3) and Y (n x 3) colours.
+    cost='hash': iid uniform C generated on the device from hash_seed.
+    prec='f64' | 'f32' is the storage / evaluation precision of the cost.
+    """
+
+    def __init__(self, a, b, lam, *, C=None, X=None, Y=None, cost="dense", prec="f64", hash_seed=0, slab_cap=31,
+                 device=0, stream=None, ld=None):
+        L = load_library()
+        self._L = L
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        self.m, self.n = len(a), len(b)
+        self.lam = float(lam)
+        kind = COST_KINDS[cost]
+        pr = PRECS[prec]
+        dt = np.float32 if prec == "f32" else np.float64
+        keep = []
+        c = SroCost(kind=kind, prec=pr, data=None, ld=0, x=None, y=None, hash_seed=hash_seed, data_on_device=0)
+        if kind == 0:
+            if _is_cuda(C):
+                # device tensor, column-major storage: shape (n, ld) row-major
+                c.data, c.data_on_device = _ptr(C), 1
+                c.ld = ld if ld is not None else C.shape[1]
+            else:
+                Cm = np.asarray(C, dtype=dt)
+                assert Cm.shape == (self.m, self.n)
+                Ccm = np.ascontiguousarray(Cm.T)        # column i contiguous
+                keep.append(Ccm)
+                c.data, c.ld = _ptr(Ccm), self.m
+        elif kind in (1, 2):
+            if _is_cuda(X):
+                c.x, c.y, c.data_on_device = _ptr(X), _ptr(Y), 1
+            else:
+                Xc = np.ascontiguousarray(X, dtype=dt)
+                Yc = np.ascontiguousarray(Y, dtype=dt)
+                keep += [Xc, Yc]
+                c.x, c.y = _ptr(Xc), _ptr(Yc)
+        p = SroParams(m=self.m, n=self.n, lambda_=self.lam, slab_cap=slab_cap, device=device,
+                      cuda_stream=ct.c_void_p(stream) if stream else None)
+        h = ct.c_void_p()
+        st = L.sro_create(_ptr(a), _ptr(b), ct.byref(c), ct.byref(p), ct.byref(h))
+        if st != OK:
+            raise SroError(st, L.sro_last_error(None).decode())
+        self.h = h
+        self.cap = slab_cap
+
+    def _check(self, st, allow=(OK,)):
+        if st not in allow:
+            raise SroError(st, self._L.sro_last_error(self.h).decode())
+        return st
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._L.sro_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def solve(self, variant, iters, seed=0, *, step=STEP_ELS, sampling=SAMPLE_U, epsilon=1e-6, gap_period=1, ga_M=1,
+              ga_inner=1, ga_post_update=1, block_size=1, visit=None, trace=False):
+        vis = None
+        if visit is not None:
+            vis = np.ascontiguousarray(visit, dtype=np.int32)
+            assert len(vis) >= iters
+        tr = np.zeros(max(iters, 1), dtype=TRACE_DTYPE) if trace else None
+        o = SroOptions(step=step, sampling=sampling, epsilon=epsilon, gap_period=gap_period, ga_M=ga_M,
+                       ga_inner=ga_inner, ga_post_update=ga_post_update, block_size=block_size,
+                       visit=_ptr(vis), trace=_ptr(tr))
+        r = SroResult()
+        st = self._L.sro_solve(self.h, variant, ct.byref(o), iters, seed, ct.byref(r))
+        self._check(st, (OK, NOT_CONVERGED))
+        out = {f: getattr(r, f) for f, _ in SroResult._fields_}
+        out["status"] = st
+        if trace:
+            out["trace"] = tr[: r.iters_done]
+        return out
+
+    def gap(self):
+        tot = ct.c_double()
+        g = np.empty(self.n)
+        j = np.empty(self.n, dtype=np.int32)
+        self._check(self._L.sro_gap(self.h, ct.byref(tot), _ptr(g), _ptr(j)))
+        return tot.value, g, j
+
+    def objective(self):
+        f = ct.c_double()
+        self._check(self._L.sro_objective(self.h, ct.byref(f)))
+        return f.value
+
+    def plan(self):
+        T = np.empty(self.m * self.n)
+        nnz = ct.c_int64()
+        self._check(self._L.sro_get_plan(self.h, _ptr(T), None, None, None, 0, ct.byref(nnz)))
+        return T.reshape(self.n, self.m).T.copy()
+
+    def plan_coo(self):
+        nnz = ct.c_int64()
+        self._check(self._L.sro_get_plan(self.h, None, None, None, None, 0, ct.byref(nnz)))
+        k = nnz.value
+        r = np.empty(k, dtype=np.int32)
+        c = np.empty(k, dtype=np.int32)
+        v = np.empty(k)
+        self._check(self._L.sro_get_plan(self.h, None, _ptr(r), _ptr(c), _ptr(v), k, ct.byref(nnz)))
+        return r, c, v
+
+    def rowsums(self):
+        r = np.empty(self.m)
+        self._check(self._L.sro_get_rowsums(self.h, _ptr(r)))
+        return r
+
+    def reset(self):
+        self._check(self._L.sro_reset(self.h))
