@@ -117,6 +117,21 @@ typedef struct {
   double device_ms;       /* device time of the call (CUDA events on the solver stream) */
 } sro_result;
 
+/* Kernel accounting of a handle (for benchmarks): launches of this library's
+ * kernels and, when timing is on, device milliseconds per kernel family,
+ * measured with CUDA events on the solver stream around each launch. */
+typedef struct {
+  int64_t kernel_launches;  /* every kernel this handle launched */
+  int64_t bcfw_launches;    /* persistent sequential-BCFW kernel (k_bcfw) */
+  int64_t bcfw_steps;
+  double bcfw_ms;
+  int64_t sweep_launches;   /* LMO sweeps (gap checks, GA refresh, FW / batched LMO) */
+  int64_t sweep_columns;
+  double sweep_ms;
+  int64_t block_steps;      /* FW / batched plain steps (all their kernels) */
+  double block_ms;
+} sro_stats;
+
 /* Create a solver. a: host fp64[m] (source marginal), b: host fp64[n] (target
  * marginal), copied. cost as described above. T starts at the first-row
  * vertex T^(0) = (b_1 e_1, ..., b_n e_1).
@@ -151,6 +166,12 @@ sro_status sro_get_rowsums(sro_handle h, double* r);
 
 /* Back to T^(0), k = 0; clears the variant/options/seed lock. */
 sro_status sro_reset(sro_handle h);
+
+/* Copy the accounting into *out; reset it to zero if reset != 0. */
+sro_status sro_get_stats(sro_handle h, sro_stats* out, int32_t reset);
+
+/* Enable (1) / disable (0) per-kernel CUDA-event timing (adds no host syncs). */
+sro_status sro_set_timing(sro_handle h, int32_t on);
 
 void sro_destroy(sro_handle h);
 const char* sro_last_error(sro_handle h);

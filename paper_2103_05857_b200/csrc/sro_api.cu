@@ -72,7 +72,50 @@ struct Solver {
   int *rowcnt = nullptr, *rowstart = nullptr, *cursor = nullptr, *tmp = nullptr, *sorted = nullptr;
   double* X = nullptr;
   int num_sms = 148;
+  // accounting
+  sro_stats stats{};
+  bool timing = false;
+  struct Pending { cudaEvent_t a, b; int cat; int64_t units; };
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<Pending> pending;
 };
+
+enum { CAT_BCFW = 0, CAT_SWEEP = 1, CAT_BLOCK = 2 };
+
+cudaEvent_t take_event(Solver* s) {
+  if (s->ev_pool.empty()) { cudaEvent_t e; cudaEventCreate(&e); return e; }
+  cudaEvent_t e = s->ev_pool.back();
+  s->ev_pool.pop_back();
+  return e;
+}
+// open a timed region on the solver stream (no-op unless timing is on)
+int timed_begin(Solver* s) {
+  if (!s->timing) return -1;
+  Solver::Pending p{take_event(s), take_event(s), 0, 0};
+  cudaEventRecord(p.a, s->stream);
+  s->pending.push_back(p);
+  return (int)s->pending.size() - 1;
+}
+void timed_end(Solver* s, int idx, int cat, int64_t units) {
+  if (idx < 0) return;
+  Solver::Pending& p = s->pending[idx];
+  p.cat = cat; p.units = units;
+  cudaEventRecord(p.b, s->stream);
+}
+// after a stream sync: fold every completed region into the stats
+void resolve_timing(Solver* s) {
+  for (auto& p : s->pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+      if (p.cat == CAT_BCFW) s->stats.bcfw_ms += ms;
+      else if (p.cat == CAT_SWEEP) s->stats.sweep_ms += ms;
+      else s->stats.block_ms += ms;
+    }
+    s->ev_pool.push_back(p.a);
+    s->ev_pool.push_back(p.b);
+  }
+  s->pending.clear();
+}
 
 #define CUDA_TRY(s, call)                                                                  \
   do {                                                                                     \
@@ -279,6 +322,10 @@ sro_status sweep(Solver* s, const int* col0_dev, int col0_mul, int col0_host, in
     SweepOut o;
     if (nslabs == 1) { o.j = out_j; o.minval = out_min; o.g = out_g; }
     else { o.j = s->part_j; o.minval = s->part_min; o.g = nullptr; }
+    const int tr = timed_begin(s);
+    s->stats.kernel_launches += nslabs > 1 ? 2 : 1;
+    s->stats.sweep_launches += 1;
+    s->stats.sweep_columns += L;
     kern<<<dim3(gx, nslabs), SWEEP_THREADS, smem, s->stream>>>(src, s->m, s->h, col0_dev, col0_mul, col0_host, L,
                                                              s->cnt, s->srow, s->sval, s->cap, s->b, o, stop,
                                                              s->status);
@@ -291,6 +338,7 @@ sro_status sweep(Solver* s, const int* col0_dev, int col0_mul, int col0_host, in
                                                             s->part_min, out_j, out_min, out_g, stop, s->status);
       CUDA_TRY(s, cudaGetLastError());
     }
+    timed_end(s, tr, CAT_SWEEP, L);
     return SRO_OK;
   });
 }
@@ -300,9 +348,11 @@ sro_status gap_sweep(Solver* s, double* total) {
   sro_status st = sweep(s, nullptr, 0, 0, s->n, s->sw_j, s->sw_min, s->sw_g, nullptr);
   if (st) return st;
   k_psum256<<<1, 256, 0, s->stream>>>(s->sw_g, s->n, s->scal + 4, nullptr, nullptr, nullptr);
+  s->stats.kernel_launches += 1;
   CUDA_TRY(s, cudaGetLastError());
   CUDA_TRY(s, cudaMemcpyAsync(total, s->scal + 4, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
   st = check_status(s);  // synchronises
+  resolve_timing(s);
   return st;
 }
 
@@ -345,8 +395,13 @@ template <class Col, int VAR, bool GA>
 sro_status launch_bcfw(Solver* s, BcfwArgs& A, Col col, size_t smem) {
   auto kern = k_bcfw<Col, VAR, GA>;
   CUDA_TRY(s, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int tr = timed_begin(s);
   kern<<<1, BCFW_THREADS, smem, s->stream>>>(A, col);
   CUDA_TRY(s, cudaGetLastError());
+  timed_end(s, tr, CAT_BCFW, A.steps);
+  s->stats.kernel_launches += 1;
+  s->stats.bcfw_launches += 1;
+  s->stats.bcfw_steps += A.steps;
   return SRO_OK;
 }
 
@@ -401,6 +456,7 @@ sro_status ga_global_refresh(Solver* s) {
   sro_status st = sweep(s, nullptr, 0, 0, s->n, s->sw_j, s->sw_min, s->G, nullptr);
   if (st) return st;
   k_fen_build<<<1, 32, 0, s->stream>>>(s->G, s->fen, s->n);
+  s->stats.kernel_launches += 1;
   CUDA_TRY(s, cudaGetLastError());
   return SRO_OK;
 }
@@ -416,6 +472,7 @@ sro_status ga_initialise(Solver* s) {
   if (st) return st;
   k_ga_init<<<64, 256, 0, s->stream>>>(s->G, s->fen, s->n, d_cmax, s->lambda);
   k_fen_build<<<1, 32, 0, s->stream>>>(s->G, s->fen, s->n);
+  s->stats.kernel_launches += 3;
   CUDA_TRY(s, cudaGetLastError());
   return SRO_OK;
 }
@@ -446,6 +503,7 @@ sro_status plain_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
                             bool stop_check, double* trace_dev) {
   sro_status st = ensure_block_ws(s, L);
   if (st) return st;
+  const int trb = timed_begin(s);
   const int* stop = stop_check ? s->stop : nullptr;
   st = sweep(s, col0_dev, col0_mul, 0, L, s->sw_j, s->sw_min, s->sw_g, stop);
   if (st) return st;
@@ -477,6 +535,9 @@ sro_status plain_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
   k_update_cols<<<gL, tpb, 0, s->stream>>>(A);
   k_rowsum_update<<<gM, tpb, 0, s->stream>>>(A);
   CUDA_TRY(s, cudaGetLastError());
+  s->stats.kernel_launches += 14;
+  s->stats.block_steps += 1;
+  timed_end(s, trb, CAT_BLOCK, L);
   return SRO_OK;
 }
 
@@ -497,6 +558,7 @@ sro_status objective_dev(Solver* s, double* f_host) {
   k_pen<<<(s->m + 255) / 256, 256, 0, s->stream>>>(s->r, s->a, s->m, s->sw_min);
   k_psum256<<<1, 256, 0, s->stream>>>(s->sw_min, s->m, s->scal + 5, nullptr, nullptr, nullptr);
   k_objective_final<<<1, 1, 0, s->stream>>>(s->scal + 4, s->scal + 5, s->lambda, s->scal + 7);
+  s->stats.kernel_launches += 5;
   CUDA_TRY(s, cudaGetLastError());
   CUDA_TRY(s, cudaMemcpyAsync(f_host, s->scal + 7, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
   CUDA_TRY(s, cudaStreamSynchronize(s->stream));
@@ -506,6 +568,7 @@ sro_status objective_dev(Solver* s, double* f_host) {
 sro_status do_reset(Solver* s) {
   k_init_plan<<<s->num_sms, 256, 0, s->stream>>>(s->b, s->a, s->r, s->h, s->cnt, s->srow, s->sval, s->m, s->n, s->cap,
                                                 s->lambda);
+  s->stats.kernel_launches += 1;
   CUDA_TRY(s, cudaGetLastError());
   CUDA_TRY(s, cudaMemsetAsync(s->stop, 0, sizeof(int), s->stream));
   s->k = 0;
@@ -521,6 +584,8 @@ void free_solver(Solver* s) {
                   s->rowcnt, s->rowstart, s->cursor, s->tmp, s->sorted, s->X};
   for (void* p : ptrs) if (p) cudaFree(p);
   if (s->owns_cost) { if (s->C) cudaFree(s->C); if (s->x) cudaFree(s->x); if (s->y) cudaFree(s->y); }
+  for (auto& p : s->pending) { s->ev_pool.push_back(p.a); s->ev_pool.push_back(p.b); }
+  for (auto e : s->ev_pool) cudaEventDestroy(e);
   if (s->ev0) cudaEventDestroy(s->ev0);
   if (s->ev1) cudaEventDestroy(s->ev1);
   if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
@@ -695,6 +760,7 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
       CUDA_TRY(s, cudaMemcpyAsync(&G, s->scal + 0, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
       CUDA_TRY(s, cudaMemcpyAsync(&stopped, s->stop, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
       st = check_status(s);
+      resolve_timing(s);
       if (st) return st;
       out->gap = G; out->gap_checks++;
       out->entries_scanned += (int64_t)m * n;
@@ -726,6 +792,7 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
                               o->trace ? s->trace + 9 * done : nullptr);
         if (st) return st;
         st = check_status(s);
+        resolve_timing(s);
         if (st) return st;
         out->entries_scanned += (int64_t)m * o->block_size;
         s->k++; done++;
@@ -740,6 +807,7 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
       int sd = 0;
       CUDA_TRY(s, cudaMemcpyAsync(&sd, s->steps_done, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
       st = check_status(s);
+      resolve_timing(s);
       s->k += sd; done += sd;
       out->entries_scanned += (int64_t)m * sd * ((ga && o->ga_inner && o->ga_post_update) ? 2 : 1);
       if (st) break;
@@ -821,6 +889,23 @@ sro_status sro_get_plan(sro_handle h, double* dense, int32_t* rows, int32_t* col
     }
   if (nnz) *nnz = q;
   if (rows && cols && vals && q > cap) { s->err = "COO capacity too small"; return SRO_ERR_CAPACITY; }
+  return SRO_OK;
+}
+
+sro_status sro_get_stats(sro_handle h, sro_stats* out, int32_t reset) {
+  if (!h || !out) return SRO_ERR_INVALID_ARG;
+  Solver* s = static_cast<Solver*>(h);
+  cudaSetDevice(s->device);
+  CUDA_TRY(s, cudaStreamSynchronize(s->stream));
+  resolve_timing(s);
+  *out = s->stats;
+  if (reset) s->stats = sro_stats{};
+  return SRO_OK;
+}
+
+sro_status sro_set_timing(sro_handle h, int32_t on) {
+  if (!h) return SRO_ERR_INVALID_ARG;
+  static_cast<Solver*>(h)->timing = on != 0;
   return SRO_OK;
 }
 

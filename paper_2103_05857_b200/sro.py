@@ -25,7 +25,7 @@ COST_KINDS = {"dense": 0, "sqeuclid": 1, "euclid": 2, "hash": 3}
 PRECS = {"f64": 0, "f32": 1}
 OK, NOT_CONVERGED = 0, 1
 EXPORTED_SYMBOLS = ("sro_create", "sro_solve", "sro_gap", "sro_objective", "sro_get_plan", "sro_get_rowsums",
-                    "sro_reset", "sro_destroy", "sro_last_error", "sro_version")
+                    "sro_reset", "sro_destroy", "sro_last_error", "sro_version", "sro_get_stats", "sro_set_timing")
 
 _STATUS = {0: "OK", 1: "NOT_CONVERGED", 2: "ERR_INVALID_ARG", 3: "ERR_DIMENSION", 4: "ERR_MARGINALS",
            5: "ERR_NONFINITE", 6: "ERR_CAPACITY", 7: "ERR_CUDA", 8: "ERR_NCCL", 9: "ERR_OOM", 10: "ERR_STATE"}
@@ -70,6 +70,12 @@ class SroResult(ct.Structure):
                 ("device_ms", ct.c_double)]
 
 
+class SroStats(ct.Structure):
+    _fields_ = [("kernel_launches", ct.c_int64), ("bcfw_launches", ct.c_int64), ("bcfw_steps", ct.c_int64),
+                ("bcfw_ms", ct.c_double), ("sweep_launches", ct.c_int64), ("sweep_columns", ct.c_int64),
+                ("sweep_ms", ct.c_double), ("block_steps", ct.c_int64), ("block_ms", ct.c_double)]
+
+
 _lib = None
 
 
@@ -99,6 +105,10 @@ def load_library():
         L.sro_destroy.restype = None
         L.sro_last_error.argtypes = [vp]
         L.sro_last_error.restype = ct.c_char_p
+        L.sro_get_stats.argtypes = [vp, ct.POINTER(SroStats), i32]
+        L.sro_get_stats.restype = ct.c_int
+        L.sro_set_timing.argtypes = [vp, i32]
+        L.sro_set_timing.restype = ct.c_int
         L.sro_version.argtypes = []
         L.sro_version.restype = ct.c_char_p
         _lib = L
@@ -238,3 +248,11 @@ class Solver:
 
     def reset(self):
         self._check(self._L.sro_reset(self.h))
+
+    def set_timing(self, on=True):
+        self._check(self._L.sro_set_timing(self.h, 1 if on else 0))
+
+    def stats(self, reset=False):
+        s = SroStats()
+        self._check(self._L.sro_get_stats(self.h, ct.byref(s), 1 if reset else 0))
+        return {f: getattr(s, f) for f, _ in SroStats._fields_}
