@@ -30,7 +30,11 @@ def needs_build() -> bool:
     return any(os.path.getmtime(s) > t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, phase_timing: bool = False) -> str:
+    if phase_timing:   # debug build with per-phase clock64 accounting in k_bcfw
+        out = os.path.join(HERE, "libsro_phase.so")
+        subprocess.check_call([NVCC, *FLAGS, "-DSRO_PHASE_TIMING", "-o", out, os.path.join(CSRC, "sro_api.cu")])
+        return out
     if force or needs_build():
         cmd = [NVCC, *FLAGS, "-o", LIB + ".tmp", os.path.join(CSRC, "sro_api.cu")]
         if verbose:
@@ -41,4 +45,4 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, phase_timing="--phase" in sys.argv))

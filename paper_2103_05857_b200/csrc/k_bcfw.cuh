@@ -3,14 +3,20 @@
 // (Alg. A.3), each with U / P / GA sampling (Alg. A.4,
 // P:1848-1869) and the decay or exact line-search step (Eq. 10, Eq. 14).
 //
-// One CTA runs a whole segment of dependent steps (up to the next gap check
-// or GA refresh) with no host round trip. h lives in shared memory; the next
-// visited column is prefetched into registers while the current step's
-// reduction and update run (U / P / explicit visit orders are known ahead).
-// Per step: all warps do the LMO over the column (Eq. 9) and a CTA argmin;
-// warp 0 then does the O(|supp|) part — column gap, line search, sparse
-// column update and the r/h update of the touched rows — one support entry
-// per lane (slab_cap <= 31). Roofline: latency (one dependent step at a time).
+// One CTA runs a whole segment of dependent steps (up to the next gap check or
+// GA refresh) with no host round trip. Per step:
+//   1. all 16 warps: LMO over the visited column (Eq. 9) -> CTA argmin;
+//   2. warp 0: the O(|supp|) part — column gap (Eq. 11), line search (Eq. 10 /
+//      Eq. 14), sparse column update and the r/h refresh of the touched rows —
+//      one support entry per lane (slab_cap <= 31).
+// Fast layout (SMEM = true): h, r and the per-column support counts live in
+// shared memory for the whole segment; the next visited column is staged into
+// a shared-memory double buffer with cp.async while the current step runs
+// (colour costs: the source colours are staged once), and warp 0 prefetches
+// the next column's support slab into registers, so the serial part touches
+// no global memory on its critical path. Generic layout (SMEM = false): the
+// same arithmetic on global arrays, for sizes that do not fit.
+// Roofline: latency of one dependent step.
 #pragma once
 #include "k_sweep.cuh"
 #include "sro_device.cuh"
@@ -36,90 +42,316 @@ struct BcfwArgs {
   int steps;
   long long k0;          // global step counter at segment start
   int step_rule;         // 0 DEC, 1 ELS
-  // GA
-  double* G;             // n stored gaps
-  double* fen;           // n+1 Fenwick tree
+  double* G;             // GA stored gaps (n)
+  double* fen;           // GA Fenwick tree (n+1)
   int ga_inner, ga_post;
   unsigned long long seed;
-  int ga_smem;           // 1: G and fen staged in shared memory
-  int x_smem;            // colour sources: 1 = x staged in shared memory
-  int h_smem;            // 1: h staged in shared memory (m small enough)
-  // outputs
+  int ga_smem;           // GA arrays staged in shared memory
   int* status;
   int* steps_done;
   double* trace;         // optional: 9 doubles per step (k,i,j,v,dir,gamma,num,den,minval)
+  long long* phase;      // SRO_PHASE_TIMING builds only: 8 accumulated clock64 phase totals
+  double cmax;           // max_{k,i} |C_ki| (fp32 LMO filter window)
+  int a_smem;            // a staged in shared memory
+  int visit_smem;        // the segment's visit list staged in shared memory
 };
 
+#ifdef SRO_PHASE_TIMING
+struct PhaseState { long long acc[16]; long long t; };
+#define PHASE_MARK(idx)                                       \
+  do {                                                        \
+    if (threadIdx.x == 0) {                                   \
+      const long long t_ = clock64();                         \
+      g_ph->acc[idx] += t_ - g_ph->t;                         \
+      g_ph->t = t_;                                           \
+    }                                                         \
+  } while (0)
+#else
+#define PHASE_MARK(idx) do {} while (0)
+#endif
+
+__device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
+__device__ __forceinline__ double dninf() { return __longlong_as_double(0xfff0000000000000LL); }
+__host__ __device__ __forceinline__ size_t rup16(size_t x) { return (x + 15) / 16 * 16; }
+
 // ---------------------------------------------------------------------------
-// Column providers: the LMO over one column with rows split across the CTA.
+// cp.async helpers
 // ---------------------------------------------------------------------------
-template <typename T, int MAXV>
-struct BcDense {
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
+}
+template <int BYTES>
+__device__ __forceinline__ void cp_async_small(void* sdst, const void* gsrc) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gsrc), "n"(BYTES));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
+// ---------------------------------------------------------------------------
+// Column providers
+// ---------------------------------------------------------------------------
+// Dense column staged in a shared-memory double buffer by cp.async (fast layout).
+template <typename T>
+struct ColStaged {
   using V = typename Vec<T>::type;
   static constexpr int W = Vec<T>::W;
+  static constexpr bool STAGED = true;
+  static constexpr bool FILTER = sizeof(T) == 4;   // binary32 costs: fp32 filter + exact fp64 check
   const T* C;
   int64_t ld;
-  int m, nvec;
-  V cur[MAXV], nxt[MAXV];
-  __device__ void init(const T* C_, int64_t ld_, int m_) { C = C_; ld = ld_; m = m_; nvec = m_ / W; }
-  __device__ __forceinline__ void fetch(int i) {
-    const V* p = reinterpret_cast<const V*>(C + (int64_t)i * ld);
-#pragma unroll
-    for (int u = 0; u < MAXV; u++) {
-      int q = threadIdx.x + u * BCFW_THREADS;
-      if (q < nvec) nxt[u] = __ldg(p + q);
-    }
+  int m;
+  T* buf0;
+  T* buf1;
+  static size_t smem_bytes(int m) { return 2 * rup16((size_t)m * sizeof(T)); }
+  __device__ __forceinline__ T* buf(int slot) const { return slot ? buf1 : buf0; }
+  __device__ __forceinline__ void setup(char* region) {
+    buf0 = reinterpret_cast<T*>(region);
+    buf1 = reinterpret_cast<T*>(region + rup16((size_t)m * sizeof(T)));
   }
-  __device__ __forceinline__ void advance() {
-#pragma unroll
-    for (int u = 0; u < MAXV; u++) cur[u] = nxt[u];
+  // every thread issues its share of the copy of column i into buffer `slot`
+  __device__ __forceinline__ void issue(int i, int slot) const {
+    const T* src = C + (int64_t)i * ld;
+    T* dst = buf(slot);
+    const int nvec = m / W;
+    for (int q = threadIdx.x; q < nvec; q += BCFW_THREADS) cp_async16(dst + W * q, src + W * q);
+    const int k = nvec * W + threadIdx.x;
+    if (k < m) cp_async_small<sizeof(T)>(dst + k, src + k);
+    cp_async_commit();
   }
-  __device__ __forceinline__ void local_argmin(int i, const double* hs, double& best, int& bj) const {
-#pragma unroll
-    for (int u = 0; u < MAXV; u++) {
-      int q = threadIdx.x + u * BCFW_THREADS;
-      if (q < nvec) proc4(cur[u], W * q, hs, best, bj);
-    }
-    // rows beyond the register-prefetched part: direct loads (large m)
-    const V* p = reinterpret_cast<const V*>(C + (int64_t)i * ld);
-    for (int q = threadIdx.x + MAXV * BCFW_THREADS; q < nvec; q += BCFW_THREADS) proc4(__ldg(p + q), W * q, hs, best, bj);
-    int k = nvec * W + threadIdx.x;  // tail rows (m % W)
+  __device__ __forceinline__ void local_argmin(int, int slot, const double* hs, double& best, int& bj) const {
+    const T* c = buf(slot);
+    const V* cv = reinterpret_cast<const V*>(c);
+    const int nvec = m / W;
+    for (int q = threadIdx.x; q < nvec; q += BCFW_THREADS) proc4(cv[q], W * q, hs, best, bj);
+    const int k = nvec * W + threadIdx.x;
     if (k < m) {
-      double x = d_add((double)C[(int64_t)i * ld + k], hs[k]);
+      const double x = d_add((double)c[k], hs[k]);
       if (x < best) { best = x; bj = k; }
     }
   }
-  __device__ __forceinline__ double cost(int k, int i) const { return (double)C[(int64_t)i * ld + k]; }
+  __device__ __forceinline__ double cost(int k, int, int slot) const { return (double)buf(slot)[k]; }
+  // Exact LMO with a binary32 filter: F_k = fl32(c_k + fl32(h_k)) is within
+  // eps = 2^-24 (cmax + (2 + 2^-24) hmax) of c_k + h_k and the exact value
+  // V_k = fl64(c_k + h_k) within 2^-53 (cmax + hmax), so every row that ties
+  // or beats the thread's exact minimum has F_k <= min F + delta with
+  // delta = 2^-22 (cmax + 2 hmax) + 1e-30 >= 2 eps + 2 * 2^-53 (...). Only those
+  // candidate rows are evaluated exactly in binary64 (ascending rows, strict <),
+  // so the result is the thread's exact lowest-index argmin of V.
+  __device__ __forceinline__ void local_argmin_filt(int slot, const double* hs, const float* hs32, float delta,
+                                                    double& best, int& bj) const {
+    const float4* cv = reinterpret_cast<const float4*>(buf(slot));
+    const float4* hv = reinterpret_cast<const float4*>(hs32);
+    const int nvec = m / 4;
+    float4 cq[4], fq[4];
+    float fmin = __int_as_float(0x7f800000);
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int q = threadIdx.x + u * BCFW_THREADS;
+      if (q < nvec) {
+        cq[u] = reinterpret_cast<const float4*>(cv)[q];
+        const float4 hh = hv[q];
+        fq[u] = make_float4(__fadd_rn(cq[u].x, hh.x), __fadd_rn(cq[u].y, hh.y), __fadd_rn(cq[u].z, hh.z),
+                            __fadd_rn(cq[u].w, hh.w));
+        fmin = fminf(fmin, fminf(fminf(fq[u].x, fq[u].y), fminf(fq[u].z, fq[u].w)));
+      }
+    }
+    const int kt = nvec * 4 + threadIdx.x;
+    float ct = 0.f, ft = __int_as_float(0x7f800000);
+    if (kt < m) { ct = buf(slot)[kt]; ft = __fadd_rn(ct, hs32[kt]); fmin = fminf(fmin, ft); }
+    const float thr = __fadd_ru(fmin, delta);
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int q = threadIdx.x + u * BCFW_THREADS;
+      if (q < nvec) {
+        const int k = 4 * q;
+        if (fq[u].x <= thr) { const double v = d_add((double)cq[u].x, hs[k]); if (v < best) { best = v; bj = k; } }
+        if (fq[u].y <= thr) { const double v = d_add((double)cq[u].y, hs[k + 1]); if (v < best) { best = v; bj = k + 1; } }
+        if (fq[u].z <= thr) { const double v = d_add((double)cq[u].z, hs[k + 2]); if (v < best) { best = v; bj = k + 2; } }
+        if (fq[u].w <= thr) { const double v = d_add((double)cq[u].w, hs[k + 3]); if (v < best) { best = v; bj = k + 3; } }
+      }
+    }
+    if (kt < m && ft <= thr) { const double v = d_add((double)ct, hs[kt]); if (v < best) { best = v; bj = kt; } }
+  }
 };
 
-template <typename T, bool EUCLID>
-struct BcColour {
-  const T* x;    // global 3m
-  const T* xs;   // SoA in smem (x_smem) or nullptr
+// Dense column read straight from global memory (generic layout).
+template <typename T>
+struct ColDirect {
+  using V = typename Vec<T>::type;
+  static constexpr int W = Vec<T>::W;
+  static constexpr bool STAGED = false;
+  static constexpr bool FILTER = false;
+  const T* C;
+  int64_t ld;
+  int m;
+  static size_t smem_bytes(int) { return 0; }
+  __device__ __forceinline__ void local_argmin_filt(int, const double*, const float*, float, double&, int&) const {}
+  __device__ __forceinline__ void setup(char*) {}
+  __device__ __forceinline__ void issue(int, int) const {}
+  __device__ __forceinline__ void local_argmin(int i, int, const double* hs, double& best, int& bj) const {
+    const V* p = reinterpret_cast<const V*>(C + (int64_t)i * ld);
+    const int nvec = m / W;
+    for (int q = threadIdx.x; q < nvec; q += BCFW_THREADS) proc4(__ldg(p + q), W * q, hs, best, bj);
+    const int k = nvec * W + threadIdx.x;
+    if (k < m) {
+      const double x = d_add((double)__ldg(C + (int64_t)i * ld + k), hs[k]);
+      if (x < best) { best = x; bj = k; }
+    }
+  }
+  __device__ __forceinline__ double cost(int k, int i, int) const { return (double)__ldg(C + (int64_t)i * ld + k); }
+};
+
+// Colour costs computed on the fly; source colours staged (SoA) in shared memory if XS.
+template <typename T, bool XS>
+struct ColColour {
+  static constexpr bool STAGED = false;
+  static constexpr bool FILTER = false;
+  __device__ __forceinline__ void local_argmin_filt(int, const double*, const float*, float, double&, int&) const {}
+  const T* x;
   const T* y;
   int m;
-  __device__ void init(const T* x_, const T* xs_, const T* y_, int m_) { x = x_; xs = xs_; y = y_; m = m_; }
-  __device__ __forceinline__ void fetch(int) {}
-  __device__ __forceinline__ void advance() {}
-  __device__ __forceinline__ void local_argmin(int i, const double* hs, double& best, int& bj) const {
+  int euclid;
+  T* xs;
+  static size_t smem_bytes(int m) { return XS ? rup16((size_t)3 * m * sizeof(T)) : 0; }
+  __device__ __forceinline__ void setup(char* region) {
+    if (XS) {
+      xs = reinterpret_cast<T*>(region);
+      for (int k = threadIdx.x; k < m; k += BCFW_THREADS) {
+        xs[k] = x[3 * (int64_t)k];
+        xs[m + k] = x[3 * (int64_t)k + 1];
+        xs[2 * m + k] = x[3 * (int64_t)k + 2];
+      }
+    }
+  }
+  __device__ __forceinline__ void issue(int, int) const {}
+  __device__ __forceinline__ void xk(int k, T& x0, T& x1, T& x2) const {
+    if (XS) { x0 = xs[k]; x1 = xs[m + k]; x2 = xs[2 * m + k]; }
+    else { x0 = x[3 * (int64_t)k]; x1 = x[3 * (int64_t)k + 1]; x2 = x[3 * (int64_t)k + 2]; }
+  }
+  __device__ __forceinline__ double c(T x0, T x1, T x2, T y0, T y1, T y2) const {
+    return euclid ? colour_cost<true>(x0, x1, x2, y0, y1, y2) : colour_cost<false>(x0, x1, x2, y0, y1, y2);
+  }
+  __device__ __forceinline__ void local_argmin(int i, int, const double* hs, double& best, int& bj) const {
     const T y0 = y[3 * (int64_t)i], y1 = y[3 * (int64_t)i + 1], y2 = y[3 * (int64_t)i + 2];
     for (int k = threadIdx.x; k < m; k += BCFW_THREADS) {
       T x0, x1, x2;
-      if (xs) { x0 = xs[k]; x1 = xs[m + k]; x2 = xs[2 * m + k]; }
-      else { x0 = x[3 * (int64_t)k]; x1 = x[3 * (int64_t)k + 1]; x2 = x[3 * (int64_t)k + 2]; }
-      double v = d_add(colour_cost<EUCLID>(x0, x1, x2, y0, y1, y2), hs[k]);
+      xk(k, x0, x1, x2);
+      const double v = d_add(c(x0, x1, x2, y0, y1, y2), hs[k]);
       if (v < best) { best = v; bj = k; }
     }
   }
-  __device__ __forceinline__ double cost(int k, int i) const {
-    return colour_cost<EUCLID>(x[3 * (int64_t)k], x[3 * (int64_t)k + 1], x[3 * (int64_t)k + 2], y[3 * (int64_t)i],
-                               y[3 * (int64_t)i + 1], y[3 * (int64_t)i + 2]);
+  __device__ __forceinline__ double cost(int k, int i, int) const {
+    T x0, x1, x2;
+    xk(k, x0, x1, x2);
+    return c(x0, x1, x2, y[3 * (int64_t)i], y[3 * (int64_t)i + 1], y[3 * (int64_t)i + 2]);
   }
 };
 
 // ---------------------------------------------------------------------------
+// psum256 over m rows of a vector that is zero except at up to 32 rows, one
+// per lane, rows strictly ascending with the lane (R19). Chunk partials are
+// left-to-right sums from +0.0; entries of one chunk are consecutive lanes,
+// so the partials are a segmented sequential scan costing (longest segment)
+// dependent adds. `slots` is warp-private __shared__ double[256], +0.0 on
+// entry and exit.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sparse_psum256_seg(int m, int cnt, int row, double x, double* slots) {
+  const int lane = threadIdx.x & 31;
+  const bool valid = lane < cnt;
+  const int c = valid ? chunk_index(row, m, 256) : -1;
+  const int cprev = __shfl_up_sync(FULL, c, 1);
+  const int cnext = __shfl_down_sync(FULL, c, 1);
+  const bool start = valid && (lane == 0 || cprev != c);
+  const bool last = valid && (lane == cnt - 1 || cnext != c);
+  const unsigned smask = __ballot_sync(FULL, start);
+  const int seg0 = 31 - __clz(smask & (0xffffffffu >> (31 - lane)));
+  const int pos = valid ? lane - seg0 : 0;
+  double acc = valid ? d_add(0.0, x) : 0.0;
+  const int maxpos = (int)__reduce_max_sync(FULL, (unsigned)pos);
+  for (int t = 1; t <= maxpos; t++) {
+    const double prev = __shfl_up_sync(FULL, acc, 1);
+    if (pos == t) acc = d_add(prev, x);
+  }
+  if (last) slots[c] = acc;
+  __syncwarp();
+  double s[8];
+#pragma unroll
+  for (int t = 0; t < 8; t++) s[t] = slots[8 * lane + t];
+  const double v = warp_pair_tree(tree8(s));
+  __syncwarp();
+  if (last) slots[c] = 0.0;
+  __syncwarp();
+  return v;
+}
+
+// Sequential left-to-right sum (from +0.0) of the values of lanes 0..cnt-1,
+// done by lane 0 from shared memory (independent loads, one dependent add per
+// term). `buf` is warp-private __shared__ double[32]. Result in every lane.
+__device__ __forceinline__ double warp_seq_sum_sm(double x, int cnt, double* buf) {
+  const int lane = threadIdx.x & 31;
+  if (lane < cnt) buf[lane] = x;
+  __syncwarp();
+  double acc = 0.0;
+  if (lane == 0)
+    for (int q = 0; q < cnt; q++) acc = d_add(acc, buf[q]);
+  acc = __shfl_sync(FULL, acc, 0);
+  __syncwarp();
+  return acc;
+}
+
+// psum256 over m rows of a vector that is zero except at up to 32 rows (one per
+// lane, rows ascending with the lane), i.e. exactly chunk_tree_sum(x, m, 256)
+// of R19. Lane 0 forms the chunk partials (left-to-right from +0.0) of the K
+// non-empty chunks, then combines them in the shape of the 256-leaf
+// adjacent-pair tree: zero leaves are additive identities, so the dense tree
+// reduces to merging, K-1 times, the adjacent pair of non-empty subtrees whose
+// lowest common ancestor is lowest (smallest highest-differing chunk bit).
+// bx: warp-private __shared__ double[32]; bc: int[32].
+__device__ __forceinline__ double warp_sparse_psum256_l0(int m, int cnt, int row, double x, double* bx, int* bc) {
+  const int lane = threadIdx.x & 31;
+  if (lane < cnt) { bc[lane] = chunk_index(row, m, 256); bx[lane] = x; }
+  __syncwarp();
+  double res = 0.0;
+  if (lane == 0) {
+    int K = 0;
+    for (int q = 0; q < cnt; q++) {
+      const int c = bc[q];
+      const double v = bx[q];
+      if (K > 0 && bc[K - 1] == c) bx[K - 1] = d_add(bx[K - 1], v);
+      else { bc[K] = c; bx[K] = d_add(0.0, v); K++; }
+    }
+    while (K > 1) {
+      int t = 0, best = 32;
+      for (int u = 0; u + 1 < K; u++) {
+        const int hdb = 31 - __clz(bc[u] ^ bc[u + 1]);
+        if (hdb < best) { best = hdb; t = u; }
+      }
+      bx[t] = d_add(bx[t], bx[t + 1]);
+      for (int u = t + 1; u + 1 < K; u++) { bx[u] = bx[u + 1]; bc[u] = bc[u + 1]; }
+      K--;
+    }
+    res = K ? bx[0] : 0.0;
+  }
+  res = __shfl_sync(FULL, res, 0);
+  __syncwarp();
+  return res;
+}
+
+// Warp argmax of (value, row), lowest row on ties, via REDUX on order keys.
+__device__ __forceinline__ void warp_argmax_redux(double& v, int& j, bool valid) {
+  const unsigned long long key = valid ? okey(v) : 0ULL;
+  const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+  const unsigned m1 = __reduce_max_sync(FULL, hi);
+  const unsigned m2 = __reduce_max_sync(FULL, hi == m1 ? lo : 0u);
+  const unsigned m3 = __reduce_min_sync(FULL, (valid && hi == m1 && lo == m2) ? (unsigned)j : 0x7fffffffu);
+  j = (int)m3;
+  v = okey_inv(((unsigned long long)m1 << 32) | m2);
+}
+
+// ---------------------------------------------------------------------------
 // GA sampler on a Fenwick tree over max(G_i, 0) (Alg. A.4 line 2; R14-R17).
-// Single-thread functions; fen is 1-based, fen[1..n].
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ double wpos(double g) { return g > 0.0 ? g : 0.0; }
 
@@ -148,237 +380,407 @@ __device__ __forceinline__ void ga_add(double* fen, int n, int i0, double delta)
 }
 
 // ---------------------------------------------------------------------------
+// Warp 0: the O(|supp|) part of one step (all 32 lanes call it).
+// In: column i, LMO result (j, mv), b_i, support size c0 and the lane's slab
+// entry (rw, tv) with its gradient gk = C_{rw,i} + h_rw (lanes < c0).
+// Applies the update to (r, h) and to the slab of column i.
+// Out (per lane): the new entries (erow, tnew, keep) for reuse by the caller.
+// ---------------------------------------------------------------------------
+struct StepOut {
+  int dir, vrow, nk, erow;
+  bool abort, keep, noop, ev;
+  double gamma, num, den, gfw, tnew, hnew;
+  unsigned kmask;
+};
+
+#ifdef SRO_PHASE_TIMING
+#define SP_MARK(idx) do { if (threadIdx.x == 0 && sp_ph) { const long long t_ = clock64(); sp_ph->acc[idx] += t_ - sp_ph->t; sp_ph->t = t_; } } while (0)
+#define SP_PARAM , PhaseState* sp_ph
+#define SP_ARG , g_ph
+#else
+#define SP_MARK(idx) do {} while (0)
+#define SP_PARAM
+#define SP_ARG
+#endif
+template <int VAR>
+__device__ __forceinline__ StepOut serial_step(const BcfwArgs& A, long long kk, int i, int j, double mv, double bi,
+                                               int c0, int rw, double tv, double gk, double* r, double* h,
+                                               float* h32, const double* a, int* cnt2, double* slots,
+                                               float* hmax SP_PARAM) {
+  const int lane = threadIdx.x & 31;
+  const int m = A.m, n = A.n, cap = A.cap;
+  const double lam = A.lambda;
+  StepOut o;
+  o.dir = 0; o.vrow = -1; o.gamma = 0.0; o.num = 0.0; o.den = 0.0; o.hnew = 0.0;
+  double* bx = slots;
+  int* bc = reinterpret_cast<int*>(slots + 32);
+  double* sb = slots + 64;
+  const double dot = warp_seq_sum_sm(d_mul(tv, gk), c0, sb);
+  o.gfw = d_sub(dot, d_mul(bi, mv));
+  SP_MARK(8);
+  o.abort = !(mv < 1.0e308 && mv > -1.0e308);
+  double gv = dninf();
+  int vrow = 0x7fffffff;
+  if (VAR != VAR_PLAIN) {
+    gv = lane < c0 ? gk : dninf();
+    vrow = lane < c0 ? rw : 0x7fffffff;
+    warp_argmax_redux(gv, vrow, lane < c0);
+    o.vrow = vrow;
+  }
+  const bool j_in = __ballot_sync(FULL, lane < c0 && rw == j) != 0u;
+  const int ins = __popc(__ballot_sync(FULL, lane < c0 && rw < j));
+  // merged support supp(t_i) U {j}, rows ascending, one entry per lane
+  const int M = c0 + (j_in ? 0 : 1);
+  int src = (j_in || lane < ins) ? lane : lane - 1;
+  if (src < 0) src = 0;
+  int mrow = __shfl_sync(FULL, rw, src);
+  double mt = __shfl_sync(FULL, tv, src);
+  if (!j_in && lane == ins) { mrow = j; mt = 0.0; }
+  const bool mvalid = lane < M;
+  SP_MARK(9);
+  // source marginal of the rows this lane may update (loads issued early)
+  const double a_m = a[mvalid ? mrow : 0];
+  const double a_s = (VAR == VAR_AWAY && lane < c0) ? a[rw] : 0.0;
+
+  double tnew = mt;
+  bool use_merged = true;
+  if (VAR == VAR_PLAIN) {
+    const double d = d_sub((mvalid && mrow == j) ? bi : 0.0, mvalid ? mt : 0.0);
+    const double D = d_add(0.0, d);
+    o.den = warp_sparse_psum256_l0(m, M, mrow, d_mul(D, D), bx, bc);
+    SP_MARK(10);
+    o.num = d_mul(lam, d_add(0.0, o.gfw));
+    if (A.step_rule == 1) {
+      if (!(o.num > 0.0) || o.den == 0.0) o.gamma = 0.0;
+      else { o.gamma = d_div(o.num, o.den); if (o.gamma > 1.0) o.gamma = 1.0; }
+    } else {
+      o.gamma = d_div((double)(2LL * n), (double)(kk + 2LL * n));
+    }
+    const double omg = d_sub(1.0, o.gamma), gb = d_mul(o.gamma, bi);
+    tnew = d_mul(omg, mt);
+    if (mrow == j) tnew = d_add(tnew, gb);
+    SP_MARK(11);
+  } else if (VAR == VAR_AWAY) {
+    const double gaw = d_sub(d_mul(bi, gv), dot);
+    const bool use_fw = (c0 == 1) || (o.gfw >= gaw);
+    if (use_fw) {
+      const double d = d_sub((mvalid && mrow == j) ? bi : 0.0, mvalid ? mt : 0.0);
+      o.den = warp_sparse_psum256_l0(m, M, mrow, d_mul(d, d), bx, bc);
+      o.num = d_mul(lam, d_add(o.gfw, 0.0));
+      if (!(o.num > 0.0) || o.den == 0.0) o.gamma = 0.0;
+      else { o.gamma = d_div(o.num, o.den); if (o.gamma > 1.0) o.gamma = 1.0; }
+      const double omg = d_sub(1.0, o.gamma), gb = d_mul(o.gamma, bi);
+      tnew = d_mul(omg, mt);
+      if (mrow == j) tnew = d_add(tnew, gb);
+    } else {
+      o.dir = 1;
+      use_merged = false;
+      const double tvv = __shfl_sync(FULL, tv, __ffs(__ballot_sync(FULL, lane < c0 && rw == vrow)) - 1);
+      const double d = (lane < c0) ? ((rw == vrow) ? d_sub(tv, bi) : tv) : 0.0;
+      o.den = warp_sparse_psum256_l0(m, c0, rw, d_mul(d, d), bx, bc);
+      o.num = d_mul(lam, d_add(gaw, 0.0));
+      const double alpha = d_div(tvv, bi);
+      const double gmax = d_div(alpha, d_sub(1.0, alpha));
+      if (!(o.num > 0.0) || o.den == 0.0) o.gamma = 0.0;
+      else { o.gamma = d_div(o.num, o.den); if (o.gamma > gmax) o.gamma = gmax; }
+      const double opg = d_add(1.0, o.gamma), gb = d_mul(o.gamma, bi);
+      tnew = d_mul(opg, tv);
+      if (lane < c0 && rw == vrow) {
+        tnew = d_sub(tnew, gb);
+        if (o.gamma == gmax || tnew < 0.0) tnew = 0.0;
+      }
+    }
+  } else {  // VAR_PAIR
+    if (vrow == j) {
+      o.dir = 3;
+    } else {
+      o.dir = 2;
+      const double tvv = __shfl_sync(FULL, tv, __ffs(__ballot_sync(FULL, lane < c0 && rw == vrow)) - 1);
+      const double dv = d_sub(gv, mv);
+      o.num = d_mul(lam, dv);
+      o.den = d_mul(2.0, bi);
+      const double alpha = d_div(tvv, bi);
+      if (!(o.num > 0.0)) o.gamma = 0.0;
+      else { o.gamma = d_div(o.num, o.den); if (o.gamma > alpha) o.gamma = alpha; }
+      double mu = d_mul(o.gamma, bi);
+      const bool drop = (o.gamma == alpha) || (mu >= tvv);
+      if (drop) mu = tvv;
+      tnew = mt;
+      if (mrow == j) tnew = d_add(mt, mu);
+      if (mrow == vrow) tnew = drop ? 0.0 : d_sub(mt, mu);
+    }
+  }
+  // apply: new column (exact zeros dropped), r += (t' - t), h refresh
+  o.noop = (VAR == VAR_PAIR && o.dir == 3);
+  const int E = use_merged ? M : c0;
+  const int erow = use_merged ? mrow : rw;
+  const double eold = use_merged ? mt : tv;
+  const double aval = use_merged ? a_m : a_s;
+  if (o.noop) tnew = eold;
+  const bool ev = lane < E;
+  const bool keep = ev && tnew != 0.0;
+  o.kmask = __ballot_sync(FULL, keep);
+  o.nk = __popc(o.kmask);
+  if (!o.noop && o.nk > cap) o.abort = true;
+  SP_MARK(12);
+  if (!o.abort && !o.noop) {
+    if (ev) {
+      const double Dp = d_add(0.0, d_sub(tnew, eold));
+      const double rn = d_add(r[erow], Dp);
+      const double hn = d_div(d_sub(rn, aval), lam);
+      r[erow] = rn;
+      h[erow] = hn;
+      o.hnew = hn;
+      if (h32) h32[erow] = __double2float_rn(hn);
+    }
+    if (hmax) {
+      // running upper bound of max_k |h_k| for the LMO filter window
+      const float ah = ev ? __double2float_ru(fabs(h[erow])) : 0.f;
+      const unsigned mb = __reduce_max_sync(FULL, (unsigned)__float_as_int(ah));
+      if (lane == 0) *hmax = fmaxf(*hmax, __int_as_float((int)mb));
+    }
+    if (keep) {
+      const int pos = __popc(o.kmask & ((1u << lane) - 1u));
+      A.srow[(int64_t)i * cap + pos] = erow;
+      A.sval[(int64_t)i * cap + pos] = tnew;
+    }
+    if (lane == 0) { A.cnt[i] = o.nk; if (cnt2) cnt2[i] = o.nk; }
+  }
+  SP_MARK(13);
+  o.erow = erow;
+  o.tnew = tnew;
+  o.keep = keep;
+  o.ev = ev && !o.abort && !o.noop;
+  return o;
+}
+
+// lane p <- the p-th kept entry (ascending rows): the column's new support slab.
+__device__ __forceinline__ void new_slab_entry(const StepOut& o, int& rw, double& tv) {
+  const int lane = threadIdx.x & 31;
+  const int srcl = lane < o.nk ? (int)__fns(o.kmask, 0, lane + 1) : 0;
+  const int r2 = __shfl_sync(FULL, o.erow, srcl);
+  const double t2 = __shfl_sync(FULL, o.tnew, srcl);
+  rw = lane < o.nk ? r2 : 0x7fffffff;
+  tv = lane < o.nk ? t2 : 0.0;
+}
+
+// Shared-memory layout of the persistent kernel (host and device agree):
+// fixed | [SMEM: h, r, counts, h32] | [GA: G, fen] | [a] | [visits] | column region.
+struct BcfwLayout {
+  size_t fixed, state, ga, a, visit;
+  __host__ __device__ static size_t fixed_bytes() {
+    return 256 * 8 + BCFW_WARPS * 8 + BCFW_WARPS * 4 + 16 * 4 + 8 * 8;
+  }
+  __host__ __device__ static size_t state_bytes(int m, int n) {
+    return 2 * rup16((size_t)m * 8) + rup16((size_t)n * 4) + rup16((size_t)m * 4);
+  }
+  __host__ __device__ static size_t ga_bytes(int n) { return rup16((size_t)n * 8) + rup16((size_t)(n + 1) * 8); }
+  __host__ __device__ static size_t a_bytes(int m) { return rup16((size_t)m * 8); }
+  __host__ __device__ static size_t visit_bytes(int steps) { return rup16((size_t)steps * 4); }
+};
+
+// ---------------------------------------------------------------------------
 // The persistent kernel.
 // ---------------------------------------------------------------------------
-template <class Col, int VAR, bool GA>
+template <class Col, int VAR, bool GA, bool SMEM>
 __global__ void __launch_bounds__(BCFW_THREADS, 1) k_bcfw(BcfwArgs A, Col col) {
-  extern __shared__ __align__(16) double sm[];
-  double* sh_h = sm;                                   // m
-  double* slots = sh_h + (A.h_smem ? ((A.m + 1) & ~1) : 0);  // 256 (warp 0 sparse psum256)
-  double* wbest = slots + 256;                         // BCFW_WARPS
-  int* wj = reinterpret_cast<int*>(wbest + BCFW_WARPS); // BCFW_WARPS
-  int* misc = wj + BCFW_WARPS;                         // [0]=i [1]=j [2]=abort
-  double* miscd = reinterpret_cast<double*>(misc + 4); // [0]=minval [1]=g_pre
-  double* ga_base = miscd + 2;
-  double* Gs = A.G;
-  double* fens = A.fen;
-  if (GA && A.ga_smem) { Gs = ga_base; fens = ga_base + A.n; }
-
+  extern __shared__ __align__(16) char smraw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int m = A.m, n = A.n, cap = A.cap;
-  double* hs = A.h_smem ? sh_h : A.h;   // h staged in shared memory when it fits
-  if (A.h_smem) for (int k = tid; k < m; k += BCFW_THREADS) sh_h[k] = A.h[k];
+  double* slots = reinterpret_cast<double*>(smraw);                           // 256
+  unsigned long long* wkey = reinterpret_cast<unsigned long long*>(slots + 256);  // 16
+  int* wj = reinterpret_cast<int*>(wkey + BCFW_WARPS);                        // 16
+  int* misc = wj + BCFW_WARPS;                                                // 16 ints
+  double* miscd = reinterpret_cast<double*>(misc + 16);                       // 8
+  float* hmaxp = reinterpret_cast<float*>(miscd + 6);                         // miscd[6..7] as floats
+  char* p = smraw + BcfwLayout::fixed_bytes();
+  double* sh_h = nullptr;
+  double* sh_r = nullptr;
+  int* sh_cnt = nullptr;
+  float* sh_h32 = nullptr;
+  if (SMEM) {
+    sh_h = reinterpret_cast<double*>(p); p += rup16((size_t)m * 8);
+    sh_r = reinterpret_cast<double*>(p); p += rup16((size_t)m * 8);
+    sh_cnt = reinterpret_cast<int*>(p); p += rup16((size_t)n * 4);
+    sh_h32 = reinterpret_cast<float*>(p); p += rup16((size_t)m * 4);
+  }
+  double* Gs = A.G;
+  double* fens = A.fen;
+  if (GA && A.ga_smem) {
+    Gs = reinterpret_cast<double*>(p); p += rup16((size_t)n * 8);
+    fens = reinterpret_cast<double*>(p); p += rup16((size_t)(n + 1) * 8);
+  }
+  const double* aa = A.a;
+  if (A.a_smem) {
+    double* sa = reinterpret_cast<double*>(p); p += rup16((size_t)m * 8);
+    for (int k = tid; k < m; k += BCFW_THREADS) sa[k] = A.a[k];
+    aa = sa;
+  }
+  const int* vis = A.visit;
+  if (!GA && A.visit_smem) {
+    int* sv = reinterpret_cast<int*>(p); p += rup16((size_t)A.steps * 4);
+    for (int q = tid; q < A.steps; q += BCFW_THREADS) sv[q] = A.visit[q];
+    vis = sv;
+  }
+  col.setup(p);
+  double* hs = SMEM ? sh_h : A.h;
+  double* rr = SMEM ? sh_r : A.r;
+  const int* cnt_rd = SMEM ? sh_cnt : A.cnt;
+  const bool FILT = SMEM && Col::FILTER && m <= 4 * 4 * BCFW_THREADS;
+
   for (int c = tid; c < 256; c += BCFW_THREADS) slots[c] = 0.0;
+  float hloc = 0.f;
+  if (SMEM) {
+    for (int k = tid; k < m; k += BCFW_THREADS) {
+      const double hk = A.h[k];
+      sh_h[k] = hk; sh_r[k] = A.r[k];
+      sh_h32[k] = __double2float_rn(hk);
+      hloc = fmaxf(hloc, __double2float_ru(fabs(hk)));
+    }
+    for (int c = tid; c < n; c += BCFW_THREADS) sh_cnt[c] = A.cnt[c];
+  }
   if (GA && A.ga_smem) {
     for (int c = tid; c < n; c += BCFW_THREADS) Gs[c] = A.G[c];
     for (int c = tid; c <= n; c += BCFW_THREADS) fens[c] = A.fen[c];
   }
-  if (tid == 0) misc[2] = 0;
+  if (tid == 0) { misc[2] = 0; *hmaxp = 0.f; }
+  __syncthreads();
+  if (FILT) {
+    const unsigned mb = __reduce_max_sync(FULL, (unsigned)__float_as_int(hloc));
+    if (lane == 0) atomicMax(reinterpret_cast<unsigned*>(hmaxp), mb);   // non-negative floats order as ints
+  }
+  int i_cur = 0, i_nxt = 0;
+  if (!GA && A.steps > 0) {
+    i_cur = vis[0];
+    i_nxt = A.steps > 1 ? vis[1] : i_cur;
+    if (Col::STAGED) { col.issue(i_cur, 0); cp_async_wait_all(); }
+  }
   __syncthreads();
 
-  const double lam = A.lambda;
+  // warp 0's register copy of the visited column's support slab (prefetched)
+  int rw = 0x7fffffff, c0 = 0;
+  double tv = 0.0, bi = 0.0;
+  if (!GA && warp == 0 && A.steps > 0) {
+    c0 = cnt_rd[i_cur];
+    bi = A.b[i_cur];
+    if (lane < c0) { rw = A.srow[(int64_t)i_cur * cap + lane]; tv = A.sval[(int64_t)i_cur * cap + lane]; }
+  }
   int done = 0;
-  if (!GA && A.steps > 0) col.fetch(A.visit[0]);
-
+#ifdef SRO_PHASE_TIMING
+  PhaseState ph_state;
+  for (int q = 0; q < 16; q++) ph_state.acc[q] = 0;
+  ph_state.t = clock64();
+  PhaseState* g_ph = &ph_state;
+#endif
   for (int s = 0; s < A.steps; s++) {
     const long long kk = A.k0 + s;
+    const int slot = s & 1;
     int i;
     if (GA) {
       if (tid == 0) misc[0] = ga_draw(fens, Gs, n, uniform53(rng_u64(A.seed, 1, (uint64_t)kk)));
       __syncthreads();
       i = misc[0];
-      col.fetch(i);
-      col.advance();
+      if (Col::STAGED) { col.issue(i, slot); cp_async_wait_all(); __syncthreads(); }
     } else {
-      i = A.visit[s];
-      col.advance();
-      if (s + 1 < A.steps) col.fetch(A.visit[s + 1]);
+      i = i_cur;
+      if (Col::STAGED && s + 1 < A.steps) col.issue(i_nxt, slot ^ 1);      // lands during this step
     }
+    PHASE_MARK(0);
     // ---- LMO (Eq. 9): CTA argmin of c_i + h, lowest row on ties
-    double best = __longlong_as_double(0x7ff0000000000000LL);
+    double best = dinf();
     int bj = 0x7fffffff;
-    col.local_argmin(i, hs, best, bj);
-    warp_argmin(best, bj);
-    if (lane == 0) { wbest[warp] = best; wj[warp] = bj; }
+    if (FILT) {
+      const float delta = __double2float_ru(d_add(d_mul(0x1p-22, d_add(A.cmax, d_mul(2.0, (double)*hmaxp))), 1e-30));
+      col.local_argmin_filt(slot, hs, sh_h32, delta, best, bj);
+    } else {
+      col.local_argmin(i, slot, hs, best, bj);
+    }
+    PHASE_MARK(1);
+    unsigned long long key = okey(best);
+    warp_argmin_redux(key, bj);
+    if (lane == 0) { wkey[warp] = key; wj[warp] = bj; }
+    PHASE_MARK(2);
     __syncthreads();
+    PHASE_MARK(3);
     if (warp == 0) {
-      double mv = lane < BCFW_WARPS ? wbest[lane] : __longlong_as_double(0x7ff0000000000000LL);
+      unsigned long long k2 = lane < BCFW_WARPS ? wkey[lane] : ~0ULL;
       int j = lane < BCFW_WARPS ? wj[lane] : 0x7fffffff;
-      warp_argmin(mv, j);
-      // ---- O(|supp|) part, one support entry per lane
-      const double bi = A.b[i];
-      const int c0 = A.cnt[i];
-      int rw = 0x7fffffff;
-      double tv = 0.0, gk = 0.0;
-      if (lane < c0) {
-        rw = A.srow[(int64_t)i * cap + lane];
-        tv = A.sval[(int64_t)i * cap + lane];
-        gk = d_add(col.cost(rw, i), hs[rw]);
+      warp_argmin_redux(k2, j);
+      const double mv = okey_inv(k2);
+      PHASE_MARK(4);
+      if (GA) {
+        c0 = cnt_rd[i];
+        bi = A.b[i];
+        rw = 0x7fffffff; tv = 0.0;
+        if (lane < c0) { rw = A.srow[(int64_t)i * cap + lane]; tv = A.sval[(int64_t)i * cap + lane]; }
       }
-      const double dot = warp_seq_sum(d_mul(tv, gk), c0);
-      const double gfw = d_sub(dot, d_mul(bi, mv));
-      bool abort = !(mv < 1.0e308 && mv > -1.0e308);
-      // away atom v = argmax_{k in supp} grad_ki (Eq. 13), lowest row on ties
-      double gv = __longlong_as_double(0xfff0000000000000LL);  // -inf
-      int vrow = 0x7fffffff;
-      if (VAR != VAR_PLAIN) {
-        double x = lane < c0 ? gk : __longlong_as_double(0xfff0000000000000LL);
-        int xr = lane < c0 ? rw : 0x7fffffff;
-        gv = x; vrow = xr;
-        warp_argmax(gv, vrow);
-      }
-      const unsigned inmask = __ballot_sync(FULL, lane < c0 && rw == j);
-      const bool j_in = inmask != 0u;
-      const int ins = __popc(__ballot_sync(FULL, lane < c0 && rw < j));
-      // merged support supp(t_i) U {j}, rows ascending, one entry per lane
-      const int M = c0 + (j_in ? 0 : 1);
-      int src = (j_in || lane < ins) ? lane : lane - 1;
-      if (src < 0) src = 0;
-      int mrow = __shfl_sync(FULL, rw, src & 31);
-      double mt = __shfl_sync(FULL, tv, src & 31);
-      if (!j_in && lane == ins) { mrow = j; mt = 0.0; }
-      const bool mvalid = lane < M;
-
-      int dir = 0;
-      double gamma = 0.0, num = 0.0, den = 0.0;
-      double tnew = mt;        // new value of the merged entry (plain / FW / pairwise)
-      bool use_merged = true;  // false: away direction over supp only
-      if (VAR == VAR_PLAIN) {
-        double d = d_sub((mvalid && mrow == j) ? bi : 0.0, mvalid ? mt : 0.0);
-        double D = d_add(0.0, d);
-        den = warp_sparse_psum256(m, M, mrow, d_mul(D, D), slots);
-        num = d_mul(lam, d_add(0.0, gfw));
-        if (A.step_rule == 1) {
-          if (!(num > 0.0) || den == 0.0) gamma = 0.0;
-          else { gamma = d_div(num, den); if (gamma > 1.0) gamma = 1.0; }
-        } else {
-          gamma = d_div((double)(2LL * n), (double)(kk + 2LL * n));
-        }
-        const double omg = d_sub(1.0, gamma), gb = d_mul(gamma, bi);
-        tnew = d_mul(omg, mt);
-        if (mrow == j) tnew = d_add(tnew, gb);
-      } else if (VAR == VAR_AWAY) {
-        const double gaw = d_sub(d_mul(bi, gv), dot);
-        const bool use_fw = (c0 == 1) || (gfw >= gaw);
-        if (use_fw) {
-          double d = d_sub((mvalid && mrow == j) ? bi : 0.0, mvalid ? mt : 0.0);
-          den = warp_sparse_psum256(m, M, mrow, d_mul(d, d), slots);
-          num = d_mul(lam, d_add(gfw, 0.0));
-          if (!(num > 0.0) || den == 0.0) gamma = 0.0;
-          else { gamma = d_div(num, den); if (gamma > 1.0) gamma = 1.0; }
-          const double omg = d_sub(1.0, gamma), gb = d_mul(gamma, bi);
-          tnew = d_mul(omg, mt);
-          if (mrow == j) tnew = d_add(tnew, gb);
-        } else {
-          dir = 1;
-          use_merged = false;
-          const double tvv = __shfl_sync(FULL, tv, __ffs(__ballot_sync(FULL, lane < c0 && rw == vrow)) - 1);
-          double d = (lane < c0) ? ((rw == vrow) ? d_sub(tv, bi) : tv) : 0.0;
-          den = warp_sparse_psum256(m, c0, rw, d_mul(d, d), slots);
-          num = d_mul(lam, d_add(gaw, 0.0));
-          const double alpha = d_div(tvv, bi);
-          const double gmax = d_div(alpha, d_sub(1.0, alpha));
-          if (!(num > 0.0) || den == 0.0) gamma = 0.0;
-          else { gamma = d_div(num, den); if (gamma > gmax) gamma = gmax; }
-          const double opg = d_add(1.0, gamma), gb = d_mul(gamma, bi);
-          tnew = d_mul(opg, tv);
-          if (lane < c0 && rw == vrow) {
-            tnew = d_sub(tnew, gb);
-            if (gamma == gmax || tnew < 0.0) tnew = 0.0;
-          }
-        }
-      } else {  // VAR_PAIR
-        if (vrow == j) {
-          dir = 3;
-        } else {
-          dir = 2;
-          const double tvv = __shfl_sync(FULL, tv, __ffs(__ballot_sync(FULL, lane < c0 && rw == vrow)) - 1);
-          const double dv = d_sub(gv, mv);
-          num = d_mul(lam, dv);
-          den = d_mul(2.0, bi);
-          const double alpha = d_div(tvv, bi);
-          if (!(num > 0.0)) gamma = 0.0;
-          else { gamma = d_div(num, den); if (gamma > alpha) gamma = alpha; }
-          double mu = d_mul(gamma, bi);
-          const bool drop = (gamma == alpha) || (mu >= tvv);
-          if (drop) mu = tvv;
-          tnew = mt;
-          if (mrow == j) tnew = d_add(mt, mu);
-          if (mrow == vrow) tnew = drop ? 0.0 : d_sub(mt, mu);
-        }
-      }
-      // ---- apply: new column (drop exact zeros), r += (t' - t), h refresh
-      const bool noop = (VAR == VAR_PAIR && dir == 3);
-      const int E = use_merged ? M : c0;
-      const int erow = use_merged ? mrow : rw;
-      const double eold = use_merged ? mt : tv;
-      const bool ev = lane < E;
-      const bool keep = ev && tnew != 0.0;
-      const unsigned kmask = __ballot_sync(FULL, keep);
-      const int nk = __popc(kmask);
-      if (!noop && nk > cap) abort = true;
-      if (!abort && !noop) {
-        if (ev) {
-          const double Dp = d_add(0.0, d_sub(tnew, eold));
-          const double rn = d_add(A.r[erow], Dp);
-          const double hn = d_div(d_sub(rn, A.a[erow]), lam);
-          A.r[erow] = rn;
-          A.h[erow] = hn;
-          if (A.h_smem) sh_h[erow] = hn;
-        }
-        if (keep) {
-          const int pos = __popc(kmask & ((1u << lane) - 1u));
-          A.srow[(int64_t)i * cap + pos] = erow;
-          A.sval[(int64_t)i * cap + pos] = tnew;
-        }
-        if (lane == 0) A.cnt[i] = nk;
-      }
+      const double gk = lane < c0 ? d_add(col.cost(rw, i, slot), hs[rw]) : 0.0;
+      const StepOut o = serial_step<VAR>(A, kk, i, j, mv, bi, c0, rw, tv, gk, rr, hs, FILT ? sh_h32 : nullptr, aa,
+                                         SMEM ? sh_cnt : nullptr, slots, FILT ? hmaxp : nullptr SP_ARG);
+      PHASE_MARK(5);
       if (lane == 0) {
-        misc[1] = j;
-        miscd[0] = mv;
-        miscd[1] = gfw;
-        if (abort) {
+        miscd[1] = o.gfw;
+        if (o.abort) {
           misc[2] = 1;
           set_status(A.status, !(mv < 1.0e308 && mv > -1.0e308) ? 5 : 6);
         } else if (A.trace) {
           double* tr = A.trace + 9 * (int64_t)s;
-          tr[0] = (double)kk; tr[1] = i; tr[2] = j; tr[3] = (VAR == VAR_PLAIN) ? -1 : vrow;
-          tr[4] = dir; tr[5] = gamma; tr[6] = num; tr[7] = den; tr[8] = mv;
+          tr[0] = (double)kk; tr[1] = i; tr[2] = j; tr[3] = (VAR == VAR_PLAIN) ? -1 : o.vrow;
+          tr[4] = o.dir; tr[5] = o.gamma; tr[6] = o.num; tr[7] = o.den; tr[8] = mv;
+        }
+      }
+      if (!o.abort) {
+        if (GA || i_nxt == i) {
+          // column i stays in hand (GA post-update refresh, or the same column next)
+          new_slab_entry(o, rw, tv);
+          c0 = o.nk;
+        } else if (s + 1 < A.steps) {
+          // prefetch the next visited column's slab into warp-0 registers
+          c0 = cnt_rd[i_nxt];
+          bi = A.b[i_nxt];
+          rw = 0x7fffffff; tv = 0.0;
+          if (lane < c0) { rw = A.srow[(int64_t)i_nxt * cap + lane]; tv = A.sval[(int64_t)i_nxt * cap + lane]; }
         }
       }
     }
+    if (!GA) { i_cur = i_nxt; i_nxt = (s + 2 < A.steps) ? vis[s + 2] : i_nxt; }
+    PHASE_MARK(6);
+    if (!GA && Col::STAGED) cp_async_wait_all();
     __syncthreads();
+    PHASE_MARK(7);
     if (misc[2]) break;
     // ---- GA: refresh the visited column's stored gap (Alg. A.4 line 6)
     if (GA && A.ga_inner) {
-      double gnew = miscd[1];
       if (A.ga_post) {
-        double b2 = __longlong_as_double(0x7ff0000000000000LL);
+        double b2 = dinf();
         int j2 = 0x7fffffff;
-        col.local_argmin(i, hs, b2, j2);
-        warp_argmin(b2, j2);
-        if (lane == 0) { wbest[warp] = b2; wj[warp] = j2; }
+        if (FILT) {
+          const float delta = __double2float_ru(d_add(d_mul(0x1p-22, d_add(A.cmax, d_mul(2.0, (double)*hmaxp))), 1e-30));
+          col.local_argmin_filt(slot, hs, sh_h32, delta, b2, j2);
+        } else {
+          col.local_argmin(i, slot, hs, b2, j2);
+        }
+        unsigned long long key2 = okey(b2);
+        warp_argmin_redux(key2, j2);
+        if (lane == 0) { wkey[warp] = key2; wj[warp] = j2; }
         __syncthreads();
         if (warp == 0) {
-          double mv2 = lane < BCFW_WARPS ? wbest[lane] : __longlong_as_double(0x7ff0000000000000LL);
+          unsigned long long k3 = lane < BCFW_WARPS ? wkey[lane] : ~0ULL;
           int jj2 = lane < BCFW_WARPS ? wj[lane] : 0x7fffffff;
-          warp_argmin(mv2, jj2);
-          const int c1 = A.cnt[i];
-          double term = 0.0;
-          if (lane < c1) {
-            int k2 = A.srow[(int64_t)i * cap + lane];
-            term = d_mul(A.sval[(int64_t)i * cap + lane], d_add(col.cost(k2, i), hs[k2]));
-          }
-          const double dot2 = warp_seq_sum(term, c1);
-          gnew = d_sub(dot2, d_mul(A.b[i], mv2));
+          warp_argmin_redux(k3, jj2);
+          const double mv2 = okey_inv(k3);
+          const double term = lane < c0 ? d_mul(tv, d_add(col.cost(rw, i, slot), hs[rw])) : 0.0;
+          const double dot2 = warp_seq_sum(term, c0);
+          const double gnew = d_sub(dot2, d_mul(bi, mv2));
           if (lane == 0) {
-            double delta = d_sub(wpos(gnew), wpos(Gs[i]));
+            const double delta = d_sub(wpos(gnew), wpos(Gs[i]));
             Gs[i] = gnew;
             ga_add(fens, n, i, delta);
           }
         }
       } else if (tid == 0) {
-        double delta = d_sub(wpos(gnew), wpos(Gs[i]));
+        const double gnew = miscd[1];
+        const double delta = d_sub(wpos(gnew), wpos(Gs[i]));
         Gs[i] = gnew;
         ga_add(fens, n, i, delta);
       }
@@ -386,28 +788,355 @@ __global__ void __launch_bounds__(BCFW_THREADS, 1) k_bcfw(BcfwArgs A, Col col) {
     }
     done = s + 1;
   }
+  __syncthreads();
+  if (SMEM) {
+    for (int k = tid; k < m; k += BCFW_THREADS) { A.h[k] = sh_h[k]; A.r[k] = sh_r[k]; }
+  }
   if (GA && A.ga_smem) {
-    __syncthreads();
     for (int c = tid; c < n; c += BCFW_THREADS) A.G[c] = Gs[c];
     for (int c = tid; c <= n; c += BCFW_THREADS) A.fen[c] = fens[c];
   }
   if (tid == 0) *A.steps_done = done;
+#ifdef SRO_PHASE_TIMING
+  if (tid == 0 && A.phase) for (int q = 0; q < 16; q++) A.phase[q] += ph_state.acc[q];
+#endif
+}
+
+// ---------------------------------------------------------------------------
+// Register-file variant for dense costs (the config [0]/[1] path).
+// Thread t owns the rows of the 128-bit vectors q = t + u*NT (u < MAXV) plus one
+// tail row; it keeps those rows of h (fp64) in registers for the whole segment
+// and prefetches its part of the next visited column into registers one step
+// ahead, so the LMO touches neither shared nor global memory. Warp 0 keeps the
+// master copies of h and r in shared memory; after each update it publishes
+// the touched rows in a small list and marks their owners dirty, and each
+// owner refreshes its registers at the next step (a shared-memory
+// LMO costs ~1250 cycles per step, a register-file LMO ~420).
+// ---------------------------------------------------------------------------
+template <typename T, int MAXV>
+struct RegCol {
+  using V = typename Vec<T>::type;
+  static constexpr int W = Vec<T>::W;
+  const T* C;
+  int64_t ld;
+  int m, nvec;
+  V cur[MAXV], nxt[MAXV];
+  T ctail, ntail;
+  __device__ __forceinline__ void fetch(int i) {
+    const V* p = reinterpret_cast<const V*>(C + (int64_t)i * ld);
+#pragma unroll
+    for (int u = 0; u < MAXV; u++) {
+      const int q = threadIdx.x + u * BCFW_THREADS;
+      if (q < nvec) nxt[u] = __ldg(p + q);
+    }
+    const int kt = nvec * W + threadIdx.x;
+    if (kt < m) ntail = __ldg(C + (int64_t)i * ld + kt);
+  }
+  __device__ __forceinline__ void advance() {
+#pragma unroll
+    for (int u = 0; u < MAXV; u++) cur[u] = nxt[u];
+    ctail = ntail;
+  }
+};
+
+__device__ __forceinline__ void vproc(const float4& v, const double* hd, int k, double& best, int& bj) {
+  const double x0 = d_add((double)v.x, hd[0]), x1 = d_add((double)v.y, hd[1]);
+  const double x2 = d_add((double)v.z, hd[2]), x3 = d_add((double)v.w, hd[3]);
+  if (x0 < best) { best = x0; bj = k; }
+  if (x1 < best) { best = x1; bj = k + 1; }
+  if (x2 < best) { best = x2; bj = k + 2; }
+  if (x3 < best) { best = x3; bj = k + 3; }
+}
+__device__ __forceinline__ void vproc(const double2& v, const double* hd, int k, double& best, int& bj) {
+  const double x0 = d_add(v.x, hd[0]), x1 = d_add(v.y, hd[1]);
+  if (x0 < best) { best = x0; bj = k; }
+  if (x1 < best) { best = x1; bj = k + 1; }
+}
+
+struct RfLayout {
+  __host__ __device__ static size_t bytes(int m, int n, int steps, bool ga_smem, bool visit_smem) {
+    size_t b = 256 * 8 + BCFW_WARPS * 8 + BCFW_WARPS * 4 + 16 * 4 + 8 * 8;   // fixed
+    b += 32 * 4 + 32 * 8 + rup16(BCFW_THREADS);                               // update list + dirty flags
+    b += 3 * rup16((size_t)m * 8) + rup16((size_t)n * 4);                     // h, r, a, counts
+    if (ga_smem) b += rup16((size_t)n * 8) + rup16((size_t)(n + 1) * 8);
+    if (visit_smem) b += rup16((size_t)steps * 4);
+    return b;
+  }
+};
+
+template <typename T, int MAXV, int VAR, bool GA>
+__global__ void __launch_bounds__(BCFW_THREADS, 1) k_bcfw_rf(BcfwArgs A, const T* __restrict__ Cg, int64_t ld) {
+  using Col = RegCol<T, MAXV>;
+  constexpr int W = Col::W;
+  extern __shared__ __align__(16) char smraw[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m = A.m, n = A.n, cap = A.cap;
+  double* slots = reinterpret_cast<double*>(smraw);
+  unsigned long long* wkey = reinterpret_cast<unsigned long long*>(slots + 256);
+  int* wj = reinterpret_cast<int*>(wkey + BCFW_WARPS);
+  int* misc = wj + BCFW_WARPS;                                   // [0]=i [2]=abort [3]=upd count
+  double* miscd = reinterpret_cast<double*>(misc + 16);
+  char* p = smraw + (256 * 8 + BCFW_WARPS * 8 + BCFW_WARPS * 4 + 16 * 4 + 8 * 8);
+  int* upd_row = reinterpret_cast<int*>(p); p += 32 * 4;
+  double* upd_h = reinterpret_cast<double*>(p); p += 32 * 8;
+  unsigned char* dirty = reinterpret_cast<unsigned char*>(p); p += rup16(BCFW_THREADS);
+  double* sh_h = reinterpret_cast<double*>(p); p += rup16((size_t)m * 8);
+  double* sh_r = reinterpret_cast<double*>(p); p += rup16((size_t)m * 8);
+  double* sh_a = reinterpret_cast<double*>(p); p += rup16((size_t)m * 8);
+  int* sh_cnt = reinterpret_cast<int*>(p); p += rup16((size_t)n * 4);
+  double* Gs = A.G;
+  double* fens = A.fen;
+  if (GA && A.ga_smem) {
+    Gs = reinterpret_cast<double*>(p); p += rup16((size_t)n * 8);
+    fens = reinterpret_cast<double*>(p); p += rup16((size_t)(n + 1) * 8);
+  }
+  const int* vis = A.visit;
+  if (!GA && A.visit_smem) {
+    int* sv = reinterpret_cast<int*>(p); p += rup16((size_t)A.steps * 4);
+    for (int q = tid; q < A.steps; q += BCFW_THREADS) sv[q] = A.visit[q];
+    vis = sv;
+  }
+  for (int c = tid; c < 256; c += BCFW_THREADS) slots[c] = 0.0;
+  for (int k = tid; k < m; k += BCFW_THREADS) { sh_h[k] = A.h[k]; sh_r[k] = A.r[k]; sh_a[k] = A.a[k]; }
+  for (int c = tid; c < n; c += BCFW_THREADS) sh_cnt[c] = A.cnt[c];
+  if (GA && A.ga_smem) {
+    for (int c = tid; c < n; c += BCFW_THREADS) Gs[c] = A.G[c];
+    for (int c = tid; c <= n; c += BCFW_THREADS) fens[c] = A.fen[c];
+  }
+  dirty[tid] = 0;
+  if (tid == 0) { misc[2] = 0; misc[3] = 0; }
+  Col col;
+  col.C = Cg; col.ld = ld; col.m = m; col.nvec = m / W;
+  // owned rows of h in registers
+  double hd[MAXV * W];
+  double htail = 0.0;
+  const int kt = col.nvec * W + tid;
+#pragma unroll
+  for (int u = 0; u < MAXV; u++) {
+    const int q = tid + u * BCFW_THREADS;
+#pragma unroll
+    for (int t = 0; t < W; t++) hd[u * W + t] = q < col.nvec ? A.h[W * q + t] : 0.0;
+  }
+  if (kt < m) htail = A.h[kt];
+  int i_cur = 0, i_nxt = 0;
+  if (!GA && A.steps > 0) {
+    i_cur = A.visit[0];
+    i_nxt = A.steps > 1 ? A.visit[1] : i_cur;
+    col.fetch(i_cur);
+  }
+  __syncthreads();
+
+  int rw = 0x7fffffff, c0 = 0;
+  double tv = 0.0, bi = 0.0, cw = 0.0;
+  int rwn = 0x7fffffff, c0n = 0;         // next visited column's slab (prefetched)
+  double tvn = 0.0, bin = 0.0;
+  if (!GA && warp == 0 && A.steps > 0) {
+    c0 = sh_cnt[i_cur];
+    bi = A.b[i_cur];
+    if (lane < c0) { rw = A.srow[(int64_t)i_cur * cap + lane]; tv = A.sval[(int64_t)i_cur * cap + lane]; }
+    if (lane < c0) cw = (double)__ldg(Cg + (int64_t)i_cur * ld + rw);
+  }
+  int done = 0;
+#ifdef SRO_PHASE_TIMING
+  PhaseState ph_state;
+  for (int q = 0; q < 16; q++) ph_state.acc[q] = 0;
+  ph_state.t = clock64();
+  PhaseState* g_ph = &ph_state;
+#endif
+  for (int s = 0; s < A.steps; s++) {
+    const long long kk = A.k0 + s;
+    int i;
+    // ---- refresh owned h registers touched by the previous step
+    if (dirty[tid]) {
+      dirty[tid] = 0;
+      const int nu = misc[3];
+      for (int e = 0; e < nu; e++) {
+        const int k = upd_row[e];
+        const double hv = upd_h[e];
+#pragma unroll
+        for (int u = 0; u < MAXV; u++)
+#pragma unroll
+          for (int t = 0; t < W; t++)
+            if (k == W * (tid + u * BCFW_THREADS) + t) hd[u * W + t] = hv;
+        if (k == kt) htail = hv;
+      }
+    }
+    if (GA) {
+      if (tid == 0) misc[0] = ga_draw(fens, Gs, n, uniform53(rng_u64(A.seed, 1, (uint64_t)kk)));
+      __syncthreads();
+      i = misc[0];
+      col.fetch(i);
+      col.advance();
+    } else {
+      i = i_cur;
+      col.advance();
+      if (s + 1 < A.steps) col.fetch(i_nxt);                      // lands during this step
+      if (warp == 0 && s + 1 < A.steps && i_nxt != i) {           // next slab, a step ahead
+        c0n = sh_cnt[i_nxt];
+        bin = A.b[i_nxt];
+        rwn = 0x7fffffff; tvn = 0.0;
+        if (lane < c0n) { rwn = A.srow[(int64_t)i_nxt * cap + lane]; tvn = A.sval[(int64_t)i_nxt * cap + lane]; }
+      }
+    }
+    PHASE_MARK(0);
+    // ---- LMO (Eq. 9) from registers: CTA argmin of c_i + h, lowest row on ties
+    double best = dinf();
+    int bj = 0x7fffffff;
+#pragma unroll
+    for (int u = 0; u < MAXV; u++) {
+      const int q = tid + u * BCFW_THREADS;
+      if (q < col.nvec) vproc(col.cur[u], hd + u * W, W * q, best, bj);
+    }
+    if (kt < m) {
+      const double x = d_add((double)col.ctail, htail);
+      if (x < best) { best = x; bj = kt; }
+    }
+    PHASE_MARK(1);
+    unsigned long long key = okey(best);
+    warp_argmin_redux(key, bj);
+    if (lane == 0) { wkey[warp] = key; wj[warp] = bj; }
+    PHASE_MARK(2);
+    __syncthreads();
+    PHASE_MARK(3);
+    if (warp == 0) {
+      unsigned long long k2 = lane < BCFW_WARPS ? wkey[lane] : ~0ULL;
+      int j = lane < BCFW_WARPS ? wj[lane] : 0x7fffffff;
+      warp_argmin_redux(k2, j);
+      const double mv = okey_inv(k2);
+      PHASE_MARK(4);
+      if (GA) {
+        c0 = sh_cnt[i];
+        bi = A.b[i];
+        rw = 0x7fffffff; tv = 0.0;
+        if (lane < c0) { rw = A.srow[(int64_t)i * cap + lane]; tv = A.sval[(int64_t)i * cap + lane]; }
+        if (lane < c0) cw = (double)__ldg(Cg + (int64_t)i * ld + rw);
+      }
+      const double gk = lane < c0 ? d_add(cw, sh_h[rw]) : 0.0;
+      const StepOut o = serial_step<VAR>(A, kk, i, j, mv, bi, c0, rw, tv, gk, sh_r, sh_h, nullptr, sh_a, sh_cnt, slots,
+                                         nullptr SP_ARG);
+      PHASE_MARK(5);
+      // publish the touched rows of h for their register owners
+      if (o.ev) {
+        upd_row[lane] = o.erow;
+        upd_h[lane] = o.hnew;
+        const int kr = o.erow;
+        const int owner = kr < col.nvec * W ? (kr / W) % BCFW_THREADS : kr - col.nvec * W;
+        dirty[owner] = 1;
+      }
+      const unsigned evm = __ballot_sync(FULL, o.ev);
+      if (lane == 0) {
+        misc[3] = __popc(evm);
+        miscd[1] = o.gfw;
+        if (o.abort) {
+          misc[2] = 1;
+          set_status(A.status, !(mv < 1.0e308 && mv > -1.0e308) ? 5 : 6);
+        } else if (A.trace) {
+          double* tr = A.trace + 9 * (int64_t)s;
+          tr[0] = (double)kk; tr[1] = i; tr[2] = j; tr[3] = (VAR == VAR_PLAIN) ? -1 : o.vrow;
+          tr[4] = o.dir; tr[5] = o.gamma; tr[6] = o.num; tr[7] = o.den; tr[8] = mv;
+        }
+      }
+      if (!o.abort) {
+        if (GA || i_nxt == i) {
+          new_slab_entry(o, rw, tv);
+          c0 = o.nk;
+          if (!GA && lane < c0) cw = (double)__ldg(Cg + (int64_t)i * ld + rw);
+        } else if (s + 1 < A.steps) {
+          c0 = c0n; bi = bin; rw = rwn; tv = tvn;
+          if (lane < c0) cw = (double)__ldg(Cg + (int64_t)i_nxt * ld + rw);   // consumed next step
+        }
+      }
+    }
+    if (!GA) { i_cur = i_nxt; i_nxt = (s + 2 < A.steps) ? vis[s + 2] : i_nxt; }
+    PHASE_MARK(6);
+    __syncthreads();
+    PHASE_MARK(7);
+    if (misc[2]) break;
+    // ---- GA: refresh the visited column's stored gap (Alg. A.4 line 6)
+    if (GA && A.ga_inner) {
+      if (A.ga_post) {
+        if (dirty[tid]) {
+          dirty[tid] = 0;
+          const int nu = misc[3];
+          for (int e = 0; e < nu; e++) {
+            const int k = upd_row[e];
+            const double hv = upd_h[e];
+#pragma unroll
+            for (int u = 0; u < MAXV; u++)
+#pragma unroll
+              for (int t = 0; t < W; t++)
+                if (k == W * (tid + u * BCFW_THREADS) + t) hd[u * W + t] = hv;
+            if (k == kt) htail = hv;
+          }
+        }
+        double b2 = dinf();
+        int j2 = 0x7fffffff;
+#pragma unroll
+        for (int u = 0; u < MAXV; u++) {
+          const int q = tid + u * BCFW_THREADS;
+          if (q < col.nvec) vproc(col.cur[u], hd + u * W, W * q, b2, j2);
+        }
+        if (kt < m) {
+          const double x = d_add((double)col.ctail, htail);
+          if (x < b2) { b2 = x; j2 = kt; }
+        }
+        unsigned long long key2 = okey(b2);
+        warp_argmin_redux(key2, j2);
+        if (lane == 0) { wkey[warp] = key2; wj[warp] = j2; }
+        __syncthreads();
+        if (warp == 0) {
+          unsigned long long k3 = lane < BCFW_WARPS ? wkey[lane] : ~0ULL;
+          int jj2 = lane < BCFW_WARPS ? wj[lane] : 0x7fffffff;
+          warp_argmin_redux(k3, jj2);
+          const double mv2 = okey_inv(k3);
+          const double c2 = lane < c0 ? (double)__ldg(Cg + (int64_t)i * ld + rw) : 0.0;
+          const double term = lane < c0 ? d_mul(tv, d_add(c2, sh_h[rw])) : 0.0;
+          const double dot2 = warp_seq_sum(term, c0);
+          const double gnew = d_sub(dot2, d_mul(bi, mv2));
+          if (lane == 0) {
+            const double delta = d_sub(wpos(gnew), wpos(Gs[i]));
+            Gs[i] = gnew;
+            ga_add(fens, n, i, delta);
+            misc[3] = 0;
+          }
+        }
+      } else if (tid == 0) {
+        const double gnew = miscd[1];
+        const double delta = d_sub(wpos(gnew), wpos(Gs[i]));
+        Gs[i] = gnew;
+        ga_add(fens, n, i, delta);
+      }
+      __syncthreads();
+    }
+    done = s + 1;
+  }
+  __syncthreads();
+  for (int k = tid; k < m; k += BCFW_THREADS) { A.h[k] = sh_h[k]; A.r[k] = sh_r[k]; }
+  if (GA && A.ga_smem) {
+    for (int c = tid; c < n; c += BCFW_THREADS) A.G[c] = Gs[c];
+    for (int c = tid; c <= n; c += BCFW_THREADS) A.fen[c] = fens[c];
+  }
+  if (tid == 0) *A.steps_done = done;
+#ifdef SRO_PHASE_TIMING
+  if (tid == 0 && A.phase) for (int q = 0; q < 16; q++) A.phase[q] += ph_state.acc[q];
+#endif
 }
 
 // Fenwick rebuild after a GA global refresh: fen[i] = max(G_{i-1}, 0), then
-// the standard linear build (R14). One thread, in order.
-__global__ void k_fen_build(const double* __restrict__ G, double* fen, int n) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  fen[0] = 0.0;
-  for (int i = 1; i <= n; i++) fen[i] = wpos(G[i - 1]);
-  for (int i = 1; i <= n; i++) {
-    int p = i + (i & -i);
-    if (p <= n) fen[p] = d_add(fen[p], fen[i]);
+// the standard linear build (R14), in order, in shared memory when it fits.
+__global__ void k_fen_build(const double* __restrict__ G, double* fen, int n, int use_smem) {
+  extern __shared__ double fs[];
+  double* f = use_smem ? fs : fen;
+  for (int i = threadIdx.x; i <= n; i += blockDim.x) f[i] = i == 0 ? 0.0 : wpos(G[i - 1]);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i <= n; i++) {
+      const int p = i + (i & -i);
+      if (p <= n) f[p] = d_add(f[p], f[i]);
+    }
   }
-}
-
-__global__ void k_fill(double* x, int n, double v) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) x[i] = v;
+  __syncthreads();
+  if (use_smem) for (int i = threadIdx.x; i <= n; i += blockDim.x) fen[i] = f[i];
 }
 
 }  // namespace sro

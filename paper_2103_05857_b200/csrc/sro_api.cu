@@ -73,6 +73,9 @@ struct Solver {
   double* X = nullptr;
   int num_sms = 148;
   // accounting
+  long long* phase = nullptr;   // device [8] clock64 totals (SRO_PHASE_TIMING builds)
+  double cmax = -1.0;           // max cost, computed once (ensure_cmax)
+  bool no_rf = getenv("SRO_NO_RF") != nullptr;  // debug: force the shared-memory kernel
   sro_stats stats{};
   bool timing = false;
   struct Pending { cudaEvent_t a, b; int cat; int64_t units; };
@@ -225,9 +228,6 @@ __global__ void k_ga_init(double* G, double* fen, int n, const unsigned long lon
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) G[i] = cinit;
 }
 
-__global__ void k_copy(const double* __restrict__ s, double* d, int n) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) d[i] = s[i];
-}
 
 // ---------------------------------------------------------------------------
 // Host helpers: visit order (R21-R22), identical definition to the paper reading
@@ -391,9 +391,9 @@ void copy_trace_out(const std::vector<double>& tr, int64_t count, sro_trace_rec*
 // ---------------------------------------------------------------------------
 // Sequential BCFW family: persistent kernel segments
 // ---------------------------------------------------------------------------
-template <class Col, int VAR, bool GA>
+template <class Col, int VAR, bool GA, bool SMEM>
 sro_status launch_bcfw(Solver* s, BcfwArgs& A, Col col, size_t smem) {
-  auto kern = k_bcfw<Col, VAR, GA>;
+  auto kern = k_bcfw<Col, VAR, GA, SMEM>;
   CUDA_TRY(s, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int tr = timed_begin(s);
   kern<<<1, BCFW_THREADS, smem, s->stream>>>(A, col);
@@ -405,28 +405,98 @@ sro_status launch_bcfw(Solver* s, BcfwArgs& A, Col col, size_t smem) {
   return SRO_OK;
 }
 
+// Layout choice: the fast layout keeps h, r, counts (and the staged column or
+// the source colours) in shared memory when they fit; GA arrays go to shared
+// memory when they still fit, else stay in global memory.
+sro_status ensure_cmax(Solver* s);
+
 template <int VAR, bool GA>
-sro_status bcfw_segment_var(Solver* s, BcfwArgs& A, size_t smem_base) {
-  const int m = s->m;
-  if (s->kind == SRO_COST_DENSE || s->kind == SRO_COST_HASH_UNIFORM) {
+sro_status bcfw_dispatch(Solver* s, BcfwArgs& A) {
+  const int m = s->m, n = s->n;
+  const bool dense = s->kind == SRO_COST_DENSE || s->kind == SRO_COST_HASH_UNIFORM;
+  const size_t elem = s->prec == SRO_FP32 ? 4 : 8;
+  const size_t col_fast = dense ? 2 * rup16((size_t)m * elem) : rup16((size_t)3 * m * elem);
+  const size_t limit = 226 * 1024;
+  size_t total = BcfwLayout::fixed_bytes();
+  const bool smem = total + BcfwLayout::state_bytes(m, n) + col_fast <= limit;
+  if (smem) total += BcfwLayout::state_bytes(m, n) + col_fast;
+  A.ga_smem = 0; A.a_smem = 0; A.visit_smem = 0;
+  if (GA && total + BcfwLayout::ga_bytes(n) <= limit) { A.ga_smem = 1; total += BcfwLayout::ga_bytes(n); }
+  if (smem && total + BcfwLayout::a_bytes(m) <= limit) { A.a_smem = 1; total += BcfwLayout::a_bytes(m); }
+  if (!GA && total + BcfwLayout::visit_bytes(A.steps) <= limit) { A.visit_smem = 1; total += BcfwLayout::visit_bytes(A.steps); }
+  if (dense) {
     if (s->prec == SRO_FP32) {
-      BcDense<float, 4> c; c.C = (const float*)s->C; c.ld = s->ld; c.m = m; c.nvec = m / 4;
-      return launch_bcfw<BcDense<float, 4>, VAR, GA>(s, A, c, smem_base);
+      if (smem) {
+        ColStaged<float> c{}; c.C = (const float*)s->C; c.ld = s->ld; c.m = m;
+        return launch_bcfw<ColStaged<float>, VAR, GA, true>(s, A, c, total);
+      }
+      ColDirect<float> c{}; c.C = (const float*)s->C; c.ld = s->ld; c.m = m;
+      return launch_bcfw<ColDirect<float>, VAR, GA, false>(s, A, c, total);
     }
-    BcDense<double, 4> c; c.C = (const double*)s->C; c.ld = s->ld; c.m = m; c.nvec = m / 2;
-    return launch_bcfw<BcDense<double, 4>, VAR, GA>(s, A, c, smem_base);
+    if (smem) { ColStaged<double> c{}; c.C = (const double*)s->C; c.ld = s->ld; c.m = m;
+                return launch_bcfw<ColStaged<double>, VAR, GA, true>(s, A, c, total); }
+    ColDirect<double> c{}; c.C = (const double*)s->C; c.ld = s->ld; c.m = m;
+    return launch_bcfw<ColDirect<double>, VAR, GA, false>(s, A, c, total);
   }
-  const bool eu = s->kind == SRO_COST_EUCLID;
+  const int eu = s->kind == SRO_COST_EUCLID;
   if (s->prec == SRO_FP32) {
-    if (eu) { BcColour<float, true> c{(const float*)s->x, nullptr, (const float*)s->y, m};
-              return launch_bcfw<BcColour<float, true>, VAR, GA>(s, A, c, smem_base); }
-    BcColour<float, false> c{(const float*)s->x, nullptr, (const float*)s->y, m};
-    return launch_bcfw<BcColour<float, false>, VAR, GA>(s, A, c, smem_base);
+    if (smem) { ColColour<float, true> c{}; c.x = (const float*)s->x; c.y = (const float*)s->y; c.m = m; c.euclid = eu;
+                return launch_bcfw<ColColour<float, true>, VAR, GA, true>(s, A, c, total); }
+    ColColour<float, false> c{}; c.x = (const float*)s->x; c.y = (const float*)s->y; c.m = m; c.euclid = eu;
+    return launch_bcfw<ColColour<float, false>, VAR, GA, false>(s, A, c, total);
   }
-  if (eu) { BcColour<double, true> c{(const double*)s->x, nullptr, (const double*)s->y, m};
-            return launch_bcfw<BcColour<double, true>, VAR, GA>(s, A, c, smem_base); }
-  BcColour<double, false> c{(const double*)s->x, nullptr, (const double*)s->y, m};
-  return launch_bcfw<BcColour<double, false>, VAR, GA>(s, A, c, smem_base);
+  if (smem) { ColColour<double, true> c{}; c.x = (const double*)s->x; c.y = (const double*)s->y; c.m = m; c.euclid = eu;
+              return launch_bcfw<ColColour<double, true>, VAR, GA, true>(s, A, c, total); }
+  ColColour<double, false> c{}; c.x = (const double*)s->x; c.y = (const double*)s->y; c.m = m; c.euclid = eu;
+  return launch_bcfw<ColColour<double, false>, VAR, GA, false>(s, A, c, total);
+}
+
+template <typename T, int MAXV, int VAR, bool GA>
+sro_status launch_rf(Solver* s, BcfwArgs& A, size_t smem) {
+  auto kern = k_bcfw_rf<T, MAXV, VAR, GA>;
+  CUDA_TRY(s, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int tr = timed_begin(s);
+  kern<<<1, BCFW_THREADS, smem, s->stream>>>(A, (const T*)s->C, s->ld);
+  CUDA_TRY(s, cudaGetLastError());
+  timed_end(s, tr, CAT_BCFW, A.steps);
+  s->stats.kernel_launches += 1;
+  s->stats.bcfw_launches += 1;
+  s->stats.bcfw_steps += A.steps;
+  return SRO_OK;
+}
+
+// Register-file kernel for dense costs when the owned rows fit in registers
+// (<= 4 vectors per thread) and h, r, a, counts fit in shared memory.
+// Returns SRO_ERR_DIMENSION (not an error to the caller) when it does not apply.
+template <int VAR, bool GA>
+sro_status bcfw_try_rf(Solver* s, BcfwArgs& A) {
+  const bool dense = s->kind == SRO_COST_DENSE || s->kind == SRO_COST_HASH_UNIFORM;
+  if (!dense) return SRO_ERR_DIMENSION;
+  const int W = s->prec == SRO_FP32 ? 4 : 2;
+  const int nvec = s->m / W;
+  const int need = (nvec + BCFW_THREADS - 1) / BCFW_THREADS;
+  if (need > 4) return SRO_ERR_DIMENSION;
+  const size_t limit = 226 * 1024;
+  A.ga_smem = GA && RfLayout::bytes(s->m, s->n, A.steps, true, false) <= limit;
+  A.visit_smem = !GA && RfLayout::bytes(s->m, s->n, A.steps, false, true) <= limit;
+  A.a_smem = 1;
+  const size_t bytes = RfLayout::bytes(s->m, s->n, A.steps, A.ga_smem, A.visit_smem);
+  if (bytes > limit) return SRO_ERR_DIMENSION;
+  if (s->prec == SRO_FP32) {
+    if (need <= 2) return launch_rf<float, 2, VAR, GA>(s, A, bytes);
+    return launch_rf<float, 4, VAR, GA>(s, A, bytes);
+  }
+  if (need <= 2) return launch_rf<double, 2, VAR, GA>(s, A, bytes);
+  return launch_rf<double, 4, VAR, GA>(s, A, bytes);
+}
+
+template <int VAR, bool GA>
+sro_status bcfw_run(Solver* s, BcfwArgs& A) {
+  if (!s->no_rf) {
+    sro_status st = bcfw_try_rf<VAR, GA>(s, A);
+    if (st != SRO_ERR_DIMENSION) return st;
+  }
+  return bcfw_dispatch<VAR, GA>(s, A);
 }
 
 sro_status bcfw_segment(Solver* s, int variant, const sro_options* o, int steps, const int* dvisit,
@@ -437,28 +507,51 @@ sro_status bcfw_segment(Solver* s, int variant, const sro_options* o, int steps,
   A.visit = dvisit; A.steps = steps; A.k0 = s->k; A.step_rule = o->step;
   A.G = s->G; A.fen = s->fen; A.ga_inner = o->ga_inner; A.ga_post = o->ga_post_update; A.seed = s->seed;
   A.status = s->status; A.steps_done = s->steps_done; A.trace = dtrace;
+  A.phase = s->phase;
   const bool ga = o->sampling == SRO_SAMPLE_GA;
-  A.h_smem = (size_t)s->m * sizeof(double) <= 160 * 1024;
-  size_t smem = sizeof(double) * ((A.h_smem ? (size_t)((s->m + 1) & ~1) : 0) + 256 + BCFW_WARPS) +
-                sizeof(int) * (BCFW_WARPS + 4) + sizeof(double) * 2;
-  A.ga_smem = 0;
-  if (ga && smem + sizeof(double) * (2 * (size_t)s->n + 1) <= 220 * 1024) {
-    A.ga_smem = 1;
-    smem += sizeof(double) * (2 * (size_t)s->n + 1);
-  }
-  A.x_smem = 0;
-  if (variant == SRO_BCFW) return ga ? bcfw_segment_var<VAR_PLAIN, true>(s, A, smem) : bcfw_segment_var<VAR_PLAIN, false>(s, A, smem);
-  if (variant == SRO_BCAFW) return ga ? bcfw_segment_var<VAR_AWAY, true>(s, A, smem) : bcfw_segment_var<VAR_AWAY, false>(s, A, smem);
-  return ga ? bcfw_segment_var<VAR_PAIR, true>(s, A, smem) : bcfw_segment_var<VAR_PAIR, false>(s, A, smem);
+  { sro_status st = ensure_cmax(s); if (st) return st; }
+  A.cmax = s->cmax;
+  if (variant == SRO_BCFW) return ga ? bcfw_run<VAR_PLAIN, true>(s, A) : bcfw_run<VAR_PLAIN, false>(s, A);
+  if (variant == SRO_BCAFW) return ga ? bcfw_run<VAR_AWAY, true>(s, A) : bcfw_run<VAR_AWAY, false>(s, A);
+  return ga ? bcfw_run<VAR_PAIR, true>(s, A) : bcfw_run<VAR_PAIR, false>(s, A);
+}
+
+// max_{k,i} C_ki, once per handle (order-free max; the fp32 LMO filter window
+// and the GA stored-gap constant use it).
+sro_status ensure_cmax(Solver* s) {
+  if (s->cmax >= 0.0) return SRO_OK;
+  unsigned long long* d_cmax = reinterpret_cast<unsigned long long*>(s->scal + 6);
+  CUDA_TRY(s, cudaMemsetAsync(d_cmax, 0, sizeof(unsigned long long), s->stream));
+  sro_status st = with_sweep_src(s, [&](auto src) -> sro_status {
+    k_max_cost<<<s->num_sms * 4, 256, 0, s->stream>>>(src, s->m, s->n, d_cmax);
+    s->stats.kernel_launches += 1;
+    CUDA_TRY(s, cudaGetLastError());
+    return SRO_OK;
+  });
+  if (st) return st;
+  unsigned long long bits = 0;
+  CUDA_TRY(s, cudaMemcpyAsync(&bits, d_cmax, sizeof(bits), cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(s, cudaStreamSynchronize(s->stream));
+  double v;
+  memcpy(&v, &bits, sizeof(v));
+  s->cmax = v;
+  return SRO_OK;
+}
+
+sro_status fen_build(Solver* s) {
+  const size_t bytes = sizeof(double) * ((size_t)s->n + 1);
+  const int use_smem = bytes <= 200 * 1024;
+  if (use_smem) CUDA_TRY(s, cudaFuncSetAttribute(k_fen_build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  k_fen_build<<<1, 256, use_smem ? bytes : 0, s->stream>>>(s->G, s->fen, s->n, use_smem);
+  s->stats.kernel_launches += 1;
+  CUDA_TRY(s, cudaGetLastError());
+  return SRO_OK;
 }
 
 sro_status ga_global_refresh(Solver* s) {
   sro_status st = sweep(s, nullptr, 0, 0, s->n, s->sw_j, s->sw_min, s->G, nullptr);
   if (st) return st;
-  k_fen_build<<<1, 32, 0, s->stream>>>(s->G, s->fen, s->n);
-  s->stats.kernel_launches += 1;
-  CUDA_TRY(s, cudaGetLastError());
-  return SRO_OK;
+  return fen_build(s);
 }
 
 sro_status ga_initialise(Solver* s) {
@@ -471,10 +564,9 @@ sro_status ga_initialise(Solver* s) {
   });
   if (st) return st;
   k_ga_init<<<64, 256, 0, s->stream>>>(s->G, s->fen, s->n, d_cmax, s->lambda);
-  k_fen_build<<<1, 32, 0, s->stream>>>(s->G, s->fen, s->n);
-  s->stats.kernel_launches += 3;
+  s->stats.kernel_launches += 2;
   CUDA_TRY(s, cudaGetLastError());
-  return SRO_OK;
+  return fen_build(s);
 }
 
 // ---------------------------------------------------------------------------
@@ -578,7 +670,7 @@ sro_status do_reset(Solver* s) {
 
 void free_solver(Solver* s) {
   if (!s) return;
-  void* ptrs[] = {s->a, s->b, s->r, s->h, s->cnt, s->srow, s->sval, s->G, s->fen, s->status, s->steps_done,
+  void* ptrs[] = {s->phase, s->a, s->b, s->r, s->h, s->cnt, s->srow, s->sval, s->G, s->fen, s->status, s->steps_done,
                   s->stop, s->scal, s->epsd, s->visit, s->trace, s->sw_j, s->sw_min, s->sw_g, s->part_j,
                   s->part_min, s->pcount, s->poff, s->ptotal, s->prow, s->ppos, s->pd, s->pt, s->pdelta,
                   s->rowcnt, s->rowstart, s->cursor, s->tmp, s->sorted, s->X};
@@ -636,6 +728,8 @@ sro_status sro_create(const double* a, const double* b, const sro_cost* cost, co
   ALLOC(s->a, m); ALLOC(s->b, n); ALLOC(s->r, m); ALLOC(s->h, m);
   ALLOC(s->cnt, n); ALLOC(s->srow, (size_t)n * cap); ALLOC(s->sval, (size_t)n * cap);
   ALLOC(s->G, n); ALLOC(s->fen, (size_t)n + 1);
+  ALLOC(s->phase, 16);
+  cudaMemsetAsync(s->phase, 0, 16 * sizeof(long long), s->stream);
   ALLOC(s->status, 1); ALLOC(s->steps_done, 1); ALLOC(s->stop, 1); ALLOC(s->scal, 8); ALLOC(s->epsd, 1);
   ALLOC(s->sw_j, n); ALLOC(s->sw_min, (size_t)(m > n ? m : n)); ALLOC(s->sw_g, (size_t)(m > n ? m : n));
   cudaMemsetAsync(s->status, 0, sizeof(int), s->stream);
@@ -900,6 +994,16 @@ sro_status sro_get_stats(sro_handle h, sro_stats* out, int32_t reset) {
   resolve_timing(s);
   *out = s->stats;
   if (reset) s->stats = sro_stats{};
+  return SRO_OK;
+}
+
+// Debug: copy the 8 accumulated clock64 phase totals of the persistent kernel
+// (non-zero only in builds compiled with -DSRO_PHASE_TIMING). Not in sro.h.
+sro_status sro_debug_phase(sro_handle h, long long* out8) {
+  if (!h || !out8) return SRO_ERR_INVALID_ARG;
+  Solver* s = static_cast<Solver*>(h);
+  CUDA_TRY(s, cudaMemcpyAsync(out8, s->phase, 16 * sizeof(long long), cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(s, cudaStreamSynchronize(s->stream));
   return SRO_OK;
 }
 

@@ -45,12 +45,32 @@ __device__ __forceinline__ void warp_argmax(double& v, int& j) {
 }
 
 // Chunk c of W covers positions [floor(c L / W), floor((c+1) L / W)) (R19).
+// Position p lies in chunk c = max{c : floor(c L / W) <= p} = floor((W (p+1) - 1) / L).
 __device__ __forceinline__ int64_t chunk_lo(int c, int64_t L, int W) { return ((int64_t)c * L) / W; }
 __device__ __forceinline__ int chunk_index(int64_t p, int64_t L, int W) {
-  int c = (int)((p * W) / L);
-  while (c > 0 && chunk_lo(c, L, W) > p) c--;
-  while (c < W - 1 && chunk_lo(c + 1, L, W) <= p) c++;
-  return c;
+  if (L < (1LL << 23)) return (int)(((unsigned)W * (unsigned)(p + 1) - 1u) / (unsigned)L);
+  return (int)(((int64_t)W * (p + 1) - 1) / L);
+}
+
+// Order-preserving 64-bit key of a double: keys compare as unsigned integers
+// exactly like the values (after -0 -> +0, so equal values share a key).
+__device__ __forceinline__ unsigned long long okey(double v) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(d_add(v, 0.0));
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ULL);
+}
+__device__ __forceinline__ double okey_inv(unsigned long long k) {
+  const unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k;
+  return __longlong_as_double((long long)u);
+}
+// Warp argmin of (value, row), lowest row on ties, with three REDUX.MIN
+// instructions on (key high word, key low word, row). Result in every lane.
+__device__ __forceinline__ void warp_argmin_redux(unsigned long long& key, int& j) {
+  const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+  const unsigned m1 = __reduce_min_sync(FULL, hi);
+  const unsigned m2 = __reduce_min_sync(FULL, hi == m1 ? lo : 0xffffffffu);
+  const unsigned m3 = __reduce_min_sync(FULL, (hi == m1 && lo == m2) ? (unsigned)j : 0x7fffffffu);
+  key = ((unsigned long long)m1 << 32) | m2;
+  j = (int)m3;
 }
 
 // Adjacent-pair tree over 8 values: ((x0+x1)+(x2+x3)) + ((x4+x5)+(x6+x7)).

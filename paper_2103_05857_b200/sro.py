@@ -16,7 +16,7 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsro.so")
+LIB_PATH = os.environ.get("SRO_LIB", os.path.join(HERE, "libsro.so"))
 
 SRO_FW, SRO_BCFW, SRO_BCAFW, SRO_BCPFW, SRO_BATCHED = 0, 1, 2, 3, 4
 STEP_DEC, STEP_ELS = 0, 1

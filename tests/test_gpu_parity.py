@@ -261,3 +261,16 @@ def test_config1_full_size_converges_certified():
     assert o.gap()[0] <= 1e-6 + 1e-12
     fo = o.objective()
     assert abs(fo - g.objective()) <= 1e-9 * abs(fo)
+
+
+@pytest.mark.parametrize("name,ov,gv,kw", [VARIANTS[0], VARIANTS[3], VARIANTS[5]], ids=["bcfw", "bcafw", "ga"])
+def test_config0_shared_memory_kernel_bitexact(name, ov, gv, kw, monkeypatch):
+    """The shared-memory persistent kernel (used when the register-file kernel does not
+    apply) forced on config [0]: same bit-exact trajectory as the oracle."""
+    monkeypatch.setenv("SRO_NO_RF", "1")
+    d = instance(0, seed=0)
+    g, o = pair(d)
+    ro = o.solve(ov, 4 * 256, seed=7, trace=True, epsilon=1e-12, **kw)
+    rg = g.solve(gv, 4 * 256, seed=7, trace=True, epsilon=1e-12, **_gpu_opts(kw))
+    assert_same_trace(rg["trace"], ro["trace"])
+    assert_same_state(g, o)
