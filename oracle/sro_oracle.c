@@ -59,8 +59,10 @@ struct or_state {
   double* G;            /* stored per-column gaps */
   double* fen;          /* Fenwick tree, 1-based, fen[1..n] */
   /* scratch */
-  double* acc8;         /* 8*m per-chunk row accumulators */
+  double* acc256;       /* 256*m per-chunk row accumulators (allocated on first block step) */
   unsigned char* touched;
+  int32_t* trows;       /* touched rows of the current step */
+  int32_t ntrows;
   double* xbuf;         /* max(m, n) */
 };
 
@@ -116,9 +118,6 @@ double or_chunk_tree_sum(const double* x, int64_t L, int32_t W) {
   return part[0];
 }
 
-static double tree8(const double* x8) {
-  return ((x8[0] + x8[1]) + (x8[2] + x8[3])) + ((x8[4] + x8[5]) + (x8[6] + x8[7]));
-}
 
 /* chunk index of position p among L positions split into W chunks */
 static int32_t chunk_of(int64_t p, int64_t L, int32_t W) {
@@ -230,7 +229,7 @@ static void free_state(or_state* s) {
   if (!s) return;
   free(s->a); free(s->b); free(s->C); free(s->X); free(s->Y);
   free(s->cnt); free(s->rows); free(s->vals); free(s->r); free(s->h);
-  free(s->perm); free(s->G); free(s->fen); free(s->acc8); free(s->touched); free(s->xbuf);
+  free(s->perm); free(s->G); free(s->fen); free(s->acc256); free(s->touched); free(s->trows); free(s->xbuf);
   free(s);
 }
 
@@ -302,10 +301,10 @@ or_state* or_create(int32_t m, int32_t n, double lambda, const double* a, const 
   s->perm = (int32_t*)malloc(sizeof(int32_t) * n);
   s->G = (double*)malloc(sizeof(double) * n);
   s->fen = (double*)malloc(sizeof(double) * ((size_t)n + 1));
-  s->acc8 = (double*)calloc((size_t)8 * m, sizeof(double));
   s->touched = (unsigned char*)calloc((size_t)m, 1);
+  s->trows = (int32_t*)malloc(sizeof(int32_t) * (size_t)m);
   s->xbuf = (double*)malloc(sizeof(double) * (size_t)(m > n ? m : n));
-  if (!s->cnt || !s->rows || !s->vals || !s->r || !s->h || !s->perm || !s->G || !s->fen || !s->acc8 ||
+  if (!s->cnt || !s->rows || !s->vals || !s->r || !s->h || !s->perm || !s->G || !s->fen || !s->trows ||
       !s->touched || !s->xbuf) { free_state(s); return NULL; }
   or_reset(s);
   *status = OR_OK;
@@ -474,16 +473,41 @@ static int32_t merged_rows(const or_state* s, int32_t i, int32_t j, int32_t* mr,
   return c;
 }
 
-static void clear_acc8(or_state* s) {
-  memset(s->acc8, 0, sizeof(double) * 8 * (size_t)s->m);
-  memset(s->touched, 0, (size_t)s->m);
+/* Per-row sums of per-column contributions over U (R19): for row k the
+ * contributions of the columns at positions p of U are summed left to right
+ * inside each of the 256 position chunks, and the 256 chunk partials are
+ * combined by adjacent pairs — chunk_tree_sum over U's positions. acc256[c][k]
+ * holds the partial of chunk c for row k (+0.0 when nothing was added). */
+static int acc_begin(or_state* s) {
+  if (!s->acc256) {
+    s->acc256 = (double*)calloc((size_t)256 * s->m, sizeof(double));
+    if (!s->acc256) return OR_ERR_ARG;
+  }
+  s->ntrows = 0;
+  return OR_OK;
 }
 
-/* per-row tree8 of the 8 chunk accumulators */
-static double row_tree8(const or_state* s, int32_t k) {
-  double x8[8];
-  for (int c = 0; c < 8; c++) x8[c] = s->acc8[(size_t)c * s->m + k];
-  return tree8(x8);
+static void acc_add(or_state* s, int32_t c, int32_t k, double v) {
+  double* a = &s->acc256[(size_t)c * s->m + k];
+  *a = *a + v;
+  if (!s->touched[k]) { s->touched[k] = 1; s->trows[s->ntrows++] = k; }
+}
+
+static double row_tree256(const or_state* s, int32_t k) {
+  double part[256];
+  for (int c = 0; c < 256; c++) part[c] = s->acc256[(size_t)c * s->m + k];
+  for (int width = 256; width > 1; width /= 2)
+    for (int c = 0; c < width / 2; c++) part[c] = part[2 * c] + part[2 * c + 1];
+  return part[0];
+}
+
+static void acc_clear(or_state* s) {
+  for (int32_t t = 0; t < s->ntrows; t++) {
+    const int32_t k = s->trows[t];
+    for (int c = 0; c < 256; c++) s->acc256[(size_t)c * s->m + k] = 0.0;
+    s->touched[k] = 0;
+  }
+  s->ntrows = 0;
 }
 
 static int plain_update(or_state* s, const plain_lmo_out* o, int32_t step_rule, int64_t nprime,
@@ -495,25 +519,27 @@ static int plain_update(or_state* s, const plain_lmo_out* o, int32_t step_rule, 
   int32_t* mc = (int32_t*)malloc(sizeof(int32_t) * (size_t)L);
   if (!mr || !mt || !mc) { free(mr); free(mt); free(mc); return OR_ERR_ARG; }
 
-  /* 2. direction d_i = s_i - t_i on supp(t_i) U {j_i}; Delta_k = tree8 over U */
-  clear_acc8(s);
+  /* 2. direction d_i = s_i - t_i on supp(t_i) U {j_i}; Delta_k = per-row psum256 over U */
+  if (acc_begin(s)) { free(mr); free(mt); free(mc); return OR_ERR_ARG; }
   for (int64_t p = 0; p < L; p++) {
     int32_t i = o->U[p];
-    int32_t c8 = chunk_of(p, L, 8);
+    int32_t c256 = chunk_of(p, L, 256);
     mc[p] = merged_rows(s, i, o->j[p], mr + p * cap1, mt + p * cap1);
     for (int32_t q = 0; q < mc[p]; q++) {
       int32_t k = mr[p * cap1 + q];
       double sk = (k == o->j[p]) ? s->b[i] : 0.0;
       double d = sk - mt[p * cap1 + q];
-      s->acc8[(size_t)c8 * s->m + k] = s->acc8[(size_t)c8 * s->m + k] + d;
-      s->touched[k] = 1;
+      acc_add(s, c256, k, d);
     }
   }
   double* x = s->xbuf;
-  for (int32_t k = 0; k < s->m; k++) {
-    if (s->touched[k]) { double D = row_tree8(s, k); x[k] = D * D; }
-    else x[k] = 0.0;
+  for (int32_t k = 0; k < s->m; k++) x[k] = 0.0;
+  for (int32_t t = 0; t < s->ntrows; t++) {
+    const int32_t k = s->trows[t];
+    double D = row_tree256(s, k);
+    x[k] = D * D;
   }
+  acc_clear(s);
   double den = or_chunk_tree_sum(x, s->m, 256);
   double num = s->lambda * o->G;
 
@@ -526,7 +552,7 @@ static int plain_update(or_state* s, const plain_lmo_out* o, int32_t step_rule, 
     gamma = (double)(2 * nprime) / (double)(s->k + 2 * nprime);
   }
 
-  /* 4. update t_i <- (1-gamma) t_i + gamma s_i; r += tree8(t'-t) */
+  /* 4. update t_i <- (1-gamma) t_i + gamma s_i; r += psum256_U(t' - t) */
   double omg = 1.0 - gamma;
   /* capacity check before mutating */
   for (int64_t p = 0; p < L; p++) {
@@ -541,10 +567,10 @@ static int plain_update(or_state* s, const plain_lmo_out* o, int32_t step_rule, 
     }
     if (keep > s->cap) { free(mr); free(mt); free(mc); return OR_ERR_CAPACITY; }
   }
-  clear_acc8(s);
+  acc_begin(s);
   for (int64_t p = 0; p < L; p++) {
     int32_t i = o->U[p];
-    int32_t c8 = chunk_of(p, L, 8);
+    int32_t c256 = chunk_of(p, L, 256);
     double gb = gamma * s->b[i];
     int32_t* rw = s->rows + (int64_t)i * s->cap;
     double* vl = s->vals + (int64_t)i * s->cap;
@@ -555,18 +581,18 @@ static int plain_update(or_state* s, const plain_lmo_out* o, int32_t step_rule, 
       double tn = omg * told;
       if (k == o->j[p]) tn = tn + gb;
       double delta = tn - told;
-      s->acc8[(size_t)c8 * s->m + k] = s->acc8[(size_t)c8 * s->m + k] + delta;
-      s->touched[k] = 1;
+      acc_add(s, c256, k, delta);
       if (tn != 0.0) { rw[keep] = k; vl[keep] = tn; keep++; }   /* drop exact zeros (R13) */
     }
     s->cnt[i] = keep;
   }
   for (int32_t k = 0; k < s->m; k++) {
     if (!s->touched[k]) continue;
-    double D = row_tree8(s, k);
+    double D = row_tree256(s, k);
     s->r[k] = s->r[k] + D;
     s->h[k] = (s->r[k] - s->a[k]) / s->lambda;
   }
+  acc_clear(s);
   free(mr); free(mt); free(mc);
   *gamma_out = gamma; *num_out = num; *den_out = den;
   return OR_OK;
@@ -583,7 +609,7 @@ static void apply_column(or_state* s, int32_t i, const int32_t* mr, const double
   for (int32_t q = 0; q < c; q++) {
     int32_t k = mr[q];
     double delta = tnew[q] - told[q];
-    double D = delta + 0.0;              /* tree8 of a single column's term (R19) */
+    double D = delta + 0.0;              /* per-row psum256 of a single column's term (R19) */
     s->r[k] = s->r[k] + D;
     s->h[k] = (s->r[k] - s->a[k]) / s->lambda;
     if (tnew[q] != 0.0) { rw[keep] = k; vl[keep] = tnew[q]; keep++; }

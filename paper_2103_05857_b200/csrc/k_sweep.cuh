@@ -197,18 +197,4 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_merge(Src src, int nslabs
   }
 }
 
-// psum256 of x[0..L) -> *out (one CTA of 256 threads). If stop_eps is given,
-// sets *stop = (total <= eps) (FW stop check, Alg. A.1 line 4).
-__global__ void __launch_bounds__(256) k_psum256(const double* __restrict__ x, int64_t L, double* out,
-                                                 const double* __restrict__ eps, int* stop_flag,
-                                                 const int* __restrict__ stop_in) {
-  if (stop_in && *stop_in) return;
-  __shared__ double red[8];
-  double v = block_psum256(x, L, red);
-  if (threadIdx.x == 0) {
-    *out = v;
-    if (stop_flag && eps) { if (v <= *eps) *stop_flag = 1; }
-  }
-}
-
 }  // namespace sro

@@ -71,11 +71,16 @@ struct Solver {
   double *pd = nullptr, *pt = nullptr, *pdelta = nullptr;
   int *rowcnt = nullptr, *rowstart = nullptr, *cursor = nullptr, *tmp = nullptr, *sorted = nullptr;
   double* X = nullptr;
+  int* trows = nullptr;
+  int* ntouch = nullptr;
+  unsigned long long* dsteps = nullptr;   // device count of completed block steps
+  long long k_pending = 0;                // block steps enqueued since the last sync
   int num_sms = 148;
   // accounting
   long long* phase = nullptr;   // device [8] clock64 totals (SRO_PHASE_TIMING builds)
   double cmax = -1.0;           // max cost, computed once (ensure_cmax)
-  bool no_rf = getenv("SRO_NO_RF") != nullptr;  // debug: force the shared-memory kernel
+  bool no_rf = getenv("SRO_NO_RF") != nullptr;      // debug: force the shared-memory kernel
+  bool no_tail = getenv("SRO_NO_TAIL") != nullptr;  // debug: force the multi-kernel block step
   sro_stats stats{};
   bool timing = false;
   struct Pending { cudaEvent_t a, b; int cat; int64_t units; };
@@ -580,6 +585,7 @@ sro_status ensure_block_ws(Solver* s, int64_t L) {
   if (!s->rowcnt) {
     CUDA_TRY(s, dalloc(&s->rowcnt, s->m)); CUDA_TRY(s, dalloc(&s->rowstart, s->m + 1));
     CUDA_TRY(s, dalloc(&s->cursor, s->m + 1)); CUDA_TRY(s, dalloc(&s->X, s->m));
+    CUDA_TRY(s, dalloc(&s->trows, s->m)); CUDA_TRY(s, dalloc(&s->ntouch, 1));
   }
   s->blk_L = L; s->blk_P = P;
   CUDA_TRY(s, dalloc(&s->pcount, L)); CUDA_TRY(s, dalloc(&s->poff, L + 1)); CUDA_TRY(s, dalloc(&s->ptotal, 1));
@@ -590,47 +596,79 @@ sro_status ensure_block_ws(Solver* s, int64_t L) {
 }
 
 // One plain step over [col0, col0+L). For FW (stop_check) the gap G_[n] is
-// checked against epsilon before the update (Alg. A.1 line 4).
+// checked against epsilon before the update (Alg. A.1 line 4). Small U: the
+// LMO sweep plus one single-CTA launch for the rest of the step; large U: one
+// kernel per phase.
 sro_status plain_block_step(Solver* s, const int* col0_dev, int col0_mul, int L, int step_rule, long long nprime,
                             bool stop_check, double* trace_dev) {
   sro_status st = ensure_block_ws(s, L);
   if (st) return st;
   const int trb = timed_begin(s);
-  const int* stop = stop_check ? s->stop : nullptr;
+  int* stop = stop_check ? s->stop : nullptr;
   st = sweep(s, col0_dev, col0_mul, 0, L, s->sw_j, s->sw_min, s->sw_g, stop);
   if (st) return st;
-  k_psum256<<<1, 256, 0, s->stream>>>(s->sw_g, L, s->scal + 0, stop_check ? s->epsd : nullptr,
-                                      stop_check ? s->stop : nullptr, nullptr);
   BlockArgs A{};
   A.m = s->m; A.n = s->n; A.cap = s->cap; A.lambda = s->lambda; A.a = s->a; A.b = s->b; A.r = s->r; A.h = s->h;
   A.cnt = s->cnt; A.srow = s->srow; A.sval = s->sval; A.col0_dev = col0_dev; A.col0_mul = col0_mul; A.L = L;
-  A.j = s->sw_j; A.minval = s->sw_min; A.pcount = s->pcount; A.poff = s->poff; A.ptotal = s->ptotal;
-  A.prow = s->prow; A.ppos = s->ppos; A.pd = s->pd; A.pt = s->pt; A.pdelta = s->pdelta; A.rowcnt = s->rowcnt;
+  A.j = s->sw_j; A.minval = s->sw_min; A.g = s->sw_g; A.pcount = s->pcount; A.poff = s->poff; A.ptotal = s->ptotal;
+  A.prow = s->prow; A.ppos = s->ppos; A.pd = s->pd; A.gsum = s->pt; A.pdelta = s->pdelta; A.rowcnt = s->rowcnt;
   A.rowstart = s->rowstart; A.cursor = s->cursor; A.tmp = s->tmp; A.sorted = s->sorted; A.X = s->X;
-  A.scal = s->scal; A.stop = stop; A.status = s->status;
-  const int tpb = 256;
-  int gL = (L + tpb - 1) / tpb; if (gL > s->num_sms * 8) gL = s->num_sms * 8;
-  int gM = (s->m + tpb - 1) / tpb; if (gM > s->num_sms * 8) gM = s->num_sms * 8;
-  const int gP = s->num_sms * 8;
-  k_pairs_count<<<gL, tpb, 0, s->stream>>>(A);
-  k_scan_excl<<<1, 1024, 0, s->stream>>>(s->pcount, L, s->poff, nullptr, s->ptotal, stop, s->status);
-  CUDA_TRY(s, cudaMemsetAsync(s->rowcnt, 0, sizeof(int) * s->m, s->stream));
-  k_pairs_gen<<<gL, tpb, 0, s->stream>>>(A);
-  k_scan_excl<<<1, 1024, 0, s->stream>>>(s->rowcnt, s->m, s->rowstart, s->cursor, nullptr, stop, s->status);
-  k_place<<<gP, tpb, 0, s->stream>>>(A);
-  k_rank<<<gP, tpb, 0, s->stream>>>(A);
-  k_rowsum_dir<<<gM, tpb, 0, s->stream>>>(A);
-  k_psum256<<<1, 256, 0, s->stream>>>(s->X, s->m, s->scal + 1, nullptr, nullptr, stop);
-  const long long kk = s->k;
-  k_gamma<<<1, 32, 0, s->stream>>>(A, step_rule, kk, nprime, trace_dev);
-  k_cap_check<<<gL, tpb, 0, s->stream>>>(A);
-  k_update_cols<<<gL, tpb, 0, s->stream>>>(A);
-  k_rowsum_update<<<gM, tpb, 0, s->stream>>>(A);
-  CUDA_TRY(s, cudaGetLastError());
-  s->stats.kernel_launches += 14;
+  A.scal = s->scal; A.eps = stop_check ? s->epsd : nullptr; A.stop = stop; A.status = s->status;
+  A.trows = s->trows; A.ntouch = s->ntouch;
+  A.step_rule = step_rule; A.kk = s->k + s->k_pending; A.nprime = nprime; A.trace = trace_dev;
+  A.dsteps = s->dsteps;
+  if (L <= 1024 && !s->no_tail) {
+    const size_t smem = sizeof(double) * 32 * 256;
+    CUDA_TRY(s, cudaFuncSetAttribute(k_block_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_block_tail<<<1, 1024, smem, s->stream>>>(A);
+    CUDA_TRY(s, cudaGetLastError());
+    s->stats.kernel_launches += 1;
+  } else {
+    const int tpb = 256;
+    int gL = (L + tpb - 1) / tpb; if (gL > s->num_sms * 8) gL = s->num_sms * 8;
+    const int gP = s->num_sms * 8;
+    const int gG = (s->m + 7) / 8 < s->num_sms * 8 ? (s->m + 7) / 8 : s->num_sms * 8;
+    k_psum256<<<1, 256, 0, s->stream>>>(s->sw_g, L, s->scal + 0, A.eps, stop, nullptr);
+    k_pairs_count<<<gL, tpb, 0, s->stream>>>(A);
+    k_scan_excl<<<1, 1024, 0, s->stream>>>(s->pcount, L, s->poff, nullptr, s->ptotal, stop, s->status);
+    CUDA_TRY(s, cudaMemsetAsync(s->rowcnt, 0, sizeof(int) * s->m, s->stream));
+    CUDA_TRY(s, cudaMemsetAsync(s->ntouch, 0, sizeof(int), s->stream));
+    k_pairs_gen<<<gL, tpb, 0, s->stream>>>(A);
+    k_scan_excl<<<1, 1024, 0, s->stream>>>(s->rowcnt, s->m, s->rowstart, s->cursor, nullptr, stop, s->status);
+    k_place<<<gP, tpb, 0, s->stream>>>(A);
+    k_rank<<<gP, tpb, 0, s->stream>>>(A);
+    CUDA_TRY(s, cudaMemsetAsync(s->X, 0, sizeof(double) * s->m, s->stream));
+    k_row_groups<<<gP, tpb, 0, s->stream>>>(A, s->pd);
+    k_row_tree<0><<<gG, 256, 0, s->stream>>>(A);
+    k_psum256<<<1, 256, 0, s->stream>>>(s->X, s->m, s->scal + 1, nullptr, nullptr, stop);
+    k_gamma<<<1, 32, 0, s->stream>>>(A);
+    k_cap_check<<<gL, tpb, 0, s->stream>>>(A);
+    k_update_cols<<<gL, tpb, 0, s->stream>>>(A);
+    k_row_groups<<<gP, tpb, 0, s->stream>>>(A, s->pdelta);
+    k_row_tree<1><<<gG, 256, 0, s->stream>>>(A);
+    k_step_done<<<1, 32, 0, s->stream>>>(A);
+    CUDA_TRY(s, cudaGetLastError());
+    s->stats.kernel_launches += 16;
+  }
   s->stats.block_steps += 1;
+  s->k_pending += 1;
   timed_end(s, trb, CAT_BLOCK, L);
   return SRO_OK;
+}
+
+// Sync point for asynchronously enqueued block steps: read how many completed
+// (a skipped step — FW stop or an error — does not count), advance k, and
+// report a device error.
+sro_status drain_block_steps(Solver* s, int64_t* done) {
+  unsigned long long ds = 0;
+  CUDA_TRY(s, cudaMemcpyAsync(&ds, s->dsteps, sizeof(ds), cudaMemcpyDeviceToHost, s->stream));
+  sro_status st = check_status(s);   // synchronises
+  resolve_timing(s);
+  CUDA_TRY(s, cudaMemsetAsync(s->dsteps, 0, sizeof(unsigned long long), s->stream));
+  s->k += (long long)ds;
+  *done += (int64_t)ds;
+  s->k_pending = 0;
+  return st;
 }
 
 bool options_equal(const sro_options& x, const sro_options& y) {
@@ -670,10 +708,10 @@ sro_status do_reset(Solver* s) {
 
 void free_solver(Solver* s) {
   if (!s) return;
-  void* ptrs[] = {s->phase, s->a, s->b, s->r, s->h, s->cnt, s->srow, s->sval, s->G, s->fen, s->status, s->steps_done,
+  void* ptrs[] = {s->dsteps, s->phase, s->a, s->b, s->r, s->h, s->cnt, s->srow, s->sval, s->G, s->fen, s->status, s->steps_done,
                   s->stop, s->scal, s->epsd, s->visit, s->trace, s->sw_j, s->sw_min, s->sw_g, s->part_j,
                   s->part_min, s->pcount, s->poff, s->ptotal, s->prow, s->ppos, s->pd, s->pt, s->pdelta,
-                  s->rowcnt, s->rowstart, s->cursor, s->tmp, s->sorted, s->X};
+                  s->rowcnt, s->rowstart, s->cursor, s->tmp, s->sorted, s->X, s->trows, s->ntouch};
   for (void* p : ptrs) if (p) cudaFree(p);
   if (s->owns_cost) { if (s->C) cudaFree(s->C); if (s->x) cudaFree(s->x); if (s->y) cudaFree(s->y); }
   for (auto& p : s->pending) { s->ev_pool.push_back(p.a); s->ev_pool.push_back(p.b); }
@@ -729,6 +767,8 @@ sro_status sro_create(const double* a, const double* b, const sro_cost* cost, co
   ALLOC(s->cnt, n); ALLOC(s->srow, (size_t)n * cap); ALLOC(s->sval, (size_t)n * cap);
   ALLOC(s->G, n); ALLOC(s->fen, (size_t)n + 1);
   ALLOC(s->phase, 16);
+  ALLOC(s->dsteps, 1);
+  cudaMemsetAsync(s->dsteps, 0, sizeof(unsigned long long), s->stream);
   cudaMemsetAsync(s->phase, 0, 16 * sizeof(long long), s->stream);
   ALLOC(s->status, 1); ALLOC(s->steps_done, 1); ALLOC(s->stop, 1); ALLOC(s->scal, 8); ALLOC(s->epsd, 1);
   ALLOC(s->sw_j, n); ALLOC(s->sw_min, (size_t)(m > n ? m : n)); ALLOC(s->sw_g, (size_t)(m > n ? m : n));
@@ -843,23 +883,24 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
   if (o->trace) { st = ensure_trace(s, iters > 0 ? iters : 1); if (st) return st; }
 
   if (variant == SRO_FW) {
-    const int one = 0;
-    (void)one;
     CUDA_TRY(s, cudaMemsetAsync(s->stop, 0, sizeof(int), s->stream));
     while (done < iters) {
-      st = plain_block_step(s, nullptr, 0, n, o->step, 1, true, o->trace ? s->trace + 9 * done : nullptr);
-      if (st) return st;
+      const int64_t chunk = (iters - done) < 8 ? (iters - done) : 8;
+      for (int64_t q = 0; q < chunk; q++) {
+        st = plain_block_step(s, nullptr, 0, n, o->step, 1, true, o->trace ? s->trace + 9 * (done + q) : nullptr);
+        if (st) return st;
+      }
+      const int64_t before = done;
       double G = 0.0;
       int stopped = 0;
       CUDA_TRY(s, cudaMemcpyAsync(&G, s->scal + 0, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
       CUDA_TRY(s, cudaMemcpyAsync(&stopped, s->stop, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
-      st = check_status(s);
-      resolve_timing(s);
+      st = drain_block_steps(s, &done);
       if (st) return st;
-      out->gap = G; out->gap_checks++;
-      out->entries_scanned += (int64_t)m * n;
+      out->gap = G;
+      out->gap_checks += (int)(done - before) + (stopped ? 1 : 0);
+      out->entries_scanned += (int64_t)m * n * ((done - before) + (stopped ? 1 : 0));
       if (stopped) { out->converged = 1; break; }
-      s->k++; done++;
     }
     CUDA_TRY(s, cudaMemsetAsync(s->stop, 0, sizeof(int), s->stream));
   } else {
@@ -882,14 +923,19 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
       }
       if (done >= iters) break;
       if (variant == SRO_BATCHED) {
-        st = plain_block_step(s, s->visit + done, o->block_size, o->block_size, o->step, nprime, false,
-                              o->trace ? s->trace + 9 * done : nullptr);
-        if (st) return st;
-        st = check_status(s);
-        resolve_timing(s);
-        if (st) return st;
-        out->entries_scanned += (int64_t)m * o->block_size;
-        s->k++; done++;
+        // enqueue every block step up to the next gap check, then one sync
+        long long seg = iters - done;
+        const long long to_check = period - s->k % period;
+        if (seg > to_check) seg = to_check;
+        const int64_t before = done;
+        for (long long q = 0; q < seg; q++) {
+          st = plain_block_step(s, s->visit + done + q, o->block_size, o->block_size, o->step, nprime, false,
+                                o->trace ? s->trace + 9 * (done + q) : nullptr);
+          if (st) return st;
+        }
+        st = drain_block_steps(s, &done);
+        out->entries_scanned += (int64_t)m * o->block_size * (done - before);
+        if (st) break;
         continue;
       }
       long long seg = iters - done;

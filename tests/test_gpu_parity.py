@@ -274,3 +274,18 @@ def test_config0_shared_memory_kernel_bitexact(name, ov, gv, kw, monkeypatch):
     rg = g.solve(gv, 4 * 256, seed=7, trace=True, epsilon=1e-12, **_gpu_opts(kw))
     assert_same_trace(rg["trace"], ro["trace"])
     assert_same_state(g, o)
+
+
+@pytest.mark.parametrize("variant,B", [(BATCHED, 16), (FW, 0)])
+def test_block_step_multikernel_path_bitexact(variant, B, monkeypatch):
+    """The multi-kernel block step (used for large U) forced on small instances: same
+    bit-exact trajectory as the single-CTA tail path and the oracle."""
+    monkeypatch.setenv("SRO_NO_TAIL", "1")
+    d = instance(1, m=300, n=256, seed=8)
+    g, o = pair(d, prec="f32")
+    kw = dict(block_size=B, sampling=P) if B else {}
+    gv = sro.SRO_BATCHED if B else sro.SRO_FW
+    ro = o.solve(variant, 40, seed=3, trace=True, step=ELS, epsilon=1e-9, **kw)
+    rg = g.solve(gv, 40, seed=3, trace=True, step=sro.STEP_ELS, epsilon=1e-9, **kw)
+    assert_same_trace(rg["trace"], ro["trace"])
+    assert_same_state(g, o)
