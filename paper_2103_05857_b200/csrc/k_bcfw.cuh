@@ -378,6 +378,15 @@ __device__ int ga_draw(const double* fen, const double* G, int n, double u53) {
 __device__ __forceinline__ void ga_add(double* fen, int n, int i0, double delta) {
   for (int p = i0 + 1; p <= n; p += p & -p) fen[p] = d_add(fen[p], delta);
 }
+// Same update with lane t of a warp updating the t-th node of the path (the
+// nodes are distinct, so each node receives exactly the one add it gets above).
+__device__ __forceinline__ void ga_add_warp(double* fen, int n, int i0, double delta) {
+  const int lane = threadIdx.x & 31;
+  int p = i0 + 1;
+  for (int t = 0; t < lane && p <= n; t++) p += p & -p;
+  if (p <= n) fen[p] = d_add(fen[p], delta);
+  __syncwarp();
+}
 
 // ---------------------------------------------------------------------------
 // Warp 0: the O(|supp|) part of one step (all 32 lanes call it).
@@ -884,12 +893,11 @@ __global__ void __launch_bounds__(BCFW_THREADS, 1) k_bcfw_rf(BcfwArgs A, const T
   double* sh_r = reinterpret_cast<double*>(p); p += rup16((size_t)m * 8);
   double* sh_a = reinterpret_cast<double*>(p); p += rup16((size_t)m * 8);
   int* sh_cnt = reinterpret_cast<int*>(p); p += rup16((size_t)n * 4);
-  double* Gs = A.G;
-  double* fens = A.fen;
-  if (GA && A.ga_smem) {
-    Gs = reinterpret_cast<double*>(p); p += rup16((size_t)n * 8);
-    fens = reinterpret_cast<double*>(p); p += rup16((size_t)(n + 1) * 8);
-  }
+  // GA: stored gaps and Fenwick tree always in shared memory here (the host
+  // falls back to the generic kernel when they do not fit)
+  double* Gs = reinterpret_cast<double*>(p);
+  double* fens = reinterpret_cast<double*>(p + rup16((size_t)n * 8));
+  if (GA) p += rup16((size_t)n * 8) + rup16((size_t)(n + 1) * 8);
   const int* vis = A.visit;
   if (!GA && A.visit_smem) {
     int* sv = reinterpret_cast<int*>(p); p += rup16((size_t)A.steps * 4);
@@ -899,7 +907,7 @@ __global__ void __launch_bounds__(BCFW_THREADS, 1) k_bcfw_rf(BcfwArgs A, const T
   for (int c = tid; c < 256; c += BCFW_THREADS) slots[c] = 0.0;
   for (int k = tid; k < m; k += BCFW_THREADS) { sh_h[k] = A.h[k]; sh_r[k] = A.r[k]; sh_a[k] = A.a[k]; }
   for (int c = tid; c < n; c += BCFW_THREADS) sh_cnt[c] = A.cnt[c];
-  if (GA && A.ga_smem) {
+  if (GA) {
     for (int c = tid; c < n; c += BCFW_THREADS) Gs[c] = A.G[c];
     for (int c = tid; c <= n; c += BCFW_THREADS) fens[c] = A.fen[c];
   }
@@ -966,6 +974,12 @@ __global__ void __launch_bounds__(BCFW_THREADS, 1) k_bcfw_rf(BcfwArgs A, const T
       __syncthreads();
       i = misc[0];
       col.fetch(i);
+      if (warp == 0) {            // slab of the drawn column, overlapping the column fetch
+        c0 = sh_cnt[i];
+        bi = A.b[i];
+        rw = 0x7fffffff; tv = 0.0;
+        if (lane < c0) { rw = A.srow[(int64_t)i * cap + lane]; tv = A.sval[(int64_t)i * cap + lane]; }
+      }
       col.advance();
     } else {
       i = i_cur;
@@ -1004,13 +1018,7 @@ __global__ void __launch_bounds__(BCFW_THREADS, 1) k_bcfw_rf(BcfwArgs A, const T
       warp_argmin_redux(k2, j);
       const double mv = okey_inv(k2);
       PHASE_MARK(4);
-      if (GA) {
-        c0 = sh_cnt[i];
-        bi = A.b[i];
-        rw = 0x7fffffff; tv = 0.0;
-        if (lane < c0) { rw = A.srow[(int64_t)i * cap + lane]; tv = A.sval[(int64_t)i * cap + lane]; }
-        if (lane < c0) cw = (double)__ldg(Cg + (int64_t)i * ld + rw);
-      }
+      if (GA && lane < c0) cw = (double)__ldg(Cg + (int64_t)i * ld + rw);
       const double gk = lane < c0 ? d_add(cw, sh_h[rw]) : 0.0;
       const StepOut o = serial_step<VAR>(A, kk, i, j, mv, bi, c0, rw, tv, gk, sh_r, sh_h, nullptr, sh_a, sh_cnt, slots,
                                          nullptr SP_ARG);
@@ -1093,18 +1101,17 @@ __global__ void __launch_bounds__(BCFW_THREADS, 1) k_bcfw_rf(BcfwArgs A, const T
           const double term = lane < c0 ? d_mul(tv, d_add(c2, sh_h[rw])) : 0.0;
           const double dot2 = warp_seq_sum(term, c0);
           const double gnew = d_sub(dot2, d_mul(bi, mv2));
-          if (lane == 0) {
-            const double delta = d_sub(wpos(gnew), wpos(Gs[i]));
-            Gs[i] = gnew;
-            ga_add(fens, n, i, delta);
-            misc[3] = 0;
-          }
+          const double delta = d_sub(wpos(gnew), wpos(Gs[i]));
+          __syncwarp();
+          ga_add_warp(fens, n, i, delta);
+          if (lane == 0) { Gs[i] = gnew; misc[3] = 0; }
         }
-      } else if (tid == 0) {
+      } else if (warp == 0) {
         const double gnew = miscd[1];
         const double delta = d_sub(wpos(gnew), wpos(Gs[i]));
-        Gs[i] = gnew;
-        ga_add(fens, n, i, delta);
+        __syncwarp();
+        ga_add_warp(fens, n, i, delta);
+        if (lane == 0) Gs[i] = gnew;
       }
       __syncthreads();
     }
@@ -1112,7 +1119,7 @@ __global__ void __launch_bounds__(BCFW_THREADS, 1) k_bcfw_rf(BcfwArgs A, const T
   }
   __syncthreads();
   for (int k = tid; k < m; k += BCFW_THREADS) { A.h[k] = sh_h[k]; A.r[k] = sh_r[k]; }
-  if (GA && A.ga_smem) {
+  if (GA) {
     for (int c = tid; c < n; c += BCFW_THREADS) A.G[c] = Gs[c];
     for (int c = tid; c <= n; c += BCFW_THREADS) A.fen[c] = fens[c];
   }

@@ -482,7 +482,7 @@ sro_status bcfw_try_rf(Solver* s, BcfwArgs& A) {
   const int need = (nvec + BCFW_THREADS - 1) / BCFW_THREADS;
   if (need > 4) return SRO_ERR_DIMENSION;
   const size_t limit = 226 * 1024;
-  A.ga_smem = GA && RfLayout::bytes(s->m, s->n, A.steps, true, false) <= limit;
+  A.ga_smem = GA;   // the register-file kernel keeps GA arrays in shared memory (else generic kernel)
   A.visit_smem = !GA && RfLayout::bytes(s->m, s->n, A.steps, false, true) <= limit;
   A.a_smem = 1;
   const size_t bytes = RfLayout::bytes(s->m, s->n, A.steps, A.ga_smem, A.visit_smem);
