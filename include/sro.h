@@ -76,6 +76,26 @@ typedef struct {
   int32_t slab_cap;     /* per-column support capacity (<= 31; 0 -> default 31) */
   int32_t device;       /* CUDA device ordinal */
   void* cuda_stream;    /* cudaStream_t to run on (NULL -> a stream owned by the handle) */
+  /* Column sharding. The LMO sweeps, full FW (Alg. A.1) and
+   * batched steps are independent per column except for the per-row sums
+   * r = T 1_n, Delta = sum_i (s_i - t_i) and the scalar sums of the line search
+   * (P:1786-1795), so the columns split over G shards; every shard keeps a
+   * replica of r and h and the per-row / scalar sums are exchanged as
+   * subtrees of the fixed 256-chunk tree (R19): the trajectory is bitwise the
+   * unsharded one for every G. The sequential BCFW family (Alg. 1, A.2-A.4)
+   * does not shard (each step reads the r of the previous one). */
+  int32_t shards;       /* G: number of column shards, a power of two <= 64 (0 or 1: unsharded) */
+  int32_t shard_block;  /* B_o: shard s holds, in every group of B_o consecutive columns, the
+                           s-th contiguous B_o/G of them. 0 -> n (contiguous column slices, FW).
+                           Batched steps need block_size == B_o, FW needs B_o == n. n % B_o == 0,
+                           B_o % G == 0. */
+  int32_t nranks;       /* processes sharing the G shards: 1 = this process holds all G shards and
+                           runs them in sequence on its stream (exchanges are in-place device
+                           writes), or G = one shard per process exchanged with NCCL all-gathers
+                           on cuda_stream (libnccl.so.2 loaded at run time) */
+  int32_t rank;         /* this process's shard when nranks == G */
+  const void* nccl_id;  /* 128-byte ncclUniqueId (sro_nccl_unique_id on rank 0, shared by the
+                           caller), required when nranks > 1 */
 } sro_params;
 
 typedef enum { SRO_FW = 0, SRO_BCFW = 1, SRO_BCAFW = 2, SRO_BCPFW = 3, SRO_BATCHED = 4 } sro_variant;
@@ -133,9 +153,16 @@ typedef struct {
 } sro_stats;
 
 /* Create a solver. a: host fp64[m] (source marginal), b: host fp64[n] (target
- * marginal), copied. cost as described above. T starts at the first-row
- * vertex T^(0) = (b_1 e_1, ..., b_n e_1).
- * Errors: INVALID_ARG, DIMENSION, MARGINALS, NONFINITE, OOM, CUDA. */
+ * marginal, all n columns even when sharded), copied. cost as described above;
+ * for a sharded handle it covers the columns this process holds ("held
+ * columns", ascending global index: all n when nranks == 1, the shard's n/G
+ * when nranks == G): DENSE data is m x n_held column-major, colour y is
+ * n_held x 3 (x always m x 3), HASH_UNIFORM is generated for the held columns.
+ * Borrowed device DENSE / colour data with nranks == 1 and G > 1 needs
+ * shard_block == n. T starts at the first-row vertex T^(0) = (b_1 e_1, ...,
+ * b_n e_1). With nranks > 1 every rank calls
+ * sro_create collectively (NCCL communicator set-up).
+ * Errors: INVALID_ARG, DIMENSION, MARGINALS, NONFINITE, OOM, CUDA, NCCL. */
 sro_status sro_create(const double* a, const double* b, const sro_cost* cost, const sro_params* params,
                       sro_handle* out);
 
@@ -144,20 +171,26 @@ sro_status sro_create(const double* a, const double* b, const sro_cost* cost, co
  * continuing from the handle's state. Gap checks at epoch boundaries
  * and, for FW, every iteration. seed selects the sampling
  * stream. Returns OK (converged), NOT_CONVERGED (budget spent) or an error.
- * Two calls with iters a and b equal one call with a + b. */
+ * Two calls with iters a and b equal one call with a + b. Sharded handles
+ * run FW and BATCHED only (INVALID_ARG otherwise); with nranks > 1 every rank
+ * calls sro_solve collectively with identical arguments; entries_scanned
+ * counts the held columns. */
 sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* opts, int64_t iters, uint64_t seed,
                      sro_result* out);
 
 /* Duality gap g(T) (Thm 2) as sum_i g_i (Eq. 11).
- * per_column: host fp64[n] or NULL; argmin_rows: host int32[n] or NULL. */
+ * per_column: host fp64[n_held] or NULL; argmin_rows: host int32[n_held] or NULL
+ * (held columns in ascending global order; n_held = n when unsharded).
+ * Sharded handles with nranks > 1: collective. */
 sro_status sro_gap(sro_handle h, double* total, double* per_column, int32_t* argmin_rows);
 
-/* Objective f(T) (Eq. 7). */
+/* Objective f(T) (Eq. 7). Sharded handles with nranks > 1: collective. */
 sro_status sro_objective(sro_handle h, double* f);
 
-/* Plan export. dense_colmajor: host fp64[m*n] or NULL. COO triplets (rows, cols,
- * vals; host, capacity cap) may be NULL; *nnz receives the number of nonzeros
- * (COO is written column by column, rows ascending). */
+/* Plan export of the held columns. dense_colmajor: host fp64[m*n_held] (held
+ * columns in ascending global order) or NULL. COO triplets (rows, GLOBAL column
+ * indices, vals; host, capacity cap) may be NULL; *nnz receives the number of
+ * nonzeros (COO is written column by column, rows ascending). */
 sro_status sro_get_plan(sro_handle h, double* dense_colmajor, int32_t* rows, int32_t* cols, double* vals,
                         int64_t cap, int64_t* nnz);
 
@@ -166,6 +199,14 @@ sro_status sro_get_rowsums(sro_handle h, double* r);
 
 /* Back to T^(0), k = 0; clears the variant/options/seed lock. */
 sro_status sro_reset(sro_handle h);
+
+/* Global indices (ascending) of the columns this handle holds: cols host
+ * int32[n_held] or NULL; *n_held receives the count (n when unsharded). */
+sro_status sro_held_columns(sro_handle h, int32_t* cols, int32_t* n_held);
+
+/* A fresh NCCL unique id (128 bytes) for sro_params.nccl_id, to be created on
+ * rank 0 and shared with the other ranks by the caller. Errors: NCCL. */
+sro_status sro_nccl_unique_id(uint8_t* out128);
 
 /* Copy the accounting into *out; reset it to zero if reset != 0. */
 sro_status sro_get_stats(sro_handle h, sro_stats* out, int32_t reset);

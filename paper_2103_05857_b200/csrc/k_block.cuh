@@ -4,20 +4,34 @@
 // (k_sweep.cuh) the step needs two per-row sums over the block's columns:
 //   Delta_k  = sum_{i in U} (s_ik - t_ik)     (direction, for the Eq. A.1 denominator)
 //   Delta'_k = sum_{i in U} (t'_ik - t_ik)    (row-sum update r += Delta')
-// Both are segment-reduced, never atomically scattered: the (row, column)
-// pairs of the merged supports are grouped by row with a counting sort whose
-// within-row order is restored by rank (ascending column position); each
-// (row, 256-chunk) run is summed left to right by one thread and a warp per
-// row combines the chunk partials with the adjacent-pair tree (R19). The
-// result is deterministic and identical to the oracle.
+// Both follow R19: U's positions are split in 256 chunks, each (row, chunk)
+// run is summed left to right (ascending column), and the 256 chunk partials
+// of a row combine by adjacent pairs. No float atomics anywhere:
+//   1. every column of U lists its merged support supp(t_i) U {j_i} as
+//      (row, d) pairs, rows ascending (pairs_count / scan / pairs_gen);
+//   2. the first pair of each (row, chunk) run sums the run in column order
+//      and writes the partial to acc[row][chunk] (dev_runs) — work per pair is
+//      O(chunk length x |supp|), independent of how many columns share a row;
+//   3. a warp per touched row combines its 256 chunk slots (dev_row_tree) and
+//      clears them, so acc stays zero outside a step.
+//
+// Sharded mode: the G shards of U hold the contiguous position
+// ranges [s L/G, (s+1) L/G), which are exactly the chunks [s 256/G, (s+1) 256/G)
+// of U (G a power of two dividing L). A shard runs the same phases with
+// W = 256/G chunks over its own positions, so its row tree yields the subtree
+// of the global 256-leaf tree; the G subtree values (per row, plus the
+// block's G_U subtree and status flags) are exchanged and every shard combines
+// them with the same adjacent-pair tree — bitwise the unsharded result.
 //
 // Every phase is a __device__ function over grid-stride loops, so the same
-// code runs either as one kernel per phase (large U, many CTAs) or inside the
-// single-CTA k_block_tail (small U: one launch for the whole post-LMO step).
+// code runs either as one kernel per phase (large U, many CTAs) or inside a
+// single CTA (small U: one launch for the whole post-LMO step).
 #pragma once
 #include "sro_device.cuh"
 
 namespace sro {
+
+constexpr int ACC_W = 256;   // chunk slots per row of the accumulation matrix
 
 struct BlockArgs {
   int m, n, cap;
@@ -30,30 +44,28 @@ struct BlockArgs {
   int* srow;
   double* sval;
   const int* col0_dev;   // block index pointer (batched) or nullptr
-  int col0_mul;          // B
+  int col0_mul;          // columns of U held here (B, or B/G for a shard)
   int L;
+  int W;                 // chunks over the positions held here: 256, or 256/G for a shard
   // LMO outputs over U
   const int* j;
   const double* minval;
   const double* g;       // column gaps over U
-  // pair workspace
+  // pair workspace (P = L (cap+1))
   int* pcount;           // L
   int* poff;             // L+1
   int* ptotal;           // 1
-  int* prow;
-  int* ppos;             // the pair's column chunk (R19)
-  double* pd;
-  double* gsum;          // per-slot run partials
-  double* pdelta;
-  int* rowcnt;           // m
-  int* rowstart;         // m+1
-  int* cursor;           // m+1
-  int* tmp;              // slot -> pair (unordered), then run-start flags
-  int* sorted;
-  double* X;             // m (Delta^2 dense)
+  int* prow;             // P: row of the pair
+  int* ppos;             // P: position of the pair's column in U
+  double* pd;            // P: s_ik - t_ik
+  double* ptold;         // P: t_ik (sharded mode: rollback after a remote capacity error)
+  double* pdelta;        // P: t'_ik - t_ik
+  double* acc;           // m x 256 chunk partials, zero outside a step
+  int* rowcnt;           // m: pairs per row in this step, zero outside a step
   int* trows;            // touched rows (unordered; every row's work is independent)
   int* ntouch;           // number of touched rows
-  double* scal;          // [0]=G [1]=den [2]=gamma [3]=num
+  double* X;             // m: Delta_k^2, zero outside a step
+  double* scal;          // [0]=G_U [1]=den [2]=gamma [3]=num
   const double* eps;     // FW stop check (nullptr for batched)
   int* stop;             // FW stop flag (nullptr for batched)
   int* status;
@@ -61,10 +73,18 @@ struct BlockArgs {
   int step_rule;
   long long kk, nprime;
   double* trace;
+  int trace_col0_mul;    // global block size (trace records the global first column)
   unsigned long long* dsteps;   // completed steps (device counter; host reads at sync points)
+  // sharded mode (G > 1)
+  int G, shard, slot_len;
+  double* x1;            // G slots of slot_len: Delta subtree per row, [m] = G_U subtree, [m+1] = status
+  double* x2;            // G slots: Delta' subtree per row, [m] = capacity failure, [m+1] = status
+  int* capfail;          // this shard's capacity check failed (nullptr when unsharded)
 };
 
-__device__ __forceinline__ bool blk_skip(const BlockArgs& A) { return (A.stop && *A.stop) || *A.status; }
+__device__ __forceinline__ bool blk_skip(const BlockArgs& A) {
+  return (A.stop && *A.stop) || *A.status || (A.capfail && *A.capfail);
+}
 __device__ __forceinline__ int block_col0(const BlockArgs& A) { return A.col0_dev ? (*A.col0_dev) * A.col0_mul : 0; }
 __device__ __forceinline__ int gtid() { return blockIdx.x * blockDim.x + threadIdx.x; }
 __device__ __forceinline__ int gstride() { return gridDim.x * blockDim.x; }
@@ -89,12 +109,25 @@ __device__ __forceinline__ void for_merged(const BlockArgs& A, int i, int j, F f
   }
 }
 
+// Adjacent-pair tree over G (a power of two) values get(0..G-1), evaluated
+// left to right with a stack of completed subtrees.
+template <class F>
+__device__ __forceinline__ double pair_tree_pow2(int G, F get) {
+  double st[10];
+  int sz[10];
+  int top = 0;
+  for (int s = 0; s < G; s++) {
+    double v = get(s);
+    int w = 1;
+    while (top > 0 && sz[top - 1] == w) { v = d_add(st[top - 1], v); w *= 2; top--; }
+    st[top] = v; sz[top] = w; top++;
+  }
+  return st[0];
+}
+
 // ---------------------------------------------------------------------------
 // Phases
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void dev_zero_int(int* x, int N) {
-  for (int q = gtid(); q < N; q += gstride()) x[q] = 0;
-}
 __device__ __forceinline__ void dev_zero_dbl(double* x, int N) {
   for (int q = gtid(); q < N; q += gstride()) x[q] = 0.0;
 }
@@ -106,7 +139,7 @@ __device__ __forceinline__ void dev_pairs_count(const BlockArgs& A) {
 
 // Exclusive scan of x[0..N) into y[0..N], y[N] = total (integers: order-free).
 // One CTA of exactly 1024 threads.
-__device__ __forceinline__ void dev_scan_excl(const int* __restrict__ x, int N, int* y, int* y2, int* total) {
+__device__ __forceinline__ void dev_scan_excl(const int* __restrict__ x, int N, int* y, int* total) {
   __shared__ int ws[32];
   const int t = threadIdx.x;
   const int per = (N + 1023) / 1024;
@@ -124,118 +157,106 @@ __device__ __forceinline__ void dev_scan_excl(const int* __restrict__ x, int N, 
   }
   __syncthreads();
   int run = incl - s + ((t >> 5) ? ws[(t >> 5) - 1] : 0);
-  for (int q = lo; q < hi; q++) { y[q] = run; if (y2) y2[q] = run; run += x[q]; }
+  for (int q = lo; q < hi; q++) { y[q] = run; run += x[q]; }
   if (t == 1023) { y[N] = run; if (total) *total = run; }
   __syncthreads();
 }
 
-// pairs of every merged support: row, column chunk of position p in U, d = s - t
+// pairs of every merged support (rows ascending within a column): row, column
+// position, d = s - t (and t itself in sharded mode); touched-row list.
 __device__ __forceinline__ void dev_pairs_gen(const BlockArgs& A) {
   const int col0 = block_col0(A);
   for (int p = gtid(); p < A.L; p += gstride()) {
     const int i = col0 + p, j = A.j[p];
     const double bi = A.b[i];
     const int base = A.poff[p];
-    const int ch = chunk_index(p, A.L, 256);
     for_merged(A, i, j, [&](int e, int row, double told) {
       const int q = base + e;
       A.prow[q] = row;
-      A.ppos[q] = ch;
+      A.ppos[q] = p;
       A.pd[q] = d_sub(row == j ? bi : 0.0, told);
+      if (A.ptold) A.ptold[q] = told;
       if (atomicAdd(&A.rowcnt[row], 1) == 0) A.trows[atomicAdd(A.ntouch, 1)] = row;   // order-free
     });
   }
 }
 
-__device__ __forceinline__ void dev_place(const BlockArgs& A) {
+// pair index of row k in column position pp's merged support (rows ascending), or -1
+__device__ __forceinline__ int find_pair(const BlockArgs& A, int pp, int k) {
+  const int hi = A.poff[pp + 1];
+  for (int q = A.poff[pp]; q < hi; q++) {
+    const int r = A.prow[q];
+    if (r >= k) return r == k ? q : -1;
+  }
+  return -1;
+}
+
+// acc[k][c] = sum of val over the (row k, chunk c) run, ascending column
+// position, from +0.0 (R19). Computed by the run's first pair.
+__device__ __forceinline__ void dev_runs(const BlockArgs& A, const double* __restrict__ val) {
   const int P = *A.ptotal;
   for (int q = gtid(); q < P; q += gstride()) {
-    const int slot = atomicAdd(&A.cursor[A.prow[q]], 1);
-    A.tmp[slot] = q;
-  }
-}
-
-// Restore ascending pair order (= ascending column position) inside each row segment.
-__device__ __forceinline__ void dev_rank(const BlockArgs& A) {
-  const int P = *A.ptotal;
-  for (int s = gtid(); s < P; s += gstride()) {
-    const int q = A.tmp[s];
-    const int row = A.prow[q];
-    const int lo = A.rowstart[row], c = A.rowcnt[row];
-    int rank = 0;
-    for (int t = lo; t < lo + c; t++) rank += (A.tmp[t] < q);
-    A.sorted[lo + rank] = q;
-  }
-}
-
-// gsum[s] = left-to-right sum of the run of slots starting at s with the same
-// (row, chunk); tmp[s] = 1 at run starts.
-__device__ __forceinline__ void dev_row_groups(const BlockArgs& A, const double* __restrict__ val) {
-  const int P = *A.ptotal;
-  for (int s = gtid(); s < P; s += gstride()) {
-    const int q = A.sorted[s];
-    const int row = A.prow[q];
-    const int lo = A.rowstart[row], hi = lo + A.rowcnt[row];
-    const int c = A.ppos[q];
-    const bool start = (s == lo) || (A.ppos[A.sorted[s - 1]] != c);
-    A.tmp[s] = start;
-    if (start) {
-      double acc = 0.0;
-      for (int t = s; t < hi; t++) {
-        const int qt = A.sorted[t];
-        if (A.ppos[qt] != c) break;
-        acc = d_add(acc, val[qt]);
-      }
-      A.gsum[s] = acc;
+    const int p = A.ppos[q], k = A.prow[q];
+    const int c = chunk_index(p, A.L, A.W);
+    const int lo = (int)chunk_lo(c, A.L, A.W), hi = (int)chunk_lo(c + 1, A.L, A.W);
+    bool start = true;
+    for (int pp = lo; pp < p && start; pp++) start = find_pair(A, pp, k) < 0;
+    if (!start) continue;
+    double s = d_add(0.0, val[q]);
+    for (int pp = p + 1; pp < hi; pp++) {
+      const int qq = find_pair(A, pp, k);
+      if (qq >= 0) s = d_add(s, val[qq]);
     }
+    A.acc[(size_t)k * ACC_W + c] = s;
   }
 }
 
-// Warp per touched row: scatter the row's run partials into 256 shared slots
-// (one per chunk), then the 256-leaf adjacent-pair tree. MODE 0: X[k] = D^2;
-// MODE 1: r_k += D, h_k = (r_k - a_k)/lambda.
+// Warp per touched row: the 256-leaf adjacent-pair tree over acc[k][*] (then
+// cleared). MODE 0: X[k] = D^2; MODE 1: r_k += D, h_k = (r_k - a_k)/lambda;
+// MODE 2: slot[k] = D (a shard's subtree). clear: reset rowcnt[k] (last tree of a step).
 template <int MODE>
-__device__ __forceinline__ void dev_row_tree(const BlockArgs& A, double* slots_all) {
+__device__ __forceinline__ void dev_row_tree(const BlockArgs& A, double* slot, bool clear) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
-  double* slots = slots_all + 256 * warp;
   const int T = *A.ntouch;
   for (int w = blockIdx.x * nwarps + warp; w < T; w += gridDim.x * nwarps) {
     const int k = A.trows[w];
-    const int c = A.rowcnt[k];
-    const int lo = A.rowstart[k];
-    for (int t = lane; t < 256; t += 32) slots[t] = 0.0;
-    __syncwarp();
-    for (int s = lo + lane; s < lo + c; s += 32)
-      if (A.tmp[s]) slots[A.ppos[A.sorted[s]]] = A.gsum[s];
-    __syncwarp();
+    double2* rowp = reinterpret_cast<double2*>(A.acc + (size_t)k * ACC_W + 8 * lane);
     double x[8];
 #pragma unroll
-    for (int t = 0; t < 8; t++) x[t] = slots[8 * lane + t];
+    for (int t = 0; t < 4; t++) { const double2 v = rowp[t]; x[2 * t] = v.x; x[2 * t + 1] = v.y; }
     const double D = warp_pair_tree(tree8(x));
-    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < 4; t++) rowp[t] = make_double2(0.0, 0.0);
     if (lane == 0) {
       if (MODE == 0) {
         A.X[k] = d_mul(D, D);
-      } else {
+      } else if (MODE == 1) {
         const double rn = d_add(A.r[k], D);
         A.r[k] = rn;
         A.h[k] = d_div(d_sub(rn, A.a[k]), A.lambda);
+        A.X[k] = 0.0;
+      } else {
+        slot[k] = D;
       }
+      if (clear) A.rowcnt[k] = 0;
     }
   }
 }
 
-// psum256 (R19) of x[0..L) for a CTA of >= 256 threads (threads >= 256 idle
+// Chunked pairwise sum (R19) of x[0..L) with W chunks (W = 256: psum256; W =
+// 256/G: a shard's subtree) for a CTA of >= 256 threads (threads >= 256 idle
 // but present at the barriers). Result in *out; optional FW stop check.
-__device__ __forceinline__ double dev_psum256(const double* __restrict__ x, int64_t L, double* out,
-                                              const double* eps, int* stop_flag) {
+__device__ __forceinline__ double dev_psumW(const double* __restrict__ x, int64_t L, int W, double* out,
+                                            const double* eps, int* stop_flag) {
   __shared__ double red[8];
   const int c = threadIdx.x;
   double acc = 0.0;
   if (c < 256) {
-    const int64_t lo = chunk_lo(c, L, 256), hi = chunk_lo(c + 1, L, 256);
-    for (int64_t p = lo; p < hi; p++) acc = d_add(acc, x[p]);
+    if (c < W) {
+      const int64_t lo = chunk_lo(c, L, W), hi = chunk_lo(c + 1, L, W);
+      for (int64_t p = lo; p < hi; p++) acc = d_add(acc, x[p]);
+    }
     acc = warp_pair_tree(acc);
     if ((c & 31) == 0) red[c >> 5] = acc;
   }
@@ -246,7 +267,7 @@ __device__ __forceinline__ double dev_psum256(const double* __restrict__ x, int6
     for (int o = 1; o < 8; o <<= 1) v = d_add(v, __shfl_xor_sync(FULL, v, o));
     if (c == 0) {
       red[0] = v;
-      *out = v;
+      if (out) *out = v;
       if (stop_flag && eps && v <= *eps) *stop_flag = 1;
     }
   }
@@ -272,12 +293,13 @@ __device__ __forceinline__ void dev_gamma(const BlockArgs& A) {
   A.scal[3] = num;
   if (A.trace) {
     double* tr = A.trace;
-    tr[0] = (double)A.kk; tr[1] = block_col0(A); tr[2] = A.j[0]; tr[3] = -1; tr[4] = 0;
-    tr[5] = gamma; tr[6] = num; tr[7] = den; tr[8] = A.minval[0];
+    tr[0] = (double)A.kk; tr[1] = A.col0_dev ? (*A.col0_dev) * A.trace_col0_mul : 0; tr[2] = A.j[0]; tr[3] = -1;
+    tr[4] = 0; tr[5] = gamma; tr[6] = num; tr[7] = den; tr[8] = A.minval[0];
   }
 }
 
-// Capacity check for every column of U before anything is mutated.
+// Capacity check for every column of U before anything is mutated: sets the
+// status word (unsharded) or this shard's capfail flag (sharded).
 __device__ __forceinline__ void dev_cap_check(const BlockArgs& A) {
   const int col0 = block_col0(A);
   const double gamma = A.scal[2];
@@ -291,7 +313,10 @@ __device__ __forceinline__ void dev_cap_check(const BlockArgs& A) {
       if (row == j) tn = d_add(tn, gb);
       keep += (tn != 0.0);
     });
-    if (keep > A.cap) set_status(A.status, 6);
+    if (keep > A.cap) {
+      if (A.capfail) atomicOr(A.capfail, 1);
+      else set_status(A.status, 6);
+    }
   }
 }
 
@@ -325,57 +350,59 @@ __device__ __forceinline__ void dev_update_cols(const BlockArgs& A) {
 // Kernels: one per phase (multi-CTA path) ...
 // ---------------------------------------------------------------------------
 __global__ void k_pairs_count(BlockArgs A) { if (!blk_skip(A)) dev_pairs_count(A); }
-__global__ void __launch_bounds__(1024) k_scan_excl(const int* __restrict__ x, int N, int* y, int* y2, int* total,
-                                                    const int* stop, const int* status) {
-  if ((stop && *stop) || (status && *status)) return;
-  dev_scan_excl(x, N, y, y2, total);
+__global__ void __launch_bounds__(1024) k_scan_pairs(BlockArgs A) {
+  if (blk_skip(A)) return;
+  dev_scan_excl(A.pcount, A.L, A.poff, A.ptotal);
 }
 __global__ void k_pairs_gen(BlockArgs A) { if (!blk_skip(A)) dev_pairs_gen(A); }
-__global__ void k_place(BlockArgs A) { if (!blk_skip(A)) dev_place(A); }
-__global__ void k_rank(BlockArgs A) { if (!blk_skip(A)) dev_rank(A); }
-__global__ void k_row_groups(BlockArgs A, const double* __restrict__ val) { if (!blk_skip(A)) dev_row_groups(A, val); }
+__global__ void k_runs(BlockArgs A, const double* __restrict__ val) { if (!blk_skip(A)) dev_runs(A, val); }
 template <int MODE>
-__global__ void __launch_bounds__(256) k_row_tree(BlockArgs A) {
-  __shared__ double sl[8 * 256];
-  if (!blk_skip(A)) dev_row_tree<MODE>(A, sl);
+__global__ void __launch_bounds__(256) k_row_tree(BlockArgs A, double* slot, int clear) {
+  if (!blk_skip(A)) dev_row_tree<MODE>(A, slot, clear != 0);
 }
 __global__ void k_gamma(BlockArgs A) { if (!blk_skip(A)) dev_gamma(A); }
 __global__ void k_cap_check(BlockArgs A) { if (!blk_skip(A)) dev_cap_check(A); }
 __global__ void k_update_cols(BlockArgs A) { if (!blk_skip(A)) dev_update_cols(A); }
+__global__ void k_zero_slot(BlockArgs A, double* slot) { if (!blk_skip(A)) dev_zero_dbl(slot, A.m); }
+
+// Step start: G_U = psumW(g) (FW: stop check, Alg. A.1 line 4) into *out,
+// touched-row count and capacity flag reset. One CTA of 256 threads.
+__global__ void __launch_bounds__(256) k_step_begin(BlockArgs A, double* out) {
+  if (A.stop && *A.stop) return;
+  if (*A.status) return;
+  if (threadIdx.x == 0) { *A.ntouch = 0; if (A.capfail) *A.capfail = 0; }
+  dev_psumW(A.g, A.L, A.W, out, A.G > 1 ? nullptr : A.eps, A.G > 1 ? nullptr : A.stop);
+}
 
 // psum256 of x[0..L) -> *out (one CTA of 256 threads). If stop_flag is given,
-// sets *stop_flag = (total <= *eps) (FW stop check, Alg. A.1 line 4).
+// sets *stop_flag = (total <= *eps).
 __global__ void __launch_bounds__(256) k_psum256(const double* __restrict__ x, int64_t L, double* out,
                                                  const double* __restrict__ eps, int* stop_flag,
                                                  const int* __restrict__ stop_in) {
   if (stop_in && *stop_in) return;
-  dev_psum256(x, L, out, eps, stop_flag);
+  dev_psumW(x, L, 256, out, eps, stop_flag);
+}
+
+__global__ void k_step_done(BlockArgs A) {
+  if (!blk_skip(A) && threadIdx.x == 0) atomicAdd(A.dsteps, 1ULL);
 }
 
 // ... and the whole post-LMO step in one CTA of 1024 threads (small U).
 __global__ void __launch_bounds__(1024, 1) k_block_tail(BlockArgs A) {
-  extern __shared__ double tail_slots[];   // 32 warps x 256
   if (*A.status) return;
-  dev_psum256(A.g, A.L, A.scal + 0, A.eps, A.stop);        // G_U (FW: stop check)
+  if (threadIdx.x == 0) *A.ntouch = 0;
+  dev_psumW(A.g, A.L, 256, A.scal + 0, A.eps, A.stop);        // G_U (FW: stop check)
   if (A.stop && *A.stop) return;
   dev_pairs_count(A);
-  dev_zero_int(A.rowcnt, A.m);
-  if (threadIdx.x == 0) *A.ntouch = 0;
   __syncthreads();
-  dev_scan_excl(A.pcount, A.L, A.poff, nullptr, A.ptotal);
+  dev_scan_excl(A.pcount, A.L, A.poff, A.ptotal);
   dev_pairs_gen(A);
   __syncthreads();
-  dev_scan_excl(A.rowcnt, A.m, A.rowstart, A.cursor, nullptr);
-  dev_place(A);
-  dev_zero_dbl(A.X, A.m);
+  dev_runs(A, A.pd);
   __syncthreads();
-  dev_rank(A);
+  dev_row_tree<0>(A, nullptr, false);
   __syncthreads();
-  dev_row_groups(A, A.pd);
-  __syncthreads();
-  dev_row_tree<0>(A, tail_slots);
-  __syncthreads();
-  dev_psum256(A.X, A.m, A.scal + 1, nullptr, nullptr);
+  dev_psumW(A.X, A.m, 256, A.scal + 1, nullptr, nullptr);
   dev_gamma(A);
   __syncthreads();
   dev_cap_check(A);
@@ -383,14 +410,165 @@ __global__ void __launch_bounds__(1024, 1) k_block_tail(BlockArgs A) {
   if (*A.status) return;
   dev_update_cols(A);
   __syncthreads();
-  dev_row_groups(A, A.pdelta);
+  dev_runs(A, A.pdelta);
   __syncthreads();
-  dev_row_tree<1>(A, tail_slots);
+  dev_row_tree<1>(A, nullptr, true);
   if (threadIdx.x == 0) atomicAdd(A.dsteps, 1ULL);
 }
 
-__global__ void k_step_done(BlockArgs A) {
-  if (!blk_skip(A) && threadIdx.x == 0) atomicAdd(A.dsteps, 1ULL);
+// ---------------------------------------------------------------------------
+// Sharded step (G > 1): phase A (LMO partials) -> exchange x1 -> phase B
+// (gamma, update, Delta' partials) -> exchange x2 -> apply (r, h).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double* slot_of(const BlockArgs& A, double* x, int s) {
+  return x + (size_t)s * A.slot_len;
+}
+
+// After phase A: publish this shard's status (its G_U subtree and Delta
+// subtrees are already in its x1 slot).
+__global__ void k_publish_a(BlockArgs A) {
+  if (threadIdx.x == 0) slot_of(A, A.x1, A.shard)[A.m + 1] = (double)*A.status;
+}
+// After phase B: publish this shard's capacity flag and status (its Delta'
+// subtrees are already in its x2 slot).
+__global__ void k_publish_b(BlockArgs A) {
+  if (threadIdx.x != 0) return;
+  double* s2 = slot_of(A, A.x2, A.shard);
+  s2[A.m] = (A.stop && *A.stop) ? 0.0 : (double)*A.capfail;
+  s2[A.m + 1] = (double)*A.status;
+}
+
+// Combine the G phase-A slots: first error in shard order -> local status;
+// G_U = tree over the shards' subtrees (FW: stop check); den = psum256 over
+// rows of (tree over the shards' Delta subtrees)^2; gamma. >= 256 threads.
+__device__ __forceinline__ void dev_shard_gamma(const BlockArgs& A) {
+  int st = 0;
+  for (int s = 0; s < A.G && !st; s++) st = (int)slot_of(A, A.x1, s)[A.m + 1];
+  __syncthreads();
+  if (st) { if (threadIdx.x == 0) set_status(A.status, st); return; }
+  const double GU = pair_tree_pow2(A.G, [&](int s) { return slot_of(A, A.x1, s)[A.m]; });
+  if (A.eps && GU <= *A.eps) {   // FW stop (every shard takes the same decision)
+    if (threadIdx.x == 0) { A.scal[0] = GU; *A.stop = 1; }
+    return;
+  }
+  __shared__ double red[8];
+  const int c = threadIdx.x;
+  double acc = 0.0;
+  if (c < 256) {
+    const int lo = (int)chunk_lo(c, A.m, 256), hi = (int)chunk_lo(c + 1, A.m, 256);
+    for (int k = lo; k < hi; k++) {
+      const double D = pair_tree_pow2(A.G, [&](int s) { return slot_of(A, A.x1, s)[k]; });
+      acc = d_add(acc, d_mul(D, D));
+    }
+    acc = warp_pair_tree(acc);
+    if ((c & 31) == 0) red[c >> 5] = acc;
+  }
+  __syncthreads();
+  if (c < 32) {
+    double v = (c < 8) ? red[c] : 0.0;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) v = d_add(v, __shfl_xor_sync(FULL, v, o));
+    if (c == 0) { A.scal[0] = GU; A.scal[1] = v; }
+  }
+  __syncthreads();
+  dev_gamma(A);
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_shard_gamma(BlockArgs A) {
+  if ((A.stop && *A.stop) || *A.status) return;
+  dev_shard_gamma(A);
+}
+
+// Combine the G phase-B slots. Any capacity failure: every shard restores its
+// columns of U (if it had updated them) and reports SRO_ERR_CAPACITY, leaving
+// the state before the step. Otherwise r_k += tree over the shards' Delta'
+// subtrees and h_k = (r_k - a_k)/lambda on every row (an untouched row adds
+// +0.0, which leaves r and h bitwise unchanged).
+__global__ void k_shard_apply(BlockArgs A) {
+  if ((A.stop && *A.stop) || *A.status) return;
+  int st = 0, cf = 0;
+  for (int s = 0; s < A.G; s++) {
+    const double* x = slot_of(A, A.x2, s);
+    if (!st) st = (int)x[A.m + 1];
+    cf |= (x[A.m] != 0.0);
+  }
+  if (st) { if (gtid() == 0) set_status(A.status, st); return; }
+  if (cf) {
+    const int col0 = block_col0(A);
+    if (!*A.capfail) {
+      for (int p = gtid(); p < A.L; p += gstride()) {
+        const int i = col0 + p;
+        int keep = 0;
+        for (int q = A.poff[p]; q < A.poff[p + 1]; q++) {
+          if (A.ptold[q] != 0.0) {
+            A.srow[(int64_t)i * A.cap + keep] = A.prow[q];
+            A.sval[(int64_t)i * A.cap + keep] = A.ptold[q];
+            keep++;
+          }
+        }
+        A.cnt[i] = keep;
+      }
+    }
+    for (int w = gtid(); w < *A.ntouch; w += gstride()) A.rowcnt[A.trows[w]] = 0;
+    if (gtid() == 0) set_status(A.status, 6);
+    return;
+  }
+  for (int k = gtid(); k < A.m; k += gstride()) {
+    const double D = pair_tree_pow2(A.G, [&](int s) { return slot_of(A, A.x2, s)[k]; });
+    const double rn = d_add(A.r[k], D);
+    A.r[k] = rn;
+    A.h[k] = d_div(d_sub(rn, A.a[k]), A.lambda);
+  }
+  if (gtid() == 0) atomicAdd(A.dsteps, 1ULL);
+}
+
+// Phase A in one CTA of 1024 threads (small U).
+__global__ void __launch_bounds__(1024, 1) k_shard_tail_a(BlockArgs A) {
+  double* s1 = slot_of(A, A.x1, A.shard);
+  if (!(A.stop && *A.stop) && !*A.status) {
+    if (threadIdx.x == 0) { *A.ntouch = 0; *A.capfail = 0; }
+    dev_psumW(A.g, A.L, A.W, s1 + A.m, nullptr, nullptr);
+    dev_pairs_count(A);
+    dev_zero_dbl(s1, A.m);
+    __syncthreads();
+    dev_scan_excl(A.pcount, A.L, A.poff, A.ptotal);
+    dev_pairs_gen(A);
+    __syncthreads();
+    dev_runs(A, A.pd);
+    __syncthreads();
+    dev_row_tree<2>(A, s1, false);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) s1[A.m + 1] = (double)*A.status;
+}
+
+// Phase B in one CTA of 1024 threads (small U).
+__global__ void __launch_bounds__(1024, 1) k_shard_tail_b(BlockArgs A) {
+  double* s2 = slot_of(A, A.x2, A.shard);
+  bool run = !(A.stop && *A.stop) && !*A.status;
+  if (run) {
+    dev_shard_gamma(A);
+    __syncthreads();
+    run = !(A.stop && *A.stop) && !*A.status;
+  }
+  if (run) {
+    dev_cap_check(A);
+    dev_zero_dbl(s2, A.m);
+    __syncthreads();
+    if (*A.capfail == 0) {
+      dev_update_cols(A);
+      __syncthreads();
+      dev_runs(A, A.pdelta);
+      __syncthreads();
+      dev_row_tree<2>(A, s2, true);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s2[A.m] = run ? (double)*A.capfail : 0.0;
+    s2[A.m + 1] = (double)*A.status;
+  }
 }
 
 }  // namespace sro

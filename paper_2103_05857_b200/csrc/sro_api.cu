@@ -4,13 +4,24 @@
 // column-visit order from the counter-based SplitMix64 stream (R21-R22) and
 // sequences kernels on the solver stream; every step of the method runs in
 // the kernels of k_sweep.cuh, k_bcfw.cuh and k_block.cuh.
+//
+// Column sharding: a handle holds one or more shards (struct
+// Solver each: its columns' cost, slabs and workspaces, plus replicas of r
+// and h). The lead shard is the handle; with nranks == 1 it also owns the
+// other G-1 shards ("peers") and runs every phase for each of them in turn on
+// one stream, each shard writing its partials straight into its slot of the
+// shared exchange buffers; with nranks == G each process holds one shard and
+// the slots are filled by in-place NCCL all-gathers on the solver stream.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <algorithm>
 #include <vector>
 
 #include "../../include/sro.h"
@@ -23,8 +34,35 @@ using namespace sro;
 
 namespace {
 
+// NCCL, loaded at run time (only sharded handles with nranks > 1 need it).
+struct NcclApi {
+  bool tried = false, ok = false;
+  std::string err;
+  decltype(&ncclGetUniqueId) get_id = nullptr;
+  decltype(&ncclCommInitRank) init = nullptr;
+  decltype(&ncclCommDestroy) destroy = nullptr;
+  decltype(&ncclAllGather) allgather = nullptr;
+  decltype(&ncclGetErrorString) errstr = nullptr;
+};
+NcclApi& nccl() {
+  static NcclApi api;
+  if (api.tried) return api;
+  api.tried = true;
+  void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!lib) { api.err = std::string("cannot load libnccl.so.2: ") + dlerror(); return api; }
+  api.get_id = (decltype(api.get_id))dlsym(lib, "ncclGetUniqueId");
+  api.init = (decltype(api.init))dlsym(lib, "ncclCommInitRank");
+  api.destroy = (decltype(api.destroy))dlsym(lib, "ncclCommDestroy");
+  api.allgather = (decltype(api.allgather))dlsym(lib, "ncclAllGather");
+  api.errstr = (decltype(api.errstr))dlsym(lib, "ncclGetErrorString");
+  api.ok = api.get_id && api.init && api.destroy && api.allgather && api.errstr;
+  if (!api.ok) api.err = "libnccl.so.2 lacks a required symbol";
+  return api;
+}
+
 struct Solver {
-  int m = 0, n = 0, cap = 31, device = 0;
+  int m = 0, n = 0, cap = 31, device = 0;   // n: columns held by this shard
   double lambda = 1.0;
   int kind = 0, prec = 0, borrowed = 0;
   cudaStream_t stream = nullptr;
@@ -33,11 +71,20 @@ struct Solver {
   std::string err;
   // problem
   double *a = nullptr, *b = nullptr;
+  double* b_full = nullptr;   // all n_glob target weights (r_0 = sum_i b_i, global order)
   void* C = nullptr;     // dense (fp32 or fp64), ld elements
   int64_t ld = 0;
   void* x = nullptr;     // colours
   void* y = nullptr;
   bool owns_cost = false;
+  // sharding: shard `shard` of G; global column of local p = (p / Bl) Bo + shard Bl + p % Bl
+  int G = 1, shard = 0, nranks = 1, n_glob = 0, Bo = 0, Bl = 0;
+  Solver* lead = this;                 // the handle (owns peers, exchange buffers, stats)
+  std::vector<Solver*> peers;          // other shards held by this process (nranks == 1)
+  ncclComm_t comm = nullptr;
+  int slot_len = 0;
+  double *x1 = nullptr, *x2 = nullptr, *gx = nullptr;   // exchange buffers (lead-owned)
+  int* capfail = nullptr;
   // state
   double *r = nullptr, *h = nullptr;
   int *cnt = nullptr, *srow = nullptr;
@@ -48,7 +95,7 @@ struct Solver {
   sro_options opt{};
   uint64_t seed = 0;
   // GA
-  double *G = nullptr, *fen = nullptr;
+  double *G_ga = nullptr, *fen = nullptr;
   // scratch
   int* status = nullptr;      // device status word
   int* steps_done = nullptr;
@@ -68,9 +115,10 @@ struct Solver {
   // block-step workspace
   int64_t blk_L = 0, blk_P = 0;
   int *pcount = nullptr, *poff = nullptr, *ptotal = nullptr, *prow = nullptr, *ppos = nullptr;
-  double *pd = nullptr, *pt = nullptr, *pdelta = nullptr;
-  int *rowcnt = nullptr, *rowstart = nullptr, *cursor = nullptr, *tmp = nullptr, *sorted = nullptr;
-  double* X = nullptr;
+  double *pd = nullptr, *ptold = nullptr, *pdelta = nullptr;
+  double* acc = nullptr;       // m x 256 chunk partials (zero outside a step)
+  int* rowcnt = nullptr;       // m (zero outside a step)
+  double* X = nullptr;         // m (zero outside a step)
   int* trows = nullptr;
   int* ntouch = nullptr;
   unsigned long long* dsteps = nullptr;   // device count of completed block steps
@@ -88,6 +136,24 @@ struct Solver {
   std::vector<Pending> pending;
 };
 
+// shards held by this process, lead first
+std::vector<Solver*> held(Solver* s) {
+  std::vector<Solver*> v{s};
+  for (Solver* p : s->peers) v.push_back(p);
+  return v;
+}
+int global_col(const Solver* s, int p) { return (p / s->Bl) * s->Bo + s->shard * s->Bl + p % s->Bl; }
+// held columns in ascending global order: (global index, held-shard index, local column)
+struct HeldCol { int global, hq, p; };
+std::vector<HeldCol> held_order(Solver* s) {
+  std::vector<HeldCol> v;
+  auto H = held(s);
+  for (size_t q = 0; q < H.size(); q++)
+    for (int p = 0; p < H[q]->n; p++) v.push_back({H[q]->G == 1 ? p : global_col(H[q], p), (int)q, p});
+  std::sort(v.begin(), v.end(), [](const HeldCol& x, const HeldCol& y) { return x.global < y.global; });
+  return v;
+}
+
 enum { CAT_BCFW = 0, CAT_SWEEP = 1, CAT_BLOCK = 2 };
 
 cudaEvent_t take_event(Solver* s) {
@@ -98,6 +164,7 @@ cudaEvent_t take_event(Solver* s) {
 }
 // open a timed region on the solver stream (no-op unless timing is on)
 int timed_begin(Solver* s) {
+  s = s->lead;
   if (!s->timing) return -1;
   Solver::Pending p{take_event(s), take_event(s), 0, 0};
   cudaEventRecord(p.a, s->stream);
@@ -105,6 +172,7 @@ int timed_begin(Solver* s) {
   return (int)s->pending.size() - 1;
 }
 void timed_end(Solver* s, int idx, int cat, int64_t units) {
+  s = s->lead;
   if (idx < 0) return;
   Solver::Pending& p = s->pending[idx];
   p.cat = cat; p.units = units;
@@ -144,9 +212,11 @@ cudaError_t dalloc(T** p, size_t count) {
 // ---------------------------------------------------------------------------
 // Small kernels: init, validation, hash generator, objective pieces, max cost
 // ---------------------------------------------------------------------------
-__global__ void k_init_plan(const double* __restrict__ b, const double* __restrict__ a, double* r, double* h,
-                            int* cnt, int* srow, double* sval, int m, int n, int cap, double lambda) {
-  // T^(0) = (b_1 e_1, ..., b_n e_1); r_0 = sum_i b_i left to right.
+__global__ void k_init_plan(const double* __restrict__ b, const double* __restrict__ b_full, int n_full,
+                            const double* __restrict__ a, double* r, double* h, int* cnt, int* srow, double* sval,
+                            int m, int n, int cap, double lambda) {
+  // T^(0) = (b_1 e_1, ..., b_n e_1) on the held columns;
+  // r_0 = sum_i b_i over all n columns, left to right (every shard alike).
   const int tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
   for (int i = tid; i < n; i += stride) {
     cnt[i] = 1;
@@ -156,7 +226,7 @@ __global__ void k_init_plan(const double* __restrict__ b, const double* __restri
   for (int k = tid; k < m; k += stride) {
     if (k == 0) {
       double r0 = 0.0;
-      for (int i = 0; i < n; i++) r0 = d_add(r0, b[i]);
+      for (int i = 0; i < n_full; i++) r0 = d_add(r0, b_full[i]);
       r[0] = r0;
       h[0] = d_div(d_sub(r0, a[0]), lambda);
     } else {
@@ -184,13 +254,39 @@ __global__ void k_check_finite(const T* __restrict__ x, int64_t count, int* stat
   }
 }
 
-// SRO_COST_HASH_UNIFORM: C_ki = (splitmix64(seed + (i m + k + 1) GOLDEN) >> 40) 2^-24, fp32 exact.
-__global__ void k_gen_hash(float* C, int64_t ld, int m, int n, uint64_t seed) {
+// SRO_COST_HASH_UNIFORM: C_ki = (splitmix64(seed + (i m + k + 1) GOLDEN) >> 40) 2^-24, fp32 exact,
+// for the held local columns p (global column i = (p / Bl) Bo + shard Bl + p % Bl).
+__global__ void k_gen_hash(float* C, int64_t ld, int m, int n, uint64_t seed, int Bo, int Bl, int shard) {
   const int64_t total = (int64_t)m * n;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = q / m, k = q % m;
-    const uint64_t z = mix64(seed + ((uint64_t)q + 1) * GOLDEN);
-    C[i * ld + k] = (float)(z >> 40) * 0x1p-24f;
+    const int64_t p = q / m, k = q % m;
+    const int64_t i = (p / Bl) * Bo + (int64_t)shard * Bl + p % Bl;
+    const uint64_t z = mix64(seed + ((uint64_t)(i * m + k) + 1) * GOLDEN);
+    C[p * ld + k] = (float)(z >> 40) * 0x1p-24f;
+  }
+}
+
+// psum256 (R19) over the n global columns of per-column values gathered from
+// the G shards: x[s * nl + p] holds the value of local column p of shard s.
+__global__ void __launch_bounds__(256) k_psum256_gathered(const double* __restrict__ x, int n, int Bo, int Bl, int nl,
+                                                          double* out, const int* __restrict__ stop_in) {
+  if (stop_in && *stop_in) return;
+  __shared__ double red[8];
+  const int c = threadIdx.x;
+  const int lo = (int)chunk_lo(c, n, 256), hi = (int)chunk_lo(c + 1, n, 256);
+  double acc = 0.0;
+  for (int i = lo; i < hi; i++) {
+    const int q = i / Bo, rem = i % Bo, s = rem / Bl;
+    acc = d_add(acc, x[(size_t)s * nl + (size_t)q * Bl + rem % Bl]);
+  }
+  acc = warp_pair_tree(acc);
+  if ((c & 31) == 0) red[c >> 5] = acc;
+  __syncthreads();
+  if (c < 32) {
+    double v = (c < 8) ? red[c] : 0.0;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) v = d_add(v, __shfl_xor_sync(FULL, v, o));
+    if (c == 0) *out = v;
   }
 }
 
@@ -288,15 +384,45 @@ sro_status with_sweep_src(Solver* s, F f) {
   return f(SrcColour<double, false>{(const double*)s->x, (const double*)s->y});
 }
 
+// After a failed step the row workspace (zero outside a step) may hold
+// partials of the aborted step: clear it.
+sro_status ws_clean(Solver* s) {
+  if (s->rowcnt) CUDA_TRY(s, cudaMemsetAsync(s->rowcnt, 0, sizeof(int) * s->m, s->stream));
+  if (s->X) CUDA_TRY(s, cudaMemsetAsync(s->X, 0, sizeof(double) * s->m, s->stream));
+  if (s->acc) CUDA_TRY(s, cudaMemsetAsync(s->acc, 0, sizeof(double) * (size_t)s->m * ACC_W, s->stream));
+  return SRO_OK;
+}
+
+// Synchronise and read the status word of every held shard (they agree: the
+// sharded phases propagate the first error of any shard to all of them).
 sro_status check_status(Solver* s) {
-  int st = 0;
-  CUDA_TRY(s, cudaMemcpyAsync(&st, s->status, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+  auto H = held(s->lead);
+  std::vector<int> st(H.size(), 0);
+  for (size_t q = 0; q < H.size(); q++)
+    CUDA_TRY(s, cudaMemcpyAsync(&st[q], H[q]->status, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
   CUDA_TRY(s, cudaStreamSynchronize(s->stream));
-  if (st) {
-    s->err = st == 5 ? "non-finite value met in the LMO" : st == 6 ? "column support exceeds slab_cap" : "device error";
-    CUDA_TRY(s, cudaMemsetAsync(s->status, 0, sizeof(int), s->stream));
-    return (sro_status)st;
+  int first = 0;
+  for (int v : st) if (v && !first) first = v;
+  if (first) {
+    s->lead->err = first == 5 ? "non-finite value met in the LMO" : first == 6 ? "column support exceeds slab_cap" : "device error";
+    for (Solver* t : H) {
+      CUDA_TRY(s, cudaMemsetAsync(t->status, 0, sizeof(int), s->stream));
+      sro_status e = ws_clean(t);
+      if (e) return e;
+    }
+    return (sro_status)first;
   }
+  return SRO_OK;
+}
+
+// Sharded exchange of `count` doubles per shard: buf holds G slots of `count`;
+// every shard has written its own slot. nranks == 1: all slots are local
+// already. nranks == G: in-place all-gather on the solver stream.
+sro_status exchange(Solver* s, double* buf, size_t count) {
+  if (s->nranks == 1) return SRO_OK;
+  NcclApi& api = nccl();
+  ncclResult_t r = api.allgather(buf + (size_t)s->shard * count, buf, count, ncclFloat64, s->comm, s->stream);
+  if (r != ncclSuccess) { s->err = std::string("ncclAllGather: ") + api.errstr(r); return SRO_ERR_NCCL; }
   return SRO_OK;
 }
 
@@ -328,9 +454,9 @@ sro_status sweep(Solver* s, const int* col0_dev, int col0_mul, int col0_host, in
     if (nslabs == 1) { o.j = out_j; o.minval = out_min; o.g = out_g; }
     else { o.j = s->part_j; o.minval = s->part_min; o.g = nullptr; }
     const int tr = timed_begin(s);
-    s->stats.kernel_launches += nslabs > 1 ? 2 : 1;
-    s->stats.sweep_launches += 1;
-    s->stats.sweep_columns += L;
+    s->lead->stats.kernel_launches += nslabs > 1 ? 2 : 1;
+    s->lead->stats.sweep_launches += 1;
+    s->lead->stats.sweep_columns += L;
     kern<<<dim3(gx, nslabs), SWEEP_THREADS, smem, s->stream>>>(src, s->m, s->h, col0_dev, col0_mul, col0_host, L,
                                                              s->cnt, s->srow, s->sval, s->cap, s->b, o, stop,
                                                              s->status);
@@ -348,12 +474,25 @@ sro_status sweep(Solver* s, const int* col0_dev, int col0_mul, int col0_host, in
   });
 }
 
-// Full gap sweep: g(T) = psum256_i g_i (Thm 2 / Eq. 11) -> host.
+// Full gap sweep: g(T) = psum256_i g_i (Thm 2 / Eq. 11) -> host. Sharded:
+// every held shard sweeps its columns into its slot of gx, the slots are
+// exchanged and the total is the psum256 over the n global columns.
 sro_status gap_sweep(Solver* s, double* total) {
-  sro_status st = sweep(s, nullptr, 0, 0, s->n, s->sw_j, s->sw_min, s->sw_g, nullptr);
-  if (st) return st;
-  k_psum256<<<1, 256, 0, s->stream>>>(s->sw_g, s->n, s->scal + 4, nullptr, nullptr, nullptr);
-  s->stats.kernel_launches += 1;
+  sro_status st;
+  if (s->G == 1) {
+    st = sweep(s, nullptr, 0, 0, s->n, s->sw_j, s->sw_min, s->sw_g, nullptr);
+    if (st) return st;
+    k_psum256<<<1, 256, 0, s->stream>>>(s->sw_g, s->n, s->scal + 4, nullptr, nullptr, nullptr);
+  } else {
+    for (Solver* t : held(s)) {
+      st = sweep(t, nullptr, 0, 0, t->n, t->sw_j, t->sw_min, s->gx + (size_t)t->shard * t->n, nullptr);
+      if (st) return st;
+    }
+    st = exchange(s, s->gx, s->n);
+    if (st) return st;
+    k_psum256_gathered<<<1, 256, 0, s->stream>>>(s->gx, s->n_glob, s->Bo, s->Bl, s->n, s->scal + 4, nullptr);
+  }
+  s->lead->stats.kernel_launches += 1;
   CUDA_TRY(s, cudaGetLastError());
   CUDA_TRY(s, cudaMemcpyAsync(total, s->scal + 4, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
   st = check_status(s);  // synchronises
@@ -404,9 +543,9 @@ sro_status launch_bcfw(Solver* s, BcfwArgs& A, Col col, size_t smem) {
   kern<<<1, BCFW_THREADS, smem, s->stream>>>(A, col);
   CUDA_TRY(s, cudaGetLastError());
   timed_end(s, tr, CAT_BCFW, A.steps);
-  s->stats.kernel_launches += 1;
-  s->stats.bcfw_launches += 1;
-  s->stats.bcfw_steps += A.steps;
+  s->lead->stats.kernel_launches += 1;
+  s->lead->stats.bcfw_launches += 1;
+  s->lead->stats.bcfw_steps += A.steps;
   return SRO_OK;
 }
 
@@ -464,9 +603,9 @@ sro_status launch_rf(Solver* s, BcfwArgs& A, size_t smem) {
   kern<<<1, BCFW_THREADS, smem, s->stream>>>(A, (const T*)s->C, s->ld);
   CUDA_TRY(s, cudaGetLastError());
   timed_end(s, tr, CAT_BCFW, A.steps);
-  s->stats.kernel_launches += 1;
-  s->stats.bcfw_launches += 1;
-  s->stats.bcfw_steps += A.steps;
+  s->lead->stats.kernel_launches += 1;
+  s->lead->stats.bcfw_launches += 1;
+  s->lead->stats.bcfw_steps += A.steps;
   return SRO_OK;
 }
 
@@ -510,7 +649,7 @@ sro_status bcfw_segment(Solver* s, int variant, const sro_options* o, int steps,
   A.m = s->m; A.n = s->n; A.cap = s->cap; A.lambda = s->lambda;
   A.a = s->a; A.b = s->b; A.r = s->r; A.h = s->h; A.cnt = s->cnt; A.srow = s->srow; A.sval = s->sval;
   A.visit = dvisit; A.steps = steps; A.k0 = s->k; A.step_rule = o->step;
-  A.G = s->G; A.fen = s->fen; A.ga_inner = o->ga_inner; A.ga_post = o->ga_post_update; A.seed = s->seed;
+  A.G = s->G_ga; A.fen = s->fen; A.ga_inner = o->ga_inner; A.ga_post = o->ga_post_update; A.seed = s->seed;
   A.status = s->status; A.steps_done = s->steps_done; A.trace = dtrace;
   A.phase = s->phase;
   const bool ga = o->sampling == SRO_SAMPLE_GA;
@@ -529,7 +668,7 @@ sro_status ensure_cmax(Solver* s) {
   CUDA_TRY(s, cudaMemsetAsync(d_cmax, 0, sizeof(unsigned long long), s->stream));
   sro_status st = with_sweep_src(s, [&](auto src) -> sro_status {
     k_max_cost<<<s->num_sms * 4, 256, 0, s->stream>>>(src, s->m, s->n, d_cmax);
-    s->stats.kernel_launches += 1;
+    s->lead->stats.kernel_launches += 1;
     CUDA_TRY(s, cudaGetLastError());
     return SRO_OK;
   });
@@ -547,14 +686,14 @@ sro_status fen_build(Solver* s) {
   const size_t bytes = sizeof(double) * ((size_t)s->n + 1);
   const int use_smem = bytes <= 200 * 1024;
   if (use_smem) CUDA_TRY(s, cudaFuncSetAttribute(k_fen_build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  k_fen_build<<<1, 256, use_smem ? bytes : 0, s->stream>>>(s->G, s->fen, s->n, use_smem);
-  s->stats.kernel_launches += 1;
+  k_fen_build<<<1, 256, use_smem ? bytes : 0, s->stream>>>(s->G_ga, s->fen, s->n, use_smem);
+  s->lead->stats.kernel_launches += 1;
   CUDA_TRY(s, cudaGetLastError());
   return SRO_OK;
 }
 
 sro_status ga_global_refresh(Solver* s) {
-  sro_status st = sweep(s, nullptr, 0, 0, s->n, s->sw_j, s->sw_min, s->G, nullptr);
+  sro_status st = sweep(s, nullptr, 0, 0, s->n, s->sw_j, s->sw_min, s->G_ga, nullptr);
   if (st) return st;
   return fen_build(s);
 }
@@ -568,8 +707,8 @@ sro_status ga_initialise(Solver* s) {
     return SRO_OK;
   });
   if (st) return st;
-  k_ga_init<<<64, 256, 0, s->stream>>>(s->G, s->fen, s->n, d_cmax, s->lambda);
-  s->stats.kernel_launches += 2;
+  k_ga_init<<<64, 256, 0, s->stream>>>(s->G_ga, s->fen, s->n, d_cmax, s->lambda);
+  s->lead->stats.kernel_launches += 2;
   CUDA_TRY(s, cudaGetLastError());
   return fen_build(s);
 }
@@ -579,20 +718,40 @@ sro_status ga_initialise(Solver* s) {
 // ---------------------------------------------------------------------------
 sro_status ensure_block_ws(Solver* s, int64_t L) {
   const int64_t P = L * (s->cap + 1);
+  if (!s->rowcnt) {   // row workspace: zero outside a step
+    CUDA_TRY(s, dalloc(&s->rowcnt, s->m)); CUDA_TRY(s, dalloc(&s->X, s->m));
+    CUDA_TRY(s, dalloc(&s->trows, s->m)); CUDA_TRY(s, dalloc(&s->ntouch, 1));
+    CUDA_TRY(s, dalloc(&s->acc, (size_t)s->m * ACC_W)); CUDA_TRY(s, dalloc(&s->capfail, 1));
+    { sro_status e = ws_clean(s); if (e) return e; }
+    CUDA_TRY(s, cudaMemsetAsync(s->capfail, 0, sizeof(int), s->stream));
+  }
   if (L <= s->blk_L && P <= s->blk_P) return SRO_OK;
   cudaFree(s->pcount); cudaFree(s->poff); cudaFree(s->ptotal); cudaFree(s->prow); cudaFree(s->ppos);
-  cudaFree(s->pd); cudaFree(s->pt); cudaFree(s->pdelta); cudaFree(s->tmp); cudaFree(s->sorted);
-  if (!s->rowcnt) {
-    CUDA_TRY(s, dalloc(&s->rowcnt, s->m)); CUDA_TRY(s, dalloc(&s->rowstart, s->m + 1));
-    CUDA_TRY(s, dalloc(&s->cursor, s->m + 1)); CUDA_TRY(s, dalloc(&s->X, s->m));
-    CUDA_TRY(s, dalloc(&s->trows, s->m)); CUDA_TRY(s, dalloc(&s->ntouch, 1));
-  }
+  cudaFree(s->pd); cudaFree(s->ptold); cudaFree(s->pdelta);
   s->blk_L = L; s->blk_P = P;
   CUDA_TRY(s, dalloc(&s->pcount, L)); CUDA_TRY(s, dalloc(&s->poff, L + 1)); CUDA_TRY(s, dalloc(&s->ptotal, 1));
   CUDA_TRY(s, dalloc(&s->prow, P)); CUDA_TRY(s, dalloc(&s->ppos, P)); CUDA_TRY(s, dalloc(&s->pd, P));
-  CUDA_TRY(s, dalloc(&s->pt, P)); CUDA_TRY(s, dalloc(&s->pdelta, P)); CUDA_TRY(s, dalloc(&s->tmp, P));
-  CUDA_TRY(s, dalloc(&s->sorted, P));
+  CUDA_TRY(s, dalloc(&s->ptold, P)); CUDA_TRY(s, dalloc(&s->pdelta, P));
   return SRO_OK;
+}
+
+BlockArgs block_args(Solver* s, const int* col0_dev, int col0_mul, int L, int step_rule, long long nprime,
+                     bool stop_check, double* trace_dev) {
+  BlockArgs A{};
+  A.m = s->m; A.n = s->n; A.cap = s->cap; A.lambda = s->lambda; A.a = s->a; A.b = s->b; A.r = s->r; A.h = s->h;
+  A.cnt = s->cnt; A.srow = s->srow; A.sval = s->sval; A.col0_dev = col0_dev; A.col0_mul = col0_mul; A.L = L;
+  A.W = 256 / s->G;
+  A.j = s->sw_j; A.minval = s->sw_min; A.g = s->sw_g; A.pcount = s->pcount; A.poff = s->poff; A.ptotal = s->ptotal;
+  A.prow = s->prow; A.ppos = s->ppos; A.pd = s->pd; A.ptold = s->G > 1 ? s->ptold : nullptr; A.pdelta = s->pdelta;
+  A.acc = s->acc; A.rowcnt = s->rowcnt; A.trows = s->trows; A.ntouch = s->ntouch; A.X = s->X;
+  A.scal = s->scal; A.eps = stop_check ? s->epsd : nullptr; A.stop = stop_check ? s->stop : nullptr;
+  A.status = s->status;
+  A.step_rule = step_rule; A.kk = s->lead->k + s->lead->k_pending; A.nprime = nprime; A.trace = trace_dev;
+  A.trace_col0_mul = col0_mul * s->G;
+  A.dsteps = s->dsteps;
+  A.G = s->G; A.shard = s->shard; A.slot_len = s->lead->slot_len; A.x1 = s->lead->x1; A.x2 = s->lead->x2;
+  A.capfail = s->G > 1 ? s->capfail : nullptr;
+  return A;
 }
 
 // One plain step over [col0, col0+L). For FW (stop_check) the gap G_[n] is
@@ -607,52 +766,112 @@ sro_status plain_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
   int* stop = stop_check ? s->stop : nullptr;
   st = sweep(s, col0_dev, col0_mul, 0, L, s->sw_j, s->sw_min, s->sw_g, stop);
   if (st) return st;
-  BlockArgs A{};
-  A.m = s->m; A.n = s->n; A.cap = s->cap; A.lambda = s->lambda; A.a = s->a; A.b = s->b; A.r = s->r; A.h = s->h;
-  A.cnt = s->cnt; A.srow = s->srow; A.sval = s->sval; A.col0_dev = col0_dev; A.col0_mul = col0_mul; A.L = L;
-  A.j = s->sw_j; A.minval = s->sw_min; A.g = s->sw_g; A.pcount = s->pcount; A.poff = s->poff; A.ptotal = s->ptotal;
-  A.prow = s->prow; A.ppos = s->ppos; A.pd = s->pd; A.gsum = s->pt; A.pdelta = s->pdelta; A.rowcnt = s->rowcnt;
-  A.rowstart = s->rowstart; A.cursor = s->cursor; A.tmp = s->tmp; A.sorted = s->sorted; A.X = s->X;
-  A.scal = s->scal; A.eps = stop_check ? s->epsd : nullptr; A.stop = stop; A.status = s->status;
-  A.trows = s->trows; A.ntouch = s->ntouch;
-  A.step_rule = step_rule; A.kk = s->k + s->k_pending; A.nprime = nprime; A.trace = trace_dev;
-  A.dsteps = s->dsteps;
+  BlockArgs A = block_args(s, col0_dev, col0_mul, L, step_rule, nprime, stop_check, trace_dev);
   if (L <= 1024 && !s->no_tail) {
-    const size_t smem = sizeof(double) * 32 * 256;
-    CUDA_TRY(s, cudaFuncSetAttribute(k_block_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_block_tail<<<1, 1024, smem, s->stream>>>(A);
+    k_block_tail<<<1, 1024, 0, s->stream>>>(A);
     CUDA_TRY(s, cudaGetLastError());
-    s->stats.kernel_launches += 1;
+    s->lead->stats.kernel_launches += 1;
   } else {
     const int tpb = 256;
     int gL = (L + tpb - 1) / tpb; if (gL > s->num_sms * 8) gL = s->num_sms * 8;
     const int gP = s->num_sms * 8;
-    const int gG = (s->m + 7) / 8 < s->num_sms * 8 ? (s->m + 7) / 8 : s->num_sms * 8;
-    k_psum256<<<1, 256, 0, s->stream>>>(s->sw_g, L, s->scal + 0, A.eps, stop, nullptr);
+    const int gR = (s->m + 7) / 8 < s->num_sms * 8 ? (s->m + 7) / 8 : s->num_sms * 8;
+    k_step_begin<<<1, 256, 0, s->stream>>>(A, s->scal + 0);
     k_pairs_count<<<gL, tpb, 0, s->stream>>>(A);
-    k_scan_excl<<<1, 1024, 0, s->stream>>>(s->pcount, L, s->poff, nullptr, s->ptotal, stop, s->status);
-    CUDA_TRY(s, cudaMemsetAsync(s->rowcnt, 0, sizeof(int) * s->m, s->stream));
-    CUDA_TRY(s, cudaMemsetAsync(s->ntouch, 0, sizeof(int), s->stream));
+    k_scan_pairs<<<1, 1024, 0, s->stream>>>(A);
     k_pairs_gen<<<gL, tpb, 0, s->stream>>>(A);
-    k_scan_excl<<<1, 1024, 0, s->stream>>>(s->rowcnt, s->m, s->rowstart, s->cursor, nullptr, stop, s->status);
-    k_place<<<gP, tpb, 0, s->stream>>>(A);
-    k_rank<<<gP, tpb, 0, s->stream>>>(A);
-    CUDA_TRY(s, cudaMemsetAsync(s->X, 0, sizeof(double) * s->m, s->stream));
-    k_row_groups<<<gP, tpb, 0, s->stream>>>(A, s->pd);
-    k_row_tree<0><<<gG, 256, 0, s->stream>>>(A);
+    k_runs<<<gP, tpb, 0, s->stream>>>(A, s->pd);
+    k_row_tree<0><<<gR, 256, 0, s->stream>>>(A, nullptr, 0);
     k_psum256<<<1, 256, 0, s->stream>>>(s->X, s->m, s->scal + 1, nullptr, nullptr, stop);
     k_gamma<<<1, 32, 0, s->stream>>>(A);
     k_cap_check<<<gL, tpb, 0, s->stream>>>(A);
     k_update_cols<<<gL, tpb, 0, s->stream>>>(A);
-    k_row_groups<<<gP, tpb, 0, s->stream>>>(A, s->pdelta);
-    k_row_tree<1><<<gG, 256, 0, s->stream>>>(A);
+    k_runs<<<gP, tpb, 0, s->stream>>>(A, s->pdelta);
+    k_row_tree<1><<<gR, 256, 0, s->stream>>>(A, nullptr, 1);
     k_step_done<<<1, 32, 0, s->stream>>>(A);
     CUDA_TRY(s, cudaGetLastError());
-    s->stats.kernel_launches += 16;
+    s->lead->stats.kernel_launches += 13;
   }
+  s->lead->stats.block_steps += 1;
+  s->lead->k_pending += 1;
+  timed_end(s, trb, CAT_BLOCK, L);
+  return SRO_OK;
+}
+
+// The same step over G column shards: U's positions split in
+// G contiguous ranges (local [col0, col0 + L) of every shard, L = |U| / G).
+// Phase A per shard (LMO sweep, G_U subtree, Delta subtrees) -> exchange x1
+// -> phase B per shard (combine, gamma, capacity check, update, Delta'
+// subtrees) -> exchange x2 -> apply per shard (combine, r and h).
+sro_status shard_block_step(Solver* s, const int* col0_dev, int col0_mul, int L, int step_rule, long long nprime,
+                            bool stop_check, double* trace_dev) {
+  auto H = held(s);
+  for (Solver* t : H) { sro_status st = ensure_block_ws(t, L); if (st) return st; }
+  const int trb = timed_begin(s);
+  const bool tail = L <= 1024 && !s->no_tail;
+  const int tpb = 256;
+  int gL = (L + tpb - 1) / tpb; if (gL > s->num_sms * 8) gL = s->num_sms * 8;
+  const int gP = s->num_sms * 8;
+  const int gR = (s->m + 7) / 8 < s->num_sms * 8 ? (s->m + 7) / 8 : s->num_sms * 8;
+  std::vector<BlockArgs> AA;
+  for (Solver* t : H)
+    AA.push_back(block_args(t, col0_dev, col0_mul, L, step_rule, nprime, stop_check,
+                            t->shard == 0 ? trace_dev : nullptr));
+  // phase A
+  for (size_t q = 0; q < H.size(); q++) {
+    Solver* t = H[q];
+    BlockArgs& A = AA[q];
+    sro_status st = sweep(t, col0_dev, col0_mul, 0, L, t->sw_j, t->sw_min, t->sw_g, stop_check ? t->stop : nullptr);
+    if (st) return st;
+    double* s1 = s->x1 + (size_t)t->shard * s->slot_len;
+    if (tail) {
+      k_shard_tail_a<<<1, 1024, 0, s->stream>>>(A);
+      s->stats.kernel_launches += 1;
+    } else {
+      k_step_begin<<<1, 256, 0, s->stream>>>(A, s1 + s->m);
+      k_pairs_count<<<gL, tpb, 0, s->stream>>>(A);
+      k_scan_pairs<<<1, 1024, 0, s->stream>>>(A);
+      k_zero_slot<<<gR, 256, 0, s->stream>>>(A, s1);
+      k_pairs_gen<<<gL, tpb, 0, s->stream>>>(A);
+      k_runs<<<gP, tpb, 0, s->stream>>>(A, t->pd);
+      k_row_tree<2><<<gR, 256, 0, s->stream>>>(A, s1, 0);
+      k_publish_a<<<1, 32, 0, s->stream>>>(A);
+      s->stats.kernel_launches += 8;
+    }
+    CUDA_TRY(s, cudaGetLastError());
+  }
+  { sro_status st = exchange(s, s->x1, s->slot_len); if (st) return st; }
+  // phase B
+  for (size_t q = 0; q < H.size(); q++) {
+    Solver* t = H[q];
+    BlockArgs& A = AA[q];
+    double* s2 = s->x2 + (size_t)t->shard * s->slot_len;
+    if (tail) {
+      k_shard_tail_b<<<1, 1024, 0, s->stream>>>(A);
+      s->stats.kernel_launches += 1;
+    } else {
+      k_shard_gamma<<<1, 256, 0, s->stream>>>(A);
+      k_cap_check<<<gL, tpb, 0, s->stream>>>(A);
+      k_zero_slot<<<gR, 256, 0, s->stream>>>(A, s2);
+      k_update_cols<<<gL, tpb, 0, s->stream>>>(A);
+      k_runs<<<gP, tpb, 0, s->stream>>>(A, t->pdelta);
+      k_row_tree<2><<<gR, 256, 0, s->stream>>>(A, s2, 1);
+      k_publish_b<<<1, 32, 0, s->stream>>>(A);
+      s->stats.kernel_launches += 7;
+    }
+    CUDA_TRY(s, cudaGetLastError());
+  }
+  { sro_status st = exchange(s, s->x2, s->slot_len); if (st) return st; }
+  // apply
+  const int gA = std::max(gL, gR);
+  for (size_t q = 0; q < H.size(); q++) {
+    k_shard_apply<<<gA, tpb, 0, s->stream>>>(AA[q]);
+    s->stats.kernel_launches += 1;
+  }
+  CUDA_TRY(s, cudaGetLastError());
   s->stats.block_steps += 1;
   s->k_pending += 1;
-  timed_end(s, trb, CAT_BLOCK, L);
+  timed_end(s, trb, CAT_BLOCK, L * (int64_t)H.size());
   return SRO_OK;
 }
 
@@ -664,7 +883,7 @@ sro_status drain_block_steps(Solver* s, int64_t* done) {
   CUDA_TRY(s, cudaMemcpyAsync(&ds, s->dsteps, sizeof(ds), cudaMemcpyDeviceToHost, s->stream));
   sro_status st = check_status(s);   // synchronises
   resolve_timing(s);
-  CUDA_TRY(s, cudaMemsetAsync(s->dsteps, 0, sizeof(unsigned long long), s->stream));
+  for (Solver* t : held(s)) CUDA_TRY(s, cudaMemsetAsync(t->dsteps, 0, sizeof(unsigned long long), s->stream));
   s->k += (long long)ds;
   *done += (int64_t)ds;
   s->k_pending = 0;
@@ -677,18 +896,29 @@ bool options_equal(const sro_options& x, const sro_options& y) {
          x.block_size == y.block_size;
 }
 
+// f(T) = psum256_i lin_i + psum256_k (r_k - a_k)^2 / (2 lambda) (Eq. 7). Sharded:
+// lin of the held columns goes to the shards' gx slots, which are exchanged.
 sro_status objective_dev(Solver* s, double* f_host) {
-  sro_status st = with_sweep_src(s, [&](auto src) -> sro_status {
-    k_lin<<<(s->n + 255) / 256, 256, 0, s->stream>>>(src, s->cnt, s->srow, s->sval, s->cap, s->n, s->sw_g);
-    CUDA_TRY(s, cudaGetLastError());
-    return SRO_OK;
-  });
-  if (st) return st;
-  k_psum256<<<1, 256, 0, s->stream>>>(s->sw_g, s->n, s->scal + 4, nullptr, nullptr, nullptr);
+  for (Solver* t : held(s)) {
+    double* out = s->G == 1 ? t->sw_g : s->gx + (size_t)t->shard * t->n;
+    sro_status st = with_sweep_src(t, [&](auto src) -> sro_status {
+      k_lin<<<(t->n + 255) / 256, 256, 0, s->stream>>>(src, t->cnt, t->srow, t->sval, t->cap, t->n, out);
+      CUDA_TRY(s, cudaGetLastError());
+      return SRO_OK;
+    });
+    if (st) return st;
+  }
+  if (s->G == 1) {
+    k_psum256<<<1, 256, 0, s->stream>>>(s->sw_g, s->n, s->scal + 4, nullptr, nullptr, nullptr);
+  } else {
+    sro_status st = exchange(s, s->gx, s->n);
+    if (st) return st;
+    k_psum256_gathered<<<1, 256, 0, s->stream>>>(s->gx, s->n_glob, s->Bo, s->Bl, s->n, s->scal + 4, nullptr);
+  }
   k_pen<<<(s->m + 255) / 256, 256, 0, s->stream>>>(s->r, s->a, s->m, s->sw_min);
   k_psum256<<<1, 256, 0, s->stream>>>(s->sw_min, s->m, s->scal + 5, nullptr, nullptr, nullptr);
   k_objective_final<<<1, 1, 0, s->stream>>>(s->scal + 4, s->scal + 5, s->lambda, s->scal + 7);
-  s->stats.kernel_launches += 5;
+  s->lead->stats.kernel_launches += 4 + (int64_t)held(s).size();
   CUDA_TRY(s, cudaGetLastError());
   CUDA_TRY(s, cudaMemcpyAsync(f_host, s->scal + 7, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
   CUDA_TRY(s, cudaStreamSynchronize(s->stream));
@@ -696,22 +926,24 @@ sro_status objective_dev(Solver* s, double* f_host) {
 }
 
 sro_status do_reset(Solver* s) {
-  k_init_plan<<<s->num_sms, 256, 0, s->stream>>>(s->b, s->a, s->r, s->h, s->cnt, s->srow, s->sval, s->m, s->n, s->cap,
-                                                s->lambda);
-  s->stats.kernel_launches += 1;
-  CUDA_TRY(s, cudaGetLastError());
-  CUDA_TRY(s, cudaMemsetAsync(s->stop, 0, sizeof(int), s->stream));
+  for (Solver* t : held(s)) {
+    k_init_plan<<<s->num_sms, 256, 0, s->stream>>>(t->b, t->b_full, t->n_glob, t->a, t->r, t->h, t->cnt, t->srow,
+                                                  t->sval, t->m, t->n, t->cap, t->lambda);
+    s->lead->stats.kernel_launches += 1;
+    CUDA_TRY(s, cudaGetLastError());
+    CUDA_TRY(s, cudaMemsetAsync(t->stop, 0, sizeof(int), s->stream));
+  }
   s->k = 0;
   s->configured = false;
   return SRO_OK;
 }
 
-void free_solver(Solver* s) {
+void free_shard(Solver* s) {
   if (!s) return;
-  void* ptrs[] = {s->dsteps, s->phase, s->a, s->b, s->r, s->h, s->cnt, s->srow, s->sval, s->G, s->fen, s->status, s->steps_done,
-                  s->stop, s->scal, s->epsd, s->visit, s->trace, s->sw_j, s->sw_min, s->sw_g, s->part_j,
-                  s->part_min, s->pcount, s->poff, s->ptotal, s->prow, s->ppos, s->pd, s->pt, s->pdelta,
-                  s->rowcnt, s->rowstart, s->cursor, s->tmp, s->sorted, s->X, s->trows, s->ntouch};
+  void* ptrs[] = {s->dsteps, s->phase, s->a, s->b, s->b_full, s->r, s->h, s->cnt, s->srow, s->sval, s->G_ga, s->fen,
+                  s->status, s->steps_done, s->stop, s->scal, s->epsd, s->visit, s->trace, s->sw_j, s->sw_min,
+                  s->sw_g, s->part_j, s->part_min, s->pcount, s->poff, s->ptotal, s->prow, s->ppos, s->pd,
+                  s->ptold, s->pdelta, s->acc, s->rowcnt, s->X, s->trows, s->ntouch, s->capfail};
   for (void* p : ptrs) if (p) cudaFree(p);
   if (s->owns_cost) { if (s->C) cudaFree(s->C); if (s->x) cudaFree(s->x); if (s->y) cudaFree(s->y); }
   for (auto& p : s->pending) { s->ev_pool.push_back(p.a); s->ev_pool.push_back(p.b); }
@@ -720,6 +952,85 @@ void free_solver(Solver* s) {
   if (s->ev1) cudaEventDestroy(s->ev1);
   if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
   delete s;
+}
+
+void free_solver(Solver* s) {
+  if (!s) return;
+  for (Solver* p : s->peers) free_shard(p);
+  s->peers.clear();
+  if (s->x1) cudaFree(s->x1);
+  if (s->x2) cudaFree(s->x2);
+  if (s->gx) cudaFree(s->gx);
+  if (s->comm) nccl().destroy(s->comm);
+  free_shard(s);
+}
+
+// One shard's device state. b_loc: host fp64[n_loc] (its columns' weights);
+// b_all: host fp64[n_glob]; the cost arguments describe its columns only.
+// Cost pointers: dense `data` (column-major, cost_ld), colours x (m x 3) and
+// y (n_loc x 3), each host (copied) or device (borrowed) per on_dev.
+sro_status build_shard(Solver* s, const double* a, const double* b_loc, const double* b_all, const sro_cost* cost,
+                       const void* data, int64_t cost_ld, const void* y, bool on_dev) {
+  const int m = s->m, n = s->n;
+  cudaEventCreate(&s->ev0); cudaEventCreate(&s->ev1);
+#define ALLOC(ptr, cnt_)                                                              \
+  if (dalloc(&(ptr), (cnt_)) != cudaSuccess) { s->err = "device allocation failed"; return SRO_ERR_OOM; }
+  ALLOC(s->a, m); ALLOC(s->b, n); ALLOC(s->b_full, s->n_glob); ALLOC(s->r, m); ALLOC(s->h, m);
+  ALLOC(s->cnt, n); ALLOC(s->srow, (size_t)n * s->cap); ALLOC(s->sval, (size_t)n * s->cap);
+  if (s->G == 1) { ALLOC(s->G_ga, n); ALLOC(s->fen, (size_t)n + 1); }
+  ALLOC(s->phase, 16);
+  ALLOC(s->dsteps, 1);
+  ALLOC(s->status, 1); ALLOC(s->steps_done, 1); ALLOC(s->stop, 1); ALLOC(s->scal, 8); ALLOC(s->epsd, 1);
+  ALLOC(s->sw_j, n); ALLOC(s->sw_min, (size_t)(m > n ? m : n)); ALLOC(s->sw_g, (size_t)(m > n ? m : n));
+#undef ALLOC
+  cudaMemsetAsync(s->dsteps, 0, sizeof(unsigned long long), s->stream);
+  cudaMemsetAsync(s->phase, 0, 16 * sizeof(long long), s->stream);
+  cudaMemsetAsync(s->status, 0, sizeof(int), s->stream);
+  cudaMemcpyAsync(s->a, a, sizeof(double) * m, cudaMemcpyHostToDevice, s->stream);
+  cudaMemcpyAsync(s->b, b_loc, sizeof(double) * n, cudaMemcpyHostToDevice, s->stream);
+  cudaMemcpyAsync(s->b_full, b_all, sizeof(double) * s->n_glob, cudaMemcpyHostToDevice, s->stream);
+  const size_t esz = s->prec == SRO_FP32 ? 4 : 8;
+  const int vec = 16 / (int)esz;
+  if (s->kind == SRO_COST_DENSE) {
+    if (on_dev) {
+      s->C = const_cast<void*>(data); s->ld = cost_ld;
+    } else {
+      s->ld = ((int64_t)m + vec - 1) / vec * vec;
+      if (cudaMalloc(&s->C, esz * (size_t)s->ld * n) != cudaSuccess) { s->err = "cost allocation failed"; return SRO_ERR_OOM; }
+      s->owns_cost = true;
+      if (cudaMemcpy2DAsync(s->C, esz * s->ld, data, esz * cost_ld, esz * m, n, cudaMemcpyHostToDevice, s->stream) != cudaSuccess)
+        { s->err = "cost upload failed"; return SRO_ERR_CUDA; }
+    }
+    if (s->prec == SRO_FP32) k_check_dense<float><<<s->num_sms * 4, 256, 0, s->stream>>>((const float*)s->C, s->ld, m, n, s->status);
+    else k_check_dense<double><<<s->num_sms * 4, 256, 0, s->stream>>>((const double*)s->C, s->ld, m, n, s->status);
+  } else if (s->kind == SRO_COST_HASH_UNIFORM) {
+    s->ld = ((int64_t)m + 3) / 4 * 4;
+    if (cudaMalloc(&s->C, 4 * (size_t)s->ld * n) != cudaSuccess) { s->err = "cost allocation failed"; return SRO_ERR_OOM; }
+    s->owns_cost = true;
+    k_gen_hash<<<s->num_sms * 8, 256, 0, s->stream>>>((float*)s->C, s->ld, m, n, cost->hash_seed, s->Bo, s->Bl, s->shard);
+  } else {
+    if (on_dev) { s->x = const_cast<void*>(cost->x); s->y = const_cast<void*>(y); }
+    else {
+      if (cudaMalloc(&s->x, esz * 3 * (size_t)m) != cudaSuccess || cudaMalloc(&s->y, esz * 3 * (size_t)n) != cudaSuccess)
+        { s->err = "colour allocation failed"; return SRO_ERR_OOM; }
+      s->owns_cost = true;
+      cudaMemcpyAsync(s->x, cost->x, esz * 3 * (size_t)m, cudaMemcpyHostToDevice, s->stream);
+      cudaMemcpyAsync(s->y, y, esz * 3 * (size_t)n, cudaMemcpyHostToDevice, s->stream);
+    }
+    if (s->prec == SRO_FP32) {
+      k_check_finite<float><<<64, 256, 0, s->stream>>>((const float*)s->x, 3LL * m, s->status);
+      k_check_finite<float><<<64, 256, 0, s->stream>>>((const float*)s->y, 3LL * n, s->status);
+    } else {
+      k_check_finite<double><<<64, 256, 0, s->stream>>>((const double*)s->x, 3LL * m, s->status);
+      k_check_finite<double><<<64, 256, 0, s->stream>>>((const double*)s->y, 3LL * n, s->status);
+    }
+  }
+  if (cudaGetLastError() != cudaSuccess) { s->err = "kernel launch failed at create"; return SRO_ERR_CUDA; }
+  int st = 0;
+  cudaMemcpyAsync(&st, s->status, sizeof(int), cudaMemcpyDeviceToHost, s->stream);
+  if (cudaStreamSynchronize(s->stream) != cudaSuccess) { s->err = "create failed"; return SRO_ERR_CUDA; }
+  if (st) { s->err = "cost must be finite and >= 0"; return SRO_ERR_NONFINITE; }
+  return SRO_OK;
 }
 
 }  // namespace
@@ -749,77 +1060,93 @@ sro_status sro_create(const double* a, const double* b, const sro_cost* cost, co
   for (int k = 0; k < p->m; k++) { if (!(a[k] >= 0.0) || !std::isfinite(a[k])) { g_create_err = "a must be finite and >= 0"; return SRO_ERR_MARGINALS; } sa += a[k]; }
   for (int i = 0; i < p->n; i++) { if (!(b[i] > 0.0) || !std::isfinite(b[i])) { g_create_err = "b must be finite and > 0"; return SRO_ERR_MARGINALS; } sb += b[i]; }
   if (std::fabs(sa - 1.0) > 1e-12 || std::fabs(sb - 1.0) > 1e-12) { g_create_err = "marginals must sum to 1 within 1e-12"; return SRO_ERR_MARGINALS; }
+  // sharding
+  const int G = p->shards <= 1 ? 1 : p->shards;
+  const int Bo = (G == 1 || p->shard_block == 0) ? p->n : p->shard_block;
+  const int nranks = p->nranks <= 1 ? 1 : p->nranks;
+  if (G > 1) {
+    if (G > 64 || (G & (G - 1))) { g_create_err = "shards must be a power of two <= 64"; return SRO_ERR_INVALID_ARG; }
+    if (Bo < 1 || p->n % Bo != 0 || Bo % G != 0) { g_create_err = "shard_block must divide n and be a multiple of shards"; return SRO_ERR_INVALID_ARG; }
+    if (nranks != 1 && nranks != G) { g_create_err = "nranks must be 1 or shards"; return SRO_ERR_INVALID_ARG; }
+    if (nranks > 1 && (p->rank < 0 || p->rank >= G || !p->nccl_id)) { g_create_err = "nranks > 1 needs rank in [0, shards) and nccl_id"; return SRO_ERR_INVALID_ARG; }
+    if (nranks == 1 && cost->data_on_device && cost->kind != SRO_COST_HASH_UNIFORM && Bo != p->n) {
+      g_create_err = "borrowed device cost with nranks == 1 needs shard_block == n"; return SRO_ERR_INVALID_ARG;
+    }
+  } else if (nranks != 1) { g_create_err = "nranks > 1 needs shards > 1"; return SRO_ERR_INVALID_ARG; }
+  const int nl = p->n / G, Bl = Bo / G;
+  const int kind = cost->kind, prec = kind == SRO_COST_HASH_UNIFORM ? (int)SRO_FP32 : cost->prec;
+  const size_t esz = prec == SRO_FP32 ? 4 : 8;
+  if (kind == SRO_COST_DENSE) {
+    if (!cost->data || cost->ld < p->m) { g_create_err = "dense cost needs data and ld >= m"; return SRO_ERR_INVALID_ARG; }
+    if (cost->data_on_device && (((uintptr_t)cost->data % 16) != 0 || (cost->ld * (int64_t)esz) % 16 != 0)) {
+      g_create_err = "borrowed dense cost must be 16-byte aligned with ld*elem % 16 == 0"; return SRO_ERR_INVALID_ARG;
+    }
+  } else if (kind != SRO_COST_HASH_UNIFORM && (!cost->x || !cost->y)) {
+    g_create_err = "colour cost needs x and y"; return SRO_ERR_INVALID_ARG;
+  }
 
   Solver* s = new Solver();
-  s->m = p->m; s->n = p->n; s->cap = cap; s->lambda = p->lambda; s->device = p->device;
-  s->kind = cost->kind; s->prec = cost->prec; s->borrowed = cost->data_on_device;
-  if (s->kind == SRO_COST_HASH_UNIFORM) s->prec = SRO_FP32;
   auto fail = [&](sro_status st, const std::string& msg) { g_create_err = msg.empty() ? s->err : msg; free_solver(s); return st; };
   if (cudaSetDevice(p->device) != cudaSuccess) return fail(SRO_ERR_CUDA, "cudaSetDevice failed (no CUDA device?)");
-  cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, p->device);
+  int num_sms = 148;
+  cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, p->device);
   if (p->cuda_stream) s->stream = (cudaStream_t)p->cuda_stream;
   else { if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess) return fail(SRO_ERR_CUDA, "stream"); s->own_stream = true; }
-  cudaEventCreate(&s->ev0); cudaEventCreate(&s->ev1);
-  const int m = s->m, n = s->n;
-#define ALLOC(ptr, cnt_)                                                              \
-  if (dalloc(&(ptr), (cnt_)) != cudaSuccess) return fail(SRO_ERR_OOM, "device allocation failed");
-  ALLOC(s->a, m); ALLOC(s->b, n); ALLOC(s->r, m); ALLOC(s->h, m);
-  ALLOC(s->cnt, n); ALLOC(s->srow, (size_t)n * cap); ALLOC(s->sval, (size_t)n * cap);
-  ALLOC(s->G, n); ALLOC(s->fen, (size_t)n + 1);
-  ALLOC(s->phase, 16);
-  ALLOC(s->dsteps, 1);
-  cudaMemsetAsync(s->dsteps, 0, sizeof(unsigned long long), s->stream);
-  cudaMemsetAsync(s->phase, 0, 16 * sizeof(long long), s->stream);
-  ALLOC(s->status, 1); ALLOC(s->steps_done, 1); ALLOC(s->stop, 1); ALLOC(s->scal, 8); ALLOC(s->epsd, 1);
-  ALLOC(s->sw_j, n); ALLOC(s->sw_min, (size_t)(m > n ? m : n)); ALLOC(s->sw_g, (size_t)(m > n ? m : n));
-  cudaMemsetAsync(s->status, 0, sizeof(int), s->stream);
-  cudaMemcpyAsync(s->a, a, sizeof(double) * m, cudaMemcpyHostToDevice, s->stream);
-  cudaMemcpyAsync(s->b, b, sizeof(double) * n, cudaMemcpyHostToDevice, s->stream);
-  const size_t esz = s->prec == SRO_FP32 ? 4 : 8;
-  const int vec = 16 / (int)esz;
-  if (s->kind == SRO_COST_DENSE) {
-    if (!cost->data || cost->ld < m) return fail(SRO_ERR_INVALID_ARG, "dense cost needs data and ld >= m");
-    if (cost->data_on_device) {
-      if (((uintptr_t)cost->data % 16) != 0 || (cost->ld * (int64_t)esz) % 16 != 0)
-        return fail(SRO_ERR_INVALID_ARG, "borrowed dense cost must be 16-byte aligned with ld*elem % 16 == 0");
-      s->C = const_cast<void*>(cost->data); s->ld = cost->ld;
-    } else {
-      s->ld = ((int64_t)m + vec - 1) / vec * vec;
-      if (cudaMalloc(&s->C, esz * (size_t)s->ld * n) != cudaSuccess) return fail(SRO_ERR_OOM, "cost allocation failed");
-      s->owns_cost = true;
-      if (cudaMemcpy2DAsync(s->C, esz * s->ld, cost->data, esz * cost->ld, esz * m, n, cudaMemcpyHostToDevice, s->stream) != cudaSuccess)
-        return fail(SRO_ERR_CUDA, "cost upload failed");
+  std::vector<int> shards_held;
+  if (nranks == 1) for (int q = 0; q < G; q++) shards_held.push_back(q);
+  else shards_held.push_back(p->rank);
+  for (size_t hq = 0; hq < shards_held.size(); hq++) {
+    Solver* t = hq == 0 ? s : new Solver();
+    if (hq > 0) { t->stream = s->stream; s->peers.push_back(t); }
+    t->lead = s;
+    t->m = p->m; t->n = nl; t->cap = cap; t->lambda = p->lambda; t->device = p->device; t->num_sms = num_sms;
+    t->kind = kind; t->prec = prec; t->borrowed = cost->data_on_device;
+    t->G = G; t->shard = shards_held[hq]; t->nranks = nranks; t->n_glob = p->n; t->Bo = Bo; t->Bl = Bl;
+    // this shard's columns: weights, cost data
+    std::vector<double> b_loc(nl);
+    for (int q = 0; q < nl; q++) b_loc[q] = b[global_col(t, q)];
+    const bool gather = G > 1 && nranks == 1;   // inputs cover all n columns: pick this shard's
+    const void* data = cost->data;
+    int64_t cld = cost->ld;
+    const void* y = cost->y;
+    std::vector<unsigned char> hdata, hy;
+    if (gather && kind == SRO_COST_DENSE) {
+      if (cost->data_on_device) data = (const char*)cost->data + esz * (size_t)cost->ld * (size_t)t->shard * Bl;
+      else {
+        hdata.resize(esz * (size_t)p->m * nl);
+        for (int q = 0; q < nl; q++)
+          memcpy(&hdata[esz * (size_t)p->m * q], (const char*)cost->data + esz * (size_t)cost->ld * global_col(t, q),
+                 esz * p->m);
+        data = hdata.data(); cld = p->m;
+      }
     }
-    if (s->prec == SRO_FP32) k_check_dense<float><<<s->num_sms * 4, 256, 0, s->stream>>>((const float*)s->C, s->ld, m, n, s->status);
-    else k_check_dense<double><<<s->num_sms * 4, 256, 0, s->stream>>>((const double*)s->C, s->ld, m, n, s->status);
-  } else if (s->kind == SRO_COST_HASH_UNIFORM) {
-    s->ld = ((int64_t)m + 3) / 4 * 4;
-    if (cudaMalloc(&s->C, 4 * (size_t)s->ld * n) != cudaSuccess) return fail(SRO_ERR_OOM, "cost allocation failed");
-    s->owns_cost = true;
-    k_gen_hash<<<s->num_sms * 8, 256, 0, s->stream>>>((float*)s->C, s->ld, m, n, cost->hash_seed);
-  } else {
-    if (!cost->x || !cost->y) return fail(SRO_ERR_INVALID_ARG, "colour cost needs x and y");
-    if (cost->data_on_device) { s->x = const_cast<void*>(cost->x); s->y = const_cast<void*>(cost->y); }
-    else {
-      if (cudaMalloc(&s->x, esz * 3 * (size_t)m) != cudaSuccess || cudaMalloc(&s->y, esz * 3 * (size_t)n) != cudaSuccess)
-        return fail(SRO_ERR_OOM, "colour allocation failed");
-      s->owns_cost = true;
-      cudaMemcpyAsync(s->x, cost->x, esz * 3 * (size_t)m, cudaMemcpyHostToDevice, s->stream);
-      cudaMemcpyAsync(s->y, cost->y, esz * 3 * (size_t)n, cudaMemcpyHostToDevice, s->stream);
+    if (gather && (kind == SRO_COST_SQEUCLID || kind == SRO_COST_EUCLID)) {
+      if (cost->data_on_device) y = (const char*)cost->y + esz * 3 * (size_t)t->shard * Bl;
+      else {
+        hy.resize(esz * 3 * (size_t)nl);
+        for (int q = 0; q < nl; q++) memcpy(&hy[esz * 3 * q], (const char*)cost->y + esz * 3 * (size_t)global_col(t, q), esz * 3);
+        y = hy.data();
+      }
     }
-    if (s->prec == SRO_FP32) {
-      k_check_finite<float><<<64, 256, 0, s->stream>>>((const float*)s->x, 3LL * m, s->status);
-      k_check_finite<float><<<64, 256, 0, s->stream>>>((const float*)s->y, 3LL * n, s->status);
-    } else {
-      k_check_finite<double><<<64, 256, 0, s->stream>>>((const double*)s->x, 3LL * m, s->status);
-      k_check_finite<double><<<64, 256, 0, s->stream>>>((const double*)s->y, 3LL * n, s->status);
+    sro_status st = build_shard(t, a, b_loc.data(), b, cost, data, cld, y, cost->data_on_device != 0);
+    if (st) return fail(st, t->err);
+  }
+  if (G > 1) {
+    s->slot_len = p->m + 8;
+    if (dalloc(&s->x1, (size_t)G * s->slot_len) != cudaSuccess || dalloc(&s->x2, (size_t)G * s->slot_len) != cudaSuccess ||
+        dalloc(&s->gx, (size_t)p->n) != cudaSuccess)
+      return fail(SRO_ERR_OOM, "device allocation failed");
+    cudaMemsetAsync(s->x1, 0, sizeof(double) * G * s->slot_len, s->stream);
+    cudaMemsetAsync(s->x2, 0, sizeof(double) * G * s->slot_len, s->stream);
+    if (nranks > 1) {
+      NcclApi& api = nccl();
+      if (!api.ok) return fail(SRO_ERR_NCCL, api.err);
+      ncclUniqueId id;
+      memcpy(&id, p->nccl_id, sizeof(id));
+      ncclResult_t r = api.init(&s->comm, nranks, id, p->rank);
+      if (r != ncclSuccess) { s->comm = nullptr; return fail(SRO_ERR_NCCL, std::string("ncclCommInitRank: ") + api.errstr(r)); }
     }
   }
-  if (cudaGetLastError() != cudaSuccess) return fail(SRO_ERR_CUDA, "kernel launch failed at create");
-  int st = 0;
-  cudaMemcpyAsync(&st, s->status, sizeof(int), cudaMemcpyDeviceToHost, s->stream);
-  if (cudaStreamSynchronize(s->stream) != cudaSuccess) return fail(SRO_ERR_CUDA, "create failed");
-  if (st) return fail(SRO_ERR_NONFINITE, "cost must be finite and >= 0");
   if (do_reset(s) != SRO_OK) return fail(SRO_ERR_CUDA, "");
   if (cudaStreamSynchronize(s->stream) != cudaSuccess) return fail(SRO_ERR_CUDA, "init failed");
   *out = static_cast<sro_handle>(static_cast<sro_solver*>(s));
@@ -857,12 +1184,23 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
   if (o->sampling == SRO_SAMPLE_GA && !(variant == SRO_BCFW || variant == SRO_BCAFW || variant == SRO_BCPFW)) { s->err = "GA sampling needs a BCFW-family variant"; return SRO_ERR_INVALID_ARG; }
   if (o->sampling == SRO_SAMPLE_GA && o->ga_M < 1) { s->err = "ga_M must be >= 1"; return SRO_ERR_INVALID_ARG; }
   if (o->sampling < 0 || o->sampling > 2 || o->step < 0 || o->step > 1) { s->err = "bad sampling/step"; return SRO_ERR_INVALID_ARG; }
+  const int n = s->n_glob;                                   // all columns
+  const int64_t n_held = (int64_t)s->n * (int64_t)held(s).size();   // columns this process sweeps
+  if (s->G > 1) {
+    if (variant != SRO_FW && variant != SRO_BATCHED) { s->err = "a sharded handle runs FW and BATCHED only (the sequential BCFW family does not shard)"; return SRO_ERR_INVALID_ARG; }
+    if (variant == SRO_FW && s->Bo != n) { s->err = "sharded FW needs shard_block == n"; return SRO_ERR_INVALID_ARG; }
+    if (variant == SRO_BATCHED && o->block_size != s->Bo) { s->err = "sharded BATCHED needs block_size == shard_block"; return SRO_ERR_INVALID_ARG; }
+  }
   long long nprime;
   if (variant == SRO_FW) nprime = 1;
   else if (variant == SRO_BATCHED) {
-    if (o->block_size < 1 || s->n % o->block_size != 0) { s->err = "block_size must divide n"; return SRO_ERR_INVALID_ARG; }
-    nprime = s->n / o->block_size;
-  } else nprime = s->n;
+    if (o->block_size < 1 || n % o->block_size != 0) { s->err = "block_size must divide n"; return SRO_ERR_INVALID_ARG; }
+    nprime = n / o->block_size;
+  } else nprime = n;
+  auto block_step = [&](const int* col0_dev, int B, bool stop_check, double* tr) -> sro_status {
+    if (s->G == 1) return plain_block_step(s, col0_dev, B, B, o->step, nprime, stop_check, tr);
+    return shard_block_step(s, col0_dev, B / s->G, B / s->G, o->step, nprime, stop_check, tr);
+  };
   if (s->configured) {
     if (s->variant != variant || s->seed != seed || !options_equal(s->opt, *o)) { s->err = "solver configured differently; call sro_reset"; return SRO_ERR_STATE; }
   }
@@ -874,8 +1212,8 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
     s->opt.visit = nullptr; s->opt.trace = nullptr;
     if (ga) { st = ga_initialise(s); if (st) return st; }
   }
-  CUDA_TRY(s, cudaMemcpyAsync(s->epsd, &o->epsilon, sizeof(double), cudaMemcpyHostToDevice, s->stream));
-  const int m = s->m, n = s->n;
+  for (Solver* t : held(s)) CUDA_TRY(s, cudaMemcpyAsync(t->epsd, &o->epsilon, sizeof(double), cudaMemcpyHostToDevice, s->stream));
+  const int m = s->m;
   int64_t done = 0;
   const long long period = (long long)o->gap_period * nprime;
   std::vector<int> hv;
@@ -883,11 +1221,11 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
   if (o->trace) { st = ensure_trace(s, iters > 0 ? iters : 1); if (st) return st; }
 
   if (variant == SRO_FW) {
-    CUDA_TRY(s, cudaMemsetAsync(s->stop, 0, sizeof(int), s->stream));
+    for (Solver* t : held(s)) CUDA_TRY(s, cudaMemsetAsync(t->stop, 0, sizeof(int), s->stream));
     while (done < iters) {
       const int64_t chunk = (iters - done) < 8 ? (iters - done) : 8;
       for (int64_t q = 0; q < chunk; q++) {
-        st = plain_block_step(s, nullptr, 0, n, o->step, 1, true, o->trace ? s->trace + 9 * (done + q) : nullptr);
+        st = block_step(nullptr, n, true, o->trace ? s->trace + 9 * (done + q) : nullptr);
         if (st) return st;
       }
       const int64_t before = done;
@@ -899,10 +1237,10 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
       if (st) return st;
       out->gap = G;
       out->gap_checks += (int)(done - before) + (stopped ? 1 : 0);
-      out->entries_scanned += (int64_t)m * n * ((done - before) + (stopped ? 1 : 0));
+      out->entries_scanned += (int64_t)m * n_held * ((done - before) + (stopped ? 1 : 0));
       if (stopped) { out->converged = 1; break; }
     }
-    CUDA_TRY(s, cudaMemsetAsync(s->stop, 0, sizeof(int), s->stream));
+    for (Solver* t : held(s)) CUDA_TRY(s, cudaMemsetAsync(t->stop, 0, sizeof(int), s->stream));
   } else {
     // visit order for the whole call (U / P / explicit); GA draws on the device
     if (!ga) {
@@ -918,7 +1256,7 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
         st = gap_sweep(s, &g);
         if (st) return st;
         out->gap = g; out->gap_checks++;
-        out->entries_scanned += (int64_t)m * n;
+        out->entries_scanned += (int64_t)m * n_held;
         if (g <= o->epsilon) { out->converged = 1; break; }
       }
       if (done >= iters) break;
@@ -929,12 +1267,11 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
         if (seg > to_check) seg = to_check;
         const int64_t before = done;
         for (long long q = 0; q < seg; q++) {
-          st = plain_block_step(s, s->visit + done + q, o->block_size, o->block_size, o->step, nprime, false,
-                                o->trace ? s->trace + 9 * (done + q) : nullptr);
+          st = block_step(s->visit + done + q, o->block_size, false, o->trace ? s->trace + 9 * (done + q) : nullptr);
           if (st) return st;
         }
         st = drain_block_steps(s, &done);
-        out->entries_scanned += (int64_t)m * o->block_size * (done - before);
+        out->entries_scanned += (int64_t)m * (o->block_size / s->G) * (int64_t)held(s).size() * (done - before);
         if (st) break;
         continue;
       }
@@ -984,9 +1321,21 @@ sro_status sro_gap(sro_handle h, double* total, double* per_column, int32_t* arg
   cudaSetDevice(s->device);
   sro_status st = gap_sweep(s, total);
   if (st) return st;
-  if (per_column) CUDA_TRY(s, cudaMemcpyAsync(per_column, s->sw_g, sizeof(double) * s->n, cudaMemcpyDeviceToHost, s->stream));
-  if (argmin_rows) CUDA_TRY(s, cudaMemcpyAsync(argmin_rows, s->sw_j, sizeof(int) * s->n, cudaMemcpyDeviceToHost, s->stream));
+  if (!per_column && !argmin_rows) return SRO_OK;
+  auto cols = held_order(s);
+  auto H = held(s);
+  std::vector<std::vector<double>> g(H.size(), std::vector<double>(s->n));
+  std::vector<std::vector<int>> j(H.size(), std::vector<int>(s->n));
+  for (size_t q = 0; q < H.size(); q++) {
+    const double* src = s->G == 1 ? s->sw_g : s->gx + (size_t)H[q]->shard * s->n;
+    CUDA_TRY(s, cudaMemcpyAsync(g[q].data(), src, sizeof(double) * s->n, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(s, cudaMemcpyAsync(j[q].data(), H[q]->sw_j, sizeof(int) * s->n, cudaMemcpyDeviceToHost, s->stream));
+  }
   CUDA_TRY(s, cudaStreamSynchronize(s->stream));
+  for (size_t c = 0; c < cols.size(); c++) {
+    if (per_column) per_column[c] = g[cols[c].hq][cols[c].p];
+    if (argmin_rows) argmin_rows[c] = j[cols[c].hq][cols[c].p];
+  }
   return SRO_OK;
 }
 
@@ -1011,24 +1360,51 @@ sro_status sro_get_plan(sro_handle h, double* dense, int32_t* rows, int32_t* col
   if (!h) return SRO_ERR_INVALID_ARG;
   Solver* s = static_cast<Solver*>(h);
   cudaSetDevice(s->device);
-  std::vector<int> hc(s->n), hr((size_t)s->n * s->cap);
-  std::vector<double> hv((size_t)s->n * s->cap);
-  CUDA_TRY(s, cudaMemcpyAsync(hc.data(), s->cnt, sizeof(int) * s->n, cudaMemcpyDeviceToHost, s->stream));
-  CUDA_TRY(s, cudaMemcpyAsync(hr.data(), s->srow, sizeof(int) * hr.size(), cudaMemcpyDeviceToHost, s->stream));
-  CUDA_TRY(s, cudaMemcpyAsync(hv.data(), s->sval, sizeof(double) * hv.size(), cudaMemcpyDeviceToHost, s->stream));
+  auto H = held(s);
+  std::vector<std::vector<int>> hc(H.size()), hr(H.size());
+  std::vector<std::vector<double>> hv(H.size());
+  for (size_t q = 0; q < H.size(); q++) {
+    Solver* t = H[q];
+    hc[q].resize(t->n); hr[q].resize((size_t)t->n * t->cap); hv[q].resize((size_t)t->n * t->cap);
+    CUDA_TRY(s, cudaMemcpyAsync(hc[q].data(), t->cnt, sizeof(int) * t->n, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(s, cudaMemcpyAsync(hr[q].data(), t->srow, sizeof(int) * hr[q].size(), cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(s, cudaMemcpyAsync(hv[q].data(), t->sval, sizeof(double) * hv[q].size(), cudaMemcpyDeviceToHost, s->stream));
+  }
   CUDA_TRY(s, cudaStreamSynchronize(s->stream));
-  if (dense) memset(dense, 0, sizeof(double) * (size_t)s->m * s->n);
+  auto order = held_order(s);
+  if (dense) memset(dense, 0, sizeof(double) * (size_t)s->m * order.size());
   int64_t q = 0;
-  for (int i = 0; i < s->n; i++)
-    for (int e = 0; e < hc[i]; e++) {
-      const int k = hr[(size_t)i * s->cap + e];
-      const double v = hv[(size_t)i * s->cap + e];
-      if (dense) dense[(size_t)i * s->m + k] = v;
-      if (rows && cols && vals && q < cap) { rows[q] = k; cols[q] = i; vals[q] = v; }
+  for (size_t c = 0; c < order.size(); c++) {
+    const int hq = order[c].hq, p = order[c].p;
+    for (int e = 0; e < hc[hq][p]; e++) {
+      const int k = hr[hq][(size_t)p * s->cap + e];
+      const double v = hv[hq][(size_t)p * s->cap + e];
+      if (dense) dense[c * (size_t)s->m + k] = v;
+      if (rows && cols && vals && q < cap) { rows[q] = k; cols[q] = order[c].global; vals[q] = v; }
       q++;
     }
+  }
   if (nnz) *nnz = q;
   if (rows && cols && vals && q > cap) { s->err = "COO capacity too small"; return SRO_ERR_CAPACITY; }
+  return SRO_OK;
+}
+
+sro_status sro_held_columns(sro_handle h, int32_t* cols, int32_t* n_held) {
+  if (!h || !n_held) return SRO_ERR_INVALID_ARG;
+  auto order = held_order(static_cast<Solver*>(h));
+  *n_held = (int32_t)order.size();
+  if (cols) for (size_t c = 0; c < order.size(); c++) cols[c] = order[c].global;
+  return SRO_OK;
+}
+
+sro_status sro_nccl_unique_id(uint8_t* out128) {
+  if (!out128) return SRO_ERR_INVALID_ARG;
+  NcclApi& api = nccl();
+  if (!api.ok) { g_create_err = api.err; return SRO_ERR_NCCL; }
+  ncclUniqueId id;
+  ncclResult_t r = api.get_id(&id);
+  if (r != ncclSuccess) { g_create_err = std::string("ncclGetUniqueId: ") + api.errstr(r); return SRO_ERR_NCCL; }
+  memcpy(out128, &id, sizeof(id));
   return SRO_OK;
 }
 

@@ -13,6 +13,7 @@ import numpy as np
 __all__ = [
     "load_library", "Solver", "SroError", "SRO_FW", "SRO_BCFW", "SRO_BCAFW", "SRO_BCPFW", "SRO_BATCHED",
     "STEP_DEC", "STEP_ELS", "SAMPLE_U", "SAMPLE_P", "SAMPLE_GA", "TRACE_DTYPE", "EXPORTED_SYMBOLS",
+    "nccl_unique_id",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -25,7 +26,8 @@ COST_KINDS = {"dense": 0, "sqeuclid": 1, "euclid": 2, "hash": 3}
 PRECS = {"f64": 0, "f32": 1}
 OK, NOT_CONVERGED = 0, 1
 EXPORTED_SYMBOLS = ("sro_create", "sro_solve", "sro_gap", "sro_objective", "sro_get_plan", "sro_get_rowsums",
-                    "sro_reset", "sro_destroy", "sro_last_error", "sro_version", "sro_get_stats", "sro_set_timing")
+                    "sro_reset", "sro_destroy", "sro_last_error", "sro_version", "sro_get_stats", "sro_set_timing",
+                    "sro_held_columns", "sro_nccl_unique_id")
 
 _STATUS = {0: "OK", 1: "NOT_CONVERGED", 2: "ERR_INVALID_ARG", 3: "ERR_DIMENSION", 4: "ERR_MARGINALS",
            5: "ERR_NONFINITE", 6: "ERR_CAPACITY", 7: "ERR_CUDA", 8: "ERR_NCCL", 9: "ERR_OOM", 10: "ERR_STATE"}
@@ -44,7 +46,8 @@ class SroCost(ct.Structure):
 
 class SroParams(ct.Structure):
     _fields_ = [("m", ct.c_int32), ("n", ct.c_int32), ("lambda_", ct.c_double), ("slab_cap", ct.c_int32),
-                ("device", ct.c_int32), ("cuda_stream", ct.c_void_p)]
+                ("device", ct.c_int32), ("cuda_stream", ct.c_void_p), ("shards", ct.c_int32),
+                ("shard_block", ct.c_int32), ("nranks", ct.c_int32), ("rank", ct.c_int32), ("nccl_id", ct.c_void_p)]
 
 
 class SroTraceRec(ct.Structure):
@@ -111,6 +114,10 @@ def load_library():
         L.sro_set_timing.restype = ct.c_int
         L.sro_version.argtypes = []
         L.sro_version.restype = ct.c_char_p
+        L.sro_held_columns.argtypes = [vp, vp, ct.POINTER(i32)]
+        L.sro_held_columns.restype = ct.c_int
+        L.sro_nccl_unique_id.argtypes = [vp]
+        L.sro_nccl_unique_id.restype = ct.c_int
         _lib = L
     return _lib
 
@@ -138,7 +145,7 @@ class Solver:
     """
 
     def __init__(self, a, b, lam, *, C=None, X=None, Y=None, cost="dense", prec="f64", hash_seed=0, slab_cap=31,
-                 device=0, stream=None, ld=None):
+                 device=0, stream=None, ld=None, shards=1, shard_block=0, nranks=1, rank=0, nccl_id=None):
         L = load_library()
         self._L = L
         a = np.ascontiguousarray(a, dtype=np.float64)
@@ -157,7 +164,7 @@ class Solver:
                 c.ld = ld if ld is not None else C.shape[1]
             else:
                 Cm = np.asarray(C, dtype=dt)
-                assert Cm.shape == (self.m, self.n)
+                assert Cm.shape[0] == self.m
                 Ccm = np.ascontiguousarray(Cm.T)        # column i contiguous
                 keep.append(Ccm)
                 c.data, c.ld = _ptr(Ccm), self.m
@@ -169,14 +176,23 @@ class Solver:
                 Yc = np.ascontiguousarray(Y, dtype=dt)
                 keep += [Xc, Yc]
                 c.x, c.y = _ptr(Xc), _ptr(Yc)
+        idbuf = None
+        if nccl_id is not None:
+            idbuf = ct.create_string_buffer(bytes(nccl_id), 128)
         p = SroParams(m=self.m, n=self.n, lambda_=self.lam, slab_cap=slab_cap, device=device,
-                      cuda_stream=ct.c_void_p(stream) if stream else None)
+                      cuda_stream=ct.c_void_p(stream) if stream else None, shards=shards, shard_block=shard_block,
+                      nranks=nranks, rank=rank, nccl_id=ct.cast(idbuf, ct.c_void_p) if idbuf is not None else None)
         h = ct.c_void_p()
         st = L.sro_create(_ptr(a), _ptr(b), ct.byref(c), ct.byref(p), ct.byref(h))
         if st != OK:
             raise SroError(st, L.sro_last_error(None).decode())
         self.h = h
         self.cap = slab_cap
+        nh = ct.c_int32()
+        self._check(L.sro_held_columns(h, None, ct.byref(nh)))
+        self.held = np.empty(nh.value, dtype=np.int32)
+        self._check(L.sro_held_columns(h, _ptr(self.held), ct.byref(nh)))
+        self.n_held = nh.value
 
     def _check(self, st, allow=(OK,)):
         if st not in allow:
@@ -215,8 +231,8 @@ class Solver:
 
     def gap(self):
         tot = ct.c_double()
-        g = np.empty(self.n)
-        j = np.empty(self.n, dtype=np.int32)
+        g = np.empty(self.n_held)
+        j = np.empty(self.n_held, dtype=np.int32)
         self._check(self._L.sro_gap(self.h, ct.byref(tot), _ptr(g), _ptr(j)))
         return tot.value, g, j
 
@@ -226,10 +242,10 @@ class Solver:
         return f.value
 
     def plan(self):
-        T = np.empty(self.m * self.n)
+        T = np.empty(self.m * self.n_held)
         nnz = ct.c_int64()
         self._check(self._L.sro_get_plan(self.h, _ptr(T), None, None, None, 0, ct.byref(nnz)))
-        return T.reshape(self.n, self.m).T.copy()
+        return T.reshape(self.n_held, self.m).T.copy()
 
     def plan_coo(self):
         nnz = ct.c_int64()
@@ -256,3 +272,13 @@ class Solver:
         s = SroStats()
         self._check(self._L.sro_get_stats(self.h, ct.byref(s), 1 if reset else 0))
         return {f: getattr(s, f) for f, _ in SroStats._fields_}
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte NCCL unique id (create on rank 0, share with the other ranks)."""
+    L = load_library()
+    buf = ct.create_string_buffer(128)
+    st = L.sro_nccl_unique_id(ct.cast(buf, ct.c_void_p))
+    if st != OK:
+        raise SroError(st, L.sro_last_error(None).decode())
+    return buf.raw
