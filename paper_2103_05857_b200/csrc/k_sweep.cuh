@@ -8,8 +8,9 @@
 // coalesced column read, BASELINE north_star), h staged per row slab in
 // shared memory and reused by every column the CTA visits. One warp owns one
 // column at a time; a CTA of 8 warps streams many columns. Rows are split in
-// slabs of at most SLAB rows (blockIdx.y); with more than one slab the
-// per-slab (min, row) partials are merged in slab order by k_lmo_merge.
+// slabs of slab_rows rows (blockIdx.y; the host sizes slabs for occupancy);
+// with more than one slab the per-slab (min, row) partials are merged in slab
+// order by k_lmo_merge.
 // Roofline: HBM (dense, 4 or 8 B per entry) or FP32/FP64 issue (colours).
 #pragma once
 #include "sro_device.cuh"
@@ -18,7 +19,7 @@ namespace sro {
 
 constexpr int SWEEP_THREADS = 256;
 constexpr int SWEEP_WARPS = SWEEP_THREADS / 32;
-constexpr int SLAB = 8192;
+constexpr int SLAB_MAX = 8192;   // rows of h staged per CTA at most (the host picks the slab)
 
 __device__ __forceinline__ float4 ld_stream(const float4* p) { return __ldcs(p); }
 __device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
@@ -44,15 +45,20 @@ __device__ __forceinline__ void proc4(const double2& v, int k, const double* hs,
   if (x1 < best) { best = x1; bj = k + 1; }
 }
 
+// Dense column-major cost. h is staged in shared memory in W planes
+// (plane t holds h[row0 + W v + t], v < rows / W; rows past the last full
+// vector follow the planes), so a lane's W consecutive rows read W
+// conflict-free doubles (consecutive lanes -> consecutive addresses).
 template <typename T>
 struct SrcDense {
   const T* C;
   int64_t ld;
   static constexpr int SMEM_PER_ROW = 0;
+  static constexpr bool PLANAR = true;
   __device__ __forceinline__ void stage(int, int, char*) const {}
   __device__ __forceinline__ double cost(int k, int i) const { return (double)C[(int64_t)i * ld + k]; }
   // Scan rows [row0, row0+rows) of column i; lane-strided 128-bit vectors,
-  // rows ascending within a lane. hs is the slab of h (index k - row0).
+  // rows ascending within a lane, 8 vectors in flight per lane.
   __device__ __forceinline__ void scan(int i, int row0, int rows, const double* hs, const char*, double& best,
                                        int& bj) const {
     using V = typename Vec<T>::type;
@@ -61,20 +67,43 @@ struct SrcDense {
     const V* p = reinterpret_cast<const V*>(C + (int64_t)i * ld + row0);
     const int nvec = rows / W;
     int q = lane;
-    for (; q + 96 < nvec; q += 128) {
-      V a = ld_stream(p + q), b = ld_stream(p + q + 32), c = ld_stream(p + q + 64), d = ld_stream(p + q + 96);
-      proc4(a, W * q, hs, best, bj);
-      proc4(b, W * (q + 32), hs, best, bj);
-      proc4(c, W * (q + 64), hs, best, bj);
-      proc4(d, W * (q + 96), hs, best, bj);
+    for (; q + 224 < nvec; q += 256) {
+      V v[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) v[u] = ld_stream(p + q + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 8; u++) procW(v[u], q + 32 * u, nvec, hs, best, bj);
     }
-    for (; q < nvec; q += 32) proc4(ld_stream(p + q), W * q, hs, best, bj);
+    for (; q < nvec; q += 32) procW(ld_stream(p + q), q, nvec, hs, best, bj);
     const int k = nvec * W + lane;
     if (k < rows) {
       double x = d_add((double)C[(int64_t)i * ld + row0 + k], hs[k]);
       if (x < best) { best = x; bj = k; }
     }
     // bj is slab-relative here; caller adds row0
+  }
+  __device__ __forceinline__ static void procW(const float4& v, int q, int nvec, const double* hs, double& best,
+                                               int& bj) {
+    const int k = 4 * q;
+    double x0 = d_add((double)v.x, hs[q]), x1 = d_add((double)v.y, hs[nvec + q]);
+    double x2 = d_add((double)v.z, hs[2 * nvec + q]), x3 = d_add((double)v.w, hs[3 * nvec + q]);
+    if (x0 < best) { best = x0; bj = k; }
+    if (x1 < best) { best = x1; bj = k + 1; }
+    if (x2 < best) { best = x2; bj = k + 2; }
+    if (x3 < best) { best = x3; bj = k + 3; }
+  }
+  __device__ __forceinline__ static void procW(const double2& v, int q, int nvec, const double* hs, double& best,
+                                               int& bj) {
+    const int k = 2 * q;
+    double x0 = d_add(v.x, hs[q]), x1 = d_add(v.y, hs[nvec + q]);
+    if (x0 < best) { best = x0; bj = k; }
+    if (x1 < best) { best = x1; bj = k + 1; }
+  }
+  // shared-memory index of slab row k
+  __device__ __forceinline__ static int hidx(int k, int rows) {
+    constexpr int W = Vec<T>::W;
+    const int nvec = rows / W;
+    return k < nvec * W ? (k % W) * nvec + k / W : k;
   }
 };
 
@@ -83,6 +112,8 @@ struct SrcColour {
   const T* x;   // 3m
   const T* y;   // 3n
   static constexpr int SMEM_PER_ROW = 3 * sizeof(T);
+  static constexpr bool PLANAR = false;
+  __device__ __forceinline__ static int hidx(int k, int) { return k; }
   __device__ __forceinline__ void stage(int row0, int rows, char* sm) const {
     T* xs = reinterpret_cast<T*>(sm);
     for (int k = threadIdx.x; k < rows; k += blockDim.x) {
@@ -136,7 +167,7 @@ struct SweepOut {
 
 // grid = (gx, nslabs). col0 = col0_dev ? *col0_dev * col0_mul : col0_host.
 template <class Src>
-__global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_sweep(Src src, int m, const double* __restrict__ h,
+__global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_sweep(Src src, int m, int slab_rows, const double* __restrict__ h,
                                                              const int* __restrict__ col0_dev, int col0_mul,
                                                              int col0_host, int L, const int* __restrict__ cnt,
                                                              const int* __restrict__ srow,
@@ -146,9 +177,9 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_sweep(Src src, int m, con
   if (stop && *stop) return;
   extern __shared__ __align__(16) double sm_h[];
   const int nslabs = gridDim.y, slab = blockIdx.y;
-  const int row0 = slab * SLAB;
-  const int rows = min(SLAB, m - row0);
-  for (int k = threadIdx.x; k < rows; k += blockDim.x) sm_h[k] = h[row0 + k];
+  const int row0 = slab * slab_rows;
+  const int rows = min(slab_rows, m - row0);
+  for (int k = threadIdx.x; k < rows; k += blockDim.x) sm_h[Src::hidx(k, rows)] = h[row0 + k];
   char* sm_src = reinterpret_cast<char*>(sm_h + ((rows + 1) & ~1));
   src.stage(row0, rows, sm_src);
   __syncthreads();
@@ -194,6 +225,134 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_merge(Src src, int nslabs
     if (!(best < 1.0e308 && best > -1.0e308)) { if (lane == 0) set_status(status, 5); }
     const double g = column_gap_epilogue(src, col0 + p, best, cnt, srow, sval, cap, b, h);
     if (lane == 0) { out_j[p] = bj; out_min[p] = best; out_g[p] = g; }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Dense sweep with bulk asynchronous copies (TMA engine, cp.async.bulk ->
+// SASS UBLKCP): every warp runs its own S-stage ring of 4 KiB shared-memory
+// buffers, refilled by one lane with an mbarrier completion per stage, so
+// S x 4 KiB per warp are in flight independently of the register file (the
+// LDG version issues loads just in time and keeps ~1 KiB per warp in flight).
+// Work = (slab, column) items, slab-major, split into one contiguous range per
+// CTA of a grid sized to the SM count: a CTA restages h (planar, as
+// SrcDense) only when its range enters the next slab.
+// ---------------------------------------------------------------------------
+constexpr int BULK_WARPS = 8;
+constexpr int BULK_CH = 4096;   // bytes per stage
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+template <typename T, int S>
+__global__ void __launch_bounds__(BULK_WARPS * 32, 1)
+    k_lmo_sweep_bulk(SrcDense<T> src, int m, int slab_rows, int nslabs, const double* __restrict__ h,
+                     const int* __restrict__ col0_dev, int col0_mul, int col0_host, int L,
+                     const int* __restrict__ cnt, const int* __restrict__ srow, const double* __restrict__ sval,
+                     int cap, const double* __restrict__ b, SweepOut out, const int* __restrict__ stop,
+                     int* status) {
+  using V = typename Vec<T>::type;
+  constexpr int W = Vec<T>::W;
+  constexpr int CHV = BULK_CH / 16;   // vectors per stage
+  if (stop && *stop) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+  unsigned char* bufs = smem + 1024;
+  double* hs = reinterpret_cast<double*>(bufs + (size_t)BULK_WARPS * S * BULK_CH);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x < BULK_WARPS * S) mbar_init(&bars[threadIdx.x], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  uint64_t* wb = bars + warp * S;
+  unsigned char* wbuf = bufs + (size_t)warp * S * BULK_CH;
+  const int col0 = col0_dev ? (*col0_dev) * col0_mul : col0_host;
+  const int64_t ntot = (int64_t)nslabs * L;
+  const int64_t lo = ntot * blockIdx.x / gridDim.x, hi = ntot * (blockIdx.x + 1) / gridDim.x;
+  long long tcons = 0, tiss = 0;   // per-warp stage counters (uniform across the warp)
+  for (int64_t seg = lo; seg < hi;) {
+    const int slab = (int)(seg / L);
+    const int64_t seg_end = min(hi, (int64_t)(slab + 1) * L);
+    const int row0 = slab * slab_rows;
+    const int rows = min(slab_rows, m - row0);
+    const int nvec = rows / W;
+    const int nch = (nvec + CHV - 1) / CHV;
+    __syncthreads();
+    for (int k = threadIdx.x; k < rows; k += blockDim.x) hs[SrcDense<T>::hidx(k, rows)] = h[row0 + k];
+    __syncthreads();
+    const int p_first = (int)(seg - (int64_t)slab * L) + warp;
+    const int p_end = (int)(seg_end - (int64_t)slab * L);
+    const int ncol = p_first < p_end ? (p_end - p_first + BULK_WARPS - 1) / BULK_WARPS : 0;
+    const int64_t tot = (int64_t)ncol * nch;
+    int64_t e_iss = 0;
+    auto issue = [&]() {
+      const int jc = (int)(e_iss / nch), c = (int)(e_iss % nch);
+      const int i = col0 + p_first + jc * BULK_WARPS;
+      const int v0 = c * CHV, nv = min(CHV, nvec - v0);
+      const int slot = (int)(tiss % S);
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const T* g = src.C + (int64_t)i * src.ld + row0 + (int64_t)v0 * W;
+        mbar_expect_tx(&wb[slot], (uint32_t)nv * 16u);
+        bulk_g2s(wbuf + (size_t)slot * BULK_CH, g, (uint32_t)nv * 16u, &wb[slot]);
+      }
+      tiss++;
+      e_iss++;
+    };
+    while (e_iss < tot && e_iss < S) issue();
+    for (int jc = 0; jc < ncol; jc++) {
+      const int p = p_first + jc * BULK_WARPS;
+      const int i = col0 + p;
+      double best = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+      int bj = 0x7fffffff;
+      for (int c = 0; c < nch; c++) {
+        const int slot = (int)(tcons % S);
+        const uint32_t parity = (uint32_t)((tcons / S) & 1);
+        while (!mbar_try_wait(&wb[slot], parity)) {
+        }
+        const V* vb = reinterpret_cast<const V*>(wbuf + (size_t)slot * BULK_CH);
+        const int v0 = c * CHV, nv = min(CHV, nvec - v0);
+#pragma unroll 4
+        for (int u = lane; u < nv; u += 32) SrcDense<T>::procW(vb[u], v0 + u, nvec, hs, best, bj);
+        tcons++;
+        __syncwarp();
+        if (e_iss < tot) issue();
+      }
+      const int k = nvec * W + lane;   // rows past the last full vector
+      if (k < rows) {
+        const double x = d_add((double)src.C[(int64_t)i * src.ld + row0 + k], hs[k]);
+        if (x < best) { best = x; bj = k; }
+      }
+      if (bj != 0x7fffffff) bj += row0;
+      warp_argmin(best, bj);
+      if (nslabs == 1) {
+        if (!(best < 1.0e308 && best > -1.0e308)) { if (lane == 0) set_status(status, 5); }
+        const double g = column_gap_epilogue(src, i, best, cnt, srow, sval, cap, b, h);
+        if (lane == 0) { out.j[p] = bj; out.minval[p] = best; out.g[p] = g; }
+      } else if (lane == 0) {
+        out.j[(int64_t)slab * L + p] = bj;
+        out.minval[(int64_t)slab * L + p] = best;
+      }
+    }
+    seg = seg_end;
   }
 }
 

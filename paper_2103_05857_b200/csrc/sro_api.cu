@@ -22,6 +22,7 @@
 #include <cstring>
 #include <string>
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/sro.h"
@@ -124,6 +125,10 @@ struct Solver {
   unsigned long long* dsteps = nullptr;   // device count of completed block steps
   long long k_pending = 0;                // block steps enqueued since the last sync
   int num_sms = 148;
+  // rows of h per sweep CTA (occupancy vs. merge work; SRO_SLAB overrides, multiple of 4, <= SLAB_MAX)
+  int slab_rows = getenv("SRO_SLAB") ? std::max(4, std::min(SLAB_MAX, atoi(getenv("SRO_SLAB")) / 4 * 4)) : 4096;
+  int slab_bulk = getenv("SRO_SLAB") ? std::max(4, std::min(SLAB_MAX, atoi(getenv("SRO_SLAB")) / 4 * 4)) : 8192;
+  bool sweep_ldg = getenv("SRO_SWEEP_LDG") != nullptr;   // debug / A-B: dense sweeps without bulk copies
   // accounting
   long long* phase = nullptr;   // device [8] clock64 totals (SRO_PHASE_TIMING builds)
   double cmax = -1.0;           // max cost, computed once (ensure_cmax)
@@ -426,10 +431,65 @@ sro_status exchange(Solver* s, double* buf, size_t count) {
   return SRO_OK;
 }
 
+sro_status ensure_partials(Solver* s, int nslabs, int L) {
+  if (nslabs > 1 && (int64_t)nslabs * L > s->part_cap) {
+    cudaFree(s->part_j); cudaFree(s->part_min);
+    s->part_cap = (int64_t)nslabs * L;
+    CUDA_TRY(s, dalloc(&s->part_j, s->part_cap));
+    CUDA_TRY(s, dalloc(&s->part_min, s->part_cap));
+  }
+  return SRO_OK;
+}
+
+// Dense LMO sweep through the bulk-copy pipeline (k_lmo_sweep_bulk): one CTA
+// per SM, (slab, column) items split evenly over the grid.
+template <class Src>
+sro_status sweep_bulk(Solver* s, Src src, const int* col0_dev, int col0_mul, int col0_host, int L, int* out_j,
+                      double* out_min, double* out_g, const int* stop) {
+  using T = std::remove_cv_t<std::remove_pointer_t<decltype(src.C)>>;
+  constexpr int S = 4;
+  const int slab = s->slab_bulk;
+  const int nslabs = (s->m + slab - 1) / slab;
+  { sro_status st = ensure_partials(s, nslabs, L); if (st) return st; }
+  const int rows = s->m < slab ? s->m : slab;
+  const size_t smem = 1024 + (size_t)BULK_WARPS * S * BULK_CH + sizeof(double) * (size_t)rows;
+  auto kern = k_lmo_sweep_bulk<T, S>;
+  CUDA_TRY(s, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BULK_WARPS * 32, smem));
+  if (per_sm < 1) per_sm = 1;
+  const int64_t ntot = (int64_t)nslabs * L;
+  int64_t nb = (int64_t)s->num_sms * per_sm;
+  const int64_t need = (ntot + BULK_WARPS - 1) / BULK_WARPS;
+  if (nb > need) nb = need;
+  if (nb < 1) nb = 1;
+  SweepOut o;
+  if (nslabs == 1) { o.j = out_j; o.minval = out_min; o.g = out_g; }
+  else { o.j = s->part_j; o.minval = s->part_min; o.g = nullptr; }
+  const int tr = timed_begin(s);
+  s->lead->stats.kernel_launches += nslabs > 1 ? 2 : 1;
+  s->lead->stats.sweep_launches += 1;
+  s->lead->stats.sweep_columns += L;
+  kern<<<(int)nb, BULK_WARPS * 32, smem, s->stream>>>(src, s->m, slab, nslabs, s->h, col0_dev, col0_mul, col0_host, L,
+                                                    s->cnt, s->srow, s->sval, s->cap, s->b, o, stop, s->status);
+  CUDA_TRY(s, cudaGetLastError());
+  if (nslabs > 1) {
+    int gm = (L + SWEEP_WARPS - 1) / SWEEP_WARPS;
+    if (gm > s->num_sms * 8) gm = s->num_sms * 8;
+    k_lmo_merge<Src><<<gm, SWEEP_THREADS, 0, s->stream>>>(src, nslabs, s->h, col0_dev, col0_mul, col0_host, L, s->cnt,
+                                                          s->srow, s->sval, s->cap, s->b, s->part_j, s->part_min,
+                                                          out_j, out_min, out_g, stop, s->status);
+    CUDA_TRY(s, cudaGetLastError());
+  }
+  timed_end(s, tr, CAT_SWEEP, L);
+  return SRO_OK;
+}
+
 // LMO sweep over [col0, col0+L) -> out_j, out_min, out_g (device arrays of length >= L).
 sro_status sweep(Solver* s, const int* col0_dev, int col0_mul, int col0_host, int L, int* out_j, double* out_min,
                  double* out_g, const int* stop) {
-  const int nslabs = (s->m + SLAB - 1) / SLAB;
+  const int slab = s->slab_rows;
+  const int nslabs = (s->m + slab - 1) / slab;
   if (nslabs > 1 && (int64_t)nslabs * L > s->part_cap) {
     cudaFree(s->part_j); cudaFree(s->part_min);
     s->part_cap = (int64_t)nslabs * L;
@@ -438,7 +498,10 @@ sro_status sweep(Solver* s, const int* col0_dev, int col0_mul, int col0_host, in
   }
   return with_sweep_src(s, [&](auto src) -> sro_status {
     using Src = decltype(src);
-    const int rows = s->m < SLAB ? s->m : SLAB;
+    if constexpr (Src::PLANAR) {
+      if (!s->sweep_ldg) return sweep_bulk(s, src, col0_dev, col0_mul, col0_host, L, out_j, out_min, out_g, stop);
+    }
+    const int rows = s->m < slab ? s->m : slab;
     const size_t smem = sizeof(double) * (size_t)((rows + 1) & ~1) + (size_t)Src::SMEM_PER_ROW * rows;
     auto kern = k_lmo_sweep<Src>;
     CUDA_TRY(s, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -457,7 +520,7 @@ sro_status sweep(Solver* s, const int* col0_dev, int col0_mul, int col0_host, in
     s->lead->stats.kernel_launches += nslabs > 1 ? 2 : 1;
     s->lead->stats.sweep_launches += 1;
     s->lead->stats.sweep_columns += L;
-    kern<<<dim3(gx, nslabs), SWEEP_THREADS, smem, s->stream>>>(src, s->m, s->h, col0_dev, col0_mul, col0_host, L,
+    kern<<<dim3(gx, nslabs), SWEEP_THREADS, smem, s->stream>>>(src, s->m, slab, s->h, col0_dev, col0_mul, col0_host, L,
                                                              s->cnt, s->srow, s->sval, s->cap, s->b, o, stop,
                                                              s->status);
     CUDA_TRY(s, cudaGetLastError());

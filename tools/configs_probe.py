@@ -20,7 +20,7 @@ def emit(**kw):
     print(json.dumps(kw), flush=True)
 
 
-def cfg3(sweeps=5, fw_iters=200):
+def cfg3(sweeps=5, fw_iters=200, fw=True):
     d = instance(3, seed=0)
     t0 = time.perf_counter()
     s = sro.Solver(d["a"], d["b"], 1.0, cost="hash", hash_seed=d["hash_seed"])
@@ -33,7 +33,11 @@ def cfg3(sweeps=5, fw_iters=200):
     st = s.stats(reset=True)
     per = st["sweep_ms"] / st["sweep_launches"]
     byts = 65536.0 * 65536.0 * 4
-    emit(cfg=3, what="gap_sweep", ms=per, GBps=byts / per / 1e6, entries_per_s=65536.0 ** 2 / per * 1e3)
+    emit(cfg=3, what="gap_sweep", ms=per, GBps=byts / per / 1e6, entries_per_s=65536.0 ** 2 / per * 1e3,
+         slab=os.environ.get("SRO_SLAB", "default"))
+    if not fw:
+        s.close()
+        return
     r = s.solve(sro.SRO_FW, fw_iters, step=sro.STEP_ELS, epsilon=1e-6)
     st = s.stats(reset=True)
     emit(cfg=3, what="fw_els", iters=r["iters_done"], gap=r["gap"], converged=r["converged"], ms=r["device_ms"],
@@ -61,7 +65,8 @@ def batched(cfg, B, epochs=40):
         s.gap()
     st = s.stats(reset=True)
     per = st["sweep_ms"] / st["sweep_launches"]
-    emit(cfg=cfg, what="gap_sweep", ms=per, entries_per_s=d["m"] * d["n"] / per * 1e3)
+    emit(cfg=cfg, what="gap_sweep", ms=per, entries_per_s=d["m"] * d["n"] / per * 1e3,
+         slab=os.environ.get("SRO_SLAB", "default"))
     s.close()
 
 
@@ -70,6 +75,8 @@ if __name__ == "__main__":
     for w in which:
         if w == "3":
             cfg3()
+        elif w == "3s":
+            cfg3(fw=False)
         elif w == "2":
             batched(2, 256)
         elif w == "4":
