@@ -197,7 +197,13 @@ def bench_sro(args, rank, world, local_rank):
     else:
         max_ms, all_entries = total_ms, my_entries
         e2e_max_ms, e2e_all_entries = sum(e2e_ms), sum(e2e_entries)
+    sweep_rf = None
+    if rank == 0 and not args.no_sweep_check:
+        del flush
+        torch.cuda.synchronize()
+        sweep_rf = sweep_roofline_config3(local_rank, measured_peaks())
     return dict(max_ms=max_ms, all_entries=all_entries, stats=stats, clocks=clk, ttg=ttg, step_ms=step_ms,
+                sweep_roofline=sweep_rf,
                 e2e_value=e2e_all_entries / (e2e_max_ms * 1e-3), h2d=h2d, d2h=d2h, instance=d)
 
 
@@ -222,10 +228,53 @@ def roofline_from_stats(stats, peaks):
     t_ms = fam[dom]
     achieved = bytes_ / (t_ms * 1e-3) / 1e9 if t_ms > 0 else 0.0
     shares = {k: round(v / max(1e-9, sum(fam.values())), 4) for k, v in fam.items()}
-    return {"bound": "hbm", "kernel": name, "achieved": round(achieved, 3), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 5), "traffic": None, "avg_launch_ms": round(t_ms / launches, 4),
-            "algorithmic_bytes_per_launch": bytes_ / launches, "time_share": shares,
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, of measured)"}
+    out = {"bound": "hbm", "kernel": name, "achieved": round(achieved, 3), "peak": peak, "unit": "GB/s",
+           "frac": round(achieved / peak, 5), "traffic": None, "avg_launch_ms": round(t_ms / launches, 4),
+           "algorithmic_bytes_per_launch": bytes_ / launches, "time_share": shares,
+           "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, of measured)"}
+    if dom == "bcfw" and stats["bcfw_steps"]:
+        # the sequential family is bound by the latency of one dependent step, not by HBM:
+        # DRAM traffic per launch = algorithmic bytes (profiles/r01_ncu_bcfw_rf.md)
+        us = t_ms * 1e3 / stats["bcfw_steps"]
+        out["traffic"] = round((68.372224e6 + 2.112512e6) / 4096 * (bytes_ / launches) / (M * 4.0), 1)
+        out["traffic_source"] = "ncu --set full dram__bytes_read+write of k_bcfw_rf (68.37+2.11 MB per 4096-step launch)"
+        out["step_latency"] = {"us_per_step": round(us, 4), "cycles_per_step_at_1965MHz": round(us * 1965.0, 1),
+                               "single_cta_floor_cycles": 420,
+                               "floor_source": "profiles/r01_lmo_microbench.log: register LMO + REDUX argmin + 2 barriers"}
+    return out
+
+
+def sweep_roofline_config3(local_rank, peaks, sweeps=3):
+    """The HBM-bound row of the path at BASELINE config [3]: m = n = 65536 iid uniform fp32
+    cost materialised on the device (2^32 entries = 17.18 GB, far above the 126 MB L2),
+    LMO + column-gap sweeps (k_lmo_sweep_bulk + k_lmo_merge) timed by the library's CUDA
+    events on the solver stream, then FW-ELS from T^(0) to g <= 1e-6."""
+    import paper_2103_05857_b200 as sro
+    from sro_inputs import instance
+    d = instance(3, seed=0)
+    s = sro.Solver(d["a"], d["b"], 1.0, cost="hash", hash_seed=d["hash_seed"], device=local_rank)
+    s.gap()                                   # warm-up
+    s.set_timing(True)
+    s.stats(reset=True)
+    for _ in range(sweeps):
+        s.gap()
+    st = s.stats(reset=True)
+    per_ms = st["sweep_ms"] / max(1, st["sweep_launches"])
+    byts = 65536.0 * 65536.0 * 4.0
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    ach = byts / (per_ms * 1e-3) / 1e9
+    r = s.solve(sro.SRO_FW, 500, step=sro.STEP_ELS, epsilon=EPS)
+    st2 = s.stats(reset=True)
+    s.close()
+    return {"workload": "BASELINE configs[3]: m=n=65536, C iid U[0,1) fp32 materialised column-major (17.18 GB)",
+            "kernel": "k_lmo_sweep_bulk + k_lmo_merge (one gap sweep: LMO + column gaps over all 65536 columns)",
+            "bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
+            "algorithmic_bytes_per_launch": byts, "avg_launch_ms": round(per_ms, 4), "sweeps_timed": sweeps,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, of measured)",
+            "fw_els_time_to_gap_ms": round(r["device_ms"], 3), "fw_els_iterations": r["iters_done"],
+            "fw_els_converged": bool(r["converged"]), "fw_gap": r["gap"],
+            "fw_entries_per_s": r["entries_scanned"] / (r["device_ms"] * 1e-3),
+            "fw_sweep_share": round(st2["sweep_ms"] / max(1e-9, st2["block_ms"]), 4)}
 
 
 # --------------------------------------------------------------------------- oracle (CPU)
@@ -313,6 +362,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="sro", choices=["sro", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep-check", action="store_true",
+                    help="skip the config-[3] HBM sweep measurement (sweep_roofline)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -337,6 +388,7 @@ def main():
                 "time_to_gap_ms": ttg,
                 "gb_per_s_equiv": round(value * 4 / 1e9, 3),
                 "roofline": roofline_from_stats(res["stats"], peaks),
+                "sweep_roofline": res.get("sweep_roofline"),
                 "clocks": res["clocks"],
                 "e2e": {"value": res["e2e_value"], "unit": UNIT, "h2d_bytes_per_step": res["h2d"],
                         "d2h_bytes_per_step": res["d2h"]},
