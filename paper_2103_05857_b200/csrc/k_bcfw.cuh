@@ -54,6 +54,7 @@ struct BcfwArgs {
   double cmax;           // max_{k,i} |C_ki| (fp32 LMO filter window)
   int a_smem;            // a staged in shared memory
   int visit_smem;        // the segment's visit list staged in shared memory
+  int dbg;               // timing experiments only (SRO_DBG): 1 = skip the serial part, 2 = skip the LMO
 };
 
 #ifdef SRO_PHASE_TIMING
@@ -249,94 +250,70 @@ struct ColColour {
   }
 };
 
-// ---------------------------------------------------------------------------
-// psum256 over m rows of a vector that is zero except at up to 32 rows, one
-// per lane, rows strictly ascending with the lane (R19). Chunk partials are
-// left-to-right sums from +0.0; entries of one chunk are consecutive lanes,
-// so the partials are a segmented sequential scan costing (longest segment)
-// dependent adds. `slots` is warp-private __shared__ double[256], +0.0 on
-// entry and exit.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ double warp_sparse_psum256_seg(int m, int cnt, int row, double x, double* slots) {
+// psum256 over m rows of a vector that is zero except at up to 32 rows (one per
+// lane, rows ascending with the lane): exactly chunk_tree_sum(x, m, 256) of
+// R19, with shuffles only. Entries of one chunk are consecutive lanes and are
+// summed left to right from +0.0 (a segmented scan, usually of length 1).
+// The 256-leaf adjacent-pair tree restricted to the non-empty chunks is the
+// tree whose internal node between adjacent non-empty chunks c_u < c_{u+1}
+// sits at level hdb(c_u ^ c_{u+1}) (zero leaves are additive identities): every
+// lane holds the value of its current subtree and, level by level (only the
+// levels that occur), the two subtrees separated by a boundary of that level
+// merge as left + right. <= 8 rounds of 2 ballots, 2 shuffles and 1 add.
+__device__ __forceinline__ double warp_sparse_psum256_fast(int m, int cnt, int row, double x) {
   const int lane = threadIdx.x & 31;
   const bool valid = lane < cnt;
-  const int c = valid ? chunk_index(row, m, 256) : -1;
+  const int c = valid ? chunk_index(row, m, 256) : -1 - lane;
   const int cprev = __shfl_up_sync(FULL, c, 1);
   const int cnext = __shfl_down_sync(FULL, c, 1);
   const bool start = valid && (lane == 0 || cprev != c);
   const bool last = valid && (lane == cnt - 1 || cnext != c);
   const unsigned smask = __ballot_sync(FULL, start);
-  const int seg0 = 31 - __clz(smask & (0xffffffffu >> (31 - lane)));
-  const int pos = valid ? lane - seg0 : 0;
-  double acc = valid ? d_add(0.0, x) : 0.0;
-  const int maxpos = (int)__reduce_max_sync(FULL, (unsigned)pos);
-  for (int t = 1; t <= maxpos; t++) {
-    const double prev = __shfl_up_sync(FULL, acc, 1);
-    if (pos == t) acc = d_add(prev, x);
+  const unsigned lmask = __ballot_sync(FULL, last);
+  double v = valid ? d_add(0.0, x) : 0.0;
+  if (smask != lmask) {   // some chunk holds several entries: segmented left-to-right sums
+    const int seg0 = 31 - __clz(smask & (0xffffffffu >> (31 - lane)));
+    const int pos = valid ? lane - seg0 : 0;
+    const int maxpos = (int)__reduce_max_sync(FULL, (unsigned)pos);
+    for (int t = 1; t <= maxpos; t++) {
+      const double prev = __shfl_up_sync(FULL, v, 1);
+      if (pos == t) v = d_add(prev, x);
+    }
+    const unsigned after = lmask & (0xffffffffu << lane);
+    v = __shfl_sync(FULL, v, after ? __ffs(after) - 1 : lane);   // segment total to all its lanes
   }
-  if (last) slots[c] = acc;
-  __syncwarp();
-  double s[8];
+  const int hdb = (last && lane < cnt - 1) ? 31 - __clz((unsigned)(c ^ cnext)) : -1;
+  unsigned levels = __reduce_or_sync(FULL, hdb >= 0 ? (1u << hdb) : 0u);
+  while (levels) {
+    const int b = __ffs(levels) - 1;
+    levels &= levels - 1;
+    const unsigned ge = __ballot_sync(FULL, hdb >= b);
+    const unsigned eq = __ballot_sync(FULL, hdb == b);
+    const unsigned rm = ge & (0xffffffffu << lane);
+    const unsigned lm = lane ? (ge & (0xffffffffu >> (32 - lane))) : 0u;
+    const int rb = rm ? __ffs(rm) - 1 : -1;
+    const int lb = lm ? 31 - __clz(lm) : -1;
+    int u = -1;
+    if (rb >= 0 && ((eq >> rb) & 1u)) u = rb;        // this lane's subtree is the left child
+    else if (lb >= 0 && ((eq >> lb) & 1u)) u = lb;   // ... or the right child
+    const double vl = __shfl_sync(FULL, v, u < 0 ? lane : u);
+    const double vr = __shfl_sync(FULL, v, u < 0 ? lane : u + 1);
+    if (u >= 0 && valid) v = d_add(vl, vr);
+  }
+  return __shfl_sync(FULL, v, 0);
+}
+
+// Sequential left-to-right sum (from +0.0) of the values of lanes 0..cnt-1 with
+// the first 8 operands fetched by independent shuffles. Result in every lane.
+__device__ __forceinline__ double warp_seq_sum_fast(double x, int cnt) {
+  double v[8];
 #pragma unroll
-  for (int t = 0; t < 8; t++) s[t] = slots[8 * lane + t];
-  const double v = warp_pair_tree(tree8(s));
-  __syncwarp();
-  if (last) slots[c] = 0.0;
-  __syncwarp();
-  return v;
-}
-
-// Sequential left-to-right sum (from +0.0) of the values of lanes 0..cnt-1,
-// done by lane 0 from shared memory (independent loads, one dependent add per
-// term). `buf` is warp-private __shared__ double[32]. Result in every lane.
-__device__ __forceinline__ double warp_seq_sum_sm(double x, int cnt, double* buf) {
-  const int lane = threadIdx.x & 31;
-  if (lane < cnt) buf[lane] = x;
-  __syncwarp();
+  for (int q = 0; q < 8; q++) v[q] = __shfl_sync(FULL, x, q);
   double acc = 0.0;
-  if (lane == 0)
-    for (int q = 0; q < cnt; q++) acc = d_add(acc, buf[q]);
-  acc = __shfl_sync(FULL, acc, 0);
-  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < 8; q++) if (q < cnt) acc = d_add(acc, v[q]);
+  for (int q = 8; q < cnt; q++) acc = d_add(acc, __shfl_sync(FULL, x, q));
   return acc;
-}
-
-// psum256 over m rows of a vector that is zero except at up to 32 rows (one per
-// lane, rows ascending with the lane), i.e. exactly chunk_tree_sum(x, m, 256)
-// of R19. Lane 0 forms the chunk partials (left-to-right from +0.0) of the K
-// non-empty chunks, then combines them in the shape of the 256-leaf
-// adjacent-pair tree: zero leaves are additive identities, so the dense tree
-// reduces to merging, K-1 times, the adjacent pair of non-empty subtrees whose
-// lowest common ancestor is lowest (smallest highest-differing chunk bit).
-// bx: warp-private __shared__ double[32]; bc: int[32].
-__device__ __forceinline__ double warp_sparse_psum256_l0(int m, int cnt, int row, double x, double* bx, int* bc) {
-  const int lane = threadIdx.x & 31;
-  if (lane < cnt) { bc[lane] = chunk_index(row, m, 256); bx[lane] = x; }
-  __syncwarp();
-  double res = 0.0;
-  if (lane == 0) {
-    int K = 0;
-    for (int q = 0; q < cnt; q++) {
-      const int c = bc[q];
-      const double v = bx[q];
-      if (K > 0 && bc[K - 1] == c) bx[K - 1] = d_add(bx[K - 1], v);
-      else { bc[K] = c; bx[K] = d_add(0.0, v); K++; }
-    }
-    while (K > 1) {
-      int t = 0, best = 32;
-      for (int u = 0; u + 1 < K; u++) {
-        const int hdb = 31 - __clz(bc[u] ^ bc[u + 1]);
-        if (hdb < best) { best = hdb; t = u; }
-      }
-      bx[t] = d_add(bx[t], bx[t + 1]);
-      for (int u = t + 1; u + 1 < K; u++) { bx[u] = bx[u + 1]; bc[u] = bc[u + 1]; }
-      K--;
-    }
-    res = K ? bx[0] : 0.0;
-  }
-  res = __shfl_sync(FULL, res, 0);
-  __syncwarp();
-  return res;
 }
 
 // Warp argmax of (value, row), lowest row on ties, via REDUX on order keys.
@@ -406,7 +383,9 @@ struct StepOut {
 #define SP_MARK(idx) do { if (threadIdx.x == 0 && sp_ph) { const long long t_ = clock64(); sp_ph->acc[idx] += t_ - sp_ph->t; sp_ph->t = t_; } } while (0)
 #define SP_PARAM , PhaseState* sp_ph
 #define SP_ARG , g_ph
+#define SP_NULL , nullptr
 #else
+#define SP_NULL
 #define SP_MARK(idx) do {} while (0)
 #define SP_PARAM
 #define SP_ARG
@@ -421,10 +400,7 @@ __device__ __forceinline__ StepOut serial_step(const BcfwArgs& A, long long kk, 
   const double lam = A.lambda;
   StepOut o;
   o.dir = 0; o.vrow = -1; o.gamma = 0.0; o.num = 0.0; o.den = 0.0; o.hnew = 0.0;
-  double* bx = slots;
-  int* bc = reinterpret_cast<int*>(slots + 32);
-  double* sb = slots + 64;
-  const double dot = warp_seq_sum_sm(d_mul(tv, gk), c0, sb);
+  const double dot = warp_seq_sum_fast(d_mul(tv, gk), c0);
   o.gfw = d_sub(dot, d_mul(bi, mv));
   SP_MARK(8);
   o.abort = !(mv < 1.0e308 && mv > -1.0e308);
@@ -456,7 +432,7 @@ __device__ __forceinline__ StepOut serial_step(const BcfwArgs& A, long long kk, 
   if (VAR == VAR_PLAIN) {
     const double d = d_sub((mvalid && mrow == j) ? bi : 0.0, mvalid ? mt : 0.0);
     const double D = d_add(0.0, d);
-    o.den = warp_sparse_psum256_l0(m, M, mrow, d_mul(D, D), bx, bc);
+    o.den = warp_sparse_psum256_fast(m, M, mrow, d_mul(D, D));
     SP_MARK(10);
     o.num = d_mul(lam, d_add(0.0, o.gfw));
     if (A.step_rule == 1) {
@@ -474,7 +450,7 @@ __device__ __forceinline__ StepOut serial_step(const BcfwArgs& A, long long kk, 
     const bool use_fw = (c0 == 1) || (o.gfw >= gaw);
     if (use_fw) {
       const double d = d_sub((mvalid && mrow == j) ? bi : 0.0, mvalid ? mt : 0.0);
-      o.den = warp_sparse_psum256_l0(m, M, mrow, d_mul(d, d), bx, bc);
+      o.den = warp_sparse_psum256_fast(m, M, mrow, d_mul(d, d));
       o.num = d_mul(lam, d_add(o.gfw, 0.0));
       if (!(o.num > 0.0) || o.den == 0.0) o.gamma = 0.0;
       else { o.gamma = d_div(o.num, o.den); if (o.gamma > 1.0) o.gamma = 1.0; }
@@ -486,7 +462,7 @@ __device__ __forceinline__ StepOut serial_step(const BcfwArgs& A, long long kk, 
       use_merged = false;
       const double tvv = __shfl_sync(FULL, tv, __ffs(__ballot_sync(FULL, lane < c0 && rw == vrow)) - 1);
       const double d = (lane < c0) ? ((rw == vrow) ? d_sub(tv, bi) : tv) : 0.0;
-      o.den = warp_sparse_psum256_l0(m, c0, rw, d_mul(d, d), bx, bc);
+      o.den = warp_sparse_psum256_fast(m, c0, rw, d_mul(d, d));
       o.num = d_mul(lam, d_add(gaw, 0.0));
       const double alpha = d_div(tvv, bi);
       const double gmax = d_div(alpha, d_sub(1.0, alpha));
@@ -536,7 +512,7 @@ __device__ __forceinline__ StepOut serial_step(const BcfwArgs& A, long long kk, 
     if (ev) {
       const double Dp = d_add(0.0, d_sub(tnew, eold));
       const double rn = d_add(r[erow], Dp);
-      const double hn = d_div(d_sub(rn, aval), lam);
+      const double hn = lam == 1.0 ? d_sub(rn, aval) : d_div(d_sub(rn, aval), lam);   // x / 1 == x exactly
       r[erow] = rn;
       h[erow] = hn;
       o.hnew = hn;

@@ -27,6 +27,7 @@
 
 #include "../../include/sro.h"
 #include "k_bcfw.cuh"
+#include "k_bcfw_pipe.cuh"
 #include "k_block.cuh"
 #include "k_sweep.cuh"
 #include "sro_device.cuh"
@@ -134,6 +135,8 @@ struct Solver {
   double cmax = -1.0;           // max cost, computed once (ensure_cmax)
   bool no_rf = getenv("SRO_NO_RF") != nullptr;      // debug: force the shared-memory kernel
   bool no_tail = getenv("SRO_NO_TAIL") != nullptr;  // debug: force the multi-kernel block step
+  // pipelined BCFW kernel (k_bcfw_pipe.cuh): opt-in while it is slower than k_bcfw_rf (SRO_PIPE=1)
+  bool no_pipe = getenv("SRO_PIPE") == nullptr || getenv("SRO_NO_RF") != nullptr;
   sro_stats stats{};
   bool timing = false;
   struct Pending { cudaEvent_t a, b; int cat; int64_t units; };
@@ -697,8 +700,55 @@ sro_status bcfw_try_rf(Solver* s, BcfwArgs& A) {
   return launch_rf<double, 4, VAR, GA>(s, A, bytes);
 }
 
+template <typename T, int MAXV, int VAR>
+sro_status launch_pipe(Solver* s, BcfwArgs& A, size_t smem) {
+  auto kern = k_bcfw_pipe<T, MAXV, VAR>;
+  CUDA_TRY(s, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int tr = timed_begin(s);
+  kern<<<1, PIPE_THREADS, smem, s->stream>>>(A, (const T*)s->C, s->ld);
+  CUDA_TRY(s, cudaGetLastError());
+  timed_end(s, tr, CAT_BCFW, A.steps);
+  s->lead->stats.kernel_launches += 1;
+  s->lead->stats.bcfw_launches += 1;
+  s->lead->stats.bcfw_steps += A.steps;
+  return SRO_OK;
+}
+
+// Pipelined kernel (k_bcfw_pipe.cuh) for dense costs and U / P / explicit
+// visits when the rows fit in the registers of 480 threads (<= 4 vectors each).
+// Returns SRO_ERR_DIMENSION (not an error to the caller) when it does not apply.
+template <int VAR>
+sro_status bcfw_try_pipe(Solver* s, BcfwArgs& A) {
+  const bool dense = s->kind == SRO_COST_DENSE || s->kind == SRO_COST_HASH_UNIFORM;
+  if (!dense || s->no_pipe) return SRO_ERR_DIMENSION;
+  const int W = s->prec == SRO_FP32 ? 4 : 2;
+  const int nvec = s->m / W;
+  const int need = (nvec + PIPE_LMO - 1) / PIPE_LMO;
+  if (need > 4 || s->m - nvec * W > PIPE_LMO) return SRO_ERR_DIMENSION;
+  const size_t limit = 226 * 1024;
+  A.visit_smem = PipeLayout::bytes(s->m, s->n, A.steps, true) <= limit;
+  A.ga_smem = 0;
+  A.a_smem = 1;
+  const size_t bytes = PipeLayout::bytes(s->m, s->n, A.steps, A.visit_smem);
+  if (bytes > limit) return SRO_ERR_DIMENSION;
+  if (s->prec == SRO_FP32) {
+    if (need <= 1) return launch_pipe<float, 1, VAR>(s, A, bytes);
+    if (need <= 2) return launch_pipe<float, 2, VAR>(s, A, bytes);
+    if (need <= 3) return launch_pipe<float, 3, VAR>(s, A, bytes);
+    return launch_pipe<float, 4, VAR>(s, A, bytes);
+  }
+  if (need <= 1) return launch_pipe<double, 1, VAR>(s, A, bytes);
+  if (need <= 2) return launch_pipe<double, 2, VAR>(s, A, bytes);
+  if (need <= 3) return launch_pipe<double, 3, VAR>(s, A, bytes);
+  return launch_pipe<double, 4, VAR>(s, A, bytes);
+}
+
 template <int VAR, bool GA>
 sro_status bcfw_run(Solver* s, BcfwArgs& A) {
+  if (!GA) {
+    sro_status st = bcfw_try_pipe<VAR>(s, A);
+    if (st != SRO_ERR_DIMENSION) return st;
+  }
   if (!s->no_rf) {
     sro_status st = bcfw_try_rf<VAR, GA>(s, A);
     if (st != SRO_ERR_DIMENSION) return st;
@@ -715,6 +765,7 @@ sro_status bcfw_segment(Solver* s, int variant, const sro_options* o, int steps,
   A.G = s->G_ga; A.fen = s->fen; A.ga_inner = o->ga_inner; A.ga_post = o->ga_post_update; A.seed = s->seed;
   A.status = s->status; A.steps_done = s->steps_done; A.trace = dtrace;
   A.phase = s->phase;
+  A.dbg = getenv("SRO_DBG") ? atoi(getenv("SRO_DBG")) : 0;
   const bool ga = o->sampling == SRO_SAMPLE_GA;
   { sro_status st = ensure_cmax(s); if (st) return st; }
   A.cmax = s->cmax;
