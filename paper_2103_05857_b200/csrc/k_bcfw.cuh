@@ -263,7 +263,11 @@ struct ColColour {
 __device__ __forceinline__ double warp_sparse_psum256_fast(int m, int cnt, int row, double x) {
   const int lane = threadIdx.x & 31;
   const bool valid = lane < cnt;
-  const int c = valid ? chunk_index(row, m, 256) : -1 - lane;
+  // chunk of a row: floor((256 (row + 1) - 1) / m) (R19); for m = 256 * 2^s that is row >> s
+  const int dm = m >> 8;
+  int c;
+  if ((m & 255) == 0 && (dm & (dm - 1)) == 0) c = valid ? (row >> (__ffs(dm) - 1)) : -1 - lane;
+  else c = valid ? chunk_index(row, m, 256) : -1 - lane;
   const int cprev = __shfl_up_sync(FULL, c, 1);
   const int cnext = __shfl_down_sync(FULL, c, 1);
   const bool start = valid && (lane == 0 || cprev != c);
@@ -400,8 +404,27 @@ __device__ __forceinline__ StepOut serial_step(const BcfwArgs& A, long long kk, 
   const double lam = A.lambda;
   StepOut o;
   o.dir = 0; o.vrow = -1; o.gamma = 0.0; o.num = 0.0; o.den = 0.0; o.hnew = 0.0;
-  const double dot = warp_seq_sum_fast(d_mul(tv, gk), c0);
-  o.gfw = d_sub(dot, d_mul(bi, mv));
+  // <t_i, grad_i f>: operands fetched now, summed (rows ascending) once the
+  // independent merged-support / denominator work below has been issued
+  const double prod = d_mul(tv, gk);
+  double dv[8];
+#pragma unroll
+  for (int q = 0; q < 8; q++) dv[q] = __shfl_sync(FULL, prod, q);
+  auto finish_dot = [&]() {
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      if (q >= c0) break;
+      acc = d_add(acc, dv[q]);
+    }
+    for (int q = 8; q < c0; q++) acc = d_add(acc, __shfl_sync(FULL, prod, q));
+    return acc;
+  };
+  double dot = 0.0;
+  if (VAR != VAR_PLAIN) {
+    dot = finish_dot();
+    o.gfw = d_sub(dot, d_mul(bi, mv));
+  }
   SP_MARK(8);
   o.abort = !(mv < 1.0e308 && mv > -1.0e308);
   double gv = dninf();
@@ -433,6 +456,8 @@ __device__ __forceinline__ StepOut serial_step(const BcfwArgs& A, long long kk, 
     const double d = d_sub((mvalid && mrow == j) ? bi : 0.0, mvalid ? mt : 0.0);
     const double D = d_add(0.0, d);
     o.den = warp_sparse_psum256_fast(m, M, mrow, d_mul(D, D));
+    dot = finish_dot();
+    o.gfw = d_sub(dot, d_mul(bi, mv));
     SP_MARK(10);
     o.num = d_mul(lam, d_add(0.0, o.gfw));
     if (A.step_rule == 1) {

@@ -1,36 +1,50 @@
-// k_bcfw_pipe.cuh — pipelined persistent loop for the sequential BCFW family
-// (BCFW Alg. 1, BCAFW Alg. A.2, BCPFW Alg. A.3; U / P / explicit visits; DEC or
-// ELS) on dense costs: the LMO of the NEXT visited column runs concurrently
-// with the serial update of the current one.
+// k_bcfw_pipe.cuh — pipelined, warp-specialised persistent loop for the
+// sequential BCFW family (BCFW Alg. 1, BCAFW Alg. A.2, BCPFW Alg. A.3; U / P /
+// explicit visits; DEC or ELS) on dense costs: the LMO of the NEXT visited
+// column runs concurrently with the serial update of the current one.
 //
 // Why this is exact. Step s (column i_s) changes h only on its merged support
 // T_s = supp(t_{i_s}) U {j_s} (r moves on those rows only). So the
 // LMO of column i_{s+1} (Eq. 9) can be split:
-//   * warps 1..15 scan every row NOT in T_s against h before step s — the same
-//     values as after it — while warp 0 runs the serial part of step s;
-//   * after the barrier warp 0 evaluates the <= 32 rows of T_s exactly with
-//     the updated h (C_{k,i_{s+1}} prefetched during step s) and merges them with
-//     the 15 warp partials. min / argmin with the lowest-row tie-break is
-//     order-free, so j_{s+1} and its value are exactly those of a full scan.
-// Per step: max(serial part, masked LMO) + merge + 2 barriers, instead of
-// LMO + reductions + serial part + 2 barriers.
+//   * the LMO warps scan every row NOT in T_s against h before step s — the
+//     same values as after it — while warp 0 runs the serial part of step s;
+//   * then warp 0 evaluates the <= 32 rows of T_s exactly with the updated h
+//     (C_{k,i_{s+1}} prefetched during step s) and merges them with the warp
+//     partials. min / argmin with the lowest-row tie-break is order-free, so
+//     j_{s+1} and its value are exactly those of a full scan.
 //
-// Roles: warp 0 = serial part (serial_step of k_bcfw.cuh, the same arithmetic
-// as every other BCFW kernel) and the final merge; warps 1..15 (480 threads)
-// own the rows: thread lt owns the 128-bit vectors q = lt + u*480 (u < MAXV)
-// and tail row nvec*W + lt, prefetches its part of the column two visits ahead
-// into registers and reads h from a planar shared-memory copy (plane p holds
-// the pairs (h[Wq+2p], h[Wq+2p+1]) at index q: conflict-free 128-bit loads)
-// that warp 0 keeps current; the rows warp 0 writes during step s are exactly
-// the masked rows, so the concurrent reads never depend on them. Masks travel
-// as one bit word per owner thread.
+// Roles (16 warps launched; warp w runs on SM sub-partition w % 4):
+//   * warp 0: serial part (serial_step of k_bcfw.cuh — the same arithmetic as
+//     every other BCFW kernel), the merge, and publishing the next mask. Warps
+//     4, 8, 12 stay idle so warp 0 has its sub-partition to itself.
+//   * the 12 warps with w % 4 != 0 (384 threads): LMO. Thread lt owns the
+//     128-bit vectors q = lt + u*384 (u < MAXV) and tail row nvec*W + lt,
+//     prefetches its part of the column one visit ahead into registers and
+//     reads h from a planar shared-memory copy (plane p holds the pairs
+//     (h[Wq+2p], h[Wq+2p+1]) at index q: conflict-free 128-bit loads) that warp 0
+//     keeps current; the rows warp 0 writes during step s are exactly the masked
+//     rows, so the concurrent reads never depend on them. Masks travel as one
+//     bit word per owner thread.
+// Warp 0 and the LMO warps run separate loops and hand off through two named
+// barriers: BAR_PART (LMO partials ready: LMO warps arrive, warp 0 waits) and
+// BAR_MASK (next mask published: warp 0 arrives, LMO warps wait).
 #pragma once
 #include "k_bcfw.cuh"
 
 namespace sro {
 
 constexpr int PIPE_THREADS = 512;
-constexpr int PIPE_LMO = PIPE_THREADS - 32;
+constexpr int PIPE_LMO_WARPS = 12;
+constexpr int PIPE_LMO = PIPE_LMO_WARPS * 32;
+constexpr int PIPE_SYNC = PIPE_LMO + 32;   // threads taking part in the named barriers
+constexpr int BAR_PART = 1, BAR_MASK = 2;
+
+__device__ __forceinline__ void nbar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void nbar_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
 
 template <typename T, int MAXV>
 struct PipeCol {
@@ -92,8 +106,8 @@ __device__ __forceinline__ void vproc_mask(const double2& v, const double* hd, i
 
 struct PipeLayout {
   __host__ __device__ static size_t fixed() {
-    return 256 * 8 + 16 * 8 + 16 * 4 + 16 * 4 + 8 * 8      // slots, wkey, wj, misc, miscd
-           + PIPE_THREADS * 4;                               // mask words
+    return 256 * 8 + 16 * 8 + 16 * 4 + 16 * 4 + 8 * 8      // slots, wkey, wj, misc, (spare)
+           + PIPE_LMO * 4;                                   // mask words
   }
   __host__ __device__ static size_t bytes(int m, int n, int steps, bool visit_smem) {
     size_t b = fixed() + 4 * rup16((size_t)m * 8) + rup16((size_t)n * 4);
@@ -102,47 +116,45 @@ struct PipeLayout {
   }
 };
 
-// owner thread and bit of row k (rows of full vectors, then the tail rows)
+// LMO thread index and bit of row k (rows of full vectors, then the tail rows)
 template <int W>
-__device__ __forceinline__ void pipe_owner(int k, int nvec, int& tid, unsigned& bit) {
+__device__ __forceinline__ void pipe_owner(int k, int nvec, int& lt, unsigned& bit) {
   if (k < nvec * W) {
     const int q = k / W;
-    tid = 32 + q % PIPE_LMO;
+    lt = q % PIPE_LMO;
     bit = 1u << ((q / PIPE_LMO) * W + (k % W));
   } else {
-    tid = 32 + (k - nvec * W);
+    lt = k - nvec * W;
     bit = 1u << 31;
   }
 }
 
 #ifdef SRO_PHASE_TIMING
-#define PP_MARK(idx)                                          \
-  do {                                                        \
-    if (threadIdx.x == 0 || threadIdx.x == 32) {              \
-      const long long t_ = clock64();                         \
-      pp_acc[idx] += t_ - pp_t;                               \
-      pp_t = t_;                                              \
-    }                                                         \
+#define PW_MARK(idx)                          \
+  do {                                        \
+    const long long t_ = clock64();           \
+    pw_acc[idx] += t_ - pw_t;                 \
+    pw_t = t_;                                \
   } while (0)
 #else
-#define PP_MARK(idx) do {} while (0)
+#define PW_MARK(idx) do {} while (0)
 #endif
 
 template <typename T, int MAXV, int VAR>
 __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_pipe(BcfwArgs A, const T* __restrict__ Cg, int64_t ld) {
-  using Col = PipeCol<T, MAXV>;
-  constexpr int W = Col::W;
+  constexpr int W = Vec<T>::W;
   extern __shared__ __align__(16) char smraw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int lt = tid - 32;
   const int m = A.m, n = A.n, cap = A.cap;
+  const int nvec = m / W;
+  const int steps = A.steps;
   char* p = smraw;
   double* slots = reinterpret_cast<double*>(p); p += 256 * 8;
   unsigned long long* wkey = reinterpret_cast<unsigned long long*>(p); p += 16 * 8;
   int* wj = reinterpret_cast<int*>(p); p += 16 * 4;
-  int* misc = reinterpret_cast<int*>(p); p += 16 * 4;        // [2] = abort
+  volatile int* misc = reinterpret_cast<volatile int*>(p); p += 16 * 4;   // [2] = abort
   p += 8 * 8;
-  unsigned* mflag = reinterpret_cast<unsigned*>(p); p += PIPE_THREADS * 4;
+  unsigned* mflag = reinterpret_cast<unsigned*>(p); p += PIPE_LMO * 4;
   double* sh_h = reinterpret_cast<double*>(p); p += rup16((size_t)m * 8);
   double* sh_r = reinterpret_cast<double*>(p); p += rup16((size_t)m * 8);
   double* sh_a = reinterpret_cast<double*>(p); p += rup16((size_t)m * 8);
@@ -151,215 +163,194 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_pipe(BcfwArgs A, const
   int* sh_cnt = reinterpret_cast<int*>(p); p += rup16((size_t)n * 4);
   const int* vis = A.visit;
   if (A.visit_smem) {
-    int* sv = reinterpret_cast<int*>(p); p += rup16((size_t)A.steps * 4);
-    for (int q = tid; q < A.steps; q += PIPE_THREADS) sv[q] = A.visit[q];
+    int* sv = reinterpret_cast<int*>(p); p += rup16((size_t)steps * 4);
+    for (int q = tid; q < steps; q += PIPE_THREADS) sv[q] = A.visit[q];
     vis = sv;
   }
   for (int c = tid; c < 256; c += PIPE_THREADS) slots[c] = 0.0;
   for (int k = tid; k < m; k += PIPE_THREADS) {
     const double hk = A.h[k];
     sh_h[k] = hk; sh_r[k] = A.r[k]; sh_a[k] = A.a[k];
-    if (k < (m / W) * W) hpd[pipe_hidx<W>(k, m / W)] = hk;
+    if (k < nvec * W) hpd[pipe_hidx<W>(k, nvec)] = hk;
   }
   for (int c = tid; c < n; c += PIPE_THREADS) sh_cnt[c] = A.cnt[c];
-  mflag[tid] = 0;
+  for (int c = tid; c < PIPE_LMO; c += PIPE_THREADS) mflag[c] = 0;
   if (tid == 0) misc[2] = 0;
   if (tid < 16) { wkey[tid] = ~0ULL; wj[tid] = 0x7fffffff; }
-  const int steps = A.steps;
-  Col col;
-  col.C = Cg; col.ld = ld; col.m = m; col.nvec = m / W;
-  const int nvec = col.nvec;
-  const int kt = nvec * W + lt;
-  if (warp > 0 && steps > 0) col.fetch(A.visit[0], lt);
   __syncthreads();
-  if (steps == 0) {
-    if (tid == 0) *A.steps_done = 0;
-    return;
-  }
 
-  // ---- prologue: full LMO of the first visited column
-  if (warp > 0) {
-    col.advance();
-    if (steps > 1) col.fetch(vis[1], lt);
-    double best = dinf();
-    int bj = 0x7fffffff;
+  if (steps > 0 && warp > 0 && (warp & 3) != 0) {
+    // =================== LMO warps ===================
+    const int lw = warp - 1 - (warp >> 2);   // 0..11
+    const int lt = lw * 32 + lane;
+    const int kt = nvec * W + lt;
+    PipeCol<T, MAXV> col;
+    col.C = Cg; col.ld = ld; col.m = m; col.nvec = nvec;
+    col.fetch(vis[0], lt);
+    for (int t = 0; t < steps; t++) {
+      col.advance();
+      if (t + 1 < steps) col.fetch(vis[t + 1], lt);   // lands during the next step
+      nbar_sync(BAR_MASK, PIPE_SYNC);                  // mask T_{t-1} published (empty for t = 0)
+      if (misc[2]) break;
+      const unsigned mk = mflag[lt];
+      mflag[lt] = 0;
+      double hv[MAXV][W];
 #pragma unroll
-    for (int u = 0; u < MAXV; u++) {
-      const int q = lt + u * PIPE_LMO;
-      if (q < nvec) {
-        double hv[W];
-        pipe_h(hp, nvec, q, col.cur, hv);
-        vproc(col.cur[u], hv, W * q, best, bj);
+      for (int u = 0; u < MAXV; u++) {
+        const int q = lt + u * PIPE_LMO;
+        if (q < nvec) pipe_h(hp, nvec, q, col.cur, hv[u]);
       }
+      const double ht = kt < m ? sh_h[kt] : 0.0;
+      double best = dinf();
+      int bj = 0x7fffffff;
+      if (mk == 0u) {
+#pragma unroll
+        for (int u = 0; u < MAXV; u++) {
+          const int q = lt + u * PIPE_LMO;
+          if (q < nvec) vproc(col.cur[u], hv[u], W * q, best, bj);
+        }
+        if (kt < m) {
+          const double x = d_add((double)col.ctail, ht);
+          if (x < best) { best = x; bj = kt; }
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < MAXV; u++) {
+          const int q = lt + u * PIPE_LMO;
+          if (q < nvec) vproc_mask(col.cur[u], hv[u], W * q, (mk >> (u * W)) & ((1u << W) - 1u), best, bj);
+        }
+        if (kt < m && !(mk >> 31)) {
+          const double x = d_add((double)col.ctail, ht);
+          if (x < best) { best = x; bj = kt; }
+        }
+      }
+      unsigned long long key = okey(best);
+      warp_argmin_redux(key, bj);
+      if (lane == 0) { wkey[lw] = key; wj[lw] = bj; }
+      nbar_arrive(BAR_PART, PIPE_SYNC);
     }
-    if (kt < m) {
-      const double x = d_add((double)col.ctail, sh_h[kt]);
-      if (x < best) { best = x; bj = kt; }
-    }
-    unsigned long long key = okey(best);
-    warp_argmin_redux(key, bj);
-    if (lane == 0) { wkey[warp] = key; wj[warp] = bj; }
-  }
-  // warp 0 state: the visited column's slab, its LMO result, the mask rows T_s
-  int i = vis[0];
-  int rw = 0x7fffffff, c0 = 0;
-  double tv = 0.0, bi = 0.0, cw = 0.0;
-  int j = 0;
-  double mv = 0.0;
-  int trow = 0x7fffffff, MT = 0;
-  // the next visited column's slab (loaded a step ahead; C at its rows a step
-  // later), and the slab after it — so no dependent global load is on the
-  // critical path of a step
-  int i1 = steps > 1 ? vis[1] : i, c01 = 0, rw1 = 0x7fffffff;
-  double tv1 = 0.0, bi1 = 0.0;
-  int iprev = -1;
-  if (warp == 0) {
+  } else if (steps > 0 && warp == 0) {
+    // =================== serial warp ===================
+    int i = vis[0];
+    int rw = 0x7fffffff, c0 = 0;
+    double tv = 0.0, bi = 0.0, cw = 0.0;
     c0 = sh_cnt[i];
     bi = A.b[i];
     if (lane < c0) { rw = A.srow[(int64_t)i * cap + lane]; tv = A.sval[(int64_t)i * cap + lane]; }
     if (lane < c0) cw = (double)__ldg(Cg + (int64_t)i * ld + rw);
+    // the next visited column's slab (loaded a step ahead, C at its rows a step
+    // later) and the slab after it: no dependent global load on a step's critical path
+    int i1 = steps > 1 ? vis[1] : i, c01 = 0, rw1 = 0x7fffffff;
+    double tv1 = 0.0, bi1 = 0.0;
     if (steps > 1) {
       c01 = sh_cnt[i1];
       bi1 = A.b[i1];
       if (lane < c01) { rw1 = A.srow[(int64_t)i1 * cap + lane]; tv1 = A.sval[(int64_t)i1 * cap + lane]; }
     }
-  }
-  __syncthreads();
-  // merged support of (slab, j) -> this lane's mask row; set the owners' mask bits
-  auto publish_mask = [&]() {
-    const bool j_in = __ballot_sync(FULL, lane < c0 && rw == j) != 0u;
-    const int ins = __popc(__ballot_sync(FULL, lane < c0 && rw < j));
-    MT = c0 + (j_in ? 0 : 1);
-    int src = (j_in || lane < ins) ? lane : lane - 1;
-    if (src < 0) src = 0;
-    trow = __shfl_sync(FULL, rw, src);
-    if (!j_in && lane == ins) trow = j;
-    if (lane >= MT) trow = 0x7fffffff;
-    if (lane < MT) {
-      int ot;
-      unsigned bit;
-      pipe_owner<W>(trow, nvec, ot, bit);
-      atomicOr(&mflag[ot], bit);
-    }
-  };
-  if (warp == 0) {
-    unsigned long long k2 = (lane >= 1 && lane < 16) ? wkey[lane] : ~0ULL;
-    int j2 = (lane >= 1 && lane < 16) ? wj[lane] : 0x7fffffff;
-    warp_argmin_redux(k2, j2);
-    j = j2;
-    mv = okey_inv(k2);
-    publish_mask();
-  }
-  __syncthreads();
-
-  int done = 0;
-#ifdef SRO_PHASE_TIMING
-  long long pp_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long pp_t = clock64();
-#endif
-  for (int s = 0; s < steps; s++) {
-    const long long kk = A.k0 + s;
-    const bool has_next = s + 1 < steps;
-    const int inext = has_next ? vis[s + 1] : i;
-    StepOut o;
-    double cn = 0.0;
-    int c0n = 0, rwn = 0x7fffffff;
-    double tvn = 0.0, bin = 0.0, cwn = 0.0;
-    if (warp > 0) {
-      PP_MARK(0);
-      // ---- masked LMO of the next visited column (rows of T_s skipped)
-      if (has_next && !(A.dbg & 2)) {
-        col.advance();
-        if (s + 2 < steps) col.fetch(vis[s + 2], lt);
-        const unsigned mk = mflag[tid];
-        mflag[tid] = 0;
-        double best = dinf();
-        int bj = 0x7fffffff;
-        double hv[MAXV][W];
-#pragma unroll
-        for (int u = 0; u < MAXV; u++) {
-          const int q = lt + u * PIPE_LMO;
-          if (q < nvec) pipe_h(hp, nvec, q, col.cur, hv[u]);
-        }
-        const double ht = kt < m ? sh_h[kt] : 0.0;
-        if (mk == 0u) {
-#pragma unroll
-          for (int u = 0; u < MAXV; u++) {
-            const int q = lt + u * PIPE_LMO;
-            if (q < nvec) vproc(col.cur[u], hv[u], W * q, best, bj);
-          }
-          if (kt < m) {
-            const double x = d_add((double)col.ctail, ht);
-            if (x < best) { best = x; bj = kt; }
-          }
-        } else {
-#pragma unroll
-          for (int u = 0; u < MAXV; u++) {
-            const int q = lt + u * PIPE_LMO;
-            if (q < nvec) vproc_mask(col.cur[u], hv[u], W * q, (mk >> (u * W)) & ((1u << W) - 1u), best, bj);
-          }
-          if (kt < m && !(mk >> 31)) {
-            const double x = d_add((double)col.ctail, ht);
-            if (x < best) { best = x; bj = kt; }
-          }
-        }
-        PP_MARK(1);
-        unsigned long long key = okey(best);
-        warp_argmin_redux(key, bj);
-        if (lane == 0) { wkey[warp] = key; wj[warp] = bj; }
-        PP_MARK(2);
+    int iprev = -1;
+    int j = 0, trow = 0x7fffffff, MT = 0;
+    double mv = 0.0;
+    // merged support of (slab, j) -> this lane's mask row; set the owners' mask bits
+    auto publish_mask = [&]() {
+      const bool j_in = __ballot_sync(FULL, lane < c0 && rw == j) != 0u;
+      const int ins = __popc(__ballot_sync(FULL, lane < c0 && rw < j));
+      MT = c0 + (j_in ? 0 : 1);
+      int src = (j_in || lane < ins) ? lane : lane - 1;
+      if (src < 0) src = 0;
+      trow = __shfl_sync(FULL, rw, src);
+      if (!j_in && lane == ins) trow = j;
+      if (lane >= MT) trow = 0x7fffffff;
+      if (lane < MT) {
+        int ot;
+        unsigned bit;
+        pipe_owner<W>(trow, nvec, ot, bit);
+        atomicOr(&mflag[ot], bit);
       }
-    } else {
-      // ---- warp 0: prefetch what the merge and the next steps need, then the serial part of step s
-      if (has_next && !(A.dbg & 4)) {
+    };
+    // prologue: the full LMO of the first column
+    nbar_arrive(BAR_MASK, PIPE_SYNC);
+    nbar_sync(BAR_PART, PIPE_SYNC);
+    {
+      unsigned long long k2 = lane < PIPE_LMO_WARPS ? wkey[lane] : ~0ULL;
+      int j2 = lane < PIPE_LMO_WARPS ? wj[lane] : 0x7fffffff;
+      warp_argmin_redux(k2, j2);
+      j = j2;
+      mv = okey_inv(k2);
+    }
+    publish_mask();
+    __syncwarp();
+    if (steps > 1) nbar_arrive(BAR_MASK, PIPE_SYNC);
+    int done = 0;
+    int inext = steps > 1 ? vis[1] : i;   // the next visited column (carried in a register)
+#ifdef SRO_PHASE_TIMING
+    long long pw_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long pw_t = clock64();
+    PhaseState sp_state;
+    for (int q = 0; q < 16; q++) sp_state.acc[q] = 0;
+#endif
+    for (int s = 0; s < steps; s++) {
+      const long long kk = A.k0 + s;
+      const bool has_next = s + 1 < steps;
+      const int i2 = s + 2 < steps ? vis[s + 2] : inext;
+      // ---- prefetch what the merge and the next steps need
+      double cn = 0.0, cwn = 0.0, tvn = 0.0, bin = 0.0;
+      int c0n = 0, rwn = 0x7fffffff;
+      if (has_next) {
         if (lane < MT) cn = (double)__ldg(Cg + (int64_t)inext * ld + trow);
         if (lane < c01) cwn = (double)__ldg(Cg + (int64_t)inext * ld + rw1);
       }
-      if (s + 2 < steps && !(A.dbg & 4)) {
-        const int i2 = vis[s + 2];
+      PW_MARK(7);
+      if (s + 2 < steps) {
         c0n = sh_cnt[i2];
         bin = A.b[i2];
         if (lane < c0n) { rwn = A.srow[(int64_t)i2 * cap + lane]; tvn = A.sval[(int64_t)i2 * cap + lane]; }
       }
+      // ---- the serial part of step s
+      PW_MARK(0);
       const double gk = lane < c0 ? d_add(cw, sh_h[rw]) : 0.0;
-      PP_MARK(0);
-      if (A.dbg & 1) { o = StepOut{}; o.nk = c0; o.kmask = __ballot_sync(FULL, lane < c0); o.erow = rw; o.tnew = tv; if (gk == 12345.0) o.abort = true; }
-      else o = serial_step<VAR>(A, kk, i, j, mv, bi, c0, rw, tv, gk, sh_r, sh_h, nullptr, sh_a, sh_cnt, slots, nullptr SP_NULL);
-      PP_MARK(1);
+      PW_MARK(1);
+#ifdef SRO_PHASE_TIMING
+      sp_state.t = clock64();
+      const StepOut o =
+          serial_step<VAR>(A, kk, i, j, mv, bi, c0, rw, tv, gk, sh_r, sh_h, nullptr, sh_a, sh_cnt, slots, nullptr, &sp_state);
+#else
+      const StepOut o =
+          serial_step<VAR>(A, kk, i, j, mv, bi, c0, rw, tv, gk, sh_r, sh_h, nullptr, sh_a, sh_cnt, slots, nullptr);
+#endif
+      PW_MARK(2);
       if (o.ev && o.erow < nvec * W) hpd[pipe_hidx<W>(o.erow, nvec)] = o.hnew;   // planar copy for the LMO warps
-      if (lane == 0) {
-        if (o.abort) {
+      if (o.abort) {
+        if (lane == 0) {
           misc[2] = 1;
           set_status(A.status, !(mv < 1.0e308 && mv > -1.0e308) ? 5 : 6);
-        } else if (A.trace) {
-          double* tr = A.trace + 9 * (int64_t)s;
-          tr[0] = (double)kk; tr[1] = i; tr[2] = j; tr[3] = (VAR == VAR_PLAIN) ? -1 : o.vrow;
-          tr[4] = o.dir; tr[5] = o.gamma; tr[6] = o.num; tr[7] = o.den; tr[8] = mv;
         }
+        __syncwarp();
+        if (has_next) nbar_arrive(BAR_MASK, PIPE_SYNC);   // release the LMO warps (they see the abort)
+        break;
       }
-      PP_MARK(2);
-    }
-    __syncthreads();
-    PP_MARK(3);
-    if (misc[2]) break;
-    done = s + 1;
-    if (!has_next) break;
-    if (warp == 0 && !(A.dbg & 8)) {
-      // ---- merge: the rows of T_s with the updated h, and the 15 warp partials
+      if (A.trace && lane == 0) {
+        double* tr = A.trace + 9 * (int64_t)s;
+        tr[0] = (double)kk; tr[1] = i; tr[2] = j; tr[3] = (VAR == VAR_PLAIN) ? -1 : o.vrow;
+        tr[4] = o.dir; tr[5] = o.gamma; tr[6] = o.num; tr[7] = o.den; tr[8] = mv;
+      }
+      done = s + 1;
+      if (!has_next) break;
+      // ---- merge: the rows of T_s with the updated h, and the LMO warp partials
+      PW_MARK(3);
+      nbar_sync(BAR_PART, PIPE_SYNC);
       unsigned long long ka = ~0ULL;
       int ja = 0x7fffffff;
       if (lane < MT) { ka = okey(d_add(cn, sh_h[trow])); ja = trow; }
-      if (lane >= 1 && lane < 16) {
+      if (lane < PIPE_LMO_WARPS) {
         const unsigned long long kb = wkey[lane];
         const int jb = wj[lane];
         if (kb < ka || (kb == ka && jb < ja)) { ka = kb; ja = jb; }
       }
       warp_argmin_redux(ka, ja);
-      PP_MARK(4);
-      // the next column's slab: its own updated slab when the same column is
+      PW_MARK(4);
+      // ---- the next column's slab: its own updated slab when the same column is
       // visited again; reloaded when the prefetch may predate an update of it
       // (it was read before step s-1 ran); else the prefetched one
-      __syncwarp();
       if (inext == i) {
         new_slab_entry(o, rw, tv);
         c0 = o.nk;
@@ -376,21 +367,26 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_pipe(BcfwArgs A, const
       c01 = c0n; bi1 = bin; rw1 = rwn; tv1 = tvn;
       iprev = i;
       i = inext;
+      inext = i2;
       j = ja;
       mv = okey_inv(ka);
+      PW_MARK(5);
       publish_mask();
-      PP_MARK(5);
+      __syncwarp();
+      nbar_arrive(BAR_MASK, PIPE_SYNC);
+      PW_MARK(6);
     }
-    __syncthreads();
-    PP_MARK(6);
-  }
+    if (lane == 0) *A.steps_done = done;
 #ifdef SRO_PHASE_TIMING
-  if (A.phase && (tid == 0 || tid == 32))
-    for (int q = 0; q < 7; q++) A.phase[(tid ? 8 : 0) + q] += pp_acc[q];
+    if (lane == 0 && A.phase) {
+      for (int q = 0; q < 8; q++) A.phase[q] += pw_acc[q];
+      for (int q = 8; q < 16; q++) A.phase[q] += sp_state.acc[q];
+    }
 #endif
+  }
   __syncthreads();
   for (int k = tid; k < m; k += PIPE_THREADS) { A.h[k] = sh_h[k]; A.r[k] = sh_r[k]; }
-  if (tid == 0) *A.steps_done = done;
+  if (steps == 0 && tid == 0) *A.steps_done = 0;
 }
 
 }  // namespace sro

@@ -135,8 +135,8 @@ struct Solver {
   double cmax = -1.0;           // max cost, computed once (ensure_cmax)
   bool no_rf = getenv("SRO_NO_RF") != nullptr;      // debug: force the shared-memory kernel
   bool no_tail = getenv("SRO_NO_TAIL") != nullptr;  // debug: force the multi-kernel block step
-  // pipelined BCFW kernel (k_bcfw_pipe.cuh): opt-in while it is slower than k_bcfw_rf (SRO_PIPE=1)
-  bool no_pipe = getenv("SRO_PIPE") == nullptr || getenv("SRO_NO_RF") != nullptr;
+  // debug: no pipelined BCFW kernel (k_bcfw_pipe.cuh) -> register-file kernel k_bcfw_rf
+  bool no_pipe = getenv("SRO_NO_PIPE") != nullptr || getenv("SRO_NO_RF") != nullptr;
   sro_stats stats{};
   bool timing = false;
   struct Pending { cudaEvent_t a, b; int cat; int64_t units; };
