@@ -344,11 +344,27 @@ __device__ int ga_draw(const double* fen, const double* G, int n, double u53) {
     return i >= n ? n - 1 : i;
   }
   double u = d_mul(u53, W);
-  int pos = 0, bit = 1;
-  while (bit * 2 <= n) bit *= 2;
-  for (; bit > 0; bit >>= 1) {
-    if (pos + bit <= n && fen[pos + bit] <= u) { pos += bit; u = d_sub(u, fen[pos]); }
+  int pos = 0;
+  int bit = 1 << (31 - __clz(n));   // highest power of two <= n
+  // Standard descent (if (pos+bit <= n && fen[pos+bit] <= u) { pos += bit; u -= fen[pos]; }),
+  // two levels per round: both candidates of the second level are loaded with the
+  // first, so the dependent shared-memory loads halve; comparisons and
+  // subtractions are the same operations in the same order.
+  while (bit > 1) {
+    const int b2 = bit >> 1;
+    const double fa = (pos + bit <= n) ? fen[pos + bit] : 0.0;
+    const double f0 = (pos + b2 <= n) ? fen[pos + b2] : 0.0;
+    const double f1 = (pos + bit + b2 <= n) ? fen[pos + bit + b2] : 0.0;
+    const bool t1 = (pos + bit <= n) && fa <= u;
+    const double ua = d_sub(u, fa);
+    if (t1) { pos += bit; u = ua; }
+    const double fb = t1 ? f1 : f0;
+    const bool t2 = (pos + b2 <= n) && fb <= u;
+    const double ub = d_sub(u, fb);
+    if (t2) { pos += b2; u = ub; }
+    bit >>= 2;
   }
+  if (bit == 1 && pos + 1 <= n && fen[pos + 1] <= u) { pos += 1; u = d_sub(u, fen[pos]); }
   if (pos >= n) {
     for (int i = n - 1; i >= 0; i--) if (wpos(G[i]) > 0.0) return i;
     return n - 1;
@@ -361,11 +377,20 @@ __device__ __forceinline__ void ga_add(double* fen, int n, int i0, double delta)
 }
 // Same update with lane t of a warp updating the t-th node of the path (the
 // nodes are distinct, so each node receives exactly the one add it gets above).
+// With x = p - 1 a step p += p & -p sets the lowest zero bit of x, so the t-th
+// node is i0 with its t lowest zero bits set (closed form, no walk).
 __device__ __forceinline__ void ga_add_warp(double* fen, int n, int i0, double delta) {
   const int lane = threadIdx.x & 31;
-  int p = i0 + 1;
-  for (int t = 0; t < lane && p <= n; t++) p += p & -p;
-  if (p <= n) fen[p] = d_add(fen[p], delta);
+  const unsigned x0 = (unsigned)i0;
+  unsigned x = x0;
+  bool ok = true;
+  if (lane > 0) {
+    const unsigned zb = __fns(~x0, 0, lane);
+    if (zb == 0xffffffffu) ok = false;
+    else x = zb >= 31 ? 0xffffffffu : (x0 | ((2u << zb) - 1u));
+  }
+  const long long p = (long long)x + 1;
+  if (ok && p <= n) fen[p] = d_add(fen[p], delta);
   __syncwarp();
 }
 
@@ -378,7 +403,7 @@ __device__ __forceinline__ void ga_add_warp(double* fen, int n, int i0, double d
 // ---------------------------------------------------------------------------
 struct StepOut {
   int dir, vrow, nk, erow;
-  bool abort, keep, noop, ev;
+  bool abort, keep, noop, ev, merged;   // merged: entries in merged-support lane layout (else slab layout)
   double gamma, num, den, gfw, tnew, hnew;
   unsigned kmask;
 };
@@ -522,6 +547,7 @@ __device__ __forceinline__ StepOut serial_step(const BcfwArgs& A, long long kk, 
   }
   // apply: new column (exact zeros dropped), r += (t' - t), h refresh
   o.noop = (VAR == VAR_PAIR && o.dir == 3);
+  o.merged = use_merged;
   const int E = use_merged ? M : c0;
   const int erow = use_merged ? mrow : rw;
   const double eold = use_merged ? mt : tv;

@@ -389,4 +389,265 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_pipe(BcfwArgs A, const
   if (steps == 0 && tid == 0) *A.steps_done = 0;
 }
 
+// ---------------------------------------------------------------------------
+// Gap-adaptive sampling (BCFW-GA, Alg. A.4; with the away /
+// pairwise directions as in Fig. 4(c,d)) on dense costs. The next column is
+// drawn from the Fenwick tree only after the current step has refreshed its
+// stored gap, so steps cannot overlap; what the pipelined layout removes is the
+// second LMO pass of the post-update refresh G_i = g_i(T^{k+1}) (R15):
+//   min_k (C_ki + h'_k) = min( min over k not in T of (C_ki + h_k),
+//                              min over k in T of (C_ki + h'_k) ),
+// T = supp(t_i) U {j} the rows the step may change. The LMO warps get the support
+// as a mask before they scan, and return for each warp the overall (value,
+// row) minimum with its C_ki, plus the two smallest (value, row) pairs among
+// the rows outside the support; the minimum outside T is the second of those
+// if j lies outside the support, else the first. So one scan serves the step
+// and the refresh, with every value computed exactly as a full scan would.
+// Per step: draw (warp 0) -> column index to the LMO warps (BAR_COL) -> the
+// support mask (BAR_MASK) -> partials (BAR_PART) -> serial part, gap refresh,
+// Fenwick update (warp 0).
+// ---------------------------------------------------------------------------
+constexpr int BAR_COL = 3;
+
+struct GaPipeLayout {
+  __host__ __device__ static size_t fixed() {
+    return 256 * 8 + 16 * 4 * 8 + 16 * 4 * 4 + 16 * 4 + PIPE_LMO * 4;   // slots, key partials, row partials, misc, masks
+  }
+  __host__ __device__ static size_t bytes(int m, int n) {
+    return fixed() + 4 * rup16((size_t)m * 8) + rup16((size_t)n * 4) + rup16((size_t)n * 8) +
+           rup16((size_t)(n + 1) * 8);
+  }
+};
+
+// (key, row) lexicographic minimum over the warp with 3 REDUX.MIN; returns the lane that held it
+__device__ __forceinline__ int warp_argmin_key(unsigned long long& key, int& j) {
+  const unsigned long long k0 = key;
+  const int j0 = j;
+  warp_argmin_redux(key, j);
+  return __ffs(__ballot_sync(FULL, k0 == key && j0 == j)) - 1;
+}
+
+template <typename T, int MAXV, int VAR>
+__global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, const T* __restrict__ Cg, int64_t ld) {
+  constexpr int W = Vec<T>::W;
+  extern __shared__ __align__(16) char smraw[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m = A.m, n = A.n, cap = A.cap;
+  const int nvec = m / W;
+  const int steps = A.steps;
+  char* p = smraw;
+  double* slots = reinterpret_cast<double*>(p); p += 256 * 8;
+  unsigned long long* pk = reinterpret_cast<unsigned long long*>(p); p += 16 * 4 * 8;   // [4][16]: all, u1, u2, cval
+  int* pj = reinterpret_cast<int*>(p); p += 16 * 4 * 4;                               // [4][16] rows
+  volatile int* misc = reinterpret_cast<volatile int*>(p); p += 16 * 4;   // [0] = column, [2] = abort
+  unsigned* mflag = reinterpret_cast<unsigned*>(p); p += PIPE_LMO * 4;
+  double* sh_h = reinterpret_cast<double*>(p); p += rup16((size_t)m * 8);
+  double* sh_r = reinterpret_cast<double*>(p); p += rup16((size_t)m * 8);
+  double* sh_a = reinterpret_cast<double*>(p); p += rup16((size_t)m * 8);
+  double* hpd = reinterpret_cast<double*>(p); p += rup16((size_t)m * 8);
+  const double2* hp = reinterpret_cast<const double2*>(hpd);
+  int* sh_cnt = reinterpret_cast<int*>(p); p += rup16((size_t)n * 4);
+  double* Gs = reinterpret_cast<double*>(p); p += rup16((size_t)n * 8);
+  double* fens = reinterpret_cast<double*>(p); p += rup16((size_t)(n + 1) * 8);
+  for (int c = tid; c < 256; c += PIPE_THREADS) slots[c] = 0.0;
+  for (int k = tid; k < m; k += PIPE_THREADS) {
+    const double hk = A.h[k];
+    sh_h[k] = hk; sh_r[k] = A.r[k]; sh_a[k] = A.a[k];
+    if (k < nvec * W) hpd[pipe_hidx<W>(k, nvec)] = hk;
+  }
+  for (int c = tid; c < n; c += PIPE_THREADS) { sh_cnt[c] = A.cnt[c]; Gs[c] = A.G[c]; }
+  for (int c = tid; c <= n; c += PIPE_THREADS) fens[c] = A.fen[c];
+  for (int c = tid; c < PIPE_LMO; c += PIPE_THREADS) mflag[c] = 0;
+  if (tid == 0) { misc[0] = 0; misc[2] = 0; }
+  __syncthreads();
+
+  if (steps > 0 && warp > 0 && (warp & 3) != 0) {
+    // =================== LMO warps ===================
+    const int lw = warp - 1 - (warp >> 2);
+    const int lt = lw * 32 + lane;
+    const int kt = nvec * W + lt;
+    PipeCol<T, MAXV> col;
+    col.C = Cg; col.ld = ld; col.m = m; col.nvec = nvec;
+    for (int t = 0; t < steps; t++) {
+      nbar_sync(BAR_COL, PIPE_SYNC);                   // the drawn column (or abort)
+      if (misc[2]) break;
+      const int i = misc[0];
+      col.fetch(i, lt);
+      col.advance();
+      nbar_sync(BAR_MASK, PIPE_SYNC);                  // its support as a mask
+      const unsigned mk = mflag[lt];
+      mflag[lt] = 0;
+      double best = dinf(), u1 = dinf(), u2 = dinf();
+      int bj = 0x7fffffff, j1 = 0x7fffffff, j2 = 0x7fffffff;
+      double bc = 0.0;
+      auto visit = [&](double c, double h, int k, bool masked) {
+        const double x = d_add(c, h);
+        const bool nb = x < best;
+        best = nb ? x : best; bj = nb ? k : bj; bc = nb ? c : bc;
+        const bool l1 = !masked && x < u1;
+        const bool l2 = !masked && !l1 && x < u2;
+        u2 = l1 ? u1 : (l2 ? x : u2); j2 = l1 ? j1 : (l2 ? k : j2);
+        u1 = l1 ? x : u1; j1 = l1 ? k : j1;
+      };
+#pragma unroll
+      for (int u = 0; u < MAXV; u++) {
+        const int q = lt + u * PIPE_LMO;
+        if (q < nvec) {
+          double hv[W];
+          pipe_h(hp, nvec, q, col.cur, hv);
+          const unsigned mu = mk >> (u * W);
+          if constexpr (W == 4) {
+            visit((double)col.cur[u].x, hv[0], W * q, mu & 1u);
+            visit((double)col.cur[u].y, hv[1], W * q + 1, mu & 2u);
+            visit((double)col.cur[u].z, hv[2], W * q + 2, mu & 4u);
+            visit((double)col.cur[u].w, hv[3], W * q + 3, mu & 8u);
+          } else {
+            visit((double)col.cur[u].x, hv[0], W * q, mu & 1u);
+            visit((double)col.cur[u].y, hv[1], W * q + 1, mu & 2u);
+          }
+        }
+      }
+      if (kt < m) visit((double)col.ctail, sh_h[kt], kt, mk >> 31);
+      // warp partials: overall minimum (+ its cost), two smallest outside the support
+      unsigned long long ka = okey(best);
+      int ja = bj;
+      const int wl = warp_argmin_key(ka, ja);
+      const double cw = __shfl_sync(FULL, bc, wl);
+      unsigned long long k1 = okey(u1);
+      int r1 = j1;
+      const int w1 = warp_argmin_key(k1, r1);
+      unsigned long long k2 = lane == w1 ? okey(u2) : okey(u1);
+      int r2 = lane == w1 ? j2 : j1;
+      warp_argmin_redux(k2, r2);
+      if (lane == 0) {
+        pk[lw] = ka; pj[lw] = ja; pk[16 + lw] = k1; pj[16 + lw] = r1; pk[32 + lw] = k2; pj[32 + lw] = r2;
+        pk[48 + lw] = (unsigned long long)__double_as_longlong(cw);
+      }
+      nbar_arrive(BAR_PART, PIPE_SYNC);
+    }
+  } else if (steps > 0 && warp == 0) {
+    // =================== serial warp ===================
+    int done = 0;
+    auto draw = [&](double u53) {
+      int ii = 0;
+      if (lane == 0) ii = ga_draw(fens, Gs, n, u53);
+      return __shfl_sync(FULL, ii, 0);
+    };
+    int i = draw(uniform53(rng_u64(A.seed, 1, (uint64_t)A.k0)));
+    if (lane == 0) misc[0] = i;
+    __syncwarp();
+    nbar_arrive(BAR_COL, PIPE_SYNC);
+    for (int s = 0; s < steps; s++) {
+      const long long kk = A.k0 + s;
+      const double u_next = uniform53(rng_u64(A.seed, 1, (uint64_t)(kk + 1)));   // next draw's uniform, off the critical path
+      // the drawn column's slab -> support mask for the LMO warps
+      const int c0 = sh_cnt[i];
+      const double bi = A.b[i];
+      int rw = 0x7fffffff;
+      double tv = 0.0;
+      if (lane < c0) { rw = A.srow[(int64_t)i * cap + lane]; tv = A.sval[(int64_t)i * cap + lane]; }
+      if (lane < c0) {
+        int ot;
+        unsigned bit;
+        pipe_owner<W>(rw, nvec, ot, bit);
+        atomicOr(&mflag[ot], bit);
+      }
+      __syncwarp();
+      nbar_arrive(BAR_MASK, PIPE_SYNC);
+      const double cw = lane < c0 ? (double)__ldg(Cg + (int64_t)i * ld + rw) : 0.0;
+      // ---- partials -> LMO result (j, mv), C_ji, and the minimum outside T = supp U {j}
+      nbar_sync(BAR_PART, PIPE_SYNC);
+      unsigned long long ka = lane < PIPE_LMO_WARPS ? pk[lane] : ~0ULL;
+      int ja = lane < PIPE_LMO_WARPS ? pj[lane] : 0x7fffffff;
+      const double cwl = lane < PIPE_LMO_WARPS ? __longlong_as_double((long long)pk[48 + lane]) : 0.0;
+      const int wl = warp_argmin_key(ka, ja);
+      const double cj = __shfl_sync(FULL, cwl, wl);
+      const int j = ja;
+      const double mv = okey_inv(ka);
+      unsigned long long k1 = lane < PIPE_LMO_WARPS ? pk[16 + lane] : ~0ULL;
+      int r1 = lane < PIPE_LMO_WARPS ? pj[16 + lane] : 0x7fffffff;
+      unsigned long long k2l = lane < PIPE_LMO_WARPS ? pk[32 + lane] : ~0ULL;
+      int r2l = lane < PIPE_LMO_WARPS ? pj[32 + lane] : 0x7fffffff;
+      const unsigned long long k1l = k1;
+      const int r1l = r1;
+      const int w1 = warp_argmin_key(k1, r1);
+      unsigned long long k2 = lane == w1 ? k2l : k1l;
+      int r2 = lane == w1 ? r2l : r1l;
+      warp_argmin_redux(k2, r2);
+      const bool j_in_supp = __ballot_sync(FULL, lane < c0 && rw == j) != 0u;
+      const unsigned long long kout = j_in_supp ? k1 : k2;   // min over rows outside T (old h = new h there)
+      const double m_out = kout == ~0ULL ? dinf() : okey_inv(kout);
+      // ---- the serial part
+      const double gk = lane < c0 ? d_add(cw, sh_h[rw]) : 0.0;
+      const StepOut o = serial_step<VAR>(A, kk, i, j, mv, bi, c0, rw, tv, gk, sh_r, sh_h, nullptr, sh_a, sh_cnt,
+                                         slots, nullptr SP_NULL);
+      if (o.ev && o.erow < nvec * W) hpd[pipe_hidx<W>(o.erow, nvec)] = o.hnew;
+      if (o.abort) {
+        if (lane == 0) {
+          misc[2] = 1;
+          set_status(A.status, !(mv < 1.0e308 && mv > -1.0e308) ? 5 : 6);
+        }
+        __syncwarp();
+        if (s + 1 < steps) nbar_arrive(BAR_COL, PIPE_SYNC);
+        break;
+      }
+      if (A.trace && lane == 0) {
+        double* tr = A.trace + 9 * (int64_t)s;
+        tr[0] = (double)kk; tr[1] = i; tr[2] = j; tr[3] = (VAR == VAR_PLAIN) ? -1 : o.vrow;
+        tr[4] = o.dir; tr[5] = o.gamma; tr[6] = o.num; tr[7] = o.den; tr[8] = mv;
+      }
+      // ---- GA: refresh the visited column's stored gap (Alg. A.4 line 6)
+      if (A.ga_inner) {
+        double gnew = o.gfw;
+        if (A.ga_post) {
+          // T = supp U {j} in merged-support lane layout, with C at each row (C_ji from the LMO)
+          const bool j_in = __ballot_sync(FULL, lane < c0 && rw == j) != 0u;
+          const int ins = __popc(__ballot_sync(FULL, lane < c0 && rw < j));
+          int src = (j_in || lane < ins) ? lane : lane - 1;
+          if (src < 0) src = 0;
+          int mrow = __shfl_sync(FULL, rw, src);
+          double mC = __shfl_sync(FULL, cw, src);
+          if (!j_in && lane == ins) { mrow = j; mC = cj; }
+          const int M = c0 + (j_in ? 0 : 1);
+          // post-update minimum: outside T unchanged (m_out), on T with the updated h
+          const unsigned long long kt2 = okey(lane < M ? d_add(mC, sh_h[mrow]) : dinf());
+          const unsigned hi = __reduce_min_sync(FULL, (unsigned)(kt2 >> 32));
+          const unsigned lo = __reduce_min_sync(FULL, (unsigned)(kt2 >> 32) == hi ? (unsigned)kt2 : 0xffffffffu);
+          const double mT = okey_inv(((unsigned long long)hi << 32) | lo);
+          const double mnew = mT < m_out ? mT : m_out;
+          // <t', c_i + h'> over the new support, rows ascending (entries in o's lane layout)
+          const double ce = o.merged ? mC : cw;
+          const double term = o.keep ? d_mul(o.tnew, d_add(ce, sh_h[o.erow])) : 0.0;
+          double acc = 0.0;
+          unsigned km = o.kmask;
+          while (km) {
+            const int q = __ffs(km) - 1;
+            km &= km - 1;
+            acc = d_add(acc, __shfl_sync(FULL, term, q));
+          }
+          gnew = d_sub(acc, d_mul(bi, mnew));
+        }
+        const double delta = d_sub(wpos(gnew), wpos(Gs[i]));
+        __syncwarp();
+        ga_add_warp(fens, n, i, delta);
+        if (lane == 0) Gs[i] = gnew;
+        __syncwarp();
+      }
+      done = s + 1;
+      if (s + 1 < steps) {
+        i = draw(u_next);
+        if (lane == 0) misc[0] = i;
+        __syncwarp();
+        nbar_arrive(BAR_COL, PIPE_SYNC);
+      }
+    }
+    if (lane == 0) *A.steps_done = done;
+  }
+  __syncthreads();
+  for (int k = tid; k < m; k += PIPE_THREADS) { A.h[k] = sh_h[k]; A.r[k] = sh_r[k]; }
+  for (int c = tid; c < n; c += PIPE_THREADS) A.G[c] = Gs[c];
+  for (int c = tid; c <= n; c += PIPE_THREADS) A.fen[c] = fens[c];
+  if (steps == 0 && tid == 0) *A.steps_done = 0;
+}
+
 }  // namespace sro

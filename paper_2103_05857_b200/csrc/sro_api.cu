@@ -743,10 +743,49 @@ sro_status bcfw_try_pipe(Solver* s, BcfwArgs& A) {
   return launch_pipe<double, 4, VAR>(s, A, bytes);
 }
 
+template <typename T, int MAXV, int VAR>
+sro_status launch_ga_pipe(Solver* s, BcfwArgs& A, size_t smem) {
+  auto kern = k_bcfw_ga_pipe<T, MAXV, VAR>;
+  CUDA_TRY(s, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int tr = timed_begin(s);
+  kern<<<1, PIPE_THREADS, smem, s->stream>>>(A, (const T*)s->C, s->ld);
+  CUDA_TRY(s, cudaGetLastError());
+  timed_end(s, tr, CAT_BCFW, A.steps);
+  s->lead->stats.kernel_launches += 1;
+  s->lead->stats.bcfw_launches += 1;
+  s->lead->stats.bcfw_steps += A.steps;
+  return SRO_OK;
+}
+
+// GA counterpart (k_bcfw_ga_pipe): dense costs, state + stored gaps + Fenwick
+// tree in shared memory. SRO_ERR_DIMENSION when it does not apply.
+template <int VAR>
+sro_status bcfw_try_ga_pipe(Solver* s, BcfwArgs& A) {
+  const bool dense = s->kind == SRO_COST_DENSE || s->kind == SRO_COST_HASH_UNIFORM;
+  if (!dense || s->no_pipe) return SRO_ERR_DIMENSION;
+  const int W = s->prec == SRO_FP32 ? 4 : 2;
+  const int nvec = s->m / W;
+  const int need = (nvec + PIPE_LMO - 1) / PIPE_LMO;
+  if (need > 4 || s->m - nvec * W > PIPE_LMO) return SRO_ERR_DIMENSION;
+  const size_t bytes = GaPipeLayout::bytes(s->m, s->n);
+  if (bytes > 226 * 1024) return SRO_ERR_DIMENSION;
+  A.ga_smem = 1; A.a_smem = 1; A.visit_smem = 0;
+  if (s->prec == SRO_FP32) {
+    if (need <= 1) return launch_ga_pipe<float, 1, VAR>(s, A, bytes);
+    if (need <= 2) return launch_ga_pipe<float, 2, VAR>(s, A, bytes);
+    if (need <= 3) return launch_ga_pipe<float, 3, VAR>(s, A, bytes);
+    return launch_ga_pipe<float, 4, VAR>(s, A, bytes);
+  }
+  if (need <= 1) return launch_ga_pipe<double, 1, VAR>(s, A, bytes);
+  if (need <= 2) return launch_ga_pipe<double, 2, VAR>(s, A, bytes);
+  if (need <= 3) return launch_ga_pipe<double, 3, VAR>(s, A, bytes);
+  return launch_ga_pipe<double, 4, VAR>(s, A, bytes);
+}
+
 template <int VAR, bool GA>
 sro_status bcfw_run(Solver* s, BcfwArgs& A) {
-  if (!GA) {
-    sro_status st = bcfw_try_pipe<VAR>(s, A);
+  {
+    sro_status st = GA ? bcfw_try_ga_pipe<VAR>(s, A) : bcfw_try_pipe<VAR>(s, A);
     if (st != SRO_ERR_DIMENSION) return st;
   }
   if (!s->no_rf) {
