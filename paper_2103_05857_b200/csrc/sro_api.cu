@@ -22,6 +22,7 @@
 #include <cstring>
 #include <string>
 #include <algorithm>
+#include <mutex>
 #include <type_traits>
 #include <vector>
 
@@ -211,6 +212,39 @@ void resolve_timing(Solver* s) {
   } while (0)
 
 thread_local std::string g_create_err;
+
+// Per-(device, kernel) cache of the dynamic shared-memory attribute and of the
+// occupancy query: both are host API calls of several microseconds, and the
+// batched / FW loops launch kernels back to back.
+struct FuncAttrCache {
+  struct E { int dev; const void* f; int smem_set; int threads; size_t smem; int per_sm; };
+  std::vector<E> v;
+  std::mutex mu;
+};
+FuncAttrCache& fcache() { static FuncAttrCache c; return c; }
+cudaError_t set_dyn_smem(const void* f, int dev, int smem) {
+  FuncAttrCache& c = fcache();
+  std::lock_guard<std::mutex> lk(c.mu);
+  for (auto& e : c.v)
+    if (e.dev == dev && e.f == f && e.threads == 0) {
+      if (smem <= e.smem_set) return cudaSuccess;
+      cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (r == cudaSuccess) e.smem_set = smem;
+      return r;
+    }
+  cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (r == cudaSuccess) c.v.push_back({dev, f, smem, 0, 0, 0});
+  return r;
+}
+cudaError_t occupancy(const void* f, int dev, int threads, size_t smem, int* per_sm) {
+  FuncAttrCache& c = fcache();
+  std::lock_guard<std::mutex> lk(c.mu);
+  for (auto& e : c.v)
+    if (e.dev == dev && e.f == f && e.threads == threads && e.smem == smem) { *per_sm = e.per_sm; return cudaSuccess; }
+  cudaError_t r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, f, threads, smem);
+  if (r == cudaSuccess) c.v.push_back({dev, f, 0, threads, smem, *per_sm});
+  return r;
+}
 
 template <typename T>
 cudaError_t dalloc(T** p, size_t count) {
@@ -451,15 +485,22 @@ sro_status sweep_bulk(Solver* s, Src src, const int* col0_dev, int col0_mul, int
                       double* out_min, double* out_g, const int* stop) {
   using T = std::remove_cv_t<std::remove_pointer_t<decltype(src.C)>>;
   constexpr int S = 4;
-  const int slab = s->slab_bulk;
+  // rows per (slab, column) item: the default slab, smaller when the sweep has few
+  // columns (a batched block) so that every SM still gets several items
+  int slab = s->slab_bulk;
+  {
+    const int64_t target = (int64_t)s->num_sms * BULK_WARPS * 2;
+    const int64_t want = ((int64_t)s->m * L + target - 1) / target;
+    if (want < slab) slab = (int)std::max<int64_t>(256, (want + 3) / 4 * 4);
+  }
   const int nslabs = (s->m + slab - 1) / slab;
   { sro_status st = ensure_partials(s, nslabs, L); if (st) return st; }
   const int rows = s->m < slab ? s->m : slab;
   const size_t smem = 1024 + (size_t)BULK_WARPS * S * BULK_CH + sizeof(double) * (size_t)rows;
   auto kern = k_lmo_sweep_bulk<T, S>;
-  CUDA_TRY(s, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CUDA_TRY(s, set_dyn_smem((const void*)kern, s->device, (int)smem));
   int per_sm = 0;
-  CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BULK_WARPS * 32, smem));
+  CUDA_TRY(s, occupancy((const void*)kern, s->device, BULK_WARPS * 32, smem, &per_sm));
   if (per_sm < 1) per_sm = 1;
   const int64_t ntot = (int64_t)nslabs * L;
   int64_t nb = (int64_t)s->num_sms * per_sm;
@@ -507,9 +548,9 @@ sro_status sweep(Solver* s, const int* col0_dev, int col0_mul, int col0_host, in
     const int rows = s->m < slab ? s->m : slab;
     const size_t smem = sizeof(double) * (size_t)((rows + 1) & ~1) + (size_t)Src::SMEM_PER_ROW * rows;
     auto kern = k_lmo_sweep<Src>;
-    CUDA_TRY(s, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_TRY(s, set_dyn_smem((const void*)kern, s->device, (int)smem));
     int per_sm = 0;
-    CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, SWEEP_THREADS, smem));
+    CUDA_TRY(s, occupancy((const void*)kern, s->device, SWEEP_THREADS, smem, &per_sm));
     if (per_sm < 1) per_sm = 1;
     int gx = s->num_sms * per_sm;
     const int need = (L + SWEEP_WARPS - 1) / SWEEP_WARPS;
@@ -604,7 +645,7 @@ void copy_trace_out(const std::vector<double>& tr, int64_t count, sro_trace_rec*
 template <class Col, int VAR, bool GA, bool SMEM>
 sro_status launch_bcfw(Solver* s, BcfwArgs& A, Col col, size_t smem) {
   auto kern = k_bcfw<Col, VAR, GA, SMEM>;
-  CUDA_TRY(s, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CUDA_TRY(s, set_dyn_smem((const void*)kern, s->device, (int)smem));
   const int tr = timed_begin(s);
   kern<<<1, BCFW_THREADS, smem, s->stream>>>(A, col);
   CUDA_TRY(s, cudaGetLastError());
@@ -664,7 +705,7 @@ sro_status bcfw_dispatch(Solver* s, BcfwArgs& A) {
 template <typename T, int MAXV, int VAR, bool GA>
 sro_status launch_rf(Solver* s, BcfwArgs& A, size_t smem) {
   auto kern = k_bcfw_rf<T, MAXV, VAR, GA>;
-  CUDA_TRY(s, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CUDA_TRY(s, set_dyn_smem((const void*)kern, s->device, (int)smem));
   const int tr = timed_begin(s);
   kern<<<1, BCFW_THREADS, smem, s->stream>>>(A, (const T*)s->C, s->ld);
   CUDA_TRY(s, cudaGetLastError());
@@ -703,7 +744,7 @@ sro_status bcfw_try_rf(Solver* s, BcfwArgs& A) {
 template <typename T, int MAXV, int VAR>
 sro_status launch_pipe(Solver* s, BcfwArgs& A, size_t smem) {
   auto kern = k_bcfw_pipe<T, MAXV, VAR>;
-  CUDA_TRY(s, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CUDA_TRY(s, set_dyn_smem((const void*)kern, s->device, (int)smem));
   const int tr = timed_begin(s);
   kern<<<1, PIPE_THREADS, smem, s->stream>>>(A, (const T*)s->C, s->ld);
   CUDA_TRY(s, cudaGetLastError());
@@ -746,7 +787,7 @@ sro_status bcfw_try_pipe(Solver* s, BcfwArgs& A) {
 template <typename T, int MAXV, int VAR>
 sro_status launch_ga_pipe(Solver* s, BcfwArgs& A, size_t smem) {
   auto kern = k_bcfw_ga_pipe<T, MAXV, VAR>;
-  CUDA_TRY(s, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CUDA_TRY(s, set_dyn_smem((const void*)kern, s->device, (int)smem));
   const int tr = timed_begin(s);
   kern<<<1, PIPE_THREADS, smem, s->stream>>>(A, (const T*)s->C, s->ld);
   CUDA_TRY(s, cudaGetLastError());
@@ -838,7 +879,7 @@ sro_status ensure_cmax(Solver* s) {
 sro_status fen_build(Solver* s) {
   const size_t bytes = sizeof(double) * ((size_t)s->n + 1);
   const int use_smem = bytes <= 200 * 1024;
-  if (use_smem) CUDA_TRY(s, cudaFuncSetAttribute(k_fen_build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  if (use_smem) CUDA_TRY(s, set_dyn_smem((const void*)k_fen_build, s->device, (int)bytes));
   k_fen_build<<<1, 256, use_smem ? bytes : 0, s->stream>>>(s->G_ga, s->fen, s->n, use_smem);
   s->lead->stats.kernel_launches += 1;
   CUDA_TRY(s, cudaGetLastError());
