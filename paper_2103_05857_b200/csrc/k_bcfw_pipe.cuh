@@ -477,17 +477,16 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
       nbar_sync(BAR_MASK, PIPE_SYNC);                  // its support as a mask
       const unsigned mk = mflag[lt];
       mflag[lt] = 0;
-      double best = dinf(), u1 = dinf(), u2 = dinf();
-      int bj = 0x7fffffff, j1 = 0x7fffffff, j2 = 0x7fffffff;
-      double bc = 0.0;
+      // rows outside the support only: smallest (value, row) with its C, and the
+      // second smallest value (the support rows are warp 0's: it holds their C)
+      double u1 = dinf(), u2 = dinf(), c1 = 0.0;
+      int j1 = 0x7fffffff;
       auto visit = [&](double c, double h, int k, bool masked) {
         const double x = d_add(c, h);
-        const bool nb = x < best;
-        best = nb ? x : best; bj = nb ? k : bj; bc = nb ? c : bc;
         const bool l1 = !masked && x < u1;
         const bool l2 = !masked && !l1 && x < u2;
-        u2 = l1 ? u1 : (l2 ? x : u2); j2 = l1 ? j1 : (l2 ? k : j2);
-        u1 = l1 ? x : u1; j1 = l1 ? k : j1;
+        u2 = l1 ? u1 : (l2 ? x : u2);
+        u1 = l1 ? x : u1; j1 = l1 ? k : j1; c1 = l1 ? c : c1;
       };
 #pragma unroll
       for (int u = 0; u < MAXV; u++) {
@@ -508,20 +507,16 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
         }
       }
       if (kt < m) visit((double)col.ctail, sh_h[kt], kt, mk >> 31);
-      // warp partials: overall minimum (+ its cost), two smallest outside the support
-      unsigned long long ka = okey(best);
-      int ja = bj;
-      const int wl = warp_argmin_key(ka, ja);
-      const double cw = __shfl_sync(FULL, bc, wl);
       unsigned long long k1 = okey(u1);
       int r1 = j1;
       const int w1 = warp_argmin_key(k1, r1);
-      unsigned long long k2 = lane == w1 ? okey(u2) : okey(u1);
-      int r2 = lane == w1 ? j2 : j1;
-      warp_argmin_redux(k2, r2);
+      const double cw1 = __shfl_sync(FULL, c1, w1);
+      const unsigned long long k2l = lane == w1 ? okey(u2) : okey(u1);
+      const unsigned h2 = __reduce_min_sync(FULL, (unsigned)(k2l >> 32));
+      const unsigned l2 = __reduce_min_sync(FULL, (unsigned)(k2l >> 32) == h2 ? (unsigned)k2l : 0xffffffffu);
       if (lane == 0) {
-        pk[lw] = ka; pj[lw] = ja; pk[16 + lw] = k1; pj[16 + lw] = r1; pk[32 + lw] = k2; pj[32 + lw] = r2;
-        pk[48 + lw] = (unsigned long long)__double_as_longlong(cw);
+        pk[lw] = k1; pj[lw] = r1; pk[16 + lw] = ((unsigned long long)h2 << 32) | l2;
+        pk[48 + lw] = (unsigned long long)__double_as_longlong(cw1);
       }
       nbar_arrive(BAR_PART, PIPE_SYNC);
     }
@@ -556,29 +551,31 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
       nbar_arrive(BAR_MASK, PIPE_SYNC);
       const double cw = lane < c0 ? (double)__ldg(Cg + (int64_t)i * ld + rw) : 0.0;
       // ---- partials -> LMO result (j, mv), C_ji, and the minimum outside T = supp U {j}
+      const double gk = lane < c0 ? d_add(cw, sh_h[rw]) : 0.0;   // support rows: C + h (old h)
+      unsigned long long ks = lane < c0 ? okey(gk) : ~0ULL;
+      int js = lane < c0 ? rw : 0x7fffffff;
+      const int wsl = warp_argmin_key(ks, js);
+      const double csup = __shfl_sync(FULL, cw, wsl);
       nbar_sync(BAR_PART, PIPE_SYNC);
-      unsigned long long ka = lane < PIPE_LMO_WARPS ? pk[lane] : ~0ULL;
-      int ja = lane < PIPE_LMO_WARPS ? pj[lane] : 0x7fffffff;
+      unsigned long long k1 = lane < PIPE_LMO_WARPS ? pk[lane] : ~0ULL;
+      int r1 = lane < PIPE_LMO_WARPS ? pj[lane] : 0x7fffffff;
+      const unsigned long long k2lane = lane < PIPE_LMO_WARPS ? pk[16 + lane] : ~0ULL;
       const double cwl = lane < PIPE_LMO_WARPS ? __longlong_as_double((long long)pk[48 + lane]) : 0.0;
-      const int wl = warp_argmin_key(ka, ja);
-      const double cj = __shfl_sync(FULL, cwl, wl);
-      const int j = ja;
-      const double mv = okey_inv(ka);
-      unsigned long long k1 = lane < PIPE_LMO_WARPS ? pk[16 + lane] : ~0ULL;
-      int r1 = lane < PIPE_LMO_WARPS ? pj[16 + lane] : 0x7fffffff;
-      unsigned long long k2l = lane < PIPE_LMO_WARPS ? pk[32 + lane] : ~0ULL;
-      int r2l = lane < PIPE_LMO_WARPS ? pj[32 + lane] : 0x7fffffff;
-      const unsigned long long k1l = k1;
-      const int r1l = r1;
+      const unsigned long long k1lane = k1;
       const int w1 = warp_argmin_key(k1, r1);
-      unsigned long long k2 = lane == w1 ? k2l : k1l;
-      int r2 = lane == w1 ? r2l : r1l;
-      warp_argmin_redux(k2, r2);
-      const bool j_in_supp = __ballot_sync(FULL, lane < c0 && rw == j) != 0u;
-      const unsigned long long kout = j_in_supp ? k1 : k2;   // min over rows outside T (old h = new h there)
+      const double c1 = __shfl_sync(FULL, cwl, w1);
+      const unsigned long long k2c = lane == w1 ? k2lane : k1lane;
+      const unsigned h2 = __reduce_min_sync(FULL, (unsigned)(k2c >> 32));
+      const unsigned l2 = __reduce_min_sync(FULL, (unsigned)(k2c >> 32) == h2 ? (unsigned)k2c : 0xffffffffu);
+      const unsigned long long k2 = ((unsigned long long)h2 << 32) | l2;
+      // overall minimum: the outside-the-support one or the support one (disjoint rows)
+      const bool sup_wins = ks < k1 || (ks == k1 && js < r1);
+      const int j = sup_wins ? js : r1;
+      const double mv = okey_inv(sup_wins ? ks : k1);
+      const double cj = sup_wins ? csup : c1;
+      const unsigned long long kout = sup_wins ? k1 : k2;   // min over rows outside T (old h = new h there)
       const double m_out = kout == ~0ULL ? dinf() : okey_inv(kout);
       // ---- the serial part
-      const double gk = lane < c0 ? d_add(cw, sh_h[rw]) : 0.0;
       const StepOut o = serial_step<VAR>(A, kk, i, j, mv, bi, c0, rw, tv, gk, sh_r, sh_h, nullptr, sh_a, sh_cnt,
                                          slots, nullptr SP_NULL);
       if (o.ev && o.erow < nvec * W) hpd[pipe_hidx<W>(o.erow, nvec)] = o.hnew;
