@@ -9,11 +9,14 @@
 // of a row combine by adjacent pairs. No float atomics anywhere:
 //   1. every column of U lists its merged support supp(t_i) U {j_i} as
 //      (row, d) pairs, rows ascending (pairs_count / scan / pairs_gen);
-//   2. the first pair of each (row, chunk) run sums the run in column order
-//      and writes the partial to acc[row][chunk] (dev_runs) — work per pair is
-//      O(chunk length x |supp|), independent of how many columns share a row;
-//   3. a warp per touched row combines its 256 chunk slots (dev_row_tree) and
-//      clears them, so acc stays zero outside a step.
+//   2. the touched rows get contiguous run-list segments (a scan of their pair
+//      counts); the first pair of each (row, chunk) run sums the run in column
+//      order and appends (chunk, partial) to its row's list (dev_runs) — work
+//      per pair is O(chunk length x |supp|), independent of how many columns
+//      share a row;
+//   3. a warp per touched row scatters its list into 256 shared-memory slots
+//      (zero outside use) and combines them with the adjacent-pair tree
+//      (dev_row_tree); only the few nonzero chunks of a row touch memory.
 //
 // Sharded mode: the G shards of U hold the contiguous position
 // ranges [s L/G, (s+1) L/G), which are exactly the chunks [s 256/G, (s+1) 256/G)
@@ -31,7 +34,6 @@
 
 namespace sro {
 
-constexpr int ACC_W = 256;   // chunk slots per row of the accumulation matrix
 
 struct BlockArgs {
   int m, n, cap;
@@ -60,10 +62,14 @@ struct BlockArgs {
   double* pd;            // P: s_ik - t_ik
   double* ptold;         // P: t_ik (sharded mode: rollback after a remote capacity error)
   double* pdelta;        // P: t'_ik - t_ik
-  double* acc;           // m x 256 chunk partials, zero outside a step
   int* rowcnt;           // m: pairs per row in this step, zero outside a step
+  int* rowidx;           // m: touched-list index of a touched row
   int* trows;            // touched rows (unordered; every row's work is independent)
   int* ntouch;           // number of touched rows
+  int* tstart;           // touched index -> start of its run-list segment (scan of its pair count)
+  int* tcur;             // touched index -> runs appended so far (zero outside a step)
+  int* runc;             // run lists: chunk index
+  double* runv;          // run lists: partial sum
   double* X;             // m: Delta_k^2, zero outside a step
   double* scal;          // [0]=G_U [1]=den [2]=gamma [3]=num
   const double* eps;     // FW stop check (nullptr for batched)
@@ -176,7 +182,11 @@ __device__ __forceinline__ void dev_pairs_gen(const BlockArgs& A) {
       A.ppos[q] = p;
       A.pd[q] = d_sub(row == j ? bi : 0.0, told);
       if (A.ptold) A.ptold[q] = told;
-      if (atomicAdd(&A.rowcnt[row], 1) == 0) A.trows[atomicAdd(A.ntouch, 1)] = row;   // order-free
+      if (atomicAdd(&A.rowcnt[row], 1) == 0) {   // order-free touched list
+        const int w = atomicAdd(A.ntouch, 1);
+        A.trows[w] = row;
+        A.rowidx[row] = w;
+      }
     });
   }
 }
@@ -191,8 +201,33 @@ __device__ __forceinline__ int find_pair(const BlockArgs& A, int pp, int k) {
   return -1;
 }
 
-// acc[k][c] = sum of val over the (row k, chunk c) run, ascending column
-// position, from +0.0 (R19). Computed by the run's first pair.
+// Run-list segments of the touched rows: tstart = exclusive scan over the
+// touched list of the rows' pair counts (one CTA of exactly 1024 threads).
+__device__ __forceinline__ void dev_touched_scan(const BlockArgs& A) {
+  __shared__ int ws[32];
+  const int N = *A.ntouch;
+  const int t = threadIdx.x;
+  const int per = (N + 1023) / 1024;
+  const int lo = min(N, t * per), hi = min(N, lo + per);
+  int s = 0;
+  for (int q = lo; q < hi; q++) s += A.rowcnt[A.trows[q]];
+  int incl = s;
+  for (int o = 1; o < 32; o <<= 1) { int v = __shfl_up_sync(FULL, incl, o); if ((t & 31) >= o) incl += v; }
+  if ((t & 31) == 31) ws[t >> 5] = incl;
+  __syncthreads();
+  if (t < 32) {
+    int w = ws[t];
+    for (int o = 1; o < 32; o <<= 1) { int v = __shfl_up_sync(FULL, w, o); if (t >= o) w += v; }
+    ws[t] = w;
+  }
+  __syncthreads();
+  int run = incl - s + ((t >> 5) ? ws[(t >> 5) - 1] : 0);
+  for (int q = lo; q < hi; q++) { A.tstart[q] = run; run += A.rowcnt[A.trows[q]]; }
+  __syncthreads();
+}
+
+// The (row k, chunk c) run of val summed in column order from +0.0 (R19) by
+// the run's first pair, appended to row k's run list as (c, sum).
 __device__ __forceinline__ void dev_runs(const BlockArgs& A, const double* __restrict__ val) {
   const int P = *A.ptotal;
   for (int q = gtid(); q < P; q += gstride()) {
@@ -207,27 +242,36 @@ __device__ __forceinline__ void dev_runs(const BlockArgs& A, const double* __res
       const int qq = find_pair(A, pp, k);
       if (qq >= 0) s = d_add(s, val[qq]);
     }
-    A.acc[(size_t)k * ACC_W + c] = s;
+    const int w = A.rowidx[k];
+    const int slot = A.tstart[w] + atomicAdd(&A.tcur[w], 1);   // order-free: one entry per chunk
+    A.runc[slot] = c;
+    A.runv[slot] = s;
   }
 }
 
-// Warp per touched row: the 256-leaf adjacent-pair tree over acc[k][*] (then
-// cleared). MODE 0: X[k] = D^2; MODE 1: r_k += D, h_k = (r_k - a_k)/lambda;
-// MODE 2: slot[k] = D (a shard's subtree). clear: reset rowcnt[k] (last tree of a step).
+// Warp per touched row: scatter its run list into the warp's 256 shared slots
+// (zero outside use), the 256-leaf adjacent-pair tree, clear the slots.
+// MODE 0: X[k] = D^2; MODE 1: r_k += D, h_k = (r_k - a_k)/lambda;
+// MODE 2: slot[k] = D (a shard's subtree). clear: reset the row's counters
+// (last tree of a step).
 template <int MODE>
-__device__ __forceinline__ void dev_row_tree(const BlockArgs& A, double* slot, bool clear) {
+__device__ __forceinline__ void dev_row_tree(const BlockArgs& A, double* slot, bool clear, double* wslots_all) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
+  double* sl = wslots_all + 256 * warp;
   const int T = *A.ntouch;
   for (int w = blockIdx.x * nwarps + warp; w < T; w += gridDim.x * nwarps) {
     const int k = A.trows[w];
-    double2* rowp = reinterpret_cast<double2*>(A.acc + (size_t)k * ACC_W + 8 * lane);
+    const int st = A.tstart[w], K = A.tcur[w];
+    for (int e = lane; e < K; e += 32) sl[A.runc[st + e]] = A.runv[st + e];
+    __syncwarp();
     double x[8];
 #pragma unroll
-    for (int t = 0; t < 4; t++) { const double2 v = rowp[t]; x[2 * t] = v.x; x[2 * t + 1] = v.y; }
+    for (int t = 0; t < 8; t++) x[t] = sl[8 * lane + t];
     const double D = warp_pair_tree(tree8(x));
-#pragma unroll
-    for (int t = 0; t < 4; t++) rowp[t] = make_double2(0.0, 0.0);
+    __syncwarp();
+    for (int e = lane; e < K; e += 32) sl[A.runc[st + e]] = 0.0;
+    __syncwarp();
     if (lane == 0) {
       if (MODE == 0) {
         A.X[k] = d_mul(D, D);
@@ -239,6 +283,7 @@ __device__ __forceinline__ void dev_row_tree(const BlockArgs& A, double* slot, b
       } else {
         slot[k] = D;
       }
+      A.tcur[w] = 0;
       if (clear) A.rowcnt[k] = 0;
     }
   }
@@ -356,9 +401,13 @@ __global__ void __launch_bounds__(1024) k_scan_pairs(BlockArgs A) {
 }
 __global__ void k_pairs_gen(BlockArgs A) { if (!blk_skip(A)) dev_pairs_gen(A); }
 __global__ void k_runs(BlockArgs A, const double* __restrict__ val) { if (!blk_skip(A)) dev_runs(A, val); }
+__global__ void __launch_bounds__(1024) k_touched_scan(BlockArgs A) { if (!blk_skip(A)) dev_touched_scan(A); }
 template <int MODE>
 __global__ void __launch_bounds__(256) k_row_tree(BlockArgs A, double* slot, int clear) {
-  if (!blk_skip(A)) dev_row_tree<MODE>(A, slot, clear != 0);
+  __shared__ double wsl[8 * 256];
+  for (int q = threadIdx.x; q < 8 * 256; q += blockDim.x) wsl[q] = 0.0;
+  __syncthreads();
+  if (!blk_skip(A)) dev_row_tree<MODE>(A, slot, clear != 0, wsl);
 }
 __global__ void k_gamma(BlockArgs A) { if (!blk_skip(A)) dev_gamma(A); }
 __global__ void k_cap_check(BlockArgs A) { if (!blk_skip(A)) dev_cap_check(A); }
@@ -389,7 +438,9 @@ __global__ void k_step_done(BlockArgs A) {
 
 // ... and the whole post-LMO step in one CTA of 1024 threads (small U).
 __global__ void __launch_bounds__(1024, 1) k_block_tail(BlockArgs A) {
+  extern __shared__ double tail_slots[];   // 32 warps x 256, zero outside use
   if (*A.status) return;
+  for (int q = threadIdx.x; q < 32 * 256; q += blockDim.x) tail_slots[q] = 0.0;
   if (threadIdx.x == 0) *A.ntouch = 0;
   dev_psumW(A.g, A.L, 256, A.scal + 0, A.eps, A.stop);        // G_U (FW: stop check)
   if (A.stop && *A.stop) return;
@@ -398,9 +449,10 @@ __global__ void __launch_bounds__(1024, 1) k_block_tail(BlockArgs A) {
   dev_scan_excl(A.pcount, A.L, A.poff, A.ptotal);
   dev_pairs_gen(A);
   __syncthreads();
+  dev_touched_scan(A);
   dev_runs(A, A.pd);
   __syncthreads();
-  dev_row_tree<0>(A, nullptr, false);
+  dev_row_tree<0>(A, nullptr, false, tail_slots);
   __syncthreads();
   dev_psumW(A.X, A.m, 256, A.scal + 1, nullptr, nullptr);
   dev_gamma(A);
@@ -412,7 +464,7 @@ __global__ void __launch_bounds__(1024, 1) k_block_tail(BlockArgs A) {
   __syncthreads();
   dev_runs(A, A.pdelta);
   __syncthreads();
-  dev_row_tree<1>(A, nullptr, true);
+  dev_row_tree<1>(A, nullptr, true, tail_slots);
   if (threadIdx.x == 0) atomicAdd(A.dsteps, 1ULL);
 }
 
@@ -510,7 +562,7 @@ __global__ void k_shard_apply(BlockArgs A) {
         A.cnt[i] = keep;
       }
     }
-    for (int w = gtid(); w < *A.ntouch; w += gstride()) A.rowcnt[A.trows[w]] = 0;
+    for (int w = gtid(); w < *A.ntouch; w += gstride()) { A.rowcnt[A.trows[w]] = 0; A.tcur[w] = 0; }
     if (gtid() == 0) set_status(A.status, 6);
     return;
   }
@@ -525,8 +577,10 @@ __global__ void k_shard_apply(BlockArgs A) {
 
 // Phase A in one CTA of 1024 threads (small U).
 __global__ void __launch_bounds__(1024, 1) k_shard_tail_a(BlockArgs A) {
+  extern __shared__ double tail_slots[];
   double* s1 = slot_of(A, A.x1, A.shard);
   if (!(A.stop && *A.stop) && !*A.status) {
+    for (int q = threadIdx.x; q < 32 * 256; q += blockDim.x) tail_slots[q] = 0.0;
     if (threadIdx.x == 0) { *A.ntouch = 0; *A.capfail = 0; }
     dev_psumW(A.g, A.L, A.W, s1 + A.m, nullptr, nullptr);
     dev_pairs_count(A);
@@ -535,9 +589,10 @@ __global__ void __launch_bounds__(1024, 1) k_shard_tail_a(BlockArgs A) {
     dev_scan_excl(A.pcount, A.L, A.poff, A.ptotal);
     dev_pairs_gen(A);
     __syncthreads();
+    dev_touched_scan(A);
     dev_runs(A, A.pd);
     __syncthreads();
-    dev_row_tree<2>(A, s1, false);
+    dev_row_tree<2>(A, s1, false, tail_slots);
   }
   __syncthreads();
   if (threadIdx.x == 0) s1[A.m + 1] = (double)*A.status;
@@ -545,7 +600,9 @@ __global__ void __launch_bounds__(1024, 1) k_shard_tail_a(BlockArgs A) {
 
 // Phase B in one CTA of 1024 threads (small U).
 __global__ void __launch_bounds__(1024, 1) k_shard_tail_b(BlockArgs A) {
+  extern __shared__ double tail_slots[];
   double* s2 = slot_of(A, A.x2, A.shard);
+  for (int q = threadIdx.x; q < 32 * 256; q += blockDim.x) tail_slots[q] = 0.0;
   bool run = !(A.stop && *A.stop) && !*A.status;
   if (run) {
     dev_shard_gamma(A);
@@ -561,7 +618,7 @@ __global__ void __launch_bounds__(1024, 1) k_shard_tail_b(BlockArgs A) {
       __syncthreads();
       dev_runs(A, A.pdelta);
       __syncthreads();
-      dev_row_tree<2>(A, s2, true);
+      dev_row_tree<2>(A, s2, true, tail_slots);
     }
   }
   __syncthreads();

@@ -119,8 +119,10 @@ struct Solver {
   int64_t blk_L = 0, blk_P = 0;
   int *pcount = nullptr, *poff = nullptr, *ptotal = nullptr, *prow = nullptr, *ppos = nullptr;
   double *pd = nullptr, *ptold = nullptr, *pdelta = nullptr;
-  double* acc = nullptr;       // m x 256 chunk partials (zero outside a step)
   int* rowcnt = nullptr;       // m (zero outside a step)
+  int *rowidx = nullptr, *tstart = nullptr, *tcur = nullptr;   // touched-row run-list bookkeeping (tcur zero outside a step)
+  int* runc = nullptr;         // run lists (P entries)
+  double* runv = nullptr;
   double* X = nullptr;         // m (zero outside a step)
   int* trows = nullptr;
   int* ntouch = nullptr;
@@ -162,6 +164,8 @@ std::vector<HeldCol> held_order(Solver* s) {
   std::sort(v.begin(), v.end(), [](const HeldCol& x, const HeldCol& y) { return x.global < y.global; });
   return v;
 }
+
+constexpr int TAIL_SMEM = 32 * 256 * 8;   // warp-private chunk slots of the single-CTA block tails
 
 enum { CAT_BCFW = 0, CAT_SWEEP = 1, CAT_BLOCK = 2 };
 
@@ -431,7 +435,7 @@ sro_status with_sweep_src(Solver* s, F f) {
 sro_status ws_clean(Solver* s) {
   if (s->rowcnt) CUDA_TRY(s, cudaMemsetAsync(s->rowcnt, 0, sizeof(int) * s->m, s->stream));
   if (s->X) CUDA_TRY(s, cudaMemsetAsync(s->X, 0, sizeof(double) * s->m, s->stream));
-  if (s->acc) CUDA_TRY(s, cudaMemsetAsync(s->acc, 0, sizeof(double) * (size_t)s->m * ACC_W, s->stream));
+  if (s->tcur) CUDA_TRY(s, cudaMemsetAsync(s->tcur, 0, sizeof(int) * s->m, s->stream));
   return SRO_OK;
 }
 
@@ -915,17 +919,19 @@ sro_status ensure_block_ws(Solver* s, int64_t L) {
   if (!s->rowcnt) {   // row workspace: zero outside a step
     CUDA_TRY(s, dalloc(&s->rowcnt, s->m)); CUDA_TRY(s, dalloc(&s->X, s->m));
     CUDA_TRY(s, dalloc(&s->trows, s->m)); CUDA_TRY(s, dalloc(&s->ntouch, 1));
-    CUDA_TRY(s, dalloc(&s->acc, (size_t)s->m * ACC_W)); CUDA_TRY(s, dalloc(&s->capfail, 1));
+    CUDA_TRY(s, dalloc(&s->rowidx, s->m)); CUDA_TRY(s, dalloc(&s->tstart, s->m));
+    CUDA_TRY(s, dalloc(&s->tcur, s->m)); CUDA_TRY(s, dalloc(&s->capfail, 1));
     { sro_status e = ws_clean(s); if (e) return e; }
     CUDA_TRY(s, cudaMemsetAsync(s->capfail, 0, sizeof(int), s->stream));
   }
   if (L <= s->blk_L && P <= s->blk_P) return SRO_OK;
   cudaFree(s->pcount); cudaFree(s->poff); cudaFree(s->ptotal); cudaFree(s->prow); cudaFree(s->ppos);
-  cudaFree(s->pd); cudaFree(s->ptold); cudaFree(s->pdelta);
+  cudaFree(s->pd); cudaFree(s->ptold); cudaFree(s->pdelta); cudaFree(s->runc); cudaFree(s->runv);
   s->blk_L = L; s->blk_P = P;
   CUDA_TRY(s, dalloc(&s->pcount, L)); CUDA_TRY(s, dalloc(&s->poff, L + 1)); CUDA_TRY(s, dalloc(&s->ptotal, 1));
   CUDA_TRY(s, dalloc(&s->prow, P)); CUDA_TRY(s, dalloc(&s->ppos, P)); CUDA_TRY(s, dalloc(&s->pd, P));
   CUDA_TRY(s, dalloc(&s->ptold, P)); CUDA_TRY(s, dalloc(&s->pdelta, P));
+  CUDA_TRY(s, dalloc(&s->runc, P)); CUDA_TRY(s, dalloc(&s->runv, P));
   return SRO_OK;
 }
 
@@ -937,7 +943,8 @@ BlockArgs block_args(Solver* s, const int* col0_dev, int col0_mul, int L, int st
   A.W = 256 / s->G;
   A.j = s->sw_j; A.minval = s->sw_min; A.g = s->sw_g; A.pcount = s->pcount; A.poff = s->poff; A.ptotal = s->ptotal;
   A.prow = s->prow; A.ppos = s->ppos; A.pd = s->pd; A.ptold = s->G > 1 ? s->ptold : nullptr; A.pdelta = s->pdelta;
-  A.acc = s->acc; A.rowcnt = s->rowcnt; A.trows = s->trows; A.ntouch = s->ntouch; A.X = s->X;
+  A.rowcnt = s->rowcnt; A.rowidx = s->rowidx; A.trows = s->trows; A.ntouch = s->ntouch; A.X = s->X;
+  A.tstart = s->tstart; A.tcur = s->tcur; A.runc = s->runc; A.runv = s->runv;
   A.scal = s->scal; A.eps = stop_check ? s->epsd : nullptr; A.stop = stop_check ? s->stop : nullptr;
   A.status = s->status;
   A.step_rule = step_rule; A.kk = s->lead->k + s->lead->k_pending; A.nprime = nprime; A.trace = trace_dev;
@@ -962,7 +969,8 @@ sro_status plain_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
   if (st) return st;
   BlockArgs A = block_args(s, col0_dev, col0_mul, L, step_rule, nprime, stop_check, trace_dev);
   if (L <= 1024 && !s->no_tail) {
-    k_block_tail<<<1, 1024, 0, s->stream>>>(A);
+    CUDA_TRY(s, set_dyn_smem((const void*)k_block_tail, s->device, TAIL_SMEM));
+    k_block_tail<<<1, 1024, TAIL_SMEM, s->stream>>>(A);
     CUDA_TRY(s, cudaGetLastError());
     s->lead->stats.kernel_launches += 1;
   } else {
@@ -974,6 +982,7 @@ sro_status plain_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
     k_pairs_count<<<gL, tpb, 0, s->stream>>>(A);
     k_scan_pairs<<<1, 1024, 0, s->stream>>>(A);
     k_pairs_gen<<<gL, tpb, 0, s->stream>>>(A);
+    k_touched_scan<<<1, 1024, 0, s->stream>>>(A);
     k_runs<<<gP, tpb, 0, s->stream>>>(A, s->pd);
     k_row_tree<0><<<gR, 256, 0, s->stream>>>(A, nullptr, 0);
     k_psum256<<<1, 256, 0, s->stream>>>(s->X, s->m, s->scal + 1, nullptr, nullptr, stop);
@@ -984,7 +993,7 @@ sro_status plain_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
     k_row_tree<1><<<gR, 256, 0, s->stream>>>(A, nullptr, 1);
     k_step_done<<<1, 32, 0, s->stream>>>(A);
     CUDA_TRY(s, cudaGetLastError());
-    s->lead->stats.kernel_launches += 13;
+    s->lead->stats.kernel_launches += 14;
   }
   s->lead->stats.block_steps += 1;
   s->lead->k_pending += 1;
@@ -1019,7 +1028,8 @@ sro_status shard_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
     if (st) return st;
     double* s1 = s->x1 + (size_t)t->shard * s->slot_len;
     if (tail) {
-      k_shard_tail_a<<<1, 1024, 0, s->stream>>>(A);
+      CUDA_TRY(s, set_dyn_smem((const void*)k_shard_tail_a, s->device, TAIL_SMEM));
+      k_shard_tail_a<<<1, 1024, TAIL_SMEM, s->stream>>>(A);
       s->stats.kernel_launches += 1;
     } else {
       k_step_begin<<<1, 256, 0, s->stream>>>(A, s1 + s->m);
@@ -1027,10 +1037,11 @@ sro_status shard_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
       k_scan_pairs<<<1, 1024, 0, s->stream>>>(A);
       k_zero_slot<<<gR, 256, 0, s->stream>>>(A, s1);
       k_pairs_gen<<<gL, tpb, 0, s->stream>>>(A);
+      k_touched_scan<<<1, 1024, 0, s->stream>>>(A);
       k_runs<<<gP, tpb, 0, s->stream>>>(A, t->pd);
       k_row_tree<2><<<gR, 256, 0, s->stream>>>(A, s1, 0);
       k_publish_a<<<1, 32, 0, s->stream>>>(A);
-      s->stats.kernel_launches += 8;
+      s->stats.kernel_launches += 9;
     }
     CUDA_TRY(s, cudaGetLastError());
   }
@@ -1041,7 +1052,8 @@ sro_status shard_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
     BlockArgs& A = AA[q];
     double* s2 = s->x2 + (size_t)t->shard * s->slot_len;
     if (tail) {
-      k_shard_tail_b<<<1, 1024, 0, s->stream>>>(A);
+      CUDA_TRY(s, set_dyn_smem((const void*)k_shard_tail_b, s->device, TAIL_SMEM));
+      k_shard_tail_b<<<1, 1024, TAIL_SMEM, s->stream>>>(A);
       s->stats.kernel_launches += 1;
     } else {
       k_shard_gamma<<<1, 256, 0, s->stream>>>(A);
@@ -1137,7 +1149,8 @@ void free_shard(Solver* s) {
   void* ptrs[] = {s->dsteps, s->phase, s->a, s->b, s->b_full, s->r, s->h, s->cnt, s->srow, s->sval, s->G_ga, s->fen,
                   s->status, s->steps_done, s->stop, s->scal, s->epsd, s->visit, s->trace, s->sw_j, s->sw_min,
                   s->sw_g, s->part_j, s->part_min, s->pcount, s->poff, s->ptotal, s->prow, s->ppos, s->pd,
-                  s->ptold, s->pdelta, s->acc, s->rowcnt, s->X, s->trows, s->ntouch, s->capfail};
+                  s->ptold, s->pdelta, s->runc, s->runv, s->rowcnt, s->rowidx, s->tstart, s->tcur, s->X,
+                  s->trows, s->ntouch, s->capfail};
   for (void* p : ptrs) if (p) cudaFree(p);
   if (s->owns_cost) { if (s->C) cudaFree(s->C); if (s->x) cudaFree(s->x); if (s->y) cudaFree(s->y); }
   for (auto& p : s->pending) { s->ev_pool.push_back(p.a); s->ev_pool.push_back(p.b); }
