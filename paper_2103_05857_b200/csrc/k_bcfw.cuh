@@ -347,24 +347,30 @@ __device__ int ga_draw(const double* fen, const double* G, int n, double u53) {
   int pos = 0;
   int bit = 1 << (31 - __clz(n));   // highest power of two <= n
   // Standard descent (if (pos+bit <= n && fen[pos+bit] <= u) { pos += bit; u -= fen[pos]; }),
-  // two levels per round: both candidates of the second level are loaded with the
-  // first, so the dependent shared-memory loads halve; comparisons and
-  // subtractions are the same operations in the same order.
-  while (bit > 1) {
-    const int b2 = bit >> 1;
-    const double fa = (pos + bit <= n) ? fen[pos + bit] : 0.0;
-    const double f0 = (pos + b2 <= n) ? fen[pos + b2] : 0.0;
-    const double f1 = (pos + bit + b2 <= n) ? fen[pos + bit + b2] : 0.0;
-    const bool t1 = (pos + bit <= n) && fa <= u;
-    const double ua = d_sub(u, fa);
-    if (t1) { pos += bit; u = ua; }
-    const double fb = t1 ? f1 : f0;
-    const bool t2 = (pos + b2 <= n) && fb <= u;
-    const double ub = d_sub(u, fb);
-    if (t2) { pos += b2; u = ub; }
-    bit >>= 2;
+  // three levels per round: the 1 + 2 + 4 candidates of the round are loaded
+  // together, so the dependent shared-memory loads drop to a third; the
+  // comparisons and subtractions are the same operations in the same order.
+  auto ld = [&](int q) { return q <= n ? fen[q] : 0.0; };
+  auto level = [&](int b, double f) {
+    const bool t = (pos + b <= n) && f <= u;
+    const double un = d_sub(u, f);
+    if (t) { pos += b; u = un; }
+    return t;
+  };
+  while (bit >= 4) {
+    const int b2 = bit >> 1, b3 = bit >> 2;
+    const double fa = ld(pos + bit);
+    const double f0 = ld(pos + b2), f1 = ld(pos + bit + b2);
+    const double g00 = ld(pos + b3), g01 = ld(pos + b2 + b3), g10 = ld(pos + bit + b3), g11 = ld(pos + bit + b2 + b3);
+    const bool t1 = level(bit, fa);
+    const bool t2 = level(b2, t1 ? f1 : f0);
+    level(b3, t1 ? (t2 ? g11 : g10) : (t2 ? g01 : g00));
+    bit >>= 3;
   }
-  if (bit == 1 && pos + 1 <= n && fen[pos + 1] <= u) { pos += 1; u = d_sub(u, fen[pos]); }
+  while (bit >= 1) {
+    level(bit, ld(pos + bit));
+    bit >>= 1;
+  }
   if (pos >= n) {
     for (int i = n - 1; i >= 0; i--) if (wpos(G[i]) > 0.0) return i;
     return n - 1;
@@ -377,20 +383,13 @@ __device__ __forceinline__ void ga_add(double* fen, int n, int i0, double delta)
 }
 // Same update with lane t of a warp updating the t-th node of the path (the
 // nodes are distinct, so each node receives exactly the one add it gets above).
-// With x = p - 1 a step p += p & -p sets the lowest zero bit of x, so the t-th
-// node is i0 with its t lowest zero bits set (closed form, no walk).
+// With x = p - 1 a step p += p & -p sets the lowest zero bit of x (x |= x + 1).
 __device__ __forceinline__ void ga_add_warp(double* fen, int n, int i0, double delta) {
   const int lane = threadIdx.x & 31;
-  const unsigned x0 = (unsigned)i0;
-  unsigned x = x0;
-  bool ok = true;
-  if (lane > 0) {
-    const unsigned zb = __fns(~x0, 0, lane);
-    if (zb == 0xffffffffu) ok = false;
-    else x = zb >= 31 ? 0xffffffffu : (x0 | ((2u << zb) - 1u));
-  }
+  unsigned x = (unsigned)i0;
+  for (int t = 0; t < lane && x <= (unsigned)n; t++) x |= x + 1u;
   const long long p = (long long)x + 1;
-  if (ok && p <= n) fen[p] = d_add(fen[p], delta);
+  if (p <= n) fen[p] = d_add(fen[p], delta);
   __syncwarp();
 }
 

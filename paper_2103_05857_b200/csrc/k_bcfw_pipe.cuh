@@ -337,7 +337,9 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_pipe(BcfwArgs A, const
       if (!has_next) break;
       // ---- merge: the rows of T_s with the updated h, and the LMO warp partials
       PW_MARK(3);
+      PW_MARK(2);
       nbar_sync(BAR_PART, PIPE_SYNC);
+      PW_MARK(3);
       unsigned long long ka = ~0ULL;
       int ja = 0x7fffffff;
       if (lane < MT) { ka = okey(d_add(cn, sh_h[trow])); ja = trow; }
@@ -528,13 +530,17 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
       if (lane == 0) ii = ga_draw(fens, Gs, n, u53);
       return __shfl_sync(FULL, ii, 0);
     };
+#ifdef SRO_PHASE_TIMING
+    long long pw_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long pw_t = clock64();
+#endif
     int i = draw(uniform53(rng_u64(A.seed, 1, (uint64_t)A.k0)));
     if (lane == 0) misc[0] = i;
     __syncwarp();
     nbar_arrive(BAR_COL, PIPE_SYNC);
     for (int s = 0; s < steps; s++) {
       const long long kk = A.k0 + s;
-      const double u_next = uniform53(rng_u64(A.seed, 1, (uint64_t)(kk + 1)));   // next draw's uniform, off the critical path
+      PW_MARK(0);
       // the drawn column's slab -> support mask for the LMO warps
       const int c0 = sh_cnt[i];
       const double bi = A.b[i];
@@ -549,6 +555,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
       }
       __syncwarp();
       nbar_arrive(BAR_MASK, PIPE_SYNC);
+      PW_MARK(1);
       const double cw = lane < c0 ? (double)__ldg(Cg + (int64_t)i * ld + rw) : 0.0;
       // ---- partials -> LMO result (j, mv), C_ji, and the minimum outside T = supp U {j}
       const double gk = lane < c0 ? d_add(cw, sh_h[rw]) : 0.0;   // support rows: C + h (old h)
@@ -556,6 +563,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
       int js = lane < c0 ? rw : 0x7fffffff;
       const int wsl = warp_argmin_key(ks, js);
       const double csup = __shfl_sync(FULL, cw, wsl);
+      const double u_next = uniform53(rng_u64(A.seed, 1, (uint64_t)(kk + 1)));   // next draw's uniform (while the LMO warps scan)
       nbar_sync(BAR_PART, PIPE_SYNC);
       unsigned long long k1 = lane < PIPE_LMO_WARPS ? pk[lane] : ~0ULL;
       int r1 = lane < PIPE_LMO_WARPS ? pj[lane] : 0x7fffffff;
@@ -576,6 +584,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
       const unsigned long long kout = sup_wins ? k1 : k2;   // min over rows outside T (old h = new h there)
       const double m_out = kout == ~0ULL ? dinf() : okey_inv(kout);
       // ---- the serial part
+      PW_MARK(4);
       const StepOut o = serial_step<VAR>(A, kk, i, j, mv, bi, c0, rw, tv, gk, sh_r, sh_h, nullptr, sh_a, sh_cnt,
                                          slots, nullptr SP_NULL);
       if (o.ev && o.erow < nvec * W) hpd[pipe_hidx<W>(o.erow, nvec)] = o.hnew;
@@ -594,6 +603,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
         tr[4] = o.dir; tr[5] = o.gamma; tr[6] = o.num; tr[7] = o.den; tr[8] = mv;
       }
       // ---- GA: refresh the visited column's stored gap (Alg. A.4 line 6)
+      PW_MARK(5);
       if (A.ga_inner) {
         double gnew = o.gfw;
         if (A.ga_post) {
@@ -627,18 +637,23 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
         const double delta = d_sub(wpos(gnew), wpos(Gs[i]));
         __syncwarp();
         ga_add_warp(fens, n, i, delta);
+        PW_MARK(6);
         if (lane == 0) Gs[i] = gnew;
         __syncwarp();
       }
       done = s + 1;
       if (s + 1 < steps) {
         i = draw(u_next);
+        PW_MARK(7);
         if (lane == 0) misc[0] = i;
         __syncwarp();
         nbar_arrive(BAR_COL, PIPE_SYNC);
       }
     }
     if (lane == 0) *A.steps_done = done;
+#ifdef SRO_PHASE_TIMING
+    if (lane == 0 && A.phase) for (int q = 0; q < 8; q++) A.phase[q] += pw_acc[q];
+#endif
   }
   __syncthreads();
   for (int k = tid; k < m; k += PIPE_THREADS) { A.h[k] = sh_h[k]; A.r[k] = sh_r[k]; }

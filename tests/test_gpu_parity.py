@@ -289,3 +289,33 @@ def test_block_step_multikernel_path_bitexact(variant, B, monkeypatch):
     rg = g.solve(gv, 40, seed=3, trace=True, step=sro.STEP_ELS, epsilon=1e-9, **kw)
     assert_same_trace(rg["trace"], ro["trace"])
     assert_same_state(g, o)
+
+
+@pytest.mark.parametrize("name,ov,gv,kw", [VARIANTS[0], VARIANTS[3], VARIANTS[4], VARIANTS[5], VARIANTS[8]],
+                         ids=["bcfw", "bcafw", "bcpfw", "ga", "ga-pairwise"])
+def test_config0_register_file_kernel_bitexact(name, ov, gv, kw, monkeypatch):
+    """The register-file persistent kernel k_bcfw_rf (the pipelined kernels forced off):
+    same bit-exact trajectory as the oracle."""
+    monkeypatch.setenv("SRO_NO_PIPE", "1")
+    d = instance(0, seed=0)
+    g, o = pair(d)
+    ro = o.solve(ov, 4 * 256, seed=9, trace=True, epsilon=1e-12, **kw)
+    rg = g.solve(gv, 4 * 256, seed=9, trace=True, epsilon=1e-12, **_gpu_opts(kw))
+    assert_same_trace(rg["trace"], ro["trace"])
+    assert_same_state(g, o)
+
+
+@pytest.mark.parametrize("var,kw", [(BCFW, dict(step=ELS, sampling=U)), (BCPFW, dict(step=ELS, sampling=P)),
+                                    (BCFW, dict(step=ELS, sampling=GA, ga_M=1, ga_inner=1, ga_post_update=1))],
+                         ids=["bcfw-U", "bcpfw-P", "ga"])
+def test_config1_shape_pipelined_kernels_bitexact(var, kw):
+    """The pipelined kernels at the config-[1] row count (m = 4096, three 128-bit vectors per
+    LMO thread, fp32 costs) on fewer columns: every step bit-exact vs the oracle."""
+    d = instance(1, m=4096, n=512, seed=4)
+    d["C32"] = (((d["X"][:, None, :] - d["Y"][None, :, :]) ** 2).sum(-1)).astype(np.float32)
+    g, o = pair(d, prec="f32")
+    gv = {BCFW: sro.SRO_BCFW, BCPFW: sro.SRO_BCPFW}[var]
+    ro = o.solve(var, 6 * 512, seed=2, trace=True, epsilon=1e-9, **kw)
+    rg = g.solve(gv, 6 * 512, seed=2, trace=True, epsilon=1e-9, **_gpu_opts(kw))
+    assert_same_trace(rg["trace"], ro["trace"])
+    assert_same_state(g, o)
