@@ -70,6 +70,8 @@ struct BlockArgs {
   int* tcur;             // touched index -> runs appended so far (zero outside a step)
   int* runc;             // run lists: chunk index
   double* runv;          // run lists: partial sum
+  int* bigw;             // touched indices of rows with more than ROW_SMALL runs
+  int* nbig;             // [2]: their count in the first / second tree of a step
   double* X;             // m: Delta_k^2, zero outside a step
   double* scal;          // [0]=G_U [1]=den [2]=gamma [3]=num
   const double* eps;     // FW stop check (nullptr for batched)
@@ -249,18 +251,80 @@ __device__ __forceinline__ void dev_runs(const BlockArgs& A, const double* __res
   }
 }
 
-// Warp per touched row: scatter its run list into the warp's 256 shared slots
-// (zero outside use), the 256-leaf adjacent-pair tree, clear the slots.
-// MODE 0: X[k] = D^2; MODE 1: r_k += D, h_k = (r_k - a_k)/lambda;
-// MODE 2: slot[k] = D (a shard's subtree). clear: reset the row's counters
-// (last tree of a step).
+// Applies a touched row's combined sum D. MODE 0: X[k] = D^2; MODE 1: r_k += D,
+// h_k = (r_k - a_k)/lambda; MODE 2: slot[k] = D (a shard's subtree). Resets the
+// row's run counter, and its pair count when `clear` (last tree of a step).
 template <int MODE>
-__device__ __forceinline__ void dev_row_tree(const BlockArgs& A, double* slot, bool clear, double* wslots_all) {
+__device__ __forceinline__ void row_finish(const BlockArgs& A, int w, int k, double D, double* slot, bool clear) {
+  if (MODE == 0) {
+    A.X[k] = d_mul(D, D);
+  } else if (MODE == 1) {
+    const double rn = d_add(A.r[k], D);
+    A.r[k] = rn;
+    const double d = d_sub(rn, A.a[k]);
+    A.h[k] = A.lambda == 1.0 ? d : d_div(d, A.lambda);   // x / 1 == x exactly
+    A.X[k] = 0.0;
+  } else {
+    slot[k] = D;
+  }
+  A.tcur[w] = 0;
+  if (clear) A.rowcnt[k] = 0;
+}
+
+constexpr int ROW_SMALL = 8;   // rows with at most this many chunk runs: one thread per row
+
+// The 256-leaf adjacent-pair tree over the K nonzero chunk partials of a row
+// (zero leaves are additive identities): sort by chunk, then K-1 times merge
+// (left + right) the adjacent pair whose lowest common ancestor is lowest —
+// the dense tree's merges, in an order that only swaps independent ones.
+__device__ __forceinline__ double sparse_tree256(int K, int* c, double* v) {
+  for (int a = 1; a < K; a++) {
+    const int cc = c[a];
+    const double vv = v[a];
+    int b = a - 1;
+    while (b >= 0 && c[b] > cc) { c[b + 1] = c[b]; v[b + 1] = v[b]; b--; }
+    c[b + 1] = cc; v[b + 1] = vv;
+  }
+  while (K > 1) {
+    int t = 0, best = 99;
+    for (int u = 0; u + 1 < K; u++) {
+      const int hb = 31 - __clz(c[u] ^ c[u + 1]);
+      if (hb < best) { best = hb; t = u; }
+    }
+    v[t] = d_add(v[t], v[t + 1]);
+    for (int u = t + 1; u + 1 < K; u++) { c[u] = c[u + 1]; v[u] = v[u + 1]; }
+    K--;
+  }
+  return v[0];
+}
+
+// Pass 1, thread per touched row: rows with <= ROW_SMALL runs are combined in
+// registers / local memory; larger ones (hot rows) go to the big list.
+template <int MODE>
+__device__ __forceinline__ void dev_row_tree_small(const BlockArgs& A, double* slot, bool clear, int pass) {
+  const int T = *A.ntouch;
+  for (int w = gtid(); w < T; w += gstride()) {
+    const int k = A.trows[w];
+    const int st = A.tstart[w], K = A.tcur[w];
+    if (K > ROW_SMALL) { A.bigw[atomicAdd(&A.nbig[pass], 1)] = w; continue; }
+    int c[ROW_SMALL];
+    double v[ROW_SMALL];
+    for (int e = 0; e < K; e++) { c[e] = A.runc[st + e]; v[e] = A.runv[st + e]; }
+    row_finish<MODE>(A, w, k, sparse_tree256(K, c, v), slot, clear);
+  }
+}
+
+// Pass 2, warp per big row: scatter its runs into the warp's 256 shared slots
+// (zero outside use), the dense 256-leaf tree, clear the slots.
+template <int MODE>
+__device__ __forceinline__ void dev_row_tree_big(const BlockArgs& A, double* slot, bool clear, int pass,
+                                                 double* wslots_all, bool all_rows = false) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
   double* sl = wslots_all + 256 * warp;
-  const int T = *A.ntouch;
-  for (int w = blockIdx.x * nwarps + warp; w < T; w += gridDim.x * nwarps) {
+  const int NB = all_rows ? *A.ntouch : A.nbig[pass];
+  for (int b = blockIdx.x * nwarps + warp; b < NB; b += gridDim.x * nwarps) {
+    const int w = all_rows ? b : A.bigw[b];
     const int k = A.trows[w];
     const int st = A.tstart[w], K = A.tcur[w];
     for (int e = lane; e < K; e += 32) sl[A.runc[st + e]] = A.runv[st + e];
@@ -272,21 +336,17 @@ __device__ __forceinline__ void dev_row_tree(const BlockArgs& A, double* slot, b
     __syncwarp();
     for (int e = lane; e < K; e += 32) sl[A.runc[st + e]] = 0.0;
     __syncwarp();
-    if (lane == 0) {
-      if (MODE == 0) {
-        A.X[k] = d_mul(D, D);
-      } else if (MODE == 1) {
-        const double rn = d_add(A.r[k], D);
-        A.r[k] = rn;
-        A.h[k] = d_div(d_sub(rn, A.a[k]), A.lambda);
-        A.X[k] = 0.0;
-      } else {
-        slot[k] = D;
-      }
-      A.tcur[w] = 0;
-      if (clear) A.rowcnt[k] = 0;
-    }
+    if (lane == 0) row_finish<MODE>(A, w, k, D, slot, clear);
   }
+}
+
+// Both passes inside one CTA (single-CTA tails).
+template <int MODE>
+__device__ __forceinline__ void dev_row_tree(const BlockArgs& A, double* slot, bool clear, int pass,
+                                             double* wslots_all) {
+  dev_row_tree_small<MODE>(A, slot, clear, pass);
+  __syncthreads();
+  dev_row_tree_big<MODE>(A, slot, clear, pass, wslots_all);
 }
 
 // Chunked pairwise sum (R19) of x[0..L) with W chunks (W = 256: psum256; W =
@@ -403,11 +463,25 @@ __global__ void k_pairs_gen(BlockArgs A) { if (!blk_skip(A)) dev_pairs_gen(A); }
 __global__ void k_runs(BlockArgs A, const double* __restrict__ val) { if (!blk_skip(A)) dev_runs(A, val); }
 __global__ void __launch_bounds__(1024) k_touched_scan(BlockArgs A) { if (!blk_skip(A)) dev_touched_scan(A); }
 template <int MODE>
-__global__ void __launch_bounds__(256) k_row_tree(BlockArgs A, double* slot, int clear) {
+__global__ void __launch_bounds__(256) k_row_tree_small(BlockArgs A, double* slot, int clear, int pass) {
+  if (!blk_skip(A)) dev_row_tree_small<MODE>(A, slot, clear != 0, pass);
+}
+// Warp per touched row over every touched row (the multi-CTA path: one launch).
+template <int MODE>
+__global__ void __launch_bounds__(256) k_row_tree_all(BlockArgs A, double* slot, int clear) {
   __shared__ double wsl[8 * 256];
+  if (blk_skip(A)) return;
   for (int q = threadIdx.x; q < 8 * 256; q += blockDim.x) wsl[q] = 0.0;
   __syncthreads();
-  if (!blk_skip(A)) dev_row_tree<MODE>(A, slot, clear != 0, wsl);
+  dev_row_tree_big<MODE>(A, slot, clear != 0, 0, wsl, true);
+}
+template <int MODE>
+__global__ void __launch_bounds__(256) k_row_tree_big(BlockArgs A, double* slot, int clear, int pass) {
+  __shared__ double wsl[8 * 256];
+  if (blk_skip(A) || A.nbig[pass] == 0) return;
+  for (int q = threadIdx.x; q < 8 * 256; q += blockDim.x) wsl[q] = 0.0;
+  __syncthreads();
+  dev_row_tree_big<MODE>(A, slot, clear != 0, pass, wsl);
 }
 __global__ void k_gamma(BlockArgs A) { if (!blk_skip(A)) dev_gamma(A); }
 __global__ void k_cap_check(BlockArgs A) { if (!blk_skip(A)) dev_cap_check(A); }
@@ -419,7 +493,7 @@ __global__ void k_zero_slot(BlockArgs A, double* slot) { if (!blk_skip(A)) dev_z
 __global__ void __launch_bounds__(256) k_step_begin(BlockArgs A, double* out) {
   if (A.stop && *A.stop) return;
   if (*A.status) return;
-  if (threadIdx.x == 0) { *A.ntouch = 0; if (A.capfail) *A.capfail = 0; }
+  if (threadIdx.x == 0) { *A.ntouch = 0; A.nbig[0] = 0; A.nbig[1] = 0; if (A.capfail) *A.capfail = 0; }
   dev_psumW(A.g, A.L, A.W, out, A.G > 1 ? nullptr : A.eps, A.G > 1 ? nullptr : A.stop);
 }
 
@@ -441,7 +515,7 @@ __global__ void __launch_bounds__(1024, 1) k_block_tail(BlockArgs A) {
   extern __shared__ double tail_slots[];   // 32 warps x 256, zero outside use
   if (*A.status) return;
   for (int q = threadIdx.x; q < 32 * 256; q += blockDim.x) tail_slots[q] = 0.0;
-  if (threadIdx.x == 0) *A.ntouch = 0;
+  if (threadIdx.x == 0) { *A.ntouch = 0; A.nbig[0] = 0; A.nbig[1] = 0; }
   dev_psumW(A.g, A.L, 256, A.scal + 0, A.eps, A.stop);        // G_U (FW: stop check)
   if (A.stop && *A.stop) return;
   dev_pairs_count(A);
@@ -452,7 +526,7 @@ __global__ void __launch_bounds__(1024, 1) k_block_tail(BlockArgs A) {
   dev_touched_scan(A);
   dev_runs(A, A.pd);
   __syncthreads();
-  dev_row_tree<0>(A, nullptr, false, tail_slots);
+  dev_row_tree<0>(A, nullptr, false, 0, tail_slots);
   __syncthreads();
   dev_psumW(A.X, A.m, 256, A.scal + 1, nullptr, nullptr);
   dev_gamma(A);
@@ -464,7 +538,7 @@ __global__ void __launch_bounds__(1024, 1) k_block_tail(BlockArgs A) {
   __syncthreads();
   dev_runs(A, A.pdelta);
   __syncthreads();
-  dev_row_tree<1>(A, nullptr, true, tail_slots);
+  dev_row_tree<1>(A, nullptr, true, 1, tail_slots);
   if (threadIdx.x == 0) atomicAdd(A.dsteps, 1ULL);
 }
 
@@ -581,7 +655,7 @@ __global__ void __launch_bounds__(1024, 1) k_shard_tail_a(BlockArgs A) {
   double* s1 = slot_of(A, A.x1, A.shard);
   if (!(A.stop && *A.stop) && !*A.status) {
     for (int q = threadIdx.x; q < 32 * 256; q += blockDim.x) tail_slots[q] = 0.0;
-    if (threadIdx.x == 0) { *A.ntouch = 0; *A.capfail = 0; }
+    if (threadIdx.x == 0) { *A.ntouch = 0; *A.capfail = 0; A.nbig[0] = 0; A.nbig[1] = 0; }
     dev_psumW(A.g, A.L, A.W, s1 + A.m, nullptr, nullptr);
     dev_pairs_count(A);
     dev_zero_dbl(s1, A.m);
@@ -592,7 +666,7 @@ __global__ void __launch_bounds__(1024, 1) k_shard_tail_a(BlockArgs A) {
     dev_touched_scan(A);
     dev_runs(A, A.pd);
     __syncthreads();
-    dev_row_tree<2>(A, s1, false, tail_slots);
+    dev_row_tree<2>(A, s1, false, 0, tail_slots);
   }
   __syncthreads();
   if (threadIdx.x == 0) s1[A.m + 1] = (double)*A.status;
@@ -618,7 +692,7 @@ __global__ void __launch_bounds__(1024, 1) k_shard_tail_b(BlockArgs A) {
       __syncthreads();
       dev_runs(A, A.pdelta);
       __syncthreads();
-      dev_row_tree<2>(A, s2, true, tail_slots);
+      dev_row_tree<2>(A, s2, true, 1, tail_slots);
     }
   }
   __syncthreads();

@@ -122,6 +122,7 @@ struct Solver {
   int* rowcnt = nullptr;       // m (zero outside a step)
   int *rowidx = nullptr, *tstart = nullptr, *tcur = nullptr;   // touched-row run-list bookkeeping (tcur zero outside a step)
   int* runc = nullptr;         // run lists (P entries)
+  int *bigw = nullptr, *nbig = nullptr;   // hot rows of a step (m), their counts [2]
   double* runv = nullptr;
   double* X = nullptr;         // m (zero outside a step)
   int* trows = nullptr;
@@ -921,6 +922,7 @@ sro_status ensure_block_ws(Solver* s, int64_t L) {
     CUDA_TRY(s, dalloc(&s->trows, s->m)); CUDA_TRY(s, dalloc(&s->ntouch, 1));
     CUDA_TRY(s, dalloc(&s->rowidx, s->m)); CUDA_TRY(s, dalloc(&s->tstart, s->m));
     CUDA_TRY(s, dalloc(&s->tcur, s->m)); CUDA_TRY(s, dalloc(&s->capfail, 1));
+    CUDA_TRY(s, dalloc(&s->bigw, s->m)); CUDA_TRY(s, dalloc(&s->nbig, 2));
     { sro_status e = ws_clean(s); if (e) return e; }
     CUDA_TRY(s, cudaMemsetAsync(s->capfail, 0, sizeof(int), s->stream));
   }
@@ -944,7 +946,7 @@ BlockArgs block_args(Solver* s, const int* col0_dev, int col0_mul, int L, int st
   A.j = s->sw_j; A.minval = s->sw_min; A.g = s->sw_g; A.pcount = s->pcount; A.poff = s->poff; A.ptotal = s->ptotal;
   A.prow = s->prow; A.ppos = s->ppos; A.pd = s->pd; A.ptold = s->G > 1 ? s->ptold : nullptr; A.pdelta = s->pdelta;
   A.rowcnt = s->rowcnt; A.rowidx = s->rowidx; A.trows = s->trows; A.ntouch = s->ntouch; A.X = s->X;
-  A.tstart = s->tstart; A.tcur = s->tcur; A.runc = s->runc; A.runv = s->runv;
+  A.tstart = s->tstart; A.tcur = s->tcur; A.runc = s->runc; A.runv = s->runv; A.bigw = s->bigw; A.nbig = s->nbig;
   A.scal = s->scal; A.eps = stop_check ? s->epsd : nullptr; A.stop = stop_check ? s->stop : nullptr;
   A.status = s->status;
   A.step_rule = step_rule; A.kk = s->lead->k + s->lead->k_pending; A.nprime = nprime; A.trace = trace_dev;
@@ -984,13 +986,13 @@ sro_status plain_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
     k_pairs_gen<<<gL, tpb, 0, s->stream>>>(A);
     k_touched_scan<<<1, 1024, 0, s->stream>>>(A);
     k_runs<<<gP, tpb, 0, s->stream>>>(A, s->pd);
-    k_row_tree<0><<<gR, 256, 0, s->stream>>>(A, nullptr, 0);
+    k_row_tree_all<0><<<gR, 256, 0, s->stream>>>(A, nullptr, 0);
     k_psum256<<<1, 256, 0, s->stream>>>(s->X, s->m, s->scal + 1, nullptr, nullptr, stop);
     k_gamma<<<1, 32, 0, s->stream>>>(A);
     k_cap_check<<<gL, tpb, 0, s->stream>>>(A);
     k_update_cols<<<gL, tpb, 0, s->stream>>>(A);
     k_runs<<<gP, tpb, 0, s->stream>>>(A, s->pdelta);
-    k_row_tree<1><<<gR, 256, 0, s->stream>>>(A, nullptr, 1);
+    k_row_tree_all<1><<<gR, 256, 0, s->stream>>>(A, nullptr, 1);
     k_step_done<<<1, 32, 0, s->stream>>>(A);
     CUDA_TRY(s, cudaGetLastError());
     s->lead->stats.kernel_launches += 14;
@@ -1039,7 +1041,7 @@ sro_status shard_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
       k_pairs_gen<<<gL, tpb, 0, s->stream>>>(A);
       k_touched_scan<<<1, 1024, 0, s->stream>>>(A);
       k_runs<<<gP, tpb, 0, s->stream>>>(A, t->pd);
-      k_row_tree<2><<<gR, 256, 0, s->stream>>>(A, s1, 0);
+      k_row_tree_all<2><<<gR, 256, 0, s->stream>>>(A, s1, 0);
       k_publish_a<<<1, 32, 0, s->stream>>>(A);
       s->stats.kernel_launches += 9;
     }
@@ -1061,7 +1063,7 @@ sro_status shard_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
       k_zero_slot<<<gR, 256, 0, s->stream>>>(A, s2);
       k_update_cols<<<gL, tpb, 0, s->stream>>>(A);
       k_runs<<<gP, tpb, 0, s->stream>>>(A, t->pdelta);
-      k_row_tree<2><<<gR, 256, 0, s->stream>>>(A, s2, 1);
+      k_row_tree_all<2><<<gR, 256, 0, s->stream>>>(A, s2, 1);
       k_publish_b<<<1, 32, 0, s->stream>>>(A);
       s->stats.kernel_launches += 7;
     }
@@ -1150,7 +1152,7 @@ void free_shard(Solver* s) {
                   s->status, s->steps_done, s->stop, s->scal, s->epsd, s->visit, s->trace, s->sw_j, s->sw_min,
                   s->sw_g, s->part_j, s->part_min, s->pcount, s->poff, s->ptotal, s->prow, s->ppos, s->pd,
                   s->ptold, s->pdelta, s->runc, s->runv, s->rowcnt, s->rowidx, s->tstart, s->tcur, s->X,
-                  s->trows, s->ntouch, s->capfail};
+                  s->trows, s->ntouch, s->capfail, s->bigw, s->nbig};
   for (void* p : ptrs) if (p) cudaFree(p);
   if (s->owns_cost) { if (s->C) cudaFree(s->C); if (s->x) cudaFree(s->x); if (s->y) cudaFree(s->y); }
   for (auto& p : s->pending) { s->ev_pool.push_back(p.a); s->ev_pool.push_back(p.b); }
