@@ -200,6 +200,21 @@ sro_status sro_get_rowsums(sro_handle h, double* r);
 /* Back to T^(0), k = 0; clears the variant/options/seed lock. */
 sro_status sro_reset(sro_handle h);
 
+/* Barycentric projection (Eq. 15) of the source colours
+ * through the current plan: xhat_k = (sum_i T_ki y_i) / (sum_i T_ki), both sums
+ * over the n columns as the 256-chunk pairwise sums of DESIGN.md R19; a row
+ * without mass keeps x_k. x: host fp64 m x 3 (source colours),
+ * y: host fp64 n x 3 (target colours), xhat: host fp64 m x 3 (output).
+ * Unsharded handles only (INVALID_ARG otherwise). Errors: INVALID_ARG, CUDA, OOM. */
+sro_status sro_barycentric(sro_handle h, const double* x, const double* y, double* xhat);
+
+/* Evaluation metrics of P:415-421 on the current plan: *e_c = ||T 1_n - a||_2 +
+ * ||T^T 1_m - b||_2 (metric iii; row sums as in sro_barycentric, column sums over
+ * each support rows ascending, each norm the square root of a 256-chunk sum of
+ * squares), *sparsity = ratio of zero entries of T (metric iv), *lin = <T, C>
+ * (the plan's value in metric vi). Unsharded handles only. */
+sro_status sro_metrics(sro_handle h, double* e_c, double* sparsity, double* lin);
+
 /* Global indices (ascending) of the columns this handle holds: cols host
  * int32[n_held] or NULL; *n_held receives the count (n when unsharded). */
 sro_status sro_held_columns(sro_handle h, int32_t* cols, int32_t* n_held);

@@ -76,6 +76,8 @@ def _L():
         _lib.or_gap_thm2.argtypes = [vp, ct.POINTER(d)]
         _lib.or_lagrangian_dual.argtypes = [vp, ct.POINTER(d)]
         _lib.or_objective.argtypes = [vp, ct.POINTER(d)]
+        _lib.or_barycentric.argtypes = [vp, vp, vp, vp]
+        _lib.or_metrics.argtypes = [vp, ct.POINTER(d), ct.POINTER(d), ct.POINTER(d)]
         _lib.or_get_plan_dense.argtypes = [vp, vp]
         _lib.or_get_plan_coo.argtypes = [vp, vp, vp, vp, i64, ct.POINTER(i64)]
         _lib.or_get_r.argtypes = [vp, vp]
@@ -224,6 +226,24 @@ class Oracle:
         f = ct.c_double()
         _L().or_objective(self.h, ct.byref(f))
         return f.value
+
+    def barycentric(self, X, Y):
+        """Eq. 15: new source colours (m x 3); rows without mass keep X."""
+        X = np.ascontiguousarray(X, dtype=np.float64)
+        Y = np.ascontiguousarray(Y, dtype=np.float64)
+        out = np.empty((self.m, 3))
+        st = _L().or_barycentric(self.h, _p(X), _p(Y), _p(out))
+        if st:
+            raise OracleError(st, "barycentric")
+        return out
+
+    def metrics(self):
+        """(e_c, sparsity, <T, C>) — metrics (iii), (iv) and the <T,C> of (vi), P:415-421."""
+        e, sp, lin = ct.c_double(), ct.c_double(), ct.c_double()
+        st = _L().or_metrics(self.h, ct.byref(e), ct.byref(sp), ct.byref(lin))
+        if st:
+            raise OracleError(st, "metrics")
+        return e.value, sp.value, lin.value
 
     def plan(self):
         T = np.empty(self.m * self.n)

@@ -330,6 +330,69 @@ int or_objective(or_state* s, double* f) {
   return OR_OK;
 }
 
+/* dense copy of row k of T (columns 0..n-1; exact zeros off the support) */
+static void plan_row(const or_state* s, int32_t k, double* row) {
+  for (int32_t i = 0; i < s->n; i++) {
+    row[i] = 0.0;
+    for (int32_t p = 0; p < s->cnt[i]; p++)
+      if (s->rows[(int64_t)i * s->cap + p] == k) row[i] = s->vals[(int64_t)i * s->cap + p];
+  }
+}
+
+/* Barycentric projection, Eq. 15; zero rows keep x_k. */
+int or_barycentric(or_state* s, const double* X, const double* Y, double* xhat) {
+  double* row = (double*)malloc(sizeof(double) * (size_t)s->n);
+  double* tmp = (double*)malloc(sizeof(double) * (size_t)s->n);
+  if (!row || !tmp) { free(row); free(tmp); return OR_ERR_ARG; }
+  for (int32_t k = 0; k < s->m; k++) {
+    plan_row(s, k, row);
+    double den = or_chunk_tree_sum(row, s->n, 256);               /* sum_i T_ki */
+    for (int d = 0; d < 3; d++) {
+      if (den == 0.0) { xhat[3 * (int64_t)k + d] = X[3 * (int64_t)k + d]; continue; }
+      for (int32_t i = 0; i < s->n; i++) tmp[i] = row[i] * Y[3 * (int64_t)i + d];
+      double num = or_chunk_tree_sum(tmp, s->n, 256);             /* sum_i T_ki y_id */
+      xhat[3 * (int64_t)k + d] = num / den;
+    }
+  }
+  free(row); free(tmp);
+  return OR_OK;
+}
+
+/* Metrics (iii), (iv) and <T, C> of (vi). */
+int or_metrics(or_state* s, double* e_c, double* sparsity, double* lin) {
+  const int32_t mx = s->m > s->n ? s->m : s->n;
+  double* row = (double*)malloc(sizeof(double) * (size_t)s->n);
+  double* sq = (double*)malloc(sizeof(double) * (size_t)mx);
+  if (!row || !sq) { free(row); free(sq); return OR_ERR_ARG; }
+  for (int32_t k = 0; k < s->m; k++) {                            /* (T 1 - a)_k^2 */
+    plan_row(s, k, row);
+    double rk = or_chunk_tree_sum(row, s->n, 256);
+    double d = rk - s->a[k];
+    sq[k] = d * d;
+  }
+  double e1 = sqrt(or_chunk_tree_sum(sq, s->m, 256));
+  int64_t nnz = 0;
+  for (int32_t i = 0; i < s->n; i++) {                            /* (T^T 1 - b)_i^2 */
+    double ci = 0.0;
+    for (int32_t p = 0; p < s->cnt[i]; p++) ci = ci + s->vals[(int64_t)i * s->cap + p];
+    nnz += s->cnt[i];
+    double d = ci - s->b[i];
+    sq[i] = d * d;
+  }
+  double e2 = sqrt(or_chunk_tree_sum(sq, s->n, 256));
+  *e_c = e1 + e2;
+  *sparsity = 1.0 - (double)nnz / ((double)s->m * (double)s->n);
+  for (int32_t i = 0; i < s->n; i++) {                            /* <t_i, c_i>, rows ascending */
+    double acc = 0.0;
+    for (int32_t p = 0; p < s->cnt[i]; p++)
+      acc = acc + s->vals[(int64_t)i * s->cap + p] * cost(s, s->rows[(int64_t)i * s->cap + p], i);
+    sq[i] = acc;
+  }
+  *lin = or_chunk_tree_sum(sq, s->n, 256);
+  free(row); free(sq);
+  return OR_OK;
+}
+
 int or_gap(or_state* s, double* total, double* per_column, int32_t* argmin_rows, double* minvals) {
   return gap_sweep(s, total, per_column, argmin_rows, minvals);
 }

@@ -73,6 +73,15 @@ int or_gap(or_state* s, double* total, double* per_column, int32_t* argmin_rows,
 int or_gap_thm2(or_state* s, double* g);           /* Thm 2 form */
 int or_lagrangian_dual(or_state* s, double* w);    /* App. D */
 int or_objective(or_state* s, double* f);
+/* Barycentric projection (Eq. 15): xhat_k = (sum_i T_ki y_i) / (sum_i T_ki) for
+ * every row with mass; a row without mass keeps x_k. Both sums run over the n columns
+ * as R19's 256-chunk pairwise sum over column positions. X: m x 3, Y: n x 3, xhat: m x 3. */
+int or_barycentric(or_state* s, const double* X, const double* Y, double* xhat);
+/* Metrics (iii), (iv) and the <T, C> of (vi): e_c = ||T 1 - a||_2 + ||T^T 1 - b||_2
+ * (row sums as in or_barycentric, column sums over the support rows ascending, each norm the
+ * square root of a 256-chunk sum of squares); sparsity = 1 - nnz(T) / (m n);
+ * lin = 256-chunk sum over columns of <t_i, c_i>. */
+int or_metrics(or_state* s, double* e_c, double* sparsity, double* lin);
 int or_get_plan_dense(or_state* s, double* T);     /* m*n column-major */
 int or_get_plan_coo(or_state* s, int32_t* rows, int32_t* cols, double* vals, int64_t cap, int64_t* nnz);
 int or_get_r(or_state* s, double* r);

@@ -30,6 +30,7 @@
 #include "k_bcfw.cuh"
 #include "k_bcfw_pipe.cuh"
 #include "k_block.cuh"
+#include "k_plan.cuh"
 #include "k_sweep.cuh"
 #include "sro_device.cuh"
 
@@ -1595,6 +1596,113 @@ sro_status sro_get_plan(sro_handle h, double* dense, int32_t* rows, int32_t* col
   }
   if (nnz) *nnz = q;
   if (rows && cols && vals && q > cap) { s->err = "COO capacity too small"; return SRO_ERR_CAPACITY; }
+  return SRO_OK;
+}
+
+}  // extern "C"
+
+namespace {
+// Per-row sums over the n columns of the plan (R19 shape), for channel d = -1
+// (sum_i T_ki) and d = 0..2 (sum_i T_ki y_id); out[c] device arrays of length m.
+sro_status plan_row_sums(Solver* s, const double* y_dev, const int* chans, int nch, double** out) {
+  sro_status st = ensure_block_ws(s, s->n);
+  if (st) return st;
+  BlockArgs A = block_args(s, nullptr, 0, s->n, 0, 1, false, nullptr);
+  const int tpb = 256;
+  int gL = (s->n + tpb - 1) / tpb; if (gL > s->num_sms * 8) gL = s->num_sms * 8;
+  const int gP = s->num_sms * 8;
+  const int gR = (s->m + 7) / 8 < s->num_sms * 8 ? (s->m + 7) / 8 : s->num_sms * 8;
+  k_plan_begin<<<1, 32, 0, s->stream>>>(A);
+  k_plan_pairs_count<<<gL, tpb, 0, s->stream>>>(A);
+  k_scan_pairs<<<1, 1024, 0, s->stream>>>(A);
+  k_plan_pairs_gen<<<gL, tpb, 0, s->stream>>>(A);
+  k_touched_scan<<<1, 1024, 0, s->stream>>>(A);
+  for (int c = 0; c < nch; c++) {
+    CUDA_TRY(s, cudaMemsetAsync(out[c], 0, sizeof(double) * s->m, s->stream));
+    k_plan_channel<<<gP, tpb, 0, s->stream>>>(A, y_dev, chans[c], s->pdelta);
+    k_runs<<<gP, tpb, 0, s->stream>>>(A, s->pdelta);
+    k_row_tree_all<2><<<gR, 256, 0, s->stream>>>(A, out[c], c == nch - 1 ? 1 : 0);
+  }
+  s->lead->stats.kernel_launches += 5 + 3 * nch;
+  CUDA_TRY(s, cudaGetLastError());
+  return SRO_OK;
+}
+}  // namespace
+
+extern "C" {
+
+sro_status sro_barycentric(sro_handle h, const double* x, const double* y, double* xhat) {
+  if (!h || !x || !y || !xhat) return SRO_ERR_INVALID_ARG;
+  Solver* s = static_cast<Solver*>(h);
+  cudaSetDevice(s->device);
+  if (s->G > 1) { s->err = "sro_barycentric: unsharded handles only"; return SRO_ERR_INVALID_ARG; }
+  const int m = s->m, n = s->n;
+  double *buf = nullptr;
+  CUDA_TRY(s, dalloc(&buf, (size_t)4 * m + 3 * (size_t)m + 3 * (size_t)n + 3 * (size_t)m));
+  double* sums[4] = {buf, buf + m, buf + 2 * (size_t)m, buf + 3 * (size_t)m};
+  double* xd = buf + 4 * (size_t)m;
+  double* yd = xd + 3 * (size_t)m;
+  double* xo = yd + 3 * (size_t)n;
+  sro_status st = SRO_OK;
+  do {
+    if (cudaMemcpyAsync(xd, x, sizeof(double) * 3 * m, cudaMemcpyHostToDevice, s->stream) != cudaSuccess ||
+        cudaMemcpyAsync(yd, y, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s->stream) != cudaSuccess) {
+      s->err = "barycentric upload failed"; st = SRO_ERR_CUDA; break;
+    }
+    const int chans[4] = {-1, 0, 1, 2};
+    st = plan_row_sums(s, yd, chans, 4, sums);
+    if (st) break;
+    k_plan_project<<<(m + 255) / 256, 256, 0, s->stream>>>(m, sums[0], sums[1], sums[2], sums[3], xd, xo);
+    s->stats.kernel_launches += 1;
+    if (cudaMemcpyAsync(xhat, xo, sizeof(double) * 3 * m, cudaMemcpyDeviceToHost, s->stream) != cudaSuccess ||
+        cudaStreamSynchronize(s->stream) != cudaSuccess) {
+      s->err = "barycentric failed"; st = SRO_ERR_CUDA; break;
+    }
+  } while (0);
+  cudaFree(buf);
+  return st;
+}
+
+sro_status sro_metrics(sro_handle h, double* e_c, double* sparsity, double* lin) {
+  if (!h || !e_c || !sparsity || !lin) return SRO_ERR_INVALID_ARG;
+  Solver* s = static_cast<Solver*>(h);
+  cudaSetDevice(s->device);
+  if (s->G > 1) { s->err = "sro_metrics: unsharded handles only"; return SRO_ERR_INVALID_ARG; }
+  const int m = s->m, n = s->n;
+  double* buf = nullptr;
+  CUDA_TRY(s, dalloc(&buf, (size_t)m + (size_t)(m > n ? m : n)));
+  double* rs = buf;
+  double* sq = buf + m;
+  sro_status st = SRO_OK;
+  double e1 = 0.0, e2 = 0.0;
+  std::vector<int> hc(n);
+  do {
+    const int chans[1] = {-1};
+    st = plan_row_sums(s, nullptr, chans, 1, &rs);
+    if (st) break;
+    k_plan_sq_rows<<<(m + 255) / 256, 256, 0, s->stream>>>(m, rs, s->a, sq);
+    k_psum256<<<1, 256, 0, s->stream>>>(sq, m, s->scal + 4, nullptr, nullptr, nullptr);
+    k_plan_sq_cols<<<(n + 255) / 256, 256, 0, s->stream>>>(n, s->cap, s->cnt, s->sval, s->b, sq);
+    k_psum256<<<1, 256, 0, s->stream>>>(sq, n, s->scal + 5, nullptr, nullptr, nullptr);
+    s->stats.kernel_launches += 4;
+    if (cudaMemcpyAsync(&e1, s->scal + 4, sizeof(double), cudaMemcpyDeviceToHost, s->stream) != cudaSuccess ||
+        cudaMemcpyAsync(&e2, s->scal + 5, sizeof(double), cudaMemcpyDeviceToHost, s->stream) != cudaSuccess ||
+        cudaMemcpyAsync(hc.data(), s->cnt, sizeof(int) * n, cudaMemcpyDeviceToHost, s->stream) != cudaSuccess) {
+      s->err = "metrics failed"; st = SRO_ERR_CUDA; break;
+    }
+    double f = 0.0;
+    st = objective_dev(s, &f);   // leaves psum256_i <t_i, c_i> in scal[4] (synchronises)
+    if (st) break;
+    if (cudaMemcpy(lin, s->scal + 4, sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess) {
+      s->err = "metrics failed"; st = SRO_ERR_CUDA; break;
+    }
+  } while (0);
+  cudaFree(buf);
+  if (st) return st;
+  int64_t nnz = 0;
+  for (int v : hc) nnz += v;
+  *e_c = std::sqrt(e1) + std::sqrt(e2);
+  *sparsity = 1.0 - (double)nnz / ((double)m * (double)n);
   return SRO_OK;
 }
 

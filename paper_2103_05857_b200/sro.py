@@ -27,7 +27,7 @@ PRECS = {"f64": 0, "f32": 1}
 OK, NOT_CONVERGED = 0, 1
 EXPORTED_SYMBOLS = ("sro_create", "sro_solve", "sro_gap", "sro_objective", "sro_get_plan", "sro_get_rowsums",
                     "sro_reset", "sro_destroy", "sro_last_error", "sro_version", "sro_get_stats", "sro_set_timing",
-                    "sro_held_columns", "sro_nccl_unique_id")
+                    "sro_held_columns", "sro_nccl_unique_id", "sro_barycentric", "sro_metrics")
 
 _STATUS = {0: "OK", 1: "NOT_CONVERGED", 2: "ERR_INVALID_ARG", 3: "ERR_DIMENSION", 4: "ERR_MARGINALS",
            5: "ERR_NONFINITE", 6: "ERR_CAPACITY", 7: "ERR_CUDA", 8: "ERR_NCCL", 9: "ERR_OOM", 10: "ERR_STATE"}
@@ -118,6 +118,10 @@ def load_library():
         L.sro_held_columns.restype = ct.c_int
         L.sro_nccl_unique_id.argtypes = [vp]
         L.sro_nccl_unique_id.restype = ct.c_int
+        L.sro_barycentric.argtypes = [vp, vp, vp, vp]
+        L.sro_barycentric.restype = ct.c_int
+        L.sro_metrics.argtypes = [vp, ct.POINTER(d), ct.POINTER(d), ct.POINTER(d)]
+        L.sro_metrics.restype = ct.c_int
         _lib = L
     return _lib
 
@@ -256,6 +260,21 @@ class Solver:
         v = np.empty(k)
         self._check(self._L.sro_get_plan(self.h, None, _ptr(r), _ptr(c), _ptr(v), k, ct.byref(nnz)))
         return r, c, v
+
+    def barycentric(self, X, Y):
+        """Eq. 15: new source colours (m x 3); rows without mass keep X."""
+        X = np.ascontiguousarray(X, dtype=np.float64)
+        Y = np.ascontiguousarray(Y, dtype=np.float64)
+        assert X.shape == (self.m, 3) and Y.shape == (self.n, 3)
+        out = np.empty((self.m, 3))
+        self._check(self._L.sro_barycentric(self.h, _ptr(X), _ptr(Y), _ptr(out)))
+        return out
+
+    def metrics(self):
+        """(e_c, sparsity, <T, C>): metrics (iii), (iv) and the plan value of (vi)."""
+        e, sp, lin = ct.c_double(), ct.c_double(), ct.c_double()
+        self._check(self._L.sro_metrics(self.h, ct.byref(e), ct.byref(sp), ct.byref(lin)))
+        return e.value, sp.value, lin.value
 
     def rowsums(self):
         r = np.empty(self.m)
