@@ -216,7 +216,7 @@ def roofline_from_stats(stats, peaks):
         # one fp32 column (m entries x 4 B) per BCFW step, + its support, per launch
         bytes_ = stats["bcfw_steps"] * M * 4.0
         launches = max(1, stats["bcfw_launches"])
-        name = "k_bcfw (persistent sequential BCFW-family loop, 1 CTA)"
+        name = "k_bcfw_pipe / k_bcfw_ga_pipe (persistent sequential BCFW-family loop, 1 CTA)"
     elif dom == "sweep":
         bytes_ = stats["sweep_columns"] * M * 4.0
         launches = max(1, stats["sweep_launches"])
@@ -236,8 +236,9 @@ def roofline_from_stats(stats, peaks):
         # the sequential family is bound by the latency of one dependent step, not by HBM:
         # DRAM traffic per launch = algorithmic bytes (profiles/r01_ncu_bcfw_rf.md)
         us = t_ms * 1e3 / stats["bcfw_steps"]
-        out["traffic"] = round((68.372224e6 + 2.112512e6) / 4096 * (bytes_ / launches) / (M * 4.0), 1)
-        out["traffic_source"] = "ncu --set full dram__bytes_read+write of k_bcfw_rf (68.37+2.11 MB per 4096-step launch)"
+        out["traffic"] = round((68.409856e6 + 1.813504e6) / 4096 * (bytes_ / launches) / (M * 4.0), 1)
+        out["traffic_source"] = ("ncu --set full dram__bytes_read+write of k_bcfw_pipe (68.41+1.81 MB per 4096-step "
+                                 "launch, profiles/r01_ncu_bcfw_pipe.md)")
         out["step_latency"] = {"us_per_step": round(us, 4), "cycles_per_step_at_1965MHz": round(us * 1965.0, 1),
                                "single_cta_floor_cycles": 420,
                                "floor_source": "profiles/r01_lmo_microbench.log: register LMO + REDUX argmin + 2 barriers"}

@@ -1,0 +1,9 @@
+"""Two gap sweeps at config [3] (for an ncu capture of k_lmo_sweep_bulk)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2103_05857_b200 as sro  # noqa: E402
+from sro_inputs import instance  # noqa: E402
+d = instance(3, seed=0)
+s = sro.Solver(d["a"], d["b"], 1.0, cost="hash", hash_seed=d["hash_seed"])
+for _ in range(2):
+    print(s.gap()[0])
