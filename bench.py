@@ -8,7 +8,9 @@ histogram marginals, squared-Euclidean cost materialised in fp32 (promoted to fp
 lambda = 1. One step = one pass of the whole hot path (every SURVEY §8(a) row) over
 that instance: BCFW-P-ELS, BCAFW, BCPFW and BCFW-GA (the paper's BCFW + three fast
 variants) plus full FW (Alg. A.1) and batched BCFW (B = 256), each from T^(0) to
-g <= 1e-6. value = cost entries scanned by all LMO calls / device time.
+g <= 1e-6. The six solves are independent and run concurrently (one handle and CUDA stream
+each; a sequential solve is one persistent CTA); --serial-solves runs them one after
+another. value = cost entries scanned by all LMO calls / device time of the step.
 
 N > 1 (torchrun): the sequential BCFW family does not shard (each step depends on
 the previous r), so ranks are independent replicas on their own seeded instances
@@ -107,27 +109,98 @@ def make_instance(seed):
 
 
 # --------------------------------------------------------------------------- CUDA path
-def run_step(solver, entries_acc, ttg):
-    import paper_2103_05857_b200 as sro
-    for name, variant, opts, cap in PLAN:
-        solver.reset()
-        r = solver.solve(variant, cap, seed=11, epsilon=EPS, **opts)
-        if not r["converged"]:
-            raise RuntimeError(f"{name} did not reach g <= {EPS} within {cap} iterations (gap {r['gap']})")
-        entries_acc.append(r["entries_scanned"])
-        ttg[name] = ttg.get(name, []) + [r["device_ms"]]
-    _ = sro
+class StepRunner:
+    """One step = the six solves of PLAN from T^(0) to g <= EPS on one instance. Each solve has
+    its own Solver handle and CUDA stream and all six run concurrently from host threads (the
+    C-ABI calls release the GIL): a sequential BCFW-family solve is one persistent CTA (one SM,
+    bound by the latency of its dependent steps), so independent solves share the GPU
+    instead of queueing. The cost matrix is ONE device copy borrowed by every handle (column-major,
+    ld = m), so the L2 holds it once."""
+
+    def __init__(self, d, dev, Cd, concurrent=True):
+        import torch
+        import paper_2103_05857_b200 as sro
+        self.torch = torch
+        self.concurrent = concurrent
+        self.streams = [torch.cuda.Stream(dev) for _ in PLAN]
+        self.solvers = [sro.Solver(d["a"], d["b"], 1.0, C=Cd, prec="f32", device=dev.index, stream=st.cuda_stream,
+                                   ld=M) for st in self.streams]
+
+    def run(self, entries_acc, ttg):
+        """Enqueue the step after the current stream's pending work; returns after it completes.
+        Device time: (e0 on the caller's stream) ... (e1 after every solver stream)."""
+        torch = self.torch
+        main = torch.cuda.current_stream()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(main)
+        for st in self.streams:
+            st.wait_event(e0)
+        results = [None] * len(PLAN)
+        errors = []
+
+        def work(q):
+            try:
+                name, variant, opts, cap = PLAN[q]
+                s = self.solvers[q]
+                s.reset()
+                results[q] = s.solve(variant, cap, seed=11, epsilon=EPS, **opts)
+            except Exception as e:  # noqa: BLE001
+                errors.append(e)
+
+        if self.concurrent:
+            threads = [threading.Thread(target=work, args=(q,)) for q in range(len(PLAN))]
+            for t in threads:
+                t.start()
+            for t in threads:
+                t.join()
+        else:
+            for q in range(len(PLAN)):
+                work(q)
+        if errors:
+            raise errors[0]
+        for st in self.streams:
+            ev = torch.cuda.Event()
+            ev.record(st)
+            main.wait_event(ev)
+        e1.record(main)
+        e1.synchronize()
+        for (name, _, _, cap), r in zip(PLAN, results):
+            if not r["converged"]:
+                raise RuntimeError(f"{name} did not reach g <= {EPS} within {cap} iterations (gap {r['gap']})")
+            entries_acc.append(r["entries_scanned"])
+            ttg[name] = ttg.get(name, []) + [r["device_ms"]]
+        return e0.elapsed_time(e1)
+
+    def objective(self):
+        return [s.objective() for s in self.solvers]
+
+    def stats(self, reset=False):
+        tot = {}
+        for s in self.solvers:
+            for k, v in s.stats(reset).items():
+                tot[k] = tot.get(k, 0) + v
+        return tot
+
+    def set_timing(self, on):
+        for s in self.solvers:
+            s.set_timing(on)
+
+    def close(self):
+        for s in self.solvers:
+            s.close()
 
 
 def bench_sro(args, rank, world, local_rank):
     import torch
-    import paper_2103_05857_b200 as sro
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     stream = torch.cuda.current_stream(dev)
     d = make_instance(seed=rank)
-    solver = sro.Solver(d["a"], d["b"], 1.0, C=d["C32"], prec="f32", device=local_rank, stream=stream.cuda_stream)
+    C32 = torch.from_numpy(np.ascontiguousarray(d["C32"].T)).pin_memory()   # column-major (n, m)
+    Cd = C32.to(dev)
+    runner = StepRunner(d, dev, Cd, concurrent=not args.serial_solves)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
 
     def barrier():
@@ -137,10 +210,10 @@ def bench_sro(args, rank, world, local_rank):
 
     # warm-up
     for _ in range(args.warmup):
-        run_step(solver, [], {})
+        runner.run([], {})
     torch.cuda.synchronize()
-    solver.stats(reset=True)
-    solver.set_timing(True)
+    runner.stats(reset=True)
+    runner.set_timing(True)
     entries, ttg = [], {}
     step_ms = []
     clocks = ClockSampler(local_rank)
@@ -149,23 +222,18 @@ def bench_sro(args, rank, world, local_rank):
     clocks.start()
     for _ in range(args.steps):
         flush.fill_(1.0)                      # L2 flushed between timed steps (outside the events)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        run_step(solver, entries, ttg)
-        e1.record(stream)
-        e1.synchronize()
-        step_ms.append(e0.elapsed_time(e1))
+        step_ms.append(runner.run(entries, ttg))
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
-    stats = solver.stats(reset=True)
-    solver.set_timing(False)
+    stats = runner.stats(reset=True)
+    runner.set_timing(False)
+    runner.close()
     total_ms = float(sum(step_ms))
     my_entries = float(sum(entries))
 
-    # e2e: same step through the public API from pinned host buffers, H2D + D2H inside
-    C32 = torch.from_numpy(np.ascontiguousarray(d["C32"].T)).pin_memory()   # column-major
+    # e2e: the same step through the public API from pinned host buffers: H2D of C, a, b and
+    # handle creation inside the timed region, D2H of every solve's objective at the end
     a_h = torch.from_numpy(d["a"]).pin_memory()
     b_h = torch.from_numpy(d["b"]).pin_memory()
     e2e_ms, e2e_entries = [], []
@@ -173,19 +241,20 @@ def bench_sro(args, rank, world, local_rank):
         flush.fill_(1.0)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        Cd = C32.to(dev, non_blocking=True)
-        s2 = sro.Solver(a_h.numpy(), b_h.numpy(), 1.0, C=Cd, prec="f32", device=local_rank,
-                        stream=stream.cuda_stream, ld=M)
+        Cd2 = C32.to(dev, non_blocking=True)
+        d2 = dict(d, a=a_h.numpy(), b=b_h.numpy())
+        r2 = StepRunner(d2, dev, Cd2, concurrent=not args.serial_solves)
         ent = []
-        run_step(s2, ent, {})
-        f = s2.objective()                     # D2H of the step's result
-        s2.close()
+        r2.run(ent, {})
+        fs = r2.objective()                    # D2H of the step's results
+        r2.close()
         torch.cuda.synchronize()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
         e2e_entries.append(sum(ent))
-        assert np.isfinite(f)
+        assert np.all(np.isfinite(fs))
+        del Cd2
     h2d = C32.numel() * 4 + a_h.numel() * 8 + b_h.numel() * 8
-    d2h = 8 * len(PLAN) * 4 + 8      # per-solve result scalars + objective
+    d2h = (8 * 4 + 8) * len(PLAN)      # per-solve result scalars + objective
 
     if world > 1:
         import torch.distributed as dist
@@ -199,12 +268,13 @@ def bench_sro(args, rank, world, local_rank):
         e2e_max_ms, e2e_all_entries = sum(e2e_ms), sum(e2e_entries)
     sweep_rf = None
     if rank == 0 and not args.no_sweep_check:
-        del flush
+        del flush, Cd
         torch.cuda.synchronize()
         sweep_rf = sweep_roofline_config3(local_rank, measured_peaks())
     return dict(max_ms=max_ms, all_entries=all_entries, stats=stats, clocks=clk, ttg=ttg, step_ms=step_ms,
                 sweep_roofline=sweep_rf,
-                e2e_value=e2e_all_entries / (e2e_max_ms * 1e-3), h2d=h2d, d2h=d2h, instance=d)
+                e2e_value=e2e_all_entries / (e2e_max_ms * 1e-3), h2d=h2d, d2h=d2h, instance=d,
+                e2e_ms=[round(x, 2) for x in e2e_ms])
 
 
 def roofline_from_stats(stats, peaks):
@@ -352,6 +422,7 @@ def config_block(world):
                         "density marginals), squared-Euclidean C materialised fp32 -> fp64, lambda=1",
             "m": M, "n": N, "lambda": 1.0, "epsilon": EPS, "cost_storage": "f32",
             "variants": [p[0] for p in PLAN], "replicas": world, "parallelism": f"replicas{world}",
+            "solves": "the six solves of a step run concurrently, one stream and handle each (--serial-solves: one after another)",
             "l2": "flushed between timed steps (256 MiB write outside the timed events)",
             "global_batch": world, "seq_len": None}
 
@@ -363,6 +434,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="sro", choices=["sro", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--serial-solves", action="store_true",
+                    help="run the six solves of a step one after another instead of concurrently")
     ap.add_argument("--no-sweep-check", action="store_true",
                     help="skip the config-[3] HBM sweep measurement (sweep_roofline)")
     args = ap.parse_args()
@@ -382,17 +455,21 @@ def main():
         peaks = measured_peaks()
         value = res["all_entries"] / (res["max_ms"] * 1e-3)
         ttg = {k: round(statistics.median(v), 3) for k, v in res["ttg"].items()}
+        cfg = config_block(world)
+        cfg["host_cpus"] = {"os_cpu_count": os.cpu_count(), "affinity": cpu_cores()}
+        if args.serial_solves:
+            cfg["solves"] = "the six solves of a step run one after another on one stream each"
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": res["max_ms"] / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": config_block(world),
+                "config": cfg,
                 "time_to_gap_ms": ttg,
                 "gb_per_s_equiv": round(value * 4 / 1e9, 3),
                 "roofline": roofline_from_stats(res["stats"], peaks),
                 "sweep_roofline": res.get("sweep_roofline"),
                 "clocks": res["clocks"],
                 "e2e": {"value": res["e2e_value"], "unit": UNIT, "h2d_bytes_per_step": res["h2d"],
-                        "d2h_bytes_per_step": res["d2h"]},
+                        "d2h_bytes_per_step": res["d2h"], "ms_per_step": res["e2e_ms"]},
                 "gpu_launches": int(res["stats"]["kernel_launches"])}
         if world == 1 and not args.no_cpu_baseline:
             e, t, done = oracle_sample(res["instance"], epochs=3)

@@ -336,7 +336,7 @@ __device__ __forceinline__ void warp_argmax_redux(double& v, int& j, bool valid)
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ double wpos(double g) { return g > 0.0 ? g : 0.0; }
 
-__device__ int ga_draw(const double* fen, const double* G, int n, double u53) {
+__device__ __forceinline__ int ga_draw(const double* fen, const double* G, int n, double u53) {
   double W = 0.0;
   for (int p = n; p > 0; p -= p & -p) W = d_add(W, fen[p]);
   if (!(W > 0.0)) {

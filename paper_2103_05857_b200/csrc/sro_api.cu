@@ -72,6 +72,7 @@ struct Solver {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev_sync = nullptr;   // blocking-sync event: host waits yield the CPU instead of spinning
   std::string err;
   // problem
   double *a = nullptr, *b = nullptr;
@@ -255,6 +256,39 @@ cudaError_t occupancy(const void* f, int dev, int threads, size_t smem, int* per
 template <typename T>
 cudaError_t dalloc(T** p, size_t count) {
   return cudaMalloc((void**)p, sizeof(T) * (count ? count : 1));
+}
+// Wait for the solver stream with a blocking-sync event (several handles may
+// run concurrently from host threads: a spinning wait would starve the
+// threads that are launching kernels).
+cudaError_t stream_wait(Solver* s) {
+  Solver* L = s->lead;
+  if (!L->ev_sync) {
+    cudaError_t e = cudaEventCreateWithFlags(&L->ev_sync, cudaEventBlockingSync | cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  }
+  cudaError_t e = cudaEventRecord(L->ev_sync, s->stream);
+  if (e != cudaSuccess) return e;
+  return cudaEventSynchronize(L->ev_sync);
+}
+
+// Stream-ordered (re)allocation of solve-time workspaces: no device-wide
+// synchronisation, so handles running on other streams are not stalled.
+template <typename T>
+cudaError_t salloc(T** p, size_t count, cudaStream_t st) {
+  static bool pool_set = false;   // keep freed blocks in the device's default pool (cheap reuse)
+  if (!pool_set) {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool_set = true;
+  }
+  return cudaMallocAsync((void**)p, sizeof(T) * (count ? count : 1), st);
+}
+inline void sfree(void* p, cudaStream_t st) {
+  if (p) cudaFreeAsync(p, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -448,7 +482,7 @@ sro_status check_status(Solver* s) {
   std::vector<int> st(H.size(), 0);
   for (size_t q = 0; q < H.size(); q++)
     CUDA_TRY(s, cudaMemcpyAsync(&st[q], H[q]->status, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
-  CUDA_TRY(s, cudaStreamSynchronize(s->stream));
+  CUDA_TRY(s, stream_wait(s));
   int first = 0;
   for (int v : st) if (v && !first) first = v;
   if (first) {
@@ -476,10 +510,10 @@ sro_status exchange(Solver* s, double* buf, size_t count) {
 
 sro_status ensure_partials(Solver* s, int nslabs, int L) {
   if (nslabs > 1 && (int64_t)nslabs * L > s->part_cap) {
-    cudaFree(s->part_j); cudaFree(s->part_min);
+    sfree(s->part_j, s->stream); sfree(s->part_min, s->stream);
     s->part_cap = (int64_t)nslabs * L;
-    CUDA_TRY(s, dalloc(&s->part_j, s->part_cap));
-    CUDA_TRY(s, dalloc(&s->part_min, s->part_cap));
+    CUDA_TRY(s, salloc(&s->part_j, s->part_cap, s->stream));
+    CUDA_TRY(s, salloc(&s->part_min, s->part_cap, s->stream));
   }
   return SRO_OK;
 }
@@ -541,10 +575,10 @@ sro_status sweep(Solver* s, const int* col0_dev, int col0_mul, int col0_host, in
   const int slab = s->slab_rows;
   const int nslabs = (s->m + slab - 1) / slab;
   if (nslabs > 1 && (int64_t)nslabs * L > s->part_cap) {
-    cudaFree(s->part_j); cudaFree(s->part_min);
+    sfree(s->part_j, s->stream); sfree(s->part_min, s->stream);
     s->part_cap = (int64_t)nslabs * L;
-    CUDA_TRY(s, dalloc(&s->part_j, s->part_cap));
-    CUDA_TRY(s, dalloc(&s->part_min, s->part_cap));
+    CUDA_TRY(s, salloc(&s->part_j, s->part_cap, s->stream));
+    CUDA_TRY(s, salloc(&s->part_min, s->part_cap, s->stream));
   }
   return with_sweep_src(s, [&](auto src) -> sro_status {
     using Src = decltype(src);
@@ -615,17 +649,17 @@ sro_status gap_sweep(Solver* s, double* total) {
 
 sro_status ensure_visit(Solver* s, int64_t count) {
   if (count > s->visit_cap) {
-    cudaFree(s->visit);
+    sfree(s->visit, s->stream);
     s->visit_cap = count < 4096 ? 4096 : count;
-    CUDA_TRY(s, dalloc(&s->visit, s->visit_cap));
+    CUDA_TRY(s, salloc(&s->visit, s->visit_cap, s->stream));
   }
   return SRO_OK;
 }
 sro_status ensure_trace(Solver* s, int64_t count) {
   if (count > s->trace_cap) {
-    cudaFree(s->trace);
+    sfree(s->trace, s->stream);
     s->trace_cap = count;
-    CUDA_TRY(s, dalloc(&s->trace, 9 * s->trace_cap));
+    CUDA_TRY(s, salloc(&s->trace, 9 * s->trace_cap, s->stream));
   }
   return SRO_OK;
 }
@@ -875,7 +909,7 @@ sro_status ensure_cmax(Solver* s) {
   if (st) return st;
   unsigned long long bits = 0;
   CUDA_TRY(s, cudaMemcpyAsync(&bits, d_cmax, sizeof(bits), cudaMemcpyDeviceToHost, s->stream));
-  CUDA_TRY(s, cudaStreamSynchronize(s->stream));
+  CUDA_TRY(s, stream_wait(s));
   double v;
   memcpy(&v, &bits, sizeof(v));
   s->cmax = v;
@@ -919,22 +953,23 @@ sro_status ga_initialise(Solver* s) {
 sro_status ensure_block_ws(Solver* s, int64_t L) {
   const int64_t P = L * (s->cap + 1);
   if (!s->rowcnt) {   // row workspace: zero outside a step
-    CUDA_TRY(s, dalloc(&s->rowcnt, s->m)); CUDA_TRY(s, dalloc(&s->X, s->m));
-    CUDA_TRY(s, dalloc(&s->trows, s->m)); CUDA_TRY(s, dalloc(&s->ntouch, 1));
-    CUDA_TRY(s, dalloc(&s->rowidx, s->m)); CUDA_TRY(s, dalloc(&s->tstart, s->m));
-    CUDA_TRY(s, dalloc(&s->tcur, s->m)); CUDA_TRY(s, dalloc(&s->capfail, 1));
-    CUDA_TRY(s, dalloc(&s->bigw, s->m)); CUDA_TRY(s, dalloc(&s->nbig, 2));
+    CUDA_TRY(s, salloc(&s->rowcnt, s->m, s->stream)); CUDA_TRY(s, salloc(&s->X, s->m, s->stream));
+    CUDA_TRY(s, salloc(&s->trows, s->m, s->stream)); CUDA_TRY(s, salloc(&s->ntouch, 1, s->stream));
+    CUDA_TRY(s, salloc(&s->rowidx, s->m, s->stream)); CUDA_TRY(s, salloc(&s->tstart, s->m, s->stream));
+    CUDA_TRY(s, salloc(&s->tcur, s->m, s->stream)); CUDA_TRY(s, salloc(&s->capfail, 1, s->stream));
+    CUDA_TRY(s, salloc(&s->bigw, s->m, s->stream)); CUDA_TRY(s, salloc(&s->nbig, 2, s->stream));
     { sro_status e = ws_clean(s); if (e) return e; }
     CUDA_TRY(s, cudaMemsetAsync(s->capfail, 0, sizeof(int), s->stream));
   }
   if (L <= s->blk_L && P <= s->blk_P) return SRO_OK;
-  cudaFree(s->pcount); cudaFree(s->poff); cudaFree(s->ptotal); cudaFree(s->prow); cudaFree(s->ppos);
-  cudaFree(s->pd); cudaFree(s->ptold); cudaFree(s->pdelta); cudaFree(s->runc); cudaFree(s->runv);
+  for (void* q : {(void*)s->pcount, (void*)s->poff, (void*)s->ptotal, (void*)s->prow, (void*)s->ppos, (void*)s->pd,
+                  (void*)s->ptold, (void*)s->pdelta, (void*)s->runc, (void*)s->runv})
+    sfree(q, s->stream);
   s->blk_L = L; s->blk_P = P;
-  CUDA_TRY(s, dalloc(&s->pcount, L)); CUDA_TRY(s, dalloc(&s->poff, L + 1)); CUDA_TRY(s, dalloc(&s->ptotal, 1));
-  CUDA_TRY(s, dalloc(&s->prow, P)); CUDA_TRY(s, dalloc(&s->ppos, P)); CUDA_TRY(s, dalloc(&s->pd, P));
-  CUDA_TRY(s, dalloc(&s->ptold, P)); CUDA_TRY(s, dalloc(&s->pdelta, P));
-  CUDA_TRY(s, dalloc(&s->runc, P)); CUDA_TRY(s, dalloc(&s->runv, P));
+  CUDA_TRY(s, salloc(&s->pcount, L, s->stream)); CUDA_TRY(s, salloc(&s->poff, L + 1, s->stream)); CUDA_TRY(s, salloc(&s->ptotal, 1, s->stream));
+  CUDA_TRY(s, salloc(&s->prow, P, s->stream)); CUDA_TRY(s, salloc(&s->ppos, P, s->stream)); CUDA_TRY(s, salloc(&s->pd, P, s->stream));
+  CUDA_TRY(s, salloc(&s->ptold, P, s->stream)); CUDA_TRY(s, salloc(&s->pdelta, P, s->stream));
+  CUDA_TRY(s, salloc(&s->runc, P, s->stream)); CUDA_TRY(s, salloc(&s->runv, P, s->stream));
   return SRO_OK;
 }
 
@@ -1130,7 +1165,7 @@ sro_status objective_dev(Solver* s, double* f_host) {
   s->lead->stats.kernel_launches += 4 + (int64_t)held(s).size();
   CUDA_TRY(s, cudaGetLastError());
   CUDA_TRY(s, cudaMemcpyAsync(f_host, s->scal + 7, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
-  CUDA_TRY(s, cudaStreamSynchronize(s->stream));
+  CUDA_TRY(s, stream_wait(s));
   return SRO_OK;
 }
 
@@ -1149,16 +1184,20 @@ sro_status do_reset(Solver* s) {
 
 void free_shard(Solver* s) {
   if (!s) return;
+  // stream-ordered workspaces (salloc) go back to the pool on the stream; the rest with cudaFree
+  void* aptrs[] = {s->visit, s->trace, s->part_j, s->part_min, s->pcount, s->poff, s->ptotal, s->prow, s->ppos, s->pd,
+                   s->ptold, s->pdelta, s->runc, s->runv, s->rowcnt, s->rowidx, s->tstart, s->tcur, s->X,
+                   s->trows, s->ntouch, s->capfail, s->bigw, s->nbig};
+  for (void* p : aptrs) sfree(p, s->stream);
+  if (s->stream) stream_wait(s);
   void* ptrs[] = {s->dsteps, s->phase, s->a, s->b, s->b_full, s->r, s->h, s->cnt, s->srow, s->sval, s->G_ga, s->fen,
-                  s->status, s->steps_done, s->stop, s->scal, s->epsd, s->visit, s->trace, s->sw_j, s->sw_min,
-                  s->sw_g, s->part_j, s->part_min, s->pcount, s->poff, s->ptotal, s->prow, s->ppos, s->pd,
-                  s->ptold, s->pdelta, s->runc, s->runv, s->rowcnt, s->rowidx, s->tstart, s->tcur, s->X,
-                  s->trows, s->ntouch, s->capfail, s->bigw, s->nbig};
+                  s->status, s->steps_done, s->stop, s->scal, s->epsd, s->sw_j, s->sw_min, s->sw_g};
   for (void* p : ptrs) if (p) cudaFree(p);
   if (s->owns_cost) { if (s->C) cudaFree(s->C); if (s->x) cudaFree(s->x); if (s->y) cudaFree(s->y); }
   for (auto& p : s->pending) { s->ev_pool.push_back(p.a); s->ev_pool.push_back(p.b); }
   for (auto e : s->ev_pool) cudaEventDestroy(e);
   if (s->ev0) cudaEventDestroy(s->ev0);
+  if (s->ev_sync) cudaEventDestroy(s->ev_sync);
   if (s->ev1) cudaEventDestroy(s->ev1);
   if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
   delete s;
@@ -1238,7 +1277,7 @@ sro_status build_shard(Solver* s, const double* a, const double* b_loc, const do
   if (cudaGetLastError() != cudaSuccess) { s->err = "kernel launch failed at create"; return SRO_ERR_CUDA; }
   int st = 0;
   cudaMemcpyAsync(&st, s->status, sizeof(int), cudaMemcpyDeviceToHost, s->stream);
-  if (cudaStreamSynchronize(s->stream) != cudaSuccess) { s->err = "create failed"; return SRO_ERR_CUDA; }
+  if (stream_wait(s) != cudaSuccess) { s->err = "create failed"; return SRO_ERR_CUDA; }
   if (st) { s->err = "cost must be finite and >= 0"; return SRO_ERR_NONFINITE; }
   return SRO_OK;
 }
@@ -1358,7 +1397,7 @@ sro_status sro_create(const double* a, const double* b, const sro_cost* cost, co
     }
   }
   if (do_reset(s) != SRO_OK) return fail(SRO_ERR_CUDA, "");
-  if (cudaStreamSynchronize(s->stream) != cudaSuccess) return fail(SRO_ERR_CUDA, "init failed");
+  if (stream_wait(s) != cudaSuccess) return fail(SRO_ERR_CUDA, "init failed");
   *out = static_cast<sro_handle>(static_cast<sro_solver*>(s));
   return SRO_OK;
 }
@@ -1367,7 +1406,7 @@ void sro_destroy(sro_handle h) {
   if (!h) return;
   Solver* s = static_cast<Solver*>(h);
   cudaSetDevice(s->device);
-  cudaStreamSynchronize(s->stream);
+  stream_wait(s);
   free_solver(s);
 }
 
@@ -1377,7 +1416,7 @@ sro_status sro_reset(sro_handle h) {
   cudaSetDevice(s->device);
   sro_status st = do_reset(s);
   if (st) return st;
-  CUDA_TRY(s, cudaStreamSynchronize(s->stream));
+  CUDA_TRY(s, stream_wait(s));
   return SRO_OK;
 }
 
@@ -1512,7 +1551,7 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
     htr.resize(9 * (size_t)done);
     CUDA_TRY(s, cudaMemcpyAsync(htr.data(), s->trace, sizeof(double) * 9 * done, cudaMemcpyDeviceToHost, s->stream));
   }
-  CUDA_TRY(s, cudaStreamSynchronize(s->stream));
+  CUDA_TRY(s, stream_wait(s));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, s->ev0, s->ev1);
   out->device_ms = ms;
@@ -1541,7 +1580,7 @@ sro_status sro_gap(sro_handle h, double* total, double* per_column, int32_t* arg
     CUDA_TRY(s, cudaMemcpyAsync(g[q].data(), src, sizeof(double) * s->n, cudaMemcpyDeviceToHost, s->stream));
     CUDA_TRY(s, cudaMemcpyAsync(j[q].data(), H[q]->sw_j, sizeof(int) * s->n, cudaMemcpyDeviceToHost, s->stream));
   }
-  CUDA_TRY(s, cudaStreamSynchronize(s->stream));
+  CUDA_TRY(s, stream_wait(s));
   for (size_t c = 0; c < cols.size(); c++) {
     if (per_column) per_column[c] = g[cols[c].hq][cols[c].p];
     if (argmin_rows) argmin_rows[c] = j[cols[c].hq][cols[c].p];
@@ -1561,7 +1600,7 @@ sro_status sro_get_rowsums(sro_handle h, double* r) {
   Solver* s = static_cast<Solver*>(h);
   cudaSetDevice(s->device);
   CUDA_TRY(s, cudaMemcpyAsync(r, s->r, sizeof(double) * s->m, cudaMemcpyDeviceToHost, s->stream));
-  CUDA_TRY(s, cudaStreamSynchronize(s->stream));
+  CUDA_TRY(s, stream_wait(s));
   return SRO_OK;
 }
 
@@ -1580,7 +1619,7 @@ sro_status sro_get_plan(sro_handle h, double* dense, int32_t* rows, int32_t* col
     CUDA_TRY(s, cudaMemcpyAsync(hr[q].data(), t->srow, sizeof(int) * hr[q].size(), cudaMemcpyDeviceToHost, s->stream));
     CUDA_TRY(s, cudaMemcpyAsync(hv[q].data(), t->sval, sizeof(double) * hv[q].size(), cudaMemcpyDeviceToHost, s->stream));
   }
-  CUDA_TRY(s, cudaStreamSynchronize(s->stream));
+  CUDA_TRY(s, stream_wait(s));
   auto order = held_order(s);
   if (dense) memset(dense, 0, sizeof(double) * (size_t)s->m * order.size());
   int64_t q = 0;
@@ -1655,7 +1694,7 @@ sro_status sro_barycentric(sro_handle h, const double* x, const double* y, doubl
     k_plan_project<<<(m + 255) / 256, 256, 0, s->stream>>>(m, sums[0], sums[1], sums[2], sums[3], xd, xo);
     s->stats.kernel_launches += 1;
     if (cudaMemcpyAsync(xhat, xo, sizeof(double) * 3 * m, cudaMemcpyDeviceToHost, s->stream) != cudaSuccess ||
-        cudaStreamSynchronize(s->stream) != cudaSuccess) {
+        stream_wait(s) != cudaSuccess) {
       s->err = "barycentric failed"; st = SRO_ERR_CUDA; break;
     }
   } while (0);
@@ -1729,7 +1768,7 @@ sro_status sro_get_stats(sro_handle h, sro_stats* out, int32_t reset) {
   if (!h || !out) return SRO_ERR_INVALID_ARG;
   Solver* s = static_cast<Solver*>(h);
   cudaSetDevice(s->device);
-  CUDA_TRY(s, cudaStreamSynchronize(s->stream));
+  CUDA_TRY(s, stream_wait(s));
   resolve_timing(s);
   *out = s->stats;
   if (reset) s->stats = sro_stats{};
@@ -1742,7 +1781,7 @@ sro_status sro_debug_phase(sro_handle h, long long* out8) {
   if (!h || !out8) return SRO_ERR_INVALID_ARG;
   Solver* s = static_cast<Solver*>(h);
   CUDA_TRY(s, cudaMemcpyAsync(out8, s->phase, 16 * sizeof(long long), cudaMemcpyDeviceToHost, s->stream));
-  CUDA_TRY(s, cudaStreamSynchronize(s->stream));
+  CUDA_TRY(s, stream_wait(s));
   return SRO_OK;
 }
 
