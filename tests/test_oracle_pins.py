@@ -589,3 +589,50 @@ def test_chunk_tree_sum_shape():
         z = rs.standard_normal(L)
         s = chunk_tree_sum(z, 256)
         assert abs(s - math.fsum(z)) <= 1e-15 * (L / 256 + 8) * np.abs(z).sum()
+
+
+# --------------------------------------------------------------------------- Theorem 1, qualitative claims
+def test_theorem1_decay_envelope_over_seeds():
+    """Theorem 1 (proof P:2213-2223): with the decay step 2n/(k+2n) and uniform
+    sampling, E[f(T^k)] - f* <= 2n/(k+2n) (C_f^x + h0), with the product curvature
+    C_f^x = sum_i C_f^(i) <= sum_i 4 b_i^2 / lambda (Def. 1 / App. C) and
+    h0 = f(T^0) - f*. The expectation is the mean over 20 seeds; f* comes from a long ELS run
+    whose certified gap bounds its own suboptimality (Thm 2)."""
+    d = instance(1, m=24, n=16, seed=6)
+    lam = 0.5
+    ref = Oracle(d["a"], d["b"], lam, C=d["C64"], cap=24)
+    ref.solve(BCPFW, 5000 * 16, seed=1, step=ELS, sampling=U, epsilon=1e-10)   # pairwise: fast to 1e-10
+    g = ref.gap()[0]
+    assert 0.0 <= g <= 1e-6
+    fstar = ref.objective() - g                      # f* >= f(T) - g(T) (Thm 2): conservative
+    n = 16
+    o0 = Oracle(d["a"], d["b"], lam, C=d["C64"], cap=24)
+    h0 = o0.objective() - fstar
+    Cx = float((4.0 * d["b"] ** 2 / lam).sum())
+    checkpoints = [n, 4 * n, 16 * n, 64 * n]
+    subopt = np.zeros((20, len(checkpoints)))
+    for s in range(20):
+        o = Oracle(d["a"], d["b"], lam, C=d["C64"], cap=24)
+        done = 0
+        for c, k in enumerate(checkpoints):
+            o.solve(BCFW, k - done, seed=100 + s, step=DEC, sampling=U, epsilon=-1.0)
+            done = k
+            subopt[s, c] = o.objective() - fstar
+    for c, k in enumerate(checkpoints):
+        assert subopt[:, c].mean() <= 2.0 * n / (k + 2.0 * n) * (Cx + h0)
+    assert (subopt >= -1e-12).all()
+    assert subopt[:, -1].mean() < subopt[:, 0].mean()
+
+
+def test_pairwise_needs_fewer_epochs_than_bcfw_u():
+    """Qualitative claim: BCPFW reaches the gap threshold in fewer epochs than
+    BCFW-U with the line search (median over seeds; scratch at m = n = 256: 123 vs 250)."""
+    d = instance(1, m=96, n=96, seed=7)
+    ep = {BCFW: [], BCPFW: []}
+    for seed in range(5):
+        for var in (BCFW, BCPFW):
+            o = Oracle(d["a"], d["b"], 1.0, C=d["C64"], cap=31)
+            r = o.solve(var, 3000 * 96, seed=seed, step=ELS, sampling=U, epsilon=1e-6)
+            assert r["converged"]
+            ep[var].append(r["iters_done"] / 96)
+    assert np.median(ep[BCPFW]) < np.median(ep[BCFW])
