@@ -55,6 +55,7 @@ struct SrcDense {
   int64_t ld;
   static constexpr int SMEM_PER_ROW = 0;
   static constexpr bool PLANAR = true;
+  static constexpr int COLS = 1;
   __device__ __forceinline__ void stage(int, int, char*) const {}
   __device__ __forceinline__ double cost(int k, int i) const { return (double)C[(int64_t)i * ld + k]; }
   // Scan rows [row0, row0+rows) of column i; lane-strided 128-bit vectors,
@@ -113,6 +114,7 @@ struct SrcColour {
   const T* y;   // 3n
   static constexpr int SMEM_PER_ROW = 3 * sizeof(T);
   static constexpr bool PLANAR = false;
+  static constexpr int COLS = 4;   // columns a warp evaluates per loaded row (registers hold their y)
   __device__ __forceinline__ static int hidx(int k, int) { return k; }
   __device__ __forceinline__ void stage(int row0, int rows, char* sm) const {
     T* xs = reinterpret_cast<T*>(sm);
@@ -136,6 +138,30 @@ struct SrcColour {
       double c = colour_cost<EUCLID>(xs[k], xs[rows + k], xs[2 * rows + k], y0, y1, y2);
       double v = d_add(c, hs[k]);
       if (v < best) { best = v; bj = k; }
+    }
+  }
+  // columns i0 .. i0+nc-1 (nc <= COLS) against every row of the slab: one load of
+  // (x_k, h_k) per row serves all of them; rows ascending per lane and column.
+  template <int NC>
+  __device__ __forceinline__ void scan_multi(int i0, int nc, int rows, const double* hs, const char* sm,
+                                             double* best, int* bj) const {
+    const T* xs = reinterpret_cast<const T*>(sm);
+    T yv[NC][3];
+#pragma unroll
+    for (int c = 0; c < NC; c++) {
+      const int i = i0 + (c < nc ? c : 0);
+      yv[c][0] = y[3 * (int64_t)i]; yv[c][1] = y[3 * (int64_t)i + 1]; yv[c][2] = y[3 * (int64_t)i + 2];
+    }
+    const int lane = threadIdx.x & 31;
+#pragma unroll 2
+    for (int k = lane; k < rows; k += 32) {
+      const T x0 = xs[k], x1 = xs[rows + k], x2 = xs[2 * rows + k];
+      const double hk = hs[k];
+#pragma unroll
+      for (int c = 0; c < NC; c++) {
+        const double v = d_add(colour_cost<EUCLID>(x0, x1, x2, yv[c][0], yv[c][1], yv[c][2]), hk);
+        if (v < best[c]) { best[c] = v; bj[c] = k; }
+      }
     }
   }
 };
@@ -166,7 +192,7 @@ struct SweepOut {
 };
 
 // grid = (gx, nslabs). col0 = col0_dev ? *col0_dev * col0_mul : col0_host.
-template <class Src>
+template <class Src, int NCOL = Src::COLS>
 __global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_sweep(Src src, int m, int slab_rows, const double* __restrict__ h,
                                                              const int* __restrict__ col0_dev, int col0_mul,
                                                              int col0_host, int L, const int* __restrict__ cnt,
@@ -185,6 +211,34 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_sweep(Src src, int m, int
   __syncthreads();
   const int col0 = col0_dev ? (*col0_dev) * col0_mul : col0_host;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if constexpr (NCOL > 1) {
+    constexpr int NC = NCOL;
+    for (int p0 = (blockIdx.x * SWEEP_WARPS + warp) * NC; p0 < L; p0 += gridDim.x * SWEEP_WARPS * NC) {
+      const int nc = min(NC, L - p0);
+      double best[NC];
+      int bj[NC];
+#pragma unroll
+      for (int c = 0; c < NC; c++) { best[c] = __longlong_as_double(0x7ff0000000000000LL); bj[c] = 0x7fffffff; }
+      src.template scan_multi<NC>(col0 + p0, nc, rows, sm_h, sm_src, best, bj);
+#pragma unroll
+      for (int c = 0; c < NC; c++) {
+        if (c >= nc) break;
+        const int p = p0 + c, i = col0 + p;
+        double bv = best[c];
+        int bjc = bj[c];
+        if (bjc != 0x7fffffff) bjc += row0;
+        warp_argmin(bv, bjc);
+        if (nslabs == 1) {
+          if (!(bv < 1.0e308 && bv > -1.0e308)) { if (lane == 0) set_status(status, 5); }
+          const double g = column_gap_epilogue(src, i, bv, cnt, srow, sval, cap, b, h);
+          if (lane == 0) { out.j[p] = bjc; out.minval[p] = bv; out.g[p] = g; }
+        } else if (lane == 0) {
+          out.j[(int64_t)slab * L + p] = bjc;
+          out.minval[(int64_t)slab * L + p] = bv;
+        }
+      }
+    }
+  } else {
   for (int p = blockIdx.x * SWEEP_WARPS + warp; p < L; p += gridDim.x * SWEEP_WARPS) {
     const int i = col0 + p;
     double best = __longlong_as_double(0x7ff0000000000000LL);  // +inf
@@ -201,6 +255,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_sweep(Src src, int m, int
       out.minval[(int64_t)slab * L + p] = best;
     }
   }
+}
 }
 
 // Merge per-slab partials in slab order and apply the gap epilogue. One warp per column.

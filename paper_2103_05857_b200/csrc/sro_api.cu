@@ -587,13 +587,16 @@ sro_status sweep(Solver* s, const int* col0_dev, int col0_mul, int col0_host, in
     }
     const int rows = s->m < slab ? s->m : slab;
     const size_t smem = sizeof(double) * (size_t)((rows + 1) & ~1) + (size_t)Src::SMEM_PER_ROW * rows;
-    auto kern = k_lmo_sweep<Src>;
+    // several columns per warp only when there are enough columns to fill the GPU that way
+    const bool multi = Src::COLS > 1 && (int64_t)L * nslabs >= (int64_t)s->num_sms * SWEEP_WARPS * Src::COLS * 2;
+    const int cols = multi ? Src::COLS : 1;
+    auto kern = multi ? k_lmo_sweep<Src, Src::COLS> : k_lmo_sweep<Src, 1>;
     CUDA_TRY(s, set_dyn_smem((const void*)kern, s->device, (int)smem));
     int per_sm = 0;
     CUDA_TRY(s, occupancy((const void*)kern, s->device, SWEEP_THREADS, smem, &per_sm));
     if (per_sm < 1) per_sm = 1;
     int gx = s->num_sms * per_sm;
-    const int need = (L + SWEEP_WARPS - 1) / SWEEP_WARPS;
+    const int need = (L + SWEEP_WARPS * cols - 1) / (SWEEP_WARPS * cols);
     if (nslabs > 1) gx = (gx + nslabs - 1) / nslabs;
     if (gx > need) gx = need;
     if (gx < 1) gx = 1;
