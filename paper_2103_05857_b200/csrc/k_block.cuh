@@ -88,6 +88,7 @@ struct BlockArgs {
   double* x1;            // G slots of slot_len: Delta subtree per row, [m] = G_U subtree, [m+1] = status
   double* x2;            // G slots: Delta' subtree per row, [m] = capacity failure, [m+1] = status
   int* capfail;          // this shard's capacity check failed (nullptr when unsharded)
+  long long* phase;      // SRO_PHASE_TIMING builds only: clock64 phase totals
 };
 
 __device__ __forceinline__ bool blk_skip(const BlockArgs& A) {
@@ -511,13 +512,10 @@ __global__ void k_step_done(BlockArgs A) {
 }
 
 // ... and the whole post-LMO step in one CTA of 1024 threads (small U).
-__global__ void __launch_bounds__(1024, 1) k_block_tail(BlockArgs A) {
-  extern __shared__ double tail_slots[];   // 32 warps x 256, zero outside use
-  if (*A.status) return;
+// dev_tail_rest: everything after G_U (also the fallback of k_block_tail_sm).
+__device__ __forceinline__ void dev_tail_rest(BlockArgs& A, double* tail_slots) {   // 32 warps x 256
   for (int q = threadIdx.x; q < 32 * 256; q += blockDim.x) tail_slots[q] = 0.0;
   if (threadIdx.x == 0) { *A.ntouch = 0; A.nbig[0] = 0; A.nbig[1] = 0; }
-  dev_psumW(A.g, A.L, 256, A.scal + 0, A.eps, A.stop);        // G_U (FW: stop check)
-  if (A.stop && *A.stop) return;
   dev_pairs_count(A);
   __syncthreads();
   dev_scan_excl(A.pcount, A.L, A.poff, A.ptotal);
@@ -540,6 +538,14 @@ __global__ void __launch_bounds__(1024, 1) k_block_tail(BlockArgs A) {
   __syncthreads();
   dev_row_tree<1>(A, nullptr, true, 1, tail_slots);
   if (threadIdx.x == 0) atomicAdd(A.dsteps, 1ULL);
+}
+
+__global__ void __launch_bounds__(1024, 1) k_block_tail(BlockArgs A) {
+  extern __shared__ double tail_slots[];   // zero outside use
+  if (*A.status) return;
+  dev_psumW(A.g, A.L, 256, A.scal + 0, A.eps, A.stop);        // G_U (FW: stop check)
+  if (A.stop && *A.stop) return;
+  dev_tail_rest(A, tail_slots);
 }
 
 // ---------------------------------------------------------------------------

@@ -1,0 +1,388 @@
+// k_block_tail.cuh — the whole post-LMO part of a plain step over a small
+// column set (|U| <= 1024: batched blocks, FW on small n) in ONE CTA with the
+// step's pairs resident in shared memory (the global-memory tail of
+// k_block.cuh spends its time on dependent L2 round trips between ~15
+// barrier phases).
+//
+// Same arithmetic and summation shapes as every other block step (R19):
+//   * the merged supports supp(t_i) U {j_i} become (row, pair) keys,
+//     key = row << 12 | q with q the pair index (q ascends with the column
+//     position), sorted in shared memory (bitonic);
+//   * along a row the sorted keys are in ascending position, so one thread
+//     per row sums each (row, chunk) run left to right from +0.0 and combines
+//     the run partials — chunks ascending — with an O(runs) stack evaluation
+//     of the 256-leaf adjacent-pair tree (zero leaves are identities);
+//   * the denominator is the 256-chunk sum over the m rows of Delta_k^2 with the
+//     touched rows (ascending) found per chunk by binary search.
+// Steps whose pair count exceeds TS_PMAX run the global-memory tail instead.
+// Host side: used for L <= 1024 and m < 2^20 (the row field of a key).
+#pragma once
+#include "k_block.cuh"
+
+namespace sro {
+
+constexpr int TS_PMAX = 4096;   // pairs held in shared memory
+constexpr int TS_SORT = 8192;   // bitonic buffer (power of two >= TS_PMAX)
+
+struct TailSmem {
+  uint32_t key[TS_SORT];
+  union {
+    double pd[TS_PMAX];   // s - t, then t' - t
+    double rX[TS_PMAX];   // Delta_k^2 of the touched rows (after the Delta run sums)
+  };
+  double ptold[TS_PMAX];
+  int prow[TS_PMAX];
+  uint8_t pchunk[TS_PMAX];  // 256-chunk of the pair's column position
+  double runv[TS_PMAX];   // (row, chunk) run sums, sorted order
+  uint8_t runc[TS_PMAX];  // their chunks
+  uint16_t runu[TS_PMAX + 1];  // their first sorted index
+  int rowrun[TS_PMAX + 1];  // touched row -> its first run
+  int rrow[TS_PMAX];      // touched rows, ascending
+  int hot[TS_PMAX / 8];   // touched rows with more than TS_SMALL (= 8) runs
+  int wsum[32];
+  int misc[8];
+  double red[8];
+};
+static_assert(sizeof(TailSmem) + 1408 <= 232448, "k_block_tail_sm shared memory");
+constexpr size_t TAIL_SM_BYTES = sizeof(TailSmem) > 32 * 256 * 8 ? sizeof(TailSmem) : 32 * 256 * 8;
+
+// 256-leaf adjacent-pair tree over leaves pushed in ascending chunk order: a
+// stack of completed subtrees (their boundary heights strictly decrease
+// towards the top, so at most 9 entries), kept in registers — every index is
+// static, the stack shifts instead (the top is entry 0).
+struct TreeStack {
+  double v[9];
+  int c[9];
+  int n = 0;
+  __device__ __forceinline__ void pop_merge() {   // top two -> left + right
+    v[1] = d_add(v[1], v[0]);
+#pragma unroll
+    for (int e = 0; e < 8; e++) { v[e] = v[e + 1]; c[e] = c[e + 1]; }
+    n--;
+  }
+  __device__ __forceinline__ void push(int cc, double x) {
+    while (n >= 2 && (31 - __clz(c[1] ^ c[0])) < (31 - __clz(c[0] ^ cc))) pop_merge();
+#pragma unroll
+    for (int e = 8; e > 0; e--) { v[e] = v[e - 1]; c[e] = c[e - 1]; }
+    v[0] = x; c[0] = cc; n++;
+  }
+  __device__ __forceinline__ double finish() {
+    while (n >= 2) pop_merge();
+    return n ? v[0] : 0.0;
+  }
+};
+
+// Bitonic sort of Pp = 1024 E keys in buf[0, Pp) (buf holds 2 Pp), thread t
+// owning keys [t E, t E + E): exchanges inside a thread in registers, inside a
+// warp by shuffles, across warps through alternating halves of buf (one
+// barrier per stage). Result back in buf[0, Pp).
+template <int E>
+__device__ __forceinline__ void ts_sort(uint32_t* buf, int Pp) {
+  const int t = threadIdx.x;
+  uint32_t x[E];
+#pragma unroll
+  for (int e = 0; e < E; e++) x[e] = buf[t * E + e];
+  int half = 1;
+  for (int k = 2; k <= Pp; k <<= 1) {
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      if (jj < E) {
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+#pragma unroll
+          for (int d = 1; d < E; d <<= 1) {
+            if (d != jj || (e & d)) continue;
+            const bool up = ((t * E + e) & k) == 0;
+            const uint32_t a = x[e], b = x[e | d];
+            if ((a > b) == up) { x[e] = b; x[e | d] = a; }
+          }
+        }
+      } else if (jj < 32 * E) {
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+          const uint32_t y = __shfl_xor_sync(FULL, x[e], jj / E);
+          const int u = t * E + e;
+          const bool keep_min = ((u & jj) == 0) == ((u & k) == 0);
+          x[e] = keep_min ? min(x[e], y) : max(x[e], y);
+        }
+      } else {
+        uint32_t* hb = buf + half * Pp;
+#pragma unroll
+        for (int e = 0; e < E; e++) hb[t * E + e] = x[e];
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+          const int u = t * E + e;
+          const uint32_t y = hb[u ^ jj];
+          const bool keep_min = ((u & jj) == 0) == ((u & k) == 0);
+          x[e] = keep_min ? min(x[e], y) : max(x[e], y);
+        }
+        half ^= 1;
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < E; e++) buf[t * E + e] = x[e];
+  __syncthreads();
+}
+
+// Block-wide exclusive scan of one int per thread (1024 threads); returns the
+// thread's offset, *total the sum.
+__device__ __forceinline__ int block_scan1024(int x, int* wsum, int* total) {
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  int incl = x;
+  for (int o = 1; o < 32; o <<= 1) { const int v = __shfl_up_sync(FULL, incl, o); if (lane >= o) incl += v; }
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int s = wsum[lane];
+    for (int o = 1; o < 32; o <<= 1) { const int v = __shfl_up_sync(FULL, s, o); if (lane >= o) s += v; }
+    wsum[lane] = s;
+  }
+  __syncthreads();
+  const int off = incl - x + (w ? wsum[w - 1] : 0);
+  *total = wsum[31];
+  __syncthreads();
+  return off;
+}
+
+#ifdef SRO_PHASE_TIMING
+#define TS_MARK(idx)                                                     \
+  do {                                                                   \
+    if (threadIdx.x == 0) {                                              \
+      const long long t_ = clock64();                                    \
+      A.phase[idx] += t_ - ts_t;                                         \
+      ts_t = t_;                                                         \
+    }                                                                    \
+  } while (0)
+#else
+#define TS_MARK(idx) do {} while (0)
+#endif
+
+// Per-row sums over the sorted pairs (R19), in two parts. ts_structure (once
+// per step; the pair set and its order are the same for Delta and Delta'):
+// the (row, chunk) runs of the sorted keys (start index runu, chunk runc), the
+// touched rows ascending (rrow) with their first run (rowrun), and the rows
+// with more than TS_SMALL runs (hot). ts_sums<MODE>(vals): thread per run
+// sums it left to right from +0.0; thread per touched row with at most
+// TS_SMALL runs combines the run partials (chunks ascending) with TreeStack;
+// warp per hot row: lane l gathers chunks [8l, 8l+8), tree8 + butterfly (the
+// dense tree with zero leaves). MODE 0: rX (Delta_k^2, for the denominator;
+// rX aliases the pair values, dead by then); MODE 1: r_k += D,
+// h_k = (r_k - a_k)/lambda.
+constexpr int TS_SMALL = 8;   // TailSmem::hot holds P / (TS_SMALL + 1) rows
+template <int E>
+__device__ __forceinline__ void ts_structure(TailSmem& S, int P) {
+  const int t = threadIdx.x;
+  uint32_t key[E + 1];
+#pragma unroll
+  for (int e = 0; e <= E; e++) {
+    const int u = t * E + e - 1;
+    key[e] = (u >= 0 && u < P) ? S.key[u] : 0xffffffffu;
+  }
+  int runf = 0, rowf = 0, packed = 0;
+#pragma unroll
+  for (int e = 0; e < E; e++) {
+    const int u = t * E + e;
+    if (u >= P) continue;
+    const bool row_start = u == 0 || (key[e + 1] >> 12) != (key[e] >> 12);
+    const bool run_start = row_start || S.pchunk[key[e + 1] & 4095u] != S.pchunk[key[e] & 4095u];
+    runf |= (int)run_start << e;
+    rowf |= (int)row_start << e;
+    packed += (int)run_start + ((int)row_start << 16);
+  }
+  int total;
+  const int off = block_scan1024(packed, S.wsum, &total);
+  int ri = off & 0xffff, wi = off >> 16;
+#pragma unroll
+  for (int e = 0; e < E; e++) {
+    if (!((runf >> e) & 1)) continue;
+    S.runu[ri] = (uint16_t)(t * E + e);
+    S.runc[ri] = S.pchunk[key[e + 1] & 4095u];
+    if ((rowf >> e) & 1) { S.rowrun[wi] = ri; S.rrow[wi] = (int)(key[e + 1] >> 12); wi++; }
+    ri++;
+  }
+  const int T = total >> 16, R = total & 0xffff;
+  if (t == 0) { S.rowrun[T] = R; S.runu[R] = (uint16_t)P; S.misc[0] = T; S.misc[1] = R; S.misc[2] = 0; }
+  __syncthreads();
+  for (int w = t; w < T; w += 1024)
+    if (S.rowrun[w + 1] - S.rowrun[w] > TS_SMALL) S.hot[atomicAdd(&S.misc[2], 1)] = w;
+  __syncthreads();
+}
+
+template <int MODE>
+__device__ __forceinline__ void ts_sums(const BlockArgs& A, TailSmem& S, const double* vals) {
+  const int t = threadIdx.x;
+  const int T = S.misc[0], R = S.misc[1], NH = S.misc[2];
+  for (int ri = t; ri < R; ri += 1024) {
+    const int u1 = S.runu[ri + 1];
+    int u = S.runu[ri];
+    double run = d_add(0.0, vals[S.key[u] & 4095u]);
+    for (u++; u < u1; u++) run = d_add(run, vals[S.key[u] & 4095u]);
+    S.runv[ri] = run;
+  }
+  __syncthreads();
+  auto finish = [&](int w, double D, double rk, double ak) {
+    if (MODE == 0) {
+      S.rX[w] = d_mul(D, D);
+    } else {
+      const double rn = d_add(rk, D);
+      A.r[S.rrow[w]] = rn;
+      const double dd = d_sub(rn, ak);
+      A.h[S.rrow[w]] = A.lambda == 1.0 ? dd : d_div(dd, A.lambda);
+    }
+  };
+  for (int w = t; w < T; w += 1024) {
+    const int r0 = S.rowrun[w], r1 = S.rowrun[w + 1];
+    if (r1 - r0 > TS_SMALL) continue;
+    double rk = 0.0, ak = 0.0;
+    if (MODE == 1) { const int row = S.rrow[w]; rk = A.r[row]; ak = A.a[row]; }
+    TreeStack st;
+    for (int q = r0; q < r1; q++) st.push(S.runc[q], S.runv[q]);
+    finish(w, st.finish(), rk, ak);
+  }
+  const int lane = t & 31;
+  for (int b = t >> 5; b < NH; b += 32) {
+    const int w = S.hot[b];
+    const int r0 = S.rowrun[w], r1 = S.rowrun[w + 1];
+    double rk = 0.0, ak = 0.0;
+    if (MODE == 1 && lane == 0) { const int row = S.rrow[w]; rk = A.r[row]; ak = A.a[row]; }
+    int lo = r0, hi = r1;   // first run with chunk >= 8 lane
+    while (lo < hi) { const int mid = (lo + hi) >> 1; if (S.runc[mid] < 8 * lane) lo = mid + 1; else hi = mid; }
+    double x[8];
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+      const bool hit = lo < r1 && S.runc[lo] == 8 * lane + e;
+      x[e] = hit ? S.runv[lo] : 0.0;
+      lo += hit;
+    }
+    const double D = warp_pair_tree(tree8(x));
+    if (lane == 0) finish(w, D, rk, ak);
+  }
+  __syncthreads();
+}
+
+// psum256 over the m rows of X (zero off the touched rows) -> *out. 1024 threads.
+__device__ __forceinline__ void ts_den(const BlockArgs& A, TailSmem& S, double* out) {
+  const int T = S.misc[0];
+  const int c = threadIdx.x;
+  double acc = 0.0;
+  if (c < 256) {
+    const int lo = (int)chunk_lo(c, A.m, 256), hi = (int)chunk_lo(c + 1, A.m, 256);
+    int a = 0, b = T;   // first touched row >= lo
+    while (a < b) { const int mid = (a + b) >> 1; if (S.rrow[mid] < lo) a = mid + 1; else b = mid; }
+    for (int u = a; u < T && S.rrow[u] < hi; u++) acc = d_add(acc, S.rX[u]);
+    acc = warp_pair_tree(acc);
+    if ((c & 31) == 0) S.red[c >> 5] = acc;
+  }
+  __syncthreads();
+  if (c < 32) {
+    double v = (c < 8) ? S.red[c] : 0.0;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) v = d_add(v, __shfl_xor_sync(FULL, v, o));
+    if (c == 0) *out = v;
+  }
+  __syncthreads();
+}
+
+
+__global__ void __launch_bounds__(1024, 1) k_block_tail_sm(BlockArgs A) {
+  extern __shared__ __align__(16) unsigned char tail_raw[];
+#ifdef SRO_PHASE_TIMING
+  long long ts_t = clock64();
+#endif
+  TailSmem& S = *reinterpret_cast<TailSmem*>(tail_raw);
+  if (*A.status) return;
+  const int t = threadIdx.x, L = A.L;
+  dev_psumW(A.g, L, 256, A.scal + 0, A.eps, A.stop);        // G_U (FW: stop check)
+  TS_MARK(0);
+  if (A.stop && *A.stop) return;
+  const int col0 = block_col0(A);
+  // merged support sizes -> offsets
+  int i = 0, j = 0, Mp = 0;
+  double bi = 0.0;
+  if (t < L) {
+    i = col0 + t;
+    j = A.j[t];
+    bi = A.b[i];
+    Mp = merged_count(A, i, j);
+  }
+  int P;
+  const int off = block_scan1024(Mp, S.wsum, &P);
+  TS_MARK(1);
+  if (P > TS_PMAX) {   // too many pairs for shared memory: the global-memory tail
+    dev_tail_rest(A, reinterpret_cast<double*>(tail_raw));
+    return;
+  }
+  if (t < L) {
+    const int c_t = chunk_index(t, L, 256);
+    for_merged(A, i, j, [&](int e, int row, double told) {
+      const int q = off + e;
+      S.prow[q] = row;
+      S.ptold[q] = told;
+      S.pd[q] = d_sub(row == j ? bi : 0.0, told);
+      S.pchunk[q] = (uint8_t)c_t;
+      S.key[q] = ((uint32_t)row << 12) | (uint32_t)q;
+    });
+  }
+  int Pp = 1024;
+  while (Pp < P) Pp <<= 1;
+  for (int u = P + t; u < Pp; u += 1024) S.key[u] = 0xffffffffu;
+  __syncthreads();
+  TS_MARK(2);
+  // sort of the keys (unique: one pair per (row, column))
+  if (Pp == 1024) ts_sort<1>(S.key, Pp);
+  else if (Pp == 2048) ts_sort<2>(S.key, Pp);
+  else ts_sort<4>(S.key, Pp);
+  TS_MARK(3);
+  // Delta_k per touched row -> denominator -> gamma
+  if (Pp == 1024) ts_structure<1>(S, P);
+  else if (Pp == 2048) ts_structure<2>(S, P);
+  else ts_structure<4>(S, P);
+  TS_MARK(9);
+  ts_sums<0>(A, S, S.pd);
+  TS_MARK(4);
+  ts_den(A, S, A.scal + 1);
+  dev_gamma(A);
+  __syncthreads();
+  TS_MARK(5);
+  // capacity check before anything is mutated
+  const double gamma = A.scal[2];
+  const double omg = d_sub(1.0, gamma);
+  const double gb = d_mul(gamma, bi);
+  if (t < L) {
+    int keep = 0;
+    for (int q = off; q < off + Mp; q++) {
+      double tn = d_mul(omg, S.ptold[q]);
+      if (S.prow[q] == j) tn = d_add(tn, gb);
+      keep += (tn != 0.0);
+    }
+    if (keep > A.cap) set_status(A.status, 6);
+  }
+  __syncthreads();
+  TS_MARK(6);
+  if (*A.status) return;
+  // t_i <- (1-gamma) t_i + gamma s_i; exact zeros dropped (R13); Delta' = t' - t
+  if (t < L) {
+    int keep = 0;
+    for (int q = off; q < off + Mp; q++) {
+      const double told = S.ptold[q];
+      double tn = d_mul(omg, told);
+      if (S.prow[q] == j) tn = d_add(tn, gb);
+      S.pd[q] = d_sub(tn, told);
+      if (tn != 0.0) {
+        A.srow[(int64_t)i * A.cap + keep] = S.prow[q];
+        A.sval[(int64_t)i * A.cap + keep] = tn;
+        keep++;
+      }
+    }
+    A.cnt[i] = keep;
+  }
+  __syncthreads();
+  TS_MARK(7);
+  ts_sums<1>(A, S, S.pd);
+  TS_MARK(8);
+  if (t == 0) atomicAdd(A.dsteps, 1ULL);
+}
+
+}  // namespace sro

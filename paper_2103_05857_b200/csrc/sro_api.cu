@@ -30,6 +30,7 @@
 #include "k_bcfw.cuh"
 #include "k_bcfw_pipe.cuh"
 #include "k_block.cuh"
+#include "k_block_tail.cuh"
 #include "k_plan.cuh"
 #include "k_sweep.cuh"
 #include "sro_device.cuh"
@@ -141,6 +142,7 @@ struct Solver {
   double cmax = -1.0;           // max cost, computed once (ensure_cmax)
   bool no_rf = getenv("SRO_NO_RF") != nullptr;      // debug: force the shared-memory kernel
   bool no_tail = getenv("SRO_NO_TAIL") != nullptr;  // debug: force the multi-kernel block step
+  bool no_smtail = getenv("SRO_NO_SMTAIL") != nullptr;  // debug: force the global-memory single-CTA tail
   // debug: no pipelined BCFW kernel (k_bcfw_pipe.cuh) -> register-file kernel k_bcfw_rf
   bool no_pipe = getenv("SRO_NO_PIPE") != nullptr || getenv("SRO_NO_RF") != nullptr;
   sro_stats stats{};
@@ -993,6 +995,7 @@ BlockArgs block_args(Solver* s, const int* col0_dev, int col0_mul, int L, int st
   A.dsteps = s->dsteps;
   A.G = s->G; A.shard = s->shard; A.slot_len = s->lead->slot_len; A.x1 = s->lead->x1; A.x2 = s->lead->x2;
   A.capfail = s->G > 1 ? s->capfail : nullptr;
+  A.phase = s->phase;
   return A;
 }
 
@@ -1009,7 +1012,13 @@ sro_status plain_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
   st = sweep(s, col0_dev, col0_mul, 0, L, s->sw_j, s->sw_min, s->sw_g, stop);
   if (st) return st;
   BlockArgs A = block_args(s, col0_dev, col0_mul, L, step_rule, nprime, stop_check, trace_dev);
-  if (L <= 1024 && !s->no_tail) {
+  if (L <= 1024 && !s->no_tail && !s->no_smtail && s->m < (1 << 20) - 1) {
+    // pairs resident in shared memory (k_block_tail.cuh)
+    CUDA_TRY(s, set_dyn_smem((const void*)k_block_tail_sm, s->device, (int)TAIL_SM_BYTES));
+    k_block_tail_sm<<<1, 1024, TAIL_SM_BYTES, s->stream>>>(A);
+    CUDA_TRY(s, cudaGetLastError());
+    s->lead->stats.kernel_launches += 1;
+  } else if (L <= 1024 && !s->no_tail) {
     CUDA_TRY(s, set_dyn_smem((const void*)k_block_tail, s->device, TAIL_SMEM));
     k_block_tail<<<1, 1024, TAIL_SMEM, s->stream>>>(A);
     CUDA_TRY(s, cudaGetLastError());
