@@ -14,12 +14,41 @@
 //     of the 256-leaf adjacent-pair tree (zero leaves are identities);
 //   * the denominator is the 256-chunk sum over the m rows of Delta_k^2 with the
 //     touched rows (ascending) found per chunk by binary search.
+// When the LMO sweep left per-slab partials, the tail merges them itself
+// (thread per column, slab order) and evaluates the column gaps (Eq. 11) —
+// the k_lmo_merge launch folded into this one.
 // Steps whose pair count exceeds TS_PMAX run the global-memory tail instead.
 // Host side: used for L <= 1024 and m < 2^20 (the row field of a key).
 #pragma once
 #include "k_block.cuh"
+#include "k_sweep.cuh"
 
 namespace sro {
+
+// The sweep's slab partials and the cost source for the gap epilogue.
+struct TailMerge {
+  int nslabs;            // <= 1: the sweep wrote the final j / minval / g itself
+  const int* pj;         // [nslabs * L] partial argmin rows
+  const double* pmin;    // [nslabs * L] partial minima
+  int* j;                // outputs over U (the arrays BlockArgs::j / minval / g read)
+  double* minval;
+  double* g;
+  int kind;              // 0/1 dense f32/f64; 2/3 colour f32 sqeuclid/euclid; 4/5 colour f64 sqeuclid/euclid
+  const void* C;
+  int64_t ld;
+  const void* x;
+  const void* y;
+};
+__device__ __forceinline__ double tm_cost(const TailMerge& M, int k, int i) {
+  switch (M.kind) {
+    case 0: return SrcDense<float>{(const float*)M.C, M.ld}.cost(k, i);
+    case 1: return SrcDense<double>{(const double*)M.C, M.ld}.cost(k, i);
+    case 2: return SrcColour<float, false>{(const float*)M.x, (const float*)M.y}.cost(k, i);
+    case 3: return SrcColour<float, true>{(const float*)M.x, (const float*)M.y}.cost(k, i);
+    case 4: return SrcColour<double, false>{(const double*)M.x, (const double*)M.y}.cost(k, i);
+    default: return SrcColour<double, true>{(const double*)M.x, (const double*)M.y}.cost(k, i);
+  }
+}
 
 constexpr int TS_PMAX = 4096;   // pairs held in shared memory
 constexpr int TS_SORT = 8192;   // bitonic buffer (power of two >= TS_PMAX)
@@ -286,18 +315,40 @@ __device__ __forceinline__ void ts_den(const BlockArgs& A, TailSmem& S, double* 
 }
 
 
-__global__ void __launch_bounds__(1024, 1) k_block_tail_sm(BlockArgs A) {
+__global__ void __launch_bounds__(1024, 1) k_block_tail_sm(BlockArgs A, TailMerge M) {
   extern __shared__ __align__(16) unsigned char tail_raw[];
 #ifdef SRO_PHASE_TIMING
   long long ts_t = clock64();
 #endif
   TailSmem& S = *reinterpret_cast<TailSmem*>(tail_raw);
-  if (*A.status) return;
+  if (*A.status || (A.stop && *A.stop)) return;
   const int t = threadIdx.x, L = A.L;
+  const int col0 = block_col0(A);
+  if (M.nslabs > 1) {
+    // LMO merge over the slabs (argmin, lowest row on ties: R1) and the column
+    // gap g_i = sum_{k in supp, ascending} t_ki (C_ki + h_k) - b_i min_k (C_ki + h_k)
+    if (t < L) {
+      const int i = col0 + t;
+      double best = __longlong_as_double(0x7ff0000000000000LL);
+      int bj = 0x7fffffff;
+      for (int q = 0; q < M.nslabs; q++) argmin_merge(best, bj, M.pmin[(int64_t)q * L + t], M.pj[(int64_t)q * L + t]);
+      if (!(best < 1.0e308 && best > -1.0e308)) set_status(A.status, 5);
+      const int c = A.cnt[i];
+      double dot = 0.0;
+      for (int e = 0; e < c; e++) {
+        const int k = A.srow[(int64_t)i * A.cap + e];
+        dot = d_add(dot, d_mul(A.sval[(int64_t)i * A.cap + e], d_add(tm_cost(M, k, i), A.h[k])));
+      }
+      M.j[t] = bj;
+      M.minval[t] = best;
+      M.g[t] = d_sub(dot, d_mul(A.b[i], best));
+    }
+    __syncthreads();
+    if (*A.status) return;
+  }
   dev_psumW(A.g, L, 256, A.scal + 0, A.eps, A.stop);        // G_U (FW: stop check)
   TS_MARK(0);
   if (A.stop && *A.stop) return;
-  const int col0 = block_col0(A);
   // merged support sizes -> offsets
   int i = 0, j = 0, Mp = 0;
   double bi = 0.0;

@@ -118,6 +118,8 @@ struct Solver {
   int* part_j = nullptr;      // slab partials
   double* part_min = nullptr;
   int64_t part_cap = 0;
+  bool defer_merge = false;   // the next sweep leaves its slab partials to the block tail
+  int last_nslabs = 1;        // slabs of the last sweep
   // block-step workspace
   int64_t blk_L = 0, blk_P = 0;
   int *pcount = nullptr, *poff = nullptr, *ptotal = nullptr, *prow = nullptr, *ppos = nullptr;
@@ -553,13 +555,14 @@ sro_status sweep_bulk(Solver* s, Src src, const int* col0_dev, int col0_mul, int
   if (nslabs == 1) { o.j = out_j; o.minval = out_min; o.g = out_g; }
   else { o.j = s->part_j; o.minval = s->part_min; o.g = nullptr; }
   const int tr = timed_begin(s);
-  s->lead->stats.kernel_launches += nslabs > 1 ? 2 : 1;
+  s->lead->stats.kernel_launches += (nslabs > 1 && !s->defer_merge) ? 2 : 1;
   s->lead->stats.sweep_launches += 1;
   s->lead->stats.sweep_columns += L;
   kern<<<(int)nb, BULK_WARPS * 32, smem, s->stream>>>(src, s->m, slab, nslabs, s->h, col0_dev, col0_mul, col0_host, L,
                                                     s->cnt, s->srow, s->sval, s->cap, s->b, o, stop, s->status);
   CUDA_TRY(s, cudaGetLastError());
-  if (nslabs > 1) {
+  s->last_nslabs = nslabs;
+  if (nslabs > 1 && !s->defer_merge) {
     int gm = (L + SWEEP_WARPS - 1) / SWEEP_WARPS;
     if (gm > s->num_sms * 8) gm = s->num_sms * 8;
     k_lmo_merge<Src><<<gm, SWEEP_THREADS, 0, s->stream>>>(src, nslabs, s->h, col0_dev, col0_mul, col0_host, L, s->cnt,
@@ -606,14 +609,15 @@ sro_status sweep(Solver* s, const int* col0_dev, int col0_mul, int col0_host, in
     if (nslabs == 1) { o.j = out_j; o.minval = out_min; o.g = out_g; }
     else { o.j = s->part_j; o.minval = s->part_min; o.g = nullptr; }
     const int tr = timed_begin(s);
-    s->lead->stats.kernel_launches += nslabs > 1 ? 2 : 1;
+    s->lead->stats.kernel_launches += (nslabs > 1 && !s->defer_merge) ? 2 : 1;
     s->lead->stats.sweep_launches += 1;
     s->lead->stats.sweep_columns += L;
     kern<<<dim3(gx, nslabs), SWEEP_THREADS, smem, s->stream>>>(src, s->m, slab, s->h, col0_dev, col0_mul, col0_host, L,
                                                              s->cnt, s->srow, s->sval, s->cap, s->b, o, stop,
                                                              s->status);
     CUDA_TRY(s, cudaGetLastError());
-    if (nslabs > 1) {
+    s->last_nslabs = nslabs;
+    if (nslabs > 1 && !s->defer_merge) {
       int gm = (L + SWEEP_WARPS - 1) / SWEEP_WARPS;
       if (gm > s->num_sms * 8) gm = s->num_sms * 8;
       k_lmo_merge<Src><<<gm, SWEEP_THREADS, 0, s->stream>>>(src, nslabs, s->h, col0_dev, col0_mul, col0_host, L,
@@ -1009,13 +1013,23 @@ sro_status plain_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
   if (st) return st;
   const int trb = timed_begin(s);
   int* stop = stop_check ? s->stop : nullptr;
+  const bool smtail = L <= 1024 && !s->no_tail && !s->no_smtail && s->m < (1 << 20) - 1;
+  s->defer_merge = smtail;
   st = sweep(s, col0_dev, col0_mul, 0, L, s->sw_j, s->sw_min, s->sw_g, stop);
+  s->defer_merge = false;
   if (st) return st;
   BlockArgs A = block_args(s, col0_dev, col0_mul, L, step_rule, nprime, stop_check, trace_dev);
-  if (L <= 1024 && !s->no_tail && !s->no_smtail && s->m < (1 << 20) - 1) {
-    // pairs resident in shared memory (k_block_tail.cuh)
+  if (smtail) {
+    // pairs resident in shared memory (k_block_tail.cuh); the sweep's slab merge folded in
+    TailMerge M{};
+    M.nslabs = s->last_nslabs; M.pj = s->part_j; M.pmin = s->part_min;
+    M.j = s->sw_j; M.minval = s->sw_min; M.g = s->sw_g;
+    const bool dense = s->kind == SRO_COST_DENSE || s->kind == SRO_COST_HASH_UNIFORM;
+    const bool f32 = s->prec == SRO_FP32, eu = s->kind == SRO_COST_EUCLID;
+    M.kind = dense ? (f32 ? 0 : 1) : (f32 ? (eu ? 3 : 2) : (eu ? 5 : 4));
+    M.C = s->C; M.ld = s->ld; M.x = s->x; M.y = s->y;
     CUDA_TRY(s, set_dyn_smem((const void*)k_block_tail_sm, s->device, (int)TAIL_SM_BYTES));
-    k_block_tail_sm<<<1, 1024, TAIL_SM_BYTES, s->stream>>>(A);
+    k_block_tail_sm<<<1, 1024, TAIL_SM_BYTES, s->stream>>>(A, M);
     CUDA_TRY(s, cudaGetLastError());
     s->lead->stats.kernel_launches += 1;
   } else if (L <= 1024 && !s->no_tail) {
