@@ -68,9 +68,11 @@ struct TailSmem {
   int rowrun[TS_PMAX + 1];  // touched row -> its first run
   int rrow[TS_PMAX];      // touched rows, ascending
   int hot[TS_PMAX / 8];   // touched rows with more than TS_SMALL (= 8) runs
+  double gcol[1024];       // column gaps over U (G_U = psum256 of them)
   int wsum[32];
-  int misc[8];
+  int misc[8];            // [0] touched rows [1] runs [2] hot rows [3] abort flag
   double red[8];
+  double bc[4];           // broadcasts: [2] gamma
 };
 static_assert(sizeof(TailSmem) + 1408 <= 232448, "k_block_tail_sm shared memory");
 constexpr size_t TAIL_SM_BYTES = sizeof(TailSmem) > 32 * 256 * 8 ? sizeof(TailSmem) : 32 * 256 * 8;
@@ -291,8 +293,32 @@ __device__ __forceinline__ void ts_sums(const BlockArgs& A, TailSmem& S, const d
   __syncthreads();
 }
 
-// psum256 over the m rows of X (zero off the touched rows) -> *out. 1024 threads.
-__device__ __forceinline__ void ts_den(const BlockArgs& A, TailSmem& S, double* out) {
+// Step size (ELS, Eq. 10 / A.1 / joint block search; or DEC 2n'/(k'+2n')) from
+// G_U and the denominator, by one thread; scal[1..3] and the trace as dev_gamma.
+__device__ __forceinline__ double ts_gamma(const BlockArgs& A, double GU, double den) {
+  const double num = d_mul(A.lambda, GU);
+  double gamma;
+  if (A.step_rule == 1) {
+    if (!(num > 0.0) || den == 0.0) gamma = 0.0;
+    else { gamma = d_div(num, den); if (gamma > 1.0) gamma = 1.0; }
+  } else {
+    gamma = d_div((double)(2LL * A.nprime), (double)(A.kk + 2LL * A.nprime));
+  }
+  A.scal[1] = den;
+  A.scal[2] = gamma;
+  A.scal[3] = num;
+  if (A.trace) {
+    double* tr = A.trace;
+    tr[0] = (double)A.kk; tr[1] = A.col0_dev ? (*A.col0_dev) * A.trace_col0_mul : 0; tr[2] = A.j[0]; tr[3] = -1;
+    tr[4] = 0; tr[5] = gamma; tr[6] = num; tr[7] = den; tr[8] = A.minval[0];
+  }
+  return gamma;
+}
+
+// Denominator: psum256 over the m rows of Delta_k^2 (zero off the touched
+// rows; ascending touched rows found per chunk by binary search), then gamma
+// -> S.bc[2] for every thread. 1024 threads.
+__device__ __forceinline__ double ts_den_gamma(const BlockArgs& A, TailSmem& S, double GU) {
   const int T = S.misc[0];
   const int c = threadIdx.x;
   double acc = 0.0;
@@ -309,11 +335,29 @@ __device__ __forceinline__ void ts_den(const BlockArgs& A, TailSmem& S, double* 
     double v = (c < 8) ? S.red[c] : 0.0;
 #pragma unroll
     for (int o = 1; o < 8; o <<= 1) v = d_add(v, __shfl_xor_sync(FULL, v, o));
-    if (c == 0) *out = v;
+    if (c == 0) S.bc[2] = ts_gamma(A, GU, v);
   }
   __syncthreads();
+  return S.bc[2];
 }
 
+// merged support supp(t_i) U {j} in ascending rows from a register copy of
+// the first KP support entries (c <= KP): entry e -> (row, told)
+template <int KP, class F>
+__device__ __forceinline__ void for_merged_reg(int c, const int* crow, const double* cval, int j, F f) {
+  int e_out = 0;
+  bool ins = false;
+#pragma unroll
+  for (int e = 0; e < KP; e++) {
+    if (e < c) {
+      const int rw = crow[e];
+      if (!ins && j < rw) { f(e_out++, j, 0.0); ins = true; }
+      if (rw == j) ins = true;
+      f(e_out++, rw, cval[e]);
+    }
+  }
+  if (!ins) f(e_out++, j, 0.0);
+}
 
 __global__ void __launch_bounds__(1024, 1) k_block_tail_sm(BlockArgs A, TailMerge M) {
   extern __shared__ __align__(16) unsigned char tail_raw[];
@@ -322,41 +366,108 @@ __global__ void __launch_bounds__(1024, 1) k_block_tail_sm(BlockArgs A, TailMerg
 #endif
   TailSmem& S = *reinterpret_cast<TailSmem*>(tail_raw);
   if (*A.status || (A.stop && *A.stop)) return;
-  const int t = threadIdx.x, L = A.L;
+  TS_MARK(12);
+  const int t = threadIdx.x, L = A.L, cap = A.cap;
   const int col0 = block_col0(A);
+  const int i = col0 + t;
+  const bool own = t < L;
+  // Per-column state of column i = col0 + t in registers, loaded in one round
+  // trip: support size, its first KP entries (read whether or not they are in
+  // use), b_i, and the sweep's j / g when it merged its slabs itself.
+  constexpr int KP = 4;
+  int c = 0, j = 0;
+  int crow[KP];
+  double cval[KP];
+  double bi = 0.0, gcol = 0.0;
+#pragma unroll
+  for (int e = 0; e < KP; e++) { crow[e] = 0; cval[e] = 0.0; }
+  if (own) {
+    c = A.cnt[i];
+    bi = A.b[i];
+    crow[0] = A.srow[(int64_t)i * cap];   // every support has an entry (b_i > 0)
+    cval[0] = A.sval[(int64_t)i * cap];
+    if (M.nslabs <= 1) { j = A.j[t]; gcol = A.g[t]; }
+#pragma unroll
+    for (int e = 1; e < KP; e++)
+      if (e < c) { crow[e] = A.srow[(int64_t)i * cap + e]; cval[e] = A.sval[(int64_t)i * cap + e]; }
+  }
+  if (t == 0) S.misc[3] = 0;
   if (M.nslabs > 1) {
-    // LMO merge over the slabs (argmin, lowest row on ties: R1) and the column
-    // gap g_i = sum_{k in supp, ascending} t_ki (C_ki + h_k) - b_i min_k (C_ki + h_k)
-    if (t < L) {
-      const int i = col0 + t;
+    // LMO merge over the slabs (argmin, lowest row on ties: R1 — the result does
+    // not depend on the merge order): R = 1024 / L threads per column each merge
+    // a strided subset of the slabs (8 loads in flight), then one combines the R
+    // results and evaluates the column gap (Eq. 11)
+    // g_i = sum_{k in supp, ascending} t_ki (C_ki + h_k) - b_i min_k (C_ki + h_k).
+    const int R = 1024 / L;
+    double* mv = S.pd;   // free until the pairs are generated
+    int* mj = S.prow;
+    if (t < R * L) {
+      const int p = t % L, r = t / L;
       double best = __longlong_as_double(0x7ff0000000000000LL);
       int bj = 0x7fffffff;
-      for (int q = 0; q < M.nslabs; q++) argmin_merge(best, bj, M.pmin[(int64_t)q * L + t], M.pj[(int64_t)q * L + t]);
-      if (!(best < 1.0e308 && best > -1.0e308)) set_status(A.status, 5);
-      const int c = A.cnt[i];
-      double dot = 0.0;
-      for (int e = 0; e < c; e++) {
-        const int k = A.srow[(int64_t)i * A.cap + e];
-        dot = d_add(dot, d_mul(A.sval[(int64_t)i * A.cap + e], d_add(tm_cost(M, k, i), A.h[k])));
+      for (int q0 = r; q0 < M.nslabs; q0 += 8 * R) {
+        double pv[8];
+        int pjv[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          const int q = q0 + u * R;
+          const bool in = q < M.nslabs;
+          pv[u] = in ? M.pmin[(int64_t)q * L + p] : __longlong_as_double(0x7ff0000000000000LL);
+          pjv[u] = in ? M.pj[(int64_t)q * L + p] : 0x7fffffff;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) argmin_merge(best, bj, pv[u], pjv[u]);
       }
-      M.j[t] = bj;
-      M.minval[t] = best;
-      M.g[t] = d_sub(dot, d_mul(A.b[i], best));
+      mv[t] = best;
+      mj[t] = bj;
     }
     __syncthreads();
-    if (*A.status) return;
+    TS_MARK(11);
+    if (own) {
+      double best = mv[t];
+      int bj = mj[t];
+      for (int r = 1; r < R; r++) argmin_merge(best, bj, mv[r * L + t], mj[r * L + t]);
+      if (!(best < 1.0e308 && best > -1.0e308)) { set_status(A.status, 5); S.misc[3] = 1; }
+      double dot = 0.0;
+      if (c <= KP) {
+        double term[KP];
+#pragma unroll
+        for (int e = 0; e < KP; e++)
+          term[e] = e < c ? d_mul(cval[e], d_add(tm_cost(M, crow[e], i), A.h[crow[e]])) : 0.0;
+#pragma unroll
+        for (int e = 0; e < KP; e++)
+          if (e < c) dot = d_add(dot, term[e]);
+      } else {
+        for (int e = 0; e < c; e++) {
+          const int k = A.srow[(int64_t)i * cap + e];
+          dot = d_add(dot, d_mul(A.sval[(int64_t)i * cap + e], d_add(tm_cost(M, k, i), A.h[k])));
+        }
+      }
+      j = bj;
+      gcol = d_sub(dot, d_mul(bi, best));
+      M.j[t] = bj;
+      M.minval[t] = best;
+      M.g[t] = gcol;
+    }
   }
-  dev_psumW(A.g, L, 256, A.scal + 0, A.eps, A.stop);        // G_U (FW: stop check)
+  if (own) S.gcol[t] = gcol;
+  __syncthreads();
+  TS_MARK(10);
+  if (S.misc[3]) return;
+  const double GU = dev_psumW(S.gcol, L, 256, A.scal + 0, A.eps, A.stop);   // G_U (FW: stop check)
   TS_MARK(0);
-  if (A.stop && *A.stop) return;
+  if (A.stop && GU <= *A.eps) return;
   // merged support sizes -> offsets
-  int i = 0, j = 0, Mp = 0;
-  double bi = 0.0;
-  if (t < L) {
-    i = col0 + t;
-    j = A.j[t];
-    bi = A.b[i];
-    Mp = merged_count(A, i, j);
+  int Mp = 0;
+  if (own) {
+    bool in = false;
+    if (c <= KP) {
+#pragma unroll
+      for (int e = 0; e < KP; e++) in |= (e < c && crow[e] == j);
+    } else {
+      for (int e = 0; e < c; e++) in |= (A.srow[(int64_t)i * cap + e] == j);
+    }
+    Mp = c + (in ? 0 : 1);
   }
   int P;
   const int off = block_scan1024(Mp, S.wsum, &P);
@@ -365,16 +476,18 @@ __global__ void __launch_bounds__(1024, 1) k_block_tail_sm(BlockArgs A, TailMerg
     dev_tail_rest(A, reinterpret_cast<double*>(tail_raw));
     return;
   }
-  if (t < L) {
+  if (own) {
     const int c_t = chunk_index(t, L, 256);
-    for_merged(A, i, j, [&](int e, int row, double told) {
+    auto put = [&](int e, int row, double told) {
       const int q = off + e;
       S.prow[q] = row;
       S.ptold[q] = told;
       S.pd[q] = d_sub(row == j ? bi : 0.0, told);
       S.pchunk[q] = (uint8_t)c_t;
       S.key[q] = ((uint32_t)row << 12) | (uint32_t)q;
-    });
+    };
+    if (c <= KP) for_merged_reg<KP>(c, crow, cval, j, put);
+    else for_merged(A, i, j, put);
   }
   int Pp = 1024;
   while (Pp < P) Pp <<= 1;
@@ -393,28 +506,25 @@ __global__ void __launch_bounds__(1024, 1) k_block_tail_sm(BlockArgs A, TailMerg
   TS_MARK(9);
   ts_sums<0>(A, S, S.pd);
   TS_MARK(4);
-  ts_den(A, S, A.scal + 1);
-  dev_gamma(A);
-  __syncthreads();
+  const double gamma = ts_den_gamma(A, S, GU);
   TS_MARK(5);
   // capacity check before anything is mutated
-  const double gamma = A.scal[2];
   const double omg = d_sub(1.0, gamma);
   const double gb = d_mul(gamma, bi);
-  if (t < L) {
+  if (own) {
     int keep = 0;
     for (int q = off; q < off + Mp; q++) {
       double tn = d_mul(omg, S.ptold[q]);
       if (S.prow[q] == j) tn = d_add(tn, gb);
       keep += (tn != 0.0);
     }
-    if (keep > A.cap) set_status(A.status, 6);
+    if (keep > cap) { set_status(A.status, 6); S.misc[3] = 1; }
   }
   __syncthreads();
   TS_MARK(6);
-  if (*A.status) return;
+  if (S.misc[3]) return;
   // t_i <- (1-gamma) t_i + gamma s_i; exact zeros dropped (R13); Delta' = t' - t
-  if (t < L) {
+  if (own) {
     int keep = 0;
     for (int q = off; q < off + Mp; q++) {
       const double told = S.ptold[q];
@@ -422,8 +532,8 @@ __global__ void __launch_bounds__(1024, 1) k_block_tail_sm(BlockArgs A, TailMerg
       if (S.prow[q] == j) tn = d_add(tn, gb);
       S.pd[q] = d_sub(tn, told);
       if (tn != 0.0) {
-        A.srow[(int64_t)i * A.cap + keep] = S.prow[q];
-        A.sval[(int64_t)i * A.cap + keep] = tn;
+        A.srow[(int64_t)i * cap + keep] = S.prow[q];
+        A.sval[(int64_t)i * cap + keep] = tn;
         keep++;
       }
     }

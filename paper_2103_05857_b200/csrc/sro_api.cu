@@ -512,6 +512,11 @@ sro_status exchange(Solver* s, double* buf, size_t count) {
   return SRO_OK;
 }
 
+bool getenv_slab_fixed() {
+  static const bool fixed = getenv("SRO_SLAB") != nullptr;   // debug / A-B: the slab the environment names
+  return fixed;
+}
+
 sro_status ensure_partials(Solver* s, int nslabs, int L) {
   if (nslabs > 1 && (int64_t)nslabs * L > s->part_cap) {
     sfree(s->part_j, s->stream); sfree(s->part_min, s->stream);
@@ -577,23 +582,30 @@ sro_status sweep_bulk(Solver* s, Src src, const int* col0_dev, int col0_mul, int
 // LMO sweep over [col0, col0+L) -> out_j, out_min, out_g (device arrays of length >= L).
 sro_status sweep(Solver* s, const int* col0_dev, int col0_mul, int col0_host, int L, int* out_j, double* out_min,
                  double* out_g, const int* stop) {
-  const int slab = s->slab_rows;
-  const int nslabs = (s->m + slab - 1) / slab;
-  if (nslabs > 1 && (int64_t)nslabs * L > s->part_cap) {
-    sfree(s->part_j, s->stream); sfree(s->part_min, s->stream);
-    s->part_cap = (int64_t)nslabs * L;
-    CUDA_TRY(s, salloc(&s->part_j, s->part_cap, s->stream));
-    CUDA_TRY(s, salloc(&s->part_min, s->part_cap, s->stream));
-  }
   return with_sweep_src(s, [&](auto src) -> sro_status {
     using Src = decltype(src);
     if constexpr (Src::PLANAR) {
       if (!s->sweep_ldg) return sweep_bulk(s, src, col0_dev, col0_mul, col0_host, L, out_j, out_min, out_g, stop);
     }
+    int slab = s->slab_rows;
+    // several columns per warp when there are enough columns to fill the GPU that
+    // way; a block with few columns (batched) splits the rows into more, shorter
+    // slabs instead, so that about two CTAs per SM still get work
+    bool multi = Src::COLS > 1 && (int64_t)L * ((s->m + slab - 1) / slab) >=
+                                      (int64_t)s->num_sms * SWEEP_WARPS * Src::COLS * 2;
+    if (Src::COLS > 1 && !multi && !getenv_slab_fixed()) {
+      multi = true;
+      const int64_t per_slab = (L + SWEEP_WARPS * Src::COLS - 1) / (SWEEP_WARPS * Src::COLS);
+      const int64_t want = std::max<int64_t>(1, (int64_t)s->num_sms * 2 / per_slab);
+      int64_t rows_want = (s->m + want - 1) / want;
+      rows_want = (rows_want + 31) / 32 * 32;
+      if (rows_want < 128) rows_want = 128;
+      if (rows_want < slab) slab = (int)rows_want;
+    }
+    const int nslabs = (s->m + slab - 1) / slab;
+    { sro_status st = ensure_partials(s, nslabs, L); if (st) return st; }
     const int rows = s->m < slab ? s->m : slab;
     const size_t smem = sizeof(double) * (size_t)((rows + 1) & ~1) + (size_t)Src::SMEM_PER_ROW * rows;
-    // several columns per warp only when there are enough columns to fill the GPU that way
-    const bool multi = Src::COLS > 1 && (int64_t)L * nslabs >= (int64_t)s->num_sms * SWEEP_WARPS * Src::COLS * 2;
     const int cols = multi ? Src::COLS : 1;
     auto kern = multi ? k_lmo_sweep<Src, Src::COLS> : k_lmo_sweep<Src, 1>;
     CUDA_TRY(s, set_dyn_smem((const void*)kern, s->device, (int)smem));

@@ -13,7 +13,7 @@ from sro_inputs import instance  # noqa: E402
 
 L = sro.load_library()
 L.sro_debug_phase.argtypes = [ct.c_void_p, ct.c_void_p]
-names = ["G_U", "count+scan", "pairs", "sort", "sums0", "den+gamma", "cap", "update", "sums1", "structure"]
+names = ["G_U", "count+scan", "pairs", "sort", "sums0", "den+gamma", "cap", "update", "sums1", "structure", "merge:epi", "merge:partials", "entry"]
 for cfg, B in ((1, 256), (2, 256), (4, 1024)):
     d = instance(cfg, seed=0)
     if cfg == 1:
@@ -24,5 +24,5 @@ for cfg, B in ((1, 256), (2, 256), (4, 1024)):
     s.solve(sro.SRO_BATCHED, steps, seed=1, epsilon=-1.0, step=sro.STEP_ELS, sampling=sro.SAMPLE_P, block_size=B)
     ph = np.zeros(16, dtype=np.int64)
     L.sro_debug_phase(s.h, ph.ctypes.data_as(ct.c_void_p))
-    print(cfg, B, "cycles/step", round(ph[:10].sum() / steps), {n: round(float(v) / steps) for n, v in zip(names, ph)})
+    print(cfg, B, "cycles/step", round(ph[:13].sum() / steps), {n: round(float(v) / steps) for n, v in zip(names, ph)})
     s.close()
