@@ -1265,13 +1265,13 @@ sro_status build_shard(Solver* s, const double* a, const double* b_loc, const do
   ALLOC(s->a, m); ALLOC(s->b, n); ALLOC(s->b_full, s->n_glob); ALLOC(s->r, m); ALLOC(s->h, m);
   ALLOC(s->cnt, n); ALLOC(s->srow, (size_t)n * s->cap); ALLOC(s->sval, (size_t)n * s->cap);
   if (s->G == 1) { ALLOC(s->G_ga, n); ALLOC(s->fen, (size_t)n + 1); }
-  ALLOC(s->phase, 16);
+  ALLOC(s->phase, 32);
   ALLOC(s->dsteps, 1);
   ALLOC(s->status, 1); ALLOC(s->steps_done, 1); ALLOC(s->stop, 1); ALLOC(s->scal, 8); ALLOC(s->epsd, 1);
   ALLOC(s->sw_j, n); ALLOC(s->sw_min, (size_t)(m > n ? m : n)); ALLOC(s->sw_g, (size_t)(m > n ? m : n));
 #undef ALLOC
   cudaMemsetAsync(s->dsteps, 0, sizeof(unsigned long long), s->stream);
-  cudaMemsetAsync(s->phase, 0, 16 * sizeof(long long), s->stream);
+  cudaMemsetAsync(s->phase, 0, 32 * sizeof(long long), s->stream);
   cudaMemsetAsync(s->status, 0, sizeof(int), s->stream);
   cudaMemcpyAsync(s->a, a, sizeof(double) * m, cudaMemcpyHostToDevice, s->stream);
   cudaMemcpyAsync(s->b, b_loc, sizeof(double) * n, cudaMemcpyHostToDevice, s->stream);
@@ -1818,7 +1818,7 @@ sro_status sro_get_stats(sro_handle h, sro_stats* out, int32_t reset) {
 sro_status sro_debug_phase(sro_handle h, long long* out8) {
   if (!h || !out8) return SRO_ERR_INVALID_ARG;
   Solver* s = static_cast<Solver*>(h);
-  CUDA_TRY(s, cudaMemcpyAsync(out8, s->phase, 16 * sizeof(long long), cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(s, cudaMemcpyAsync(out8, s->phase, 32 * sizeof(long long), cudaMemcpyDeviceToHost, s->stream));
   CUDA_TRY(s, stream_wait(s));
   return SRO_OK;
 }

@@ -17,7 +17,7 @@ d = instance(1, seed=0)
 names = ["top(u53)", "slab+mask", "cw+gk+supp", "BAR_PART", "merge", "serial", "refresh+fenwick", "draw"]
 s = sro.Solver(d["a"], d["b"], 1.0, C=d["C32"], prec="f32")
 s.solve(1, 4096 * 4, seed=1, epsilon=-1.0, step=1, sampling=2, ga_M=1, ga_inner=1, ga_post_update=1)
-ph = np.zeros(16, dtype=np.int64)
+ph = np.zeros(32, dtype=np.int64)
 L.sro_debug_phase(s.h, ph.ctypes.data_as(ct.c_void_p))
 steps = 4096 * 4
 print("ga warp0 cycles/step", round(ph[:8].sum() / steps, 1), {n: round(float(v) / steps, 1) for n, v in zip(names, ph[:8])})

@@ -21,7 +21,7 @@ for name, var, kw in [("bcfw-P-ELS", 1, dict(step=1, sampling=1)), ("bcpfw-U", 3
                       ("bcafw-U", 2, dict(step=1, sampling=0))]:
     s = sro.Solver(d["a"], d["b"], 1.0, C=d["C32"], prec="f32")
     s.solve(var, 4096 * 4, seed=1, epsilon=-1.0, **kw)
-    ph = np.zeros(16, dtype=np.int64)
+    ph = np.zeros(32, dtype=np.int64)
     L.sro_debug_phase(s.h, ph.ctypes.data_as(ct.c_void_p))
     steps = 4096 * 4
     print(name, "warp0", round(ph[:8].sum() / steps, 1), {n: round(float(v) / steps, 1) for n, v in zip(w0, ph) if v})

@@ -22,7 +22,7 @@ for cfg, B in ((1, 256), (2, 256), (4, 1024)):
         s = sro.Solver(d["a"], d["b"], 1.0, X=d["X"], Y=d["Y"], cost="sqeuclid", prec="f32")
     steps = 3 * (len(d["b"]) // B)
     s.solve(sro.SRO_BATCHED, steps, seed=1, epsilon=-1.0, step=sro.STEP_ELS, sampling=sro.SAMPLE_P, block_size=B)
-    ph = np.zeros(16, dtype=np.int64)
+    ph = np.zeros(32, dtype=np.int64)
     L.sro_debug_phase(s.h, ph.ctypes.data_as(ct.c_void_p))
     print(cfg, B, "cycles/step", round(ph[:13].sum() / steps), {n: round(float(v) / steps) for n, v in zip(names, ph)})
     s.close()
