@@ -268,6 +268,22 @@ __device__ __forceinline__ double warp_sparse_psum256_fast(int m, int cnt, int r
   int c;
   if ((m & 255) == 0 && (dm & (dm - 1)) == 0) c = valid ? (row >> (__ffs(dm) - 1)) : -1 - lane;
   else c = valid ? chunk_index(row, m, 256) : -1 - lane;
+  if (cnt <= 3) {
+    // the same tree for at most three entries, evaluated directly: runs of one
+    // chunk summed left to right from +0.0, distinct chunks merged at their
+    // lowest common ancestor (three distinct chunks: the lower of the two
+    // adjacent LCAs first; they are never equal)
+    const double x0 = __shfl_sync(FULL, x, 0), x1 = __shfl_sync(FULL, x, 1), x2 = __shfl_sync(FULL, x, 2);
+    const int c0 = __shfl_sync(FULL, c, 0), c1 = __shfl_sync(FULL, c, 1), c2 = __shfl_sync(FULL, c, 2);
+    const double v0 = d_add(0.0, x0);
+    if (cnt <= 1) return cnt == 1 ? v0 : 0.0;
+    if (cnt == 2) return c0 == c1 ? d_add(v0, x1) : d_add(v0, d_add(0.0, x1));
+    if (c0 == c1 && c1 == c2) return d_add(d_add(v0, x1), x2);
+    if (c0 == c1) return d_add(d_add(v0, x1), d_add(0.0, x2));
+    if (c1 == c2) return d_add(v0, d_add(d_add(0.0, x1), x2));
+    const double v1 = d_add(0.0, x1), v2 = d_add(0.0, x2);
+    return (31 - __clz(c0 ^ c1)) < (31 - __clz(c1 ^ c2)) ? d_add(d_add(v0, v1), v2) : d_add(v0, d_add(v1, v2));
+  }
   const int cprev = __shfl_up_sync(FULL, c, 1);
   const int cnext = __shfl_down_sync(FULL, c, 1);
   const bool start = valid && (lane == 0 || cprev != c);
