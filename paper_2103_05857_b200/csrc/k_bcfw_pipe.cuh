@@ -46,7 +46,7 @@ __device__ __forceinline__ void nbar_arrive(int id, int count) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-template <typename T, int MAXV>
+template <typename T, int MAXV, int NL = PIPE_LMO>
 struct PipeCol {
   using V = typename Vec<T>::type;
   static constexpr int W = Vec<T>::W;
@@ -59,7 +59,7 @@ struct PipeCol {
     const V* p = reinterpret_cast<const V*>(C + (int64_t)i * ld);
 #pragma unroll
     for (int u = 0; u < MAXV; u++) {
-      const int q = lt + u * PIPE_LMO;
+      const int q = lt + u * NL;
       if (q < nvec) nxt[u] = __ldg(p + q);
     }
     const int kt = nvec * W + lt;
@@ -117,12 +117,12 @@ struct PipeLayout {
 };
 
 // LMO thread index and bit of row k (rows of full vectors, then the tail rows)
-template <int W>
+template <int W, int NL = PIPE_LMO>
 __device__ __forceinline__ void pipe_owner(int k, int nvec, int& lt, unsigned& bit) {
   if (k < nvec * W) {
     const int q = k / W;
-    lt = q % PIPE_LMO;
-    bit = 1u << ((q / PIPE_LMO) * W + (k % W));
+    lt = q % NL;
+    bit = 1u << ((q / NL) * W + (k % W));
   } else {
     lt = k - nvec * W;
     bit = 1u << 31;
@@ -410,10 +410,16 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_pipe(BcfwArgs A, const
 // Fenwick update (warp 0).
 // ---------------------------------------------------------------------------
 constexpr int BAR_COL = 3;
+// The GA kernel has no slab prefetch to overlap: its column scan is on the
+// critical path, so every warp but warp 0 scans (warp 0 shares its SMSP with
+// three of them; it waits at BAR_PART while they scan).
+constexpr int GA_LMO_WARPS = PIPE_THREADS / 32 - 1;
+constexpr int GA_LMO = GA_LMO_WARPS * 32;
+constexpr int GA_SYNC = GA_LMO + 32;
 
 struct GaPipeLayout {
   __host__ __device__ static size_t fixed() {
-    return 256 * 8 + 16 * 4 * 8 + 16 * 4 * 4 + 16 * 4 + PIPE_LMO * 4;   // slots, key partials, row partials, misc, masks
+    return 256 * 8 + 16 * 4 * 8 + 16 * 4 * 4 + 16 * 4 + GA_LMO * 4;   // slots, key partials, row partials, misc, masks
   }
   __host__ __device__ static size_t bytes(int m, int n) {
     return fixed() + 4 * rup16((size_t)m * 8) + rup16((size_t)n * 4) + rup16((size_t)n * 8) +
@@ -442,7 +448,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
   unsigned long long* pk = reinterpret_cast<unsigned long long*>(p); p += 16 * 4 * 8;   // [4][16]: all, u1, u2, cval
   int* pj = reinterpret_cast<int*>(p); p += 16 * 4 * 4;                               // [4][16] rows
   volatile int* misc = reinterpret_cast<volatile int*>(p); p += 16 * 4;   // [0] = column, [2] = abort
-  unsigned* mflag = reinterpret_cast<unsigned*>(p); p += PIPE_LMO * 4;
+  unsigned* mflag = reinterpret_cast<unsigned*>(p); p += GA_LMO * 4;
   double* sh_h = reinterpret_cast<double*>(p); p += rup16((size_t)m * 8);
   double* sh_r = reinterpret_cast<double*>(p); p += rup16((size_t)m * 8);
   double* sh_a = reinterpret_cast<double*>(p); p += rup16((size_t)m * 8);
@@ -459,24 +465,24 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
   }
   for (int c = tid; c < n; c += PIPE_THREADS) { sh_cnt[c] = A.cnt[c]; Gs[c] = A.G[c]; }
   for (int c = tid; c <= n; c += PIPE_THREADS) fens[c] = A.fen[c];
-  for (int c = tid; c < PIPE_LMO; c += PIPE_THREADS) mflag[c] = 0;
+  for (int c = tid; c < GA_LMO; c += PIPE_THREADS) mflag[c] = 0;
   if (tid == 0) { misc[0] = 0; misc[2] = 0; }
   __syncthreads();
 
-  if (steps > 0 && warp > 0 && (warp & 3) != 0) {
+  if (steps > 0 && warp > 0) {
     // =================== LMO warps ===================
-    const int lw = warp - 1 - (warp >> 2);
+    const int lw = warp - 1;
     const int lt = lw * 32 + lane;
     const int kt = nvec * W + lt;
-    PipeCol<T, MAXV> col;
+    PipeCol<T, MAXV, GA_LMO> col;
     col.C = Cg; col.ld = ld; col.m = m; col.nvec = nvec;
     for (int t = 0; t < steps; t++) {
-      nbar_sync(BAR_COL, PIPE_SYNC);                   // the drawn column (or abort)
+      nbar_sync(BAR_COL, GA_SYNC);                   // the drawn column (or abort)
       if (misc[2]) break;
       const int i = misc[0];
       col.fetch(i, lt);
       col.advance();
-      nbar_sync(BAR_MASK, PIPE_SYNC);                  // its support as a mask
+      nbar_sync(BAR_MASK, GA_SYNC);                  // its support as a mask
       const unsigned mk = mflag[lt];
       mflag[lt] = 0;
       // rows outside the support only: smallest (value, row) with its C, and the
@@ -492,7 +498,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
       };
 #pragma unroll
       for (int u = 0; u < MAXV; u++) {
-        const int q = lt + u * PIPE_LMO;
+        const int q = lt + u * GA_LMO;
         if (q < nvec) {
           double hv[W];
           pipe_h(hp, nvec, q, col.cur, hv);
@@ -520,7 +526,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
         pk[lw] = k1; pj[lw] = r1; pk[16 + lw] = ((unsigned long long)h2 << 32) | l2;
         pk[48 + lw] = (unsigned long long)__double_as_longlong(cw1);
       }
-      nbar_arrive(BAR_PART, PIPE_SYNC);
+      nbar_arrive(BAR_PART, GA_SYNC);
     }
   } else if (steps > 0 && warp == 0) {
     // =================== serial warp ===================
@@ -537,7 +543,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
     int i = draw(uniform53(rng_u64(A.seed, 1, (uint64_t)A.k0)));
     if (lane == 0) misc[0] = i;
     __syncwarp();
-    nbar_arrive(BAR_COL, PIPE_SYNC);
+    nbar_arrive(BAR_COL, GA_SYNC);
     for (int s = 0; s < steps; s++) {
       const long long kk = A.k0 + s;
       PW_MARK(0);
@@ -550,11 +556,11 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
       if (lane < c0) {
         int ot;
         unsigned bit;
-        pipe_owner<W>(rw, nvec, ot, bit);
+        pipe_owner<W, GA_LMO>(rw, nvec, ot, bit);
         atomicOr(&mflag[ot], bit);
       }
       __syncwarp();
-      nbar_arrive(BAR_MASK, PIPE_SYNC);
+      nbar_arrive(BAR_MASK, GA_SYNC);
       PW_MARK(1);
       const double cw = lane < c0 ? (double)__ldg(Cg + (int64_t)i * ld + rw) : 0.0;
       // ---- partials -> LMO result (j, mv), C_ji, and the minimum outside T = supp U {j}
@@ -564,11 +570,11 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
       const int wsl = warp_argmin_key(ks, js);
       const double csup = __shfl_sync(FULL, cw, wsl);
       const double u_next = uniform53(rng_u64(A.seed, 1, (uint64_t)(kk + 1)));   // next draw's uniform (while the LMO warps scan)
-      nbar_sync(BAR_PART, PIPE_SYNC);
-      unsigned long long k1 = lane < PIPE_LMO_WARPS ? pk[lane] : ~0ULL;
-      int r1 = lane < PIPE_LMO_WARPS ? pj[lane] : 0x7fffffff;
-      const unsigned long long k2lane = lane < PIPE_LMO_WARPS ? pk[16 + lane] : ~0ULL;
-      const double cwl = lane < PIPE_LMO_WARPS ? __longlong_as_double((long long)pk[48 + lane]) : 0.0;
+      nbar_sync(BAR_PART, GA_SYNC);
+      unsigned long long k1 = lane < GA_LMO_WARPS ? pk[lane] : ~0ULL;
+      int r1 = lane < GA_LMO_WARPS ? pj[lane] : 0x7fffffff;
+      const unsigned long long k2lane = lane < GA_LMO_WARPS ? pk[16 + lane] : ~0ULL;
+      const double cwl = lane < GA_LMO_WARPS ? __longlong_as_double((long long)pk[48 + lane]) : 0.0;
       const unsigned long long k1lane = k1;
       const int w1 = warp_argmin_key(k1, r1);
       const double c1 = __shfl_sync(FULL, cwl, w1);
@@ -594,7 +600,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
           set_status(A.status, !(mv < 1.0e308 && mv > -1.0e308) ? 5 : 6);
         }
         __syncwarp();
-        if (s + 1 < steps) nbar_arrive(BAR_COL, PIPE_SYNC);
+        if (s + 1 < steps) nbar_arrive(BAR_COL, GA_SYNC);
         break;
       }
       if (A.trace && lane == 0) {
@@ -647,7 +653,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
         PW_MARK(7);
         if (lane == 0) misc[0] = i;
         __syncwarp();
-        nbar_arrive(BAR_COL, PIPE_SYNC);
+        nbar_arrive(BAR_COL, GA_SYNC);
       }
     }
     if (lane == 0) *A.steps_done = done;

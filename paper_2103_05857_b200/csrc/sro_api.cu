@@ -867,8 +867,8 @@ sro_status bcfw_try_ga_pipe(Solver* s, BcfwArgs& A) {
   if (!dense || s->no_pipe) return SRO_ERR_DIMENSION;
   const int W = s->prec == SRO_FP32 ? 4 : 2;
   const int nvec = s->m / W;
-  const int need = (nvec + PIPE_LMO - 1) / PIPE_LMO;
-  if (need > 4 || s->m - nvec * W > PIPE_LMO) return SRO_ERR_DIMENSION;
+  const int need = (nvec + GA_LMO - 1) / GA_LMO;
+  if (need > 4 || s->m - nvec * W > GA_LMO) return SRO_ERR_DIMENSION;
   const size_t bytes = GaPipeLayout::bytes(s->m, s->n);
   if (bytes > 226 * 1024) return SRO_ERR_DIMENSION;
   A.ga_smem = 1; A.a_smem = 1; A.visit_smem = 0;
