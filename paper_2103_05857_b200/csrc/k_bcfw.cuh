@@ -400,6 +400,18 @@ __device__ __forceinline__ void ga_add(double* fen, int n, int i0, double delta)
 // Same update with lane t of a warp updating the t-th node of the path (the
 // nodes are distinct, so each node receives exactly the one add it gets above).
 // With x = p - 1 a step p += p & -p sets the lowest zero bit of x (x |= x + 1).
+// The node lane t of a warp updates for leaf i0 (> n: none), so that the
+// update itself (ga_add_node) is one read-modify-write once delta is known.
+__device__ __forceinline__ long long ga_path_node(int n, int i0) {
+  const int lane = threadIdx.x & 31;
+  unsigned x = (unsigned)i0;
+  for (int t = 0; t < lane && x <= (unsigned)n; t++) x |= x + 1u;
+  return (long long)x + 1;
+}
+__device__ __forceinline__ void ga_add_node(double* fen, int n, long long p, double delta) {
+  if (p <= n) fen[p] = d_add(fen[p], delta);
+  __syncwarp();
+}
 __device__ __forceinline__ void ga_add_warp(double* fen, int n, int i0, double delta) {
   const int lane = threadIdx.x & 31;
   unsigned x = (unsigned)i0;

@@ -8,7 +8,7 @@ import bench  # noqa: E402
 d = bench.make_instance(0)
 dev = torch.device("cuda", 0)
 C32 = torch.from_numpy(np.ascontiguousarray(d["C32"].T)).pin_memory()
-for rep in range(3):
+for rep in range(int(os.environ.get("REPS", "6"))):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     Cd = C32.to(dev, non_blocking=True)
     torch.cuda.synchronize(); t1 = time.perf_counter()
