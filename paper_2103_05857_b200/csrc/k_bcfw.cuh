@@ -352,9 +352,20 @@ __device__ __forceinline__ void warp_argmax_redux(double& v, int& j, bool valid)
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ double wpos(double g) { return g > 0.0 ? g : 0.0; }
 
-__device__ __forceinline__ int ga_draw(const double* fen, const double* G, int n, double u53) {
+// fen lives in shared memory: loads through its 32-bit shared address (no
+// generic-to-shared conversion per load); clamped address, then the select.
+__device__ __forceinline__ double sh_ld_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+// SH: fen is known to be in shared memory (else any generic pointer).
+template <bool SH>
+__device__ __forceinline__ int ga_draw_t(const double* fen, const double* G, int n, double u53) {
+  const uint32_t fb = SH ? (uint32_t)__cvta_generic_to_shared(fen) : 0u;
+  auto ldn = [&](int q) { return SH ? sh_ld_f64(fb + 8u * (uint32_t)q) : fen[q]; };
   double W = 0.0;
-  for (int p = n; p > 0; p -= p & -p) W = d_add(W, fen[p]);
+  for (int p = n; p > 0; p -= p & -p) W = d_add(W, ldn(p));
   if (!(W > 0.0)) {
     int i = (int)d_mul(u53, (double)n);
     return i >= n ? n - 1 : i;
@@ -366,7 +377,10 @@ __device__ __forceinline__ int ga_draw(const double* fen, const double* G, int n
   // three levels per round: the 1 + 2 + 4 candidates of the round are loaded
   // together, so the dependent shared-memory loads drop to a third; the
   // comparisons and subtractions are the same operations in the same order.
-  auto ld = [&](int q) { return q <= n ? fen[q] : 0.0; };
+  auto ld = [&](int q) {
+    const double v = ldn(q <= n ? q : n);
+    return q <= n ? v : 0.0;
+  };
   auto level = [&](int b, double f) {
     const bool t = (pos + b <= n) && f <= u;
     const double un = d_sub(u, f);
@@ -392,6 +406,12 @@ __device__ __forceinline__ int ga_draw(const double* fen, const double* G, int n
     return n - 1;
   }
   return pos;
+}
+__device__ __forceinline__ int ga_draw(const double* fen, const double* G, int n, double u53) {
+  return ga_draw_t<false>(fen, G, n, u53);
+}
+__device__ __forceinline__ int ga_draw_sh(const double* fen, const double* G, int n, double u53) {
+  return ga_draw_t<true>(fen, G, n, u53);
 }
 
 __device__ __forceinline__ void ga_add(double* fen, int n, int i0, double delta) {
@@ -1024,7 +1044,7 @@ __global__ void __launch_bounds__(BCFW_THREADS, 1) k_bcfw_rf(BcfwArgs A, const T
       }
     }
     if (GA) {
-      if (tid == 0) misc[0] = ga_draw(fens, Gs, n, uniform53(rng_u64(A.seed, 1, (uint64_t)kk)));
+      if (tid == 0) misc[0] = ga_draw_sh(fens, Gs, n, uniform53(rng_u64(A.seed, 1, (uint64_t)kk)));
       __syncthreads();
       i = misc[0];
       col.fetch(i);

@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
     int done = 0;
     auto draw = [&](double u53) {
       int ii = 0;
-      if (lane == 0) ii = ga_draw(fens, Gs, n, u53);
+      if (lane == 0) ii = ga_draw_sh(fens, Gs, n, u53);
       return __shfl_sync(FULL, ii, 0);
     };
 #ifdef SRO_PHASE_TIMING

@@ -19,7 +19,7 @@ __global__ void k(double* out, int n, int iters) {
     for (int it = 0; it < iters; it++) {
       int ii = 0;
       const double u = uniform53(rng_u64(12345, 1, (uint64_t)(it + acc)));
-      if (threadIdx.x == 0) ii = ga_draw(fen, G, n, u);
+      if (threadIdx.x == 0) ii = ga_draw_sh(fen, G, n, u);
       acc += __shfl_sync(0xffffffffu, ii, 0) & 1;
     }
     long long t1 = clock64();
