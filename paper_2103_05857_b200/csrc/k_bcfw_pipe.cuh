@@ -29,6 +29,7 @@
 // barriers: BAR_PART (LMO partials ready: LMO warps arrive, warp 0 waits) and
 // BAR_MASK (next mask published: warp 0 arrives, LMO warps wait).
 #pragma once
+#include <type_traits>
 #include "k_bcfw.cuh"
 
 namespace sro {
@@ -487,38 +488,45 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
       mflag[lt] = 0;
       // rows outside the support only: smallest (value, row) with its C, and the
       // second smallest value (the support rows are warp 0's: it holds their C)
-      double u1 = dinf(), u2 = dinf(), c1 = 0.0;
+      // (only warps holding a support row run the variant with the mask tests)
+      double u1 = dinf(), u2 = dinf();
+      T c1 = T(0);
       int j1 = 0x7fffffff;
-      auto visit = [&](double c, double h, int k, bool masked) {
-        const double x = d_add(c, h);
-        const bool l1 = !masked && x < u1;
-        const bool l2 = !masked && !l1 && x < u2;
-        u2 = l1 ? u1 : (l2 ? x : u2);
-        u1 = l1 ? x : u1; j1 = l1 ? k : j1; c1 = l1 ? c : c1;
-      };
+      auto scan = [&](auto masked_tag) {
+        constexpr bool MASKED = decltype(masked_tag)::value;
+        auto visit = [&](T c, double h, int k, bool masked) {
+          const double x = d_add((double)c, h);
+          const bool l1 = !(MASKED && masked) && x < u1;
+          const bool l2 = !(MASKED && masked) && !l1 && x < u2;
+          u2 = l1 ? u1 : (l2 ? x : u2);
+          u1 = l1 ? x : u1; j1 = l1 ? k : j1; c1 = l1 ? c : c1;
+        };
 #pragma unroll
-      for (int u = 0; u < MAXV; u++) {
-        const int q = lt + u * GA_LMO;
-        if (q < nvec) {
-          double hv[W];
-          pipe_h(hp, nvec, q, col.cur, hv);
-          const unsigned mu = mk >> (u * W);
-          if constexpr (W == 4) {
-            visit((double)col.cur[u].x, hv[0], W * q, mu & 1u);
-            visit((double)col.cur[u].y, hv[1], W * q + 1, mu & 2u);
-            visit((double)col.cur[u].z, hv[2], W * q + 2, mu & 4u);
-            visit((double)col.cur[u].w, hv[3], W * q + 3, mu & 8u);
-          } else {
-            visit((double)col.cur[u].x, hv[0], W * q, mu & 1u);
-            visit((double)col.cur[u].y, hv[1], W * q + 1, mu & 2u);
+        for (int u = 0; u < MAXV; u++) {
+          const int q = lt + u * GA_LMO;
+          if (q < nvec) {
+            double hv[W];
+            pipe_h(hp, nvec, q, col.cur, hv);
+            const unsigned mu = mk >> (u * W);
+            if constexpr (W == 4) {
+              visit(col.cur[u].x, hv[0], W * q, mu & 1u);
+              visit(col.cur[u].y, hv[1], W * q + 1, mu & 2u);
+              visit(col.cur[u].z, hv[2], W * q + 2, mu & 4u);
+              visit(col.cur[u].w, hv[3], W * q + 3, mu & 8u);
+            } else {
+              visit(col.cur[u].x, hv[0], W * q, mu & 1u);
+              visit(col.cur[u].y, hv[1], W * q + 1, mu & 2u);
+            }
           }
         }
-      }
-      if (kt < m) visit((double)col.ctail, sh_h[kt], kt, mk >> 31);
+        if (kt < m) visit(col.ctail, sh_h[kt], kt, mk >> 31);
+      };
+      if (__any_sync(FULL, mk != 0u)) scan(std::true_type{});
+      else scan(std::false_type{});
       unsigned long long k1 = okey(u1);
       int r1 = j1;
       const int w1 = warp_argmin_key(k1, r1);
-      const double cw1 = __shfl_sync(FULL, c1, w1);
+      const double cw1 = (double)__shfl_sync(FULL, c1, w1);
       const unsigned long long k2l = lane == w1 ? okey(u2) : okey(u1);
       const unsigned h2 = __reduce_min_sync(FULL, (unsigned)(k2l >> 32));
       const unsigned l2 = __reduce_min_sync(FULL, (unsigned)(k2l >> 32) == h2 ? (unsigned)k2l : 0xffffffffu);
