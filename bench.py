@@ -122,7 +122,11 @@ class StepRunner:
         import paper_2103_05857_b200 as sro
         self.torch = torch
         self.concurrent = concurrent
-        self.streams = [torch.cuda.Stream(dev) for _ in PLAN]
+        # the sequential solves (one persistent CTA each, latency-bound, with short full-GPU gap
+        # sweeps between segments) get high-priority streams, so those sweeps are not queued
+        # behind the FW / batched solves' GPU-wide kernels
+        self.streams = [torch.cuda.Stream(dev, priority=-1 if variant in (1, 2, 3) else 0)
+                        for _, variant, _, _ in PLAN]
         self.solvers = [sro.Solver(d["a"], d["b"], 1.0, C=Cd, prec="f32", device=dev.index, stream=st.cuda_stream,
                                    ld=M) for st in self.streams]
 

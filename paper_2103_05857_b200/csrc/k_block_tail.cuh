@@ -73,6 +73,7 @@ struct TailSmem {
   int misc[8];            // [0] touched rows [1] runs [2] hot rows [3] abort flag
   double red[8];
   double bc[4];           // broadcasts: [2] gamma
+  long long tsacc[16];    // SRO_PHASE_TIMING builds: phase clocks (thread 0), added to A.phase at exit
 };
 static_assert(sizeof(TailSmem) + 1408 <= 232448, "k_block_tail_sm shared memory");
 constexpr size_t TAIL_SM_BYTES = sizeof(TailSmem) > 32 * 256 * 8 ? sizeof(TailSmem) : 32 * 256 * 8;
@@ -182,7 +183,7 @@ __device__ __forceinline__ int block_scan1024(int x, int* wsum, int* total) {
   do {                                                                   \
     if (threadIdx.x == 0) {                                              \
       const long long t_ = clock64();                                    \
-      A.phase[idx] += t_ - ts_t;                                         \
+      S.tsacc[idx] += t_ - ts_t;                                         \
       ts_t = t_;                                                         \
     }                                                                    \
   } while (0)
@@ -243,6 +244,9 @@ __device__ __forceinline__ void ts_structure(TailSmem& S, int P) {
 
 template <int MODE>
 __device__ __forceinline__ void ts_sums(const BlockArgs& A, TailSmem& S, const double* vals) {
+#ifdef SRO_PHASE_TIMING
+  const long long ts_t0 = clock64();
+#endif
   const int t = threadIdx.x;
   const int T = S.misc[0], R = S.misc[1], NH = S.misc[2];
   for (int ri = t; ri < R; ri += 1024) {
@@ -253,6 +257,9 @@ __device__ __forceinline__ void ts_sums(const BlockArgs& A, TailSmem& S, const d
     S.runv[ri] = run;
   }
   __syncthreads();
+#ifdef SRO_PHASE_TIMING
+  if (threadIdx.x == 0) S.tsacc[15] += clock64() - ts_t0;
+#endif
   auto finish = [&](int w, double D, double rk, double ak) {
     if (MODE == 0) {
       S.rX[w] = d_mul(D, D);
@@ -294,8 +301,8 @@ __device__ __forceinline__ void ts_sums(const BlockArgs& A, TailSmem& S, const d
 }
 
 // Step size (ELS, Eq. 10 / A.1 / joint block search; or DEC 2n'/(k'+2n')) from
-// G_U and the denominator, by one thread; scal[1..3] and the trace as dev_gamma.
-__device__ __forceinline__ double ts_gamma(const BlockArgs& A, double GU, double den) {
+// G_U and the denominator; scal[1..3] and the trace as dev_gamma.
+__device__ __forceinline__ double ts_gamma_value(const BlockArgs& A, double GU, double den) {
   const double num = d_mul(A.lambda, GU);
   double gamma;
   if (A.step_rule == 1) {
@@ -304,6 +311,10 @@ __device__ __forceinline__ double ts_gamma(const BlockArgs& A, double GU, double
   } else {
     gamma = d_div((double)(2LL * A.nprime), (double)(A.kk + 2LL * A.nprime));
   }
+  return gamma;
+}
+__device__ __forceinline__ void ts_gamma_record(const BlockArgs& A, double GU, double den, double gamma) {
+  const double num = d_mul(A.lambda, GU);
   A.scal[1] = den;
   A.scal[2] = gamma;
   A.scal[3] = num;
@@ -312,13 +323,15 @@ __device__ __forceinline__ double ts_gamma(const BlockArgs& A, double GU, double
     tr[0] = (double)A.kk; tr[1] = A.col0_dev ? (*A.col0_dev) * A.trace_col0_mul : 0; tr[2] = A.j[0]; tr[3] = -1;
     tr[4] = 0; tr[5] = gamma; tr[6] = num; tr[7] = den; tr[8] = A.minval[0];
   }
-  return gamma;
 }
 
 // Denominator: psum256 over the m rows of Delta_k^2 (zero off the touched
 // rows; ascending touched rows found per chunk by binary search), then gamma
-// -> S.bc[2] for every thread. 1024 threads.
+// for every thread. 1024 threads.
 __device__ __forceinline__ double ts_den_gamma(const BlockArgs& A, TailSmem& S, double GU) {
+#ifdef SRO_PHASE_TIMING
+  long long ts_t = clock64();
+#endif
   const int T = S.misc[0];
   const int c = threadIdx.x;
   double acc = 0.0;
@@ -331,14 +344,17 @@ __device__ __forceinline__ double ts_den_gamma(const BlockArgs& A, TailSmem& S, 
     if ((c & 31) == 0) S.red[c >> 5] = acc;
   }
   __syncthreads();
-  if (c < 32) {
-    double v = (c < 8) ? S.red[c] : 0.0;
+  TS_MARK(13);
+  // every warp combines the 8 warp partials and computes gamma itself (the
+  // same operations, so the same value everywhere); thread 0 records it
+  double v = ((c & 31) < 8) ? S.red[c & 31] : 0.0;
 #pragma unroll
-    for (int o = 1; o < 8; o <<= 1) v = d_add(v, __shfl_xor_sync(FULL, v, o));
-    if (c == 0) S.bc[2] = ts_gamma(A, GU, v);
-  }
-  __syncthreads();
-  return S.bc[2];
+  for (int o = 1; o < 8; o <<= 1) v = d_add(v, __shfl_xor_sync(FULL, v, o));
+  v = __shfl_sync(FULL, v, 0);
+  const double gamma = ts_gamma_value(A, GU, v);
+  if (c == 0) ts_gamma_record(A, GU, v, gamma);
+  TS_MARK(14);
+  return gamma;
 }
 
 // merged support supp(t_i) U {j} in ascending rows from a register copy of
@@ -365,6 +381,13 @@ __global__ void __launch_bounds__(1024, 1) k_block_tail_sm(BlockArgs A, TailMerg
   long long ts_t = clock64();
 #endif
   TailSmem& S = *reinterpret_cast<TailSmem*>(tail_raw);
+#ifdef SRO_PHASE_TIMING
+  if (threadIdx.x == 0) for (int q = 0; q < 16; q++) S.tsacc[q] = 0;
+  struct Flush {   // adds the phase clocks to A.phase on every exit path
+    const BlockArgs& A; TailSmem& S;
+    __device__ ~Flush() { if (threadIdx.x == 0 && A.phase) for (int q = 0; q < 16; q++) A.phase[q] += S.tsacc[q]; }
+  } ts_flush{A, S};
+#endif
   if (*A.status || (A.stop && *A.stop)) return;
   TS_MARK(12);
   const int t = threadIdx.x, L = A.L, cap = A.cap;

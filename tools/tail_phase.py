@@ -13,7 +13,7 @@ from sro_inputs import instance  # noqa: E402
 
 L = sro.load_library()
 L.sro_debug_phase.argtypes = [ct.c_void_p, ct.c_void_p]
-names = ["G_U", "count+scan", "pairs", "sort", "sums0", "den+gamma", "cap", "update", "sums1", "structure", "merge:epi", "merge:partials", "entry"]
+names = ["G_U", "count+scan", "pairs", "sort", "sums0", "den+gamma", "cap", "update", "sums1", "structure", "merge:epi", "merge:partials", "entry", "den:chunks", "den:gamma", "sums:runs"]
 for cfg, B in ((1, 256), (2, 256), (4, 1024)):
     d = instance(cfg, seed=0)
     if cfg == 1:
