@@ -46,6 +46,7 @@ struct BlockArgs {
   int* srow;
   double* sval;
   const int* col0_dev;   // block index pointer (batched) or nullptr
+  unsigned* cur;         // device step cursor (nullptr: none): col0_dev, kk and trace advance by it
   int col0_mul;          // columns of U held here (B, or B/G for a shard)
   int L;
   int W;                 // chunks over the positions held here: 256, or 256/G for a shard
@@ -94,7 +95,10 @@ struct BlockArgs {
 __device__ __forceinline__ bool blk_skip(const BlockArgs& A) {
   return (A.stop && *A.stop) || *A.status || (A.capfail && *A.capfail);
 }
-__device__ __forceinline__ int block_col0(const BlockArgs& A) { return A.col0_dev ? (*A.col0_dev) * A.col0_mul : 0; }
+__device__ __forceinline__ unsigned blk_cur(const BlockArgs& A) { return A.cur ? *A.cur : 0u; }
+__device__ __forceinline__ int block_col0(const BlockArgs& A) { return A.col0_dev ? A.col0_dev[blk_cur(A)] * A.col0_mul : 0; }
+__device__ __forceinline__ long long blk_kk(const BlockArgs& A) { return A.kk + (long long)blk_cur(A); }
+__device__ __forceinline__ double* blk_trace(const BlockArgs& A) { return A.trace ? A.trace + 9 * (int64_t)blk_cur(A) : nullptr; }
 __device__ __forceinline__ int gtid() { return blockIdx.x * blockDim.x + threadIdx.x; }
 __device__ __forceinline__ int gstride() { return gridDim.x * blockDim.x; }
 
@@ -393,13 +397,13 @@ __device__ __forceinline__ void dev_gamma(const BlockArgs& A) {
     if (!(num > 0.0) || den == 0.0) gamma = 0.0;
     else { gamma = d_div(num, den); if (gamma > 1.0) gamma = 1.0; }
   } else {
-    gamma = d_div((double)(2LL * A.nprime), (double)(A.kk + 2LL * A.nprime));
+    gamma = d_div((double)(2LL * A.nprime), (double)(blk_kk(A) + 2LL * A.nprime));
   }
   A.scal[2] = gamma;
   A.scal[3] = num;
   if (A.trace) {
-    double* tr = A.trace;
-    tr[0] = (double)A.kk; tr[1] = A.col0_dev ? (*A.col0_dev) * A.trace_col0_mul : 0; tr[2] = A.j[0]; tr[3] = -1;
+    double* tr = blk_trace(A);
+    tr[0] = (double)blk_kk(A); tr[1] = A.col0_dev ? A.col0_dev[blk_cur(A)] * A.trace_col0_mul : 0; tr[2] = A.j[0]; tr[3] = -1;
     tr[4] = 0; tr[5] = gamma; tr[6] = num; tr[7] = den; tr[8] = A.minval[0];
   }
 }
@@ -509,6 +513,20 @@ __global__ void __launch_bounds__(256) k_psum256(const double* __restrict__ x, i
 
 __global__ void k_step_done(BlockArgs A) {
   if (!blk_skip(A) && threadIdx.x == 0) atomicAdd(A.dsteps, 1ULL);
+  if (A.cur && threadIdx.x == 0) *A.cur += 1u;   // the step's last kernel advances the cursor
+}
+
+// Single-CTA kernels: take the cursor's values once, then advance it (every
+// thread has read it before thread 0 writes).
+__device__ __forceinline__ void blk_take_cursor(BlockArgs& A) {
+  if (!A.cur) return;
+  const unsigned c = *A.cur;
+  A.kk += (long long)c;
+  if (A.trace) A.trace += 9 * (int64_t)c;
+  if (A.col0_dev) A.col0_dev += c;
+  __syncthreads();
+  if (threadIdx.x == 0) *A.cur = c + 1u;
+  A.cur = nullptr;
 }
 
 // ... and the whole post-LMO step in one CTA of 1024 threads (small U).
@@ -542,6 +560,7 @@ __device__ __forceinline__ void dev_tail_rest(BlockArgs& A, double* tail_slots) 
 
 __global__ void __launch_bounds__(1024, 1) k_block_tail(BlockArgs A) {
   extern __shared__ double tail_slots[];   // zero outside use
+  blk_take_cursor(A);
   if (*A.status) return;
   dev_psumW(A.g, A.L, 256, A.scal + 0, A.eps, A.stop);        // G_U (FW: stop check)
   if (A.stop && *A.stop) return;

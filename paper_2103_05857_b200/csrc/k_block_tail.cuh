@@ -309,7 +309,7 @@ __device__ __forceinline__ double ts_gamma_value(const BlockArgs& A, double GU, 
     if (!(num > 0.0) || den == 0.0) gamma = 0.0;
     else { gamma = d_div(num, den); if (gamma > 1.0) gamma = 1.0; }
   } else {
-    gamma = d_div((double)(2LL * A.nprime), (double)(A.kk + 2LL * A.nprime));
+    gamma = d_div((double)(2LL * A.nprime), (double)(blk_kk(A) + 2LL * A.nprime));
   }
   return gamma;
 }
@@ -319,8 +319,8 @@ __device__ __forceinline__ void ts_gamma_record(const BlockArgs& A, double GU, d
   A.scal[2] = gamma;
   A.scal[3] = num;
   if (A.trace) {
-    double* tr = A.trace;
-    tr[0] = (double)A.kk; tr[1] = A.col0_dev ? (*A.col0_dev) * A.trace_col0_mul : 0; tr[2] = A.j[0]; tr[3] = -1;
+    double* tr = blk_trace(A);
+    tr[0] = (double)blk_kk(A); tr[1] = A.col0_dev ? A.col0_dev[blk_cur(A)] * A.trace_col0_mul : 0; tr[2] = A.j[0]; tr[3] = -1;
     tr[4] = 0; tr[5] = gamma; tr[6] = num; tr[7] = den; tr[8] = A.minval[0];
   }
 }
@@ -388,6 +388,7 @@ __global__ void __launch_bounds__(1024, 1) k_block_tail_sm(BlockArgs A, TailMerg
     __device__ ~Flush() { if (threadIdx.x == 0 && A.phase) for (int q = 0; q < 16; q++) A.phase[q] += S.tsacc[q]; }
   } ts_flush{A, S};
 #endif
+  blk_take_cursor(A);
   if (*A.status || (A.stop && *A.stop)) return;
   TS_MARK(12);
   const int t = threadIdx.x, L = A.L, cap = A.cap;

@@ -191,10 +191,11 @@ struct SweepOut {
   double* g;       // [L] column gaps (single slab only)
 };
 
-// grid = (gx, nslabs). col0 = col0_dev ? *col0_dev * col0_mul : col0_host.
+// grid = (gx, nslabs). col0 = col0_dev ? col0_dev[cur ? *cur : 0] * col0_mul : col0_host
+// (cur: a device step cursor, so that the launches of consecutive block steps are identical).
 template <class Src, int NCOL = Src::COLS>
 __global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_sweep(Src src, int m, int slab_rows, const double* __restrict__ h,
-                                                             const int* __restrict__ col0_dev, int col0_mul,
+                                                             const int* __restrict__ col0_dev, const unsigned* __restrict__ cur, int col0_mul,
                                                              int col0_host, int L, const int* __restrict__ cnt,
                                                              const int* __restrict__ srow,
                                                              const double* __restrict__ sval, int cap,
@@ -209,7 +210,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_sweep(Src src, int m, int
   char* sm_src = reinterpret_cast<char*>(sm_h + ((rows + 1) & ~1));
   src.stage(row0, rows, sm_src);
   __syncthreads();
-  const int col0 = col0_dev ? (*col0_dev) * col0_mul : col0_host;
+  const int col0 = col0_dev ? col0_dev[cur ? *cur : 0u] * col0_mul : col0_host;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if constexpr (NCOL > 1) {
     constexpr int NC = NCOL;
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_sweep(Src src, int m, int
 // Merge per-slab partials in slab order and apply the gap epilogue. One warp per column.
 template <class Src>
 __global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_merge(Src src, int nslabs, const double* __restrict__ h,
-                                                             const int* __restrict__ col0_dev, int col0_mul,
+                                                             const int* __restrict__ col0_dev, const unsigned* __restrict__ cur, int col0_mul,
                                                              int col0_host, int L, const int* __restrict__ cnt,
                                                              const int* __restrict__ srow,
                                                              const double* __restrict__ sval, int cap,
@@ -270,7 +271,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_merge(Src src, int nslabs
                                                              double* out_min, double* out_g,
                                                              const int* __restrict__ stop, int* status) {
   if (stop && *stop) return;
-  const int col0 = col0_dev ? (*col0_dev) * col0_mul : col0_host;
+  const int col0 = col0_dev ? col0_dev[cur ? *cur : 0u] * col0_mul : col0_host;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int p = blockIdx.x * SWEEP_WARPS + warp; p < L; p += gridDim.x * SWEEP_WARPS) {
     double best = __longlong_as_double(0x7ff0000000000000LL);
@@ -322,7 +323,7 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 template <typename T, int S>
 __global__ void __launch_bounds__(BULK_WARPS * 32, 1)
     k_lmo_sweep_bulk(SrcDense<T> src, int m, int slab_rows, int nslabs, const double* __restrict__ h,
-                     const int* __restrict__ col0_dev, int col0_mul, int col0_host, int L,
+                     const int* __restrict__ col0_dev, const unsigned* __restrict__ cur, int col0_mul, int col0_host, int L,
                      const int* __restrict__ cnt, const int* __restrict__ srow, const double* __restrict__ sval,
                      int cap, const double* __restrict__ b, SweepOut out, const int* __restrict__ stop,
                      int* status) {
@@ -339,7 +340,7 @@ __global__ void __launch_bounds__(BULK_WARPS * 32, 1)
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   uint64_t* wb = bars + warp * S;
   unsigned char* wbuf = bufs + (size_t)warp * S * BULK_CH;
-  const int col0 = col0_dev ? (*col0_dev) * col0_mul : col0_host;
+  const int col0 = col0_dev ? col0_dev[cur ? *cur : 0u] * col0_mul : col0_host;
   const int64_t ntot = (int64_t)nslabs * L;
   const int64_t lo = ntot * blockIdx.x / gridDim.x, hi = ntot * (blockIdx.x + 1) / gridDim.x;
   long long tcons = 0, tiss = 0;   // per-warp stage counters (uniform across the warp)

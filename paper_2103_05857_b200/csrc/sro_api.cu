@@ -119,6 +119,10 @@ struct Solver {
   double* part_min = nullptr;
   int64_t part_cap = 0;
   bool defer_merge = false;   // the next sweep leaves its slab partials to the block tail
+  const unsigned* sweep_cur = nullptr;   // the next sweep's block index is col0_dev[*sweep_cur]
+  unsigned* cur = nullptr;    // device step cursor of the current solve call (block steps enqueued)
+  cudaGraphExec_t gexec = nullptr;       // captured block steps of the current solve call
+  int gexec_steps = 0;
   int last_nslabs = 1;        // slabs of the last sweep
   // block-step workspace
   int64_t blk_L = 0, blk_P = 0;
@@ -563,14 +567,14 @@ sro_status sweep_bulk(Solver* s, Src src, const int* col0_dev, int col0_mul, int
   s->lead->stats.kernel_launches += (nslabs > 1 && !s->defer_merge) ? 2 : 1;
   s->lead->stats.sweep_launches += 1;
   s->lead->stats.sweep_columns += L;
-  kern<<<(int)nb, BULK_WARPS * 32, smem, s->stream>>>(src, s->m, slab, nslabs, s->h, col0_dev, col0_mul, col0_host, L,
+  kern<<<(int)nb, BULK_WARPS * 32, smem, s->stream>>>(src, s->m, slab, nslabs, s->h, col0_dev, s->sweep_cur, col0_mul, col0_host, L,
                                                     s->cnt, s->srow, s->sval, s->cap, s->b, o, stop, s->status);
   CUDA_TRY(s, cudaGetLastError());
   s->last_nslabs = nslabs;
   if (nslabs > 1 && !s->defer_merge) {
     int gm = (L + SWEEP_WARPS - 1) / SWEEP_WARPS;
     if (gm > s->num_sms * 8) gm = s->num_sms * 8;
-    k_lmo_merge<Src><<<gm, SWEEP_THREADS, 0, s->stream>>>(src, nslabs, s->h, col0_dev, col0_mul, col0_host, L, s->cnt,
+    k_lmo_merge<Src><<<gm, SWEEP_THREADS, 0, s->stream>>>(src, nslabs, s->h, col0_dev, s->sweep_cur, col0_mul, col0_host, L, s->cnt,
                                                           s->srow, s->sval, s->cap, s->b, s->part_j, s->part_min,
                                                           out_j, out_min, out_g, stop, s->status);
     CUDA_TRY(s, cudaGetLastError());
@@ -624,7 +628,7 @@ sro_status sweep(Solver* s, const int* col0_dev, int col0_mul, int col0_host, in
     s->lead->stats.kernel_launches += (nslabs > 1 && !s->defer_merge) ? 2 : 1;
     s->lead->stats.sweep_launches += 1;
     s->lead->stats.sweep_columns += L;
-    kern<<<dim3(gx, nslabs), SWEEP_THREADS, smem, s->stream>>>(src, s->m, slab, s->h, col0_dev, col0_mul, col0_host, L,
+    kern<<<dim3(gx, nslabs), SWEEP_THREADS, smem, s->stream>>>(src, s->m, slab, s->h, col0_dev, s->sweep_cur, col0_mul, col0_host, L,
                                                              s->cnt, s->srow, s->sval, s->cap, s->b, o, stop,
                                                              s->status);
     CUDA_TRY(s, cudaGetLastError());
@@ -632,7 +636,7 @@ sro_status sweep(Solver* s, const int* col0_dev, int col0_mul, int col0_host, in
     if (nslabs > 1 && !s->defer_merge) {
       int gm = (L + SWEEP_WARPS - 1) / SWEEP_WARPS;
       if (gm > s->num_sms * 8) gm = s->num_sms * 8;
-      k_lmo_merge<Src><<<gm, SWEEP_THREADS, 0, s->stream>>>(src, nslabs, s->h, col0_dev, col0_mul, col0_host, L,
+      k_lmo_merge<Src><<<gm, SWEEP_THREADS, 0, s->stream>>>(src, nslabs, s->h, col0_dev, s->sweep_cur, col0_mul, col0_host, L,
                                                             s->cnt, s->srow, s->sval, s->cap, s->b, s->part_j,
                                                             s->part_min, out_j, out_min, out_g, stop, s->status);
       CUDA_TRY(s, cudaGetLastError());
@@ -995,7 +999,7 @@ sro_status ensure_block_ws(Solver* s, int64_t L) {
 }
 
 BlockArgs block_args(Solver* s, const int* col0_dev, int col0_mul, int L, int step_rule, long long nprime,
-                     bool stop_check, double* trace_dev) {
+                     bool stop_check, double* trace_dev, unsigned* cur = nullptr, long long kbase = 0) {
   BlockArgs A{};
   A.m = s->m; A.n = s->n; A.cap = s->cap; A.lambda = s->lambda; A.a = s->a; A.b = s->b; A.r = s->r; A.h = s->h;
   A.cnt = s->cnt; A.srow = s->srow; A.sval = s->sval; A.col0_dev = col0_dev; A.col0_mul = col0_mul; A.L = L;
@@ -1006,7 +1010,8 @@ BlockArgs block_args(Solver* s, const int* col0_dev, int col0_mul, int L, int st
   A.tstart = s->tstart; A.tcur = s->tcur; A.runc = s->runc; A.runv = s->runv; A.bigw = s->bigw; A.nbig = s->nbig;
   A.scal = s->scal; A.eps = stop_check ? s->epsd : nullptr; A.stop = stop_check ? s->stop : nullptr;
   A.status = s->status;
-  A.step_rule = step_rule; A.kk = s->lead->k + s->lead->k_pending; A.nprime = nprime; A.trace = trace_dev;
+  A.step_rule = step_rule; A.kk = cur ? kbase : s->lead->k + s->lead->k_pending; A.nprime = nprime; A.trace = trace_dev;
+  A.cur = cur;
   A.trace_col0_mul = col0_mul * s->G;
   A.dsteps = s->dsteps;
   A.G = s->G; A.shard = s->shard; A.slot_len = s->lead->slot_len; A.x1 = s->lead->x1; A.x2 = s->lead->x2;
@@ -1019,18 +1024,23 @@ BlockArgs block_args(Solver* s, const int* col0_dev, int col0_mul, int L, int st
 // checked against epsilon before the update (Alg. A.1 line 4). Small U: the
 // LMO sweep plus one single-CTA launch for the rest of the step; large U: one
 // kernel per phase.
+// Cursor mode (cur != nullptr): col0_dev, trace_dev and kbase are the solve call's bases and the
+// step reads its block index, iteration and trace slot at *cur (advanced by the step's last
+// kernel), so consecutive steps are identical launches (capturable in one CUDA graph).
 sro_status plain_block_step(Solver* s, const int* col0_dev, int col0_mul, int L, int step_rule, long long nprime,
-                            bool stop_check, double* trace_dev) {
+                            bool stop_check, double* trace_dev, unsigned* cur = nullptr, long long kbase = 0) {
   sro_status st = ensure_block_ws(s, L);
   if (st) return st;
   const int trb = timed_begin(s);
   int* stop = stop_check ? s->stop : nullptr;
   const bool smtail = L <= 1024 && !s->no_tail && !s->no_smtail && s->m < (1 << 20) - 1;
   s->defer_merge = smtail;
+  s->sweep_cur = cur;
   st = sweep(s, col0_dev, col0_mul, 0, L, s->sw_j, s->sw_min, s->sw_g, stop);
   s->defer_merge = false;
+  s->sweep_cur = nullptr;
   if (st) return st;
-  BlockArgs A = block_args(s, col0_dev, col0_mul, L, step_rule, nprime, stop_check, trace_dev);
+  BlockArgs A = block_args(s, col0_dev, col0_mul, L, step_rule, nprime, stop_check, trace_dev, cur, kbase);
   if (smtail) {
     // pairs resident in shared memory (k_block_tail.cuh); the sweep's slab merge folded in
     TailMerge M{};
@@ -1228,8 +1238,9 @@ void free_shard(Solver* s) {
                    s->trows, s->ntouch, s->capfail, s->bigw, s->nbig};
   for (void* p : aptrs) sfree(p, s->stream);
   if (s->stream) stream_wait(s);
-  void* ptrs[] = {s->dsteps, s->phase, s->a, s->b, s->b_full, s->r, s->h, s->cnt, s->srow, s->sval, s->G_ga, s->fen,
-                  s->status, s->steps_done, s->stop, s->scal, s->epsd, s->sw_j, s->sw_min, s->sw_g};
+  void* ptrs[] = {s->dsteps, s->cur, s->phase, s->a, s->b, s->b_full, s->r, s->h, s->cnt, s->srow, s->sval, s->G_ga,
+                  s->fen, s->status, s->steps_done, s->stop, s->scal, s->epsd, s->sw_j, s->sw_min, s->sw_g};
+  if (s->gexec) cudaGraphExecDestroy(s->gexec);
   for (void* p : ptrs) if (p) cudaFree(p);
   if (s->owns_cost) { if (s->C) cudaFree(s->C); if (s->x) cudaFree(s->x); if (s->y) cudaFree(s->y); }
   for (auto& p : s->pending) { s->ev_pool.push_back(p.a); s->ev_pool.push_back(p.b); }
@@ -1267,6 +1278,7 @@ sro_status build_shard(Solver* s, const double* a, const double* b_loc, const do
   if (s->G == 1) { ALLOC(s->G_ga, n); ALLOC(s->fen, (size_t)n + 1); }
   ALLOC(s->phase, 32);
   ALLOC(s->dsteps, 1);
+  ALLOC(s->cur, 1);
   ALLOC(s->status, 1); ALLOC(s->steps_done, 1); ALLOC(s->stop, 1); ALLOC(s->scal, 8); ALLOC(s->epsd, 1);
   ALLOC(s->sw_j, n); ALLOC(s->sw_min, (size_t)(m > n ? m : n)); ALLOC(s->sw_g, (size_t)(m > n ? m : n));
 #undef ALLOC
@@ -1488,6 +1500,64 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
     if (s->G == 1) return plain_block_step(s, col0_dev, B, B, o->step, nprime, stop_check, tr);
     return shard_block_step(s, col0_dev, B / s->G, B / s->G, o->step, nprime, stop_check, tr);
   };
+  // Unsharded FW / batched: cursor-mode steps (every step the same launches, reading its block
+  // index, iteration and trace slot at the device cursor = steps enqueued in this call), replayed
+  // from one CUDA graph of GRAPH_STEPS steps captured at the first segment (timing off).
+  const long long kbase = s->k;
+  const bool cursor_mode = s->G == 1 && (variant == SRO_FW || variant == SRO_BATCHED);
+  if (cursor_mode) CUDA_TRY(s, cudaMemsetAsync(s->cur, 0, sizeof(unsigned), s->stream));
+  if (s->gexec) { cudaGraphExecDestroy(s->gexec); s->gexec = nullptr; s->gexec_steps = 0; }
+  const bool use_graph = cursor_mode && !s->timing && !getenv("SRO_NO_GRAPH");
+  sro_stats gdelta{};
+  long long gdelta_k = 0;
+  auto run_steps = [&](int64_t count, int graph_steps, auto&& one) -> sro_status {
+    int64_t q = 0;
+    if (use_graph && count >= graph_steps + 1) {
+      if (!s->gexec) {
+        sro_status st1 = one();   // uncaptured: workspaces reach their size here
+        if (st1) return st1;
+        q++;
+        const sro_stats st0 = s->stats;
+        const long long kp0 = s->k_pending;
+        cudaGraph_t g = nullptr;
+        CUDA_TRY(s, cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
+        sro_status cst = SRO_OK;
+        for (int k = 0; k < graph_steps && cst == SRO_OK; k++) cst = one();
+        const cudaError_t ce = cudaStreamEndCapture(s->stream, &g);
+        gdelta.kernel_launches = s->stats.kernel_launches - st0.kernel_launches;
+        gdelta.sweep_launches = s->stats.sweep_launches - st0.sweep_launches;
+        gdelta.sweep_columns = s->stats.sweep_columns - st0.sweep_columns;
+        gdelta.block_steps = s->stats.block_steps - st0.block_steps;
+        gdelta_k = s->k_pending - kp0;
+        s->stats = st0;
+        s->k_pending = kp0;
+        if (cst != SRO_OK || ce != cudaSuccess) {
+          if (g) cudaGraphDestroy(g);
+          if (cst != SRO_OK) return cst;
+          s->err = cudaGetErrorString(ce);
+          return SRO_ERR_CUDA;
+        }
+        const cudaError_t ie = cudaGraphInstantiate(&s->gexec, g, 0);
+        cudaGraphDestroy(g);
+        if (ie != cudaSuccess) { s->gexec = nullptr; s->err = cudaGetErrorString(ie); return SRO_ERR_CUDA; }
+        s->gexec_steps = graph_steps;
+      }
+      while (count - q >= s->gexec_steps) {
+        CUDA_TRY(s, cudaGraphLaunch(s->gexec, s->stream));
+        s->stats.kernel_launches += gdelta.kernel_launches;
+        s->stats.sweep_launches += gdelta.sweep_launches;
+        s->stats.sweep_columns += gdelta.sweep_columns;
+        s->stats.block_steps += gdelta.block_steps;
+        s->k_pending += gdelta_k;
+        q += s->gexec_steps;
+      }
+    }
+    for (; q < count; q++) {
+      sro_status st1 = one();
+      if (st1) return st1;
+    }
+    return SRO_OK;
+  };
   if (s->configured) {
     if (s->variant != variant || s->seed != seed || !options_equal(s->opt, *o)) { s->err = "solver configured differently; call sro_reset"; return SRO_ERR_STATE; }
   }
@@ -1511,9 +1581,16 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
     for (Solver* t : held(s)) CUDA_TRY(s, cudaMemsetAsync(t->stop, 0, sizeof(int), s->stream));
     while (done < iters) {
       const int64_t chunk = (iters - done) < 8 ? (iters - done) : 8;
-      for (int64_t q = 0; q < chunk; q++) {
-        st = block_step(nullptr, n, true, o->trace ? s->trace + 9 * (done + q) : nullptr);
+      if (cursor_mode) {
+        st = run_steps(chunk, 7, [&]() {
+          return plain_block_step(s, nullptr, n, n, o->step, nprime, true, o->trace ? s->trace : nullptr, s->cur, kbase);
+        });
         if (st) return st;
+      } else {
+        for (int64_t q = 0; q < chunk; q++) {
+          st = block_step(nullptr, n, true, o->trace ? s->trace + 9 * (done + q) : nullptr);
+          if (st) return st;
+        }
       }
       const int64_t before = done;
       double G = 0.0;
@@ -1553,9 +1630,18 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
         const long long to_check = period - s->k % period;
         if (seg > to_check) seg = to_check;
         const int64_t before = done;
-        for (long long q = 0; q < seg; q++) {
-          st = block_step(s->visit + done + q, o->block_size, false, o->trace ? s->trace + 9 * (done + q) : nullptr);
+        if (cursor_mode) {
+          const int gsteps = seg - 1 < 16 ? (int)(seg - 1 > 1 ? seg - 1 : 1) : 16;
+          st = run_steps(seg, gsteps, [&]() {
+            return plain_block_step(s, s->visit, o->block_size, o->block_size, o->step, nprime, false,
+                                    o->trace ? s->trace : nullptr, s->cur, kbase);
+          });
           if (st) return st;
+        } else {
+          for (long long q = 0; q < seg; q++) {
+            st = block_step(s->visit + done + q, o->block_size, false, o->trace ? s->trace + 9 * (done + q) : nullptr);
+            if (st) return st;
+          }
         }
         st = drain_block_steps(s, &done);
         out->entries_scanned += (int64_t)m * (o->block_size / s->G) * (int64_t)held(s).size() * (done - before);
