@@ -104,12 +104,17 @@ struct TreeStack {
   }
 };
 
-// Bitonic sort of Pp = 1024 E keys in buf[0, Pp) (buf holds 2 Pp), thread t
-// owning keys [t E, t E + E): exchanges inside a thread in registers, inside a
-// warp by shuffles, across warps through alternating halves of buf (one
-// barrier per stage). Result back in buf[0, Pp).
+// Ascending bitonic sort of the P keys in buf[0, P) (Pp = 1024 E >= P, buf holds 2 Pp
+// with positions [P, Pp) of both halves set to the maximal key): every merge of
+// block size k starts by comparing u with its mirror u ^ (k - 1), then halves
+// with u ^ jj, always keeping the minimum at the lower index, so the padding
+// stays at positions >= P.
+// Thread t owns keys [t E, t E + E): exchanges inside a thread in registers,
+// inside a warp by shuffles, across warps through alternating halves of buf
+// (one barrier per stage). Result back in buf[0, Pp). (Skipping the compares of
+// warps that hold only padding measured slower on B200: kept uniform.)
 template <int E>
-__device__ __forceinline__ void ts_sort(uint32_t* buf, int Pp) {
+__device__ __forceinline__ void ts_sort(uint32_t* buf, int Pp, int P) {
   const int t = threadIdx.x;
   uint32_t x[E];
 #pragma unroll
@@ -117,36 +122,45 @@ __device__ __forceinline__ void ts_sort(uint32_t* buf, int Pp) {
   int half = 1;
   for (int k = 2; k <= Pp; k <<= 1) {
     for (int jj = k >> 1; jj > 0; jj >>= 1) {
-      if (jj < E) {
+      const bool mirror = jj == (k >> 1);
+      const int pm = mirror ? k - 1 : jj;   // partner of u: u ^ pm
+      if (pm < E) {
 #pragma unroll
-        for (int e = 0; e < E; e++) {
+        for (int c = 1; c < E; c++) {
+          if (c != pm) continue;
 #pragma unroll
-          for (int d = 1; d < E; d <<= 1) {
-            if (d != jj || (e & d)) continue;
-            const bool up = ((t * E + e) & k) == 0;
-            const uint32_t a = x[e], b = x[e | d];
-            if ((a > b) == up) { x[e] = b; x[e | d] = a; }
+          for (int e = 0; e < E; e++) {
+            const int f = e ^ c;
+            if (f <= e) continue;
+            const uint32_t a = x[e], b = x[f];
+            x[e] = min(a, b);
+            x[f] = max(a, b);
           }
         }
-      } else if (jj < 32 * E) {
+      } else if (pm < 32 * E) {
+        const int lx = pm / E;
+        uint32_t y[E];
+#pragma unroll
+        for (int e = 0; e < E; e++) y[e] = __shfl_xor_sync(FULL, mirror ? x[E - 1 - e] : x[e], lx);
 #pragma unroll
         for (int e = 0; e < E; e++) {
-          const uint32_t y = __shfl_xor_sync(FULL, x[e], jj / E);
           const int u = t * E + e;
-          const bool keep_min = ((u & jj) == 0) == ((u & k) == 0);
-          x[e] = keep_min ? min(x[e], y) : max(x[e], y);
+          const bool low = (u & jj) == 0;
+          x[e] = low ? min(x[e], y[e]) : max(x[e], y[e]);
         }
       } else {
         uint32_t* hb = buf + half * Pp;
 #pragma unroll
         for (int e = 0; e < E; e++) hb[t * E + e] = x[e];
         __syncthreads();
+        uint32_t y[E];
+#pragma unroll
+        for (int e = 0; e < E; e++) y[e] = hb[(t * E + e) ^ pm];
 #pragma unroll
         for (int e = 0; e < E; e++) {
           const int u = t * E + e;
-          const uint32_t y = hb[u ^ jj];
-          const bool keep_min = ((u & jj) == 0) == ((u & k) == 0);
-          x[e] = keep_min ? min(x[e], y) : max(x[e], y);
+          const bool low = (u & jj) == 0;
+          x[e] = low ? min(x[e], y[e]) : max(x[e], y[e]);
         }
         half ^= 1;
       }
@@ -515,13 +529,13 @@ __global__ void __launch_bounds__(1024, 1) k_block_tail_sm(BlockArgs A, TailMerg
   }
   int Pp = 1024;
   while (Pp < P) Pp <<= 1;
-  for (int u = P + t; u < Pp; u += 1024) S.key[u] = 0xffffffffu;
+  for (int u = P + t; u < Pp; u += 1024) { S.key[u] = 0xffffffffu; S.key[Pp + u] = 0xffffffffu; }
   __syncthreads();
   TS_MARK(2);
   // sort of the keys (unique: one pair per (row, column))
-  if (Pp == 1024) ts_sort<1>(S.key, Pp);
-  else if (Pp == 2048) ts_sort<2>(S.key, Pp);
-  else ts_sort<4>(S.key, Pp);
+  if (Pp == 1024) ts_sort<1>(S.key, Pp, P);
+  else if (Pp == 2048) ts_sort<2>(S.key, Pp, P);
+  else ts_sort<4>(S.key, Pp, P);
   TS_MARK(3);
   // Delta_k per touched row -> denominator -> gamma
   if (Pp == 1024) ts_structure<1>(S, P);
