@@ -18,6 +18,7 @@ __all__ = [
     "GOLDEN", "splitmix64_mix", "rng_u64", "uniform53", "normals",
     "uniform_colours", "mixture_colours", "density_weights", "uniform_weights",
     "sqeuclid_cost", "hash_uniform_cost", "instance", "CONFIGS",
+    "synthetic_image", "kmeans_init",
 ]
 
 GOLDEN = np.uint64(0x9E3779B97F4A7C15)
@@ -149,4 +150,38 @@ def instance(cfg: int, m: int | None = None, n: int | None = None, seed: int = 0
             out["C64"] = out["C32"].astype(np.float64)
     elif cfg == 3:
         out.update(a=uniform_weights(m), b=uniform_weights(n), hash_seed=0x5EED0003 + seed)
+    return out
+
+
+# --------------------------------------------------------------------------- colour-transfer front end
+def synthetic_image(height: int, width: int, K: int = 8, sigma: float = 0.05, seed: int = 0) -> np.ndarray:
+    """An 8-bit RGB image (height*width x 3, row-major pixels) standing in for the paper's photos
+    (P:422): K smooth regions (nearest of K random seed points), each region's pixels
+    drawn from its own Gaussian colour (mean ~ U[0,1]^3, sd sigma), clipped and rounded to
+    0..255. Exact duplicate pixel colours occur, as in real 8-bit images."""
+    N = height * width
+    pts = uniform53(rng_u64(seed * 104729 + 11, 2 * K)).reshape(K, 2)
+    means = uniform53(rng_u64(seed * 104729 + 12, 3 * K)).reshape(K, 3)
+    yy, xx = np.meshgrid((np.arange(height) + 0.5) / height, (np.arange(width) + 0.5) / width, indexing="ij")
+    d = (yy.reshape(-1, 1) - pts[None, :, 0]) ** 2 + (xx.reshape(-1, 1) - pts[None, :, 1]) ** 2
+    z = np.argmin(d, axis=1)
+    X = means[z] + sigma * normals(seed * 104729 + 13, 3 * N).reshape(N, 3)
+    return np.round(255.0 * np.clip(X, 0.0, 1.0)).astype(np.uint8)
+
+
+def kmeans_init(npix: int, k: int, seed: int) -> np.ndarray:
+    """k distinct pixel indices (the k-means initial centres, drawn by sampling without
+    replacement: a partial Fisher-Yates shuffle on the seed's uniform stream). This is the
+    random draw of the k-means front end, passed as an input to both the oracle and the GPU."""
+    if not 1 <= k <= npix:
+        raise ValueError("need 1 <= k <= number of pixels")
+    u = uniform53(rng_u64(seed * 1000003 + 17, k))
+    perm = {}
+    out = np.empty(k, dtype=np.int32)
+    for t in range(k):
+        r = t + int(u[t] * (npix - t))
+        r = min(r, npix - 1)
+        vt, vr = perm.get(t, t), perm.get(r, r)
+        perm[t], perm[r] = vr, vt
+        out[t] = vr
     return out

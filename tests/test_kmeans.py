@@ -1,0 +1,116 @@
+"""Colour-transfer front end: k-means quantisation.
+
+CPU: the oracle (oracle/kmeans.py) pinned by closed forms (k distinct colours, k = 1), the
+Lloyd fixed-point conditions checked by brute force, and the empty-cluster rule on a worked
+example. GPU: sro_kmeans bit-exact against the oracle (centroids, labels, counts, iterations).
+"""
+from __future__ import annotations
+
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from oracle.kmeans import colour_features, kmeans_quantize, recolour
+from sro_inputs import kmeans_init, synthetic_image
+
+
+def test_k_distinct_colours_are_recovered_exactly():
+    rng = np.random.default_rng(0)
+    k = 7
+    cols = rng.integers(0, 256, size=(k, 3)).astype(np.uint8)
+    mult = rng.integers(1, 20, size=k)
+    pix = np.repeat(cols, mult, axis=0)
+    order = rng.permutation(len(pix))
+    pix = pix[order]
+    first = np.array([int(np.nonzero((pix == c).all(1))[0][0]) for c in cols], dtype=np.int32)
+    cen, lab, cnt, it, conv = kmeans_quantize(pix, k, first, 50)
+    assert conv and it == 2
+    assert np.array_equal(cen, cols.astype(np.float64))
+    assert np.array_equal(cnt, mult)
+    assert np.array_equal(cols[lab], pix)
+
+
+def test_single_class_is_the_exact_mean():
+    pix = synthetic_image(10, 13, seed=3)
+    cen, lab, cnt, it, conv = kmeans_quantize(pix, 1, np.array([5], dtype=np.int32), 10)
+    assert conv and cnt[0] == len(pix) and np.all(lab == 0)
+    for c in range(3):   # the correctly rounded quotient of the exact integer sum
+        assert cen[0, c] == float(int(pix[:, c].astype(np.int64).sum())) / len(pix)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_converged_point_satisfies_lloyd_conditions(seed):
+    """Brute force on a small image: every pixel's class is its nearest centroid (first
+    minimum, exact rational distances) and every centroid is its members' mean."""
+    pix = synthetic_image(12, 15, K=4, seed=seed)
+    k = 6
+    cen, lab, cnt, it, conv = kmeans_quantize(pix, k, kmeans_init(len(pix), k, seed), 200)
+    assert conv
+    P = [[Fraction(int(v)) for v in p] for p in pix]
+    C = [[Fraction(float(v)) for v in c] for c in cen]
+    for q in range(len(pix)):
+        d = [sum((P[q][t] - C[c][t]) ** 2 for t in range(3)) for c in range(k)]
+        best = min(d)
+        # exact-rational nearest; ties / 1-ulp fp64 differences resolved to the lowest index
+        assert d[lab[q]] == best or abs(float(d[lab[q]] - best)) <= 1e-9 * float(best + 1)
+    for c in range(k):
+        mem = pix[lab == c].astype(np.int64)
+        assert len(mem) == cnt[c]
+        if len(mem):
+            for t in range(3):
+                assert cen[c, t] == float(int(mem[:, t].sum())) / len(mem)
+
+
+def test_empty_cluster_takes_the_farthest_pixel():
+    """Worked example: both initial centres black -> the second class is empty after the
+    first assignment; the update puts class 0 at the mean (53, 53, 53) and the repair gives
+    class 1 the farthest pixel (white); the next update moves class 0 to the mean of the rest."""
+    pix = np.array([[0, 0, 0], [0, 0, 0], [0, 0, 0], [255, 255, 255], [10, 10, 10]], dtype=np.uint8)
+    cen, lab, cnt, it, conv = kmeans_quantize(pix, 2, np.array([0, 1], dtype=np.int32), 20)
+    assert conv and it == 3
+    assert np.array_equal(lab, [0, 0, 0, 1, 0])
+    assert np.array_equal(cnt, [4, 1])
+    assert np.array_equal(cen, [[2.5, 2.5, 2.5], [255.0, 255.0, 255.0]])
+
+
+def test_features_and_recolour():
+    cen = np.array([[0.0, 127.5, 255.0], [10.2, 20.7, 30.5]])
+    x, a = colour_features(cen, np.array([3, 1]), 4)
+    assert np.array_equal(a, [0.75, 0.25]) and np.array_equal(x[0], [0.0, 0.5, 1.0])
+    out = recolour(np.array([0, 1, 1]), np.array([[0.5, 1.2, -0.1], [0.002, 0.998, 0.5]]))
+    assert out.tolist() == [[128, 255, 0], [1, 254, 128], [1, 254, 128]]
+
+
+# --------------------------------------------------------------------------- GPU parity
+@pytest.mark.gpu
+@pytest.mark.parametrize("h,w,k,seed", [(16, 16, 5, 0), (64, 48, 32, 1), (128, 128, 256, 2), (97, 101, 300, 3),
+                                          (256, 256, 1024, 4)])
+def test_gpu_kmeans_bitexact(h, w, k, seed):
+    sro = pytest.importorskip("paper_2103_05857_b200")
+    pix = synthetic_image(h, w, seed=seed)
+    init = kmeans_init(len(pix), k, seed + 7)
+    cen, lab, cnt, it, conv = kmeans_quantize(pix, k, init, 60)
+    gc, gl, gn, git, gconv = sro.kmeans_quantize(pix, k, init, 60)
+    assert git == it and gconv == conv
+    assert np.array_equal(gl, lab) and np.array_equal(gn, cnt) and np.array_equal(gc, cen)
+
+
+@pytest.mark.gpu
+def test_gpu_kmeans_empty_cluster_repair_bitexact():
+    sro = pytest.importorskip("paper_2103_05857_b200")
+    pix = synthetic_image(40, 40, K=3, seed=9)
+    # initial centres with repeated colours force empty classes (and repairs) in the first pass
+    _, first, inv = np.unique(pix, axis=0, return_index=True, return_inverse=True)
+    rep = np.nonzero(np.bincount(inv.ravel()) >= 2)[0][:4]
+    pairs = [np.nonzero(inv.ravel() == r)[0][:2] for r in rep]
+    init = np.unique(np.concatenate([np.concatenate(pairs), kmeans_init(len(pix), 12, 3)])).astype(np.int32)
+    k = len(init)
+    cen, lab, cnt, it, conv = kmeans_quantize(pix, k, init, 60)
+    gc, gl, gn, git, gconv = sro.kmeans_quantize(pix, k, init, 60)
+    assert git == it and np.array_equal(gl, lab) and np.array_equal(gn, cnt) and np.array_equal(gc, cen)
+    # the worked example as well
+    pix2 = np.array([[0, 0, 0], [0, 0, 0], [0, 0, 0], [255, 255, 255], [10, 10, 10]], dtype=np.uint8)
+    gc, gl, gn, git, gconv = sro.kmeans_quantize(pix2, 2, np.array([0, 1], dtype=np.int32), 20)
+    assert git == 3 and gl.tolist() == [0, 0, 0, 1, 0] and gn.tolist() == [4, 1]
+    assert gc.tolist() == [[2.5, 2.5, 2.5], [255.0, 255.0, 255.0]]
