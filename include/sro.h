@@ -223,6 +223,34 @@ sro_status sro_held_columns(sro_handle h, int32_t* cols, int32_t* n_held);
  * rank 0 and shared with the other ranks by the caller. Errors: NCCL. */
 sro_status sro_nccl_unique_id(uint8_t* out128);
 
+/* Colour-transfer front end: k-means
+ * quantisation of an 8-bit RGB image. pixels: npix x 3 uint8 (row-major RGB;
+ * host memory copied in, or device memory borrowed when pixels_on_device != 0);
+ * init_idx: host int32[k], k distinct pixel indices (the initial centres, drawn
+ * by the caller); Lloyd iterations with squared-Euclidean fp64 distances and the
+ * lowest class index on ties, centroids = exact integer channel sums / count,
+ * stop when an assignment repeats the previous one and no class was repaired; an
+ * empty class takes the pixel farthest from its own centroid (lowest index on
+ * ties; never emptying another class), empty classes in ascending order
+ * (R28-R30). Outputs (host): centroids fp64 k x 3 in 0..255 units,
+ * labels int32[npix] (or NULL), counts int64[k], *iters (assignment passes run),
+ * *converged. cuda_stream: the stream to run on (NULL: the default stream).
+ * Errors: INVALID_ARG (sizes, k > npix, init indices), DIMENSION (k > 8192),
+ * CUDA; sro_kmeans_error() describes the last failure of this thread. */
+sro_status sro_kmeans(const uint8_t* pixels, int64_t npix, int32_t k, const int32_t* init_idx, int32_t max_iters,
+                      int32_t pixels_on_device, void* cuda_stream, double* centroids, int32_t* labels,
+                      int64_t* counts, int32_t* iters, int32_t* converged);
+
+/* Recolouring: out_pixels[p] = clip(rint(255 * xhat[labels[p]]), 0, 255)
+ * per channel. labels: host int32[npix] in [0, k); xhat: host fp64 k x 3 (e.g.
+ * sro_barycentric's output); out_pixels: host uint8 npix x 3. Errors:
+ * INVALID_ARG, CUDA. */
+sro_status sro_recolour(const int32_t* labels, int64_t npix, const double* xhat, int32_t k, void* cuda_stream,
+                        uint8_t* out_pixels);
+
+/* Text of the last sro_kmeans / sro_recolour failure on this thread ("" if none). */
+const char* sro_kmeans_error(void);
+
 /* Copy the accounting into *out; reset it to zero if reset != 0. */
 sro_status sro_get_stats(sro_handle h, sro_stats* out, int32_t reset);
 

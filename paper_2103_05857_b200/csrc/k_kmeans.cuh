@@ -1,0 +1,149 @@
+// k_kmeans.cuh — the colour-transfer front end: k-means
+// quantisation of an 8-bit RGB image into k colours with their pixel histogram
+// (readings R28-R30 in DESIGN.md).
+//
+// Lloyd iterations, every quantity exact or correctly rounded so the result is
+// bit-identical to the oracle whatever the thread order:
+//   * assignment: ((d0^2 + d1^2) + d2^2) in fp64 against every centroid (staged
+//     in shared memory, broadcast reads), first minimum; four pixels per thread;
+//   * update: integer channel sums and counts (64-bit integer atomics: order-free),
+//     centroid = sum / count (one correctly rounded division);
+//   * empty-cluster repair: the pixel farthest from its own centroid (first
+//     maximum: an atomicMax over the fp64 bit pattern, then an atomicMin over the
+//     indices attaining it), one empty cluster at a time in ascending order.
+#pragma once
+#include "sro_device.cuh"
+
+namespace sro {
+
+constexpr int KM_THREADS = 256;
+constexpr int KM_PIX = 4;          // pixels per thread in the assignment
+constexpr int KM_KMAX = 8192;      // centroids staged in shared memory (3 x 8 B each)
+
+__global__ void k_km_init(const uint8_t* __restrict__ px, const int32_t* __restrict__ init, int k, double* cen) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < k; c += gridDim.x * blockDim.x) {
+    const int64_t p = init[c];
+    cen[c] = (double)px[3 * p];
+    cen[k + c] = (double)px[3 * p + 1];
+    cen[2 * k + c] = (double)px[3 * p + 2];
+  }
+}
+
+// Nearest centroid of every pixel; labels, changed count, integer sums and counts.
+__global__ void __launch_bounds__(KM_THREADS) k_km_assign(const uint8_t* __restrict__ px, int64_t N,
+                                                         const double* __restrict__ cen, int k, int32_t* labels,
+                                                         unsigned long long* sums, unsigned long long* counts,
+                                                         unsigned long long* changed) {
+  extern __shared__ double kc[];   // planar: c0[k], c1[k], c2[k]
+  for (int c = threadIdx.x; c < 3 * k; c += blockDim.x) kc[c] = cen[c];
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * KM_PIX;
+  unsigned long long nchg = 0;
+  for (int64_t p0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * KM_PIX; p0 < N; p0 += stride) {
+    double x0[KM_PIX], x1[KM_PIX], x2[KM_PIX], best[KM_PIX];
+    int bj[KM_PIX];
+#pragma unroll
+    for (int q = 0; q < KM_PIX; q++) {
+      const int64_t p = p0 + q < N ? p0 + q : N - 1;
+      x0[q] = (double)px[3 * p]; x1[q] = (double)px[3 * p + 1]; x2[q] = (double)px[3 * p + 2];
+      best[q] = __longlong_as_double(0x7ff0000000000000LL);
+      bj[q] = 0;
+    }
+    for (int c = 0; c < k; c++) {
+      const double c0 = kc[c], c1 = kc[k + c], c2 = kc[2 * k + c];
+#pragma unroll
+      for (int q = 0; q < KM_PIX; q++) {
+        const double d0 = d_sub(x0[q], c0), d1 = d_sub(x1[q], c1), d2 = d_sub(x2[q], c2);
+        const double d = d_add(d_add(d_mul(d0, d0), d_mul(d1, d1)), d_mul(d2, d2));
+        if (d < best[q]) { best[q] = d; bj[q] = c; }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < KM_PIX; q++) {
+      const int64_t p = p0 + q;
+      if (p >= N) break;
+      const int j = bj[q];
+      nchg += labels[p] != j;
+      labels[p] = j;
+      atomicAdd(&counts[j], 1ULL);
+      atomicAdd(&sums[3 * j], (unsigned long long)px[3 * p]);
+      atomicAdd(&sums[3 * j + 1], (unsigned long long)px[3 * p + 1]);
+      atomicAdd(&sums[3 * j + 2], (unsigned long long)px[3 * p + 2]);
+    }
+  }
+  for (int o = 16; o; o >>= 1) nchg += __shfl_xor_sync(FULL, nchg, o);
+  if ((threadIdx.x & 31) == 0 && nchg) atomicAdd(changed, nchg);
+}
+
+// centroid = sum / count for every non-empty class; empties counted.
+__global__ void k_km_update(const unsigned long long* __restrict__ sums, const unsigned long long* __restrict__ counts,
+                            int k, double* cen, unsigned long long* nempty) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < k; c += gridDim.x * blockDim.x) {
+    const unsigned long long n = counts[c];
+    if (n == 0) { atomicAdd(nempty, 1ULL); continue; }
+    const double dn = (double)n;
+    cen[c] = d_div((double)sums[3 * c], dn);
+    cen[k + c] = d_div((double)sums[3 * c + 1], dn);
+    cen[2 * k + c] = d_div((double)sums[3 * c + 2], dn);
+  }
+}
+
+__device__ __forceinline__ double km_own_dist(const uint8_t* px, const double* cen, int k, int64_t p, int j) {
+  const double d0 = d_sub((double)px[3 * p], cen[j]), d1 = d_sub((double)px[3 * p + 1], cen[k + j]);
+  const double d2 = d_sub((double)px[3 * p + 2], cen[2 * k + j]);
+  return d_add(d_add(d_mul(d0, d0), d_mul(d1, d1)), d_mul(d2, d2));
+}
+// pass 1: the largest distance to the own centroid among pixels whose class keeps a member
+__global__ void k_km_far_max(const uint8_t* __restrict__ px, int64_t N, const double* __restrict__ cen, int k,
+                             const int32_t* __restrict__ labels, const unsigned long long* __restrict__ counts,
+                             unsigned long long* dmax) {
+  unsigned long long best = 0ULL;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (int64_t)gridDim.x * blockDim.x) {
+    const int j = labels[p];
+    if (counts[j] <= 1) continue;
+    // d >= 0: its bit pattern orders as the value; +1 so that 0 means "no candidate"
+    const unsigned long long key = (unsigned long long)__double_as_longlong(km_own_dist(px, cen, k, p, j)) + 1ULL;
+    if (key > best) best = key;
+  }
+  if (best) atomicMax(dmax, best);
+}
+// pass 2: the lowest index attaining it
+__global__ void k_km_far_arg(const uint8_t* __restrict__ px, int64_t N, const double* __restrict__ cen, int k,
+                             const int32_t* __restrict__ labels, const unsigned long long* __restrict__ counts,
+                             const unsigned long long* __restrict__ dmax, unsigned long long* parg) {
+  const unsigned long long want = *dmax;
+  if (want == 0ULL) return;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (int64_t)gridDim.x * blockDim.x) {
+    const int j = labels[p];
+    if (counts[j] <= 1) continue;
+    const unsigned long long key = (unsigned long long)__double_as_longlong(km_own_dist(px, cen, k, p, j)) + 1ULL;
+    if (key == want) { atomicMin(parg, (unsigned long long)p); break; }
+  }
+}
+// class c takes pixel *parg (if any)
+__global__ void k_km_move(const uint8_t* __restrict__ px, int k, int c, const unsigned long long* __restrict__ parg,
+                          double* cen, int32_t* labels, unsigned long long* counts, int* moved) {
+  const unsigned long long p = *parg;
+  if (p == ~0ULL) return;
+  cen[c] = (double)px[3 * p];
+  cen[k + c] = (double)px[3 * p + 1];
+  cen[2 * k + c] = (double)px[3 * p + 2];
+  counts[labels[p]] -= 1ULL;
+  labels[p] = c;
+  counts[c] = 1ULL;
+  *moved = 1;
+}
+
+// every pixel takes its class's projected colour, rint(255 x_hat) clipped to 0..255.
+__global__ void k_km_recolour(const int32_t* __restrict__ labels, int64_t N, const double* __restrict__ xhat,
+                              uint8_t* out) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < 3 * N; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = q / 3;
+    const int t = (int)(q - 3 * p);
+    double v = rint(d_mul(255.0, xhat[3 * (int64_t)labels[p] + t]));
+    v = v < 0.0 ? 0.0 : (v > 255.0 ? 255.0 : v);
+    out[q] = (uint8_t)v;
+  }
+}
+
+}  // namespace sro

@@ -32,6 +32,7 @@
 #include "k_block.cuh"
 #include "k_block_tail.cuh"
 #include "k_plan.cuh"
+#include "k_kmeans.cuh"
 #include "k_sweep.cuh"
 #include "sro_device.cuh"
 
@@ -1913,6 +1914,161 @@ sro_status sro_set_timing(sro_handle h, int32_t on) {
   if (!h) return SRO_ERR_INVALID_ARG;
   static_cast<Solver*>(h)->timing = on != 0;
   return SRO_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// Colour-transfer front end: k-means quantisation and
+// recolouring (k_kmeans.cuh). Handle-free; scratch allocated per call.
+// ---------------------------------------------------------------------------
+static thread_local std::string g_km_err;
+
+const char* sro_kmeans_error(void) { return g_km_err.c_str(); }
+
+#define KM_TRY(call)                                                          \
+  do {                                                                        \
+    cudaError_t e_ = (call);                                                  \
+    if (e_ != cudaSuccess) { g_km_err = cudaGetErrorString(e_); st = SRO_ERR_CUDA; goto done; } \
+  } while (0)
+
+sro_status sro_kmeans(const uint8_t* pixels, int64_t npix, int32_t k, const int32_t* init_idx, int32_t max_iters,
+                      int32_t pixels_on_device, void* cuda_stream, double* centroids, int32_t* labels,
+                      int64_t* counts, int32_t* iters, int32_t* converged) {
+  g_km_err.clear();
+  if (!pixels || !init_idx || !centroids || !counts || !iters || !converged || npix < 1 || k < 1 || k > npix ||
+      max_iters < 1) {
+    g_km_err = "bad argument";
+    return SRO_ERR_INVALID_ARG;
+  }
+  if (k > KM_KMAX) { g_km_err = "k exceeds the shared-memory centroid stage (8192)"; return SRO_ERR_DIMENSION; }
+  {
+    std::vector<int32_t> chk(init_idx, init_idx + k);
+    std::sort(chk.begin(), chk.end());
+    for (int c = 0; c < k; c++)
+      if (chk[c] < 0 || chk[c] >= npix || (c && chk[c] == chk[c - 1])) { g_km_err = "init_idx: k distinct pixel indices"; return SRO_ERR_INVALID_ARG; }
+  }
+  sro_status st = SRO_OK;
+  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  uint8_t* dpx = nullptr;
+  int32_t *dinit = nullptr, *dlab = nullptr;
+  double* dcen = nullptr;
+  unsigned long long *dsums = nullptr, *dcnt = nullptr, *dsc = nullptr;   // dsc: changed, nempty, dmax, parg
+  int* dmoved = nullptr;
+  std::vector<double> hc;
+  std::vector<unsigned long long> hcnt;
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const size_t smem = (size_t)3 * k * sizeof(double);
+  int it = 0;
+  bool conv = false, repaired = false;
+  int gA = 0;
+  if (!pixels_on_device) {
+    KM_TRY(cudaMallocAsync(&dpx, (size_t)3 * npix, stream));
+    KM_TRY(cudaMemcpyAsync(dpx, pixels, (size_t)3 * npix, cudaMemcpyHostToDevice, stream));
+  }
+  KM_TRY(cudaMallocAsync(&dinit, sizeof(int32_t) * k, stream));
+  KM_TRY(cudaMallocAsync(&dlab, sizeof(int32_t) * npix, stream));
+  KM_TRY(cudaMallocAsync(&dcen, sizeof(double) * 3 * k, stream));
+  KM_TRY(cudaMallocAsync(&dsums, sizeof(unsigned long long) * 3 * k, stream));
+  KM_TRY(cudaMallocAsync(&dcnt, sizeof(unsigned long long) * k, stream));
+  KM_TRY(cudaMallocAsync(&dsc, sizeof(unsigned long long) * 4, stream));
+  KM_TRY(cudaMallocAsync(&dmoved, sizeof(int), stream));
+  KM_TRY(cudaMemcpyAsync(dinit, init_idx, sizeof(int32_t) * k, cudaMemcpyHostToDevice, stream));
+  KM_TRY(cudaMemsetAsync(dlab, 0xff, sizeof(int32_t) * npix, stream));   // no class yet
+  {
+    const uint8_t* px = pixels_on_device ? pixels : dpx;
+    k_km_init<<<(k + 255) / 256, 256, 0, stream>>>(px, dinit, k, dcen);
+    KM_TRY(cudaGetLastError());
+    KM_TRY(cudaFuncSetAttribute((const void*)k_km_assign, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_km_assign, KM_THREADS, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t need = (npix + (int64_t)KM_THREADS * KM_PIX - 1) / ((int64_t)KM_THREADS * KM_PIX);
+    gA = (int)std::min<int64_t>(need, (int64_t)nsm * per_sm);
+    const int gP = (int)std::min<int64_t>((npix + 255) / 256, (int64_t)nsm * 8);
+    while (it < max_iters) {
+      it++;
+      KM_TRY(cudaMemsetAsync(dsums, 0, sizeof(unsigned long long) * 3 * k, stream));
+      KM_TRY(cudaMemsetAsync(dcnt, 0, sizeof(unsigned long long) * k, stream));
+      KM_TRY(cudaMemsetAsync(dsc, 0, sizeof(unsigned long long) * 2, stream));
+      k_km_assign<<<gA, KM_THREADS, smem, stream>>>(px, npix, dcen, k, dlab, dsums, dcnt, dsc);
+      KM_TRY(cudaGetLastError());
+      unsigned long long chg = 0;
+      KM_TRY(cudaMemcpyAsync(&chg, dsc, sizeof(chg), cudaMemcpyDeviceToHost, stream));
+      KM_TRY(cudaStreamSynchronize(stream));
+      if (it > 1 && !repaired && chg == 0) { conv = true; break; }
+      repaired = false;
+      k_km_update<<<(k + 255) / 256, 256, 0, stream>>>(dsums, dcnt, k, dcen, dsc + 1);
+      KM_TRY(cudaGetLastError());
+      unsigned long long nempty = 0;
+      KM_TRY(cudaMemcpyAsync(&nempty, dsc + 1, sizeof(nempty), cudaMemcpyDeviceToHost, stream));
+      KM_TRY(cudaStreamSynchronize(stream));
+      if (nempty) {
+        hcnt.resize(k);
+        KM_TRY(cudaMemcpyAsync(hcnt.data(), dcnt, sizeof(unsigned long long) * k, cudaMemcpyDeviceToHost, stream));
+        KM_TRY(cudaStreamSynchronize(stream));
+        for (int c = 0; c < k; c++) {
+          if (hcnt[c]) continue;
+          const unsigned long long none = ~0ULL;
+          KM_TRY(cudaMemsetAsync(dsc + 2, 0, sizeof(unsigned long long), stream));
+          KM_TRY(cudaMemcpyAsync(dsc + 3, &none, sizeof(none), cudaMemcpyHostToDevice, stream));
+          KM_TRY(cudaMemsetAsync(dmoved, 0, sizeof(int), stream));
+          k_km_far_max<<<gP, 256, 0, stream>>>(px, npix, dcen, k, dlab, dcnt, dsc + 2);
+          k_km_far_arg<<<gP, 256, 0, stream>>>(px, npix, dcen, k, dlab, dcnt, dsc + 2, dsc + 3);
+          k_km_move<<<1, 1, 0, stream>>>(px, k, c, dsc + 3, dcen, dlab, dcnt, dmoved);
+          KM_TRY(cudaGetLastError());
+          int moved = 0;
+          KM_TRY(cudaMemcpyAsync(&moved, dmoved, sizeof(int), cudaMemcpyDeviceToHost, stream));
+          KM_TRY(cudaStreamSynchronize(stream));
+          if (moved) repaired = true;
+        }
+      }
+    }
+    hc.resize((size_t)3 * k);
+    hcnt.resize(k);
+    KM_TRY(cudaMemcpyAsync(hc.data(), dcen, sizeof(double) * 3 * k, cudaMemcpyDeviceToHost, stream));
+    KM_TRY(cudaMemcpyAsync(hcnt.data(), dcnt, sizeof(unsigned long long) * k, cudaMemcpyDeviceToHost, stream));
+    if (labels) KM_TRY(cudaMemcpyAsync(labels, dlab, sizeof(int32_t) * npix, cudaMemcpyDeviceToHost, stream));
+    KM_TRY(cudaStreamSynchronize(stream));
+    for (int c = 0; c < k; c++) {
+      centroids[3 * c] = hc[c]; centroids[3 * c + 1] = hc[k + c]; centroids[3 * c + 2] = hc[2 * k + c];
+      counts[c] = (int64_t)hcnt[c];
+    }
+    *iters = it;
+    *converged = conv ? 1 : 0;
+  }
+done:
+  for (void* q : {(void*)dpx, (void*)dinit, (void*)dlab, (void*)dcen, (void*)dsums, (void*)dcnt, (void*)dsc, (void*)dmoved})
+    if (q) cudaFreeAsync(q, stream);
+  cudaStreamSynchronize(stream);
+  return st;
+}
+
+sro_status sro_recolour(const int32_t* labels, int64_t npix, const double* xhat, int32_t k, void* cuda_stream,
+                        uint8_t* out_pixels) {
+  g_km_err.clear();
+  if (!labels || !xhat || !out_pixels || npix < 1 || k < 1) { g_km_err = "bad argument"; return SRO_ERR_INVALID_ARG; }
+  for (int64_t p = 0; p < npix; p++)
+    if (labels[p] < 0 || labels[p] >= k) { g_km_err = "label out of range"; return SRO_ERR_INVALID_ARG; }
+  sro_status st = SRO_OK;
+  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  int32_t* dl = nullptr;
+  double* dx = nullptr;
+  uint8_t* dout = nullptr;
+  KM_TRY(cudaMallocAsync(&dl, sizeof(int32_t) * npix, stream));
+  KM_TRY(cudaMallocAsync(&dx, sizeof(double) * 3 * k, stream));
+  KM_TRY(cudaMallocAsync(&dout, (size_t)3 * npix, stream));
+  KM_TRY(cudaMemcpyAsync(dl, labels, sizeof(int32_t) * npix, cudaMemcpyHostToDevice, stream));
+  KM_TRY(cudaMemcpyAsync(dx, xhat, sizeof(double) * 3 * k, cudaMemcpyHostToDevice, stream));
+  k_km_recolour<<<(int)std::min<int64_t>((3 * npix + 255) / 256, 148 * 16), 256, 0, stream>>>(dl, npix, dx, dout);
+  KM_TRY(cudaGetLastError());
+  KM_TRY(cudaMemcpyAsync(out_pixels, dout, (size_t)3 * npix, cudaMemcpyDeviceToHost, stream));
+  KM_TRY(cudaStreamSynchronize(stream));
+done:
+  for (void* q : {(void*)dl, (void*)dx, (void*)dout}) if (q) cudaFreeAsync(q, stream);
+  cudaStreamSynchronize(stream);
+  return st;
 }
 
 }  // extern "C"

@@ -13,7 +13,7 @@ import numpy as np
 __all__ = [
     "load_library", "Solver", "SroError", "SRO_FW", "SRO_BCFW", "SRO_BCAFW", "SRO_BCPFW", "SRO_BATCHED",
     "STEP_DEC", "STEP_ELS", "SAMPLE_U", "SAMPLE_P", "SAMPLE_GA", "TRACE_DTYPE", "EXPORTED_SYMBOLS",
-    "nccl_unique_id",
+    "nccl_unique_id", "kmeans_quantize", "recolour", "colour_transfer",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -27,7 +27,8 @@ PRECS = {"f64": 0, "f32": 1}
 OK, NOT_CONVERGED = 0, 1
 EXPORTED_SYMBOLS = ("sro_create", "sro_solve", "sro_gap", "sro_objective", "sro_get_plan", "sro_get_rowsums",
                     "sro_reset", "sro_destroy", "sro_last_error", "sro_version", "sro_get_stats", "sro_set_timing",
-                    "sro_held_columns", "sro_nccl_unique_id", "sro_barycentric", "sro_metrics")
+                    "sro_held_columns", "sro_nccl_unique_id", "sro_barycentric", "sro_metrics",
+                    "sro_kmeans", "sro_recolour", "sro_kmeans_error")
 
 _STATUS = {0: "OK", 1: "NOT_CONVERGED", 2: "ERR_INVALID_ARG", 3: "ERR_DIMENSION", 4: "ERR_MARGINALS",
            5: "ERR_NONFINITE", 6: "ERR_CAPACITY", 7: "ERR_CUDA", 8: "ERR_NCCL", 9: "ERR_OOM", 10: "ERR_STATE"}
@@ -122,6 +123,12 @@ def load_library():
         L.sro_barycentric.restype = ct.c_int
         L.sro_metrics.argtypes = [vp, ct.POINTER(d), ct.POINTER(d), ct.POINTER(d)]
         L.sro_metrics.restype = ct.c_int
+        L.sro_kmeans.argtypes = [vp, i64, i32, vp, i32, i32, vp, vp, vp, vp, ct.POINTER(i32), ct.POINTER(i32)]
+        L.sro_kmeans.restype = ct.c_int
+        L.sro_recolour.argtypes = [vp, i64, vp, i32, vp, vp]
+        L.sro_recolour.restype = ct.c_int
+        L.sro_kmeans_error.argtypes = []
+        L.sro_kmeans_error.restype = ct.c_char_p
         _lib = L
     return _lib
 
@@ -301,3 +308,64 @@ def nccl_unique_id() -> bytes:
     if st != OK:
         raise SroError(st, L.sro_last_error(None).decode())
     return buf.raw
+
+
+# --------------------------------------------------------------------------- colour-transfer front end
+def kmeans_quantize(pixels, k: int, init_idx, max_iters: int = 100, stream=None):
+    """sro_kmeans: k-means quantisation of npix x 3 uint8 pixels (numpy, or a CUDA uint8 tensor,
+    borrowed). Returns (centroids fp64 k x 3 in 0..255 units, labels int32, counts int64,
+    iterations, converged)."""
+    L = load_library()
+    on_dev = 1 if _is_cuda(pixels) else 0
+    if not on_dev:
+        pixels = np.ascontiguousarray(pixels, dtype=np.uint8)
+    npix = int(pixels.shape[0])
+    init = np.ascontiguousarray(init_idx, dtype=np.int32)
+    cen = np.empty((k, 3), dtype=np.float64)
+    lab = np.empty(npix, dtype=np.int32)
+    cnt = np.empty(k, dtype=np.int64)
+    it, conv = ct.c_int32(0), ct.c_int32(0)
+    st = L.sro_kmeans(_ptr(pixels), npix, int(k), _ptr(init), int(max_iters), on_dev,
+                      ct.c_void_p(stream) if stream else None, _ptr(cen), _ptr(lab), _ptr(cnt), ct.byref(it),
+                      ct.byref(conv))
+    if st != OK:
+        raise SroError(st, L.sro_kmeans_error().decode())
+    return cen, lab, cnt, int(it.value), bool(conv.value)
+
+
+def recolour(labels, xhat, stream=None):
+    """sro_recolour: npix x 3 uint8 pixels, each its class's colour rint(255 x_hat)."""
+    L = load_library()
+    lab = np.ascontiguousarray(labels, dtype=np.int32)
+    xh = np.ascontiguousarray(xhat, dtype=np.float64)
+    out = np.empty((len(lab), 3), dtype=np.uint8)
+    st = L.sro_recolour(_ptr(lab), len(lab), _ptr(xh), int(xh.shape[0]), ct.c_void_p(stream) if stream else None,
+                        _ptr(out))
+    if st != OK:
+        raise SroError(st, L.sro_kmeans_error().decode())
+    return out
+
+
+def colour_transfer(src_pixels, ref_pixels, m: int, n: int, init_src, init_ref, lam: float = 1.0,
+                    variant: int = SRO_BCFW, iters: int | None = None, epsilon: float = 1e-6, cost: str = "euclid",
+                    prec: str = "f64", kmeans_iters: int = 100, seed: int = 0, **solve_opts):
+    """The paper's colour-transfer pipeline on the GPU: quantise the source into m
+    colours x with histogram a and the reference into n colours y with b (sro_kmeans),
+    solve the semi-relaxed problem with C = ||x_k - y_i||_2 (or its square), project the
+    source colours (Eq. 15, sro_barycentric) and recolour the source pixels (sro_recolour).
+    Returns (recoloured pixels, solve result dict, (x, a, y, b, xhat))."""
+    cx, lx, ax_cnt, _, _ = kmeans_quantize(src_pixels, m, init_src, kmeans_iters)
+    cy, _, by_cnt, _, _ = kmeans_quantize(ref_pixels, n, init_ref, kmeans_iters)
+    x, y = cx / 255.0, cy / 255.0
+    a = ax_cnt.astype(np.float64) / float(len(lx))
+    b = by_cnt.astype(np.float64) / float(by_cnt.sum())
+    keep_a, keep_b = a > 0, b > 0
+    if not keep_a.all() or not keep_b.all():
+        raise SroError(2, "an empty k-means class (k larger than the distinct colours)")
+    s = Solver(a, b, lam, X=x, Y=y, cost=cost, prec=prec)
+    try:
+        res = s.solve(variant, iters if iters is not None else 1000 * n, seed=seed, epsilon=epsilon, **solve_opts)
+        xhat = s.barycentric(x, y)
+    finally:
+        s.close()
+    return recolour(lx, xhat), res, (x, a, y, b, xhat)

@@ -114,3 +114,30 @@ def test_gpu_kmeans_empty_cluster_repair_bitexact():
     gc, gl, gn, git, gconv = sro.kmeans_quantize(pix2, 2, np.array([0, 1], dtype=np.int32), 20)
     assert git == 3 and gl.tolist() == [0, 0, 0, 1, 0] and gn.tolist() == [4, 1]
     assert gc.tolist() == [[2.5, 2.5, 2.5], [255.0, 255.0, 255.0]]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cost", ["euclid", "sqeuclid"])
+def test_gpu_colour_transfer_pipeline_bitexact(cost):
+    """The whole pipeline of P:424-432 on a small image pair: k-means (m, n colours), BCFW-P-ELS
+    to g <= 1e-8, Eq. 15 projection and recolouring; the GPU's recoloured pixels, plan and
+    colours equal the oracle chain's bit for bit."""
+    sro = pytest.importorskip("paper_2103_05857_b200")
+    from oracle import BCFW, ELS, P, Oracle
+    src, ref = synthetic_image(48, 40, seed=21), synthetic_image(40, 56, seed=22)
+    m, n = 24, 20
+    init_s, init_r = kmeans_init(len(src), m, 1), kmeans_init(len(ref), n, 2)
+    out, res, (x, a, y, b, xhat) = sro.colour_transfer(src, ref, m, n, init_s, init_r, lam=1.0, variant=sro.SRO_BCFW,
+                                                       iters=400 * n, epsilon=1e-8, cost=cost, step=sro.STEP_ELS,
+                                                       sampling=sro.SAMPLE_P, seed=3)
+    cx, lx, cnx, _, _ = kmeans_quantize(src, m, init_s, 100)
+    cy, _, cny, _, _ = kmeans_quantize(ref, n, init_r, 100)
+    ox, oa = colour_features(cx, cnx, len(src))
+    oy, ob = colour_features(cy, cny, len(ref))
+    assert np.array_equal(ox, x) and np.array_equal(oa, a) and np.array_equal(oy, y) and np.array_equal(ob, b)
+    o = Oracle(oa, ob, 1.0, X=ox, Y=oy, cost=cost, prec="f64", cap=31)
+    r = o.solve(BCFW, 400 * n, seed=3, step=ELS, sampling=P, epsilon=1e-8)
+    assert r["iters_done"] == res["iters_done"] and r["gap"] == res["gap"]
+    oxh = o.barycentric(ox, oy)
+    assert np.array_equal(oxh, xhat)
+    assert np.array_equal(recolour(lx, oxh), out)
