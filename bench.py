@@ -315,8 +315,9 @@ def roofline_from_stats(stats, peaks):
         # DRAM traffic per launch = algorithmic bytes (profiles/r01_ncu_bcfw_rf.md)
         us = t_ms * 1e3 / stats["bcfw_steps"]
         out["traffic"] = round((68.409856e6 + 1.813504e6) / 4096 * (bytes_ / launches) / (M * 4.0), 1)
-        out["traffic_source"] = ("ncu --set full dram__bytes_read+write of k_bcfw_pipe (68.41+1.81 MB per 4096-step "
-                                 "launch, profiles/r01_ncu_bcfw_pipe.md)")
+        out["traffic_source"] = ("ncu --set full dram__bytes_read+write per 4096-step launch: k_bcfw_ga_pipe "
+                                 "68.44+1.75 MB (profiles/r01_ncu_ga_pipe.md), k_bcfw_pipe 68.41+1.81 MB "
+                                 "(profiles/r01_ncu_bcfw_pipe.md)")
         out["step_latency"] = {"us_per_step": round(us, 4), "cycles_per_step_at_1965MHz": round(us * 1965.0, 1),
                                "single_cta_floor_cycles": 420,
                                "floor_source": "profiles/r01_lmo_microbench.log: register LMO + REDUX argmin + 2 barriers"}
