@@ -1,0 +1,85 @@
+"""Degenerate and ragged inputs through the CUDA path, bit-exact against the oracle
+(DESIGN.md §3 fixes every operation, so the bar is equality): a single row (every LMO returns
+row 0, the plan is feasible and optimal at T^(0)), a single column (BCFW == FW), both, sizes
+that leave ragged 256-chunks and vector tails (fp64 and fp32 costs), rows with a_k = 0, constant costs (every LMO a
+full tie -> lowest row), zero costs, and extreme lambda (h dominated by r - a or vanishing).
+Every BCFW-family variant, FW and batched run a few epochs with per-step traces compared."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import BATCHED, BCAFW, BCFW, BCPFW, ELS, DEC, FW, GA, P, U, Oracle
+from sro_inputs import mixture_colours, sqeuclid_cost
+
+pytestmark = pytest.mark.gpu
+
+sro = pytest.importorskip("paper_2103_05857_b200")
+
+RUNS = [
+    ("bcfw-U-ELS", BCFW, sro.SRO_BCFW, dict(step=ELS, sampling=U)),
+    ("bcfw-P-DEC", BCFW, sro.SRO_BCFW, dict(step=DEC, sampling=P)),
+    ("bcafw-U", BCAFW, sro.SRO_BCAFW, dict(step=ELS, sampling=U)),
+    ("bcpfw-P", BCPFW, sro.SRO_BCPFW, dict(step=ELS, sampling=P)),
+    ("ga-gad", BCFW, sro.SRO_BCFW, dict(step=ELS, sampling=GA, ga_M=1, ga_inner=1, ga_post_update=1)),
+    ("fw-ELS", FW, sro.SRO_FW, dict(step=ELS)),
+    ("fw-DEC", FW, sro.SRO_FW, dict(step=DEC)),
+    ("batched", BATCHED, sro.SRO_BATCHED, dict(step=ELS, sampling=P)),
+]
+
+
+def _inst(kind, m, n, seed=0):
+    X, _, _ = mixture_colours(m, 4, 0.05, 2 * seed + 11)
+    Y, _, _ = mixture_colours(n, 4, 0.05, 2 * seed + 12)
+    rng = np.random.default_rng(seed)
+    a = rng.random(m) + 0.05
+    b = rng.random(n) + 0.05
+    if kind == "zero_rows" and m > 2:
+        a[::3] = 0.0
+    a /= a.sum()
+    b /= b.sum()
+    C = sqeuclid_cost(X, Y)
+    if kind == "const":
+        C = np.full((m, n), 0.37)
+    elif kind == "zero":
+        C = np.zeros((m, n))
+    return a, b, C
+
+
+CASES = [
+    ("one_row", 1, 37, 1.0), ("one_col", 41, 1, 1.0), ("one_by_one", 1, 1, 1.0), ("ragged", 257, 35, 1.0),
+    ("ragged", 5, 3, 1.0), ("ragged", 1031, 13, 1.0), ("zero_rows", 90, 40, 1.0), ("const", 64, 48, 1.0),
+    ("zero", 30, 20, 1.0), ("lam_small", 80, 60, 1e-6), ("lam_large", 80, 60, 1e6),
+]
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("case,m,n,lam", CASES, ids=[f"{c[0]}-{c[1]}x{c[2]}" for c in CASES])
+@pytest.mark.parametrize("name,ov,gv,kw", RUNS, ids=[r[0] for r in RUNS])
+def test_degenerate_inputs_bitexact(case, m, n, lam, name, ov, gv, kw, prec):
+    a, b, C = _inst(case, m, n)
+    if prec == "f32":
+        C = C.astype(np.float32)
+    kw = dict(kw)
+    if ov == BATCHED:
+        B = next(d for d in (16, 8, 5, 4, 3, 2, 1) if n % d == 0)
+        kw["block_size"] = B
+        iters = 3 * (n // B)
+    elif ov == FW:
+        iters = 6
+    else:
+        iters = 3 * n
+    g = sro.Solver(a, b, lam, C=C, prec=prec)
+    o = Oracle(a, b, lam, C=C, prec=prec, cap=31)
+    ro = o.solve(ov, iters, seed=5, trace=True, epsilon=-1.0, **kw)
+    rg = g.solve(gv, iters, seed=5, trace=True, epsilon=-1.0, **kw)
+    assert rg["iters_done"] == ro["iters_done"]
+    for f in ("k", "i", "j", "gamma", "num", "den", "minval"):
+        assert np.array_equal(rg["trace"][f], ro["trace"][f]), f
+    assert np.array_equal(g.plan(), o.plan())
+    assert np.array_equal(g.rowsums(), o.r())
+    tg, gg, jg = g.gap()
+    to, go, jo, _ = o.gap()
+    assert tg == to and np.array_equal(gg, go) and np.array_equal(jg, jo)
+    assert g.objective() == o.objective()
+    g.close()
