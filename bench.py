@@ -71,6 +71,8 @@ class ClockSampler:
         self.proc = None
 
     def start(self):
+        if os.environ.get("SRO_BENCH_NO_CLOCKS"):   # A/B only: the contract needs the samples
+            return
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "200"],
@@ -143,12 +145,19 @@ class StepRunner:
         results = [None] * len(PLAN)
         errors = []
 
+        dbg = os.environ.get("SRO_BENCH_DEBUG")
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in PLAN] if dbg else None
+
         def work(q):
             try:
                 name, variant, opts, cap = PLAN[q]
                 s = self.solvers[q]
+                if dbg:
+                    evs[q][0].record(self.streams[q])
                 s.reset()
                 results[q] = s.solve(variant, cap, seed=11, epsilon=EPS, **opts)
+                if dbg:
+                    evs[q][1].record(self.streams[q])
             except Exception as e:  # noqa: BLE001
                 errors.append(e)
 
@@ -169,6 +178,10 @@ class StepRunner:
             main.wait_event(ev)
         e1.record(main)
         e1.synchronize()
+        if dbg:
+            print(json.dumps({PLAN[q][0]: (round(e0.elapsed_time(evs[q][0]), 2), round(e0.elapsed_time(evs[q][1]), 2),
+                                           round(results[q]["device_ms"], 2)) for q in range(len(PLAN))}),
+                  file=sys.stderr, flush=True)
         for (name, _, _, cap), r in zip(PLAN, results):
             if not r["converged"]:
                 raise RuntimeError(f"{name} did not reach g <= {EPS} within {cap} iterations (gap {r['gap']})")
@@ -215,18 +228,21 @@ def bench_sro(args, rank, world, local_rank):
             import torch.distributed as dist
             dist.barrier()
 
-    # warm-up
-    for _ in range(args.warmup):
+    # warm-up; the clock sampler (an nvidia-smi process whose start-up stalls the GPU's host side
+    # for tens of ms) and the per-kernel event timing start before the last warm-up step, so their
+    # first-use costs stay out of the timed steps; the sampler runs through the timed region
+    clocks = ClockSampler(local_rank)
+    for w in range(args.warmup):
+        if w == args.warmup - 1:
+            clocks.start()
+            runner.set_timing(True)
         runner.run([], {})
     torch.cuda.synchronize()
     runner.stats(reset=True)
-    runner.set_timing(True)
     entries, ttg = [], {}
     step_ms = []
-    clocks = ClockSampler(local_rank)
     barrier()
     torch.cuda.synchronize()
-    clocks.start()
     for _ in range(args.steps):
         flush.fill_(1.0)                      # L2 flushed between timed steps (outside the events)
         step_ms.append(runner.run(entries, ttg))

@@ -17,7 +17,12 @@ d = bench.make_instance(0)
 dev = torch.device("cuda", 0)
 Cd = torch.from_numpy(np.ascontiguousarray(d["C32"].T)).to(dev)
 runner = bench.StepRunner(d, dev, Cd)
+flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev) if os.environ.get("FLUSH") else None
+if os.environ.get("TIMING"):
+    runner.set_timing(True)
 for rep in range(4):
+    if flush is not None:
+        flush.fill_(1.0)
     main = torch.cuda.current_stream()
     e0 = torch.cuda.Event(enable_timing=True)
     e0.record(main)
