@@ -896,8 +896,11 @@ static int32_t draw_unit(or_state* s, int32_t sampling, int64_t nprime) {
     if (e != s->perm_epoch) { or_permutation(s->seed, e, (int32_t)nprime, s->perm); s->perm_epoch = e; }
     return s->perm[s->k % nprime];
   }
-  /* GA */
-  return fen_draw(s, or_uniform53(or_rng_u64(s->seed, 1, (uint64_t)s->k)));
+  /* GA (BCFW family: a column; batched: the block of a column drawn with probability
+     proportional to max(G_i, 0), i.e. a block with probability proportional to its columns'
+     summed stored gaps — SURVEY NEXT-4, R31) */
+  int32_t i = fen_draw(s, or_uniform53(or_rng_u64(s->seed, 1, (uint64_t)s->k)));
+  return nprime == s->n ? i : i / (s->n / (int32_t)nprime);
 }
 
 int or_solve(or_state* s, int32_t variant, const or_options* o, int64_t iters, uint64_t seed,
@@ -907,7 +910,8 @@ int or_solve(or_state* s, int32_t variant, const or_options* o, int64_t iters, u
   if (variant < OR_FW || variant > OR_BATCHED || iters < 0) return OR_ERR_ARG;
   if (o->gap_period < 1) return OR_ERR_ARG;
   if ((variant == OR_BCAFW || variant == OR_BCPFW) && o->step_rule != OR_STEP_ELS) return OR_ERR_ARG;
-  if (o->sampling == OR_SAMPLE_GA && !(variant == OR_BCFW || variant == OR_BCAFW || variant == OR_BCPFW)) return OR_ERR_ARG;
+  if (o->sampling == OR_SAMPLE_GA && variant == OR_FW) return OR_ERR_ARG;
+  if (o->sampling == OR_SAMPLE_GA && variant == OR_BATCHED && o->nranks > 1) return OR_ERR_ARG;
   if (o->sampling == OR_SAMPLE_GA && o->ga_M < 1) return OR_ERR_ARG;
   int32_t G = o->nranks < 1 ? 1 : o->nranks;
   int64_t nprime;
@@ -979,18 +983,21 @@ int or_solve(or_state* s, int32_t variant, const or_options* o, int64_t iters, u
       status = plain_update(s, &po, o->step_rule, nprime, &gamma, &num, &den);
       if (status) break;
       if (tr) { tr->i = U[0]; tr->j = jj[0]; tr->dir = 0; tr->gamma = gamma; tr->num = num; tr->den = den; tr->minval = mv[0]; }
-      if (variant == OR_BCFW && o->sampling == OR_SAMPLE_GA && o->ga_inner) {
-        int32_t i = U[0];
-        double gnew = gg[0];
-        if (o->ga_post_update) {
-          int32_t j2; double m2;
-          status = column_gap(s, i, &j2, &m2, &gnew);
-          if (status) break;
-          res->entries_scanned += m;
+      if ((variant == OR_BCFW || variant == OR_BATCHED) && o->sampling == OR_SAMPLE_GA && o->ga_inner) {
+        /* stored gaps of the visited columns (Alg. A.4 line 6), columns ascending */
+        for (int64_t t = 0; t < L && status == OR_OK; t++) {
+          int32_t i = U[t];
+          double gnew = gg[t];
+          if (o->ga_post_update) {
+            int32_t j2; double m2;
+            status = column_gap(s, i, &j2, &m2, &gnew);
+            res->entries_scanned += m;
+          }
+          double delta = wpos(gnew) - wpos(s->G[i]);
+          s->G[i] = gnew;
+          fen_add(s, i, delta);
         }
-        double delta = wpos(gnew) - wpos(s->G[i]);
-        s->G[i] = gnew;
-        fen_add(s, i, delta);
+        if (status) break;
       }
     } else {
       int32_t i = visit ? visit[done] : draw_unit(s, o->sampling, nprime);
@@ -1015,8 +1022,9 @@ int or_solve(or_state* s, int32_t variant, const or_options* o, int64_t iters, u
     }
     s->k++;
     done++;
-    /* GA global refresh after step k when (k+1) mod (M n) == 0 (R16) */
-    if (o->sampling == OR_SAMPLE_GA && variant != OR_FW && s->k % ((int64_t)o->ga_M * n) == 0) {
+    /* GA global refresh after step k when (k+1) mod (M n') == 0 (R16; n' = n for the
+       BCFW family, n / B block steps for batched, R31) */
+    if (o->sampling == OR_SAMPLE_GA && variant != OR_FW && s->k % ((int64_t)o->ga_M * nprime) == 0) {
       status = ga_global_refresh(s, &res->entries_scanned);
       if (status) break;
     }

@@ -1,0 +1,61 @@
+// k_ga_block.cuh — gap-adaptive sampling for batched BCFW (SURVEY §8(f) NEXT-4,
+// DESIGN.md R31): the block of a column drawn with probability proportional to
+// max(G_i, 0) (so a block with probability proportional to its columns' summed
+// stored gaps) from the same Fenwick tree over the n stored column gaps as the
+// BCFW-family GA (Alg. A.4), and after the block step the stored
+// gaps of its B columns refreshed in ascending column order (Alg. A.4 line 6).
+// Everything runs on the device between the steps, so a GA block step is as
+// launch-invariant as a P / U one (device step cursor, one CUDA graph).
+#pragma once
+#include "k_bcfw.cuh"
+
+namespace sro {
+
+// visit[*cur] = the drawn block (the step's LMO sweep and tail read it there).
+__global__ void k_ga_block_draw(const double* __restrict__ fen, const double* __restrict__ G, int n, int B,
+                                uint64_t seed, long long kbase, const unsigned* __restrict__ cur, int* visit,
+                                const int* __restrict__ status) {
+  if (threadIdx.x != 0 || *status) return;
+  const unsigned c = *cur;
+  const double u53 = uniform53(rng_u64(seed, 1, (uint64_t)(kbase + (long long)c)));
+  visit[c] = ga_draw(fen, G, n, u53) / B;
+}
+
+// After the block step (the cursor already advanced): delta_i = max(g_i, 0) -
+// max(G_i, 0) and G_i = g_i for the block's columns, then every Fenwick node
+// covering some of them receives their deltas one by one in ascending column
+// order — the additions ga_add performs column after column. One CTA.
+__global__ void __launch_bounds__(1024) k_ga_block_refresh(double* G, double* fen, int n, int B,
+                                                           const int* __restrict__ visit,
+                                                           const unsigned* __restrict__ cur,
+                                                           const double* __restrict__ gnew,
+                                                           const int* __restrict__ status) {
+  extern __shared__ double dl[];   // B deltas
+  if (*status) return;
+  const int c0 = visit[*cur - 1u] * B;
+  for (int t = threadIdx.x; t < B; t += blockDim.x) {
+    const double gn = gnew[t];
+    dl[t] = d_sub(wpos(gn), wpos(G[c0 + t]));
+    G[c0 + t] = gn;
+  }
+  __syncthreads();
+  // thread per (leaf t, level l): the node on leaf c0+t's update path that the
+  // leaf is the first covered block column of
+  const int levels = 32 - __clz(n);
+  for (int w = threadIdx.x; w < B * levels; w += blockDim.x) {
+    const int t = w / levels, l = w % levels;
+    unsigned x = (unsigned)(c0 + t);
+    for (int q = 0; q < l && x <= (unsigned)n; q++) x |= x + 1u;
+    const long long p = (long long)x + 1;
+    if (p > n) continue;
+    const long long lo = p - (p & -p);                // covered leaves (0-based): [lo, p - 1]
+    const long long first = lo > c0 ? lo : c0;
+    if (c0 + t != first) continue;
+    const long long last = (p - 1) < (long long)(c0 + B - 1) ? (p - 1) : (long long)(c0 + B - 1);
+    double f = fen[p];
+    for (long long i = first; i <= last; i++) f = d_add(f, dl[i - c0]);
+    fen[p] = f;
+  }
+}
+
+}  // namespace sro

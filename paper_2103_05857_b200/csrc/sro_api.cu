@@ -33,6 +33,7 @@
 #include "k_block_tail.cuh"
 #include "k_plan.cuh"
 #include "k_kmeans.cuh"
+#include "k_ga_block.cuh"
 #include "k_sweep.cuh"
 #include "sro_device.cuh"
 
@@ -1481,7 +1482,8 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
   if (variant < SRO_FW || variant > SRO_BATCHED) { s->err = "bad variant"; return SRO_ERR_INVALID_ARG; }
   if (o->gap_period < 1) { s->err = "gap_period must be >= 1"; return SRO_ERR_INVALID_ARG; }
   if ((variant == SRO_BCAFW || variant == SRO_BCPFW) && o->step != SRO_STEP_ELS) { s->err = "away/pairwise need the line search (Alg. A.2/A.3)"; return SRO_ERR_INVALID_ARG; }
-  if (o->sampling == SRO_SAMPLE_GA && !(variant == SRO_BCFW || variant == SRO_BCAFW || variant == SRO_BCPFW)) { s->err = "GA sampling needs a BCFW-family variant"; return SRO_ERR_INVALID_ARG; }
+  if (o->sampling == SRO_SAMPLE_GA && variant == SRO_FW) { s->err = "GA sampling needs a BCFW-family or batched variant"; return SRO_ERR_INVALID_ARG; }
+  if (o->sampling == SRO_SAMPLE_GA && variant == SRO_BATCHED && s->G > 1) { s->err = "GA block sampling runs unsharded"; return SRO_ERR_INVALID_ARG; }
   if (o->sampling == SRO_SAMPLE_GA && o->ga_M < 1) { s->err = "ga_M must be >= 1"; return SRO_ERR_INVALID_ARG; }
   if (o->sampling < 0 || o->sampling > 2 || o->step < 0 || o->step > 1) { s->err = "bad sampling/step"; return SRO_ERR_INVALID_ARG; }
   const int n = s->n_glob;                                   // all columns
@@ -1613,8 +1615,11 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
       st = ensure_visit(s, iters > 0 ? iters : 1);
       if (st) return st;
       if (iters > 0) CUDA_TRY(s, cudaMemcpyAsync(s->visit, hv.data(), sizeof(int) * iters, cudaMemcpyHostToDevice, s->stream));
+    } else if (variant == SRO_BATCHED) {
+      st = ensure_visit(s, iters > 0 ? iters : 1);   // the device draws write the blocks here
+      if (st) return st;
     }
-    const long long gaMn = ga ? (long long)o->ga_M * n : 0;
+    const long long gaMn = ga ? (long long)o->ga_M * nprime : 0;   // global refresh period (R16, R31)
     for (;;) {
       if (s->k % period == 0) {
         double g = 0.0;
@@ -1630,12 +1635,32 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
         long long seg = iters - done;
         const long long to_check = period - s->k % period;
         if (seg > to_check) seg = to_check;
+        if (ga) { const long long to_ref = gaMn - s->k % gaMn; if (seg > to_ref) seg = to_ref; }
         const int64_t before = done;
         if (cursor_mode) {
           const int gsteps = seg - 1 < 16 ? (int)(seg - 1 > 1 ? seg - 1 : 1) : 16;
-          st = run_steps(seg, gsteps, [&]() {
-            return plain_block_step(s, s->visit, o->block_size, o->block_size, o->step, nprime, false,
-                                    o->trace ? s->trace : nullptr, s->cur, kbase);
+          const int B = o->block_size;
+          st = run_steps(seg, gsteps, [&]() -> sro_status {
+            if (ga) {   // GA block draw into visit[cursor] (k_ga_block.cuh)
+              k_ga_block_draw<<<1, 32, 0, s->stream>>>(s->fen, s->G_ga, n, B, seed, kbase, s->cur, s->visit, s->status);
+              CUDA_TRY(s, cudaGetLastError());
+              s->stats.kernel_launches += 1;
+            }
+            sro_status st1 = plain_block_step(s, s->visit, B, B, o->step, nprime, false,
+                                              o->trace ? s->trace : nullptr, s->cur, kbase);
+            if (st1 || !ga || !o->ga_inner) return st1;
+            if (o->ga_post_update) {   // g_i(T^{k+1}) of the block's columns: a sweep at the new state
+              s->sweep_cur = s->cur;
+              st1 = sweep(s, s->visit - 1, B, 0, B, s->sw_j, s->sw_min, s->sw_g, nullptr);
+              s->sweep_cur = nullptr;
+              if (st1) return st1;
+            }
+            CUDA_TRY(s, set_dyn_smem((const void*)k_ga_block_refresh, s->device, (int)(sizeof(double) * B)));
+            k_ga_block_refresh<<<1, 1024, sizeof(double) * B, s->stream>>>(s->G_ga, s->fen, n, B, s->visit, s->cur,
+                                                                            s->sw_g, s->status);
+            CUDA_TRY(s, cudaGetLastError());
+            s->stats.kernel_launches += 1;
+            return SRO_OK;
           });
           if (st) return st;
         } else {
@@ -1645,8 +1670,14 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
           }
         }
         st = drain_block_steps(s, &done);
-        out->entries_scanned += (int64_t)m * (o->block_size / s->G) * (int64_t)held(s).size() * (done - before);
+        out->entries_scanned += (int64_t)m * (o->block_size / s->G) * (int64_t)held(s).size() * (done - before) *
+                                ((ga && o->ga_inner && o->ga_post_update) ? 2 : 1);
         if (st) break;
+        if (ga && s->k % gaMn == 0) {
+          st = ga_global_refresh(s);
+          if (st) return st;
+          out->entries_scanned += (int64_t)m * n;
+        }
         continue;
       }
       long long seg = iters - done;
