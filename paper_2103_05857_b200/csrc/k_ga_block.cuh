@@ -25,11 +25,14 @@ __global__ void k_ga_block_draw(const double* __restrict__ fen, const double* __
 // max(G_i, 0) and G_i = g_i for the block's columns, then every Fenwick node
 // covering some of them receives their deltas one by one in ascending column
 // order — the additions ga_add performs column after column. One CTA.
-__global__ void __launch_bounds__(1024) k_ga_block_refresh(double* G, double* fen, int n, int B,
-                                                           const int* __restrict__ visit,
+// It then draws the next step's block (thread 0, after a barrier: the updated
+// nodes are visible), saving that step a launch; the first step of a segment
+// (and one after a global refresh) draws with k_ga_block_draw instead.
+__global__ void __launch_bounds__(1024) k_ga_block_refresh(double* G, double* fen, int n, int B, int* visit,
                                                            const unsigned* __restrict__ cur,
                                                            const double* __restrict__ gnew,
-                                                           const int* __restrict__ status) {
+                                                           const int* __restrict__ status, uint64_t seed,
+                                                           long long kbase) {
   extern __shared__ double dl[];   // B deltas
   if (*status) return;
   const int c0 = visit[*cur - 1u] * B;
@@ -55,6 +58,11 @@ __global__ void __launch_bounds__(1024) k_ga_block_refresh(double* G, double* fe
     double f = fen[p];
     for (long long i = first; i <= last; i++) f = d_add(f, dl[i - c0]);
     fen[p] = f;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned c = *cur;
+    visit[c] = ga_draw(fen, G, n, uniform53(rng_u64(seed, 1, (uint64_t)(kbase + (long long)c)))) / B;
   }
 }
 

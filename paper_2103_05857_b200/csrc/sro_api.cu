@@ -1640,12 +1640,17 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
         if (cursor_mode) {
           const int gsteps = seg - 1 < 16 ? (int)(seg - 1 > 1 ? seg - 1 : 1) : 16;
           const int B = o->block_size;
+          // GA: the segment's first block is drawn here, every later one by the previous
+          // step's refresh kernel; without the inner refresh every step draws its own
+          auto ga_draw_step = [&]() -> sro_status {
+            k_ga_block_draw<<<1, 32, 0, s->stream>>>(s->fen, s->G_ga, n, B, seed, kbase, s->cur, s->visit, s->status);
+            CUDA_TRY(s, cudaGetLastError());
+            s->stats.kernel_launches += 1;
+            return SRO_OK;
+          };
+          if (ga && o->ga_inner) { st = ga_draw_step(); if (st) return st; }
           st = run_steps(seg, gsteps, [&]() -> sro_status {
-            if (ga) {   // GA block draw into visit[cursor] (k_ga_block.cuh)
-              k_ga_block_draw<<<1, 32, 0, s->stream>>>(s->fen, s->G_ga, n, B, seed, kbase, s->cur, s->visit, s->status);
-              CUDA_TRY(s, cudaGetLastError());
-              s->stats.kernel_launches += 1;
-            }
+            if (ga && !o->ga_inner) { sro_status sd = ga_draw_step(); if (sd) return sd; }
             sro_status st1 = plain_block_step(s, s->visit, B, B, o->step, nprime, false,
                                               o->trace ? s->trace : nullptr, s->cur, kbase);
             if (st1 || !ga || !o->ga_inner) return st1;
@@ -1657,7 +1662,7 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
             }
             CUDA_TRY(s, set_dyn_smem((const void*)k_ga_block_refresh, s->device, (int)(sizeof(double) * B)));
             k_ga_block_refresh<<<1, 1024, sizeof(double) * B, s->stream>>>(s->G_ga, s->fen, n, B, s->visit, s->cur,
-                                                                            s->sw_g, s->status);
+                                                                            s->sw_g, s->status, seed, kbase);
             CUDA_TRY(s, cudaGetLastError());
             s->stats.kernel_launches += 1;
             return SRO_OK;
