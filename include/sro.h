@@ -117,8 +117,11 @@ typedef struct {
   int32_t sampling;       /* sro_sampling (BCFW family and batched; ignored by FW) */
   double epsilon;         /* stop at the first gap check with g <= epsilon */
   int32_t gap_period;     /* epochs between gap checks (>= 1) */
-  int32_t ga_M;           /* GA: global refresh of all column gaps every M*n steps (>= 1) */
-  int32_t ga_inner;       /* GA: 1 = refresh the visited column's gap each step (GAD), 0 = GAS */
+  int32_t ga_M;           /* GA: global refresh of all column gaps every M*n' steps (>= 1; n' = n,
+                             batched: n / block_size block steps) */
+  int32_t ga_inner;       /* GA: 1 = refresh the visited column's gap each step (GAD), 0 = GAS;
+                             batched GA (unsharded, R31): the block of a drawn column,
+                             all its columns' gaps refreshed after the step */
   int32_t ga_post_update; /* GA: 1 = store g_i(T^{k+1}), 0 = g_i(T^k) */
   int32_t block_size;     /* BATCHED: columns per block B (B divides n) */
   const int32_t* visit;   /* optional host array of explicit visits (columns, or block indices for
