@@ -518,9 +518,11 @@ __device__ __forceinline__ StepOut serial_step(const BcfwArgs& A, long long kk, 
   if (!j_in && lane == ins) { mrow = j; mt = 0.0; }
   const bool mvalid = lane < M;
   SP_MARK(9);
-  // source marginal of the rows this lane may update (loads issued early)
+  // source marginal and row sum of the rows this lane may update (loads issued early)
   const double a_m = a[mvalid ? mrow : 0];
   const double a_s = (VAR == VAR_AWAY && lane < c0) ? a[rw] : 0.0;
+  const double r_m = r[mvalid ? mrow : 0];
+  const double r_s = (VAR != VAR_PLAIN && lane < c0) ? r[rw] : 0.0;
 
   double tnew = mt;
   bool use_merged = true;
@@ -609,7 +611,7 @@ __device__ __forceinline__ StepOut serial_step(const BcfwArgs& A, long long kk, 
   if (!o.abort && !o.noop) {
     if (ev) {
       const double Dp = d_add(0.0, d_sub(tnew, eold));
-      const double rn = d_add(r[erow], Dp);
+      const double rn = d_add(use_merged ? r_m : r_s, Dp);
       const double hn = lam == 1.0 ? d_sub(rn, aval) : d_div(d_sub(rn, aval), lam);   // x / 1 == x exactly
       r[erow] = rn;
       h[erow] = hn;
