@@ -1235,15 +1235,16 @@ sro_status do_reset(Solver* s) {
 void free_shard(Solver* s) {
   if (!s) return;
   // stream-ordered workspaces (salloc) go back to the pool on the stream; the rest with cudaFree
+  // (the handle state too: stream-ordered from the retained pool, so creating and destroying
+  // handles neither maps new memory nor synchronises the device)
   void* aptrs[] = {s->visit, s->trace, s->part_j, s->part_min, s->pcount, s->poff, s->ptotal, s->prow, s->ppos, s->pd,
                    s->ptold, s->pdelta, s->runc, s->runv, s->rowcnt, s->rowidx, s->tstart, s->tcur, s->X,
-                   s->trows, s->ntouch, s->capfail, s->bigw, s->nbig};
-  for (void* p : aptrs) sfree(p, s->stream);
+                   s->trows, s->ntouch, s->capfail, s->bigw, s->nbig,
+                   s->dsteps, s->cur, s->phase, s->a, s->b, s->b_full, s->r, s->h, s->cnt, s->srow, s->sval, s->G_ga,
+                   s->fen, s->status, s->steps_done, s->stop, s->scal, s->epsd, s->sw_j, s->sw_min, s->sw_g};
+  if (s->stream) for (void* p : aptrs) sfree(p, s->stream);
   if (s->stream) stream_wait(s);
-  void* ptrs[] = {s->dsteps, s->cur, s->phase, s->a, s->b, s->b_full, s->r, s->h, s->cnt, s->srow, s->sval, s->G_ga,
-                  s->fen, s->status, s->steps_done, s->stop, s->scal, s->epsd, s->sw_j, s->sw_min, s->sw_g};
   if (s->gexec) cudaGraphExecDestroy(s->gexec);
-  for (void* p : ptrs) if (p) cudaFree(p);
   if (s->owns_cost) { if (s->C) cudaFree(s->C); if (s->x) cudaFree(s->x); if (s->y) cudaFree(s->y); }
   for (auto& p : s->pending) { s->ev_pool.push_back(p.a); s->ev_pool.push_back(p.b); }
   for (auto e : s->ev_pool) cudaEventDestroy(e);
@@ -1274,7 +1275,7 @@ sro_status build_shard(Solver* s, const double* a, const double* b_loc, const do
   const int m = s->m, n = s->n;
   cudaEventCreate(&s->ev0); cudaEventCreate(&s->ev1);
 #define ALLOC(ptr, cnt_)                                                              \
-  if (dalloc(&(ptr), (cnt_)) != cudaSuccess) { s->err = "device allocation failed"; return SRO_ERR_OOM; }
+  if (salloc(&(ptr), (cnt_), s->stream) != cudaSuccess) { s->err = "device allocation failed"; return SRO_ERR_OOM; }
   ALLOC(s->a, m); ALLOC(s->b, n); ALLOC(s->b_full, s->n_glob); ALLOC(s->r, m); ALLOC(s->h, m);
   ALLOC(s->cnt, n); ALLOC(s->srow, (size_t)n * s->cap); ALLOC(s->sval, (size_t)n * s->cap);
   if (s->G == 1) { ALLOC(s->G_ga, n); ALLOC(s->fen, (size_t)n + 1); }
