@@ -473,7 +473,10 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
   if (steps > 0 && warp > 0) {
     // =================== LMO warps ===================
     const int lw = warp - 1;
-    const int lt = lw * 32 + lane;
+    // logical LMO thread index: the first 64 (which get a third vector when m = 4096)
+    // go to warps 4 and 8, so every SM sub-partition scans the same number of vectors
+    const int rank = lw == 3 ? 0 : (lw == 7 ? 1 : (lw < 3 ? lw + 2 : (lw < 7 ? lw + 1 : lw)));
+    const int lt = rank * 32 + lane;
     const int kt = nvec * W + lt;
     PipeCol<T, MAXV, GA_LMO> col;
     col.C = Cg; col.ld = ld; col.m = m; col.nvec = nvec;
@@ -486,6 +489,9 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
       nbar_sync(BAR_MASK, GA_SYNC);                  // its support as a mask
       const unsigned mk = mflag[lt];
       mflag[lt] = 0;
+#ifdef SRO_PHASE_TIMING
+      long long lt0 = clock64() + (long long)(mk & 0u);
+#endif
       // rows outside the support only: smallest (value, row) with its C, and the
       // second smallest value (the support rows are warp 0's: it holds their C)
       // (only warps holding a support row run the variant with the mask tests)
@@ -523,6 +529,9 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
       };
       if (__any_sync(FULL, mk != 0u)) scan(std::true_type{});
       else scan(std::false_type{});
+#ifdef SRO_PHASE_TIMING
+      long long lt1 = clock64() + (long long)(j1 & 0);
+#endif
       unsigned long long k1 = okey(u1);
       int r1 = j1;
       const int w1 = warp_argmin_key(k1, r1);
@@ -535,6 +544,13 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
         pk[48 + lw] = (unsigned long long)__double_as_longlong(cw1);
       }
       nbar_arrive(BAR_PART, GA_SYNC);
+#ifdef SRO_PHASE_TIMING
+      const long long lt2 = clock64();
+      if (lane == 0 && (lw == 0 || lw == GA_LMO_WARPS - 1) && A.phase) {
+        atomicAdd((unsigned long long*)&A.phase[lw == 0 ? 16 : 18], (unsigned long long)(lt1 - lt0));
+        atomicAdd((unsigned long long*)&A.phase[lw == 0 ? 17 : 19], (unsigned long long)(lt2 - lt1));
+      }
+#endif
     }
   } else if (steps > 0 && warp == 0) {
     // =================== serial warp ===================

@@ -21,3 +21,5 @@ ph = np.zeros(32, dtype=np.int64)
 L.sro_debug_phase(s.h, ph.ctypes.data_as(ct.c_void_p))
 steps = 4096 * 4
 print("ga warp0 cycles/step", round(ph[:8].sum() / steps, 1), {n: round(float(v) / steps, 1) for n, v in zip(names, ph[:8])})
+print("LMO warp 1: scan", round(ph[16] / steps, 1), "reduce+arrive", round(ph[17] / steps, 1),
+      "| last LMO warp: scan", round(ph[18] / steps, 1), "reduce+arrive", round(ph[19] / steps, 1))
