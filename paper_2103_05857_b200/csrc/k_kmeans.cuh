@@ -18,7 +18,7 @@ namespace sro {
 
 constexpr int KM_THREADS = 256;
 constexpr int KM_PIX = 4;          // pixels per thread in the assignment
-constexpr int KM_KMAX = 8192;      // centroids staged in shared memory (3 x 8 B each)
+constexpr int KM_KMAX = 8192;      // centroids staged in shared memory (3 x 4 B each)
 
 __global__ void k_km_init(const uint8_t* __restrict__ px, const int32_t* __restrict__ init, int k, double* cen) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < k; c += gridDim.x * blockDim.x) {
@@ -30,33 +30,61 @@ __global__ void k_km_init(const uint8_t* __restrict__ px, const int32_t* __restr
 }
 
 // Nearest centroid of every pixel; labels, changed count, integer sums and counts.
+// An fp32 distance d_f is within M = 0.085 of the binary64 distance d for pixels and
+// centroids in [0, 255] (|fl32(c) - c| <= 2^-24 256, then the subtractions, squares and
+// sums of the fp32 formula), so a centroid can only match or beat the exact minimum
+// if its d_f is at most the running fp32 minimum + 2M: only those (centroids in index
+// order, margin 0.5) are evaluated exactly, with the same first-minimum rule, and the
+// result is the exhaustive binary64 argmin. The fp32 centroid copy is in shared
+// memory, the binary64 one is read (L1) only for candidates.
 __global__ void __launch_bounds__(KM_THREADS) k_km_assign(const uint8_t* __restrict__ px, int64_t N,
                                                          const double* __restrict__ cen, int k, int32_t* labels,
                                                          unsigned long long* sums, unsigned long long* counts,
                                                          unsigned long long* changed) {
-  extern __shared__ double kc[];   // planar: c0[k], c1[k], c2[k]
-  for (int c = threadIdx.x; c < 3 * k; c += blockDim.x) kc[c] = cen[c];
+  extern __shared__ float kcf[];   // planar fp32: c0[k], c1[k], c2[k]
+  for (int c = threadIdx.x; c < 3 * k; c += blockDim.x) kcf[c] = __double2float_rn(cen[c]);
   __syncthreads();
+  constexpr float MARGIN = 0.5f;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x * KM_PIX;
   unsigned long long nchg = 0;
-  for (int64_t p0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * KM_PIX; p0 < N; p0 += stride) {
-    double x0[KM_PIX], x1[KM_PIX], x2[KM_PIX], best[KM_PIX];
+  for (int64_t p0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * KM_PIX; p0 - (int64_t)(threadIdx.x & 31) * KM_PIX < N;
+       p0 += stride) {
+    // (the loop runs while any lane of the warp has pixels: the warp votes below)
+    float f0[KM_PIX], f1[KM_PIX], f2[KM_PIX], bf[KM_PIX];
+    double best[KM_PIX];
     int bj[KM_PIX];
 #pragma unroll
     for (int q = 0; q < KM_PIX; q++) {
       const int64_t p = p0 + q < N ? p0 + q : N - 1;
-      x0[q] = (double)px[3 * p]; x1[q] = (double)px[3 * p + 1]; x2[q] = (double)px[3 * p + 2];
+      f0[q] = (float)px[3 * p]; f1[q] = (float)px[3 * p + 1]; f2[q] = (float)px[3 * p + 2];
+      bf[q] = __int_as_float(0x7f800000);
       best[q] = __longlong_as_double(0x7ff0000000000000LL);
       bj[q] = 0;
     }
     for (int c = 0; c < k; c++) {
-      const double c0 = kc[c], c1 = kc[k + c], c2 = kc[2 * k + c];
+      const float c0 = kcf[c], c1 = kcf[k + c], c2 = kcf[2 * k + c];
+      float df[KM_PIX];
+      bool cand[KM_PIX];
+      bool any = false;
 #pragma unroll
       for (int q = 0; q < KM_PIX; q++) {
-        const double d0 = d_sub(x0[q], c0), d1 = d_sub(x1[q], c1), d2 = d_sub(x2[q], c2);
-        const double d = d_add(d_add(d_mul(d0, d0), d_mul(d1, d1)), d_mul(d2, d2));
-        if (d < best[q]) { best[q] = d; bj[q] = c; }
+        const float e0 = __fsub_rn(f0[q], c0), e1 = __fsub_rn(f1[q], c1), e2 = __fsub_rn(f2[q], c2);
+        df[q] = __fmaf_rn(e2, e2, __fmaf_rn(e1, e1, __fmul_rn(e0, e0)));
+        cand[q] = df[q] <= __fadd_ru(bf[q], MARGIN);
+        any |= cand[q];
       }
+      if (__any_sync(FULL, any)) {
+        const double c0d = cen[c], c1d = cen[k + c], c2d = cen[2 * k + c];
+#pragma unroll
+        for (int q = 0; q < KM_PIX; q++) {
+          if (!cand[q]) continue;
+          const double d0 = d_sub((double)f0[q], c0d), d1 = d_sub((double)f1[q], c1d), d2 = d_sub((double)f2[q], c2d);
+          const double d = d_add(d_add(d_mul(d0, d0), d_mul(d1, d1)), d_mul(d2, d2));
+          if (d < best[q]) { best[q] = d; bj[q] = c; }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < KM_PIX; q++) bf[q] = fminf(bf[q], df[q]);
     }
 #pragma unroll
     for (int q = 0; q < KM_PIX; q++) {

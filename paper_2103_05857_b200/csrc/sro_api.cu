@@ -1996,7 +1996,7 @@ sro_status sro_kmeans(const uint8_t* pixels, int64_t npix, int32_t k, const int3
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const size_t smem = (size_t)3 * k * sizeof(double);
+  const size_t smem = (size_t)3 * k * sizeof(float);
   int it = 0;
   bool conv = false, repaired = false;
   int gA = 0;
