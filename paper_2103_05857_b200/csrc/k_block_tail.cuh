@@ -38,6 +38,12 @@ struct TailMerge {
   int64_t ld;
   const void* x;
   const void* y;
+  // the sweep's staged supports (nslabs > 1; k_sweep.cuh stage_support): size, first SW_KP
+  // entries entry-major, b
+  const int* st_cnt;
+  const int* st_row;
+  const double* st_val;
+  const double* st_b;
 };
 __device__ __forceinline__ double tm_cost(const TailMerge& M, int k, int i) {
   switch (M.kind) {
@@ -419,15 +425,26 @@ __global__ void __launch_bounds__(1024, 1) k_block_tail_sm(BlockArgs A, TailMerg
   double bi = 0.0, gcol = 0.0;
 #pragma unroll
   for (int e = 0; e < KP; e++) { crow[e] = 0; cval[e] = 0.0; }
+  static_assert(KP == SW_KP, "staged support width");
   if (own) {
-    c = A.cnt[i];
-    bi = A.b[i];
-    crow[0] = A.srow[(int64_t)i * cap];   // every support has an entry (b_i > 0)
-    cval[0] = A.sval[(int64_t)i * cap];
-    if (M.nslabs <= 1) { j = A.j[t]; gcol = A.g[t]; }
+    if (M.nslabs > 1 && M.st_cnt) {   // staged by the sweep: coalesced reads
+      c = M.st_cnt[t];
+      bi = M.st_b[t];
+      crow[0] = M.st_row[t];
+      cval[0] = M.st_val[t];
 #pragma unroll
-    for (int e = 1; e < KP; e++)
-      if (e < c) { crow[e] = A.srow[(int64_t)i * cap + e]; cval[e] = A.sval[(int64_t)i * cap + e]; }
+      for (int e = 1; e < KP; e++)
+        if (e < c) { crow[e] = M.st_row[e * L + t]; cval[e] = M.st_val[e * L + t]; }
+    } else {
+      c = A.cnt[i];
+      bi = A.b[i];
+      crow[0] = A.srow[(int64_t)i * cap];   // every support has an entry (b_i > 0)
+      cval[0] = A.sval[(int64_t)i * cap];
+      if (M.nslabs <= 1) { j = A.j[t]; gcol = A.g[t]; }
+#pragma unroll
+      for (int e = 1; e < KP; e++)
+        if (e < c) { crow[e] = A.srow[(int64_t)i * cap + e]; cval[e] = A.sval[(int64_t)i * cap + e]; }
+    }
   }
   if (t == 0) S.misc[3] = 0;
   if (M.nslabs > 1) {

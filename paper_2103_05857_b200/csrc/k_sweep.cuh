@@ -185,11 +185,30 @@ __device__ __forceinline__ double column_gap_epilogue(const Src& src, int i, dou
   return d_sub(dot, d_mul(b[i], minval));
 }
 
+constexpr int SW_KP = 4;   // support entries per column staged for the block tail
 struct SweepOut {
   int* j;          // [L] final rows (single slab) or partial rows [nslabs*L]
   double* minval;  // [L] or partial [nslabs*L]
   double* g;       // [L] column gaps (single slab only)
+  // multi-slab block sweeps (the tail merges): slab 0's warps also stage each column's
+  // support size, first SW_KP entries (entry-major [e * L + p], so the single-CTA tail reads
+  // them coalesced instead of one scattered slab line per column) and b_i; nullptr: off
+  int* st_cnt;
+  int* st_row;
+  double* st_val;
+  double* st_b;
 };
+__device__ __forceinline__ void stage_support(const SweepOut& out, int p, int i, int L, const int* __restrict__ cnt,
+                                              const int* __restrict__ srow, const double* __restrict__ sval, int cap,
+                                              const double* __restrict__ b) {
+  const int lane = threadIdx.x & 31;
+  const int c = cnt[i];
+  if (lane == 0) { out.st_cnt[p] = c; out.st_b[p] = b[i]; }
+  if (lane < SW_KP && lane < c) {
+    out.st_row[lane * L + p] = srow[(int64_t)i * cap + lane];
+    out.st_val[lane * L + p] = sval[(int64_t)i * cap + lane];
+  }
+}
 
 // grid = (gx, nslabs). col0 = col0_dev ? col0_dev[cur ? *cur : 0] * col0_mul : col0_host
 // (cur: a device step cursor, so that the launches of consecutive block steps are identical).
@@ -233,9 +252,12 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_sweep(Src src, int m, int
           if (!(bv < 1.0e308 && bv > -1.0e308)) { if (lane == 0) set_status(status, 5); }
           const double g = column_gap_epilogue(src, i, bv, cnt, srow, sval, cap, b, h);
           if (lane == 0) { out.j[p] = bjc; out.minval[p] = bv; out.g[p] = g; }
-        } else if (lane == 0) {
-          out.j[(int64_t)slab * L + p] = bjc;
-          out.minval[(int64_t)slab * L + p] = bv;
+        } else {
+          if (lane == 0) {
+            out.j[(int64_t)slab * L + p] = bjc;
+            out.minval[(int64_t)slab * L + p] = bv;
+          }
+          if (out.st_cnt && slab == 0) stage_support(out, p, i, L, cnt, srow, sval, cap, b);
         }
       }
     }
@@ -251,9 +273,12 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_sweep(Src src, int m, int
       if (!(best < 1.0e308 && best > -1.0e308)) { if (lane == 0) set_status(status, 5); }
       const double g = column_gap_epilogue(src, i, best, cnt, srow, sval, cap, b, h);
       if (lane == 0) { out.j[p] = bj; out.minval[p] = best; out.g[p] = g; }
-    } else if (lane == 0) {
-      out.j[(int64_t)slab * L + p] = bj;
-      out.minval[(int64_t)slab * L + p] = best;
+    } else {
+      if (lane == 0) {
+        out.j[(int64_t)slab * L + p] = bj;
+        out.minval[(int64_t)slab * L + p] = best;
+      }
+      if (out.st_cnt && slab == 0) stage_support(out, p, i, L, cnt, srow, sval, cap, b);
     }
   }
 }
@@ -403,9 +428,12 @@ __global__ void __launch_bounds__(BULK_WARPS * 32, 1)
         if (!(best < 1.0e308 && best > -1.0e308)) { if (lane == 0) set_status(status, 5); }
         const double g = column_gap_epilogue(src, i, best, cnt, srow, sval, cap, b, h);
         if (lane == 0) { out.j[p] = bj; out.minval[p] = best; out.g[p] = g; }
-      } else if (lane == 0) {
-        out.j[(int64_t)slab * L + p] = bj;
-        out.minval[(int64_t)slab * L + p] = best;
+      } else {
+        if (lane == 0) {
+          out.j[(int64_t)slab * L + p] = bj;
+          out.minval[(int64_t)slab * L + p] = best;
+        }
+        if (out.st_cnt && slab == 0) stage_support(out, p, i, L, cnt, srow, sval, cap, b);
       }
     }
     seg = seg_end;

@@ -121,6 +121,10 @@ struct Solver {
   double* part_min = nullptr;
   int64_t part_cap = 0;
   bool defer_merge = false;   // the next sweep leaves its slab partials to the block tail
+  int* st_cnt = nullptr;      // supports staged by a deferred-merge sweep for the block tail
+  int* st_row = nullptr;
+  double* st_val = nullptr;
+  double* st_b = nullptr;
   const unsigned* sweep_cur = nullptr;   // the next sweep's block index is col0_dev[*sweep_cur]
   unsigned* cur = nullptr;    // device step cursor of the current solve call (block steps enqueued)
   cudaGraphExec_t gexec = nullptr;       // captured block steps of the current solve call
@@ -562,9 +566,10 @@ sro_status sweep_bulk(Solver* s, Src src, const int* col0_dev, int col0_mul, int
   const int64_t need = (ntot + BULK_WARPS - 1) / BULK_WARPS;
   if (nb > need) nb = need;
   if (nb < 1) nb = 1;
-  SweepOut o;
+  SweepOut o{};
   if (nslabs == 1) { o.j = out_j; o.minval = out_min; o.g = out_g; }
   else { o.j = s->part_j; o.minval = s->part_min; o.g = nullptr; }
+  if (nslabs > 1 && s->defer_merge && s->st_cnt) { o.st_cnt = s->st_cnt; o.st_row = s->st_row; o.st_val = s->st_val; o.st_b = s->st_b; }
   const int tr = timed_begin(s);
   s->lead->stats.kernel_launches += (nslabs > 1 && !s->defer_merge) ? 2 : 1;
   s->lead->stats.sweep_launches += 1;
@@ -623,9 +628,10 @@ sro_status sweep(Solver* s, const int* col0_dev, int col0_mul, int col0_host, in
     if (nslabs > 1) gx = (gx + nslabs - 1) / nslabs;
     if (gx > need) gx = need;
     if (gx < 1) gx = 1;
-    SweepOut o;
+    SweepOut o{};
     if (nslabs == 1) { o.j = out_j; o.minval = out_min; o.g = out_g; }
     else { o.j = s->part_j; o.minval = s->part_min; o.g = nullptr; }
+    if (nslabs > 1 && s->defer_merge && s->st_cnt) { o.st_cnt = s->st_cnt; o.st_row = s->st_row; o.st_val = s->st_val; o.st_b = s->st_b; }
     const int tr = timed_begin(s);
     s->lead->stats.kernel_launches += (nslabs > 1 && !s->defer_merge) ? 2 : 1;
     s->lead->stats.sweep_launches += 1;
@@ -1036,6 +1042,12 @@ sro_status plain_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
   const int trb = timed_begin(s);
   int* stop = stop_check ? s->stop : nullptr;
   const bool smtail = L <= 1024 && !s->no_tail && !s->no_smtail && s->m < (1 << 20) - 1;
+  if (smtail && !s->st_cnt) {
+    CUDA_TRY(s, salloc(&s->st_cnt, 1024, s->stream));
+    CUDA_TRY(s, salloc(&s->st_row, 1024 * SW_KP, s->stream));
+    CUDA_TRY(s, salloc(&s->st_val, 1024 * SW_KP, s->stream));
+    CUDA_TRY(s, salloc(&s->st_b, 1024, s->stream));
+  }
   s->defer_merge = smtail;
   s->sweep_cur = cur;
   st = sweep(s, col0_dev, col0_mul, 0, L, s->sw_j, s->sw_min, s->sw_g, stop);
@@ -1047,6 +1059,7 @@ sro_status plain_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
     // pairs resident in shared memory (k_block_tail.cuh); the sweep's slab merge folded in
     TailMerge M{};
     M.nslabs = s->last_nslabs; M.pj = s->part_j; M.pmin = s->part_min;
+    M.st_cnt = s->st_cnt; M.st_row = s->st_row; M.st_val = s->st_val; M.st_b = s->st_b;
     M.j = s->sw_j; M.minval = s->sw_min; M.g = s->sw_g;
     const bool dense = s->kind == SRO_COST_DENSE || s->kind == SRO_COST_HASH_UNIFORM;
     const bool f32 = s->prec == SRO_FP32, eu = s->kind == SRO_COST_EUCLID;
@@ -1239,7 +1252,7 @@ void free_shard(Solver* s) {
   // handles neither maps new memory nor synchronises the device)
   void* aptrs[] = {s->visit, s->trace, s->part_j, s->part_min, s->pcount, s->poff, s->ptotal, s->prow, s->ppos, s->pd,
                    s->ptold, s->pdelta, s->runc, s->runv, s->rowcnt, s->rowidx, s->tstart, s->tcur, s->X,
-                   s->trows, s->ntouch, s->capfail, s->bigw, s->nbig,
+                   s->trows, s->ntouch, s->capfail, s->bigw, s->nbig, s->st_cnt, s->st_row, s->st_val, s->st_b,
                    s->dsteps, s->cur, s->phase, s->a, s->b, s->b_full, s->r, s->h, s->cnt, s->srow, s->sval, s->G_ga,
                    s->fen, s->status, s->steps_done, s->stop, s->scal, s->epsd, s->sw_j, s->sw_min, s->sw_g};
   if (s->stream) for (void* p : aptrs) sfree(p, s->stream);
