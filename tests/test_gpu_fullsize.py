@@ -77,3 +77,26 @@ def test_config3_fullsize_fw_sampled_and_certified():
             k = rows[q]
             dot = dot + vals[q] * (c[k] + h[k])
         assert dot - d["b"][i] * v[j] == gcol[i]
+
+
+def test_bench_step_concurrent_equals_serial():
+    """bench.py's launch configuration: the six solves of a step run concurrently on their own
+    (priority) streams sharing one device copy of C; every solve's plan, row sums, gap and
+    iteration count equal those of the same solves run one after another (each solve is a
+    deterministic function of its inputs; the serial path is the one the parity tests pin)."""
+    import torch
+
+    import bench
+    d = bench.make_instance(0)
+    dev = torch.device("cuda", 0)
+    Cd = torch.from_numpy(np.ascontiguousarray(d["C32"].T)).to(dev)
+    out = {}
+    for conc in (True, False):
+        r = bench.StepRunner(d, dev, Cd, concurrent=conc)
+        ttg = {}
+        r.run([], ttg)
+        out[conc] = [(s.plan_coo(), s.rowsums(), s.gap()[0]) for s in r.solvers]
+        r.close()
+    for (pa, ra, ga), (pb, rb, gb) in zip(out[True], out[False]):
+        assert all(np.array_equal(x, y) for x, y in zip(pa, pb))
+        assert np.array_equal(ra, rb) and ga == gb and ga <= 1e-6
