@@ -120,7 +120,7 @@ typedef struct {
   int32_t ga_M;           /* GA: global refresh of all column gaps every M*n' steps (>= 1; n' = n,
                              batched: n / block_size block steps) */
   int32_t ga_inner;       /* GA: 1 = refresh the visited column's gap each step (GAD), 0 = GAS;
-                             batched GA (unsharded, R31): the block of a drawn column,
+                             batched GA (R31; sharded too): the block of a drawn column,
                              all its columns' gaps refreshed after the step */
   int32_t ga_post_update; /* GA: 1 = store g_i(T^{k+1}), 0 = g_i(T^k) */
   int32_t block_size;     /* BATCHED: columns per block B (B divides n) */

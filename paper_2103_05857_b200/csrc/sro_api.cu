@@ -125,6 +125,8 @@ struct Solver {
   int* st_row = nullptr;
   double* st_val = nullptr;
   double* st_b = nullptr;
+  double* ga_blk = nullptr;   // sharded GA: the visited block's gathered column gaps (lead)
+  int ga_blk_cap = 0;
   const unsigned* sweep_cur = nullptr;   // the next sweep's block index is col0_dev[*sweep_cur]
   unsigned* cur = nullptr;    // device step cursor of the current solve call (block steps enqueued)
   cudaGraphExec_t gexec = nullptr;       // captured block steps of the current solve call
@@ -949,11 +951,12 @@ sro_status ensure_cmax(Solver* s) {
   return SRO_OK;
 }
 
-sro_status fen_build(Solver* s) {
-  const size_t bytes = sizeof(double) * ((size_t)s->n + 1);
+sro_status fen_build(Solver* s, int n_tree = -1) {
+  const int nt = n_tree < 0 ? s->n : n_tree;
+  const size_t bytes = sizeof(double) * ((size_t)nt + 1);
   const int use_smem = bytes <= 200 * 1024;
   if (use_smem) CUDA_TRY(s, set_dyn_smem((const void*)k_fen_build, s->device, (int)bytes));
-  k_fen_build<<<1, 256, use_smem ? bytes : 0, s->stream>>>(s->G_ga, s->fen, s->n, use_smem);
+  k_fen_build<<<1, 256, use_smem ? bytes : 0, s->stream>>>(s->G_ga, s->fen, nt, use_smem);
   s->lead->stats.kernel_launches += 1;
   CUDA_TRY(s, cudaGetLastError());
   return SRO_OK;
@@ -978,6 +981,37 @@ sro_status ga_initialise(Solver* s) {
   s->lead->stats.kernel_launches += 2;
   CUDA_TRY(s, cudaGetLastError());
   return fen_build(s);
+}
+
+// Sharded GA block sampling (R31): the lead keeps the tree over all n_glob columns (every
+// process its own replica when nranks > 1); C_init from the largest cost over all shards.
+sro_status ga_initialise_sharded(Solver* s) {
+  unsigned long long* d_cmax = reinterpret_cast<unsigned long long*>(s->scal + 6);
+  CUDA_TRY(s, cudaMemsetAsync(d_cmax, 0, sizeof(unsigned long long), s->stream));
+  for (Solver* t : held(s)) {
+    sro_status st = with_sweep_src(t, [&](auto src) -> sro_status {
+      k_max_cost<<<s->num_sms * 4, 256, 0, s->stream>>>(src, t->m, t->n, d_cmax);
+      CUDA_TRY(s, cudaGetLastError());
+      return SRO_OK;
+    });
+    if (st) return st;
+  }
+  if (s->nranks > 1) {
+    k_key_to_slot<<<1, 32, 0, s->stream>>>(d_cmax, s->x1 + (size_t)s->shard * s->slot_len);
+    sro_status st = exchange(s, s->x1, s->slot_len);
+    if (st) return st;
+    k_max_slots<<<1, 32, 0, s->stream>>>(s->x1, s->G, s->slot_len, d_cmax);
+  }
+  k_ga_init<<<64, 256, 0, s->stream>>>(s->G_ga, s->fen, s->n_glob, d_cmax, s->lambda);
+  CUDA_TRY(s, cudaGetLastError());
+  return fen_build(s, s->n_glob);
+}
+sro_status ga_global_refresh_sharded(Solver* s, double* gap_out) {
+  sro_status st = gap_sweep(s, gap_out);   // every shard's column gaps, exchanged, in gx
+  if (st) return st;
+  k_ga_gather_global<<<s->num_sms * 4, 256, 0, s->stream>>>(s->gx, s->G_ga, s->n, s->G, s->Bo, s->Bl);
+  CUDA_TRY(s, cudaGetLastError());
+  return fen_build(s, s->n_glob);
 }
 
 // ---------------------------------------------------------------------------
@@ -1253,7 +1287,7 @@ void free_shard(Solver* s) {
   void* aptrs[] = {s->visit, s->trace, s->part_j, s->part_min, s->pcount, s->poff, s->ptotal, s->prow, s->ppos, s->pd,
                    s->ptold, s->pdelta, s->runc, s->runv, s->rowcnt, s->rowidx, s->tstart, s->tcur, s->X,
                    s->trows, s->ntouch, s->capfail, s->bigw, s->nbig, s->st_cnt, s->st_row, s->st_val, s->st_b,
-                   s->dsteps, s->cur, s->phase, s->a, s->b, s->b_full, s->r, s->h, s->cnt, s->srow, s->sval, s->G_ga,
+                   s->ga_blk, s->dsteps, s->cur, s->phase, s->a, s->b, s->b_full, s->r, s->h, s->cnt, s->srow, s->sval, s->G_ga,
                    s->fen, s->status, s->steps_done, s->stop, s->scal, s->epsd, s->sw_j, s->sw_min, s->sw_g};
   if (s->stream) for (void* p : aptrs) sfree(p, s->stream);
   if (s->stream) stream_wait(s);
@@ -1292,6 +1326,7 @@ sro_status build_shard(Solver* s, const double* a, const double* b_loc, const do
   ALLOC(s->a, m); ALLOC(s->b, n); ALLOC(s->b_full, s->n_glob); ALLOC(s->r, m); ALLOC(s->h, m);
   ALLOC(s->cnt, n); ALLOC(s->srow, (size_t)n * s->cap); ALLOC(s->sval, (size_t)n * s->cap);
   if (s->G == 1) { ALLOC(s->G_ga, n); ALLOC(s->fen, (size_t)n + 1); }
+  else if (s->lead == s) { ALLOC(s->G_ga, s->n_glob); ALLOC(s->fen, (size_t)s->n_glob + 1); }   // GA block sampling
   ALLOC(s->phase, 32);
   ALLOC(s->dsteps, 1);
   ALLOC(s->cur, 1);
@@ -1497,7 +1532,6 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
   if (o->gap_period < 1) { s->err = "gap_period must be >= 1"; return SRO_ERR_INVALID_ARG; }
   if ((variant == SRO_BCAFW || variant == SRO_BCPFW) && o->step != SRO_STEP_ELS) { s->err = "away/pairwise need the line search (Alg. A.2/A.3)"; return SRO_ERR_INVALID_ARG; }
   if (o->sampling == SRO_SAMPLE_GA && variant == SRO_FW) { s->err = "GA sampling needs a BCFW-family or batched variant"; return SRO_ERR_INVALID_ARG; }
-  if (o->sampling == SRO_SAMPLE_GA && variant == SRO_BATCHED && s->G > 1) { s->err = "GA block sampling runs unsharded"; return SRO_ERR_INVALID_ARG; }
   if (o->sampling == SRO_SAMPLE_GA && o->ga_M < 1) { s->err = "ga_M must be >= 1"; return SRO_ERR_INVALID_ARG; }
   if (o->sampling < 0 || o->sampling > 2 || o->step < 0 || o->step > 1) { s->err = "bad sampling/step"; return SRO_ERR_INVALID_ARG; }
   const int n = s->n_glob;                                   // all columns
@@ -1584,7 +1618,7 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
   if (!s->configured) {
     s->configured = true; s->variant = variant; s->opt = *o; s->seed = seed;
     s->opt.visit = nullptr; s->opt.trace = nullptr;
-    if (ga) { st = ga_initialise(s); if (st) return st; }
+    if (ga) { st = s->G > 1 ? ga_initialise_sharded(s) : ga_initialise(s); if (st) return st; }
   }
   for (Solver* t : held(s)) CUDA_TRY(s, cudaMemcpyAsync(t->epsd, &o->epsilon, sizeof(double), cudaMemcpyHostToDevice, s->stream));
   const int m = s->m;
@@ -1683,9 +1717,38 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
           });
           if (st) return st;
         } else {
+          const int B = o->block_size, Bs = B / s->G;
+          if (ga && o->ga_inner && s->ga_blk_cap < B) {
+            sfree(s->ga_blk, s->stream);
+            CUDA_TRY(s, salloc(&s->ga_blk, (size_t)B, s->stream));
+            s->ga_blk_cap = B;
+          }
           for (long long q = 0; q < seg; q++) {
-            st = block_step(s->visit + done + q, o->block_size, false, o->trace ? s->trace + 9 * (done + q) : nullptr);
+            int* slot = s->visit + done + q;
+            if (ga) {   // sharded GA block sampling (R31): the lead's tree over all n_glob columns
+              k_ga_block_draw_at<<<1, 32, 0, s->stream>>>(s->fen, s->G_ga, s->n_glob, B, seed, s->k + q, slot,
+                                                          s->status);
+              CUDA_TRY(s, cudaGetLastError());
+            }
+            st = block_step(slot, B, false, o->trace ? s->trace + 9 * (done + q) : nullptr);
             if (st) return st;
+            if (ga && o->ga_inner) {
+              // the block's column gaps, every shard's B/G in its slot (global position order)
+              for (Solver* t : held(s)) {
+                if (o->ga_post_update) {
+                  st = sweep(t, slot, Bs, 0, Bs, t->sw_j, t->sw_min, t->sw_g, nullptr);
+                  if (st) return st;
+                }
+                CUDA_TRY(s, cudaMemcpyAsync(s->ga_blk + (size_t)t->shard * Bs, t->sw_g, sizeof(double) * Bs,
+                                            cudaMemcpyDeviceToDevice, s->stream));
+              }
+              st = exchange(s, s->ga_blk, (size_t)Bs);
+              if (st) return st;
+              CUDA_TRY(s, set_dyn_smem((const void*)k_ga_block_refresh_at, s->device, (int)(sizeof(double) * B)));
+              k_ga_block_refresh_at<<<1, 1024, sizeof(double) * B, s->stream>>>(s->G_ga, s->fen, s->n_glob, B, slot,
+                                                                                s->ga_blk, s->status);
+              CUDA_TRY(s, cudaGetLastError());
+            }
           }
         }
         st = drain_block_steps(s, &done);
@@ -1693,7 +1756,8 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
                                 ((ga && o->ga_inner && o->ga_post_update) ? 2 : 1);
         if (st) break;
         if (ga && s->k % gaMn == 0) {
-          st = ga_global_refresh(s);
+          double gdummy = 0.0;
+          st = s->G > 1 ? ga_global_refresh_sharded(s, &gdummy) : ga_global_refresh(s);
           if (st) return st;
           out->entries_scanned += (int64_t)m * n;
         }

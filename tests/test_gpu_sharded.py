@@ -10,7 +10,7 @@ from __future__ import annotations
 import numpy as np
 import pytest
 
-from oracle import BATCHED, DEC, ELS, FW, P, U, Oracle
+from oracle import BATCHED, DEC, ELS, FW, GA, P, U, Oracle
 from sro_inputs import instance
 
 pytestmark = pytest.mark.gpu
@@ -163,3 +163,20 @@ def test_sharded_nccl_single_rank_path():
     d = _dense(32, 64, seed=25)
     with pytest.raises(sro.SroError):
         sro.Solver(d["a"], d["b"], 1.0, C=d["C32"], prec="f32", shards=2, nranks=2, rank=5, nccl_id=uid)
+
+
+@pytest.mark.parametrize("G,B,post", [(2, 64, 1), (4, 64, 0), (8, 32, 1)])
+def test_sharded_batched_ga_bitexact(G, B, post):
+    """GA block sampling (R31) over G column shards: the lead's tree over all n columns, the
+    block's gaps gathered from the shards in global position order, the global refresh from
+    the exchanged gap sweep == the unsharded oracle step for step (G-invariance)."""
+    d = _dense(257, 512, seed=23)
+    g, o = _pair(d, G, shard_block=B)
+    iters = 5 * (512 // B) + 3
+    kw = dict(step=ELS, sampling=GA, ga_M=1, ga_inner=1, ga_post_update=post, block_size=B)
+    ro = o.solve(BATCHED, iters, seed=9, trace=True, epsilon=-1.0, **kw)
+    rg = g.solve(sro.SRO_BATCHED, iters, seed=9, trace=True, epsilon=-1.0, **kw)
+    _same_trace(rg["trace"], ro["trace"])
+    assert rg["gap"] == ro["gap"]
+    assert rg["entries_scanned"] == ro["entries_scanned"]
+    _same_state(g, o)
