@@ -30,6 +30,7 @@
 // code runs either as one kernel per phase (large U, many CTAs) or inside a
 // single CTA (small U: one launch for the whole post-LMO step).
 #pragma once
+#include <cooperative_groups.h>
 #include "sro_device.cuh"
 
 namespace sro {
@@ -565,6 +566,61 @@ __global__ void __launch_bounds__(1024, 1) k_block_tail(BlockArgs A) {
   dev_psumW(A.g, A.L, 256, A.scal + 0, A.eps, A.stop);        // G_U (FW: stop check)
   if (A.stop && *A.stop) return;
   dev_tail_rest(A, tail_slots);
+}
+
+// ... and for larger U the same phases in ONE cooperative launch (every CTA resident,
+// grid-wide barriers between the phases instead of 14 dependent launches): the
+// single-CTA phases (step begin, the scans, the denominator, gamma) run on CTA 0.
+// 1024 threads per CTA; dynamic shared memory: 32 warps x 256 chunk slots. Opt-in
+// (SRO_COOP=1): ten grid barriers cost more than the per-phase kernels' gaps inside
+// a CUDA graph (FW at config [1]: 40 vs 34 ms).
+__global__ void __launch_bounds__(1024) k_block_coop(BlockArgs A) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double wsl[];   // zero outside use
+  const bool lead_cta = blockIdx.x == 0;
+  if ((A.stop && *A.stop) || *A.status) {   // uniform: nothing changes during this check
+    grid.sync();
+    if (lead_cta && threadIdx.x == 0 && A.cur) *A.cur += 1u;
+    return;
+  }
+  for (int q = threadIdx.x; q < 32 * 256; q += blockDim.x) wsl[q] = 0.0;
+  if (lead_cta) {
+    if (threadIdx.x == 0) { *A.ntouch = 0; A.nbig[0] = 0; A.nbig[1] = 0; }
+    dev_psumW(A.g, A.L, 256, A.scal + 0, A.eps, A.stop);   // G_U (FW: stop check)
+  }
+  dev_pairs_count(A);
+  grid.sync();
+  const bool stopped = A.stop && *A.stop;
+  if (!stopped) {
+    if (lead_cta) dev_scan_excl(A.pcount, A.L, A.poff, A.ptotal);
+    grid.sync();
+    dev_pairs_gen(A);
+    grid.sync();
+    if (lead_cta) dev_touched_scan(A);
+    grid.sync();
+    dev_runs(A, A.pd);
+    grid.sync();
+    dev_row_tree_big<0>(A, nullptr, false, 0, wsl, true);
+    grid.sync();
+    if (lead_cta) {
+      dev_psumW(A.X, A.m, 256, A.scal + 1, nullptr, nullptr);
+      dev_gamma(A);
+    }
+    grid.sync();
+    dev_cap_check(A);
+    grid.sync();
+    if (!*A.status) {
+      dev_update_cols(A);
+      grid.sync();
+      dev_runs(A, A.pdelta);
+      grid.sync();
+      dev_row_tree_big<1>(A, nullptr, true, 1, wsl, true);
+      if (lead_cta && threadIdx.x == 0) atomicAdd(A.dsteps, 1ULL);
+    }
+  }
+  grid.sync();   // every read of the cursor done
+  if (lead_cta && threadIdx.x == 0 && A.cur) *A.cur += 1u;
 }
 
 // ---------------------------------------------------------------------------

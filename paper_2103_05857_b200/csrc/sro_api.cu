@@ -157,6 +157,9 @@ struct Solver {
   bool no_rf = getenv("SRO_NO_RF") != nullptr;      // debug: force the shared-memory kernel
   bool no_tail = getenv("SRO_NO_TAIL") != nullptr;  // debug: force the multi-kernel block step
   bool no_smtail = getenv("SRO_NO_SMTAIL") != nullptr;  // debug: force the global-memory single-CTA tail
+  // k_block_coop (one cooperative launch, grid barriers) measured slower than the per-phase
+  // kernels replayed from a CUDA graph (FW config [1]: 40 vs 34 ms): opt-in only
+  bool no_coop = getenv("SRO_COOP") == nullptr;
   // debug: no pipelined BCFW kernel (k_bcfw_pipe.cuh) -> register-file kernel k_bcfw_rf
   bool no_pipe = getenv("SRO_NO_PIPE") != nullptr || getenv("SRO_NO_RF") != nullptr;
   sro_stats stats{};
@@ -1107,6 +1110,17 @@ sro_status plain_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
     CUDA_TRY(s, set_dyn_smem((const void*)k_block_tail, s->device, TAIL_SMEM));
     k_block_tail<<<1, 1024, TAIL_SMEM, s->stream>>>(A);
     CUDA_TRY(s, cudaGetLastError());
+    s->lead->stats.kernel_launches += 1;
+  } else if (!s->no_coop) {
+    // all phases in one cooperative launch (k_block_coop): every CTA resident, grid barriers
+    const size_t cs = (size_t)32 * 256 * sizeof(double);
+    CUDA_TRY(s, set_dyn_smem((const void*)k_block_coop, s->device, (int)cs));
+    int per_sm = 0;
+    CUDA_TRY(s, occupancy((const void*)k_block_coop, s->device, 1024, cs, &per_sm));
+    if (per_sm < 1) per_sm = 1;
+    void* args[] = {(void*)&A};
+    CUDA_TRY(s, cudaLaunchCooperativeKernel((const void*)k_block_coop, dim3(s->num_sms * per_sm), dim3(1024), args, cs,
+                                            s->stream));
     s->lead->stats.kernel_launches += 1;
   } else {
     const int tpb = 256;

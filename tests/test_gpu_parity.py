@@ -276,11 +276,14 @@ def test_config0_shared_memory_kernel_bitexact(name, ov, gv, kw, monkeypatch):
     assert_same_state(g, o)
 
 
+@pytest.mark.parametrize("coop", [True, False], ids=["cooperative", "per-phase"])
 @pytest.mark.parametrize("variant,B", [(BATCHED, 16), (FW, 0)])
-def test_block_step_multikernel_path_bitexact(variant, B, monkeypatch):
-    """The multi-kernel block step (used for large U) forced on small instances: same
-    bit-exact trajectory as the single-CTA tail path and the oracle."""
+def test_block_step_multikernel_path_bitexact(variant, B, coop, monkeypatch):
+    """The large-U block step (one cooperative launch, or the per-phase kernels) forced on
+    small instances: same bit-exact trajectory as the single-CTA tail path and the oracle."""
     monkeypatch.setenv("SRO_NO_TAIL", "1")
+    if coop:
+        monkeypatch.setenv("SRO_COOP", "1")
     d = instance(1, m=300, n=256, seed=8)
     g, o = pair(d, prec="f32")
     kw = dict(block_size=B, sampling=P) if B else {}
