@@ -141,3 +141,20 @@ def test_gpu_colour_transfer_pipeline_bitexact(cost):
     oxh = o.barycentric(ox, oy)
     assert np.array_equal(oxh, xhat)
     assert np.array_equal(recolour(lx, oxh), out)
+
+
+@pytest.mark.gpu
+def test_gpu_kmeans_errors_and_k_equals_npix():
+    sro = pytest.importorskip("paper_2103_05857_b200")
+    pix = synthetic_image(6, 5, seed=4)
+    with pytest.raises(sro.SroError):
+        sro.kmeans_quantize(pix, 3, np.array([1, 1, 2], dtype=np.int32), 10)     # repeated initial centre
+    with pytest.raises(sro.SroError):
+        sro.kmeans_quantize(pix, 31, np.arange(31, dtype=np.int32), 10)          # k > number of pixels
+    with pytest.raises(sro.SroError):
+        sro.kmeans_quantize(pix, 2, np.array([0, 30], dtype=np.int32), 10)       # index out of range
+    # k = npix: every pixel its own class unless colours repeat (repairs keep classes non-empty)
+    init = np.arange(len(pix), dtype=np.int32)
+    cen, lab, cnt, it, conv = kmeans_quantize(pix, len(pix), init, 20)
+    gc, gl, gn, git, gconv = sro.kmeans_quantize(pix, len(pix), init, 20)
+    assert git == it and np.array_equal(gc, cen) and np.array_equal(gl, lab) and np.array_equal(gn, cnt)
