@@ -1212,13 +1212,18 @@ __global__ void k_fen_build(const double* __restrict__ G, double* fen, int n, in
   double* f = use_smem ? fs : fen;
   for (int i = threadIdx.x; i <= n; i += blockDim.x) f[i] = i == 0 ? 0.0 : wpos(G[i - 1]);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int i = 1; i <= n; i++) {
-      const int p = i + (i & -i);
-      if (p <= n) f[p] = d_add(f[p], f[i]);
+  // The build `for i = 1..n: fen[i + lowbit(i)] += fen[i]` adds into node p its children
+  // i = p - 2^(k-1), ..., p - 2, p - 1 (lowbit(p) = 2^k) in that (increasing) order, each
+  // already complete: done level by level (nodes of one lowbit in parallel), the same sums.
+  for (int k = 1; (1 << k) <= n; k++) {
+    const int step = 1 << (k + 1), first = 1 << k;
+    for (int p = first + threadIdx.x * step; p <= n; p += blockDim.x * step) {
+      double v = f[p];
+      for (int jb = k - 1; jb >= 0; jb--) v = d_add(v, f[p - (1 << jb)]);
+      f[p] = v;
     }
+    __syncthreads();
   }
-  __syncthreads();
   if (use_smem) for (int i = threadIdx.x; i <= n; i += blockDim.x) fen[i] = f[i];
 }
 
