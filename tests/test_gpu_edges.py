@@ -83,3 +83,22 @@ def test_degenerate_inputs_bitexact(case, m, n, lam, name, ov, gv, kw, prec):
     assert tg == to and np.array_equal(gg, go) and np.array_equal(jg, jo)
     assert g.objective() == o.objective()
     g.close()
+
+
+@pytest.mark.parametrize("m,n", [(20000, 48), (3, 9000)])
+@pytest.mark.parametrize("name,ov,gv,kw", [RUNS[0], RUNS[2], RUNS[3], RUNS[4]], ids=[RUNS[q][0] for q in (0, 2, 3, 4)])
+def test_tall_and_wide_sequential_bitexact(m, n, name, ov, gv, kw):
+    """Shapes outside the shared-memory / register-file kernels' limits (m = 20000 rows of h
+    and r do not fit next to the GA tree; n = 9000 stored gaps): the fallback kernels
+    (global-memory state) give the same trajectories."""
+    a, b, C = _inst("ragged", m, n, seed=1)
+    C = C.astype(np.float32)
+    g = sro.Solver(a, b, 1.0, C=C, prec="f32")
+    o = Oracle(a, b, 1.0, C=C, prec="f32", cap=31)
+    iters = 2 * n if n < 1000 else 3000
+    ro = o.solve(ov, iters, seed=2, trace=True, epsilon=-1.0, **kw)
+    rg = g.solve(gv, iters, seed=2, trace=True, epsilon=-1.0, **kw)
+    for f in ("i", "j", "gamma", "num", "den", "minval"):
+        assert np.array_equal(rg["trace"][f], ro["trace"][f]), f
+    assert np.array_equal(g.plan(), o.plan())
+    g.close()
