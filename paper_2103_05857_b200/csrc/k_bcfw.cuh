@@ -377,10 +377,9 @@ __device__ __forceinline__ int ga_draw_t(const double* fen, const double* G, int
   // three levels per round: the 1 + 2 + 4 candidates of the round are loaded
   // together, so the dependent shared-memory loads drop to a third; the
   // comparisons and subtractions are the same operations in the same order.
-  auto ld = [&](int q) {
-    const double v = ldn(q <= n ? q : n);
-    return q <= n ? v : 0.0;
-  };
+  // (a candidate past n is never taken: level() tests pos + b <= n first, so its
+  // clamped load needs no zeroing)
+  auto ld = [&](int q) { return ldn(q <= n ? q : n); };
   auto level = [&](int b, double f) {
     const bool t = (pos + b <= n) && f <= u;
     const double un = d_sub(u, f);
