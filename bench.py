@@ -76,7 +76,10 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True,
+                                         # lowest CPU priority: on a host with few cores the sampler
+                                         # must not delay the solver threads' wake-ups
+                                         preexec_fn=(lambda: os.nice(19)) if hasattr(os, "nice") else None)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
         except Exception:
@@ -152,6 +155,14 @@ class StepRunner:
             try:
                 name, variant, opts, cap = PLAN[q]
                 s = self.solvers[q]
+                if self.concurrent and variant in (0, 4) and hasattr(os, "setpriority"):
+                    # FW / batched are throughput work whose host threads launch often; on a
+                    # host with few cores they would delay the wake-ups of the latency-bound
+                    # sequential solves' threads (whose GPU then idles between segments)
+                    try:
+                        os.setpriority(os.PRIO_PROCESS, threading.get_native_id(), 10)
+                    except OSError:
+                        pass
                 if dbg:
                     evs[q][0].record(self.streams[q])
                 s.reset()

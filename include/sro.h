@@ -96,6 +96,12 @@ typedef struct {
   int32_t rank;         /* this process's shard when nranks == G */
   const void* nccl_id;  /* 128-byte ncclUniqueId (sro_nccl_unique_id on rank 0, shared by the
                            caller), required when nranks > 1 */
+  int32_t max_sms;      /* SM budget of this handle's device-wide kernels (gap / LMO sweeps, block
+                           steps, plan kernels): their grids are sized for min(max_sms, SM count)
+                           SMs instead of every SM (0: every SM). For several handles sharing one
+                           GPU concurrently: it bounds how much of the L2 / HBM bandwidth one
+                           handle's sweeps take from the others' latency-bound steps. Results
+                           do not depend on it (fixed reduction orders). */
 } sro_params;
 
 typedef enum { SRO_FW = 0, SRO_BCFW = 1, SRO_BCAFW = 2, SRO_BCPFW = 3, SRO_BATCHED = 4 } sro_variant;

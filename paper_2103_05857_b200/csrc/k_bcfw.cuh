@@ -55,7 +55,18 @@ struct BcfwArgs {
   int a_smem;            // a staged in shared memory
   int visit_smem;        // the segment's visit list staged in shared memory
   int dbg;               // timing experiments only (SRO_DBG): 1 = skip the serial part, 2 = skip the LMO
+  const int* halt;       // device flag: set -> the segment is a no-op (it was enqueued ahead of
+                         // the host's check of the previous one, which converged or failed)
 };
+
+__device__ __forceinline__ bool bcfw_halted(const BcfwArgs& A) {
+  if (A.halt && *(volatile const int*)A.halt) {
+    if (threadIdx.x == 0) *A.steps_done = 0;
+    return true;
+  }
+  return false;
+}
+
 
 #ifdef SRO_PHASE_TIMING
 struct PhaseState { long long acc[16]; long long t; };
@@ -668,6 +679,7 @@ struct BcfwLayout {
 // ---------------------------------------------------------------------------
 template <class Col, int VAR, bool GA, bool SMEM>
 __global__ void __launch_bounds__(BCFW_THREADS, 1) k_bcfw(BcfwArgs A, Col col) {
+  if (bcfw_halted(A)) return;
   extern __shared__ __align__(16) char smraw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int m = A.m, n = A.n, cap = A.cap;
@@ -950,6 +962,7 @@ struct RfLayout {
 
 template <typename T, int MAXV, int VAR, bool GA>
 __global__ void __launch_bounds__(BCFW_THREADS, 1) k_bcfw_rf(BcfwArgs A, const T* __restrict__ Cg, int64_t ld) {
+  if (bcfw_halted(A)) return;
   using Col = RegCol<T, MAXV>;
   constexpr int W = Col::W;
   extern __shared__ __align__(16) char smraw[];
@@ -1206,7 +1219,8 @@ __global__ void __launch_bounds__(BCFW_THREADS, 1) k_bcfw_rf(BcfwArgs A, const T
 
 // Fenwick rebuild after a GA global refresh: fen[i] = max(G_{i-1}, 0), then
 // the standard linear build (R14), in order, in shared memory when it fits.
-__global__ void k_fen_build(const double* __restrict__ G, double* fen, int n, int use_smem) {
+__global__ void k_fen_build(const double* __restrict__ G, double* fen, int n, int use_smem, const int* stop) {
+  if (stop && *stop) return;   // a failed segment: keep the tree as it is
   extern __shared__ double fs[];
   double* f = use_smem ? fs : fen;
   for (int i = threadIdx.x; i <= n; i += blockDim.x) f[i] = i == 0 ? 0.0 : wpos(G[i - 1]);

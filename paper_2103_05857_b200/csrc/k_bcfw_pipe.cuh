@@ -143,6 +143,7 @@ __device__ __forceinline__ void pipe_owner(int k, int nvec, int& lt, unsigned& b
 
 template <typename T, int MAXV, int VAR>
 __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_pipe(BcfwArgs A, const T* __restrict__ Cg, int64_t ld) {
+  if (bcfw_halted(A)) return;
   constexpr int W = Vec<T>::W;
   extern __shared__ __align__(16) char smraw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -438,6 +439,7 @@ __device__ __forceinline__ int warp_argmin_key(unsigned long long& key, int& j) 
 
 template <typename T, int MAXV, int VAR>
 __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, const T* __restrict__ Cg, int64_t ld) {
+  if (bcfw_halted(A)) return;
   constexpr int W = Vec<T>::W;
   extern __shared__ __align__(16) char smraw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;

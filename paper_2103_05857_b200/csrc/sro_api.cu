@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <mutex>
 #include <type_traits>
+#include <thread>
 #include <vector>
 
 #include "../../include/sro.h"
@@ -76,6 +77,17 @@ struct Solver {
   bool own_stream = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t ev_sync = nullptr;   // blocking-sync event: host waits yield the CPU instead of spinning
+  // Pinned mailbox for the solve loop's small device->host readbacks (rb()): a copy into
+  // pageable memory would hold the calling thread inside cudaMemcpyAsync until the stream
+  // reached it, busy on the CPU that other handles' threads need to launch their work.
+  char* pin = nullptr;
+  size_t pin_off = 0;
+  struct PinDst { void* dst; size_t off, bytes; };
+  std::vector<PinDst> pin_pending;
+  // sequential-family epochs enqueued ahead of the host (seq_epochs): per slot, the
+  // epoch's steps done, status and gap land in pinned memory; an event marks its end
+  char* pin_ep = nullptr;
+  cudaEvent_t ev_ep[2] = {nullptr, nullptr};
   std::string err;
   // problem
   double *a = nullptr, *b = nullptr;
@@ -215,7 +227,9 @@ void timed_end(Solver* s, int idx, int cat, int64_t units) {
 }
 // after a stream sync: fold every completed region into the stats
 void resolve_timing(Solver* s) {
+  std::vector<Solver::Pending> keep;   // pairs of work still in flight (enqueued ahead)
   for (auto& p : s->pending) {
+    if (cudaEventQuery(p.b) == cudaErrorNotReady) { keep.push_back(p); continue; }
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
       if (p.cat == CAT_BCFW) s->stats.bcfw_ms += ms;
@@ -225,7 +239,7 @@ void resolve_timing(Solver* s) {
     s->ev_pool.push_back(p.a);
     s->ev_pool.push_back(p.b);
   }
-  s->pending.clear();
+  s->pending.swap(keep);
 }
 
 #define CUDA_TRY(s, call)                                                                  \
@@ -233,6 +247,7 @@ void resolve_timing(Solver* s) {
     cudaError_t e_ = (call);                                                               \
     if (e_ != cudaSuccess) {                                                               \
       (s)->err = std::string(#call) + ": " + cudaGetErrorString(e_);                       \
+      if ((s)->lead) (s)->lead->pin_pending.clear(); /* no readback outlives a failure */ \
       return e_ == cudaErrorMemoryAllocation ? SRO_ERR_OOM : SRO_ERR_CUDA;                 \
     }                                                                                      \
   } while (0)
@@ -276,9 +291,20 @@ template <typename T>
 cudaError_t dalloc(T** p, size_t count) {
   return cudaMalloc((void**)p, sizeof(T) * (count ? count : 1));
 }
-// Wait for the solver stream with a blocking-sync event (several handles may
-// run concurrently from host threads: a spinning wait would starve the
-// threads that are launching kernels).
+// Host wait for an event: poll, yielding the core between polls. A blocking-sync
+// wait sleeps until an interrupt wakes the thread (tens to hundreds of us per
+// wait, paid on every gap check); a yielding poll returns within a poll of the
+// event and still gives the core to other runnable threads (other handles'
+// launch threads) when there are any.
+cudaError_t wait_event(cudaEvent_t ev) {
+  for (;;) {
+    const cudaError_t e = cudaEventQuery(ev);
+    if (e != cudaErrorNotReady) return e;
+    std::this_thread::yield();
+  }
+}
+
+// Wait for the solver stream (record + wait_event).
 cudaError_t stream_wait(Solver* s) {
   Solver* L = s->lead;
   if (!L->ev_sync) {
@@ -287,7 +313,29 @@ cudaError_t stream_wait(Solver* s) {
   }
   cudaError_t e = cudaEventRecord(L->ev_sync, s->stream);
   if (e != cudaSuccess) return e;
-  return cudaEventSynchronize(L->ev_sync);
+  e = wait_event(L->ev_sync);
+  if (e == cudaSuccess)
+    for (const auto& q : L->pin_pending) memcpy(q.dst, L->pin + q.off, q.bytes);
+  L->pin_pending.clear();
+  L->pin_off = 0;
+  return e;
+}
+
+// Device->host readback of a few bytes through the pinned mailbox: *dst holds the
+// value after the next stream_wait (every caller synchronises before using it).
+constexpr size_t PIN_BYTES = 4096;
+cudaError_t rb(Solver* s, void* dst, const void* src, size_t bytes) {
+  Solver* L = s->lead;
+  if (!L->pin) {
+    cudaError_t e = cudaHostAlloc((void**)&L->pin, PIN_BYTES, cudaHostAllocDefault);
+    if (e != cudaSuccess) { L->pin = nullptr; return e; }
+  }
+  if (L->pin_off + bytes > PIN_BYTES) return cudaErrorInvalidValue;
+  cudaError_t e = cudaMemcpyAsync(L->pin + L->pin_off, src, bytes, cudaMemcpyDeviceToHost, s->stream);
+  if (e != cudaSuccess) return e;
+  L->pin_pending.push_back({dst, L->pin_off, bytes});
+  L->pin_off += (bytes + 15) & ~(size_t)15;
+  return cudaSuccess;
 }
 
 // Stream-ordered (re)allocation of solve-time workspaces: no device-wide
@@ -494,26 +542,31 @@ sro_status ws_clean(Solver* s) {
   return SRO_OK;
 }
 
+// A device status word read by the host: 0 -> SRO_OK; else the error, with the
+// status words and workspaces cleared for the next call.
+sro_status status_fail(Solver* s, int first) {
+  if (!first) return SRO_OK;
+  auto H = held(s->lead);
+  s->lead->err = first == 5 ? "non-finite value met in the LMO" : first == 6 ? "column support exceeds slab_cap" : "device error";
+  for (Solver* t : H) {
+    CUDA_TRY(s, cudaMemsetAsync(t->status, 0, sizeof(int), s->stream));
+    sro_status e = ws_clean(t);
+    if (e) return e;
+  }
+  return (sro_status)first;
+}
+
 // Synchronise and read the status word of every held shard (they agree: the
 // sharded phases propagate the first error of any shard to all of them).
 sro_status check_status(Solver* s) {
   auto H = held(s->lead);
   std::vector<int> st(H.size(), 0);
   for (size_t q = 0; q < H.size(); q++)
-    CUDA_TRY(s, cudaMemcpyAsync(&st[q], H[q]->status, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(s, rb(s, &st[q], H[q]->status, sizeof(int)));
   CUDA_TRY(s, stream_wait(s));
   int first = 0;
   for (int v : st) if (v && !first) first = v;
-  if (first) {
-    s->lead->err = first == 5 ? "non-finite value met in the LMO" : first == 6 ? "column support exceeds slab_cap" : "device error";
-    for (Solver* t : H) {
-      CUDA_TRY(s, cudaMemsetAsync(t->status, 0, sizeof(int), s->stream));
-      sro_status e = ws_clean(t);
-      if (e) return e;
-    }
-    return (sro_status)first;
-  }
-  return SRO_OK;
+  return status_fail(s, first);
 }
 
 // Sharded exchange of `count` doubles per shard: buf holds G slots of `count`;
@@ -662,12 +715,14 @@ sro_status sweep(Solver* s, const int* col0_dev, int col0_mul, int col0_host, in
 // Full gap sweep: g(T) = psum256_i g_i (Thm 2 / Eq. 11) -> host. Sharded:
 // every held shard sweeps its columns into its slot of gx, the slots are
 // exchanged and the total is the psum256 over the n global columns.
-sro_status gap_sweep(Solver* s, double* total) {
+// The gap sweep without the synchronisation: *total is written when the stream
+// reaches it (the caller synchronises; stop as in ga_global_refresh, unsharded only).
+sro_status gap_sweep_kernels(Solver* s, const int* stop = nullptr) {
   sro_status st;
   if (s->G == 1) {
-    st = sweep(s, nullptr, 0, 0, s->n, s->sw_j, s->sw_min, s->sw_g, nullptr);
+    st = sweep(s, nullptr, 0, 0, s->n, s->sw_j, s->sw_min, s->sw_g, stop);
     if (st) return st;
-    k_psum256<<<1, 256, 0, s->stream>>>(s->sw_g, s->n, s->scal + 4, nullptr, nullptr, nullptr);
+    k_psum256<<<1, 256, 0, s->stream>>>(s->sw_g, s->n, s->scal + 4, nullptr, nullptr, stop);
   } else {
     for (Solver* t : held(s)) {
       st = sweep(t, nullptr, 0, 0, t->n, t->sw_j, t->sw_min, s->gx + (size_t)t->shard * t->n, nullptr);
@@ -679,7 +734,18 @@ sro_status gap_sweep(Solver* s, double* total) {
   }
   s->lead->stats.kernel_launches += 1;
   CUDA_TRY(s, cudaGetLastError());
-  CUDA_TRY(s, cudaMemcpyAsync(total, s->scal + 4, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+  return SRO_OK;
+}
+sro_status gap_sweep_enqueue(Solver* s, double* total, const int* stop = nullptr) {
+  sro_status st = gap_sweep_kernels(s, stop);
+  if (st) return st;
+  CUDA_TRY(s, rb(s, total, s->scal + 4, sizeof(double)));
+  return SRO_OK;
+}
+
+sro_status gap_sweep(Solver* s, double* total) {
+  sro_status st = gap_sweep_enqueue(s, total);
+  if (st) return st;
   st = check_status(s);  // synchronises
   resolve_timing(s);
   return st;
@@ -915,11 +981,11 @@ sro_status bcfw_run(Solver* s, BcfwArgs& A) {
 }
 
 sro_status bcfw_segment(Solver* s, int variant, const sro_options* o, int steps, const int* dvisit,
-                        double* dtrace) {
+                        double* dtrace, long long k0, const int* halt) {
   BcfwArgs A{};
   A.m = s->m; A.n = s->n; A.cap = s->cap; A.lambda = s->lambda;
   A.a = s->a; A.b = s->b; A.r = s->r; A.h = s->h; A.cnt = s->cnt; A.srow = s->srow; A.sval = s->sval;
-  A.visit = dvisit; A.steps = steps; A.k0 = s->k; A.step_rule = o->step;
+  A.visit = dvisit; A.steps = steps; A.k0 = k0; A.step_rule = o->step; A.halt = halt;
   A.G = s->G_ga; A.fen = s->fen; A.ga_inner = o->ga_inner; A.ga_post = o->ga_post_update; A.seed = s->seed;
   A.status = s->status; A.steps_done = s->steps_done; A.trace = dtrace;
   A.phase = s->phase;
@@ -946,7 +1012,7 @@ sro_status ensure_cmax(Solver* s) {
   });
   if (st) return st;
   unsigned long long bits = 0;
-  CUDA_TRY(s, cudaMemcpyAsync(&bits, d_cmax, sizeof(bits), cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(s, rb(s, &bits, d_cmax, sizeof(bits)));
   CUDA_TRY(s, stream_wait(s));
   double v;
   memcpy(&v, &bits, sizeof(v));
@@ -954,21 +1020,128 @@ sro_status ensure_cmax(Solver* s) {
   return SRO_OK;
 }
 
-sro_status fen_build(Solver* s, int n_tree = -1) {
+sro_status fen_build(Solver* s, int n_tree = -1, const int* stop = nullptr) {
   const int nt = n_tree < 0 ? s->n : n_tree;
   const size_t bytes = sizeof(double) * ((size_t)nt + 1);
   const int use_smem = bytes <= 200 * 1024;
   if (use_smem) CUDA_TRY(s, set_dyn_smem((const void*)k_fen_build, s->device, (int)bytes));
-  k_fen_build<<<1, 256, use_smem ? bytes : 0, s->stream>>>(s->G_ga, s->fen, nt, use_smem);
+  k_fen_build<<<1, 256, use_smem ? bytes : 0, s->stream>>>(s->G_ga, s->fen, nt, use_smem, stop);
   s->lead->stats.kernel_launches += 1;
   CUDA_TRY(s, cudaGetLastError());
   return SRO_OK;
 }
 
-sro_status ga_global_refresh(Solver* s) {
-  sro_status st = sweep(s, nullptr, 0, 0, s->n, s->sw_j, s->sw_min, s->G_ga, nullptr);
+// stop: device flag (the solver status) that turns the refresh into a no-op when
+// the segment before it failed (enqueued before the host has seen that segment's status)
+sro_status ga_global_refresh(Solver* s, const int* stop = nullptr) {
+  sro_status st = sweep(s, nullptr, 0, 0, s->n, s->sw_j, s->sw_min, s->G_ga, stop);
   if (st) return st;
-  return fen_build(s);
+  return fen_build(s, -1, stop);
+}
+
+__global__ void k_halt_on_status(const int* status, int* halt) {
+  if (*status) *halt = 1;
+}
+__global__ void k_halt_on_gap(const double* g, double eps, int* halt) {
+  if (!*halt && *g <= eps) *halt = 1;
+}
+
+// The sequential BCFW family (Alg. 1, A.2-A.4) from s->k on, until the gap check
+// meets epsilon, iters steps are done or a segment fails. One epoch = a persistent
+// kernel segment up to the next gap check / GA global refresh (whichever is first),
+// then that refresh and check. Epoch e+1 is enqueued before the host reads epoch
+// e's outcome; its kernels test s->stop, which e's tail sets on failure or
+// convergence, so a speculative epoch changes nothing. Same kernels, same order,
+// same results as checking after every epoch.
+sro_status seq_epochs(Solver* s, int variant, const sro_options* o, int64_t iters, long long period, long long gaMn,
+                      bool ga, int64_t* done_io, sro_result* out) {
+  Solver* L = s->lead;
+  const int64_t m = s->m, n = s->n;
+  if (!L->pin_ep) {
+    if (cudaHostAlloc((void**)&L->pin_ep, 64, cudaHostAllocDefault) != cudaSuccess) {
+      L->pin_ep = nullptr; s->err = "cudaHostAlloc"; return SRO_ERR_CUDA;
+    }
+    for (int q = 0; q < 2; q++)
+      CUDA_TRY(s, cudaEventCreateWithFlags(&L->ev_ep[q], cudaEventBlockingSync | cudaEventDisableTiming));
+  }
+  struct Ep { long long k0; int64_t done0; long long seg; bool refresh, check; int slot; };
+  auto plan = [&](long long k, int64_t dn, int slot) {
+    Ep e;
+    e.k0 = k; e.done0 = dn; e.slot = slot;
+    long long sg = iters - dn;
+    const long long tc = period - k % period;
+    if (sg > tc) sg = tc;
+    if (ga) { const long long tr = gaMn - k % gaMn; if (sg > tr) sg = tr; }
+    e.seg = sg;
+    e.refresh = ga && (k + sg) % gaMn == 0;
+    e.check = (k + sg) % period == 0;
+    return e;
+  };
+  auto enqueue = [&](const Ep& e) -> sro_status {
+    sro_status st = bcfw_segment(s, variant, o, (int)e.seg, ga ? nullptr : s->visit + e.done0,
+                                 o->trace ? s->trace + 9 * e.done0 : nullptr, e.k0, s->stop);
+    if (st) return st;
+    k_halt_on_status<<<1, 1, 0, s->stream>>>(s->status, s->stop);
+    s->lead->stats.kernel_launches += 1;
+    if (e.refresh) { st = ga_global_refresh(s, s->stop); if (st) return st; }
+    if (e.check) {
+      st = gap_sweep_kernels(s, s->stop);
+      if (st) return st;
+      k_halt_on_gap<<<1, 1, 0, s->stream>>>(s->scal + 4, o->epsilon, s->stop);
+      s->lead->stats.kernel_launches += 1;
+    }
+    CUDA_TRY(s, cudaGetLastError());
+    char* slot = L->pin_ep + 32 * e.slot;
+    CUDA_TRY(s, cudaMemcpyAsync(slot, s->steps_done, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(s, cudaMemcpyAsync(slot + 4, s->status, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+    if (e.check) CUDA_TRY(s, cudaMemcpyAsync(slot + 8, s->scal + 4, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(s, cudaEventRecord(L->ev_ep[e.slot], s->stream));
+    return SRO_OK;
+  };
+  CUDA_TRY(s, cudaMemsetAsync(s->stop, 0, sizeof(int), s->stream));
+  int64_t done = *done_io;
+  sro_status st = SRO_OK;
+  Ep cur = plan(s->k, done, 0), nx{};
+  bool spec = false;   // nx enqueued and not yet consumed
+  st = enqueue(cur);
+  while (!st) {
+    const bool have_next = cur.done0 + cur.seg < iters;
+    if (have_next) {
+      nx = plan(cur.k0 + cur.seg, cur.done0 + cur.seg, cur.slot ^ 1);
+      st = enqueue(nx);
+      if (st) break;
+      spec = true;
+    }
+    if (wait_event(L->ev_ep[cur.slot]) != cudaSuccess) { s->err = "epoch synchronisation"; st = SRO_ERR_CUDA; break; }
+    const char* slot = L->pin_ep + 32 * cur.slot;
+    int sd = 0, dst = 0;
+    double g = 0.0;
+    memcpy(&sd, slot, sizeof(int));
+    memcpy(&dst, slot + 4, sizeof(int));
+    if (cur.check) memcpy(&g, slot + 8, sizeof(double));
+    resolve_timing(s);
+    s->k += sd; done += sd;
+    out->entries_scanned += m * sd * ((ga && o->ga_inner && o->ga_post_update) ? 2 : 1);
+    if (dst) { st = status_fail(s, dst); break; }
+    if (sd != cur.seg) { s->err = "segment stopped early without a status"; st = SRO_ERR_CUDA; break; }
+    if (cur.refresh) out->entries_scanned += m * n;
+    if (cur.check) {
+      out->gap = g; out->gap_checks++;
+      out->entries_scanned += m * n;
+      if (g <= o->epsilon) { out->converged = 1; break; }
+    }
+    if (!have_next) break;
+    cur = nx;
+    spec = false;
+  }
+  if (spec) {   // the epoch enqueued ahead was a no-op: its segment is not a launch of steps
+    L->stats.bcfw_launches -= 1;
+    L->stats.bcfw_steps -= nx.seg;
+  }
+  *done_io = done;
+  // after any speculative epoch still in flight (a no-op)
+  CUDA_TRY(s, cudaMemsetAsync(s->stop, 0, sizeof(int), s->stream));
+  return st;
 }
 
 sro_status ga_initialise(Solver* s) {
@@ -1235,7 +1408,7 @@ sro_status shard_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
 // report a device error.
 sro_status drain_block_steps(Solver* s, int64_t* done) {
   unsigned long long ds = 0;
-  CUDA_TRY(s, cudaMemcpyAsync(&ds, s->dsteps, sizeof(ds), cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(s, rb(s, &ds, s->dsteps, sizeof(ds)));
   sro_status st = check_status(s);   // synchronises
   resolve_timing(s);
   for (Solver* t : held(s)) CUDA_TRY(s, cudaMemsetAsync(t->dsteps, 0, sizeof(unsigned long long), s->stream));
@@ -1275,7 +1448,7 @@ sro_status objective_dev(Solver* s, double* f_host) {
   k_objective_final<<<1, 1, 0, s->stream>>>(s->scal + 4, s->scal + 5, s->lambda, s->scal + 7);
   s->lead->stats.kernel_launches += 4 + (int64_t)held(s).size();
   CUDA_TRY(s, cudaGetLastError());
-  CUDA_TRY(s, cudaMemcpyAsync(f_host, s->scal + 7, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(s, rb(s, f_host, s->scal + 7, sizeof(double)));
   CUDA_TRY(s, stream_wait(s));
   return SRO_OK;
 }
@@ -1318,6 +1491,11 @@ void free_shard(Solver* s) {
 
 void free_solver(Solver* s) {
   if (!s) return;
+  if (s->pin) cudaFreeHost(s->pin);
+  s->pin = nullptr;
+  if (s->pin_ep) cudaFreeHost(s->pin_ep);
+  s->pin_ep = nullptr;
+  for (auto& e : s->ev_ep) if (e) { cudaEventDestroy(e); e = nullptr; }
   for (Solver* p : s->peers) free_shard(p);
   s->peers.clear();
   if (s->x1) cudaFree(s->x1);
@@ -1454,6 +1632,8 @@ sro_status sro_create(const double* a, const double* b, const sro_cost* cost, co
   if (cudaSetDevice(p->device) != cudaSuccess) return fail(SRO_ERR_CUDA, "cudaSetDevice failed (no CUDA device?)");
   int num_sms = 148;
   cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, p->device);
+  if (p->max_sms < 0) return fail(SRO_ERR_INVALID_ARG, "max_sms must be >= 0");
+  if (p->max_sms > 0 && p->max_sms < num_sms) num_sms = p->max_sms;
   if (p->cuda_stream) s->stream = (cudaStream_t)p->cuda_stream;
   else { if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess) return fail(SRO_ERR_CUDA, "stream"); s->own_stream = true; }
   std::vector<int> shards_held;
@@ -1660,8 +1840,8 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
       const int64_t before = done;
       double G = 0.0;
       int stopped = 0;
-      CUDA_TRY(s, cudaMemcpyAsync(&G, s->scal + 0, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
-      CUDA_TRY(s, cudaMemcpyAsync(&stopped, s->stop, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+      CUDA_TRY(s, rb(s, &G, s->scal + 0, sizeof(double)));
+      CUDA_TRY(s, rb(s, &stopped, s->stop, sizeof(int)));
       st = drain_block_steps(s, &done);
       if (st) return st;
       out->gap = G;
@@ -1777,26 +1957,15 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
         }
         continue;
       }
-      long long seg = iters - done;
-      const long long to_check = period - s->k % period;
-      if (seg > to_check) seg = to_check;
-      if (ga) { const long long to_ref = gaMn - s->k % gaMn; if (seg > to_ref) seg = to_ref; }
-      st = bcfw_segment(s, variant, o, (int)seg, ga ? nullptr : s->visit + done, o->trace ? s->trace + 9 * done : nullptr);
-      if (st) return st;
-      int sd = 0;
-      CUDA_TRY(s, cudaMemcpyAsync(&sd, s->steps_done, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
-      st = check_status(s);
-      resolve_timing(s);
-      s->k += sd; done += sd;
-      out->entries_scanned += (int64_t)m * sd * ((ga && o->ga_inner && o->ga_post_update) ? 2 : 1);
-      if (st) break;
-      if (ga && s->k % gaMn == 0) {
-        st = ga_global_refresh(s);
-        if (st) return st;
-        out->entries_scanned += (int64_t)m * n;
-      }
-    }
-  }
+      // Sequential family: epochs (a persistent-kernel segment, then the GA global
+      // refresh and the gap check due at its end) are enqueued one ahead of the host's
+      // check, so the GPU never waits for the host between epochs. Every kernel of an
+      // epoch is guarded by the device flag s->stop, which the epoch before sets when
+      // its segment failed or its gap reached epsilon: a speculative epoch after it is
+      // then a no-op and the state is exactly the checked one.
+      st = seq_epochs(s, variant, o, iters, period, gaMn, ga, &done, out);
+      break;
+    }  }
   out->iters_done = done;
   out->k = s->k;
   CUDA_TRY(s, cudaEventRecord(s->ev1, s->stream));

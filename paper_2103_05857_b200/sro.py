@@ -48,7 +48,8 @@ class SroCost(ct.Structure):
 class SroParams(ct.Structure):
     _fields_ = [("m", ct.c_int32), ("n", ct.c_int32), ("lambda_", ct.c_double), ("slab_cap", ct.c_int32),
                 ("device", ct.c_int32), ("cuda_stream", ct.c_void_p), ("shards", ct.c_int32),
-                ("shard_block", ct.c_int32), ("nranks", ct.c_int32), ("rank", ct.c_int32), ("nccl_id", ct.c_void_p)]
+                ("shard_block", ct.c_int32), ("nranks", ct.c_int32), ("rank", ct.c_int32), ("nccl_id", ct.c_void_p),
+                ("max_sms", ct.c_int32)]
 
 
 class SroTraceRec(ct.Structure):
@@ -153,10 +154,12 @@ class Solver:
     cost='sqeuclid' / 'euclid': X (m x 3) and Y (n x 3) colours.
     cost='hash': iid uniform C generated on the device from hash_seed.
     prec='f64' | 'f32' is the storage / evaluation precision of the cost.
+    max_sms > 0 sizes the handle's device-wide kernels for that many SMs (sro_params.max_sms).
     """
 
     def __init__(self, a, b, lam, *, C=None, X=None, Y=None, cost="dense", prec="f64", hash_seed=0, slab_cap=31,
-                 device=0, stream=None, ld=None, shards=1, shard_block=0, nranks=1, rank=0, nccl_id=None):
+                 device=0, stream=None, ld=None, shards=1, shard_block=0, nranks=1, rank=0, nccl_id=None,
+                 max_sms=0):
         L = load_library()
         self._L = L
         a = np.ascontiguousarray(a, dtype=np.float64)
@@ -192,7 +195,8 @@ class Solver:
             idbuf = ct.create_string_buffer(bytes(nccl_id), 128)
         p = SroParams(m=self.m, n=self.n, lambda_=self.lam, slab_cap=slab_cap, device=device,
                       cuda_stream=ct.c_void_p(stream) if stream else None, shards=shards, shard_block=shard_block,
-                      nranks=nranks, rank=rank, nccl_id=ct.cast(idbuf, ct.c_void_p) if idbuf is not None else None)
+                      nranks=nranks, rank=rank, nccl_id=ct.cast(idbuf, ct.c_void_p) if idbuf is not None else None,
+                      max_sms=max_sms)
         h = ct.c_void_p()
         st = L.sro_create(_ptr(a), _ptr(b), ct.byref(c), ct.byref(p), ct.byref(h))
         if st != OK:
