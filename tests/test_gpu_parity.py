@@ -322,3 +322,35 @@ def test_config1_shape_pipelined_kernels_bitexact(var, kw):
     rg = g.solve(gv, 6 * 512, seed=2, trace=True, epsilon=1e-9, **_gpu_opts(kw))
     assert_same_trace(rg["trace"], ro["trace"])
     assert_same_state(g, o)
+
+
+@pytest.mark.parametrize("name,ov,gv,kw", [VARIANTS[0], VARIANTS[3], VARIANTS[5]], ids=["bcfw", "bcafw", "ga"])
+def test_converges_mid_call_then_continues_like_oracle(name, ov, gv, kw):
+    """Epochs are enqueued one ahead of the host's gap check (a speculative epoch after the
+    converging one is a no-op): the call stops at the oracle's gap check with the oracle's
+    state, and a second call continues exactly as the oracle's second call."""
+    d = instance(0, seed=3)
+    g, o = pair(d)
+    for iters, conv in ((3 * 256 + 100, False), (400 * 256, True), (400 * 256, True)):
+        ro = o.solve(ov, iters, seed=5, epsilon=1e-5, **kw)
+        rg = g.solve(gv, iters, seed=5, epsilon=1e-5, **_gpu_opts(kw))
+        assert bool(rg["converged"]) == bool(ro["converged"]) == conv
+        assert rg["iters_done"] == ro["iters_done"] and rg["gap"] == ro["gap"]
+        assert rg["gap_checks"] == ro["gap_checks"] and rg["entries_scanned"] == ro["entries_scanned"]
+        assert_same_state(g, o)
+
+
+def test_max_sms_does_not_change_results():
+    """sro_params.max_sms only resizes the device-wide kernels' grids: FW, batched and GA
+    trajectories are identical with 3 SMs and with all of them."""
+    d = instance(1, m=300, n=260, seed=8)
+    runs = [(sro.SRO_FW, dict(step=sro.STEP_ELS), 12), (sro.SRO_BATCHED, dict(step=sro.STEP_ELS, block_size=13), 60),
+            (sro.SRO_BCFW, dict(step=sro.STEP_ELS, sampling=sro.SAMPLE_GA, ga_M=1, ga_inner=1, ga_post_update=1), 1300)]
+    for v, kw, iters in runs:
+        out = []
+        for ms in (0, 3):
+            g = sro.Solver(d["a"], d["b"], d["lam"], C=d["C32"], prec="f32", max_sms=ms)
+            r = g.solve(v, iters, seed=2, trace=True, epsilon=1e-12, **kw)
+            out.append((r["trace"], g.plan(), r["gap"]))
+            g.close()
+        assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1]) and out[0][2] == out[1][2]
