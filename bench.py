@@ -25,6 +25,7 @@ import argparse
 import json
 import os
 import statistics
+import shutil
 import subprocess
 import sys
 import threading
@@ -74,12 +75,11 @@ class ClockSampler:
         if os.environ.get("SRO_BENCH_NO_CLOCKS"):   # A/B only: the contract needs the samples
             return
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True,
-                                         # lowest CPU priority: on a host with few cores the sampler
-                                         # must not delay the solver threads' wake-ups
-                                         preexec_fn=(lambda: os.nice(19)) if hasattr(os, "nice") else None)
+            # lowest CPU priority (nice 19): the sampler must not delay the solver threads
+            nice = ["nice", "-n", "19"] if shutil.which("nice") else []
+            self.proc = subprocess.Popen(nice + ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                                                 "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
         except Exception:
