@@ -76,7 +76,7 @@ struct Solver {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  cudaEvent_t ev_sync = nullptr;   // blocking-sync event: host waits yield the CPU instead of spinning
+  cudaEvent_t ev_sync = nullptr;   // marks the stream position a host wait (wait_event) polls for
   // Pinned mailbox for the solve loop's small device->host readbacks (rb()): a copy into
   // pageable memory would hold the calling thread inside cudaMemcpyAsync until the stream
   // reached it, busy on the CPU that other handles' threads need to launch their work.
@@ -308,7 +308,7 @@ cudaError_t wait_event(cudaEvent_t ev) {
 cudaError_t stream_wait(Solver* s) {
   Solver* L = s->lead;
   if (!L->ev_sync) {
-    cudaError_t e = cudaEventCreateWithFlags(&L->ev_sync, cudaEventBlockingSync | cudaEventDisableTiming);
+    cudaError_t e = cudaEventCreateWithFlags(&L->ev_sync, cudaEventDisableTiming);
     if (e != cudaSuccess) return e;
   }
   cudaError_t e = cudaEventRecord(L->ev_sync, s->stream);
@@ -1062,7 +1062,7 @@ sro_status seq_epochs(Solver* s, int variant, const sro_options* o, int64_t iter
       L->pin_ep = nullptr; s->err = "cudaHostAlloc"; return SRO_ERR_CUDA;
     }
     for (int q = 0; q < 2; q++)
-      CUDA_TRY(s, cudaEventCreateWithFlags(&L->ev_ep[q], cudaEventBlockingSync | cudaEventDisableTiming));
+      CUDA_TRY(s, cudaEventCreateWithFlags(&L->ev_ep[q], cudaEventDisableTiming));
   }
   struct Ep { long long k0; int64_t done0; long long seg; bool refresh, check; int slot; };
   auto plan = [&](long long k, int64_t dn, int slot) {
