@@ -361,6 +361,14 @@ inline void sfree(void* p, cudaStream_t st) {
 // ---------------------------------------------------------------------------
 // Small kernels: init, validation, hash generator, objective pieces, max cost
 // ---------------------------------------------------------------------------
+// r_0 = sum_i b_i over all n columns, left to right (every shard alike), into
+// b_full[n_full]: once per handle, so a reset does not repeat the serial sum.
+__global__ void k_r0(double* b_full, int n_full) {
+  double r0 = 0.0;
+  for (int i = 0; i < n_full; i++) r0 = d_add(r0, b_full[i]);
+  b_full[n_full] = r0;
+}
+
 __global__ void k_init_plan(const double* __restrict__ b, const double* __restrict__ b_full, int n_full,
                             const double* __restrict__ a, double* r, double* h, int* cnt, int* srow, double* sval,
                             int m, int n, int cap, double lambda) {
@@ -374,8 +382,7 @@ __global__ void k_init_plan(const double* __restrict__ b, const double* __restri
   }
   for (int k = tid; k < m; k += stride) {
     if (k == 0) {
-      double r0 = 0.0;
-      for (int i = 0; i < n_full; i++) r0 = d_add(r0, b_full[i]);
+      const double r0 = b_full[n_full];   // k_r0, once per handle
       r[0] = r0;
       h[0] = d_div(d_sub(r0, a[0]), lambda);
     } else {
@@ -1515,7 +1522,7 @@ sro_status build_shard(Solver* s, const double* a, const double* b_loc, const do
   cudaEventCreate(&s->ev0); cudaEventCreate(&s->ev1);
 #define ALLOC(ptr, cnt_)                                                              \
   if (salloc(&(ptr), (cnt_), s->stream) != cudaSuccess) { s->err = "device allocation failed"; return SRO_ERR_OOM; }
-  ALLOC(s->a, m); ALLOC(s->b, n); ALLOC(s->b_full, s->n_glob); ALLOC(s->r, m); ALLOC(s->h, m);
+  ALLOC(s->a, m); ALLOC(s->b, n); ALLOC(s->b_full, s->n_glob + 1); ALLOC(s->r, m); ALLOC(s->h, m);
   ALLOC(s->cnt, n); ALLOC(s->srow, (size_t)n * s->cap); ALLOC(s->sval, (size_t)n * s->cap);
   if (s->G == 1) { ALLOC(s->G_ga, n); ALLOC(s->fen, (size_t)n + 1); }
   else if (s->lead == s) { ALLOC(s->G_ga, s->n_glob); ALLOC(s->fen, (size_t)s->n_glob + 1); }   // GA block sampling
@@ -1531,6 +1538,7 @@ sro_status build_shard(Solver* s, const double* a, const double* b_loc, const do
   cudaMemcpyAsync(s->a, a, sizeof(double) * m, cudaMemcpyHostToDevice, s->stream);
   cudaMemcpyAsync(s->b, b_loc, sizeof(double) * n, cudaMemcpyHostToDevice, s->stream);
   cudaMemcpyAsync(s->b_full, b_all, sizeof(double) * s->n_glob, cudaMemcpyHostToDevice, s->stream);
+  k_r0<<<1, 1, 0, s->stream>>>(s->b_full, s->n_glob);
   const size_t esz = s->prec == SRO_FP32 ? 4 : 8;
   const int vec = 16 / (int)esz;
   if (s->kind == SRO_COST_DENSE) {
