@@ -658,8 +658,17 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
           // <t', c_i + h'> over the new support, rows ascending (entries in o's lane layout)
           const double ce = o.merged ? mC : cw;
           const double term = o.keep ? d_mul(o.tnew, d_add(ce, sh_h[o.erow])) : 0.0;
+          // same adds in the same order; the first three terms' shuffles are issued
+          // together (supports mostly hold at most three entries)
+          const unsigned km0 = o.kmask, km1 = km0 & (km0 - 1u), km2 = km1 & (km1 - 1u);
+          const double s0 = __shfl_sync(FULL, term, km0 ? __ffs(km0) - 1 : 0);
+          const double s1 = __shfl_sync(FULL, term, km1 ? __ffs(km1) - 1 : 0);
+          const double s2 = __shfl_sync(FULL, term, km2 ? __ffs(km2) - 1 : 0);
           double acc = 0.0;
-          unsigned km = o.kmask;
+          if (km0) acc = d_add(acc, s0);
+          if (km1) acc = d_add(acc, s1);
+          if (km2) acc = d_add(acc, s2);
+          unsigned km = km2 & (km2 - 1u);
           while (km) {
             const int q = __ffs(km) - 1;
             km &= km - 1;
