@@ -597,6 +597,9 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
       const double csup = __shfl_sync(FULL, cw, wsl);
       const double u_next = uniform53(rng_u64(A.seed, 1, (uint64_t)(kk + 1)));   // next draw's uniform (while the LMO warps scan)
       const long long fen_node = ga_path_node(n, i);   // this lane's Fenwick node for the refresh (idem)
+      // its value and the stored gap of column i (nothing writes either before the refresh)
+      const double fen_old = fen_node <= n ? fens[fen_node] : 0.0;
+      const double gs_old = Gs[i];
       nbar_sync(BAR_PART, GA_SYNC);
       unsigned long long k1 = lane < GA_LMO_WARPS ? pk[lane] : ~0ULL;
       int r1 = lane < GA_LMO_WARPS ? pj[lane] : 0x7fffffff;
@@ -676,9 +679,9 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
           }
           gnew = d_sub(acc, d_mul(bi, mnew));
         }
-        const double delta = d_sub(wpos(gnew), wpos(Gs[i]));
+        const double delta = d_sub(wpos(gnew), wpos(gs_old));
+        if (fen_node <= n) fens[fen_node] = d_add(fen_old, delta);   // ga_add_node with the value loaded early
         __syncwarp();
-        ga_add_node(fens, n, fen_node, delta);
         PW_MARK(6);
         if (lane == 0) Gs[i] = gnew;
         __syncwarp();
