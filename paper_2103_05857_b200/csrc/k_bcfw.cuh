@@ -476,11 +476,28 @@ struct StepOut {
 #define SP_PARAM
 #define SP_ARG
 #endif
-template <int VAR>
+// <t_i, grad_i f> over the slab (lanes < c0 hold t_ki (C_ki + h_k), rows ascending),
+// summed in slab order; needs no LMO result, so a caller may form it while the LMO runs
+__device__ __forceinline__ double slab_dot(double prod, int c0) {
+  double dv[8];
+#pragma unroll
+  for (int q = 0; q < 8; q++) dv[q] = __shfl_sync(FULL, prod, q);
+  double acc = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; q++) {
+    if (q >= c0) break;
+    acc = d_add(acc, dv[q]);
+  }
+  for (int q = 8; q < c0; q++) acc = d_add(acc, __shfl_sync(FULL, prod, q));
+  return acc;
+}
+
+// PRE_DOT: the caller passes slab_dot(t_i (C_i + h), c0) in dot_in
+template <int VAR, bool PRE_DOT = false>
 __device__ __forceinline__ StepOut serial_step(const BcfwArgs& A, long long kk, int i, int j, double mv, double bi,
                                                int c0, int rw, double tv, double gk, double* r, double* h,
                                                float* h32, const double* a, int* cnt2, double* slots,
-                                               float* hmax SP_PARAM) {
+                                               float* hmax SP_PARAM, double dot_in = 0.0) {
   const int lane = threadIdx.x & 31;
   const int m = A.m, n = A.n, cap = A.cap;
   const double lam = A.lambda;
@@ -488,11 +505,12 @@ __device__ __forceinline__ StepOut serial_step(const BcfwArgs& A, long long kk, 
   o.dir = 0; o.vrow = -1; o.gamma = 0.0; o.num = 0.0; o.den = 0.0; o.hnew = 0.0;
   // <t_i, grad_i f>: operands fetched now, summed (rows ascending) once the
   // independent merged-support / denominator work below has been issued
-  const double prod = d_mul(tv, gk);
+  const double prod = PRE_DOT ? 0.0 : d_mul(tv, gk);
   double dv[8];
 #pragma unroll
-  for (int q = 0; q < 8; q++) dv[q] = __shfl_sync(FULL, prod, q);
+  for (int q = 0; q < 8; q++) dv[q] = PRE_DOT ? 0.0 : __shfl_sync(FULL, prod, q);
   auto finish_dot = [&]() {
+    if (PRE_DOT) return dot_in;
     double acc = 0.0;
 #pragma unroll
     for (int q = 0; q < 8; q++) {

@@ -600,6 +600,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
       // its value and the stored gap of column i (nothing writes either before the refresh)
       const double fen_old = fen_node <= n ? fens[fen_node] : 0.0;
       const double gs_old = Gs[i];
+      const double dot = slab_dot(d_mul(tv, gk), c0);   // <t_i, grad_i f> (idem)
       nbar_sync(BAR_PART, GA_SYNC);
       unsigned long long k1 = lane < GA_LMO_WARPS ? pk[lane] : ~0ULL;
       int r1 = lane < GA_LMO_WARPS ? pj[lane] : 0x7fffffff;
@@ -621,8 +622,8 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
       const double m_out = kout == ~0ULL ? dinf() : okey_inv(kout);
       // ---- the serial part
       PW_MARK(4);
-      const StepOut o = serial_step<VAR>(A, kk, i, j, mv, bi, c0, rw, tv, gk, sh_r, sh_h, nullptr, sh_a, sh_cnt,
-                                         slots, nullptr SP_NULL);
+      const StepOut o = serial_step<VAR, true>(A, kk, i, j, mv, bi, c0, rw, tv, gk, sh_r, sh_h, nullptr, sh_a, sh_cnt,
+                                               slots, nullptr SP_NULL, dot);
       if (o.ev && o.erow < nvec * W) hpd[pipe_hidx<W>(o.erow, nvec)] = o.hnew;
       if (o.abort) {
         if (lane == 0) {
