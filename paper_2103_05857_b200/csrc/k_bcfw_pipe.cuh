@@ -620,6 +620,16 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
       const double cj = sup_wins ? csup : c1;
       const unsigned long long kout = sup_wins ? k1 : k2;   // min over rows outside T (old h = new h there)
       const double m_out = kout == ~0ULL ? dinf() : okey_inv(kout);
+      // T = supp U {j} in merged-support lane layout, with C at each row (C_ji from the LMO),
+      // for the gap refresh after the serial part (formed now: it needs no updated state)
+      const bool j_in = __ballot_sync(FULL, lane < c0 && rw == j) != 0u;
+      const int ins = __popc(__ballot_sync(FULL, lane < c0 && rw < j));
+      int src = (j_in || lane < ins) ? lane : lane - 1;
+      if (src < 0) src = 0;
+      int mrow = __shfl_sync(FULL, rw, src);
+      double mC = __shfl_sync(FULL, cw, src);
+      if (!j_in && lane == ins) { mrow = j; mC = cj; }
+      const int M = c0 + (j_in ? 0 : 1);
       // ---- the serial part
       PW_MARK(4);
       const StepOut o = serial_step<VAR, true>(A, kk, i, j, mv, bi, c0, rw, tv, gk, sh_r, sh_h, nullptr, sh_a, sh_cnt,
@@ -644,15 +654,6 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
       if (A.ga_inner) {
         double gnew = o.gfw;
         if (A.ga_post) {
-          // T = supp U {j} in merged-support lane layout, with C at each row (C_ji from the LMO)
-          const bool j_in = __ballot_sync(FULL, lane < c0 && rw == j) != 0u;
-          const int ins = __popc(__ballot_sync(FULL, lane < c0 && rw < j));
-          int src = (j_in || lane < ins) ? lane : lane - 1;
-          if (src < 0) src = 0;
-          int mrow = __shfl_sync(FULL, rw, src);
-          double mC = __shfl_sync(FULL, cw, src);
-          if (!j_in && lane == ins) { mrow = j; mC = cj; }
-          const int M = c0 + (j_in ? 0 : 1);
           // post-update minimum: outside T unchanged (m_out), on T with the updated h
           const unsigned long long kt2 = okey(lane < M ? d_add(mC, sh_h[mrow]) : dinf());
           const unsigned hi = __reduce_min_sync(FULL, (unsigned)(kt2 >> 32));
