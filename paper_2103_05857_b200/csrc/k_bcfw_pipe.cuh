@@ -423,9 +423,12 @@ struct GaPipeLayout {
   __host__ __device__ static size_t fixed() {
     return 256 * 8 + 16 * 4 * 8 + 16 * 4 * 4 + 16 * 4 + GA_LMO * 4;   // slots, key partials, row partials, misc, masks
   }
-  __host__ __device__ static size_t bytes(int m, int n) {
-    return fixed() + 4 * rup16((size_t)m * 8) + rup16((size_t)n * 4) + rup16((size_t)n * 8) +
-           rup16((size_t)(n + 1) * 8);
+  // a_smem / gs_smem: a and the stored gaps in shared memory (else read from / written to
+  // global memory: a is read for the touched rows only, the stored gap once per step
+  // while the scan runs, so larger m, n keep the fast kernel)
+  __host__ __device__ static size_t bytes(int m, int n, bool a_smem = true, bool gs_smem = true) {
+    return fixed() + (a_smem ? 4 : 3) * rup16((size_t)m * 8) + rup16((size_t)n * 4) +
+           (gs_smem ? rup16((size_t)n * 8) : 0) + rup16((size_t)(n + 1) * 8);
   }
 };
 
@@ -437,7 +440,8 @@ __device__ __forceinline__ int warp_argmin_key(unsigned long long& key, int& j) 
   return __ffs(__ballot_sync(FULL, k0 == key && j0 == j)) - 1;
 }
 
-template <typename T, int MAXV, int VAR>
+// GSM: a and the stored gaps in shared memory (else both in global memory)
+template <typename T, int MAXV, int VAR, bool GSM>
 __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, const T* __restrict__ Cg, int64_t ld) {
   if (bcfw_halted(A)) return;
   constexpr int W = Vec<T>::W;
@@ -454,19 +458,22 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
   unsigned* mflag = reinterpret_cast<unsigned*>(p); p += GA_LMO * 4;
   double* sh_h = reinterpret_cast<double*>(p); p += rup16((size_t)m * 8);
   double* sh_r = reinterpret_cast<double*>(p); p += rup16((size_t)m * 8);
-  double* sh_a = reinterpret_cast<double*>(p); p += rup16((size_t)m * 8);
+  double* sh_a = GSM ? reinterpret_cast<double*>(p) : const_cast<double*>(A.a);
+  if (GSM) p += rup16((size_t)m * 8);
   double* hpd = reinterpret_cast<double*>(p); p += rup16((size_t)m * 8);
   const double2* hp = reinterpret_cast<const double2*>(hpd);
   int* sh_cnt = reinterpret_cast<int*>(p); p += rup16((size_t)n * 4);
-  double* Gs = reinterpret_cast<double*>(p); p += rup16((size_t)n * 8);
+  double* Gs = GSM ? reinterpret_cast<double*>(p) : A.G;
+  if (GSM) p += rup16((size_t)n * 8);
   double* fens = reinterpret_cast<double*>(p); p += rup16((size_t)(n + 1) * 8);
   for (int c = tid; c < 256; c += PIPE_THREADS) slots[c] = 0.0;
   for (int k = tid; k < m; k += PIPE_THREADS) {
     const double hk = A.h[k];
-    sh_h[k] = hk; sh_r[k] = A.r[k]; sh_a[k] = A.a[k];
+    sh_h[k] = hk; sh_r[k] = A.r[k];
+    if (GSM) sh_a[k] = A.a[k];
     if (k < nvec * W) hpd[pipe_hidx<W>(k, nvec)] = hk;
   }
-  for (int c = tid; c < n; c += PIPE_THREADS) { sh_cnt[c] = A.cnt[c]; Gs[c] = A.G[c]; }
+  for (int c = tid; c < n; c += PIPE_THREADS) { sh_cnt[c] = A.cnt[c]; if (GSM) Gs[c] = A.G[c]; }
   for (int c = tid; c <= n; c += PIPE_THREADS) fens[c] = A.fen[c];
   for (int c = tid; c < GA_LMO; c += PIPE_THREADS) mflag[c] = 0;
   if (tid == 0) { misc[0] = 0; misc[2] = 0; }
@@ -704,7 +711,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
   }
   __syncthreads();
   for (int k = tid; k < m; k += PIPE_THREADS) { A.h[k] = sh_h[k]; A.r[k] = sh_r[k]; }
-  for (int c = tid; c < n; c += PIPE_THREADS) A.G[c] = Gs[c];
+  if (GSM) for (int c = tid; c < n; c += PIPE_THREADS) A.G[c] = Gs[c];
   for (int c = tid; c <= n; c += PIPE_THREADS) A.fen[c] = fens[c];
   if (steps == 0 && tid == 0) *A.steps_done = 0;
 }

@@ -937,7 +937,7 @@ sro_status bcfw_try_pipe(Solver* s, BcfwArgs& A) {
 
 template <typename T, int MAXV, int VAR>
 sro_status launch_ga_pipe(Solver* s, BcfwArgs& A, size_t smem) {
-  auto kern = k_bcfw_ga_pipe<T, MAXV, VAR>;
+  auto kern = A.ga_smem ? k_bcfw_ga_pipe<T, MAXV, VAR, true> : k_bcfw_ga_pipe<T, MAXV, VAR, false>;
   CUDA_TRY(s, set_dyn_smem((const void*)kern, s->device, (int)smem));
   const int tr = timed_begin(s);
   kern<<<1, PIPE_THREADS, smem, s->stream>>>(A, (const T*)s->C, s->ld);
@@ -959,9 +959,12 @@ sro_status bcfw_try_ga_pipe(Solver* s, BcfwArgs& A) {
   const int nvec = s->m / W;
   const int need = (nvec + GA_LMO - 1) / GA_LMO;
   if (need > 4 || s->m - nvec * W > GA_LMO) return SRO_ERR_DIMENSION;
-  const size_t bytes = GaPipeLayout::bytes(s->m, s->n);
-  if (bytes > 226 * 1024) return SRO_ERR_DIMENSION;
-  A.ga_smem = 1; A.a_smem = 1; A.visit_smem = 0;
+  // a and the stored gaps in shared memory when they fit, else both in global memory
+  const size_t lim = 226 * 1024;
+  const bool gsm = GaPipeLayout::bytes(s->m, s->n, true, true) <= lim;
+  const size_t bytes = GaPipeLayout::bytes(s->m, s->n, gsm, gsm);
+  if (bytes > lim) return SRO_ERR_DIMENSION;
+  A.ga_smem = gsm ? 1 : 0; A.a_smem = A.ga_smem; A.visit_smem = 0;
   if (s->prec == SRO_FP32) {
     if (need <= 1) return launch_ga_pipe<float, 1, VAR>(s, A, bytes);
     if (need <= 2) return launch_ga_pipe<float, 2, VAR>(s, A, bytes);
