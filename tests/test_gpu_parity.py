@@ -354,3 +354,17 @@ def test_max_sms_does_not_change_results():
             out.append((r["trace"], g.plan(), r["gap"]))
             g.close()
         assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1]) and out[0][2] == out[1][2]
+
+
+def test_ga_pipelined_kernel_global_gaps_bitexact():
+    """m = 4096, n = 8192: a and the stored gaps no longer fit in shared memory next to the
+    GA tree, so the pipelined GA kernel keeps them in global memory (GaPipeLayout, GSM =
+    false): every step still bit-exact against the oracle."""
+    d = instance(1, m=4096, n=8192, seed=12)
+    d["C32"] = (((d["X"][:, None, :] - d["Y"][None, :, :]) ** 2).sum(-1)).astype(np.float32)
+    g, o = pair(d, prec="f32")
+    kw = dict(step=ELS, sampling=GA, ga_M=1, ga_inner=1, ga_post_update=1)
+    ro = o.solve(BCFW, 12288, seed=3, trace=True, epsilon=1e-9, **kw)
+    rg = g.solve(sro.SRO_BCFW, 12288, seed=3, trace=True, epsilon=1e-9, **_gpu_opts(kw))
+    assert_same_trace(rg["trace"], ro["trace"])
+    assert_same_state(g, o)
