@@ -16,7 +16,7 @@ __all__ = [
     "build_oracle", "Oracle", "OrOptions", "OrResult", "TRACE_DTYPE",
     "FW", "BCFW", "BCAFW", "BCPFW", "BATCHED", "DEC", "ELS", "U", "P", "GA",
     "COST_DENSE", "COST_SQEUCLID", "COST_EUCLID", "COST_HASH",
-    "chunk_tree_sum", "rng_u64", "uniform53", "permutation", "fenwick_draw", "splitmix64_mix",
+    "chunk_tree_sum", "rng_u64", "uniform53", "permutation", "fenwick_draw", "fenwick_updates", "splitmix64_mix",
     "OracleError",
 ]
 
@@ -98,6 +98,8 @@ def _L():
         _lib.or_uniform53.restype = d
         _lib.or_permutation.argtypes = [u64, i64, i32, vp]
         _lib.or_fenwick_draw.argtypes = [vp, i32, d, ct.POINTER(i32)]
+        _lib.or_get_ga.argtypes = [vp, vp, vp]
+        _lib.or_fenwick_updates.argtypes = [vp, i32, vp, vp, i32, vp, vp, i32, vp]
     return _lib
 
 
@@ -133,6 +135,20 @@ def fenwick_draw(w, u53: float) -> int:
     out = ct.c_int32()
     _L().or_fenwick_draw(_p(w), len(w), u53, ct.byref(out))
     return out.value
+
+
+def fenwick_updates(w0, idx, newval, u53s):
+    """Tree over w0, point updates column idx[u] := newval[u] (GA inner-refresh rule), then
+    (prefix sums as the tree holds them, one draw per u53)."""
+    w0 = np.ascontiguousarray(w0, dtype=np.float64)
+    idx = np.ascontiguousarray(idx, dtype=np.int32)
+    newval = np.ascontiguousarray(newval, dtype=np.float64)
+    u53s = np.ascontiguousarray(u53s, dtype=np.float64)
+    prefix = np.empty(len(w0))
+    draws = np.empty(len(u53s), dtype=np.int32)
+    _L().or_fenwick_updates(_p(w0), len(w0), _p(idx), _p(newval), len(idx), _p(prefix), _p(u53s), len(u53s),
+                            _p(draws))
+    return prefix, draws
 
 
 def make_options(step=ELS, sampling=U, epsilon=1e-6, gap_period=1, ga_M=1, ga_inner=1, ga_post_update=1,
@@ -287,6 +303,15 @@ class Oracle:
         if st:
             raise OracleError(st)
         return j.value, v.value
+
+    def ga_state(self):
+        """(stored gaps G, prefix sums of the GA tree) after a GA solve."""
+        G = np.empty(self.n)
+        pre = np.empty(self.n)
+        st = _L().or_get_ga(self.h, _p(G), _p(pre))
+        if st:
+            raise OracleError(st, "ga_state")
+        return G, pre
 
     def max_cost(self):
         v = ct.c_double()

@@ -16,10 +16,12 @@
  * paper is silent (summation order, tie-breaks, counters, GA constants) the
  * reading R<n> is listed in DESIGN.md §3 and cited here.
  *
- * Parity pins: every function here is pinned by tests/test_oracle_*.py
+ * Parity pins: every function here is pinned by tests/test_oracle_pins*.py
  * against closed forms, brute force, exact-rational replay or values printed
- * in the paper; none is "parity unpinned" except the reading-only choices
- * marked [unpinned: reading] (DESIGN.md §3 lists them).
+ * in the paper; the GA sampler (fen_build / fen_add / fen_draw, the inner and
+ * global refreshes) by an exact-rational replay of Alg. A.4 with the paper's
+ * O(n) cumulative-sum draw (tests/test_oracle_pins_ga.py). No function is
+ * "parity unpinned".
  */
 #include "sro_oracle.h"
 
@@ -863,6 +865,46 @@ int or_fenwick_draw(const double* w, int32_t n, double u53, int32_t* out) {
   fen_build(&tmp);
   *out = fen_draw(&tmp, u53);
   free(tmp.fen);
+  return OR_OK;
+}
+
+/* GA state for pins: stored gaps G (n) and the prefix sums of the tree,
+ * prefix[i] = sum of the weights of columns 0..i as the tree holds them (n). */
+int or_get_ga(or_state* s, double* G, double* prefix) {
+  if (!s->G || !s->fen) return OR_ERR_STATE;
+  for (int32_t i = 0; i < s->n; i++) {
+    if (G) G[i] = s->G[i];
+    if (prefix) {
+      double acc = 0.0;
+      for (int32_t p = i + 1; p > 0; p -= p & -p) acc = acc + s->fen[p];
+      prefix[i] = acc;
+    }
+  }
+  return OR_OK;
+}
+
+/* Fenwick point updates in isolation (pin of fen_add): build over w0, then for
+ * u = 0..nupd-1 set column idx[u] to newval[u] exactly as the GA inner refresh does
+ * (delta = max(new,0) - max(old,0) added along the update path); then prefix[i] (n)
+ * and one draw per u53s entry (ndraw) from the updated tree. */
+int or_fenwick_updates(const double* w0, int32_t n, const int32_t* idx, const double* newval, int32_t nupd,
+                       double* prefix, const double* u53s, int32_t ndraw, int32_t* draws) {
+  or_state tmp;
+  memset(&tmp, 0, sizeof(tmp));
+  tmp.n = n;
+  tmp.G = (double*)malloc(sizeof(double) * (size_t)n);
+  tmp.fen = (double*)malloc(sizeof(double) * ((size_t)n + 1));
+  memcpy(tmp.G, w0, sizeof(double) * (size_t)n);
+  fen_build(&tmp);
+  for (int32_t u = 0; u < nupd; u++) {
+    int32_t i = idx[u];
+    double delta = wpos(newval[u]) - wpos(tmp.G[i]);
+    tmp.G[i] = newval[u];
+    fen_add(&tmp, i, delta);
+  }
+  or_get_ga(&tmp, NULL, prefix);
+  for (int32_t d = 0; d < ndraw; d++) draws[d] = fen_draw(&tmp, u53s[d]);
+  free(tmp.G); free(tmp.fen);
   return OR_OK;
 }
 

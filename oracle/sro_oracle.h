@@ -98,6 +98,10 @@ uint64_t or_rng_u64(uint64_t seed, uint32_t stream, uint64_t t);
 double or_uniform53(uint64_t x);
 int or_permutation(uint64_t seed, int64_t epoch, int32_t n, int32_t* perm);
 int or_fenwick_draw(const double* w, int32_t n, double u53, int32_t* out);
+/* GA state (stored gaps, tree prefix sums) and Fenwick point updates in isolation, for pins */
+int or_get_ga(or_state* s, double* G, double* prefix);
+int or_fenwick_updates(const double* w0, int32_t n, const int32_t* idx, const double* newval, int32_t nupd,
+                       double* prefix, const double* u53s, int32_t ndraw, int32_t* draws);
 
 #ifdef __cplusplus
 }

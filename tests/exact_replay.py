@@ -133,3 +133,79 @@ class ExactState:
         self.set_col(i, [t[k] + gamma * d[k] for k in range(self.m)])
         self.k += 1
         return j, v, gamma, kind
+
+
+# --------------------------------------------------------------------------- Alg. A.4 (BCFW-GA)
+M64 = (1 << 64) - 1
+GOLDEN = 0x9E3779B97F4A7C15
+
+
+def _mix(z):
+    """SplitMix64 finaliser (public-domain constants), plain Python integers."""
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+    return z ^ (z >> 31)
+
+
+def u53_exact(seed, stream, t):
+    """R21's counter-based draw as an exact rational in [0, 1): value t of stream s is
+    mix(mix(seed ^ 0x5851F42D4C957F2D (s+1)) + (t+1) golden), top 53 bits / 2^53."""
+    key = _mix((seed ^ ((0x5851F42D4C957F2D * (stream + 1)) & M64)) & M64)
+    x = _mix((key + (t + 1) * GOLDEN) & M64)
+    return Fr(x >> 11, 1 << 53)
+
+
+def column_gap(ex, i):
+    """g_i(T) = <t_i - s_i, grad_i f> = sum_k t_ki grad_ki - b_i min_k grad_ki (Eq. 11)."""
+    j, g = ex.lmo(i)
+    return sum(ex.T[k][i] * g[k] for k in range(ex.m)) - ex.b[i] * g[j]
+
+
+def ga_replay(ex, variant, steps, seed, M, inner, post, cinit, rule="els"):
+    """Alg. A.4 exactly as the paper states it, in exact arithmetic:
+      line 1   stored gaps G_i = C, "a large constant" (R14: cinit = max C + 2/lambda)
+      line 2   draw i with probability max(G_i, 0) / sum_l max(G_l, 0) through the O(n)
+               cumulative sum of P:407: the smallest i with w_1 + ... + w_i > u W, where
+               u is draw k of stream 1 (R21)
+      line 3-5 the block step on column i (Alg. 1 with Eq. 10 or the decay rule; away /
+               pairwise with Eq. 14)
+      line 6   G_i = g_i(T^{k+1}) after the update ("after update of t_i"; R15),
+               or g_i(T^k) with post = False
+      global   every M n steps all G_i = g_i(T) (R16: after step k when
+               (k+1) mod (M n) == 0). GAS is inner = False with M = 1.
+    Returns one record per step, stopping before a step whose draw lies within 1e-9 W of a
+    cumulative boundary or whose LMO has an exact tie: there fp64 rounding, not the
+    algorithm, decides."""
+    n = ex.n
+    G = [Fr(cinit)] * n
+    out = []
+    for k in range(steps):
+        w = [x if x > 0 else Fr(0) for x in G]
+        W = sum(w)
+        u = u53_exact(seed, 1, k)
+        if W == 0:
+            i = int(u * n)                                      # all-zero weights: uniform (R17)
+        else:
+            uw, cum, i, margin = u * W, Fr(0), None, None
+            for q in range(n):
+                cum += w[q]
+                d = abs(float((cum - uw) / W))
+                margin = d if margin is None else min(margin, d)
+                if i is None and cum > uw:
+                    i = q
+            if margin < 1e-9:
+                break
+        if ex.lmo_tied(i):
+            break
+        gpre = column_gap(ex, i)
+        if variant == "plain":
+            j, gamma = ex.bcfw_step(i, rule)
+            v, kind = -1, "fw"
+        else:
+            j, v, gamma, kind = ex.away_or_pair_step(i, pairwise=(variant == "pair"))
+        if inner:
+            G[i] = column_gap(ex, i) if post else gpre
+        if (k + 1) % (M * n) == 0:
+            G = [column_gap(ex, q) for q in range(n)]
+        out.append(dict(k=k, i=i, j=j, v=v, gamma=gamma, kind=kind, G=list(G)))
+    return out
