@@ -122,7 +122,7 @@ class StepRunner:
     instead of queueing. The cost matrix is ONE device copy borrowed by every handle (column-major,
     ld = m), so the L2 holds it once."""
 
-    def __init__(self, d, dev, Cd, concurrent=True):
+    def __init__(self, d, dev, Cd, concurrent=True, ready=None):
         import torch
         import paper_2103_05857_b200 as sro
         self.torch = torch
@@ -132,6 +132,10 @@ class StepRunner:
         # behind the FW / batched solves' GPU-wide kernels
         self.streams = [torch.cuda.Stream(dev, priority=-1 if variant in (1, 2, 3) else 0)
                         for _, variant, _, _ in PLAN]
+        # the borrowed C must be complete before sro_create validates it on each handle's stream
+        ready = ready if ready is not None else torch.cuda.current_stream(dev).record_event()
+        for st in self.streams:
+            st.wait_event(ready)
         self.solvers = [sro.Solver(d["a"], d["b"], 1.0, C=Cd, prec="f32", device=dev.index, stream=st.cuda_stream,
                                    ld=M) for st in self.streams]
 

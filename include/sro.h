@@ -66,7 +66,9 @@ typedef struct {
   const void* y;        /* SQEUCLID/EUCLID: target colours, y[3i + d] */
   uint64_t hash_seed;   /* HASH_UNIFORM */
   int32_t data_on_device; /* 0: host pointers, copied at sro_create.
-                             1: device pointers, BORROWED (must outlive the handle);
+                             1: device pointers, BORROWED (must outlive the handle, and their
+                             contents must be complete before sro_create: it validates them
+                             on the handle's stream, which does not wait on other streams);
                              DENSE requires 16-byte aligned data and ld*elem % 16 == 0 */
 } sro_cost;
 
@@ -162,7 +164,9 @@ typedef struct {
 } sro_stats;
 
 /* Create a solver. a: host fp64[m] (source marginal), b: host fp64[n] (target
- * marginal, all n columns even when sharded), copied. cost as described above;
+ * marginal, all n columns even when sharded), copied. Both >= 0 and summing to 1 within
+ * 1e-12; a zero-mass column (b_i = 0, Eq. 8 allows it) stays the zero vector, and a BCFW-family
+ * step on it is a no-op (R32). cost as described above;
  * for a sharded handle it covers the columns this process holds ("held
  * columns", ascending global index: all n when nranks == 1, the shard's n/G
  * when nranks == G): DENSE data is m x n_held column-major, colour y is
@@ -224,6 +228,18 @@ sro_status sro_barycentric(sro_handle h, const double* x, const double* y, doubl
  * (the plan's value in metric vi). Unsharded handles only. */
 sro_status sro_metrics(sro_handle h, double* e_c, double* sparsity, double* lin);
 
+/* Metrics (v) and (vi) of P:419-421 against a reference plan T* (the paper's T*_LP, the
+ * solution of the unregularised, unrelaxed OT linear program, supplied by the caller):
+ * *e_m = ||T - T*||_F / ||T*||_F and *e_v = |<T, C> - <T*, C>| / |<T*, C>|. Each squared norm
+ * and <T*, C> is a 256-chunk pairwise sum over the n columns (R19) of per-column sums over the
+ * rows ascending; <T, C> as in sro_metrics; each norm the correctly rounded square root.
+ * T*: host COO (rows, cols, vals; nnz entries) sorted by column, then strictly by row, within
+ * [0, m) x [0, n), finite values (copied). Unsharded handles only. A zero ||T*|| or <T*, C>
+ * gives inf / NaN as the division does. Errors: INVALID_ARG (unsorted, out of range, non-finite),
+ * OOM, CUDA. */
+sro_status sro_lp_metrics(sro_handle h, const int32_t* rows, const int32_t* cols, const double* vals, int64_t nnz,
+                          double* e_m, double* e_v);
+
 /* Global indices (ascending) of the columns this handle holds: cols host
  * int32[n_held] or NULL; *n_held receives the count (n when unsharded). */
 sro_status sro_held_columns(sro_handle h, int32_t* cols, int32_t* n_held);
@@ -257,7 +273,14 @@ sro_status sro_kmeans(const uint8_t* pixels, int64_t npix, int32_t k, const int3
 sro_status sro_recolour(const int32_t* labels, int64_t npix, const double* xhat, int32_t k, void* cuda_stream,
                         uint8_t* out_pixels);
 
-/* Text of the last sro_kmeans / sro_recolour failure on this thread ("" if none). */
+/* The colour-transfer features of a quantisation (R29): colours x_c =
+ * centroid_c / 255 (k x 3, in [0, 1]^3) and the histogram a_c = count_c / N, N = sum of the
+ * counts (k). centroids: host fp64 k x 3 (sro_kmeans output); counts: host int64[k] (>= 0,
+ * not all zero); colours, weights: host outputs. Errors: INVALID_ARG. */
+sro_status sro_kmeans_features(const double* centroids, const int64_t* counts, int32_t k, double* colours,
+                               double* weights);
+
+/* Text of the last sro_kmeans / sro_recolour / sro_kmeans_features failure on this thread ("" if none). */
 const char* sro_kmeans_error(void);
 
 /* Copy the accounting into *out; reset it to zero if reset != 0. */

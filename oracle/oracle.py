@@ -78,6 +78,7 @@ def _L():
         _lib.or_objective.argtypes = [vp, ct.POINTER(d)]
         _lib.or_barycentric.argtypes = [vp, vp, vp, vp]
         _lib.or_metrics.argtypes = [vp, ct.POINTER(d), ct.POINTER(d), ct.POINTER(d)]
+        _lib.or_lp_metrics.argtypes = [vp, vp, vp, vp, i64, ct.POINTER(d), ct.POINTER(d)]
         _lib.or_get_plan_dense.argtypes = [vp, vp]
         _lib.or_get_plan_coo.argtypes = [vp, vp, vp, vp, i64, ct.POINTER(i64)]
         _lib.or_get_r.argtypes = [vp, vp]
@@ -260,6 +261,17 @@ class Oracle:
         if st:
             raise OracleError(st, "metrics")
         return e.value, sp.value, lin.value
+
+    def lp_metrics(self, rows, cols, vals):
+        """(e_m, e_v) — metrics (v) and (vi) against T* in COO sorted by (column, row)."""
+        rows = np.ascontiguousarray(rows, dtype=np.int32)
+        cols = np.ascontiguousarray(cols, dtype=np.int32)
+        vals = np.ascontiguousarray(vals, dtype=np.float64)
+        em, ev = ct.c_double(), ct.c_double()
+        st = _L().or_lp_metrics(self.h, _p(rows), _p(cols), _p(vals), len(vals), ct.byref(em), ct.byref(ev))
+        if st:
+            raise OracleError(st, "lp_metrics")
+        return em.value, ev.value
 
     def plan(self):
         T = np.empty(self.m * self.n)

@@ -240,7 +240,9 @@ void or_destroy(or_state* s) { free_state(s); }
 /* T^(0) = (b_1 e_1, ..., b_n e_1): all mass on row 0 (R3). */
 int or_reset(or_state* s) {
   for (int32_t i = 0; i < s->n; i++) {
-    s->cnt[i] = 1;
+    /* t_i = b_i e_1; a zero-mass column (b_i = 0, Eq. 8 allows it) is the zero vector,
+     * whose support is empty (exact zeros are not stored, R13) */
+    s->cnt[i] = s->b[i] != 0.0 ? 1 : 0;
     s->rows[(int64_t)i * s->cap] = 0;
     s->vals[(int64_t)i * s->cap] = s->b[i];
   }
@@ -285,8 +287,8 @@ or_state* or_create(int32_t m, int32_t n, double lambda, const double* a, const 
   /* validation: a, b >= 0 summing to 1 within 1e-12; C finite, >= 0 */
   double sa = 0.0, sb = 0.0;
   for (int32_t k = 0; k < m; k++) { if (!(a[k] >= 0.0) || !isfinite(a[k])) { free_state(s); *status = 4; return NULL; } sa = sa + a[k]; }
-  /* b_i > 0: every block b_i Delta_m is a proper simplex (Eq. 8) */
-  for (int32_t i = 0; i < n; i++) { if (!(b[i] > 0.0) || !isfinite(b[i])) { free_state(s); *status = 4; return NULL; } sb = sb + b[i]; }
+  /* b_i >= 0: a zero-mass block b_i Delta_m = {0} is allowed (Eq. 8; R32) */
+  for (int32_t i = 0; i < n; i++) { if (!(b[i] >= 0.0) || !isfinite(b[i])) { free_state(s); *status = 4; return NULL; } sb = sb + b[i]; }
   if (fabs(sa - 1.0) > 1e-12 || fabs(sb - 1.0) > 1e-12) { free_state(s); *status = 4; return NULL; }
   if (cost_kind == OR_COST_DENSE) {
     for (int64_t q = 0; q < (int64_t)m * n; q++)
@@ -392,6 +394,46 @@ int or_metrics(or_state* s, double* e_c, double* sparsity, double* lin) {
   }
   *lin = or_chunk_tree_sum(sq, s->n, 256);
   free(row); free(sq);
+  return OR_OK;
+}
+
+/* Metrics (v) and (vi) against a reference plan T* (T*_LP in the paper), given as
+ * COO sorted by column then row: e_m = ||T - T*||_F / ||T*||_F, e_v = |<T,C> - <T*,C>| / |<T*,C>|.
+ * Per column i, over all rows k ascending: sum (T_ki - T*_ki)^2, sum T*_ki^2, sum T*_ki C_ki;
+ * each then a 256-chunk sum over the columns (R19); <T, C> as in or_metrics. */
+int or_lp_metrics(or_state* s, const int32_t* rows, const int32_t* cols, const double* vals, int64_t nnz,
+                  double* e_m, double* e_v) {
+  const int32_t m = s->m, n = s->n;
+  for (int64_t q = 0; q < nnz; q++)
+    if (rows[q] < 0 || rows[q] >= m || cols[q] < 0 || cols[q] >= n || !isfinite(vals[q]) ||
+        (q > 0 && (cols[q] < cols[q - 1] || (cols[q] == cols[q - 1] && rows[q] <= rows[q - 1]))))
+      return OR_ERR_ARG;
+  double* Ts = (double*)calloc((size_t)m * n, sizeof(double));   /* T* dense, column-major */
+  double* Tc = (double*)malloc(sizeof(double) * (size_t)m);
+  double* dd = (double*)malloc(sizeof(double) * (size_t)n);
+  double* ss = (double*)malloc(sizeof(double) * (size_t)n);
+  double* cc = (double*)malloc(sizeof(double) * (size_t)n);
+  if (!Ts || !Tc || !dd || !ss || !cc) { free(Ts); free(Tc); free(dd); free(ss); free(cc); return OR_ERR_ARG; }
+  for (int64_t q = 0; q < nnz; q++) Ts[(int64_t)cols[q] * m + rows[q]] = vals[q];
+  for (int32_t i = 0; i < n; i++) {
+    for (int32_t k = 0; k < m; k++) Tc[k] = 0.0;
+    for (int32_t p = 0; p < s->cnt[i]; p++) Tc[s->rows[(int64_t)i * s->cap + p]] = s->vals[(int64_t)i * s->cap + p];
+    double sd = 0.0, s2 = 0.0, sc = 0.0;
+    for (int32_t k = 0; k < m; k++) {
+      double ts = Ts[(int64_t)i * m + k];
+      double d = Tc[k] - ts;
+      sd = sd + d * d;
+      s2 = s2 + ts * ts;
+      sc = sc + ts * cost(s, k, i);
+    }
+    dd[i] = sd; ss[i] = s2; cc[i] = sc;
+  }
+  double D = or_chunk_tree_sum(dd, n, 256), S2 = or_chunk_tree_sum(ss, n, 256), SC = or_chunk_tree_sum(cc, n, 256);
+  double e_c, sp, lin;
+  or_metrics(s, &e_c, &sp, &lin);
+  *e_m = sqrt(D) / sqrt(S2);
+  *e_v = fabs(lin - SC) / fabs(SC);
+  free(Ts); free(Tc); free(dd); free(ss); free(cc);
   return OR_OK;
 }
 
@@ -709,8 +751,14 @@ static int away_step(or_state* s, int32_t i, or_trace_rec* tr, int* dir_out, dou
   }
   double bi = s->b[i];
   double gfw = dot - bi * minval;          /* <-grad, d_FW>  = g_i     */
-  double gaw = bi * gv - dot;              /* <-grad, d_Away> = g^A_i   */
   *g_pre = gfw;
+  if (c0 == 0) {
+    /* zero-mass column (b_i = 0, R32): t_i = s_i = 0, every direction is zero, no-op */
+    *dir_out = 3;
+    if (tr) { tr->i = i; tr->j = j; tr->v = -1; tr->dir = 3; tr->gamma = 0.0; tr->num = 0.0; tr->den = 0.0; tr->minval = minval; }
+    return OR_OK;
+  }
+  double gaw = bi * gv - dot;              /* <-grad, d_Away> = g^A_i   */
   int use_fw = (c0 == 1) || (gfw >= gaw); /* R12: singleton forces FW */
   int32_t cap1 = s->cap + 1;
   int32_t* mr = (int32_t*)malloc(sizeof(int32_t) * cap1);
@@ -777,8 +825,8 @@ static int pairwise_step(or_state* s, int32_t i, or_trace_rec* tr, int* dir_out,
   double bi = s->b[i];
   *g_pre = dot - bi * minval;
   double gamma = 0.0, num = 0.0, den = 0.0;
-  if (v == j) {
-    *dir_out = 3;                          /* no-op step */
+  if (v == j || c0 == 0) {
+    *dir_out = 3;                          /* no-op step (c0 == 0: zero-mass column, R32) */
   } else {
     double dv = gv - minval;               /* grad_v - grad_j >= 0 */
     num = s->lambda * dv;

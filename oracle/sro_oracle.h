@@ -82,6 +82,11 @@ int or_barycentric(or_state* s, const double* X, const double* Y, double* xhat);
  * square root of a 256-chunk sum of squares); sparsity = 1 - nnz(T) / (m n);
  * lin = 256-chunk sum over columns of <t_i, c_i>. */
 int or_metrics(or_state* s, double* e_c, double* sparsity, double* lin);
+/* Metrics (v) e_m = ||T - T*||_F / ||T*||_F and (vi) e_v = |<T,C> - <T*,C>| / |<T*,C>|
+ * against T* given as COO sorted by column then row; sums per column over all rows ascending,
+ * then 256-chunk sums over columns. */
+int or_lp_metrics(or_state* s, const int32_t* rows, const int32_t* cols, const double* vals, int64_t nnz,
+                  double* e_m, double* e_v);
 int or_get_plan_dense(or_state* s, double* T);     /* m*n column-major */
 int or_get_plan_coo(or_state* s, int32_t* rows, int32_t* cols, double* vals, int64_t cap, int64_t* nnz);
 int or_get_r(or_state* s, double* r);

@@ -572,6 +572,10 @@ __device__ __forceinline__ StepOut serial_step(const BcfwArgs& A, long long kk, 
     tnew = d_mul(omg, mt);
     if (mrow == j) tnew = d_add(tnew, gb);
     SP_MARK(11);
+  } else if (VAR != VAR_PLAIN && c0 == 0) {
+    // zero-mass column (b_i = 0, R32): t_i = s_i = v_i = 0, every direction is zero: no-op
+    o.dir = 3;
+    o.vrow = -1;
   } else if (VAR == VAR_AWAY) {
     const double gaw = d_sub(d_mul(bi, gv), dot);
     const bool use_fw = (c0 == 1) || (o.gfw >= gaw);
@@ -623,7 +627,7 @@ __device__ __forceinline__ StepOut serial_step(const BcfwArgs& A, long long kk, 
     }
   }
   // apply: new column (exact zeros dropped), r += (t' - t), h refresh
-  o.noop = (VAR == VAR_PAIR && o.dir == 3);
+  o.noop = (VAR != VAR_PLAIN && o.dir == 3);
   o.merged = use_merged;
   const int E = use_merged ? M : c0;
   const int erow = use_merged ? mrow : rw;

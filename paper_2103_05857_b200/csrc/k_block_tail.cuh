@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(1024, 1) k_block_tail_sm(BlockArgs A, TailMerg
     } else {
       c = A.cnt[i];
       bi = A.b[i];
-      crow[0] = A.srow[(int64_t)i * cap];   // every support has an entry (b_i > 0)
+      crow[0] = A.srow[(int64_t)i * cap];   // read even when c == 0 (b_i = 0): unused then
       cval[0] = A.sval[(int64_t)i * cap];
       if (M.nslabs <= 1) { j = A.j[t]; gcol = A.g[t]; }
 #pragma unroll

@@ -76,4 +76,40 @@ __global__ void k_plan_sq_cols(int n, int cap, const int* __restrict__ cnt, cons
   }
 }
 
+// Metrics (v) and (vi) against a reference plan T* (P:419-421), one thread per column i: the
+// plan's support and T*'s column (both rows ascending) merged, and over the rows ascending
+// dd_i = sum_k (T_ki - T*_ki)^2, ss_i = sum_k T*_ki^2, cc_i = sum_k T*_ki C_ki (a row in
+// neither support adds an exact +0, so this is the sum over all m rows).
+template <class Src>
+__global__ void k_lp_cols(Src src, int n, int cap, const int* __restrict__ cnt, const int* __restrict__ srow,
+                          const double* __restrict__ sval, const int64_t* __restrict__ colptr,
+                          const int* __restrict__ lrow, const double* __restrict__ lval, double* dd, double* ss,
+                          double* cc) {
+  for (int i = gtid(); i < n; i += gstride()) {
+    const int c = cnt[i];
+    int e = 0;
+    int64_t q = colptr[i];
+    const int64_t qe = colptr[i + 1];
+    double sd = 0.0, s2 = 0.0, sc = 0.0;
+    while (e < c || q < qe) {
+      const int re = e < c ? srow[(int64_t)i * cap + e] : 0x7fffffff;
+      const int rq = q < qe ? lrow[q] : 0x7fffffff;
+      const int k = re < rq ? re : rq;
+      const double t = re == k ? sval[(int64_t)i * cap + e] : 0.0;
+      const double ts = rq == k ? lval[q] : 0.0;
+      const double d = d_sub(t, ts);
+      sd = d_add(sd, d_mul(d, d));
+      if (rq == k) {
+        s2 = d_add(s2, d_mul(ts, ts));
+        sc = d_add(sc, d_mul(ts, src.cost(k, i)));
+      }
+      if (re == k) e++;
+      if (rq == k) q++;
+    }
+    dd[i] = sd;
+    ss[i] = s2;
+    cc[i] = sc;
+  }
+}
+
 }  // namespace sro

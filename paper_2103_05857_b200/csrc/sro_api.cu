@@ -376,7 +376,7 @@ __global__ void k_init_plan(const double* __restrict__ b, const double* __restri
   // r_0 = sum_i b_i over all n columns, left to right (every shard alike).
   const int tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
   for (int i = tid; i < n; i += stride) {
-    cnt[i] = 1;
+    cnt[i] = b[i] != 0.0 ? 1 : 0;   // a zero-mass column is the zero vector: empty support (R32)
     srow[(int64_t)i * cap] = 0;
     sval[(int64_t)i * cap] = b[i];
   }
@@ -1608,10 +1608,10 @@ sro_status sro_create(const double* a, const double* b, const sro_cost* cost, co
   const int cap = p->slab_cap == 0 ? 31 : p->slab_cap;
   if (cap < 1 || cap > 31) { g_create_err = "slab_cap must be in [1, 31]"; return SRO_ERR_INVALID_ARG; }
   if (cost->kind < 0 || cost->kind > 3 || cost->prec < 0 || cost->prec > 1) { g_create_err = "bad cost kind/precision"; return SRO_ERR_INVALID_ARG; }
-  // marginals: finite, a >= 0, b > 0, each summing to 1 within 1e-12
+  // marginals (Eq. 8): finite, a >= 0, b >= 0 (zero-mass columns: R32), each summing to 1 within 1e-12
   double sa = 0.0, sb = 0.0;
   for (int k = 0; k < p->m; k++) { if (!(a[k] >= 0.0) || !std::isfinite(a[k])) { g_create_err = "a must be finite and >= 0"; return SRO_ERR_MARGINALS; } sa += a[k]; }
-  for (int i = 0; i < p->n; i++) { if (!(b[i] > 0.0) || !std::isfinite(b[i])) { g_create_err = "b must be finite and > 0"; return SRO_ERR_MARGINALS; } sb += b[i]; }
+  for (int i = 0; i < p->n; i++) { if (!(b[i] >= 0.0) || !std::isfinite(b[i])) { g_create_err = "b must be finite and >= 0"; return SRO_ERR_MARGINALS; } sb += b[i]; }
   if (std::fabs(sa - 1.0) > 1e-12 || std::fabs(sb - 1.0) > 1e-12) { g_create_err = "marginals must sum to 1 within 1e-12"; return SRO_ERR_MARGINALS; }
   // sharding
   const int G = p->shards <= 1 ? 1 : p->shards;
@@ -1864,12 +1864,17 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
   } else {
     // visit order for the whole call (U / P / explicit); GA draws on the device
     if (!ga) {
+      if (o->visit)   // explicit visits index columns / blocks on the device: range-checked here
+        for (int64_t q = 0; q < iters; q++)
+          if (o->visit[q] < 0 || o->visit[q] >= nprime) { s->err = "visit entries must lie in [0, n') (n' = n, or n / block_size)"; return SRO_ERR_INVALID_ARG; }
       make_visits(o->sampling, seed, s->k, iters, (int)nprime, o->visit, 0, hv);
       st = ensure_visit(s, iters > 0 ? iters : 1);
       if (st) return st;
       if (iters > 0) CUDA_TRY(s, cudaMemcpyAsync(s->visit, hv.data(), sizeof(int) * iters, cudaMemcpyHostToDevice, s->stream));
     } else if (variant == SRO_BATCHED) {
-      st = ensure_visit(s, iters > 0 ? iters : 1);   // the device draws write the blocks here
+      // the device draws write the blocks here; the refresh after a call's last step draws the
+      // next block into slot iters (cursor mode), hence iters + 1 slots
+      st = ensure_visit(s, iters + 1);
       if (st) return st;
     }
     const long long gaMn = ga ? (long long)o->ga_M * nprime : 0;   // global refresh period (R16, R31)
@@ -2178,6 +2183,66 @@ sro_status sro_metrics(sro_handle h, double* e_c, double* sparsity, double* lin)
   return SRO_OK;
 }
 
+sro_status sro_lp_metrics(sro_handle h, const int32_t* rows, const int32_t* cols, const double* vals, int64_t nnz,
+                          double* e_m, double* e_v) {
+  if (!h || !e_m || !e_v || nnz < 0 || (nnz > 0 && (!rows || !cols || !vals))) return SRO_ERR_INVALID_ARG;
+  Solver* s = static_cast<Solver*>(h);
+  cudaSetDevice(s->device);
+  if (s->G > 1) { s->err = "sro_lp_metrics: unsharded handles only"; return SRO_ERR_INVALID_ARG; }
+  const int m = s->m, n = s->n;
+  // T* in COO sorted by (column, row), entries within range: column pointers by counting
+  std::vector<int64_t> colptr((size_t)n + 1, 0);
+  for (int64_t q = 0; q < nnz; q++) {
+    if (rows[q] < 0 || rows[q] >= m || cols[q] < 0 || cols[q] >= n || !std::isfinite(vals[q]) ||
+        (q > 0 && (cols[q] < cols[q - 1] || (cols[q] == cols[q - 1] && rows[q] <= rows[q - 1])))) {
+      s->err = "sro_lp_metrics: T* must be COO sorted by column then row (strictly), in range, finite";
+      return SRO_ERR_INVALID_ARG;
+    }
+    colptr[(size_t)cols[q] + 1]++;
+  }
+  for (int i = 0; i < n; i++) colptr[(size_t)i + 1] += colptr[i];
+  int64_t* dptr = nullptr;
+  int* drow = nullptr;
+  double *dval = nullptr, *buf = nullptr;
+  sro_status st = SRO_OK;
+  double D = 0.0, S2 = 0.0, SC = 0.0, lin = 0.0;
+  do {
+    if (dalloc(&dptr, (size_t)n + 1) != cudaSuccess || dalloc(&drow, (size_t)nnz) != cudaSuccess ||
+        dalloc(&dval, (size_t)nnz) != cudaSuccess || dalloc(&buf, 3 * (size_t)n) != cudaSuccess) {
+      s->err = "sro_lp_metrics: device allocation failed"; st = SRO_ERR_OOM; break;
+    }
+    if (cudaMemcpyAsync(dptr, colptr.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s->stream) != cudaSuccess ||
+        (nnz > 0 && (cudaMemcpyAsync(drow, rows, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s->stream) != cudaSuccess ||
+                     cudaMemcpyAsync(dval, vals, sizeof(double) * nnz, cudaMemcpyHostToDevice, s->stream) != cudaSuccess))) {
+      s->err = "sro_lp_metrics: upload failed"; st = SRO_ERR_CUDA; break;
+    }
+    double *dd = buf, *ss = buf + n, *cc = buf + 2 * (size_t)n;
+    st = with_sweep_src(s, [&](auto src) -> sro_status {
+      k_lp_cols<<<(n + 255) / 256, 256, 0, s->stream>>>(src, n, s->cap, s->cnt, s->srow, s->sval, dptr, drow, dval, dd, ss, cc);
+      CUDA_TRY(s, cudaGetLastError());
+      return SRO_OK;
+    });
+    if (st) break;
+    k_psum256<<<1, 256, 0, s->stream>>>(dd, n, s->scal + 1, nullptr, nullptr, nullptr);
+    k_psum256<<<1, 256, 0, s->stream>>>(ss, n, s->scal + 2, nullptr, nullptr, nullptr);
+    k_psum256<<<1, 256, 0, s->stream>>>(cc, n, s->scal + 3, nullptr, nullptr, nullptr);
+    s->stats.kernel_launches += 4;
+    CUDA_TRY(s, rb(s, &D, s->scal + 1, sizeof(double)));
+    CUDA_TRY(s, rb(s, &S2, s->scal + 2, sizeof(double)));
+    CUDA_TRY(s, rb(s, &SC, s->scal + 3, sizeof(double)));
+    double f = 0.0;
+    st = objective_dev(s, &f);   // psum256_i <t_i, c_i> in scal[4] (synchronises; the readbacks above land)
+    if (st) break;
+    CUDA_TRY(s, rb(s, &lin, s->scal + 4, sizeof(double)));
+    CUDA_TRY(s, stream_wait(s));
+  } while (0);
+  for (void* q : {(void*)dptr, (void*)drow, (void*)dval, (void*)buf}) if (q) cudaFree(q);
+  if (st) return st;
+  *e_m = std::sqrt(D) / std::sqrt(S2);
+  *e_v = std::fabs(lin - SC) / std::fabs(SC);
+  return SRO_OK;
+}
+
 sro_status sro_held_columns(sro_handle h, int32_t* cols, int32_t* n_held) {
   if (!h || !n_held) return SRO_ERR_INVALID_ARG;
   auto order = held_order(static_cast<Solver*>(h));
@@ -2377,6 +2442,25 @@ done:
   for (void* q : {(void*)dl, (void*)dx, (void*)dout}) if (q) cudaFreeAsync(q, stream);
   cudaStreamSynchronize(stream);
   return st;
+}
+
+sro_status sro_kmeans_features(const double* centroids, const int64_t* counts, int32_t k, double* colours,
+                               double* weights) {
+  g_km_err.clear();
+  if (!centroids || !counts || !colours || !weights || k < 1) { g_km_err = "bad argument"; return SRO_ERR_INVALID_ARG; }
+  int64_t total = 0;
+  for (int c = 0; c < k; c++) {
+    if (counts[c] < 0) { g_km_err = "negative count"; return SRO_ERR_INVALID_ARG; }
+    total += counts[c];
+  }
+  if (total == 0) { g_km_err = "no pixels"; return SRO_ERR_INVALID_ARG; }
+  // R29: colour x = centroid / 255 (one correctly rounded division per channel), histogram
+  // a = count / N with N the total pixel count
+  for (int c = 0; c < k; c++) {
+    for (int d = 0; d < 3; d++) colours[3 * c + d] = centroids[3 * c + d] / 255.0;
+    weights[c] = (double)counts[c] / (double)total;
+  }
+  return SRO_OK;
 }
 
 }  // extern "C"

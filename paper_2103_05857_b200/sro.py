@@ -13,7 +13,7 @@ import numpy as np
 __all__ = [
     "load_library", "Solver", "SroError", "SRO_FW", "SRO_BCFW", "SRO_BCAFW", "SRO_BCPFW", "SRO_BATCHED",
     "STEP_DEC", "STEP_ELS", "SAMPLE_U", "SAMPLE_P", "SAMPLE_GA", "TRACE_DTYPE", "EXPORTED_SYMBOLS",
-    "nccl_unique_id", "kmeans_quantize", "recolour", "colour_transfer",
+    "nccl_unique_id", "kmeans_quantize", "kmeans_features", "recolour", "colour_transfer",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -28,7 +28,7 @@ OK, NOT_CONVERGED = 0, 1
 EXPORTED_SYMBOLS = ("sro_create", "sro_solve", "sro_gap", "sro_objective", "sro_get_plan", "sro_get_rowsums",
                     "sro_reset", "sro_destroy", "sro_last_error", "sro_version", "sro_get_stats", "sro_set_timing",
                     "sro_held_columns", "sro_nccl_unique_id", "sro_barycentric", "sro_metrics",
-                    "sro_kmeans", "sro_recolour", "sro_kmeans_error")
+                    "sro_kmeans", "sro_recolour", "sro_kmeans_error", "sro_lp_metrics", "sro_kmeans_features")
 
 _STATUS = {0: "OK", 1: "NOT_CONVERGED", 2: "ERR_INVALID_ARG", 3: "ERR_DIMENSION", 4: "ERR_MARGINALS",
            5: "ERR_NONFINITE", 6: "ERR_CAPACITY", 7: "ERR_CUDA", 8: "ERR_NCCL", 9: "ERR_OOM", 10: "ERR_STATE"}
@@ -128,6 +128,10 @@ def load_library():
         L.sro_kmeans.restype = ct.c_int
         L.sro_recolour.argtypes = [vp, i64, vp, i32, vp, vp]
         L.sro_recolour.restype = ct.c_int
+        L.sro_lp_metrics.argtypes = [vp, vp, vp, vp, i64, ct.POINTER(d), ct.POINTER(d)]
+        L.sro_lp_metrics.restype = ct.c_int
+        L.sro_kmeans_features.argtypes = [vp, vp, i32, vp, vp]
+        L.sro_kmeans_features.restype = ct.c_int
         L.sro_kmeans_error.argtypes = []
         L.sro_kmeans_error.restype = ct.c_char_p
         _lib = L
@@ -203,6 +207,8 @@ class Solver:
             raise SroError(st, L.sro_last_error(None).decode())
         self.h = h
         self.cap = slab_cap
+        # borrowed device tensors must outlive the handle (sro.h): held until close()
+        self._borrowed = tuple(t for t in (C, X, Y) if _is_cuda(t))
         nh = ct.c_int32()
         self._check(L.sro_held_columns(h, None, ct.byref(nh)))
         self.held = np.empty(nh.value, dtype=np.int32)
@@ -218,6 +224,7 @@ class Solver:
         if getattr(self, "h", None):
             self._L.sro_destroy(self.h)
             self.h = None
+        self._borrowed = ()
 
     def __del__(self):
         try:
@@ -287,6 +294,17 @@ class Solver:
         self._check(self._L.sro_metrics(self.h, ct.byref(e), ct.byref(sp), ct.byref(lin)))
         return e.value, sp.value, lin.value
 
+    def lp_metrics(self, rows, cols, vals):
+        """(e_m, e_v): metrics (v) and (vi) of P:419-421 against a reference plan T* (e.g. T*_LP)
+        given as COO sorted by column, then row (sro_lp_metrics)."""
+        rows = np.ascontiguousarray(rows, dtype=np.int32)
+        cols = np.ascontiguousarray(cols, dtype=np.int32)
+        vals = np.ascontiguousarray(vals, dtype=np.float64)
+        em, ev = ct.c_double(), ct.c_double()
+        self._check(self._L.sro_lp_metrics(self.h, _ptr(rows), _ptr(cols), _ptr(vals), len(vals), ct.byref(em),
+                                           ct.byref(ev)))
+        return em.value, ev.value
+
     def rowsums(self):
         r = np.empty(self.m)
         self._check(self._L.sro_get_rowsums(self.h, _ptr(r)))
@@ -337,6 +355,20 @@ def kmeans_quantize(pixels, k: int, init_idx, max_iters: int = 100, stream=None)
     return cen, lab, cnt, int(it.value), bool(conv.value)
 
 
+def kmeans_features(centroids, counts):
+    """sro_kmeans_features: (colours k x 3 = centroid / 255, histogram counts / N), R29."""
+    L = load_library()
+    cen = np.ascontiguousarray(centroids, dtype=np.float64)
+    cnt = np.ascontiguousarray(counts, dtype=np.int64)
+    k = len(cnt)
+    x = np.empty((k, 3))
+    w = np.empty(k)
+    st = L.sro_kmeans_features(_ptr(cen), _ptr(cnt), k, _ptr(x), _ptr(w))
+    if st != OK:
+        raise SroError(st, L.sro_kmeans_error().decode())
+    return x, w
+
+
 def recolour(labels, xhat, stream=None):
     """sro_recolour: npix x 3 uint8 pixels, each its class's colour rint(255 x_hat)."""
     L = load_library()
@@ -360,12 +392,8 @@ def colour_transfer(src_pixels, ref_pixels, m: int, n: int, init_src, init_ref, 
     Returns (recoloured pixels, solve result dict, (x, a, y, b, xhat))."""
     cx, lx, ax_cnt, _, _ = kmeans_quantize(src_pixels, m, init_src, kmeans_iters)
     cy, _, by_cnt, _, _ = kmeans_quantize(ref_pixels, n, init_ref, kmeans_iters)
-    x, y = cx / 255.0, cy / 255.0
-    a = ax_cnt.astype(np.float64) / float(len(lx))
-    b = by_cnt.astype(np.float64) / float(by_cnt.sum())
-    keep_a, keep_b = a > 0, b > 0
-    if not keep_a.all() or not keep_b.all():
-        raise SroError(2, "an empty k-means class (k larger than the distinct colours)")
+    x, a = kmeans_features(cx, ax_cnt)
+    y, b = kmeans_features(cy, by_cnt)
     s = Solver(a, b, lam, X=x, Y=y, cost=cost, prec=prec)
     try:
         res = s.solve(variant, iters if iters is not None else 1000 * n, seed=seed, epsilon=epsilon, **solve_opts)

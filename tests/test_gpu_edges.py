@@ -102,3 +102,36 @@ def test_tall_and_wide_sequential_bitexact(m, n, name, ov, gv, kw):
         assert np.array_equal(rg["trace"][f], ro["trace"][f]), f
     assert np.array_equal(g.plan(), o.plan())
     g.close()
+
+
+def test_explicit_visits_out_of_range_rejected():
+    """sro_solve range-checks an explicit visit list (columns in [0, n), blocks in [0, n / B))
+    before it reaches the device: INVALID_ARG, state untouched."""
+    a, b, C = _inst("plain", 40, 32)
+    g = sro.Solver(a, b, 1.0, C=C)
+    T0 = g.plan()
+    for v in ([0, 5, 32], [-1], [3, 2**31 - 1]):
+        with pytest.raises(sro.SroError) as e:
+            g.solve(sro.SRO_BCFW, len(v), visit=v, step=sro.STEP_ELS, epsilon=-1.0)
+        assert e.value.status == 2
+        g.reset()
+    with pytest.raises(sro.SroError) as e:
+        g.solve(sro.SRO_BATCHED, 2, visit=[0, 4], step=sro.STEP_ELS, block_size=8, epsilon=-1.0)
+    assert e.value.status == 2
+    assert np.array_equal(g.plan(), T0)
+
+
+def test_batched_ga_past_4096_steps_bitexact():
+    """Batched GA in cursor mode draws the next block after a call's last step into visit slot
+    iters: with iters > 4096 (beyond the default visit buffer) the solve stays in bounds and
+    bit-exact against the oracle, across two calls."""
+    a, b, C = _inst("plain", 48, 64, seed=3)
+    g = sro.Solver(a, b, 1.0, C=C)
+    o = Oracle(a, b, 1.0, C=C, cap=31)
+    kw = dict(step=ELS, sampling=GA, ga_M=2, ga_inner=1, ga_post_update=1, block_size=4)
+    for iters in (4200, 300):
+        ro = o.solve(BATCHED, iters, seed=6, trace=True, epsilon=-1.0, **kw)
+        rg = g.solve(sro.SRO_BATCHED, iters, seed=6, trace=True, epsilon=-1.0, **kw)
+        for f in ("k", "i", "j", "gamma", "num", "den"):
+            assert np.array_equal(rg["trace"][f], ro["trace"][f]), f
+    assert np.array_equal(g.plan(), o.plan())

@@ -135,3 +135,88 @@ def test_gpu_barycentric_and_metrics_bitexact(m, n, prec):
         assert np.array_equal(g.plan(), o.plan())
         assert np.array_equal(g.barycentric(d["X"], d["Y"]), o.barycentric(d["X"], d["Y"]))
         assert g.metrics() == o.metrics()
+
+
+# --------------------------------------------------------------------------- metrics (v), (vi) vs T*_LP
+def _lp_plan(a, b, C):
+    """T*_LP: the unregularised, unrelaxed OT linear program of P:419 (scipy HiGHS), as COO
+    sorted by (column, row) with the LP's zeros dropped."""
+    scipy = pytest.importorskip("scipy.optimize")
+    m, n = C.shape
+    A_eq = np.zeros((m + n, m * n))
+    for k in range(m):
+        A_eq[k, k * n:(k + 1) * n] = 1.0
+    for i in range(n):
+        A_eq[m + i, i::n] = 1.0
+    res = scipy.linprog(C.ravel(), A_eq=A_eq, b_eq=np.concatenate([a, b]), bounds=(0, None), method="highs")
+    assert res.status == 0
+    T = res.x.reshape(m, n)
+    T[T < 1e-15] = 0.0
+    cols, rows = np.nonzero(T.T)
+    return T, rows.astype(np.int32), cols.astype(np.int32), T[rows, cols], res.fun
+
+
+def test_lp_metrics_closed_forms():
+    """e_m = ||T - T*|| / ||T*|| and e_v = |<T,C> - <T*,C>| / |<T*,C>| in closed form:
+    2 x 2, C = [[1, 2], [2, 1]], a = b = (1/2, 1/2): T*_LP = diag(1/2, 1/2) (cost 1); at T^(0) =
+    [[1/2, 1/2], [0, 0]] the difference is [[0, 1/2], [0, -1/2]] so e_m = 1, and <T0, C> = 3/2 so
+    e_v = 1/2; at T = T*_LP both are exactly 0."""
+    a = b = np.array([0.5, 0.5])
+    C = np.array([[1.0, 2.0], [2.0, 1.0]])
+    o = Oracle(a, b, 1.0, C=C, cap=2)
+    rows, cols, vals = np.array([0, 1]), np.array([0, 1]), np.array([0.5, 0.5])
+    assert o.lp_metrics(rows, cols, vals) == (1.0, 0.5)
+    o.set_plan(np.diag([0.5, 0.5]))
+    assert o.lp_metrics(rows, cols, vals) == (0.0, 0.0)
+
+
+def test_lp_metrics_against_highs_plan():
+    """With T*_LP from scipy HiGHS: e_m = e_v = 0 when the oracle's plan is set to T*_LP; after
+    BCFW at large lambda (where the relaxed solution approaches the LP's) e_v is
+    small and equals |<T,C> - LP| / LP with LP the solver's optimum, and e_m is the relative
+    Frobenius distance (dense numpy evaluation, 1e-12); the relaxed solution moves towards the
+    LP's as lambda shrinks (the penalty enforces the source marginal): e_v at
+    lambda = 1e-2 is far below e_v at lambda = 1; unsorted or out-of-range T* is rejected."""
+    d = instance(1, m=10, n=12, seed=6)
+    C = _sq(d["X"], d["Y"])
+    T, rows, cols, vals, lp = _lp_plan(d["a"], d["b"], C)
+    o = Oracle(d["a"], d["b"], 1.0, C=C, cap=12)
+    o.set_plan(T)
+    assert o.lp_metrics(rows, cols, vals) == (0.0, 0.0)
+    evs = []
+    for lam in (1.0, 1e-2):
+        o = Oracle(d["a"], d["b"], lam, C=C, cap=12)
+        o.solve(BCFW, 3000 * 12, seed=1, step=ELS, sampling=P, epsilon=1e-13)
+        em, ev = o.lp_metrics(rows, cols, vals)
+        Tg = o.plan()
+        assert abs(em - np.linalg.norm(Tg - T) / np.linalg.norm(T)) <= 1e-12
+        assert abs(ev - abs((Tg * C).sum() - lp) / lp) <= 1e-9
+        evs.append(ev)
+    assert evs[1] < evs[0] / 10
+    from oracle import OracleError
+    with pytest.raises(OracleError):
+        o.lp_metrics(rows[::-1], cols[::-1], vals[::-1])
+    with pytest.raises(OracleError):
+        o.lp_metrics(rows + 100, cols, vals)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n,prec", [(10, 12, "f64"), (48, 64, "f32"), (64, 40, "f64")])
+def test_gpu_lp_metrics_bitexact(m, n, prec):
+    """sro_lp_metrics against the oracle on the same plan and the same T*_LP (scipy HiGHS):
+    bit-exact e_m and e_v, at T^(0), after a few epochs, and at T = T*_LP (both 0)."""
+    sro = pytest.importorskip("paper_2103_05857_b200")
+    d = instance(1, m=m, n=n, seed=7)
+    C = _sq(d["X"], d["Y"])
+    Cs = C.astype(np.float32) if prec == "f32" else C
+    Cd = np.asarray(Cs, dtype=np.float64)
+    T, rows, cols, vals, _ = _lp_plan(d["a"], d["b"], Cd)
+    g = sro.Solver(d["a"], d["b"], 1.0, C=Cs, prec=prec)
+    o = Oracle(d["a"], d["b"], 1.0, C=Cd, cap=31)
+    for epochs in (0, 4):
+        if epochs:
+            o.solve(BCFW, epochs * n, seed=2, step=ELS, sampling=U, epsilon=-1.0)
+            g.solve(sro.SRO_BCFW, epochs * n, seed=2, step=sro.STEP_ELS, sampling=sro.SAMPLE_U, epsilon=-1.0)
+        assert g.lp_metrics(rows, cols, vals) == o.lp_metrics(rows, cols, vals)
+    with pytest.raises(sro.SroError):
+        g.lp_metrics(rows[::-1], cols[::-1], vals[::-1])
