@@ -72,6 +72,15 @@ typedef struct {
                              DENSE requires 16-byte aligned data and ld*elem % 16 == 0 */
 } sro_cost;
 
+/* Host all-gather for sharded handles whose ranks exchange through host memory instead of
+ * NCCL (sro_params.exchange): buf is host memory holding nranks slots of `count` doubles, slot
+ * `rank` written by this process; on return every slot must hold the value its rank wrote
+ * (an in-place all-gather, e.g. over a gloo process group). Return 0 on success. The library
+ * synchronises the solver stream before the call and copies the buffer back to the device
+ * after it, so every exchange is a host round trip (for hosts or tests without NCCL peers;
+ * NCCL stays the exchange of a real multi-GPU run). */
+typedef int32_t (*sro_exchange_fn)(void* user, double* buf, int64_t count, int32_t nranks, int32_t rank);
+
 typedef struct {
   int32_t m, n;         /* rows (source bins), columns (target bins), each >= 1 */
   double lambda;        /* relaxation parameter (Eq. 7), finite and > 0 */
@@ -94,7 +103,8 @@ typedef struct {
   int32_t nranks;       /* processes sharing the G shards: 1 = this process holds all G shards and
                            runs them in sequence on its stream (exchanges are in-place device
                            writes), or G = one shard per process exchanged with NCCL all-gathers
-                           on cuda_stream (libnccl.so.2 loaded at run time) */
+                           on cuda_stream (libnccl.so.2 loaded at run time) or with the host
+                           all-gather `exchange` */
   int32_t rank;         /* this process's shard when nranks == G */
   const void* nccl_id;  /* 128-byte ncclUniqueId (sro_nccl_unique_id on rank 0, shared by the
                            caller), required when nranks > 1 */
@@ -104,6 +114,9 @@ typedef struct {
                            GPU concurrently: it bounds how much of the L2 / HBM bandwidth one
                            handle's sweeps take from the others' latency-bound steps. Results
                            do not depend on it (fixed reduction orders). */
+  sro_exchange_fn exchange; /* nranks > 1: NULL -> NCCL all-gathers (nccl_id required); else this
+                               host all-gather replaces them (nccl_id ignored, no communicator) */
+  void* exchange_user;      /* passed to exchange */
 } sro_params;
 
 typedef enum { SRO_FW = 0, SRO_BCFW = 1, SRO_BCAFW = 2, SRO_BCPFW = 3, SRO_BATCHED = 4 } sro_variant;
@@ -134,7 +147,9 @@ typedef struct {
   int32_t block_size;     /* BATCHED: columns per block B (B divides n) */
   const int32_t* visit;   /* optional host array of explicit visits (columns, or block indices for
                              BATCHED), length >= iters; NULL -> the sampling rule */
-  sro_trace_rec* trace;   /* optional host array receiving one record per step, length >= iters */
+  sro_trace_rec* trace;   /* optional host array receiving one record per step, length >= iters
+                             (sharded with nranks > 1: written on the rank holding shard 0, which
+                             holds the first column of every U; other ranks' records stay zero) */
 } sro_options;
 
 typedef struct {

@@ -102,6 +102,10 @@ struct Solver {
   Solver* lead = this;                 // the handle (owns peers, exchange buffers, stats)
   std::vector<Solver*> peers;          // other shards held by this process (nranks == 1)
   ncclComm_t comm = nullptr;
+  sro_exchange_fn xfn = nullptr;       // host all-gather (sro_params.exchange) instead of NCCL
+  void* xuser = nullptr;
+  double* xhost = nullptr;             // pinned staging buffer of the host exchange
+  size_t xhost_cap = 0;
   int slot_len = 0;
   double *x1 = nullptr, *x2 = nullptr, *gx = nullptr;   // exchange buffers (lead-owned)
   int* capfail = nullptr;
@@ -581,6 +585,20 @@ sro_status check_status(Solver* s) {
 // already. nranks == G: in-place all-gather on the solver stream.
 sro_status exchange(Solver* s, double* buf, size_t count) {
   if (s->nranks == 1) return SRO_OK;
+  if (s->xfn) {   // host all-gather: device slots -> pinned host buffer -> callback -> device
+    const size_t total = count * (size_t)s->nranks;
+    if (total > s->xhost_cap) {
+      if (s->xhost) cudaFreeHost(s->xhost);
+      s->xhost = nullptr; s->xhost_cap = 0;
+      CUDA_TRY(s, cudaHostAlloc((void**)&s->xhost, sizeof(double) * total, cudaHostAllocDefault));
+      s->xhost_cap = total;
+    }
+    CUDA_TRY(s, cudaMemcpyAsync(s->xhost, buf, sizeof(double) * total, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(s, stream_wait(s));
+    if (s->xfn(s->xuser, s->xhost, (int64_t)count, s->nranks, s->shard) != 0) { s->err = "host exchange failed"; return SRO_ERR_NCCL; }
+    CUDA_TRY(s, cudaMemcpyAsync(buf, s->xhost, sizeof(double) * total, cudaMemcpyHostToDevice, s->stream));
+    return SRO_OK;
+  }
   NcclApi& api = nccl();
   ncclResult_t r = api.allgather(buf + (size_t)s->shard * count, buf, count, ncclFloat64, s->comm, s->stream);
   if (r != ncclSuccess) { s->err = std::string("ncclAllGather: ") + api.errstr(r); return SRO_ERR_NCCL; }
@@ -1512,6 +1530,7 @@ void free_solver(Solver* s) {
   if (s->x2) cudaFree(s->x2);
   if (s->gx) cudaFree(s->gx);
   if (s->comm) nccl().destroy(s->comm);
+  if (s->xhost) cudaFreeHost(s->xhost);
   free_shard(s);
 }
 
@@ -1621,7 +1640,7 @@ sro_status sro_create(const double* a, const double* b, const sro_cost* cost, co
     if (G > 64 || (G & (G - 1))) { g_create_err = "shards must be a power of two <= 64"; return SRO_ERR_INVALID_ARG; }
     if (Bo < 1 || p->n % Bo != 0 || Bo % G != 0) { g_create_err = "shard_block must divide n and be a multiple of shards"; return SRO_ERR_INVALID_ARG; }
     if (nranks != 1 && nranks != G) { g_create_err = "nranks must be 1 or shards"; return SRO_ERR_INVALID_ARG; }
-    if (nranks > 1 && (p->rank < 0 || p->rank >= G || !p->nccl_id)) { g_create_err = "nranks > 1 needs rank in [0, shards) and nccl_id"; return SRO_ERR_INVALID_ARG; }
+    if (nranks > 1 && (p->rank < 0 || p->rank >= G || (!p->nccl_id && !p->exchange))) { g_create_err = "nranks > 1 needs rank in [0, shards) and nccl_id or exchange"; return SRO_ERR_INVALID_ARG; }
     if (nranks == 1 && cost->data_on_device && cost->kind != SRO_COST_HASH_UNIFORM && Bo != p->n) {
       g_create_err = "borrowed device cost with nranks == 1 needs shard_block == n"; return SRO_ERR_INVALID_ARG;
     }
@@ -1693,7 +1712,10 @@ sro_status sro_create(const double* a, const double* b, const sro_cost* cost, co
       return fail(SRO_ERR_OOM, "device allocation failed");
     cudaMemsetAsync(s->x1, 0, sizeof(double) * G * s->slot_len, s->stream);
     cudaMemsetAsync(s->x2, 0, sizeof(double) * G * s->slot_len, s->stream);
-    if (nranks > 1) {
+    if (nranks > 1 && p->exchange) {
+      s->xfn = p->exchange;
+      s->xuser = p->exchange_user;
+    } else if (nranks > 1) {
       NcclApi& api = nccl();
       if (!api.ok) return fail(SRO_ERR_NCCL, api.err);
       ncclUniqueId id;

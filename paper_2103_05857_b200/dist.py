@@ -3,8 +3,10 @@
 One process per GPU (torch.distributed for rendezvous only). Every rank holds
 one column shard of a sharded Solver; the per-step exchanges (the subtree
 partials of the fixed 256-chunk sums, R19) run inside libsro.so as in-place
-NCCL all-gathers on the solver stream. This module only computes which
-columns a rank holds, slices its inputs and shares the NCCL unique id.
+NCCL all-gathers on the solver stream (or, transport="host", through a host
+all-gather callback over a torch.distributed group). This module only computes
+which columns a rank holds, slices its inputs and shares the NCCL unique id or
+wires the host all-gather.
 """
 from __future__ import annotations
 
@@ -27,6 +29,8 @@ def held_columns(n: int, shards: int, shard: int, shard_block: int = 0) -> np.nd
 
 def shard_cost_inputs(shards: int, shard: int, shard_block: int = 0, *, C=None, Y=None):
     """This shard's columns of a dense m x n cost and/or of the n x 3 target colours."""
+    if C is None and Y is None:
+        return None, None
     n = C.shape[1] if C is not None else Y.shape[0]
     cols = held_columns(n, shards, shard, shard_block)
     return (None if C is None else np.ascontiguousarray(C[:, cols]),
@@ -41,14 +45,30 @@ def share_unique_id(group=None) -> bytes:
     return box[0]
 
 
+def host_allgather(group=None):
+    """An exchange for sro_params.exchange over a torch.distributed group (e.g. gloo): the
+    (nranks, count) host buffer's row `rank` is all-gathered into every row, in place."""
+    import torch
+    import torch.distributed as dist
+
+    def f(buf, rank):
+        rows = list(torch.from_numpy(buf).unbind(0))            # views into buf
+        dist.all_gather(rows, torch.from_numpy(buf[rank].copy()), group=group)
+    return f
+
+
 def sharded_solver(a, b, lam, *, shard_block: int = 0, C=None, X=None, Y=None, cost="dense", group=None,
-                   **kw) -> Solver:
+                   transport: str = "nccl", **kw) -> Solver:
     """A Solver holding this rank's column shard (collective over `group`).
     C / Y are the FULL cost / target colours; each rank passes on its columns only.
-    Sequential BCFW-family variants do not shard (replicas only)."""
+    transport: "nccl" (device all-gathers on the solver stream) or "host" (sro_params.exchange
+    through `group`, e.g. gloo). Sequential BCFW-family variants do not shard (replicas only)."""
     import torch.distributed as dist
     G, rank = dist.get_world_size(group), dist.get_rank(group)
-    uid = share_unique_id(group)
     Cl, Yl = shard_cost_inputs(G, rank, shard_block, C=C, Y=Y)
+    if transport == "host":
+        return Solver(a, b, lam, C=Cl, X=X, Y=Yl, cost=cost, shards=G, shard_block=shard_block, nranks=G,
+                      rank=rank, exchange=host_allgather(group), **kw)
+    uid = share_unique_id(group)
     return Solver(a, b, lam, C=Cl, X=X, Y=Yl, cost=cost, shards=G, shard_block=shard_block, nranks=G, rank=rank,
                   nccl_id=uid, **kw)

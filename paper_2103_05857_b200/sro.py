@@ -45,11 +45,15 @@ class SroCost(ct.Structure):
                 ("x", ct.c_void_p), ("y", ct.c_void_p), ("hash_seed", ct.c_uint64), ("data_on_device", ct.c_int32)]
 
 
+# sro_exchange_fn: int32 (*)(void* user, double* buf, int64 count, int32 nranks, int32 rank)
+EXCHANGE_FN = ct.CFUNCTYPE(ct.c_int32, ct.c_void_p, ct.POINTER(ct.c_double), ct.c_int64, ct.c_int32, ct.c_int32)
+
+
 class SroParams(ct.Structure):
     _fields_ = [("m", ct.c_int32), ("n", ct.c_int32), ("lambda_", ct.c_double), ("slab_cap", ct.c_int32),
                 ("device", ct.c_int32), ("cuda_stream", ct.c_void_p), ("shards", ct.c_int32),
                 ("shard_block", ct.c_int32), ("nranks", ct.c_int32), ("rank", ct.c_int32), ("nccl_id", ct.c_void_p),
-                ("max_sms", ct.c_int32)]
+                ("max_sms", ct.c_int32), ("exchange", EXCHANGE_FN), ("exchange_user", ct.c_void_p)]
 
 
 class SroTraceRec(ct.Structure):
@@ -163,7 +167,7 @@ class Solver:
 
     def __init__(self, a, b, lam, *, C=None, X=None, Y=None, cost="dense", prec="f64", hash_seed=0, slab_cap=31,
                  device=0, stream=None, ld=None, shards=1, shard_block=0, nranks=1, rank=0, nccl_id=None,
-                 max_sms=0):
+                 max_sms=0, exchange=None):
         L = load_library()
         self._L = L
         a = np.ascontiguousarray(a, dtype=np.float64)
@@ -197,10 +201,22 @@ class Solver:
         idbuf = None
         if nccl_id is not None:
             idbuf = ct.create_string_buffer(bytes(nccl_id), 128)
+        # exchange: a Python all-gather f(buf, rank) over an (nranks, count) float64 host array whose
+        # row `rank` is filled (sro_exchange_fn); the ctypes thunk lives as long as the handle
+        self._xfn = None
+        if exchange is not None:
+            def _thunk(user, buf, count, nr, rk, _f=exchange):
+                try:
+                    _f(np.ctypeslib.as_array(buf, shape=(nr * count,)).reshape(nr, count), rk)
+                    return 0
+                except Exception:  # noqa: BLE001 — reported to the library as a failed exchange
+                    return 1
+            self._xfn = EXCHANGE_FN(_thunk)
         p = SroParams(m=self.m, n=self.n, lambda_=self.lam, slab_cap=slab_cap, device=device,
                       cuda_stream=ct.c_void_p(stream) if stream else None, shards=shards, shard_block=shard_block,
                       nranks=nranks, rank=rank, nccl_id=ct.cast(idbuf, ct.c_void_p) if idbuf is not None else None,
-                      max_sms=max_sms)
+                      max_sms=max_sms, exchange=self._xfn if self._xfn is not None else EXCHANGE_FN(),
+                      exchange_user=None)
         h = ct.c_void_p()
         st = L.sro_create(_ptr(a), _ptr(b), ct.byref(c), ct.byref(p), ct.byref(h))
         if st != OK:
