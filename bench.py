@@ -10,11 +10,17 @@ that instance: BCFW-P-ELS, BCAFW, BCPFW and BCFW-GA (the paper's BCFW + three fa
 variants) plus full FW (Alg. A.1) and batched BCFW (B = 256), each from T^(0) to
 g <= 1e-6. The six solves are independent and run concurrently (one handle and CUDA stream
 each; a sequential solve is one persistent CTA); --serial-solves runs them one after
-another. value = cost entries scanned by all LMO calls / device time of the step.
+another. value = cost entries the kernels read (sro_result.entries_read) / device time of
+the step.
+
+Extra keys: `sweep_roofline` (config [3]: the HBM-bound dense gap sweep and FW-ELS to gap),
+`configs` (configs [2] and [4]: batched BCFW to gap with fused colour costs, and their fused
+gap sweeps) at N = 1; `sharded` at N > 1: FW-ELS on [3] and batched B = 1024 on [4], column-
+sharded over the N GPUs with NCCL all-gathers, time to gap as the max over ranks.
 
 N > 1 (torchrun): the sequential BCFW family does not shard (each step depends on
-the previous r), so ranks are independent replicas on their own seeded instances
-(weak scaling, no data-path collective); value = all ranks' entries / max time.
+the previous r), so the headline step's ranks are independent replicas on their own seeded
+instances (weak scaling, no data-path collective); value = all ranks' entries / max time.
 
 --impl reference times the oracle (plain fp64 C, one host core) on a bounded sample
 of the same workload.
@@ -200,7 +206,7 @@ class StepRunner:
         for (name, _, _, cap), r in zip(PLAN, results):
             if not r["converged"]:
                 raise RuntimeError(f"{name} did not reach g <= {EPS} within {cap} iterations (gap {r['gap']})")
-            entries_acc.append(r["entries_scanned"])
+            entries_acc.append(r["entries_read"])
             ttg[name] = ttg.get(name, []) + [r["device_ms"]]
         return e0.elapsed_time(e1)
 
@@ -304,13 +310,17 @@ def bench_sro(args, rank, world, local_rank):
     else:
         max_ms, all_entries = total_ms, my_entries
         e2e_max_ms, e2e_all_entries = sum(e2e_ms), sum(e2e_entries)
-    sweep_rf = None
-    if rank == 0 and not args.no_sweep_check:
+    sweep_rf, legs, sharded = None, None, None
+    if not args.no_sweep_check:
         del flush, Cd
         torch.cuda.synchronize()
-        sweep_rf = sweep_roofline_config3(local_rank, measured_peaks())
+        if world > 1:
+            sharded = sharded_legs(rank, world, local_rank)
+        elif rank == 0:
+            sweep_rf = sweep_roofline_config3(local_rank, measured_peaks())
+            legs = configs_legs_single(local_rank)
     return dict(max_ms=max_ms, all_entries=all_entries, stats=stats, clocks=clk, ttg=ttg, step_ms=step_ms,
-                sweep_roofline=sweep_rf,
+                sweep_roofline=sweep_rf, configs_legs=legs, sharded=sharded,
                 e2e_value=e2e_all_entries / (e2e_max_ms * 1e-3), h2d=h2d, d2h=d2h, instance=d,
                 e2e_ms=[round(x, 2) for x in e2e_ms])
 
@@ -384,8 +394,96 @@ def sweep_roofline_config3(local_rank, peaks, sweeps=3):
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, of measured)",
             "fw_els_time_to_gap_ms": round(r["device_ms"], 3), "fw_els_iterations": r["iters_done"],
             "fw_els_converged": bool(r["converged"]), "fw_gap": r["gap"],
-            "fw_entries_per_s": r["entries_scanned"] / (r["device_ms"] * 1e-3),
+            "fw_entries_per_s": r["entries_read"] / (r["device_ms"] * 1e-3),
             "fw_sweep_share": round(st2["sweep_ms"] / max(1e-9, st2["block_ms"]), 4)}
+
+
+def _timed_solve(s, variant, cap, **opts):
+    """One solve from T^(0) after an untimed warm-up solve of the same call (workspaces, CUDA
+    graph capture): the device time of the call (CUDA events on the solver stream)."""
+    s.reset()
+    s.solve(variant, cap, seed=11, epsilon=EPS, **opts)
+    s.reset()
+    return s.solve(variant, cap, seed=11, epsilon=EPS, **opts)
+
+
+def configs_legs_single(local_rank):
+    """BASELINE configs [2] and [4] on one GPU (fused fp32 squared-Euclidean costs from d = 3
+    colours, batched BCFW with B = 256 / 1024, P order, exact line search) from T^(0) to
+    g <= 1e-6: time to gap, block steps, cost entries read per second, and the fused colour
+    gap sweep alone (the whole m x n LMO + column gaps, timed by the library's CUDA events)."""
+    import paper_2103_05857_b200 as sro
+    from sro_inputs import instance
+    out = {}
+    for cfg, B in ((2, 256), (4, 1024)):
+        d = instance(cfg, seed=0)
+        s = sro.Solver(d["a"], d["b"], 1.0, X=d["X"], Y=d["Y"], cost="sqeuclid", prec="f32", device=local_rank)
+        r = _timed_solve(s, sro.SRO_BATCHED, 400 * (d["n"] // B), step=sro.STEP_ELS, sampling=sro.SAMPLE_P,
+                         block_size=B)
+        s.gap()
+        s.set_timing(True)
+        s.stats(reset=True)
+        for _ in range(3):
+            s.gap()
+        st = s.stats(reset=True)
+        s.close()
+        sweep_ms = st["sweep_ms"] / max(1, st["sweep_launches"])
+        ent = float(d["m"]) * d["n"]
+        out[f"config{cfg}"] = {
+            "workload": f"BASELINE configs[{cfg}]: m={d['m']}, n={d['n']}, fused fp32 sqeuclid, batched B={B}, P, ELS",
+            "time_to_gap_ms": round(r["device_ms"], 3), "block_steps": r["iters_done"],
+            "converged": bool(r["converged"]), "gap": r["gap"], "us_per_block_step": round(
+                1e3 * r["device_ms"] / max(1, r["iters_done"]), 2),
+            "entries_per_s": r["entries_read"] / (r["device_ms"] * 1e-3),
+            "gap_sweep_ms": round(sweep_ms, 4), "gap_sweep_entries_per_s": ent / (sweep_ms * 1e-3)}
+    return out
+
+
+def sharded_legs(rank, world, local_rank):
+    """N > 1: the column-sharded variants of north_star through NCCL (one shard per GPU,
+    sro_params.nranks = shards = N). [3]: FW-ELS from T^(0) to g <= 1e-6 on the
+    m = n = 65536 iid cost, each rank generating its own 65536 x 65536/N column shard on the
+    device; [4]: batched B = 1024 (shard_block = 1024, each rank B/N columns of every block),
+    P, ELS, to g <= 1e-6. Time = max over ranks of the solve's device time; entries = all
+    ranks' cost entries read."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2103_05857_b200 as sro
+    from paper_2103_05857_b200.dist import share_unique_id, shard_cost_inputs
+    from sro_inputs import instance
+    dev = torch.device("cuda", local_rank)
+    out = {}
+    for cfg in (3, 4):
+        d = instance(cfg, seed=0)
+        uid = share_unique_id()
+        if cfg == 3:
+            s = sro.Solver(d["a"], d["b"], 1.0, cost="hash", hash_seed=d["hash_seed"], device=local_rank,
+                           shards=world, nranks=world, rank=rank, nccl_id=uid)
+            r = _timed_solve(s, sro.SRO_FW, 500, step=sro.STEP_ELS)
+            per = "FW iteration"
+        else:
+            _, Yl = shard_cost_inputs(world, rank, 1024, Y=d["Y"])
+            s = sro.Solver(d["a"], d["b"], 1.0, X=d["X"], Y=Yl, cost="sqeuclid", prec="f32", device=local_rank,
+                           shards=world, shard_block=1024, nranks=world, rank=rank, nccl_id=uid)
+            r = _timed_solve(s, sro.SRO_BATCHED, 400 * (d["n"] // 1024), step=sro.STEP_ELS, sampling=sro.SAMPLE_P,
+                             block_size=1024)
+            per = "block step"
+        s.close()
+        t = torch.tensor([r["device_ms"], float(r["entries_read"])], dtype=torch.float64, device=dev)
+        tmax, tsum = t.clone(), t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        ms = tmax[0].item()
+        out[f"config{cfg}"] = {
+            "workload": (f"BASELINE configs[{cfg}] column-sharded over {world} GPUs (" +
+                         ("FW-ELS, hash cost generated per shard" if cfg == 3 else
+                          "batched B=1024, P, ELS, fused fp32 sqeuclid") + ")"),
+            "shards": world, "exchange": "ncclAllGather of the per-shard 256-chunk subtrees (R19), 2 per " + per,
+            "time_to_gap_ms": round(ms, 3), "iterations": r["iters_done"], "converged": bool(r["converged"]),
+            "gap": r["gap"], f"ms_per_{per.replace(' ', '_')}": round(ms / max(1, r["iters_done"]), 4),
+            "entries_per_s": tsum[1].item() / (ms * 1e-3)}
+    return out
 
 
 # --------------------------------------------------------------------------- oracle (CPU)
@@ -477,7 +575,7 @@ def main():
     ap.add_argument("--serial-solves", action="store_true",
                     help="run the six solves of a step one after another instead of concurrently")
     ap.add_argument("--no-sweep-check", action="store_true",
-                    help="skip the config-[3] HBM sweep measurement (sweep_roofline)")
+                    help="skip the extra legs (sweep_roofline, configs [2]/[4], the sharded legs at N > 1)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -507,6 +605,8 @@ def main():
                 "gb_per_s_equiv": round(value * 4 / 1e9, 3),
                 "roofline": roofline_from_stats(res["stats"], peaks),
                 "sweep_roofline": res.get("sweep_roofline"),
+                "configs": res.get("configs_legs"),
+                "sharded": res.get("sharded"),
                 "clocks": res["clocks"],
                 "e2e": {"value": res["e2e_value"], "unit": UNIT, "h2d_bytes_per_step": res["h2d"],
                         "d2h_bytes_per_step": res["d2h"], "ms_per_step": res["e2e_ms"]},

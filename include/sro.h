@@ -159,8 +159,12 @@ typedef struct {
   double objective;       /* f(T) at the end of the call */
   int32_t converged;      /* 1 if a gap check met epsilon */
   int32_t gap_checks;     /* gap evaluations in this call */
-  int64_t entries_scanned;/* cost entries read by LMO calls in this call (steps + sweeps) */
+  int64_t entries_scanned;/* cost entries evaluated by the method's LMO calls in this call (steps, gap
+                             sweeps, GA refreshes — counted as the paper's algorithm calls them) */
   double device_ms;       /* device time of the call (CUDA events on the solver stream) */
+  int64_t entries_read;   /* cost entries the kernels actually read: a GAD post-update refresh reuses
+                             the step's column, and a GA global refresh due with a gap check is one
+                             sweep for both (<= entries_scanned) */
 } sro_result;
 
 /* Kernel accounting of a handle (for benchmarks): launches of this library's

@@ -1067,6 +1067,20 @@ sro_status ga_global_refresh(Solver* s, const int* stop = nullptr) {
   return fen_build(s, -1, stop);
 }
 
+// GA global refresh that is also the epoch's gap check (M = 1 and the check falls on the same
+// boundary, SURVEY c.7 / P:363): ONE sweep stores every g_i(T) as the new G_i and the gap total
+// is the psum256 of those same values — bitwise what the separate refresh + gap sweep give.
+sro_status ga_refresh_and_gap(Solver* s, const int* stop = nullptr) {
+  sro_status st = sweep(s, nullptr, 0, 0, s->n, s->sw_j, s->sw_min, s->G_ga, stop);
+  if (st) return st;
+  st = fen_build(s, -1, stop);
+  if (st) return st;
+  k_psum256<<<1, 256, 0, s->stream>>>(s->G_ga, s->n, s->scal + 4, nullptr, nullptr, stop);
+  s->lead->stats.kernel_launches += 1;
+  CUDA_TRY(s, cudaGetLastError());
+  return SRO_OK;
+}
+
 __global__ void k_halt_on_status(const int* status, int* halt) {
   if (*status) *halt = 1;
 }
@@ -1111,9 +1125,10 @@ sro_status seq_epochs(Solver* s, int variant, const sro_options* o, int64_t iter
     if (st) return st;
     k_halt_on_status<<<1, 1, 0, s->stream>>>(s->status, s->stop);
     s->lead->stats.kernel_launches += 1;
-    if (e.refresh) { st = ga_global_refresh(s, s->stop); if (st) return st; }
+    const bool fused = e.refresh && e.check && s->G == 1;
+    if (e.refresh && !fused) { st = ga_global_refresh(s, s->stop); if (st) return st; }
     if (e.check) {
-      st = gap_sweep_kernels(s, s->stop);
+      st = fused ? ga_refresh_and_gap(s, s->stop) : gap_sweep_kernels(s, s->stop);
       if (st) return st;
       k_halt_on_gap<<<1, 1, 0, s->stream>>>(s->scal + 4, o->epsilon, s->stop);
       s->lead->stats.kernel_launches += 1;
@@ -1149,13 +1164,18 @@ sro_status seq_epochs(Solver* s, int variant, const sro_options* o, int64_t iter
     if (cur.check) memcpy(&g, slot + 8, sizeof(double));
     resolve_timing(s);
     s->k += sd; done += sd;
+    // LMO-call count as the method (and the oracle) defines it: a GAD post-update refresh is a
+    // second LMO on the column; the kernels take it from the step's own column read (entries_read)
     out->entries_scanned += m * sd * ((ga && o->ga_inner && o->ga_post_update) ? 2 : 1);
+    out->entries_read += m * sd;
     if (dst) { st = status_fail(s, dst); break; }
     if (sd != cur.seg) { s->err = "segment stopped early without a status"; st = SRO_ERR_CUDA; break; }
     if (cur.refresh) out->entries_scanned += m * n;
+    if (cur.refresh && !(cur.check && s->G == 1)) out->entries_read += m * n;
     if (cur.check) {
       out->gap = g; out->gap_checks++;
       out->entries_scanned += m * n;
+      out->entries_read += m * n;
       if (g <= o->epsilon) { out->converged = 1; break; }
     }
     if (!have_next) break;
@@ -1880,6 +1900,7 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
       out->gap = G;
       out->gap_checks += (int)(done - before) + (stopped ? 1 : 0);
       out->entries_scanned += (int64_t)m * n_held * ((done - before) + (stopped ? 1 : 0));
+      out->entries_read += (int64_t)m * n_held * ((done - before) + (stopped ? 1 : 0));
       if (stopped) { out->converged = 1; break; }
     }
     for (Solver* t : held(s)) CUDA_TRY(s, cudaMemsetAsync(t->stop, 0, sizeof(int), s->stream));
@@ -1900,15 +1921,24 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
       if (st) return st;
     }
     const long long gaMn = ga ? (long long)o->ga_M * nprime : 0;   // global refresh period (R16, R31)
+    bool refreshed_with_gap = false;   // batched GA: the refresh sweep that just ran was fused with this check
     for (;;) {
       if (s->k % period == 0) {
         double g = 0.0;
-        st = gap_sweep(s, &g);
+        if (refreshed_with_gap) {
+          CUDA_TRY(s, rb(s, &g, s->scal + 4, sizeof(double)));
+          st = check_status(s);
+          resolve_timing(s);
+        } else {
+          st = gap_sweep(s, &g);
+          out->entries_read += (int64_t)m * n_held;
+        }
         if (st) return st;
         out->gap = g; out->gap_checks++;
         out->entries_scanned += (int64_t)m * n_held;
         if (g <= o->epsilon) { out->converged = 1; break; }
       }
+      refreshed_with_gap = false;
       if (done >= iters) break;
       if (variant == SRO_BATCHED) {
         // enqueue every block step up to the next gap check, then one sync
@@ -1984,14 +2014,24 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
           }
         }
         st = drain_block_steps(s, &done);
-        out->entries_scanned += (int64_t)m * (o->block_size / s->G) * (int64_t)held(s).size() * (done - before) *
-                                ((ga && o->ga_inner && o->ga_post_update) ? 2 : 1);
+        {
+          const int64_t e = (int64_t)m * (o->block_size / s->G) * (int64_t)held(s).size() * (done - before) *
+                            ((ga && o->ga_inner && o->ga_post_update) ? 2 : 1);   // post: a second sweep of the block
+          out->entries_scanned += e;
+          out->entries_read += e;
+        }
         if (st) break;
         if (ga && s->k % gaMn == 0) {
           double gdummy = 0.0;
-          st = s->G > 1 ? ga_global_refresh_sharded(s, &gdummy) : ga_global_refresh(s);
+          if (s->G == 1 && s->k % period == 0) {   // the refresh sweep also gives the gap check due now
+            st = ga_refresh_and_gap(s);
+            refreshed_with_gap = true;
+          } else {
+            st = s->G > 1 ? ga_global_refresh_sharded(s, &gdummy) : ga_global_refresh(s);
+          }
           if (st) return st;
           out->entries_scanned += (int64_t)m * n;
+          out->entries_read += (int64_t)m * n;
         }
         continue;
       }

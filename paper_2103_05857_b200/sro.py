@@ -76,7 +76,7 @@ class SroOptions(ct.Structure):
 class SroResult(ct.Structure):
     _fields_ = [("iters_done", ct.c_int64), ("k", ct.c_int64), ("gap", ct.c_double), ("objective", ct.c_double),
                 ("converged", ct.c_int32), ("gap_checks", ct.c_int32), ("entries_scanned", ct.c_int64),
-                ("device_ms", ct.c_double)]
+                ("device_ms", ct.c_double), ("entries_read", ct.c_int64)]
 
 
 class SroStats(ct.Structure):
