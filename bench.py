@@ -232,6 +232,25 @@ class StepRunner:
             s.close()
 
 
+# Test-only emulation of N ranks on ONE GPU (SRO_BENCH_EMULATE_RANKS=1 under torchrun): gloo instead
+# of NCCL for the process group, every rank on cuda:0, and the sharded legs exchange through the
+# library's host all-gather (sro_params.exchange) — so the N > 1 control flow of this file runs
+# end to end on a 1-GPU box. Its numbers are not bench values.
+EMULATE = os.environ.get("SRO_BENCH_EMULATE_RANKS") == "1"
+
+
+def _max_sum(vals, dev):
+    """Element-wise max and sum over ranks of a small float64 vector (NCCL on the device, or gloo
+    on the host in emulation)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64, device="cpu" if EMULATE else dev)
+    tmax, tsum = t.clone(), t.clone()
+    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+    return tmax.tolist(), tsum.tolist()
+
+
 def bench_sro(args, rank, world, local_rank):
     import torch
 
@@ -302,11 +321,9 @@ def bench_sro(args, rank, world, local_rank):
 
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([total_ms, my_entries, sum(e2e_ms), sum(e2e_entries)], dtype=torch.float64, device=dev)
-        tmax = t.clone(); dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        tsum = t.clone(); dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
-        max_ms, all_entries = tmax[0].item(), tsum[1].item()
-        e2e_max_ms, e2e_all_entries = tmax[2].item(), tsum[3].item()
+        tmax, tsum = _max_sum([total_ms, my_entries, sum(e2e_ms), sum(e2e_entries)], dev)
+        max_ms, all_entries = tmax[0], tsum[1]
+        e2e_max_ms, e2e_all_entries = tmax[2], tsum[3]
     else:
         max_ms, all_entries = total_ms, my_entries
         e2e_max_ms, e2e_all_entries = sum(e2e_ms), sum(e2e_entries)
@@ -450,31 +467,29 @@ def sharded_legs(rank, world, local_rank):
     import torch.distributed as dist
 
     import paper_2103_05857_b200 as sro
-    from paper_2103_05857_b200.dist import share_unique_id, shard_cost_inputs
+    from paper_2103_05857_b200.dist import host_allgather, share_unique_id, shard_cost_inputs
     from sro_inputs import instance
     dev = torch.device("cuda", local_rank)
     out = {}
     for cfg in (3, 4):
         d = instance(cfg, seed=0)
-        uid = share_unique_id()
+        # NCCL unique id (or, emulating ranks on one GPU, the host all-gather over gloo)
+        xk = dict(exchange=host_allgather()) if EMULATE else dict(nccl_id=share_unique_id())
         if cfg == 3:
             s = sro.Solver(d["a"], d["b"], 1.0, cost="hash", hash_seed=d["hash_seed"], device=local_rank,
-                           shards=world, nranks=world, rank=rank, nccl_id=uid)
+                           shards=world, nranks=world, rank=rank, **xk)
             r = _timed_solve(s, sro.SRO_FW, 500, step=sro.STEP_ELS)
             per = "FW iteration"
         else:
             _, Yl = shard_cost_inputs(world, rank, 1024, Y=d["Y"])
             s = sro.Solver(d["a"], d["b"], 1.0, X=d["X"], Y=Yl, cost="sqeuclid", prec="f32", device=local_rank,
-                           shards=world, shard_block=1024, nranks=world, rank=rank, nccl_id=uid)
+                           shards=world, shard_block=1024, nranks=world, rank=rank, **xk)
             r = _timed_solve(s, sro.SRO_BATCHED, 400 * (d["n"] // 1024), step=sro.STEP_ELS, sampling=sro.SAMPLE_P,
                              block_size=1024)
             per = "block step"
         s.close()
-        t = torch.tensor([r["device_ms"], float(r["entries_read"])], dtype=torch.float64, device=dev)
-        tmax, tsum = t.clone(), t.clone()
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
-        ms = tmax[0].item()
+        tmax, tsum = _max_sum([r["device_ms"], float(r["entries_read"])], dev)
+        ms = tmax[0]
         out[f"config{cfg}"] = {
             "workload": (f"BASELINE configs[{cfg}] column-sharded over {world} GPUs (" +
                          ("FW-ELS, hash cost generated per shard" if cfg == 3 else
@@ -482,7 +497,9 @@ def sharded_legs(rank, world, local_rank):
             "shards": world, "exchange": "ncclAllGather of the per-shard 256-chunk subtrees (R19), 2 per " + per,
             "time_to_gap_ms": round(ms, 3), "iterations": r["iters_done"], "converged": bool(r["converged"]),
             "gap": r["gap"], f"ms_per_{per.replace(' ', '_')}": round(ms / max(1, r["iters_done"]), 4),
-            "entries_per_s": tsum[1].item() / (ms * 1e-3)}
+            "entries_per_s": tsum[1] / (ms * 1e-3)}
+        if EMULATE:
+            out[f"config{cfg}"]["emulated"] = "ranks share one GPU, host all-gather over gloo: not a bench value"
     return out
 
 
@@ -579,7 +596,7 @@ def main():
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    local_rank = 0 if EMULATE else int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         line = bench_reference(args, rank, world)
         if line is not None:
@@ -587,7 +604,7 @@ def main():
         return 0
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        dist.init_process_group("gloo" if EMULATE else "nccl")
     res = bench_sro(args, rank, world, local_rank)
     if rank == 0:
         peaks = measured_peaks()

@@ -1503,6 +1503,7 @@ sro_status objective_dev(Solver* s, double* f_host) {
 
 sro_status do_reset(Solver* s) {
   for (Solver* t : held(s)) {
+    { sro_status e = ws_clean(t); if (e) return e; }
     k_init_plan<<<s->num_sms, 256, 0, s->stream>>>(t->b, t->b_full, t->n_glob, t->a, t->r, t->h, t->cnt, t->srow,
                                                   t->sval, t->m, t->n, t->cap, t->lambda);
     s->lead->stats.kernel_launches += 1;
@@ -1903,7 +1904,12 @@ sro_status sro_solve(sro_handle h, int32_t variant, const sro_options* o, int64_
       out->entries_read += (int64_t)m * n_held * ((done - before) + (stopped ? 1 : 0));
       if (stopped) { out->converged = 1; break; }
     }
-    for (Solver* t : held(s)) CUDA_TRY(s, cudaMemsetAsync(t->stop, 0, sizeof(int), s->stream));
+    for (Solver* t : held(s)) {
+      CUDA_TRY(s, cudaMemsetAsync(t->stop, 0, sizeof(int), s->stream));
+      // a sharded FW step decides to stop after its phase A (the G_U subtrees are exchanged
+      // first), so that step's row workspace is left as phase A filled it: clear it
+      if (s->G > 1) { sro_status e = ws_clean(t); if (e) return e; }
+    }
   } else {
     // visit order for the whole call (U / P / explicit); GA draws on the device
     if (!ga) {

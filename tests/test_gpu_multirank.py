@@ -53,7 +53,7 @@ def _case(name):
     raise KeyError(name)
 
 
-def _worker(rank, world, port, name, q):
+def _worker(rank, world, port, name, q, reset_first=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     import torch.distributed as dist
@@ -67,6 +67,9 @@ def _worker(rank, world, port, name, q):
         X = skw.pop("X", None)
         g = sharded_solver(d["a"], d["b"], d["lam"], shard_block=Bo, C=C, X=X, Y=Y, transport="host", **skw)
         gv = {FW: sro.SRO_FW, BATCHED: sro.SRO_BATCHED}[variant]
+        if reset_first:   # a whole solve, then sro_reset: the second solve must be the first one again
+            g.solve(gv, iters, seed=5, **opts)
+            g.reset()
         r = g.solve(gv, iters, seed=5, trace=True, **opts)
         total, gcol, jcol = g.gap()
         q.put((rank, dict(held=g.held, trace=r["trace"], gap=r["gap"], converged=r["converged"],
@@ -79,14 +82,14 @@ def _worker(rank, world, port, name, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("G", [2, 4])
+@pytest.mark.parametrize("G,reset_first", [(2, False), (4, False), (2, True)], ids=["G2", "G4", "G2-after-reset"])
 @pytest.mark.parametrize("name", ["fw-hash", "fw-dense", "batched-colour", "batched-ga"])
-def test_multiprocess_sharded_bitexact(name, G):
+def test_multiprocess_sharded_bitexact(name, G, reset_first):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, G, port, name, q)) for r in range(G)]
+    procs = [ctx.Process(target=_worker, args=(r, G, port, name, q, reset_first)) for r in range(G)]
     for p in procs:
         p.start()
     out = {}

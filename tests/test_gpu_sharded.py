@@ -180,3 +180,20 @@ def test_sharded_batched_ga_bitexact(G, B, post):
     assert rg["gap"] == ro["gap"]
     assert rg["entries_scanned"] == ro["entries_scanned"]
     _same_state(g, o)
+
+
+@pytest.mark.parametrize("G", [2, 8])
+def test_sharded_solve_after_reset_repeats_first_solve(G):
+    """A sharded handle run to convergence, reset (sro_reset) and run again repeats the first
+    solve exactly (hash cost FW-ELS, the multi-kernel step path of config [3])."""
+    m, n = 1024, 2048 * G
+    seed = 0x5EED0003
+    a = np.full(m, 1.0 / m)
+    b = np.full(n, 1.0 / n)
+    g = sro.Solver(a, b, 1.0, cost="hash", hash_seed=seed, shards=G)
+    r1 = g.solve(sro.SRO_FW, 60, trace=True, step=sro.STEP_ELS, epsilon=1e-6)
+    T1 = g.plan()
+    g.reset()
+    r2 = g.solve(sro.SRO_FW, 60, trace=True, step=sro.STEP_ELS, epsilon=1e-6)
+    assert r1["iters_done"] == r2["iters_done"] and r1["gap"] == r2["gap"] and r1["converged"] == 1
+    assert np.array_equal(r1["trace"], r2["trace"]) and np.array_equal(g.plan(), T1)
