@@ -58,6 +58,7 @@ __device__ __forceinline__ double tm_cost(const TailMerge& M, int k, int i) {
 
 constexpr int TS_PMAX = 4096;   // pairs held in shared memory
 constexpr int TS_SORT = 8192;   // bitonic buffer (power of two >= TS_PMAX)
+constexpr int TS_RADIX_HIST = 128 * 4 * 32;   // radix-sort histogram: 2^7 digits x 4 rounds x 32 warps
 
 struct TailSmem {
   uint32_t key[TS_SORT];
@@ -68,47 +69,27 @@ struct TailSmem {
   double ptold[TS_PMAX];
   int prow[TS_PMAX];
   uint8_t pchunk[TS_PMAX];  // 256-chunk of the pair's column position
-  double runv[TS_PMAX];   // (row, chunk) run sums, sorted order
-  uint8_t runc[TS_PMAX];  // their chunks
-  uint16_t runu[TS_PMAX + 1];  // their first sorted index
-  int rowrun[TS_PMAX + 1];  // touched row -> its first run
-  int rrow[TS_PMAX];      // touched rows, ascending
+  union {
+    struct {
+      double runv[TS_PMAX];   // (row, chunk) run sums, sorted order
+      uint8_t runc[TS_PMAX];  // their chunks
+      uint16_t runu[TS_PMAX + 1];  // their first sorted index
+      int rowrun[TS_PMAX + 1];  // touched row -> its first run
+      int rrow[TS_PMAX];      // touched rows, ascending
+    };
+    int rcnt[TS_RADIX_HIST];  // radix sort by row (before the runs exist): per-(digit, round, warp) counts
+  };
   int hot[TS_PMAX / 8];   // touched rows with more than TS_SMALL (= 8) runs
+  int mid[TS_PMAX / 3];   // touched rows with 3 .. TS_SMALL runs
   double gcol[1024];       // column gaps over U (G_U = psum256 of them)
   int wsum[32];
-  int misc[8];            // [0] touched rows [1] runs [2] hot rows [3] abort flag
+  int misc[8];            // [0] touched rows [1] runs [2] hot rows [3] abort flag [5] mid rows
   double red[8];
   double bc[4];           // broadcasts: [2] gamma
   long long tsacc[16];    // SRO_PHASE_TIMING builds: phase clocks (thread 0), added to A.phase at exit
 };
 static_assert(sizeof(TailSmem) + 1408 <= 232448, "k_block_tail_sm shared memory");
 constexpr size_t TAIL_SM_BYTES = sizeof(TailSmem) > 32 * 256 * 8 ? sizeof(TailSmem) : 32 * 256 * 8;
-
-// 256-leaf adjacent-pair tree over leaves pushed in ascending chunk order: a
-// stack of completed subtrees (their boundary heights strictly decrease
-// towards the top, so at most 9 entries), kept in registers — every index is
-// static, the stack shifts instead (the top is entry 0).
-struct TreeStack {
-  double v[9];
-  int c[9];
-  int n = 0;
-  __device__ __forceinline__ void pop_merge() {   // top two -> left + right
-    v[1] = d_add(v[1], v[0]);
-#pragma unroll
-    for (int e = 0; e < 8; e++) { v[e] = v[e + 1]; c[e] = c[e + 1]; }
-    n--;
-  }
-  __device__ __forceinline__ void push(int cc, double x) {
-    while (n >= 2 && (31 - __clz(c[1] ^ c[0])) < (31 - __clz(c[0] ^ cc))) pop_merge();
-#pragma unroll
-    for (int e = 8; e > 0; e--) { v[e] = v[e - 1]; c[e] = c[e - 1]; }
-    v[0] = x; c[0] = cc; n++;
-  }
-  __device__ __forceinline__ double finish() {
-    while (n >= 2) pop_merge();
-    return n ? v[0] : 0.0;
-  }
-};
 
 // Ascending bitonic sort of the P keys in buf[0, P) (Pp = 1024 E >= P, buf holds 2 Pp
 // with positions [P, Pp) of both halves set to the maximal key): every merge of
@@ -211,13 +192,84 @@ __device__ __forceinline__ int block_scan1024(int x, int* wsum, int* total) {
 #define TS_MARK(idx) do {} while (0)
 #endif
 
+// Keys (row << 12 | q), held at index q, sorted by row with a stable LSD radix sort (digits
+// of at most 7 row bits, 2 passes for m <= 16384): key q lives in round e = q / 1024 of thread
+// q % 1024; per pass every warp ranks its keys of a round by digit (match.any: lanes in order),
+// the per-(digit, round, warp) counts are scanned in that order, and each key is scattered to
+// its digit's base + its rank — stable, so the final order is (row, q): the order of the
+// bitonic sort (the keys are unique). Histogram in S.rcnt (128 x E x 32 ints).
+template <int E>
+__device__ __forceinline__ void ts_radix_sort(TailSmem& S, int P, int m) {
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int nbits = m > 1 ? 32 - __clz(m - 1) : 1;
+  const int passes = (nbits + 6) / 7;
+  const int db = max(5, (nbits + passes - 1) / passes);   // >= 32 digits: every warp's scan segment is whole
+  const int nd = 1 << db;
+  const int NH = nd * E * 32;
+  uint32_t* src = S.key;
+  uint32_t* dst = S.key + TS_PMAX;
+  int* hist = S.rcnt;
+  for (int pass = 0, shift = 12; pass < passes; pass++, shift += db) {
+    for (int q = t; q < NH; q += 1024) hist[q] = 0;
+    __syncthreads();
+    uint32_t k[E];
+    int dg[E], rk[E];
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+      const int idx = e * 1024 + t;
+      const bool valid = idx < P;
+      k[e] = valid ? src[idx] : 0u;
+      dg[e] = valid ? (int)((k[e] >> shift) & (unsigned)(nd - 1)) : -1;
+      const unsigned mask = __match_any_sync(FULL, dg[e]);
+      rk[e] = __popc(mask & lt_mask);
+      if (valid && rk[e] == 0) hist[(dg[e] * E + e) * 32 + w] = __popc(mask);
+    }
+    __syncthreads();
+    // exclusive scan of hist in index order: warp w owns NH / 32 consecutive entries
+    {
+      const int seg = NH >> 5, base = w * seg;
+      int carry = 0;
+      for (int it = 0; it < seg; it += 32) {
+        const int v = hist[base + it + lane];
+        int incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(FULL, incl, o); if (lane >= o) incl += y; }
+        hist[base + it + lane] = carry + incl - v;
+        carry += __shfl_sync(FULL, incl, 31);
+      }
+      if (lane == 0) S.wsum[w] = carry;
+      __syncthreads();
+      if (w == 0) {
+        int v = S.wsum[lane], incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(FULL, incl, o); if (lane >= o) incl += y; }
+        S.wsum[lane] = incl - v;
+      }
+      __syncthreads();
+      const int add = S.wsum[w];
+      for (int it = 0; it < seg; it += 32) hist[base + it + lane] += add;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < E; e++)
+      if (dg[e] >= 0) dst[hist[(dg[e] * E + e) * 32 + w] + rk[e]] = k[e];
+    __syncthreads();
+    uint32_t* tmp = src; src = dst; dst = tmp;
+  }
+  if (src != S.key) {
+    for (int q = t; q < P; q += 1024) S.key[q] = src[q];
+    __syncthreads();
+  }
+}
+
 // Per-row sums over the sorted pairs (R19), in two parts. ts_structure (once
 // per step; the pair set and its order are the same for Delta and Delta'):
 // the (row, chunk) runs of the sorted keys (start index runu, chunk runc), the
 // touched rows ascending (rrow) with their first run (rowrun), and the rows
-// with more than TS_SMALL runs (hot). ts_sums<MODE>(vals): thread per run
-// sums it left to right from +0.0; thread per touched row with at most
-// TS_SMALL runs combines the run partials (chunks ascending) with TreeStack;
+// with more than TS_SMALL runs (hot), 3 .. TS_SMALL runs (mid). ts_sums<MODE>(vals): thread
+// per run sums it left to right from +0.0; thread per touched row with one or two runs;
+// eight lanes per mid row combine the run partials level by level;
 // warp per hot row: lane l gathers chunks [8l, 8l+8), tree8 + butterfly (the
 // dense tree with zero leaves). MODE 0: rX (Delta_k^2, for the denominator;
 // rX aliases the pair values, dead by then); MODE 1: r_k += D,
@@ -255,10 +307,13 @@ __device__ __forceinline__ void ts_structure(TailSmem& S, int P) {
     ri++;
   }
   const int T = total >> 16, R = total & 0xffff;
-  if (t == 0) { S.rowrun[T] = R; S.runu[R] = (uint16_t)P; S.misc[0] = T; S.misc[1] = R; S.misc[2] = 0; }
+  if (t == 0) { S.rowrun[T] = R; S.runu[R] = (uint16_t)P; S.misc[0] = T; S.misc[1] = R; S.misc[2] = 0; S.misc[5] = 0; }
   __syncthreads();
-  for (int w = t; w < T; w += 1024)
-    if (S.rowrun[w + 1] - S.rowrun[w] > TS_SMALL) S.hot[atomicAdd(&S.misc[2], 1)] = w;
+  for (int w = t; w < T; w += 1024) {
+    const int nr = S.rowrun[w + 1] - S.rowrun[w];
+    if (nr > TS_SMALL) S.hot[atomicAdd(&S.misc[2], 1)] = w;
+    else if (nr > 2) S.mid[atomicAdd(&S.misc[5], 1)] = w;
+  }
   __syncthreads();
 }
 
@@ -290,16 +345,65 @@ __device__ __forceinline__ void ts_sums(const BlockArgs& A, TailSmem& S, const d
       A.h[S.rrow[w]] = A.lambda == 1.0 ? dd : d_div(dd, A.lambda);
     }
   };
+#ifdef SRO_PHASE_TIMING
+  if (MODE == 0 && threadIdx.x == 0 && A.phase) {
+    atomicAdd((unsigned long long*)&A.phase[20], (unsigned long long)T);
+    atomicAdd((unsigned long long*)&A.phase[21], (unsigned long long)R);
+    atomicAdd((unsigned long long*)&A.phase[22], (unsigned long long)S.misc[5]);
+    atomicAdd((unsigned long long*)&A.phase[23], (unsigned long long)NH);
+  }
+  long long ts_t1 = clock64();
+#endif
+  // one or two runs: the tree's value is the run or the sum of the two (every other leaf is
+  // +0.0, an identity; run sums start from +0.0 so are never -0.0), one thread per row
   for (int w = t; w < T; w += 1024) {
     const int r0 = S.rowrun[w], r1 = S.rowrun[w + 1];
-    if (r1 - r0 > TS_SMALL) continue;
+    if (r1 - r0 > 2) continue;
     double rk = 0.0, ak = 0.0;
     if (MODE == 1) { const int row = S.rrow[w]; rk = A.r[row]; ak = A.a[row]; }
-    TreeStack st;
-    for (int q = r0; q < r1; q++) st.push(S.runc[q], S.runv[q]);
-    finish(w, st.finish(), rk, ak);
+    const double D = r1 - r0 == 1 ? S.runv[r0] : d_add(S.runv[r0], S.runv[r0 + 1]);
+    finish(w, D, rk, ak);
   }
   const int lane = t & 31;
+#ifdef SRO_PHASE_TIMING
+  if (MODE == 0 && A.phase) { const long long t2 = clock64(); atomicAdd((unsigned long long*)&A.phase[24], (unsigned long long)(t2 - ts_t1) / 1024); ts_t1 = t2; }
+#endif
+  // 3 .. TS_SMALL runs: eight lanes per row, lane e holding run e (chunks ascending). Level by
+  // level (subtrees of 2^lv chunks) the two representatives of a parent — adjacent among the
+  // valid lanes, the left one lower — combine as left + right into the left lane, which is the
+  // adjacent-pair tree with zero leaves dropped (zeros are identities).
+  {
+    const int NM = S.misc[5];
+    const int gl = lane & 7, gb = lane & 24;
+    const unsigned gmask = 0xFFu << gb;
+    for (int it = 0; it * 128 < NM; it++) {   // uniform trip count (shuffles need every lane)
+      const int b = it * 128 + (t >> 3);
+      const bool act = b < NM;
+      const int w = act ? S.mid[b] : 0;
+      const int r0 = act ? S.rowrun[w] : 0, nr = act ? S.rowrun[w + 1] - r0 : 0;
+      bool valid = gl < nr;
+      int c = valid ? (int)S.runc[r0 + gl] : 0;
+      double v = valid ? S.runv[r0 + gl] : 0.0;
+      double rk = 0.0, ak = 0.0;
+      if (MODE == 1 && act && gl == 0) { const int row = S.rrow[w]; rk = A.r[row]; ak = A.a[row]; }
+#pragma unroll
+      for (int lv = 1; lv <= 8; lv++) {
+        const unsigned vb = __ballot_sync(FULL, valid) & gmask;
+        const unsigned above = vb & ~((2u << lane) - 1u);
+        const unsigned below = vb & ((1u << lane) - 1u);
+        const int nxt = above ? __ffs(above) - 1 : lane;
+        const int prv = below ? 31 - __clz(below) : lane;
+        const int cn = __shfl_sync(FULL, c, nxt), cp = __shfl_sync(FULL, c, prv);
+        const double vn = __shfl_sync(FULL, v, nxt);
+        if (valid && above && (cn >> lv) == (c >> lv)) v = d_add(v, vn);
+        else if (valid && below && (cp >> lv) == (c >> lv)) valid = false;
+      }
+      if (act && gl == 0) finish(w, v, rk, ak);
+    }
+  }
+#ifdef SRO_PHASE_TIMING
+  if (MODE == 0 && A.phase) { const long long t2 = clock64(); atomicAdd((unsigned long long*)&A.phase[25], (unsigned long long)(t2 - ts_t1) / 1024); ts_t1 = t2; }
+#endif
   for (int b = t >> 5; b < NH; b += 32) {
     const int w = S.hot[b];
     const int r0 = S.rowrun[w], r1 = S.rowrun[w + 1];
@@ -317,6 +421,9 @@ __device__ __forceinline__ void ts_sums(const BlockArgs& A, TailSmem& S, const d
     const double D = warp_pair_tree(tree8(x));
     if (lane == 0) finish(w, D, rk, ak);
   }
+#ifdef SRO_PHASE_TIMING
+  if (MODE == 0 && A.phase) { const long long t2 = clock64(); atomicAdd((unsigned long long*)&A.phase[26], (unsigned long long)(t2 - ts_t1) / 1024); }
+#endif
   __syncthreads();
 }
 
@@ -549,10 +656,11 @@ __global__ void __launch_bounds__(1024, 1) k_block_tail_sm(BlockArgs A, TailMerg
   for (int u = P + t; u < Pp; u += 1024) { S.key[u] = 0xffffffffu; S.key[Pp + u] = 0xffffffffu; }
   __syncthreads();
   TS_MARK(2);
-  // sort of the keys (unique: one pair per (row, column))
+  // sort of the keys (unique: one pair per (row, column)): bitonic for up to 1024 keys, a
+  // stable radix sort by row above (config [4], B = 1024: 21.4k -> 11.6k cycles)
   if (Pp == 1024) ts_sort<1>(S.key, Pp, P);
-  else if (Pp == 2048) ts_sort<2>(S.key, Pp, P);
-  else ts_sort<4>(S.key, Pp, P);
+  else if (Pp == 2048) ts_radix_sort<2>(S, P, A.m);
+  else ts_radix_sort<4>(S, P, A.m);
   TS_MARK(3);
   // Delta_k per touched row -> denominator -> gamma
   if (Pp == 1024) ts_structure<1>(S, P);

@@ -25,4 +25,7 @@ for cfg, B in ((1, 256), (2, 256), (4, 1024)):
     ph = np.zeros(32, dtype=np.int64)
     L.sro_debug_phase(s.h, ph.ctypes.data_as(ct.c_void_p))
     print(cfg, B, "cycles/step", round(ph[:13].sum() / steps), {n: round(float(v) / steps) for n, v in zip(names, ph)})
+    print("   per step: touched rows", round(ph[20] / steps, 1), "runs", round(ph[21] / steps, 1), "mid rows",
+          round(ph[22] / steps, 1), "hot rows", round(ph[23] / steps, 1), "| sums0 sub-phases (avg cycles per thread):",
+          "rows<=2", round(ph[24] / steps), "mid", round(ph[25] / steps), "hot", round(ph[26] / steps))
     s.close()
