@@ -460,21 +460,21 @@ __device__ __forceinline__ void dev_update_cols(const BlockArgs& A) {
 // ---------------------------------------------------------------------------
 // Kernels: one per phase (multi-CTA path) ...
 // ---------------------------------------------------------------------------
-__global__ void k_pairs_count(BlockArgs A) { if (!blk_skip(A)) dev_pairs_count(A); }
-__global__ void __launch_bounds__(1024) k_scan_pairs(BlockArgs A) {
+__global__ void k_pairs_count(BlockArgs A) { pdl_entry(); if (!blk_skip(A)) dev_pairs_count(A); }
+__global__ void __launch_bounds__(1024) k_scan_pairs(BlockArgs A) { pdl_entry();
   if (blk_skip(A)) return;
   dev_scan_excl(A.pcount, A.L, A.poff, A.ptotal);
 }
-__global__ void k_pairs_gen(BlockArgs A) { if (!blk_skip(A)) dev_pairs_gen(A); }
-__global__ void k_runs(BlockArgs A, const double* __restrict__ val) { if (!blk_skip(A)) dev_runs(A, val); }
-__global__ void __launch_bounds__(1024) k_touched_scan(BlockArgs A) { if (!blk_skip(A)) dev_touched_scan(A); }
+__global__ void k_pairs_gen(BlockArgs A) { pdl_entry(); if (!blk_skip(A)) dev_pairs_gen(A); }
+__global__ void k_runs(BlockArgs A, const double* __restrict__ val) { pdl_entry(); if (!blk_skip(A)) dev_runs(A, val); }
+__global__ void __launch_bounds__(1024) k_touched_scan(BlockArgs A) { pdl_entry(); if (!blk_skip(A)) dev_touched_scan(A); }
 template <int MODE>
 __global__ void __launch_bounds__(256) k_row_tree_small(BlockArgs A, double* slot, int clear, int pass) {
   if (!blk_skip(A)) dev_row_tree_small<MODE>(A, slot, clear != 0, pass);
 }
 // Warp per touched row over every touched row (the multi-CTA path: one launch).
 template <int MODE>
-__global__ void __launch_bounds__(256) k_row_tree_all(BlockArgs A, double* slot, int clear) {
+__global__ void __launch_bounds__(256) k_row_tree_all(BlockArgs A, double* slot, int clear) { pdl_entry();
   __shared__ double wsl[8 * 256];
   if (blk_skip(A)) return;
   for (int q = threadIdx.x; q < 8 * 256; q += blockDim.x) wsl[q] = 0.0;
@@ -489,14 +489,14 @@ __global__ void __launch_bounds__(256) k_row_tree_big(BlockArgs A, double* slot,
   __syncthreads();
   dev_row_tree_big<MODE>(A, slot, clear != 0, pass, wsl);
 }
-__global__ void k_gamma(BlockArgs A) { if (!blk_skip(A)) dev_gamma(A); }
-__global__ void k_cap_check(BlockArgs A) { if (!blk_skip(A)) dev_cap_check(A); }
-__global__ void k_update_cols(BlockArgs A) { if (!blk_skip(A)) dev_update_cols(A); }
+__global__ void k_gamma(BlockArgs A) { pdl_entry(); if (!blk_skip(A)) dev_gamma(A); }
+__global__ void k_cap_check(BlockArgs A) { pdl_entry(); if (!blk_skip(A)) dev_cap_check(A); }
+__global__ void k_update_cols(BlockArgs A) { pdl_entry(); if (!blk_skip(A)) dev_update_cols(A); }
 __global__ void k_zero_slot(BlockArgs A, double* slot) { if (!blk_skip(A)) dev_zero_dbl(slot, A.m); }
 
 // Step start: G_U = psumW(g) (FW: stop check, Alg. A.1 line 4) into *out,
 // touched-row count and capacity flag reset. One CTA of 256 threads.
-__global__ void __launch_bounds__(256) k_step_begin(BlockArgs A, double* out) {
+__global__ void __launch_bounds__(256) k_step_begin(BlockArgs A, double* out) { pdl_entry();
   if (A.stop && *A.stop) return;
   if (*A.status) return;
   if (threadIdx.x == 0) { *A.ntouch = 0; A.nbig[0] = 0; A.nbig[1] = 0; if (A.capfail) *A.capfail = 0; }
@@ -507,12 +507,12 @@ __global__ void __launch_bounds__(256) k_step_begin(BlockArgs A, double* out) {
 // sets *stop_flag = (total <= *eps).
 __global__ void __launch_bounds__(256) k_psum256(const double* __restrict__ x, int64_t L, double* out,
                                                  const double* __restrict__ eps, int* stop_flag,
-                                                 const int* __restrict__ stop_in) {
+                                                 const int* __restrict__ stop_in) { pdl_entry();
   if (stop_in && *stop_in) return;
   dev_psumW(x, L, 256, out, eps, stop_flag);
 }
 
-__global__ void k_step_done(BlockArgs A) {
+__global__ void k_step_done(BlockArgs A) { pdl_entry();
   if (!blk_skip(A) && threadIdx.x == 0) atomicAdd(A.dsteps, 1ULL);
   if (A.cur && threadIdx.x == 0) *A.cur += 1u;   // the step's last kernel advances the cursor
 }
@@ -559,7 +559,7 @@ __device__ __forceinline__ void dev_tail_rest(BlockArgs& A, double* tail_slots) 
   if (threadIdx.x == 0) atomicAdd(A.dsteps, 1ULL);
 }
 
-__global__ void __launch_bounds__(1024, 1) k_block_tail(BlockArgs A) {
+__global__ void __launch_bounds__(1024, 1) k_block_tail(BlockArgs A) { pdl_entry();
   extern __shared__ double tail_slots[];   // zero outside use
   blk_take_cursor(A);
   if (*A.status) return;

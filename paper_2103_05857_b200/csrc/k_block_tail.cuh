@@ -502,7 +502,7 @@ __device__ __forceinline__ void for_merged_reg(int c, const int* crow, const dou
   if (!ins) f(e_out++, j, 0.0);
 }
 
-__global__ void __launch_bounds__(1024, 1) k_block_tail_sm(BlockArgs A, TailMerge M) {
+__global__ void __launch_bounds__(1024, 1) k_block_tail_sm(BlockArgs A, TailMerge M) { pdl_entry();
   extern __shared__ __align__(16) unsigned char tail_raw[];
 #ifdef SRO_PHASE_TIMING
   long long ts_t = clock64();

@@ -114,7 +114,10 @@ struct SrcColour {
   const T* y;   // 3n
   static constexpr int SMEM_PER_ROW = 3 * sizeof(T);
   static constexpr bool PLANAR = false;
-  static constexpr int COLS = 4;   // columns a warp evaluates per loaded row (registers hold their y)
+#ifndef SRO_COLOUR_COLS
+#define SRO_COLOUR_COLS 4
+#endif
+  static constexpr int COLS = SRO_COLOUR_COLS;   // columns a warp evaluates per loaded row (registers hold their y)
   __device__ __forceinline__ static int hidx(int k, int) { return k; }
   __device__ __forceinline__ void stage(int row0, int rows, char* sm) const {
     T* xs = reinterpret_cast<T*>(sm);
@@ -219,7 +222,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_sweep(Src src, int m, int
                                                              const int* __restrict__ srow,
                                                              const double* __restrict__ sval, int cap,
                                                              const double* __restrict__ b, SweepOut out,
-                                                             const int* __restrict__ stop, int* status) {
+                                                             const int* __restrict__ stop, int* status) { pdl_entry();
   if (stop && *stop) return;
   extern __shared__ __align__(16) double sm_h[];
   const int nslabs = gridDim.y, slab = blockIdx.y;
@@ -294,7 +297,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_merge(Src src, int nslabs
                                                              const double* __restrict__ b, const int* __restrict__ pj,
                                                              const double* __restrict__ pmin, int* out_j,
                                                              double* out_min, double* out_g,
-                                                             const int* __restrict__ stop, int* status) {
+                                                             const int* __restrict__ stop, int* status) { pdl_entry();
   if (stop && *stop) return;
   const int col0 = col0_dev ? col0_dev[cur ? *cur : 0u] * col0_mul : col0_host;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -351,7 +354,7 @@ __global__ void __launch_bounds__(BULK_WARPS * 32, 1)
                      const int* __restrict__ col0_dev, const unsigned* __restrict__ cur, int col0_mul, int col0_host, int L,
                      const int* __restrict__ cnt, const int* __restrict__ srow, const double* __restrict__ sval,
                      int cap, const double* __restrict__ b, SweepOut out, const int* __restrict__ stop,
-                     int* status) {
+                     int* status) { pdl_entry();
   using V = typename Vec<T>::type;
   constexpr int W = Vec<T>::W;
   constexpr int CHV = BULK_CH / 16;   // vectors per stage

@@ -258,6 +258,29 @@ void resolve_timing(Solver* s) {
 
 thread_local std::string g_create_err;
 
+// Kernel launch with programmatic stream serialization (PDL, see pdl_entry in sro_device.cuh):
+// the kernel's CTAs may be scheduled while the previous kernel on the stream drains; each opens
+// with griddepcontrol.wait, so it still observes all of the previous kernel's writes. Inside CUDA
+// graph capture this becomes a programmatic edge. SRO_NO_PDL=1: ordinary launches (A/B).
+bool pdl_enabled() {
+  static const bool on = getenv("SRO_NO_PDL") == nullptr;
+  return on;
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // Per-(device, kernel) cache of the dynamic shared-memory attribute and of the
 // occupancy query: both are host API calls of several microseconds, and the
 // batched / FW loops launch kernels back to back.
@@ -657,16 +680,16 @@ sro_status sweep_bulk(Solver* s, Src src, const int* col0_dev, int col0_mul, int
   s->lead->stats.kernel_launches += (nslabs > 1 && !s->defer_merge) ? 2 : 1;
   s->lead->stats.sweep_launches += 1;
   s->lead->stats.sweep_columns += L;
-  kern<<<(int)nb, BULK_WARPS * 32, smem, s->stream>>>(src, s->m, slab, nslabs, s->h, col0_dev, s->sweep_cur, col0_mul, col0_host, L,
-                                                    s->cnt, s->srow, s->sval, s->cap, s->b, o, stop, s->status);
+  CUDA_TRY(s, launch_pdl(kern, dim3((int)nb), dim3(BULK_WARPS * 32), smem, s->stream, src, s->m, slab, nslabs, s->h, col0_dev, s->sweep_cur, col0_mul, col0_host, L,
+                                                    s->cnt, s->srow, s->sval, s->cap, s->b, o, stop, s->status));
   CUDA_TRY(s, cudaGetLastError());
   s->last_nslabs = nslabs;
   if (nslabs > 1 && !s->defer_merge) {
     int gm = (L + SWEEP_WARPS - 1) / SWEEP_WARPS;
     if (gm > s->num_sms * 8) gm = s->num_sms * 8;
-    k_lmo_merge<Src><<<gm, SWEEP_THREADS, 0, s->stream>>>(src, nslabs, s->h, col0_dev, s->sweep_cur, col0_mul, col0_host, L, s->cnt,
+    CUDA_TRY(s, launch_pdl(k_lmo_merge<Src>, dim3(gm), dim3(SWEEP_THREADS), 0, s->stream, src, nslabs, s->h, col0_dev, s->sweep_cur, col0_mul, col0_host, L, s->cnt,
                                                           s->srow, s->sval, s->cap, s->b, s->part_j, s->part_min,
-                                                          out_j, out_min, out_g, stop, s->status);
+                                                          out_j, out_min, out_g, stop, s->status));
     CUDA_TRY(s, cudaGetLastError());
   }
   timed_end(s, tr, CAT_SWEEP, L);
@@ -719,17 +742,17 @@ sro_status sweep(Solver* s, const int* col0_dev, int col0_mul, int col0_host, in
     s->lead->stats.kernel_launches += (nslabs > 1 && !s->defer_merge) ? 2 : 1;
     s->lead->stats.sweep_launches += 1;
     s->lead->stats.sweep_columns += L;
-    kern<<<dim3(gx, nslabs), SWEEP_THREADS, smem, s->stream>>>(src, s->m, slab, s->h, col0_dev, s->sweep_cur, col0_mul, col0_host, L,
+    CUDA_TRY(s, launch_pdl(kern, dim3(dim3(gx, nslabs)), dim3(SWEEP_THREADS), smem, s->stream, src, s->m, slab, s->h, col0_dev, s->sweep_cur, col0_mul, col0_host, L,
                                                              s->cnt, s->srow, s->sval, s->cap, s->b, o, stop,
-                                                             s->status);
+                                                             s->status));
     CUDA_TRY(s, cudaGetLastError());
     s->last_nslabs = nslabs;
     if (nslabs > 1 && !s->defer_merge) {
       int gm = (L + SWEEP_WARPS - 1) / SWEEP_WARPS;
       if (gm > s->num_sms * 8) gm = s->num_sms * 8;
-      k_lmo_merge<Src><<<gm, SWEEP_THREADS, 0, s->stream>>>(src, nslabs, s->h, col0_dev, s->sweep_cur, col0_mul, col0_host, L,
+      CUDA_TRY(s, launch_pdl(k_lmo_merge<Src>, dim3(gm), dim3(SWEEP_THREADS), 0, s->stream, src, nslabs, s->h, col0_dev, s->sweep_cur, col0_mul, col0_host, L,
                                                             s->cnt, s->srow, s->sval, s->cap, s->b, s->part_j,
-                                                            s->part_min, out_j, out_min, out_g, stop, s->status);
+                                                            s->part_min, out_j, out_min, out_g, stop, s->status));
       CUDA_TRY(s, cudaGetLastError());
     }
     timed_end(s, tr, CAT_SWEEP, L);
@@ -1324,12 +1347,12 @@ sro_status plain_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
     M.kind = dense ? (f32 ? 0 : 1) : (f32 ? (eu ? 3 : 2) : (eu ? 5 : 4));
     M.C = s->C; M.ld = s->ld; M.x = s->x; M.y = s->y;
     CUDA_TRY(s, set_dyn_smem((const void*)k_block_tail_sm, s->device, (int)TAIL_SM_BYTES));
-    k_block_tail_sm<<<1, 1024, TAIL_SM_BYTES, s->stream>>>(A, M);
+    CUDA_TRY(s, launch_pdl(k_block_tail_sm, dim3(1), dim3(1024), TAIL_SM_BYTES, s->stream, A, M));
     CUDA_TRY(s, cudaGetLastError());
     s->lead->stats.kernel_launches += 1;
   } else if (L <= 1024 && !s->no_tail) {
     CUDA_TRY(s, set_dyn_smem((const void*)k_block_tail, s->device, TAIL_SMEM));
-    k_block_tail<<<1, 1024, TAIL_SMEM, s->stream>>>(A);
+    CUDA_TRY(s, launch_pdl(k_block_tail, dim3(1), dim3(1024), TAIL_SMEM, s->stream, A));
     CUDA_TRY(s, cudaGetLastError());
     s->lead->stats.kernel_launches += 1;
   } else if (!s->no_coop) {
@@ -1348,20 +1371,20 @@ sro_status plain_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
     int gL = (L + tpb - 1) / tpb; if (gL > s->num_sms * 8) gL = s->num_sms * 8;
     const int gP = s->num_sms * 8;
     const int gR = (s->m + 7) / 8 < s->num_sms * 8 ? (s->m + 7) / 8 : s->num_sms * 8;
-    k_step_begin<<<1, 256, 0, s->stream>>>(A, s->scal + 0);
-    k_pairs_count<<<gL, tpb, 0, s->stream>>>(A);
-    k_scan_pairs<<<1, 1024, 0, s->stream>>>(A);
-    k_pairs_gen<<<gL, tpb, 0, s->stream>>>(A);
-    k_touched_scan<<<1, 1024, 0, s->stream>>>(A);
-    k_runs<<<gP, tpb, 0, s->stream>>>(A, s->pd);
-    k_row_tree_all<0><<<gR, 256, 0, s->stream>>>(A, nullptr, 0);
-    k_psum256<<<1, 256, 0, s->stream>>>(s->X, s->m, s->scal + 1, nullptr, nullptr, stop);
-    k_gamma<<<1, 32, 0, s->stream>>>(A);
-    k_cap_check<<<gL, tpb, 0, s->stream>>>(A);
-    k_update_cols<<<gL, tpb, 0, s->stream>>>(A);
-    k_runs<<<gP, tpb, 0, s->stream>>>(A, s->pdelta);
-    k_row_tree_all<1><<<gR, 256, 0, s->stream>>>(A, nullptr, 1);
-    k_step_done<<<1, 32, 0, s->stream>>>(A);
+    CUDA_TRY(s, launch_pdl(k_step_begin, dim3(1), dim3(256), 0, s->stream, A, s->scal + 0));
+    CUDA_TRY(s, launch_pdl(k_pairs_count, dim3(gL), dim3(tpb), 0, s->stream, A));
+    CUDA_TRY(s, launch_pdl(k_scan_pairs, dim3(1), dim3(1024), 0, s->stream, A));
+    CUDA_TRY(s, launch_pdl(k_pairs_gen, dim3(gL), dim3(tpb), 0, s->stream, A));
+    CUDA_TRY(s, launch_pdl(k_touched_scan, dim3(1), dim3(1024), 0, s->stream, A));
+    CUDA_TRY(s, launch_pdl(k_runs, dim3(gP), dim3(tpb), 0, s->stream, A, s->pd));
+    CUDA_TRY(s, launch_pdl(k_row_tree_all<0>, dim3(gR), dim3(256), 0, s->stream, A, nullptr, 0));
+    CUDA_TRY(s, launch_pdl(k_psum256, dim3(1), dim3(256), 0, s->stream, s->X, s->m, s->scal + 1, nullptr, nullptr, stop));
+    CUDA_TRY(s, launch_pdl(k_gamma, dim3(1), dim3(32), 0, s->stream, A));
+    CUDA_TRY(s, launch_pdl(k_cap_check, dim3(gL), dim3(tpb), 0, s->stream, A));
+    CUDA_TRY(s, launch_pdl(k_update_cols, dim3(gL), dim3(tpb), 0, s->stream, A));
+    CUDA_TRY(s, launch_pdl(k_runs, dim3(gP), dim3(tpb), 0, s->stream, A, s->pdelta));
+    CUDA_TRY(s, launch_pdl(k_row_tree_all<1>, dim3(gR), dim3(256), 0, s->stream, A, nullptr, 1));
+    CUDA_TRY(s, launch_pdl(k_step_done, dim3(1), dim3(32), 0, s->stream, A));
     CUDA_TRY(s, cudaGetLastError());
     s->lead->stats.kernel_launches += 14;
   }

@@ -14,6 +14,16 @@ namespace sro {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr uint64_t GOLDEN = 0x9E3779B97F4A7C15ULL;
 
+// Programmatic dependent launch (PDL): a kernel launched with programmatic stream serialization
+// may start while its predecessor finishes; griddepcontrol.wait blocks until the predecessor
+// grid has completed and its memory is visible (a no-op without PDL), and launch_dependents
+// lets the next kernel's CTAs be scheduled early (they in turn wait). Every kernel of the block
+// step / sweep chain opens with both, so only launch latency overlaps, never data.
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ double d_add(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double d_sub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double d_mul(double a, double b) { return __dmul_rn(a, b); }
