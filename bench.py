@@ -144,6 +144,7 @@ class StepRunner:
             st.wait_event(ready)
         self.solvers = [sro.Solver(d["a"], d["b"], 1.0, C=Cd, prec="f32", device=dev.index, stream=st.cuda_stream,
                                    ld=M) for st in self.streams]
+        self.ga_steps = 0   # GA steps run (the roofline's traffic weighting)
 
     def run(self, entries_acc, ttg):
         """Enqueue the step after the current stream's pending work; returns after it completes.
@@ -203,21 +204,25 @@ class StepRunner:
             print(json.dumps({PLAN[q][0]: (round(e0.elapsed_time(evs[q][0]), 2), round(e0.elapsed_time(evs[q][1]), 2),
                                            round(results[q]["device_ms"], 2)) for q in range(len(PLAN))}),
                   file=sys.stderr, flush=True)
-        for (name, _, _, cap), r in zip(PLAN, results):
+        for (name, _, opts, cap), r in zip(PLAN, results):
             if not r["converged"]:
                 raise RuntimeError(f"{name} did not reach g <= {EPS} within {cap} iterations (gap {r['gap']})")
             entries_acc.append(r["entries_read"])
             ttg[name] = ttg.get(name, []) + [r["device_ms"]]
+            if opts.get("sampling") == 2:
+                self.ga_steps += r["iters_done"]
         return e0.elapsed_time(e1)
 
     def objective(self):
         return [s.objective() for s in self.solvers]
 
     def stats(self, reset=False):
-        tot = {}
+        tot = {"ga_steps": self.ga_steps}
         for s in self.solvers:
             for k, v in s.stats(reset).items():
                 tot[k] = tot.get(k, 0) + v
+        if reset:
+            self.ga_steps = 0
         return tot
 
     def set_timing(self, on):
@@ -369,13 +374,22 @@ def roofline_from_stats(stats, peaks):
            "algorithmic_bytes_per_launch": bytes_ / launches, "time_share": shares,
            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, of measured)"}
     if dom == "bcfw" and stats["bcfw_steps"]:
-        # the sequential family is bound by the latency of one dependent step, not by HBM:
-        # DRAM traffic per launch = algorithmic bytes (profiles/r01_ncu_bcfw_rf.md)
+        # the sequential family is bound by the latency of one dependent step, not by HBM.
+        # traffic: DRAM bytes per step of each kernel from this build's ncu captures
+        # (profiles/r02_ncu_traffic.json), weighted by the steps each kernel ran in the timed region
         us = t_ms * 1e3 / stats["bcfw_steps"]
-        out["traffic"] = round((68.409856e6 + 1.813504e6) / 4096 * (bytes_ / launches) / (M * 4.0), 1)
-        out["traffic_source"] = ("ncu --set full dram__bytes_read+write per 4096-step launch: k_bcfw_ga_pipe "
-                                 "68.44+1.75 MB (profiles/r01_ncu_ga_pipe.md), k_bcfw_pipe 68.41+1.81 MB "
-                                 "(profiles/r01_ncu_bcfw_pipe.md)")
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")))
+            per = {k: (tr[k]["dram_bytes_read"] + tr[k]["dram_bytes_write"]) / tr[k]["steps"]
+                   for k in ("k_bcfw_ga_pipe", "k_bcfw_pipe")}
+            ga_steps = min(stats["bcfw_steps"], stats.get("ga_steps", 0))
+            tot = ga_steps * per["k_bcfw_ga_pipe"] + (stats["bcfw_steps"] - ga_steps) * per["k_bcfw_pipe"]
+            out["traffic"] = round(tot / launches, 1)
+            out["traffic_source"] = ("ncu --set full dram__bytes_read+write per step (profiles/r02_ncu_traffic.json): "
+                                     f"k_bcfw_ga_pipe {per['k_bcfw_ga_pipe']:.0f} B, k_bcfw_pipe {per['k_bcfw_pipe']:.0f} B, "
+                                     f"weighted by the timed region's steps ({ga_steps} GA of {stats['bcfw_steps']})")
+        except (OSError, KeyError, ValueError):
+            out["traffic"] = None
         out["step_latency"] = {"us_per_step": round(us, 4), "cycles_per_step_at_1965MHz": round(us * 1965.0, 1),
                                "single_cta_floor_cycles": 420,
                                "floor_source": "profiles/r01_lmo_microbench.log: register LMO + REDUX argmin + 2 barriers"}
@@ -446,13 +460,25 @@ def configs_legs_single(local_rank):
         s.close()
         sweep_ms = st["sweep_ms"] / max(1, st["sweep_launches"])
         ent = float(d["m"]) * d["n"]
+        # the fused colour sweep is bound by instruction issue, not memory: 16 SASS instructions
+        # per (row, column) entry in its inner loop (k_lmo_sweep<SrcColour<float>, 4>, 128 per
+        # 2 rows x 4 columns: 8 fp32 ops, F2F, DADD, DSETP, 2.75 selects, 1 LDS), one issue per
+        # cycle per SM sub-partition
+        import torch
+        sms = torch.cuda.get_device_properties(local_rank).multi_processor_count
+        mhz = float(measured_peaks().get("sm_max_mhz", 1965.0))
+        issue_peak = sms * 4 * mhz * 1e6 * 32 / 16.0
         out[f"config{cfg}"] = {
             "workload": f"BASELINE configs[{cfg}]: m={d['m']}, n={d['n']}, fused fp32 sqeuclid, batched B={B}, P, ELS",
             "time_to_gap_ms": round(r["device_ms"], 3), "block_steps": r["iters_done"],
             "converged": bool(r["converged"]), "gap": r["gap"], "us_per_block_step": round(
                 1e3 * r["device_ms"] / max(1, r["iters_done"]), 2),
             "entries_per_s": r["entries_read"] / (r["device_ms"] * 1e-3),
-            "gap_sweep_ms": round(sweep_ms, 4), "gap_sweep_entries_per_s": ent / (sweep_ms * 1e-3)}
+            "gap_sweep_ms": round(sweep_ms, 4), "gap_sweep_entries_per_s": ent / (sweep_ms * 1e-3),
+            "gap_sweep_roofline": {"bound": "alu", "achieved": ent / (sweep_ms * 1e-3), "peak": issue_peak,
+                                   "unit": "entries/s", "frac": round(ent / (sweep_ms * 1e-3) / issue_peak, 4),
+                                   "peak_derivation": f"{sms} SMs x 4 sub-partitions x {mhz:.0f} MHz x 32 lanes / "
+                                                      "16 instructions per entry (SASS of the inner loop)"}}
     return out
 
 

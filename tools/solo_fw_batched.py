@@ -1,5 +1,5 @@
 """FW-ELS on config [1] and [3] and batched on [1]/[2]/[4] to g <= 1e-6, alone, warm (probe):
-device ms per solve and per iteration (SRO_NO_PDL=1 for the A/B without programmatic launches)."""
+device ms per solve and per iteration (SRO_PDL=1 for the A/B with programmatic dependent launches)."""
 import json
 import os
 import sys
@@ -28,7 +28,7 @@ for r in runs:
             res = s.solve(sro.SRO_BATCHED, 400 * (d["n"] // B), epsilon=1e-6, step=sro.STEP_ELS,
                           sampling=sro.SAMPLE_P, block_size=B, seed=1)
         out.append(res["device_ms"])
-    print(json.dumps(dict(run=r, pdl=os.environ.get("SRO_NO_PDL") is None, iters=res["iters_done"],
+    print(json.dumps(dict(run=r, pdl=os.environ.get("SRO_PDL") is not None, iters=res["iters_done"],
                           ms=[round(x, 2) for x in out], us_per_iter=round(1e3 * min(out) / res["iters_done"], 2))),
           flush=True)
     s.close()
