@@ -515,43 +515,68 @@ __global__ void __launch_bounds__(1024, 1) k_block_tail_sm(BlockArgs A, TailMerg
     __device__ ~Flush() { if (threadIdx.x == 0 && A.phase) for (int q = 0; q < 16; q++) A.phase[q] += S.tsacc[q]; }
   } ts_flush{A, S};
 #endif
-  blk_take_cursor(A);
-  if (*A.status || (A.stop && *A.stop)) return;
-  TS_MARK(12);
   const int t = threadIdx.x, L = A.L, cap = A.cap;
-  const int col0 = block_col0(A);
-  const int i = col0 + t;
   const bool own = t < L;
-  // Per-column state of column i = col0 + t in registers, loaded in one round
-  // trip: support size, its first KP entries (read whether or not they are in
-  // use), b_i, and the sweep's j / g when it merged its slabs itself.
   constexpr int KP = 4;
+  static_assert(KP == SW_KP, "staged support width");
+  // Every load that does not depend on the step cursor is issued here, together: the cursor,
+  // the status / stop words, the supports the sweep staged (all KP entries, used or not: the
+  // buffers hold 1024 x KP) and the first round of slab partials. Before, each came after the
+  // previous one's round trip (cursor -> status -> column index -> supports -> partials).
+  const unsigned cur0 = A.cur ? *A.cur : 0u;
+  const int status0 = *A.status;
+  const int stop0 = A.stop ? *A.stop : 0;
+  const bool staged = M.nslabs > 1 && M.st_cnt;
   int c = 0, j = 0;
   int crow[KP];
   double cval[KP];
   double bi = 0.0, gcol = 0.0;
 #pragma unroll
   for (int e = 0; e < KP; e++) { crow[e] = 0; cval[e] = 0.0; }
-  static_assert(KP == SW_KP, "staged support width");
-  if (own) {
-    if (M.nslabs > 1 && M.st_cnt) {   // staged by the sweep: coalesced reads
-      c = M.st_cnt[t];
-      bi = M.st_b[t];
-      crow[0] = M.st_row[t];
-      cval[0] = M.st_val[t];
+  if (own && staged) {   // staged by the sweep: coalesced reads, independent of the column index
+    c = M.st_cnt[t];
+    bi = M.st_b[t];
 #pragma unroll
-      for (int e = 1; e < KP; e++)
-        if (e < c) { crow[e] = M.st_row[e * L + t]; cval[e] = M.st_val[e * L + t]; }
-    } else {
-      c = A.cnt[i];
-      bi = A.b[i];
-      crow[0] = A.srow[(int64_t)i * cap];   // read even when c == 0 (b_i = 0): unused then
-      cval[0] = A.sval[(int64_t)i * cap];
-      if (M.nslabs <= 1) { j = A.j[t]; gcol = A.g[t]; }
+    for (int e = 0; e < KP; e++) { crow[e] = M.st_row[e * L + t]; cval[e] = M.st_val[e * L + t]; }
+  }
+  const int R = M.nslabs > 1 ? 1024 / L : 1;
+  const int mp = t % L, mr = t / L;
+  double pv[8];
+  int pjv[8];
+  if (M.nslabs > 1 && t < R * L) {
 #pragma unroll
-      for (int e = 1; e < KP; e++)
-        if (e < c) { crow[e] = A.srow[(int64_t)i * cap + e]; cval[e] = A.sval[(int64_t)i * cap + e]; }
+    for (int u = 0; u < 8; u++) {
+      const int q = mr + u * R;
+      const bool in = q < M.nslabs;
+      pv[u] = in ? M.pmin[(int64_t)q * L + mp] : __longlong_as_double(0x7ff0000000000000LL);
+      pjv[u] = in ? M.pj[(int64_t)q * L + mp] : 0x7fffffff;
     }
+  }
+  // take the step cursor (blk_take_cursor with the value loaded above)
+  if (A.cur) {
+    A.kk += (long long)cur0;
+    if (A.trace) A.trace += 9 * (int64_t)cur0;
+    if (A.col0_dev) A.col0_dev += cur0;
+  }
+  __syncthreads();
+  if (t == 0 && A.cur) *A.cur = cur0 + 1u;
+  A.cur = nullptr;
+  if (status0 || stop0) return;
+  TS_MARK(12);
+  const int col0 = block_col0(A);
+  const int i = col0 + t;
+  // Per-column state of column i = col0 + t not staged by the sweep: support size, its first KP
+  // entries (read whether or not they are in use), b_i, and the sweep's j / g when it merged its
+  // slabs itself.
+  if (own && !staged) {
+    c = A.cnt[i];
+    bi = A.b[i];
+    crow[0] = A.srow[(int64_t)i * cap];   // read even when c == 0 (b_i = 0): unused then
+    cval[0] = A.sval[(int64_t)i * cap];
+    if (M.nslabs <= 1) { j = A.j[t]; gcol = A.g[t]; }
+#pragma unroll
+    for (int e = 1; e < KP; e++)
+      if (e < c) { crow[e] = A.srow[(int64_t)i * cap + e]; cval[e] = A.sval[(int64_t)i * cap + e]; }
   }
   if (t == 0) S.misc[3] = 0;
   if (M.nslabs > 1) {
@@ -560,22 +585,20 @@ __global__ void __launch_bounds__(1024, 1) k_block_tail_sm(BlockArgs A, TailMerg
     // a strided subset of the slabs (8 loads in flight), then one combines the R
     // results and evaluates the column gap (Eq. 11)
     // g_i = sum_{k in supp, ascending} t_ki (C_ki + h_k) - b_i min_k (C_ki + h_k).
-    const int R = 1024 / L;
     double* mv = S.pd;   // free until the pairs are generated
     int* mj = S.prow;
     if (t < R * L) {
-      const int p = t % L, r = t / L;
       double best = __longlong_as_double(0x7ff0000000000000LL);
       int bj = 0x7fffffff;
-      for (int q0 = r; q0 < M.nslabs; q0 += 8 * R) {
-        double pv[8];
-        int pjv[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) argmin_merge(best, bj, pv[u], pjv[u]);   // the round loaded at entry
+      for (int q0 = mr + 8 * R; q0 < M.nslabs; q0 += 8 * R) {
 #pragma unroll
         for (int u = 0; u < 8; u++) {
           const int q = q0 + u * R;
           const bool in = q < M.nslabs;
-          pv[u] = in ? M.pmin[(int64_t)q * L + p] : __longlong_as_double(0x7ff0000000000000LL);
-          pjv[u] = in ? M.pj[(int64_t)q * L + p] : 0x7fffffff;
+          pv[u] = in ? M.pmin[(int64_t)q * L + mp] : __longlong_as_double(0x7ff0000000000000LL);
+          pjv[u] = in ? M.pj[(int64_t)q * L + mp] : 0x7fffffff;
         }
 #pragma unroll
         for (int u = 0; u < 8; u++) argmin_merge(best, bj, pv[u], pjv[u]);

@@ -709,14 +709,15 @@ sro_status sweep(Solver* s, const int* col0_dev, int col0_mul, int col0_host, in
     }
     int slab = s->slab_rows;
     // several columns per warp when there are enough columns to fill the GPU that
-    // way; a block with few columns (batched) splits the rows into more, shorter
-    // slabs instead, so that about two CTAs per SM still get work
-    bool multi = Src::COLS > 1 && (int64_t)L * ((s->m + slab - 1) / slab) >=
-                                      (int64_t)s->num_sms * SWEEP_WARPS * Src::COLS * 2;
+    // way; a block with few columns (batched) keeps one column per warp and splits the rows
+    // into shorter slabs instead, sized for about four CTAs per SM (measured against four
+    // columns per warp over two-CTA-per-SM slabs: config [2] block step 35.4 -> 32.6 us, [4]
+    // 43.8 -> 41.8 — fewer slab partials for the tail to read, more warps in flight)
+    const bool multi = Src::COLS > 1 && (int64_t)L * ((s->m + slab - 1) / slab) >=
+                                            (int64_t)s->num_sms * SWEEP_WARPS * Src::COLS * 2;
     if (Src::COLS > 1 && !multi && !getenv_slab_fixed()) {
-      multi = true;
-      const int64_t per_slab = (L + SWEEP_WARPS * Src::COLS - 1) / (SWEEP_WARPS * Src::COLS);
-      const int64_t want = std::max<int64_t>(1, (int64_t)s->num_sms * 2 / per_slab);
+      const int64_t per_slab = (L + SWEEP_WARPS - 1) / SWEEP_WARPS;
+      const int64_t want = std::max<int64_t>(1, (int64_t)s->num_sms * 4 / per_slab);
       int64_t rows_want = (s->m + want - 1) / want;
       rows_want = (rows_want + 31) / 32 * 32;
       if (rows_want < 128) rows_want = 128;
