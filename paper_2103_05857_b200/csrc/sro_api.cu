@@ -657,7 +657,12 @@ sro_status sweep_bulk(Solver* s, Src src, const int* col0_dev, int col0_mul, int
   // columns (a batched block) so that every SM still gets several items
   int slab = s->slab_bulk;
   {
-    const int64_t target = (int64_t)s->num_sms * BULK_WARPS * 2;
+    // about one (slab, column) item per two warps of the grid: fewer, longer slabs leave fewer
+    // partials for a block step's single-CTA tail (batched config [1], B = 256: 35.3 us per block
+    // step at two items per warp, 34.5 at one, 33.7 at a half, 35.3 at 0.35, 37.5 at a quarter;
+    // SRO_BULK_ITEMS overrides for A/B)
+    static const double items_per_warp = getenv("SRO_BULK_ITEMS") ? atof(getenv("SRO_BULK_ITEMS")) : 0.5;
+    const int64_t target = (int64_t)((double)s->num_sms * BULK_WARPS * items_per_warp);
     const int64_t want = ((int64_t)s->m * L + target - 1) / target;
     if (want < slab) slab = (int)std::max<int64_t>(256, (want + 3) / 4 * 4);
   }
