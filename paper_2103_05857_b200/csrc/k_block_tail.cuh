@@ -44,6 +44,7 @@ struct TailMerge {
   const int* st_row;
   const double* st_val;
   const double* st_b;
+  const double* st_term;   // the staged gap terms (k_sweep.cuh stage_terms), or nullptr
 };
 __device__ __forceinline__ double tm_cost(const TailMerge& M, int k, int i) {
   switch (M.kind) {
@@ -533,11 +534,16 @@ __global__ void __launch_bounds__(1024, 1) k_block_tail_sm(BlockArgs A, TailMerg
   double bi = 0.0, gcol = 0.0;
 #pragma unroll
   for (int e = 0; e < KP; e++) { crow[e] = 0; cval[e] = 0.0; }
+  double stt[KP];
   if (own && staged) {   // staged by the sweep: coalesced reads, independent of the column index
     c = M.st_cnt[t];
     bi = M.st_b[t];
 #pragma unroll
-    for (int e = 0; e < KP; e++) { crow[e] = M.st_row[e * L + t]; cval[e] = M.st_val[e * L + t]; }
+    for (int e = 0; e < KP; e++) {
+      crow[e] = M.st_row[e * L + t];
+      cval[e] = M.st_val[e * L + t];
+      stt[e] = M.st_term ? M.st_term[e * L + t] : 0.0;
+    }
   }
   const int R = M.nslabs > 1 ? 1024 / L : 1;
   const int mp = t % L, mr = t / L;
@@ -614,7 +620,11 @@ __global__ void __launch_bounds__(1024, 1) k_block_tail_sm(BlockArgs A, TailMerg
       for (int r = 1; r < R; r++) argmin_merge(best, bj, mv[r * L + t], mj[r * L + t]);
       if (!(best < 1.0e308 && best > -1.0e308)) { set_status(A.status, 5); S.misc[3] = 1; }
       double dot = 0.0;
-      if (c <= KP) {
+      if (c <= KP && staged && M.st_term) {   // the sweep's slab warps staged t_ki (C_ki + h_k)
+#pragma unroll
+        for (int e = 0; e < KP; e++)
+          if (e < c) dot = d_add(dot, stt[e]);
+      } else if (c <= KP) {
         double term[KP];
 #pragma unroll
         for (int e = 0; e < KP; e++)

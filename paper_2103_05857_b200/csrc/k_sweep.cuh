@@ -200,6 +200,9 @@ struct SweepOut {
   int* st_row;
   double* st_val;
   double* st_b;
+  // ... and every slab's warps the gap terms t_ki (C_ki + h_k) of the first SW_KP support
+  // entries whose rows lie in their slab ([e * L + p]; the tail's dot is their sum in e order)
+  double* st_term;
 };
 __device__ __forceinline__ void stage_support(const SweepOut& out, int p, int i, int L, const int* __restrict__ cnt,
                                               const int* __restrict__ srow, const double* __restrict__ sval, int cap,
@@ -210,6 +213,20 @@ __device__ __forceinline__ void stage_support(const SweepOut& out, int p, int i,
   if (lane < SW_KP && lane < c) {
     out.st_row[lane * L + p] = srow[(int64_t)i * cap + lane];
     out.st_val[lane * L + p] = sval[(int64_t)i * cap + lane];
+  }
+}
+
+template <class Src>
+__device__ __forceinline__ void stage_terms(const Src& src, const SweepOut& out, int p, int i, int L, int row0,
+                                            int rows, const int* __restrict__ cnt, const int* __restrict__ srow,
+                                            const double* __restrict__ sval, int cap,
+                                            const double* __restrict__ h) {
+  const int lane = threadIdx.x & 31;
+  const int c = cnt[i];
+  if (lane < SW_KP && lane < c) {
+    const int k = srow[(int64_t)i * cap + lane];
+    if (k >= row0 && k < row0 + rows)
+      out.st_term[lane * L + p] = d_mul(sval[(int64_t)i * cap + lane], d_add(src.cost(k, i), h[k]));
   }
 }
 
@@ -261,6 +278,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_sweep(Src src, int m, int
             out.minval[(int64_t)slab * L + p] = bv;
           }
           if (out.st_cnt && slab == 0) stage_support(out, p, i, L, cnt, srow, sval, cap, b);
+          if (out.st_term) stage_terms(src, out, p, i, L, row0, rows, cnt, srow, sval, cap, h);
         }
       }
     }
@@ -282,6 +300,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_sweep(Src src, int m, int
         out.minval[(int64_t)slab * L + p] = best;
       }
       if (out.st_cnt && slab == 0) stage_support(out, p, i, L, cnt, srow, sval, cap, b);
+      if (out.st_term) stage_terms(src, out, p, i, L, row0, rows, cnt, srow, sval, cap, h);
     }
   }
 }
@@ -437,6 +456,7 @@ __global__ void __launch_bounds__(BULK_WARPS * 32, 1)
           out.minval[(int64_t)slab * L + p] = best;
         }
         if (out.st_cnt && slab == 0) stage_support(out, p, i, L, cnt, srow, sval, cap, b);
+        if (out.st_term) stage_terms(src, out, p, i, L, row0, rows, cnt, srow, sval, cap, h);
       }
     }
     seg = seg_end;

@@ -141,6 +141,7 @@ struct Solver {
   int* st_row = nullptr;
   double* st_val = nullptr;
   double* st_b = nullptr;
+  double* st_term = nullptr;
   double* ga_blk = nullptr;   // sharded GA: the visited block's gathered column gaps (lead)
   int ga_blk_cap = 0;
   const unsigned* sweep_cur = nullptr;   // the next sweep's block index is col0_dev[*sweep_cur]
@@ -683,7 +684,7 @@ sro_status sweep_bulk(Solver* s, Src src, const int* col0_dev, int col0_mul, int
   SweepOut o{};
   if (nslabs == 1) { o.j = out_j; o.minval = out_min; o.g = out_g; }
   else { o.j = s->part_j; o.minval = s->part_min; o.g = nullptr; }
-  if (nslabs > 1 && s->defer_merge && s->st_cnt) { o.st_cnt = s->st_cnt; o.st_row = s->st_row; o.st_val = s->st_val; o.st_b = s->st_b; }
+  if (nslabs > 1 && s->defer_merge && s->st_cnt) { o.st_cnt = s->st_cnt; o.st_row = s->st_row; o.st_val = s->st_val; o.st_b = s->st_b; o.st_term = s->st_term; }
   const int tr = timed_begin(s);
   s->lead->stats.kernel_launches += (nslabs > 1 && !s->defer_merge) ? 2 : 1;
   s->lead->stats.sweep_launches += 1;
@@ -746,7 +747,7 @@ sro_status sweep(Solver* s, const int* col0_dev, int col0_mul, int col0_host, in
     SweepOut o{};
     if (nslabs == 1) { o.j = out_j; o.minval = out_min; o.g = out_g; }
     else { o.j = s->part_j; o.minval = s->part_min; o.g = nullptr; }
-    if (nslabs > 1 && s->defer_merge && s->st_cnt) { o.st_cnt = s->st_cnt; o.st_row = s->st_row; o.st_val = s->st_val; o.st_b = s->st_b; }
+    if (nslabs > 1 && s->defer_merge && s->st_cnt) { o.st_cnt = s->st_cnt; o.st_row = s->st_row; o.st_val = s->st_val; o.st_b = s->st_b; o.st_term = s->st_term; }
     const int tr = timed_begin(s);
     s->lead->stats.kernel_launches += (nslabs > 1 && !s->defer_merge) ? 2 : 1;
     s->lead->stats.sweep_launches += 1;
@@ -1337,6 +1338,7 @@ sro_status plain_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
     CUDA_TRY(s, salloc(&s->st_row, 1024 * SW_KP, s->stream));
     CUDA_TRY(s, salloc(&s->st_val, 1024 * SW_KP, s->stream));
     CUDA_TRY(s, salloc(&s->st_b, 1024, s->stream));
+    CUDA_TRY(s, salloc(&s->st_term, 1024 * SW_KP, s->stream));
   }
   s->defer_merge = smtail;
   s->sweep_cur = cur;
@@ -1349,7 +1351,7 @@ sro_status plain_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
     // pairs resident in shared memory (k_block_tail.cuh); the sweep's slab merge folded in
     TailMerge M{};
     M.nslabs = s->last_nslabs; M.pj = s->part_j; M.pmin = s->part_min;
-    M.st_cnt = s->st_cnt; M.st_row = s->st_row; M.st_val = s->st_val; M.st_b = s->st_b;
+    M.st_cnt = s->st_cnt; M.st_row = s->st_row; M.st_val = s->st_val; M.st_b = s->st_b; M.st_term = s->st_term;
     M.j = s->sw_j; M.minval = s->sw_min; M.g = s->sw_g;
     const bool dense = s->kind == SRO_COST_DENSE || s->kind == SRO_COST_HASH_UNIFORM;
     const bool f32 = s->prec == SRO_FP32, eu = s->kind == SRO_COST_EUCLID;
@@ -1554,7 +1556,7 @@ void free_shard(Solver* s) {
   // handles neither maps new memory nor synchronises the device)
   void* aptrs[] = {s->visit, s->trace, s->part_j, s->part_min, s->pcount, s->poff, s->ptotal, s->prow, s->ppos, s->pd,
                    s->ptold, s->pdelta, s->runc, s->runv, s->rowcnt, s->rowidx, s->tstart, s->tcur, s->X,
-                   s->trows, s->ntouch, s->capfail, s->bigw, s->nbig, s->st_cnt, s->st_row, s->st_val, s->st_b,
+                   s->trows, s->ntouch, s->capfail, s->bigw, s->nbig, s->st_cnt, s->st_row, s->st_val, s->st_b, s->st_term,
                    s->ga_blk, s->dsteps, s->cur, s->phase, s->a, s->b, s->b_full, s->r, s->h, s->cnt, s->srow, s->sval, s->G_ga,
                    s->fen, s->status, s->steps_done, s->stop, s->scal, s->epsd, s->sw_j, s->sw_min, s->sw_g};
   if (s->stream) for (void* p : aptrs) sfree(p, s->stream);
