@@ -158,3 +158,21 @@ def test_gpu_kmeans_errors_and_k_equals_npix():
     cen, lab, cnt, it, conv = kmeans_quantize(pix, len(pix), init, 20)
     gc, gl, gn, git, gconv = sro.kmeans_quantize(pix, len(pix), init, 20)
     assert git == it and np.array_equal(gc, cen) and np.array_equal(gl, lab) and np.array_equal(gn, cnt)
+
+
+@pytest.mark.gpu
+def test_gpu_kmeans_features_match_oracle_and_reject_bad_input():
+    """sro_kmeans_features (R29 behind the C-ABI): colours = centroid / 255 and histogram = count / N
+    bit-equal to the oracle's colour_features; negative counts, all-zero counts and k < 1 raise."""
+    sro = pytest.importorskip("paper_2103_05857_b200")
+    from oracle.kmeans import colour_features
+    rng = np.random.default_rng(3)
+    cen = rng.random((17, 3)) * 255.0
+    cnt = rng.integers(0, 50, size=17).astype(np.int64)
+    cnt[4] = 0
+    x, a = sro.kmeans_features(cen, cnt)
+    xo, ao = colour_features(cen, cnt, int(cnt.sum()))
+    assert np.array_equal(x, xo) and np.array_equal(a, ao)
+    for bad in (np.array([3, -1, 2]), np.zeros(3, dtype=np.int64)):
+        with pytest.raises(sro.SroError):
+            sro.kmeans_features(np.ones((3, 3)), bad)
