@@ -269,8 +269,8 @@ __device__ __forceinline__ void ts_radix_sort(TailSmem& S, int P, int m) {
 // the (row, chunk) runs of the sorted keys (start index runu, chunk runc), the
 // touched rows ascending (rrow) with their first run (rowrun), and the rows
 // with more than TS_SMALL runs (hot), 3 .. TS_SMALL runs (mid). ts_sums<MODE>(vals): thread
-// per run sums it left to right from +0.0; thread per touched row with one or two runs;
-// eight lanes per mid row combine the run partials level by level;
+// per run sums it left to right from +0.0; thread per touched row with one or two runs, or with
+// 3 .. TS_SMALL runs (adjacent runs merged deepest common ancestor first);
 // warp per hot row: lane l gathers chunks [8l, 8l+8), tree8 + butterfly (the
 // dense tree with zero leaves). MODE 0: rX (Delta_k^2, for the denominator;
 // rX aliases the pair values, dead by then); MODE 1: r_k += D,
@@ -369,37 +369,46 @@ __device__ __forceinline__ void ts_sums(const BlockArgs& A, TailSmem& S, const d
 #ifdef SRO_PHASE_TIMING
   if (MODE == 0 && A.phase) { const long long t2 = clock64(); atomicAdd((unsigned long long*)&A.phase[24], (unsigned long long)(t2 - ts_t1) / 1024); ts_t1 = t2; }
 #endif
-  // 3 .. TS_SMALL runs: eight lanes per row, lane e holding run e (chunks ascending). Level by
-  // level (subtrees of 2^lv chunks) the two representatives of a parent — adjacent among the
-  // valid lanes, the left one lower — combine as left + right into the left lane, which is the
-  // adjacent-pair tree with zero leaves dropped (zeros are identities).
+  // 3 .. TS_SMALL runs, one thread per row: the adjacent-pair tree over the row's runs (chunks
+  // ascending; zero leaves are identities) is evaluated by merging, n - 1 times, the adjacent pair
+  // whose lowest common ancestor is deepest (31 - clz(c_e ^ c_e+1) smallest; adjacent levels
+  // differ, so the choice is unique): the merged pair's level to its right neighbour is the right
+  // one's (the left neighbour's is unchanged) — the same additions in the same order as the tree.
   {
     const int NM = S.misc[5];
-    const int gl = lane & 7, gb = lane & 24;
-    const unsigned gmask = 0xFFu << gb;
-    for (int it = 0; it * 128 < NM; it++) {   // uniform trip count (shuffles need every lane)
-      const int b = it * 128 + (t >> 3);
-      const bool act = b < NM;
-      const int w = act ? S.mid[b] : 0;
-      const int r0 = act ? S.rowrun[w] : 0, nr = act ? S.rowrun[w + 1] - r0 : 0;
-      bool valid = gl < nr;
-      int c = valid ? (int)S.runc[r0 + gl] : 0;
-      double v = valid ? S.runv[r0 + gl] : 0.0;
-      double rk = 0.0, ak = 0.0;
-      if (MODE == 1 && act && gl == 0) { const int row = S.rrow[w]; rk = A.r[row]; ak = A.a[row]; }
+    for (int b = t; b < NM; b += 1024) {
+      const int w = S.mid[b];
+      const int r0 = S.rowrun[w], nr = S.rowrun[w + 1] - r0;
+      double v[TS_SMALL];
+      int lv[TS_SMALL];
+      int cprev = 0;
 #pragma unroll
-      for (int lv = 1; lv <= 8; lv++) {
-        const unsigned vb = __ballot_sync(FULL, valid) & gmask;
-        const unsigned above = vb & ~((2u << lane) - 1u);
-        const unsigned below = vb & ((1u << lane) - 1u);
-        const int nxt = above ? __ffs(above) - 1 : lane;
-        const int prv = below ? 31 - __clz(below) : lane;
-        const int cn = __shfl_sync(FULL, c, nxt), cp = __shfl_sync(FULL, c, prv);
-        const double vn = __shfl_sync(FULL, v, nxt);
-        if (valid && above && (cn >> lv) == (c >> lv)) v = d_add(v, vn);
-        else if (valid && below && (cp >> lv) == (c >> lv)) valid = false;
+      for (int e = 0; e < TS_SMALL; e++) {
+        const bool in = e < nr;
+        const int c = in ? (int)S.runc[r0 + e] : 0;
+        v[e] = in ? S.runv[r0 + e] : 0.0;
+        if (e > 0) lv[e - 1] = in ? 31 - __clz(c ^ cprev) : 99;
+        cprev = c;
       }
-      if (act && gl == 0) finish(w, v, rk, ak);
+      lv[TS_SMALL - 1] = 99;
+#pragma unroll
+      for (int it = 0; it < TS_SMALL - 1; it++) {
+        if (it >= nr - 1) break;
+        int best = 0, bl = lv[0];
+#pragma unroll
+        for (int e = 1; e < TS_SMALL - 1; e++)
+          if (lv[e] < bl) { bl = lv[e]; best = e; }
+        // merge best and best + 1, shift the tail left by one
+#pragma unroll
+        for (int e = 0; e < TS_SMALL - 1; e++) {
+          if (e == best) { v[e] = d_add(v[e], v[e + 1]); lv[e] = lv[e + 1]; }
+          else if (e > best) { v[e] = v[e + 1]; lv[e] = lv[e + 1]; }
+        }
+        lv[TS_SMALL - 1] = 99;
+      }
+      double rk = 0.0, ak = 0.0;
+      if (MODE == 1) { const int row = S.rrow[w]; rk = A.r[row]; ak = A.a[row]; }
+      finish(w, v[0], rk, ak);
     }
   }
 #ifdef SRO_PHASE_TIMING
