@@ -15,8 +15,11 @@ namespace sro {
 __global__ void k_ga_block_draw(const double* __restrict__ fen, const double* __restrict__ G, int n, int B,
                                 uint64_t seed, long long kbase, const unsigned* __restrict__ cur, int* visit,
                                 const int* __restrict__ status) {
-  if (threadIdx.x != 0 || *status) return;
+  if (threadIdx.x != 0) return;
   const unsigned c = *cur;
+  // after a failed step every later kernel of the call skips, but a slot must still hold a
+  // valid block index for the kernels that read it before testing the status
+  if (*status) { visit[c] = 0; return; }
   const double u53 = uniform53(rng_u64(seed, 1, (uint64_t)(kbase + (long long)c)));
   visit[c] = ga_draw(fen, G, n, u53) / B;
 }
@@ -63,7 +66,10 @@ __global__ void __launch_bounds__(1024) k_ga_block_refresh(double* G, double* fe
                                                            const int* __restrict__ status, uint64_t seed,
                                                            long long kbase) {
   extern __shared__ double dl[];
-  if (*status) return;
+  if (*status) {   // the next slot still gets a valid block index (see k_ga_block_draw)
+    if (threadIdx.x == 0) visit[*cur] = 0;
+    return;
+  }
   ga_block_refresh_body(G, fen, n, B, visit[*cur - 1u] * B, gnew, dl);
   if (threadIdx.x == 0) {
     const unsigned c = *cur;
@@ -75,7 +81,8 @@ __global__ void __launch_bounds__(1024) k_ga_block_refresh(double* G, double* fe
 // draw step k's block into *slot; refresh the block *blk with the gathered gaps.
 __global__ void k_ga_block_draw_at(const double* __restrict__ fen, const double* __restrict__ G, int n, int B,
                                    uint64_t seed, long long k, int* slot, const int* __restrict__ status) {
-  if (threadIdx.x != 0 || *status) return;
+  if (threadIdx.x != 0) return;
+  if (*status) { *slot = 0; return; }   // a valid index for the skipped step's kernels
   *slot = ga_draw(fen, G, n, uniform53(rng_u64(seed, 1, (uint64_t)k))) / B;
 }
 __global__ void __launch_bounds__(1024) k_ga_block_refresh_at(double* G, double* fen, int n, int B,

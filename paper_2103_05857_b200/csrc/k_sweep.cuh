@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_sweep(Src src, int m, int
                                                              const double* __restrict__ sval, int cap,
                                                              const double* __restrict__ b, SweepOut out,
                                                              const int* __restrict__ stop, int* status) { pdl_entry();
-  if (stop && *stop) return;
+  if ((stop && *stop) || *status) return;   // FW stop, or a failed step earlier in the call
   extern __shared__ __align__(16) double sm_h[];
   const int nslabs = gridDim.y, slab = blockIdx.y;
   const int row0 = slab * slab_rows;
@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_merge(Src src, int nslabs
                                                              const double* __restrict__ pmin, int* out_j,
                                                              double* out_min, double* out_g,
                                                              const int* __restrict__ stop, int* status) { pdl_entry();
-  if (stop && *stop) return;
+  if ((stop && *stop) || *status) return;   // FW stop, or a failed step earlier in the call
   const int col0 = col0_dev ? col0_dev[cur ? *cur : 0u] * col0_mul : col0_host;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int p = blockIdx.x * SWEEP_WARPS + warp; p < L; p += gridDim.x * SWEEP_WARPS) {
@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(BULK_WARPS * 32, 1)
   using V = typename Vec<T>::type;
   constexpr int W = Vec<T>::W;
   constexpr int CHV = BULK_CH / 16;   // vectors per stage
-  if (stop && *stop) return;
+  if ((stop && *stop) || *status) return;   // FW stop, or a failed step earlier in the call
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
   unsigned char* bufs = smem + 1024;

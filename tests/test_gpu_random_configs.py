@@ -1,0 +1,109 @@
+"""Randomised GPU parity sweep (fixed seeds, so reproducible): 200 configurations drawn over the
+option space the C-ABI accepts — variant (BCFW / BCAFW / BCPFW / FW / batched), step rule, sampling
+(U / P / GA with M, inner refresh and its timing), gap period, cost kind (dense fp32 / fp64, fused
+sqeuclid / euclid in binary32 / binary64, hash), slab capacity, lambda over four decades, marginals
+with zero-mass columns and zero rows, and ragged m, n (several tiles, vector tails, block sizes
+dividing n) — each run for a few epochs through sro_solve and compared with the oracle step by step
+(Alg. 1, A.1-A.4, R18): trace, plan, row sums, gap and objective bit-exact, or the same error
+status (capacity) at the same step."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import BATCHED, BCAFW, BCFW, BCPFW, DEC, ELS, FW, GA, P, U, Oracle, OracleError
+from sro_inputs import mixture_colours
+
+pytestmark = pytest.mark.gpu
+
+sro = pytest.importorskip("paper_2103_05857_b200")
+
+GV = {BCFW: sro.SRO_BCFW, BCAFW: sro.SRO_BCAFW, BCPFW: sro.SRO_BCPFW, FW: sro.SRO_FW, BATCHED: sro.SRO_BATCHED}
+
+
+def _config(seed):
+    rs = np.random.default_rng(1000 + seed)
+    m = int(rs.choice([1, 7, 64, 129, 300, 511, 1030, 2500, 4096, 6001, 9000]))
+    n = int(rs.choice([1, 5, 33, 64, 96, 200, 257, 512, 1100]))
+    variant = int(rs.choice([BCFW, BCAFW, BCPFW, FW, BATCHED]))
+    step = ELS if variant in (BCAFW, BCPFW) else int(rs.choice([ELS, DEC]))
+    sampling = int(rs.choice([U, P, GA])) if variant != FW else U
+    opts = dict(step=step, sampling=sampling, gap_period=int(rs.choice([1, 1, 2])))
+    if sampling == GA:
+        opts.update(ga_M=int(rs.choice([1, 2])), ga_inner=int(rs.choice([0, 1])), ga_post_update=int(rs.choice([0, 1])))
+    if variant == BATCHED:
+        divs = [b for b in range(1, n + 1) if n % b == 0]
+        opts["block_size"] = int(rs.choice(divs))
+    cost = str(rs.choice(["dense32", "dense64", "sq32", "sq64", "eu32", "eu64", "hash"]))
+    lam = float(rs.choice([1e-2, 1e-1, 1.0, 10.0]))
+    cap = int(rs.choice([4, 8, 31]))
+    X, _, _ = mixture_colours(m, 4, 0.05, 2 * seed + 1)
+    Y, _, _ = mixture_colours(n, 4, 0.05, 2 * seed + 2)
+    a = rs.random(m) + 0.05
+    b = rs.random(n) + 0.05
+    if m > 3 and rs.random() < 0.3:
+        a[rs.integers(0, m, size=max(1, m // 5))] = 0.0
+    if n > 3 and rs.random() < 0.3:
+        b[rs.integers(0, n, size=max(1, n // 6))] = 0.0
+    a /= a.sum()
+    b /= b.sum()
+    epochs = 3 if variant != FW else 12
+    iters = epochs * (n // opts.get("block_size", 1) if variant == BATCHED else (1 if variant == FW else n))
+    if m * n > 2_000_000 and variant != FW:
+        epochs = 1
+        iters = n // opts.get("block_size", 1) if variant == BATCHED else n
+    return dict(m=m, n=n, variant=variant, opts=opts, cost=cost, lam=lam, cap=cap, X=X, Y=Y, a=a, b=b,
+                iters=max(1, iters), seed=int(rs.integers(0, 1 << 30)))
+
+
+def _make(cfg):
+    m, n, c = cfg["m"], cfg["n"], cfg["cost"]
+    kw = dict(cap=cfg["cap"])
+    if c.startswith("dense"):
+        C = ((cfg["X"][:, None, :] - cfg["Y"][None, :, :]) ** 2).sum(-1)
+        prec = "f32" if c == "dense32" else "f64"
+        Cs = C.astype(np.float32) if prec == "f32" else C
+        g = sro.Solver(cfg["a"], cfg["b"], cfg["lam"], C=Cs, prec=prec, slab_cap=cfg["cap"])
+        o = Oracle(cfg["a"], cfg["b"], cfg["lam"], C=np.asarray(Cs, dtype=np.float64), prec=prec, **kw)
+    elif c == "hash":
+        g = sro.Solver(cfg["a"], cfg["b"], cfg["lam"], cost="hash", hash_seed=77, slab_cap=cfg["cap"])
+        o = Oracle(cfg["a"], cfg["b"], cfg["lam"], cost="hash", hash_seed=77, **kw)
+    else:
+        kind = "sqeuclid" if c.startswith("sq") else "euclid"
+        prec = "f32" if c.endswith("32") else "f64"
+        g = sro.Solver(cfg["a"], cfg["b"], cfg["lam"], X=cfg["X"], Y=cfg["Y"], cost=kind, prec=prec,
+                       slab_cap=cfg["cap"])
+        o = Oracle(cfg["a"], cfg["b"], cfg["lam"], X=cfg["X"], Y=cfg["Y"], cost=kind, prec=prec, **kw)
+    return g, o
+
+
+@pytest.mark.parametrize("seed", range(200))
+def test_random_configuration_bitexact(seed):
+    cfg = _config(seed)
+    g, o = _make(cfg)
+    v, opts, iters = cfg["variant"], cfg["opts"], cfg["iters"]
+    err_o = err_g = None
+    ro = rg = None
+    try:
+        ro = o.solve(v, iters, seed=cfg["seed"], trace=True, epsilon=1e-12, **opts)
+    except OracleError as e:
+        err_o = e.status
+    try:
+        rg = g.solve(GV[v], iters, seed=cfg["seed"], trace=True, epsilon=1e-12, **opts)
+    except sro.SroError as e:
+        err_g = e.status
+    assert err_o == err_g, (cfg["variant"], opts, err_o, err_g)
+    if err_o is None:
+        for f in ("k", "i", "j", "v", "dir", "gamma", "num", "den", "minval"):
+            if v in (FW, BATCHED) and f in ("v", "dir"):
+                continue
+            bad = np.nonzero(rg["trace"][f] != ro["trace"][f])[0]
+            assert len(bad) == 0, (f, bad[0], {k: cfg[k] for k in ("m", "n", "variant", "opts", "cost", "lam", "cap")})
+        assert rg["iters_done"] == ro["iters_done"] and rg["gap_checks"] == ro["gap_checks"]
+        assert rg["gap"] == ro["gap"] or (np.isnan(rg["gap"]) and np.isnan(ro["gap"]))
+    assert np.array_equal(g.plan(), o.plan())
+    assert np.array_equal(g.rowsums(), o.r())
+    assert g.objective() == o.objective()
+    tg, gg, jg = g.gap()
+    to, go, jo, _ = o.gap()
+    assert tg == to and np.array_equal(gg, go) and np.array_equal(jg, jo)
