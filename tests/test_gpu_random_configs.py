@@ -193,3 +193,31 @@ def test_random_sharded_configuration_bitexact(seed):
     tg, gg, jg = g.gap()
     to, go, jo, _ = o.gap()
     assert tg == to and np.array_equal(gg, go) and np.array_equal(jg, jo)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_plan_functions_bitexact(seed):
+    """After a random solve, the functions of the plan — Eq. 15 (sro_barycentric), metrics (iii),
+    (iv), (vi) (sro_metrics) and (v), (vi) against a random reference plan (sro_lp_metrics) — equal
+    the oracle's bit for bit."""
+    cfg = _config(seed)
+    if cfg["cost"] == "hash":
+        cfg["cost"] = "dense64"
+    g, o = _make(cfg)
+    v, opts, iters = cfg["variant"], cfg["opts"], cfg["iters"]
+    for solver, var in ((o, v), (g, GV[v])):
+        try:
+            solver.solve(var, iters, seed=cfg["seed"], epsilon=1e-12, **opts)
+        except (OracleError, sro.SroError):
+            pass   # the same capacity failure on both sides (test_random_configuration_bitexact)
+    assert np.array_equal(g.plan(), o.plan())
+    X, Y = cfg["X"], cfg["Y"]
+    assert np.array_equal(g.barycentric(X, Y), o.barycentric(X, Y))
+    assert g.metrics() == o.metrics()
+    rs = np.random.default_rng(seed)
+    m, n = cfg["m"], cfg["n"]
+    nnz = int(rs.integers(1, 3 * n + 2))
+    flat = np.unique(rs.integers(0, m * n, size=nnz))
+    cols, rows = flat // m, flat % m                      # column-major order: sorted by (col, row)
+    vals = rs.random(len(flat)) / n
+    assert g.lp_metrics(rows, cols, vals) == o.lp_metrics(rows, cols, vals)
