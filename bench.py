@@ -421,6 +421,10 @@ def sweep_roofline_config3(local_rank, peaks, sweeps=3):
     return {"workload": "BASELINE configs[3]: m=n=65536, C iid U[0,1) fp32 materialised column-major (17.18 GB)",
             "kernel": "k_lmo_sweep_bulk + k_lmo_merge (one gap sweep: LMO + column gaps over all 65536 columns)",
             "bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
+            "peak_note": ("the measured peak is a copy (read + write bytes); this kernel only reads, so it can "
+                          "exceed it: against the 8 TB/s nominal HBM3e rate frac = "
+                          f"{ach / 8000.0:.3f}, against the read-only stream microbenchmark (7.3 TB/s, "
+                          f"profiles/r01_microbench.jsonl) {ach / 7300.0:.3f}"),
             "algorithmic_bytes_per_launch": byts, "avg_launch_ms": round(per_ms, 4), "sweeps_timed": sweeps,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, of measured)",
             "fw_els_time_to_gap_ms": round(r["device_ms"], 3), "fw_els_iterations": r["iters_done"],

@@ -341,8 +341,17 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_merge(Src src, int nslabs
 // CTA of a grid sized to the SM count: a CTA restages h (planar, as
 // SrcDense) only when its range enters the next slab.
 // ---------------------------------------------------------------------------
-constexpr int BULK_WARPS = 8;
-constexpr int BULK_CH = 4096;   // bytes per stage
+// 16 warps x 4 stages x 3 KiB in flight per SM (config [3] gap sweep: 6.70 TB/s, from 5.85 with 8
+// warps x 4 x 4 KiB; 12 x 4 x 4 KiB 6.49, 20 x 3 x 3 KiB 6.67, 24 x 3 x 2.5 KiB 6.52, 32 x 2 x 3 KiB
+// 6.03, 16 x 6 x 2 KiB 5.72 — tools/sweep3_timing.py); the row slab drops to 4096 to fit
+#ifndef SRO_BULK_WARPS
+#define SRO_BULK_WARPS 16
+#endif
+#ifndef SRO_BULK_CH
+#define SRO_BULK_CH 3072
+#endif
+constexpr int BULK_WARPS = SRO_BULK_WARPS;
+constexpr int BULK_CH = SRO_BULK_CH;   // bytes per stage
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {

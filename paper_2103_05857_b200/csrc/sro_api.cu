@@ -166,7 +166,7 @@ struct Solver {
   int num_sms = 148;
   // rows of h per sweep CTA (occupancy vs. merge work; SRO_SLAB overrides, multiple of 4, <= SLAB_MAX)
   int slab_rows = getenv("SRO_SLAB") ? std::max(4, std::min(SLAB_MAX, atoi(getenv("SRO_SLAB")) / 4 * 4)) : 4096;
-  int slab_bulk = getenv("SRO_SLAB") ? std::max(4, std::min(SLAB_MAX, atoi(getenv("SRO_SLAB")) / 4 * 4)) : 8192;
+  int slab_bulk = getenv("SRO_SLAB") ? std::max(4, std::min(SLAB_MAX, atoi(getenv("SRO_SLAB")) / 4 * 4)) : 4096;
   bool sweep_ldg = getenv("SRO_SWEEP_LDG") != nullptr;   // debug / A-B: dense sweeps without bulk copies
   // accounting
   long long* phase = nullptr;   // device [8] clock64 totals (SRO_PHASE_TIMING builds)
@@ -653,17 +653,19 @@ template <class Src>
 sro_status sweep_bulk(Solver* s, Src src, const int* col0_dev, int col0_mul, int col0_host, int L, int* out_j,
                       double* out_min, double* out_g, const int* stop) {
   using T = std::remove_cv_t<std::remove_pointer_t<decltype(src.C)>>;
-  constexpr int S = 4;
+#ifndef SRO_BULK_S
+#define SRO_BULK_S 4
+#endif
+  constexpr int S = SRO_BULK_S;
   // rows per (slab, column) item: the default slab, smaller when the sweep has few
   // columns (a batched block) so that every SM still gets several items
   int slab = s->slab_bulk;
   {
-    // about one (slab, column) item per two warps of the grid: fewer, longer slabs leave fewer
-    // partials for a block step's single-CTA tail (batched config [1], B = 256: 35.3 us per block
-    // step at two items per warp, 34.5 at one, 33.7 at a half, 35.3 at 0.35, 37.5 at a quarter;
-    // SRO_BULK_ITEMS overrides for A/B)
-    static const double items_per_warp = getenv("SRO_BULK_ITEMS") ? atof(getenv("SRO_BULK_ITEMS")) : 0.5;
-    const int64_t target = (int64_t)((double)s->num_sms * BULK_WARPS * items_per_warp);
+    // about four (slab, column) items per SM: fewer, longer slabs leave fewer partials for a block
+    // step's single-CTA tail (batched config [1], B = 256, with 8-warp CTAs: 35.3 us per block step
+    // at 16 items per SM, 8: 34.5, 4: 33.7, 2.8: 35.3, 2: 37.5; SRO_BULK_ITEMS overrides for A/B)
+    static const double items_per_sm = getenv("SRO_BULK_ITEMS") ? atof(getenv("SRO_BULK_ITEMS")) : 4.0;
+    const int64_t target = (int64_t)((double)s->num_sms * items_per_sm);
     const int64_t want = ((int64_t)s->m * L + target - 1) / target;
     if (want < slab) slab = (int)std::max<int64_t>(256, (want + 3) / 4 * 4);
   }
