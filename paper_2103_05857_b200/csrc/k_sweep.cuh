@@ -117,7 +117,11 @@ struct SrcColour {
 #ifndef SRO_COLOUR_COLS
 #define SRO_COLOUR_COLS 4
 #endif
-  static constexpr int COLS = SRO_COLOUR_COLS;   // columns a warp evaluates per loaded row (registers hold their y)
+#ifndef SRO_COLOUR_UNROLL   // rows per unrolled iteration of the 4-column scan: 1 / 2 / 4 / 6 / 8 measured
+#define SRO_COLOUR_UNROLL 4   // 1.26 / 1.36 / 1.46 / 1.48 / 1.48e12 entries/s at config [2]
+#endif
+  static constexpr int COLS = SRO_COLOUR_COLS;
+  static constexpr int UNROLL = SRO_COLOUR_UNROLL;   // rows per unrolled iteration of scan_multi   // columns a warp evaluates per loaded row (registers hold their y)
   __device__ __forceinline__ static int hidx(int k, int) { return k; }
   __device__ __forceinline__ void stage(int row0, int rows, char* sm) const {
     T* xs = reinterpret_cast<T*>(sm);
@@ -156,7 +160,7 @@ struct SrcColour {
       yv[c][0] = y[3 * (int64_t)i]; yv[c][1] = y[3 * (int64_t)i + 1]; yv[c][2] = y[3 * (int64_t)i + 2];
     }
     const int lane = threadIdx.x & 31;
-#pragma unroll 2
+#pragma unroll UNROLL
     for (int k = lane; k < rows; k += 32) {
       const T x0 = xs[k], x1 = xs[rows + k], x2 = xs[2 * rows + k];
       const double hk = hs[k];
