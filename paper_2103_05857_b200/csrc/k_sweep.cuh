@@ -108,11 +108,39 @@ struct SrcDense {
   }
 };
 
+// Packed binary32 pairs (sm_100 FADD2 / FMUL2): lane-wise IEEE round-to-nearest, the same
+// result as two scalar __fsub_rn / __fmul_rn. ptxas contracts a packed multiply into a following
+// packed add even under --fmad=false, so the products are only ever summed with scalar adds.
+__device__ __forceinline__ unsigned long long f2_pack(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float2 f2_unpack(unsigned long long v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+// (x - y0, x - y1) for one broadcast x (ptxas folds the pack into the .F32 operand form)
+__device__ __forceinline__ unsigned long long f2_bsub(float x, unsigned long long y) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_pack(x, x)), "l"(y));
+  return r;
+}
+__device__ __forceinline__ unsigned long long f2_sq(unsigned long long d) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(r) : "l"(d));
+  return r;
+}
+
 template <typename T, bool EUCLID>
 struct SrcColour {
   const T* x;   // 3m
   const T* y;   // 3n
-  static constexpr int SMEM_PER_ROW = 3 * sizeof(T);
+  // binary32 colours: one 16-byte (x0, x1, x2, 0) record per row (one LDS.128 per row);
+  // binary64: three planes
+  static constexpr bool PACKED = sizeof(T) == 4;
+  static constexpr int SMEM_PER_ROW = PACKED ? 16 : 3 * sizeof(T);
   static constexpr bool PLANAR = false;
 #ifndef SRO_COLOUR_COLS
 #define SRO_COLOUR_COLS 4
@@ -124,11 +152,29 @@ struct SrcColour {
   static constexpr int UNROLL = SRO_COLOUR_UNROLL;   // rows per unrolled iteration of scan_multi   // columns a warp evaluates per loaded row (registers hold their y)
   __device__ __forceinline__ static int hidx(int k, int) { return k; }
   __device__ __forceinline__ void stage(int row0, int rows, char* sm) const {
-    T* xs = reinterpret_cast<T*>(sm);
-    for (int k = threadIdx.x; k < rows; k += blockDim.x) {
-      xs[k] = x[3 * (int64_t)(row0 + k)];
-      xs[rows + k] = x[3 * (int64_t)(row0 + k) + 1];
-      xs[2 * rows + k] = x[3 * (int64_t)(row0 + k) + 2];
+    if constexpr (PACKED) {
+      float4* xs = reinterpret_cast<float4*>(sm);
+      for (int k = threadIdx.x; k < rows; k += blockDim.x) {
+        const int64_t o = 3 * (int64_t)(row0 + k);
+        xs[k] = make_float4(x[o], x[o + 1], x[o + 2], 0.f);
+      }
+    } else {
+      T* xs = reinterpret_cast<T*>(sm);
+      for (int k = threadIdx.x; k < rows; k += blockDim.x) {
+        xs[k] = x[3 * (int64_t)(row0 + k)];
+        xs[rows + k] = x[3 * (int64_t)(row0 + k) + 1];
+        xs[2 * rows + k] = x[3 * (int64_t)(row0 + k) + 2];
+      }
+    }
+  }
+  // staged colour of slab row k
+  __device__ __forceinline__ static void xrow(const char* sm, int k, int rows, T& x0, T& x1, T& x2) {
+    if constexpr (PACKED) {
+      const float4 v = reinterpret_cast<const float4*>(sm)[k];
+      x0 = v.x; x1 = v.y; x2 = v.z;
+    } else {
+      const T* xs = reinterpret_cast<const T*>(sm);
+      x0 = xs[k]; x1 = xs[rows + k]; x2 = xs[2 * rows + k];
     }
   }
   __device__ __forceinline__ double cost(int k, int i) const {
@@ -137,12 +183,13 @@ struct SrcColour {
   }
   __device__ __forceinline__ void scan(int i, int row0, int rows, const double* hs, const char* sm, double& best,
                                        int& bj) const {
-    const T* xs = reinterpret_cast<const T*>(sm);
     const T y0 = y[3 * (int64_t)i], y1 = y[3 * (int64_t)i + 1], y2 = y[3 * (int64_t)i + 2];
     const int lane = threadIdx.x & 31;
 #pragma unroll 4
     for (int k = lane; k < rows; k += 32) {
-      double c = colour_cost<EUCLID>(xs[k], xs[rows + k], xs[2 * rows + k], y0, y1, y2);
+      T x0, x1, x2;
+      xrow(sm, k, rows, x0, x1, x2);
+      double c = colour_cost<EUCLID>(x0, x1, x2, y0, y1, y2);
       double v = d_add(c, hs[k]);
       if (v < best) { best = v; bj = k; }
     }
@@ -152,7 +199,6 @@ struct SrcColour {
   template <int NC>
   __device__ __forceinline__ void scan_multi(int i0, int nc, int rows, const double* hs, const char* sm,
                                              double* best, int* bj) const {
-    const T* xs = reinterpret_cast<const T*>(sm);
     T yv[NC][3];
 #pragma unroll
     for (int c = 0; c < NC; c++) {
@@ -160,14 +206,50 @@ struct SrcColour {
       yv[c][0] = y[3 * (int64_t)i]; yv[c][1] = y[3 * (int64_t)i + 1]; yv[c][2] = y[3 * (int64_t)i + 2];
     }
     const int lane = threadIdx.x & 31;
-#pragma unroll UNROLL
-    for (int k = lane; k < rows; k += 32) {
-      const T x0 = xs[k], x1 = xs[rows + k], x2 = xs[2 * rows + k];
-      const double hk = hs[k];
+    if constexpr (PACKED && NC % 2 == 0) {
+      // binary32: the three differences and squares of two columns per packed instruction
+      // (exactly colour_cost's __fsub_rn / __fmul_rn), the two sums as scalar adds in its order
+      unsigned long long yp[NC / 2][3];
 #pragma unroll
-      for (int c = 0; c < NC; c++) {
-        const double v = d_add(colour_cost<EUCLID>(x0, x1, x2, yv[c][0], yv[c][1], yv[c][2]), hk);
-        if (v < best[c]) { best[c] = v; bj[c] = k; }
+      for (int c = 0; c < NC / 2; c++)
+#pragma unroll
+        for (int d = 0; d < 3; d++) yp[c][d] = f2_pack(yv[2 * c][d], yv[2 * c + 1][d]);
+      // the NC values of row k (packed pairs)
+      auto row_values = [&](int k, double* v) {
+        const float4 xk = reinterpret_cast<const float4*>(sm)[k];
+        const double hk = hs[k];
+#pragma unroll
+        for (int c = 0; c < NC / 2; c++) {
+          const float2 sx = f2_unpack(f2_sq(f2_bsub(xk.x, yp[c][0])));
+          const float2 sy = f2_unpack(f2_sq(f2_bsub(xk.y, yp[c][1])));
+          const float2 sz = f2_unpack(f2_sq(f2_bsub(xk.z, yp[c][2])));
+          float d0 = __fadd_rn(__fadd_rn(sx.x, sy.x), sz.x);
+          float d1 = __fadd_rn(__fadd_rn(sx.y, sy.y), sz.y);
+          if constexpr (EUCLID) { d0 = __fsqrt_rn(d0); d1 = __fsqrt_rn(d1); }
+          v[2 * c] = d_add((double)d0, hk);
+          v[2 * c + 1] = d_add((double)d1, hk);
+        }
+      };
+      int k = lane;
+#pragma unroll UNROLL
+      for (; k < rows; k += 32) {
+        double v[NC];
+        row_values(k, v);
+#pragma unroll
+        for (int c = 0; c < NC; c++)
+          if (v[c] < best[c]) { best[c] = v[c]; bj[c] = k; }
+      }
+    } else {
+#pragma unroll UNROLL
+      for (int k = lane; k < rows; k += 32) {
+        T x0, x1, x2;
+        xrow(sm, k, rows, x0, x1, x2);
+        const double hk = hs[k];
+#pragma unroll
+        for (int c = 0; c < NC; c++) {
+          const double v = d_add(colour_cost<EUCLID>(x0, x1, x2, yv[c][0], yv[c][1], yv[c][2]), hk);
+          if (v < best[c]) { best[c] = v; bj[c] = k; }
+        }
       }
     }
   }
@@ -236,8 +318,10 @@ __device__ __forceinline__ void stage_terms(const Src& src, const SweepOut& out,
 
 // grid = (gx, nslabs). col0 = col0_dev ? col0_dev[cur ? *cur : 0] * col0_mul : col0_host
 // (cur: a device step cursor, so that the launches of consecutive block steps are identical).
-template <class Src, int NCOL = Src::COLS>
-__global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_sweep(Src src, int m, int slab_rows, const double* __restrict__ h,
+// NT threads per CTA: 256, or 512 for the fused colour sweep over full slabs (two CTAs of 16 warps
+// per SM hide the fp32 -> fp64 add -> compare chains better than two of 8; <= 64 registers)
+template <class Src, int NCOL = Src::COLS, int NT = SWEEP_THREADS>
+__global__ void __launch_bounds__(NT, 1024 / NT) k_lmo_sweep(Src src, int m, int slab_rows, const double* __restrict__ h,
                                                              const int* __restrict__ col0_dev, const unsigned* __restrict__ cur, int col0_mul,
                                                              int col0_host, int L, const int* __restrict__ cnt,
                                                              const int* __restrict__ srow,
@@ -257,7 +341,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_sweep(Src src, int m, int
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if constexpr (NCOL > 1) {
     constexpr int NC = NCOL;
-    for (int p0 = (blockIdx.x * SWEEP_WARPS + warp) * NC; p0 < L; p0 += gridDim.x * SWEEP_WARPS * NC) {
+    for (int p0 = (blockIdx.x * (NT / 32) + warp) * NC; p0 < L; p0 += gridDim.x * (NT / 32) * NC) {
       const int nc = min(NC, L - p0);
       double best[NC];
       int bj[NC];
@@ -287,7 +371,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_lmo_sweep(Src src, int m, int
       }
     }
   } else {
-  for (int p = blockIdx.x * SWEEP_WARPS + warp; p < L; p += gridDim.x * SWEEP_WARPS) {
+  for (int p = blockIdx.x * (NT / 32) + warp; p < L; p += gridDim.x * (NT / 32)) {
     const int i = col0 + p;
     double best = __longlong_as_double(0x7ff0000000000000LL);  // +inf
     int bj = 0x7fffffff;

@@ -632,6 +632,10 @@ sro_status exchange(Solver* s, double* buf, size_t count) {
   return SRO_OK;
 }
 
+bool sweep_nt_wide() {
+  static const bool wide = !(getenv("SRO_COLOUR_NT") && atoi(getenv("SRO_COLOUR_NT")) == 256);   // A-B
+  return wide;
+}
 bool getenv_slab_fixed() {
   static const bool fixed = getenv("SRO_SLAB") != nullptr;   // debug / A-B: the slab the environment names
   return fixed;
@@ -731,18 +735,42 @@ sro_status sweep(Solver* s, const int* col0_dev, int col0_mul, int col0_host, in
       if (rows_want < 128) rows_want = 128;
       if (rows_want < slab) slab = (int)rows_want;
     }
+    if (multi && sweep_nt_wide() && !getenv_slab_fixed()) {
+      // a warp's work items are (slab, 4 columns); halve the slab (down to 1024 rows) while that
+      // evens out the items per warp (config [2]: 4096-row slabs leave 3.46 items per warp,
+      // 2048-row slabs 6.92)
+      auto eff = [&](int sl) {
+        const int64_t ns = (s->m + sl - 1) / sl, rw = s->m < sl ? s->m : sl;
+        const int64_t sm = 8 * ((rw + 1) & ~1) + (int64_t)Src::SMEM_PER_ROW * rw;
+        const int64_t per = std::max<int64_t>(1, std::min<int64_t>(2, (227 * 1024) / (sm + 1024)));
+        const int64_t warps_slab = std::max<int64_t>(1, (s->num_sms * per + ns - 1) / ns) * (2 * SWEEP_WARPS);
+        const int64_t items = (L + Src::COLS - 1) / Src::COLS;
+        const int64_t rounds = (items + warps_slab - 1) / warps_slab;
+        return (double)items / (double)(rounds * warps_slab);
+      };
+      double best = eff(slab);
+      for (int sl = slab / 2; sl >= 1024 && sl % 32 == 0; sl /= 2) {
+        const double e = eff(sl);
+        if (e > best + 0.02) { best = e; slab = sl; }
+      }
+    }
     const int nslabs = (s->m + slab - 1) / slab;
     { sro_status st = ensure_partials(s, nslabs, L); if (st) return st; }
     const int rows = s->m < slab ? s->m : slab;
     const size_t smem = sizeof(double) * (size_t)((rows + 1) & ~1) + (size_t)Src::SMEM_PER_ROW * rows;
     const int cols = multi ? Src::COLS : 1;
-    auto kern = multi ? k_lmo_sweep<Src, Src::COLS> : k_lmo_sweep<Src, 1>;
+    // the multi-column colour sweep runs CTAs of 16 warps (twice the warps in flight per SM
+    // for the same staged slab)
+    const int nt = multi && sweep_nt_wide() ? 2 * SWEEP_THREADS : SWEEP_THREADS;
+    auto kern = multi ? (nt > SWEEP_THREADS ? k_lmo_sweep<Src, Src::COLS, 2 * SWEEP_THREADS> : k_lmo_sweep<Src, Src::COLS>)
+                      : k_lmo_sweep<Src, 1>;
     CUDA_TRY(s, set_dyn_smem((const void*)kern, s->device, (int)smem));
     int per_sm = 0;
-    CUDA_TRY(s, occupancy((const void*)kern, s->device, SWEEP_THREADS, smem, &per_sm));
+    CUDA_TRY(s, occupancy((const void*)kern, s->device, nt, smem, &per_sm));
     if (per_sm < 1) per_sm = 1;
     int gx = s->num_sms * per_sm;
-    const int need = (L + SWEEP_WARPS * cols - 1) / (SWEEP_WARPS * cols);
+    const int warps = nt / 32;
+    const int need = (L + warps * cols - 1) / (warps * cols);
     if (nslabs > 1) gx = (gx + nslabs - 1) / nslabs;
     if (gx > need) gx = need;
     if (gx < 1) gx = 1;
@@ -754,7 +782,7 @@ sro_status sweep(Solver* s, const int* col0_dev, int col0_mul, int col0_host, in
     s->lead->stats.kernel_launches += (nslabs > 1 && !s->defer_merge) ? 2 : 1;
     s->lead->stats.sweep_launches += 1;
     s->lead->stats.sweep_columns += L;
-    CUDA_TRY(s, launch_pdl(kern, dim3(dim3(gx, nslabs)), dim3(SWEEP_THREADS), smem, s->stream, src, s->m, slab, s->h, col0_dev, s->sweep_cur, col0_mul, col0_host, L,
+    CUDA_TRY(s, launch_pdl(kern, dim3(dim3(gx, nslabs)), dim3(nt), smem, s->stream, src, s->m, slab, s->h, col0_dev, s->sweep_cur, col0_mul, col0_host, L,
                                                              s->cnt, s->srow, s->sval, s->cap, s->b, o, stop,
                                                              s->status));
     CUDA_TRY(s, cudaGetLastError());
