@@ -56,12 +56,19 @@ struct SrcDense {
   static constexpr int SMEM_PER_ROW = 0;
   static constexpr bool PLANAR = true;
   static constexpr int COLS = 1;
+  template <int NCOL>
   __device__ __forceinline__ void stage(int, int, char*) const {}
   __device__ __forceinline__ double cost(int k, int i) const { return (double)C[(int64_t)i * ld + k]; }
+  // per-column registers of a scan (none) and the raw operands of one cost (loaded early, used late)
+  struct ColReg {};
+  __device__ __forceinline__ ColReg col(int) const { return {}; }
+  struct CostPre { T c; };
+  __device__ __forceinline__ CostPre cost_load(int k, int i) const { return {C[(int64_t)i * ld + k]}; }
+  __device__ __forceinline__ static double cost_of(const CostPre& q, const ColReg&) { return (double)q.c; }
   // Scan rows [row0, row0+rows) of column i; lane-strided 128-bit vectors,
   // rows ascending within a lane, 8 vectors in flight per lane.
-  __device__ __forceinline__ void scan(int i, int row0, int rows, const double* hs, const char*, double& best,
-                                       int& bj) const {
+  __device__ __forceinline__ void scan(int i, const ColReg&, int row0, int rows, const double* hs, const char*,
+                                       double& best, int& bj) const {
     using V = typename Vec<T>::type;
     constexpr int W = Vec<T>::W;
     const int lane = threadIdx.x & 31;
@@ -127,6 +134,11 @@ __device__ __forceinline__ unsigned long long f2_bsub(float x, unsigned long lon
   asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_pack(x, x)), "l"(y));
   return r;
 }
+__device__ __forceinline__ unsigned long long f2_sub(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
 __device__ __forceinline__ unsigned long long f2_sq(unsigned long long d) {
   unsigned long long r;
   asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(r) : "l"(d));
@@ -151,8 +163,13 @@ struct SrcColour {
   static constexpr int COLS = SRO_COLOUR_COLS;
   static constexpr int UNROLL = SRO_COLOUR_UNROLL;   // rows per unrolled iteration of scan_multi   // columns a warp evaluates per loaded row (registers hold their y)
   __device__ __forceinline__ static int hidx(int k, int) { return k; }
+  // planes (x0 | x1 | x2) of the slab's colours; binary32 planes start at even offsets so that a
+  // lane reads two consecutive rows of a coordinate as one packed pair
+  __device__ __forceinline__ static int pstride(int rows) { return PACKED ? ((rows + 1) & ~1) : rows; }
+  // multi-column scans of binary32 colours read one 16-byte record per row, everything else planes
+  template <int NCOL>
   __device__ __forceinline__ void stage(int row0, int rows, char* sm) const {
-    if constexpr (PACKED) {
+    if constexpr (PACKED && NCOL > 1 && NCOL % 2 == 0) {
       float4* xs = reinterpret_cast<float4*>(sm);
       for (int k = threadIdx.x; k < rows; k += blockDim.x) {
         const int64_t o = 3 * (int64_t)(row0 + k);
@@ -160,38 +177,71 @@ struct SrcColour {
       }
     } else {
       T* xs = reinterpret_cast<T*>(sm);
+      const int ps = pstride(rows);
       for (int k = threadIdx.x; k < rows; k += blockDim.x) {
         xs[k] = x[3 * (int64_t)(row0 + k)];
-        xs[rows + k] = x[3 * (int64_t)(row0 + k) + 1];
-        xs[2 * rows + k] = x[3 * (int64_t)(row0 + k) + 2];
+        xs[ps + k] = x[3 * (int64_t)(row0 + k) + 1];
+        xs[2 * ps + k] = x[3 * (int64_t)(row0 + k) + 2];
       }
-    }
-  }
-  // staged colour of slab row k
-  __device__ __forceinline__ static void xrow(const char* sm, int k, int rows, T& x0, T& x1, T& x2) {
-    if constexpr (PACKED) {
-      const float4 v = reinterpret_cast<const float4*>(sm)[k];
-      x0 = v.x; x1 = v.y; x2 = v.z;
-    } else {
-      const T* xs = reinterpret_cast<const T*>(sm);
-      x0 = xs[k]; x1 = xs[rows + k]; x2 = xs[2 * rows + k];
     }
   }
   __device__ __forceinline__ double cost(int k, int i) const {
     return colour_cost<EUCLID>(x[3 * (int64_t)k], x[3 * (int64_t)k + 1], x[3 * (int64_t)k + 2], y[3 * (int64_t)i],
                                y[3 * (int64_t)i + 1], y[3 * (int64_t)i + 2]);
   }
-  __device__ __forceinline__ void scan(int i, int row0, int rows, const double* hs, const char* sm, double& best,
-                                       int& bj) const {
-    const T y0 = y[3 * (int64_t)i], y1 = y[3 * (int64_t)i + 1], y2 = y[3 * (int64_t)i + 2];
+  struct ColReg { T y0, y1, y2; };
+  __device__ __forceinline__ ColReg col(int i) const {
+    return {y[3 * (int64_t)i], y[3 * (int64_t)i + 1], y[3 * (int64_t)i + 2]};
+  }
+  struct CostPre { T x0, x1, x2; };
+  __device__ __forceinline__ CostPre cost_load(int k, int) const {
+    return {x[3 * (int64_t)k], x[3 * (int64_t)k + 1], x[3 * (int64_t)k + 2]};
+  }
+  __device__ __forceinline__ static double cost_of(const CostPre& q, const ColReg& c) {
+    return colour_cost<EUCLID>(q.x0, q.x1, q.x2, c.y0, c.y1, c.y2);
+  }
+  // one column against the slab (planes), rows ascending per lane
+  __device__ __forceinline__ void scan(int, const ColReg& cr, int, int rows, const double* hs, const char* sm,
+                                       double& best, int& bj) const {
     const int lane = threadIdx.x & 31;
+    const T* xs = reinterpret_cast<const T*>(sm);
+    const int ps = pstride(rows);
+    if constexpr (PACKED) {
+      // lane q takes the row pairs (2q', 2q'+1), q' = q, q + 32, ...: one packed pair per coordinate
+      // (the planes' pairs), the differences and squares of both rows per FADD2 / FMUL2 and the
+      // sums as scalar adds in colour_cost's order
+      const float2* x0 = reinterpret_cast<const float2*>(xs);
+      const float2* x1 = reinterpret_cast<const float2*>(xs + ps);
+      const float2* x2 = reinterpret_cast<const float2*>(xs + 2 * ps);
+      const double2* h2 = reinterpret_cast<const double2*>(hs);
+      const unsigned long long Y0 = f2_pack(cr.y0, cr.y0), Y1 = f2_pack(cr.y1, cr.y1), Y2 = f2_pack(cr.y2, cr.y2);
+      const int np = rows >> 1;
 #pragma unroll 4
-    for (int k = lane; k < rows; k += 32) {
-      T x0, x1, x2;
-      xrow(sm, k, rows, x0, x1, x2);
-      double c = colour_cost<EUCLID>(x0, x1, x2, y0, y1, y2);
-      double v = d_add(c, hs[k]);
-      if (v < best) { best = v; bj = k; }
+      for (int q = lane; q < np; q += 32) {
+        const float2 a0 = x0[q], a1 = x1[q], a2 = x2[q];
+        const double2 hh = h2[q];
+        const float2 sx = f2_unpack(f2_sq(f2_sub(f2_pack(a0.x, a0.y), Y0)));
+        const float2 sy = f2_unpack(f2_sq(f2_sub(f2_pack(a1.x, a1.y), Y1)));
+        const float2 sz = f2_unpack(f2_sq(f2_sub(f2_pack(a2.x, a2.y), Y2)));
+        float d0 = __fadd_rn(__fadd_rn(sx.x, sy.x), sz.x);
+        float d1 = __fadd_rn(__fadd_rn(sx.y, sy.y), sz.y);
+        if constexpr (EUCLID) { d0 = __fsqrt_rn(d0); d1 = __fsqrt_rn(d1); }
+        const double v0 = d_add((double)d0, hh.x), v1 = d_add((double)d1, hh.y);
+        if (v0 < best) { best = v0; bj = 2 * q; }
+        if (v1 < best) { best = v1; bj = 2 * q + 1; }
+      }
+      if ((rows & 1) && lane == 0) {   // the odd last row (the largest index: order kept)
+        const int k = rows - 1;
+        const double v = d_add(colour_cost<EUCLID>(xs[k], xs[ps + k], xs[2 * ps + k], cr.y0, cr.y1, cr.y2), hs[k]);
+        if (v < best) { best = v; bj = k; }
+      }
+    } else {
+#pragma unroll 4
+      for (int k = lane; k < rows; k += 32) {
+        const double c = colour_cost<EUCLID>(xs[k], xs[ps + k], xs[2 * ps + k], cr.y0, cr.y1, cr.y2);
+        const double v = d_add(c, hs[k]);
+        if (v < best) { best = v; bj = k; }
+      }
     }
   }
   // columns i0 .. i0+nc-1 (nc <= COLS) against every row of the slab: one load of
@@ -240,10 +290,11 @@ struct SrcColour {
           if (v[c] < best[c]) { best[c] = v[c]; bj[c] = k; }
       }
     } else {
+      const T* xs = reinterpret_cast<const T*>(sm);
+      const int ps = pstride(rows);
 #pragma unroll UNROLL
       for (int k = lane; k < rows; k += 32) {
-        T x0, x1, x2;
-        xrow(sm, k, rows, x0, x1, x2);
+        const T x0 = xs[k], x1 = xs[ps + k], x2 = xs[2 * ps + k];
         const double hk = hs[k];
 #pragma unroll
         for (int c = 0; c < NC; c++) {
@@ -328,18 +379,22 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_lmo_sweep(Src src, int m, int
                                                              const double* __restrict__ sval, int cap,
                                                              const double* __restrict__ b, SweepOut out,
                                                              const int* __restrict__ stop, int* status) { pdl_entry();
-  if ((stop && *stop) || *status) return;   // FW stop, or a failed step earlier in the call
+  // the step words and the cursor together, then the column offset (an FW stop, or a failed step
+  // earlier in the call: nothing to do)
+  const int stop_v = stop ? *stop : 0, status_v = *status;
+  const unsigned cur_v = cur ? *cur : 0u;
+  if (stop_v || status_v) return;
+  const int col0 = col0_dev ? col0_dev[cur_v] * col0_mul : col0_host;
   extern __shared__ __align__(16) double sm_h[];
   const int nslabs = gridDim.y, slab = blockIdx.y;
   const int row0 = slab * slab_rows;
   const int rows = min(slab_rows, m - row0);
-  for (int k = threadIdx.x; k < rows; k += blockDim.x) sm_h[Src::hidx(k, rows)] = h[row0 + k];
-  char* sm_src = reinterpret_cast<char*>(sm_h + ((rows + 1) & ~1));
-  src.stage(row0, rows, sm_src);
-  __syncthreads();
-  const int col0 = col0_dev ? col0_dev[cur ? *cur : 0u] * col0_mul : col0_host;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  char* sm_src = reinterpret_cast<char*>(sm_h + ((rows + 1) & ~1));
   if constexpr (NCOL > 1) {
+    for (int k = threadIdx.x; k < rows; k += blockDim.x) sm_h[Src::hidx(k, rows)] = h[row0 + k];
+    src.template stage<NCOL>(row0, rows, sm_src);
+    __syncthreads();
     constexpr int NC = NCOL;
     for (int p0 = (blockIdx.x * (NT / 32) + warp) * NC; p0 < L; p0 += gridDim.x * (NT / 32) * NC) {
       const int nc = min(NC, L - p0);
@@ -371,27 +426,58 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_lmo_sweep(Src src, int m, int
       }
     }
   } else {
-  for (int p = blockIdx.x * (NT / 32) + warp; p < L; p += gridDim.x * (NT / 32)) {
-    const int i = col0 + p;
-    double best = __longlong_as_double(0x7ff0000000000000LL);  // +inf
-    int bj = 0x7fffffff;
-    src.scan(i, row0, rows, sm_h, sm_src, best, bj);
-    if (bj != 0x7fffffff) bj += row0;
-    warp_argmin(best, bj);
-    if (nslabs == 1) {
-      if (!(best < 1.0e308 && best > -1.0e308)) { if (lane == 0) set_status(status, 5); }
-      const double g = column_gap_epilogue(src, i, best, cnt, srow, sval, cap, b, h);
-      if (lane == 0) { out.j[p] = bj; out.minval[p] = best; out.g[p] = g; }
-    } else {
-      if (lane == 0) {
-        out.j[(int64_t)slab * L + p] = bj;
-        out.minval[(int64_t)slab * L + p] = best;
+    // One column per warp per pass (block steps: one pass). A column's own data (the source's
+    // per-column registers, its support size, support entries and b_i) is requested before the
+    // slab is staged, and the operands of its gap terms before the scan, so that their round
+    // trips overlap the staging and the scan instead of following them.
+    constexpr int Wn = NT / 32;
+    int p = blockIdx.x * Wn + warp;
+    typename Src::ColReg cr{};
+    int pc = 0, pk = 0;
+    double pt = 0.0, pb = 0.0;
+    auto prefetch = [&](int pp) {
+      const int i = col0 + pp;
+      cr = src.col(i);
+      pc = cnt[i];
+      pb = b[i];
+      if (lane < cap) { pk = srow[(int64_t)i * cap + lane]; pt = sval[(int64_t)i * cap + lane]; }
+    };
+    if (p < L) prefetch(p);
+    for (int k = threadIdx.x; k < rows; k += blockDim.x) sm_h[Src::hidx(k, rows)] = h[row0 + k];
+    src.template stage<1>(row0, rows, sm_src);
+    __syncthreads();
+    for (; p < L; p += gridDim.x * Wn) {
+      const int i = col0 + p;
+      // this lane's gap term t_ki (C_ki + h_k): every support entry for the full epilogue, the first
+      // SW_KP entries with rows in this slab for the block tail (R19 sums them in entry order)
+      const bool need = lane < pc && (nslabs == 1 || (out.st_term && lane < SW_KP && pk >= row0 && pk < row0 + rows));
+      typename Src::CostPre q{};
+      double hk = 0.0;
+      if (need) { q = src.cost_load(pk, i); hk = h[pk]; }
+      double best = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+      int bj = 0x7fffffff;
+      src.scan(i, cr, row0, rows, sm_h, sm_src, best, bj);
+      if (bj != 0x7fffffff) bj += row0;
+      warp_argmin(best, bj);
+      const double term = need ? d_mul(pt, d_add(Src::cost_of(q, cr), hk)) : 0.0;
+      if (nslabs == 1) {
+        if (!(best < 1.0e308 && best > -1.0e308)) { if (lane == 0) set_status(status, 5); }
+        const double g = d_sub(warp_seq_sum(term, pc), d_mul(pb, best));   // Eq. 11, as column_gap_epilogue
+        if (lane == 0) { out.j[p] = bj; out.minval[p] = best; out.g[p] = g; }
+      } else {
+        if (lane == 0) {
+          out.j[(int64_t)slab * L + p] = bj;
+          out.minval[(int64_t)slab * L + p] = best;
+        }
+        if (out.st_cnt && slab == 0) {   // as stage_support
+          if (lane == 0) { out.st_cnt[p] = pc; out.st_b[p] = pb; }
+          if (lane < SW_KP && lane < pc) { out.st_row[lane * L + p] = pk; out.st_val[lane * L + p] = pt; }
+        }
+        if (need) out.st_term[lane * L + p] = term;   // as stage_terms
       }
-      if (out.st_cnt && slab == 0) stage_support(out, p, i, L, cnt, srow, sval, cap, b);
-      if (out.st_term) stage_terms(src, out, p, i, L, row0, rows, cnt, srow, sval, cap, h);
+      if (p + gridDim.x * Wn < L) prefetch(p + gridDim.x * Wn);
     }
   }
-}
 }
 
 // Merge per-slab partials in slab order and apply the gap epilogue. One warp per column.
