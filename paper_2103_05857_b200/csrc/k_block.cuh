@@ -151,28 +151,58 @@ __device__ __forceinline__ void dev_pairs_count(const BlockArgs& A) {
   for (int p = gtid(); p < A.L; p += gstride()) A.pcount[p] = merged_count(A, col0 + p, A.j[p]);
 }
 
-// Exclusive scan of x[0..N) into y[0..N], y[N] = total (integers: order-free).
-// One CTA of exactly 1024 threads.
-__device__ __forceinline__ void dev_scan_excl(const int* __restrict__ x, int N, int* y, int* total) {
+// Exclusive scan of get(0..N) (integers: order-free) -> put(q, prefix), returning the total.
+// One CTA of exactly 1024 threads over tiles of 4096 values, four consecutive per thread (the
+// CTA's loads coalesced; the next tile's values are requested while the current one is scanned).
+// A thread-per-contiguous-range scan made each warp load touch 32 lines: ~80 us for 65536
+// counts at config [3].
+template <class Get, class Put>
+__device__ __forceinline__ int block_scan_tiles(int N, Get get, Put put) {
   __shared__ int ws[32];
-  const int t = threadIdx.x;
-  const int per = (N + 1023) / 1024;
-  const int lo = min(N, t * per), hi = min(N, lo + per);
-  int s = 0;
-  for (int q = lo; q < hi; q++) s += x[q];
-  int incl = s;
-  for (int o = 1; o < 32; o <<= 1) { int v = __shfl_up_sync(FULL, incl, o); if ((t & 31) >= o) incl += v; }
-  if ((t & 31) == 31) ws[t >> 5] = incl;
-  __syncthreads();
-  if (t < 32) {
-    int w = ws[t];
-    for (int o = 1; o < 32; o <<= 1) { int v = __shfl_up_sync(FULL, w, o); if (t >= o) w += v; }
-    ws[t] = w;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  int carry = 0;
+  int v[4];
+#pragma unroll
+  for (int u = 0; u < 4; u++) v[u] = 4 * t + u < N ? get(4 * t + u) : 0;
+  for (int base = 0; base < N; base += 4096) {
+    int nv[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int q = base + 4096 + 4 * t + u;
+      nv[u] = q < N ? get(q) : 0;
+    }
+    const int s = (v[0] + v[1]) + (v[2] + v[3]);
+    int incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(FULL, incl, o); if (lane >= o) incl += y; }
+    if (lane == 31) ws[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+      int x = ws[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(FULL, x, o); if (lane >= o) x += y; }
+      ws[lane] = x;
+    }
+    __syncthreads();
+    int run = carry + (w ? ws[w - 1] : 0) + incl - s;
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int q = base + 4 * t + u;
+      if (q < N) put(q, run);
+      run += v[u];
+    }
+    carry += ws[31];
+    __syncthreads();   // ws is rewritten by the next tile
+#pragma unroll
+    for (int u = 0; u < 4; u++) v[u] = nv[u];
   }
-  __syncthreads();
-  int run = incl - s + ((t >> 5) ? ws[(t >> 5) - 1] : 0);
-  for (int q = lo; q < hi; q++) { y[q] = run; run += x[q]; }
-  if (t == 1023) { y[N] = run; if (total) *total = run; }
+  return carry;
+}
+
+// Exclusive scan of x[0..N) into y[0..N], y[N] = total. One CTA of exactly 1024 threads.
+__device__ __forceinline__ void dev_scan_excl(const int* __restrict__ x, int N, int* y, int* total) {
+  const int tot = block_scan_tiles(N, [&](int q) { return x[q]; }, [&](int q, int e) { y[q] = e; });
+  if (threadIdx.x == 0) { y[N] = tot; if (total) *total = tot; }
   __syncthreads();
 }
 
@@ -190,7 +220,11 @@ __device__ __forceinline__ void dev_pairs_gen(const BlockArgs& A) {
       A.ppos[q] = p;
       A.pd[q] = d_sub(row == j ? bi : 0.0, told);
       if (A.ptold) A.ptold[q] = told;
-      if (atomicAdd(&A.rowcnt[row], 1) == 0) {   // order-free touched list
+      // per-row pair counts, warp-aggregated (columns share their argmin rows: one atomic per
+      // distinct row of the converged lanes instead of one per pair); the first to count a row
+      // appends it to the order-free touched list
+      const unsigned grp = __match_any_sync(__activemask(), row);
+      if ((int)(threadIdx.x & 31) == __ffs(grp) - 1 && atomicAdd(&A.rowcnt[row], __popc(grp)) == 0) {
         const int w = atomicAdd(A.ntouch, 1);
         A.trows[w] = row;
         A.rowidx[row] = w;
@@ -212,39 +246,23 @@ __device__ __forceinline__ int find_pair(const BlockArgs& A, int pp, int k) {
 // Run-list segments of the touched rows: tstart = exclusive scan over the
 // touched list of the rows' pair counts (one CTA of exactly 1024 threads).
 __device__ __forceinline__ void dev_touched_scan(const BlockArgs& A) {
-  __shared__ int ws[32];
   const int N = *A.ntouch;
-  const int t = threadIdx.x;
-  const int per = (N + 1023) / 1024;
-  const int lo = min(N, t * per), hi = min(N, lo + per);
-  int s = 0;
-  for (int q = lo; q < hi; q++) s += A.rowcnt[A.trows[q]];
-  int incl = s;
-  for (int o = 1; o < 32; o <<= 1) { int v = __shfl_up_sync(FULL, incl, o); if ((t & 31) >= o) incl += v; }
-  if ((t & 31) == 31) ws[t >> 5] = incl;
-  __syncthreads();
-  if (t < 32) {
-    int w = ws[t];
-    for (int o = 1; o < 32; o <<= 1) { int v = __shfl_up_sync(FULL, w, o); if (t >= o) w += v; }
-    ws[t] = w;
-  }
-  __syncthreads();
-  int run = incl - s + ((t >> 5) ? ws[(t >> 5) - 1] : 0);
-  for (int q = lo; q < hi; q++) { A.tstart[q] = run; run += A.rowcnt[A.trows[q]]; }
+  block_scan_tiles(N, [&](int q) { return A.rowcnt[A.trows[q]]; }, [&](int q, int e) { A.tstart[q] = e; });
   __syncthreads();
 }
 
 // The (row k, chunk c) run of val summed in column order from +0.0 (R19) by
 // the run's first pair, appended to row k's run list as (c, sum).
-__device__ __forceinline__ void dev_runs(const BlockArgs& A, const double* __restrict__ val) {
-  const int P = *A.ptotal;
-  for (int q = gtid(); q < P; q += gstride()) {
+// the run that pair q starts, if it is the first pair of its row in its chunk (searching the
+// earlier positions' supports)
+__device__ __forceinline__ void run_of_pair(const BlockArgs& A, const double* __restrict__ val, int q) {
+  {
     const int p = A.ppos[q], k = A.prow[q];
     const int c = chunk_index(p, A.L, A.W);
     const int lo = (int)chunk_lo(c, A.L, A.W), hi = (int)chunk_lo(c + 1, A.L, A.W);
     bool start = true;
     for (int pp = lo; pp < p && start; pp++) start = find_pair(A, pp, k) < 0;
-    if (!start) continue;
+    if (!start) return;
     double s = d_add(0.0, val[q]);
     for (int pp = p + 1; pp < hi; pp++) {
       const int qq = find_pair(A, pp, k);
@@ -255,6 +273,10 @@ __device__ __forceinline__ void dev_runs(const BlockArgs& A, const double* __res
     A.runc[slot] = c;
     A.runv[slot] = s;
   }
+}
+__device__ __forceinline__ void dev_runs(const BlockArgs& A, const double* __restrict__ val) {
+  const int P = *A.ptotal;
+  for (int q = gtid(); q < P; q += gstride()) run_of_pair(A, val, q);
 }
 
 // Applies a touched row's combined sum D. MODE 0: X[k] = D^2; MODE 1: r_k += D,
@@ -365,8 +387,7 @@ __device__ __forceinline__ double dev_psumW(const double* __restrict__ x, int64_
   double acc = 0.0;
   if (c < 256) {
     if (c < W) {
-      const int64_t lo = chunk_lo(c, L, W), hi = chunk_lo(c + 1, L, W);
-      for (int64_t p = lo; p < hi; p++) acc = d_add(acc, x[p]);
+      acc = chunk_seq_sum(x, chunk_lo(c, L, W), chunk_lo(c + 1, L, W));
     }
     acc = warp_pair_tree(acc);
     if ((c & 31) == 0) red[c >> 5] = acc;
@@ -386,6 +407,69 @@ __device__ __forceinline__ double dev_psumW(const double* __restrict__ x, int64_
   const double v = red[0];
   __syncthreads();
   return v;
+}
+
+// dev_psumW for long chunks (one CTA of exactly 256 threads): the chunks are staged through
+// shared memory 16 elements per chunk at a time, each half-warp loading 128 contiguous bytes of
+// one chunk (the next slice requested while the current one is summed); thread c still adds
+// chunk c left to right from +0.0. Reading 256 chunks of 256 doubles directly (thread c walking
+// chunk c) touched 32 lines per warp load and took ~30 us at config [3].
+constexpr int PSUM_K = 16;
+__device__ __forceinline__ double dev_psumW_tiled(const double* __restrict__ x, int64_t L, int W, double* out,
+                                                  const double* eps, int* stop_flag) {
+  __shared__ double tile[256][PSUM_K + 1];
+  __shared__ int64_t rlo[257];
+  __shared__ double red[8];
+  const int c = threadIdx.x;
+  rlo[c] = c < W ? chunk_lo(c, L, W) : L;
+  if (c == 0) rlo[256] = L;
+  __syncthreads();
+  const int64_t maxlen = (L + W - 1) / W;
+  const int u = c & 15, r0 = c >> 4;
+  double nv[16];
+  auto load = [&](int64_t U) {
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+      const int r = r0 + 16 * k;
+      const int64_t q = rlo[r] + U + u;
+      nv[k] = (r < W && q < rlo[r + 1]) ? x[q] : 0.0;
+    }
+  };
+  load(0);
+  double acc = 0.0;
+  const int64_t len = c < W ? rlo[c + 1] - rlo[c] : 0;
+  for (int64_t U = 0; U < maxlen; U += PSUM_K) {
+#pragma unroll
+    for (int k = 0; k < 16; k++) tile[r0 + 16 * k][u] = nv[k];
+    __syncthreads();
+    if (U + PSUM_K < maxlen) load(U + PSUM_K);
+    const int64_t rem = len - U;
+    const int kk = rem < PSUM_K ? (rem > 0 ? (int)rem : 0) : PSUM_K;
+    for (int e = 0; e < kk; e++) acc = d_add(acc, tile[c][e]);
+    __syncthreads();
+  }
+  acc = warp_pair_tree(acc);
+  if ((c & 31) == 0) red[c >> 5] = acc;
+  __syncthreads();
+  if (c < 32) {
+    double v = (c < 8) ? red[c] : 0.0;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) v = d_add(v, __shfl_xor_sync(FULL, v, o));
+    if (c == 0) {
+      red[0] = v;
+      if (out) *out = v;
+      if (stop_flag && eps && v <= *eps) *stop_flag = 1;
+    }
+  }
+  __syncthreads();
+  const double v = red[0];
+  __syncthreads();
+  return v;
+}
+__device__ __forceinline__ double dev_psumW_any(const double* __restrict__ x, int64_t L, int W, double* out,
+                                                const double* eps, int* stop_flag) {
+  return (L + W - 1) / W > 2 * PSUM_K ? dev_psumW_tiled(x, L, W, out, eps, stop_flag)
+                                      : dev_psumW(x, L, W, out, eps, stop_flag);
 }
 
 // Step size: ELS (Eq. 10 / Eq. A.1 / joint block search) or DEC 2n'/(k'+2n').
@@ -457,16 +541,175 @@ __device__ __forceinline__ void dev_update_cols(const BlockArgs& A) {
   }
 }
 
+// Warp per column (the multi-CTA phase kernels): the merged support supp(t_i) U {j} held one
+// entry per lane, rows ascending (lane < M) — the entries for_merged visits, in its order. Every
+// load is issued at once (the support slab is read for lane < cap whatever its size), so a column
+// costs one round trip instead of one per support entry.
+struct WarpMerged {
+  int M;         // merged support size (<= cap + 1 <= 32)
+  int row;       // this lane's entry
+  double told;
+};
+__device__ __forceinline__ WarpMerged warp_merged(const BlockArgs& A, int i, int j) {
+  const int lane = threadIdx.x & 31;
+  const int c0 = A.cnt[i];
+  int rw = 0x7fffffff;
+  double tv = 0.0;
+  if (lane < A.cap) { rw = A.srow[(int64_t)i * A.cap + lane]; tv = A.sval[(int64_t)i * A.cap + lane]; }
+  if (lane >= c0) { rw = 0x7fffffff; tv = 0.0; }
+  const bool j_in = __ballot_sync(FULL, rw == j) != 0u;
+  const int ins = __popc(__ballot_sync(FULL, rw < j));
+  int src = (j_in || lane < ins) ? lane : lane - 1;
+  if (src < 0) src = 0;
+  WarpMerged w;
+  w.row = __shfl_sync(FULL, rw, src);
+  w.told = __shfl_sync(FULL, tv, src);
+  if (!j_in && lane == ins) { w.row = j; w.told = 0.0; }
+  w.M = c0 + (j_in ? 0 : 1);
+  return w;
+}
+__device__ __forceinline__ int gwarp() { return (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); }
+__device__ __forceinline__ int gwarps() { return (int)((gridDim.x * blockDim.x) >> 5); }
+
+__device__ __forceinline__ void dev_pairs_count_w(const BlockArgs& A) {
+  const int col0 = block_col0(A);
+  for (int p = gwarp(); p < A.L; p += gwarps()) {
+    const WarpMerged w = warp_merged(A, col0 + p, A.j[p]);
+    if ((threadIdx.x & 31) == 0) A.pcount[p] = w.M;
+  }
+}
+__device__ __forceinline__ void dev_pairs_gen_w(const BlockArgs& A) {
+  const int col0 = block_col0(A);
+  const int lane = threadIdx.x & 31;
+  for (int p = gwarp(); p < A.L; p += gwarps()) {
+    const int i = col0 + p, j = A.j[p];
+    const double bi = A.b[i];
+    const int base = A.poff[p];
+    const WarpMerged w = warp_merged(A, i, j);
+    if (lane < w.M) {
+      const int q = base + lane;
+      A.prow[q] = w.row;
+      A.ppos[q] = p;
+      A.pd[q] = d_sub(w.row == j ? bi : 0.0, w.told);
+      if (A.ptold) A.ptold[q] = w.told;
+      if (atomicAdd(&A.rowcnt[w.row], 1) == 0) {   // order-free touched list
+        const int t = atomicAdd(A.ntouch, 1);
+        A.trows[t] = w.row;
+        A.rowidx[w.row] = t;
+      }
+    }
+  }
+}
+__device__ __forceinline__ void dev_cap_check_w(const BlockArgs& A) {
+  const int col0 = block_col0(A);
+  const double gamma = A.scal[2];
+  const double omg = d_sub(1.0, gamma);
+  for (int p = gwarp(); p < A.L; p += gwarps()) {
+    const int i = col0 + p, j = A.j[p];
+    const double gb = d_mul(gamma, A.b[i]);
+    const WarpMerged w = warp_merged(A, i, j);
+    bool kept = false;
+    if ((int)(threadIdx.x & 31) < w.M) {
+      double tn = d_mul(omg, w.told);
+      if (w.row == j) tn = d_add(tn, gb);
+      kept = tn != 0.0;
+    }
+    const int keep = __popc(__ballot_sync(FULL, kept));
+    if ((threadIdx.x & 31) == 0 && keep > A.cap) {
+      if (A.capfail) atomicOr(A.capfail, 1);
+      else set_status(A.status, 6);
+    }
+  }
+}
+// t_i <- (1-gamma) t_i + gamma s_i; exact zeros dropped (R13), as dev_update_cols
+__device__ __forceinline__ void dev_update_cols_w(const BlockArgs& A) {
+  const int col0 = block_col0(A);
+  const double gamma = A.scal[2];
+  const double omg = d_sub(1.0, gamma);
+  const int lane = threadIdx.x & 31;
+  for (int p = gwarp(); p < A.L; p += gwarps()) {
+    const int i = col0 + p, j = A.j[p];
+    const double gb = d_mul(gamma, A.b[i]);
+    const int base = A.poff[p];
+    const WarpMerged w = warp_merged(A, i, j);
+    double tn = 0.0;
+    if (lane < w.M) {
+      tn = d_mul(omg, w.told);
+      if (w.row == j) tn = d_add(tn, gb);
+      A.pdelta[base + lane] = d_sub(tn, w.told);
+    }
+    const bool kept = lane < w.M && tn != 0.0;
+    const unsigned km = __ballot_sync(FULL, kept);
+    const int e = __popc(km & ((1u << lane) - 1u));
+    if (kept && e < A.cap) {
+      A.srow[(int64_t)i * A.cap + e] = w.row;
+      A.sval[(int64_t)i * A.cap + e] = tn;
+    }
+    if (lane == 0) A.cnt[i] = __popc(km);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Kernels: one per phase (multi-CTA path) ...
 // ---------------------------------------------------------------------------
-__global__ void k_pairs_count(BlockArgs A) { pdl_entry(); if (!blk_skip(A)) dev_pairs_count(A); }
+__global__ void k_pairs_count(BlockArgs A) { pdl_entry(); if (!blk_skip(A)) dev_pairs_count_w(A); }
 __global__ void __launch_bounds__(1024) k_scan_pairs(BlockArgs A) { pdl_entry();
   if (blk_skip(A)) return;
   dev_scan_excl(A.pcount, A.L, A.poff, A.ptotal);
 }
-__global__ void k_pairs_gen(BlockArgs A) { pdl_entry(); if (!blk_skip(A)) dev_pairs_gen(A); }
-__global__ void k_runs(BlockArgs A, const double* __restrict__ val) { pdl_entry(); if (!blk_skip(A)) dev_runs(A, val); }
+__global__ void k_pairs_gen(BlockArgs A) { pdl_entry(); if (!blk_skip(A)) dev_pairs_gen_w(A); }
+// The (row, chunk) runs of one step, a CTA per chunk (grid-stride over the W chunks): the chunk's
+// pairs (contiguous: positions ascending, rows ascending within one) become (row << 12 | local
+// index) keys in shared memory, sorted (bitonic), so each row's pairs are adjacent in column
+// order; the first of each row sums them left to right from +0.0 — the sums dev_runs forms
+// (R19), without its per-pair search through the earlier columns' supports in global memory
+// (config [1] FW: 18.6 us per launch). Chunks with more than RUN_KMAX pairs, or m >= 2^20 - 1,
+// take that search.
+constexpr int RUN_KMAX = 4096;
+__global__ void __launch_bounds__(256) k_runs(BlockArgs A, const double* __restrict__ val) { pdl_entry();
+  if (blk_skip(A)) return;
+  __shared__ uint32_t key[RUN_KMAX];
+  __shared__ double sv[RUN_KMAX];
+  const int t = threadIdx.x;
+  for (int c = blockIdx.x; c < A.W; c += gridDim.x) {
+    const int lo = (int)chunk_lo(c, A.L, A.W), hi = (int)chunk_lo(c + 1, A.L, A.W);
+    const int q0 = A.poff[lo], N = A.poff[hi] - q0;
+    if (N > RUN_KMAX || A.m >= (1 << 20) - 1) {
+      for (int q = q0 + t; q < q0 + N; q += blockDim.x) run_of_pair(A, val, q);
+      continue;
+    }
+    int NP = 1;
+    while (NP < N) NP <<= 1;
+    for (int u = t; u < NP; u += blockDim.x) {
+      if (u < N) { key[u] = ((uint32_t)A.prow[q0 + u] << 12) | (uint32_t)u; sv[u] = val[q0 + u]; }
+      else key[u] = 0xffffffffu;
+    }
+    __syncthreads();
+    for (int k = 2; k <= NP; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = t; i < NP; i += blockDim.x) {
+          const int ixj = i ^ j;
+          if (ixj > i) {
+            const uint32_t a = key[i], b = key[ixj];
+            if ((a > b) == ((i & k) == 0)) { key[i] = b; key[ixj] = a; }
+          }
+        }
+        __syncthreads();
+      }
+    for (int u = t; u < N; u += blockDim.x) {
+      const uint32_t ku = key[u];
+      const uint32_t row = ku >> 12;
+      if (u > 0 && (key[u - 1] >> 12) == row) continue;
+      double s = d_add(0.0, sv[ku & 4095u]);
+      for (int v = u + 1; v < N && (key[v] >> 12) == row; v++) s = d_add(s, sv[key[v] & 4095u]);
+      const int w = A.rowidx[row];
+      const int slot = A.tstart[w] + atomicAdd(&A.tcur[w], 1);   // order-free: one entry per chunk
+      A.runc[slot] = c;
+      A.runv[slot] = s;
+    }
+    __syncthreads();
+  }
+}
 __global__ void __launch_bounds__(1024) k_touched_scan(BlockArgs A) { pdl_entry(); if (!blk_skip(A)) dev_touched_scan(A); }
 template <int MODE>
 __global__ void __launch_bounds__(256) k_row_tree_small(BlockArgs A, double* slot, int clear, int pass) {
@@ -490,8 +733,8 @@ __global__ void __launch_bounds__(256) k_row_tree_big(BlockArgs A, double* slot,
   dev_row_tree_big<MODE>(A, slot, clear != 0, pass, wsl);
 }
 __global__ void k_gamma(BlockArgs A) { pdl_entry(); if (!blk_skip(A)) dev_gamma(A); }
-__global__ void k_cap_check(BlockArgs A) { pdl_entry(); if (!blk_skip(A)) dev_cap_check(A); }
-__global__ void k_update_cols(BlockArgs A) { pdl_entry(); if (!blk_skip(A)) dev_update_cols(A); }
+__global__ void k_cap_check(BlockArgs A) { pdl_entry(); if (!blk_skip(A)) dev_cap_check_w(A); }
+__global__ void k_update_cols(BlockArgs A) { pdl_entry(); if (!blk_skip(A)) dev_update_cols_w(A); }
 __global__ void k_zero_slot(BlockArgs A, double* slot) { if (!blk_skip(A)) dev_zero_dbl(slot, A.m); }
 
 // Step start: G_U = psumW(g) (FW: stop check, Alg. A.1 line 4) into *out,
@@ -500,7 +743,7 @@ __global__ void __launch_bounds__(256) k_step_begin(BlockArgs A, double* out) { 
   if (A.stop && *A.stop) return;
   if (*A.status) return;
   if (threadIdx.x == 0) { *A.ntouch = 0; A.nbig[0] = 0; A.nbig[1] = 0; if (A.capfail) *A.capfail = 0; }
-  dev_psumW(A.g, A.L, A.W, out, A.G > 1 ? nullptr : A.eps, A.G > 1 ? nullptr : A.stop);
+  dev_psumW_any(A.g, A.L, A.W, out, A.G > 1 ? nullptr : A.eps, A.G > 1 ? nullptr : A.stop);
 }
 
 // psum256 of x[0..L) -> *out (one CTA of 256 threads). If stop_flag is given,
@@ -509,7 +752,7 @@ __global__ void __launch_bounds__(256) k_psum256(const double* __restrict__ x, i
                                                  const double* __restrict__ eps, int* stop_flag,
                                                  const int* __restrict__ stop_in) { pdl_entry();
   if (stop_in && *stop_in) return;
-  dev_psumW(x, L, 256, out, eps, stop_flag);
+  dev_psumW_any(x, L, 256, out, eps, stop_flag);
 }
 
 __global__ void k_step_done(BlockArgs A) { pdl_entry();

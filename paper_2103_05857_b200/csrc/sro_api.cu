@@ -1409,7 +1409,7 @@ sro_status plain_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
     s->lead->stats.kernel_launches += 1;
   } else {
     const int tpb = 256;
-    int gL = (L + tpb - 1) / tpb; if (gL > s->num_sms * 8) gL = s->num_sms * 8;
+    int gL = (L + tpb / 32 - 1) / (tpb / 32); if (gL > s->num_sms * 8) gL = s->num_sms * 8;   // warp per column
     const int gP = s->num_sms * 8;
     const int gR = (s->m + 7) / 8 < s->num_sms * 8 ? (s->m + 7) / 8 : s->num_sms * 8;
     CUDA_TRY(s, launch_pdl(k_step_begin, dim3(1), dim3(256), 0, s->stream, A, s->scal + 0));
@@ -1417,13 +1417,13 @@ sro_status plain_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
     CUDA_TRY(s, launch_pdl(k_scan_pairs, dim3(1), dim3(1024), 0, s->stream, A));
     CUDA_TRY(s, launch_pdl(k_pairs_gen, dim3(gL), dim3(tpb), 0, s->stream, A));
     CUDA_TRY(s, launch_pdl(k_touched_scan, dim3(1), dim3(1024), 0, s->stream, A));
-    CUDA_TRY(s, launch_pdl(k_runs, dim3(gP), dim3(tpb), 0, s->stream, A, s->pd));
+    CUDA_TRY(s, launch_pdl(k_runs, dim3(A.W), dim3(tpb), 0, s->stream, A, s->pd));
     CUDA_TRY(s, launch_pdl(k_row_tree_all<0>, dim3(gR), dim3(256), 0, s->stream, A, nullptr, 0));
     CUDA_TRY(s, launch_pdl(k_psum256, dim3(1), dim3(256), 0, s->stream, s->X, s->m, s->scal + 1, nullptr, nullptr, stop));
     CUDA_TRY(s, launch_pdl(k_gamma, dim3(1), dim3(32), 0, s->stream, A));
     CUDA_TRY(s, launch_pdl(k_cap_check, dim3(gL), dim3(tpb), 0, s->stream, A));
     CUDA_TRY(s, launch_pdl(k_update_cols, dim3(gL), dim3(tpb), 0, s->stream, A));
-    CUDA_TRY(s, launch_pdl(k_runs, dim3(gP), dim3(tpb), 0, s->stream, A, s->pdelta));
+    CUDA_TRY(s, launch_pdl(k_runs, dim3(A.W), dim3(tpb), 0, s->stream, A, s->pdelta));
     CUDA_TRY(s, launch_pdl(k_row_tree_all<1>, dim3(gR), dim3(256), 0, s->stream, A, nullptr, 1));
     CUDA_TRY(s, launch_pdl(k_step_done, dim3(1), dim3(32), 0, s->stream, A));
     CUDA_TRY(s, cudaGetLastError());
@@ -1447,7 +1447,7 @@ sro_status shard_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
   const int trb = timed_begin(s);
   const bool tail = L <= 1024 && !s->no_tail;
   const int tpb = 256;
-  int gL = (L + tpb - 1) / tpb; if (gL > s->num_sms * 8) gL = s->num_sms * 8;
+  int gL = (L + tpb / 32 - 1) / (tpb / 32); if (gL > s->num_sms * 8) gL = s->num_sms * 8;   // warp per column
   const int gP = s->num_sms * 8;
   const int gR = (s->m + 7) / 8 < s->num_sms * 8 ? (s->m + 7) / 8 : s->num_sms * 8;
   std::vector<BlockArgs> AA;
@@ -1472,7 +1472,7 @@ sro_status shard_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
       k_zero_slot<<<gR, 256, 0, s->stream>>>(A, s1);
       k_pairs_gen<<<gL, tpb, 0, s->stream>>>(A);
       k_touched_scan<<<1, 1024, 0, s->stream>>>(A);
-      k_runs<<<gP, tpb, 0, s->stream>>>(A, t->pd);
+      k_runs<<<A.W, tpb, 0, s->stream>>>(A, t->pd);
       k_row_tree_all<2><<<gR, 256, 0, s->stream>>>(A, s1, 0);
       k_publish_a<<<1, 32, 0, s->stream>>>(A);
       s->stats.kernel_launches += 9;
@@ -1494,7 +1494,7 @@ sro_status shard_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
       k_cap_check<<<gL, tpb, 0, s->stream>>>(A);
       k_zero_slot<<<gR, 256, 0, s->stream>>>(A, s2);
       k_update_cols<<<gL, tpb, 0, s->stream>>>(A);
-      k_runs<<<gP, tpb, 0, s->stream>>>(A, t->pdelta);
+      k_runs<<<A.W, tpb, 0, s->stream>>>(A, t->pdelta);
       k_row_tree_all<2><<<gR, 256, 0, s->stream>>>(A, s2, 1);
       k_publish_b<<<1, 32, 0, s->stream>>>(A);
       s->stats.kernel_launches += 7;
@@ -2229,7 +2229,7 @@ sro_status plan_row_sums(Solver* s, const double* y_dev, const int* chans, int n
   for (int c = 0; c < nch; c++) {
     CUDA_TRY(s, cudaMemsetAsync(out[c], 0, sizeof(double) * s->m, s->stream));
     k_plan_channel<<<gP, tpb, 0, s->stream>>>(A, y_dev, chans[c], s->pdelta);
-    k_runs<<<gP, tpb, 0, s->stream>>>(A, s->pdelta);
+    k_runs<<<A.W, tpb, 0, s->stream>>>(A, s->pdelta);
     k_row_tree_all<2><<<gR, 256, 0, s->stream>>>(A, out[c], c == nch - 1 ? 1 : 0);
   }
   s->lead->stats.kernel_launches += 5 + 3 * nch;

@@ -96,14 +96,29 @@ __device__ __forceinline__ double warp_pair_tree(double v) {
   return v;
 }
 
+// x[lo] + x[lo+1] + ... + x[hi-1] left to right from +0.0 (a chunk of R19's 256-chunk tree),
+// with 16 loads in flight per batch: a thread's chunk is latency-bound, not bandwidth-bound
+// (config [3]: 256 doubles per chunk, the one-at-a-time loop took ~30 us per psum256)
+__device__ __forceinline__ double chunk_seq_sum(const double* __restrict__ x, int64_t lo, int64_t hi) {
+  double acc = 0.0;
+  int64_t p = lo;
+  for (; p + 16 <= hi; p += 16) {
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; u++) v[u] = x[p + u];
+#pragma unroll
+    for (int u = 0; u < 16; u++) acc = d_add(acc, v[u]);
+  }
+  for (; p < hi; p++) acc = d_add(acc, x[p]);
+  return acc;
+}
+
 // psum256 (R19) of x[0..L) for a CTA of exactly 256 threads: thread c sums
 // chunk c left to right from +0.0, then the 256 partials combine by adjacent
 // pairs. Returns the total to every thread. `red` is __shared__ double[8].
 __device__ __forceinline__ double block_psum256(const double* __restrict__ x, int64_t L, double* red) {
   const int c = threadIdx.x;
-  double acc = 0.0;
-  const int64_t lo = chunk_lo(c, L, 256), hi = chunk_lo(c + 1, L, 256);
-  for (int64_t p = lo; p < hi; p++) acc = d_add(acc, x[p]);
+  double acc = chunk_seq_sum(x, chunk_lo(c, L, 256), chunk_lo(c + 1, L, 256));
   acc = warp_pair_tree(acc);
   if ((c & 31) == 0) red[c >> 5] = acc;
   __syncthreads();
