@@ -464,14 +464,15 @@ def configs_legs_single(local_rank):
         s.close()
         sweep_ms = st["sweep_ms"] / max(1, st["sweep_launches"])
         ent = float(d["m"]) * d["n"]
-        # the fused colour sweep is bound by instruction issue, not memory: 16 SASS instructions
-        # per (row, column) entry in its inner loop (k_lmo_sweep<SrcColour<float>, 4>, 128 per
-        # 2 rows x 4 columns: 8 fp32 ops, F2F, DADD, DSETP, 2.75 selects, 1 LDS), one issue per
-        # cycle per SM sub-partition
+        # the fused colour sweep is bound by instruction issue, not memory: 201 SASS instructions
+        # per 4 rows x 4 columns in its inner loop (k_lmo_sweep<SrcColour<float>, 4, 512>: 24 FADD2 +
+        # 24 FMUL2 for the packed differences and squares, 32 FADD, 16 F2F, 16 DADD, 16 DSETP, 44
+        # selects, 8 LDS, ...), one issue per cycle per SM sub-partition
         import torch
         sms = torch.cuda.get_device_properties(local_rank).multi_processor_count
         mhz = float(measured_peaks().get("sm_max_mhz", 1965.0))
-        issue_peak = sms * 4 * mhz * 1e6 * 32 / 16.0
+        per_entry = 201 / 16.0
+        issue_peak = sms * 4 * mhz * 1e6 * 32 / per_entry
         out[f"config{cfg}"] = {
             "workload": f"BASELINE configs[{cfg}]: m={d['m']}, n={d['n']}, fused fp32 sqeuclid, batched B={B}, P, ELS",
             "time_to_gap_ms": round(r["device_ms"], 3), "block_steps": r["iters_done"],
@@ -482,7 +483,8 @@ def configs_legs_single(local_rank):
             "gap_sweep_roofline": {"bound": "alu", "achieved": ent / (sweep_ms * 1e-3), "peak": issue_peak,
                                    "unit": "entries/s", "frac": round(ent / (sweep_ms * 1e-3) / issue_peak, 4),
                                    "peak_derivation": f"{sms} SMs x 4 sub-partitions x {mhz:.0f} MHz x 32 lanes / "
-                                                      "16 instructions per entry (SASS of the inner loop)"}}
+                                                      "12.56 instructions per entry (SASS of the inner loop, "
+                                                      "packed fp32; the unpacked loop took 16)"}}
     return out
 
 
