@@ -417,30 +417,34 @@ __device__ __forceinline__ double dev_psumW(const double* __restrict__ x, int64_
 constexpr int PSUM_K = 16;
 __device__ __forceinline__ double dev_psumW_tiled(const double* __restrict__ x, int64_t L, int W, double* out,
                                                   const double* eps, int* stop_flag) {
+  // threads 0..255 load and sum; a larger CTA's other threads only take part in the barriers
   __shared__ double tile[256][PSUM_K + 1];
   __shared__ int64_t rlo[257];
   __shared__ double red[8];
   const int c = threadIdx.x;
-  rlo[c] = c < W ? chunk_lo(c, L, W) : L;
+  const bool act = c < 256;
+  if (act) rlo[c] = c < W ? chunk_lo(c, L, W) : L;
   if (c == 0) rlo[256] = L;
   __syncthreads();
   const int64_t maxlen = (L + W - 1) / W;
-  const int u = c & 15, r0 = c >> 4;
+  const int u = c & 15, r0 = (c & 255) >> 4;
   double nv[16];
   auto load = [&](int64_t U) {
 #pragma unroll
     for (int k = 0; k < 16; k++) {
       const int r = r0 + 16 * k;
       const int64_t q = rlo[r] + U + u;
-      nv[k] = (r < W && q < rlo[r + 1]) ? x[q] : 0.0;
+      nv[k] = (act && r < W && q < rlo[r + 1]) ? x[q] : 0.0;
     }
   };
   load(0);
   double acc = 0.0;
   const int64_t len = c < W ? rlo[c + 1] - rlo[c] : 0;
   for (int64_t U = 0; U < maxlen; U += PSUM_K) {
+    if (act) {
 #pragma unroll
-    for (int k = 0; k < 16; k++) tile[r0 + 16 * k][u] = nv[k];
+      for (int k = 0; k < 16; k++) tile[r0 + 16 * k][u] = nv[k];
+    }
     __syncthreads();
     if (U + PSUM_K < maxlen) load(U + PSUM_K);
     const int64_t rem = len - U;
@@ -448,8 +452,10 @@ __device__ __forceinline__ double dev_psumW_tiled(const double* __restrict__ x, 
     for (int e = 0; e < kk; e++) acc = d_add(acc, tile[c][e]);
     __syncthreads();
   }
-  acc = warp_pair_tree(acc);
-  if ((c & 31) == 0) red[c >> 5] = acc;
+  if (act) {
+    acc = warp_pair_tree(acc);
+    if ((c & 31) == 0) red[c >> 5] = acc;
+  }
   __syncthreads();
   if (c < 32) {
     double v = (c < 8) ? red[c] : 0.0;
@@ -653,6 +659,17 @@ __device__ __forceinline__ void dev_update_cols_w(const BlockArgs& A) {
 // Kernels: one per phase (multi-CTA path) ...
 // ---------------------------------------------------------------------------
 __global__ void k_pairs_count(BlockArgs A) { pdl_entry(); if (!blk_skip(A)) dev_pairs_count_w(A); }
+// Step start and pair offsets in one launch (unsharded multi-CTA step, after k_pairs_count): G_U =
+// psumW(g) with the FW stop check (Alg. A.1 line 4) and the counter resets of k_step_begin, then,
+// unless the step stops, the exclusive scan of the merged-support sizes. One CTA of 1024 threads.
+__global__ void __launch_bounds__(1024) k_begin_scan(BlockArgs A, double* out) { pdl_entry();
+  if (A.stop && *A.stop) return;
+  if (*A.status) return;
+  if (threadIdx.x == 0) { *A.ntouch = 0; A.nbig[0] = 0; A.nbig[1] = 0; if (A.capfail) *A.capfail = 0; }
+  const double gu = dev_psumW_any(A.g, A.L, A.W, out, A.eps, A.stop);
+  if (A.stop && A.eps && gu <= *A.eps) return;
+  dev_scan_excl(A.pcount, A.L, A.poff, A.ptotal);
+}
 __global__ void __launch_bounds__(1024) k_scan_pairs(BlockArgs A) { pdl_entry();
   if (blk_skip(A)) return;
   dev_scan_excl(A.pcount, A.L, A.poff, A.ptotal);
@@ -733,6 +750,13 @@ __global__ void __launch_bounds__(256) k_row_tree_big(BlockArgs A, double* slot,
   dev_row_tree_big<MODE>(A, slot, clear != 0, pass, wsl);
 }
 __global__ void k_gamma(BlockArgs A) { pdl_entry(); if (!blk_skip(A)) dev_gamma(A); }
+// The denominator psum256 of Delta_k^2 over the m rows and gamma in one launch (unsharded multi-CTA
+// step; thread 0 writes scal[1] and reads it back for gamma). One CTA of 256 threads.
+__global__ void __launch_bounds__(256) k_den_gamma(BlockArgs A) { pdl_entry();
+  if (blk_skip(A)) return;
+  dev_psumW_any(A.X, A.m, 256, A.scal + 1, nullptr, nullptr);
+  dev_gamma(A);
+}
 __global__ void k_cap_check(BlockArgs A) { pdl_entry(); if (!blk_skip(A)) dev_cap_check_w(A); }
 __global__ void k_update_cols(BlockArgs A) { pdl_entry(); if (!blk_skip(A)) dev_update_cols_w(A); }
 __global__ void k_zero_slot(BlockArgs A, double* slot) { if (!blk_skip(A)) dev_zero_dbl(slot, A.m); }

@@ -1412,22 +1412,22 @@ sro_status plain_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
     int gL = (L + tpb / 32 - 1) / (tpb / 32); if (gL > s->num_sms * 8) gL = s->num_sms * 8;   // warp per column
     const int gP = s->num_sms * 8;
     const int gR = (s->m + 7) / 8 < s->num_sms * 8 ? (s->m + 7) / 8 : s->num_sms * 8;
-    CUDA_TRY(s, launch_pdl(k_step_begin, dim3(1), dim3(256), 0, s->stream, A, s->scal + 0));
+    // k_pairs_count first (it needs nothing from the step start), then G_U / stop check / resets and
+    // the pair scan in one single-CTA launch; the denominator and gamma in one launch
     CUDA_TRY(s, launch_pdl(k_pairs_count, dim3(gL), dim3(tpb), 0, s->stream, A));
-    CUDA_TRY(s, launch_pdl(k_scan_pairs, dim3(1), dim3(1024), 0, s->stream, A));
+    CUDA_TRY(s, launch_pdl(k_begin_scan, dim3(1), dim3(1024), 0, s->stream, A, s->scal + 0));
     CUDA_TRY(s, launch_pdl(k_pairs_gen, dim3(gL), dim3(tpb), 0, s->stream, A));
     CUDA_TRY(s, launch_pdl(k_touched_scan, dim3(1), dim3(1024), 0, s->stream, A));
     CUDA_TRY(s, launch_pdl(k_runs, dim3(A.W), dim3(tpb), 0, s->stream, A, s->pd));
     CUDA_TRY(s, launch_pdl(k_row_tree_all<0>, dim3(gR), dim3(256), 0, s->stream, A, nullptr, 0));
-    CUDA_TRY(s, launch_pdl(k_psum256, dim3(1), dim3(256), 0, s->stream, s->X, s->m, s->scal + 1, nullptr, nullptr, stop));
-    CUDA_TRY(s, launch_pdl(k_gamma, dim3(1), dim3(32), 0, s->stream, A));
+    CUDA_TRY(s, launch_pdl(k_den_gamma, dim3(1), dim3(256), 0, s->stream, A));
     CUDA_TRY(s, launch_pdl(k_cap_check, dim3(gL), dim3(tpb), 0, s->stream, A));
     CUDA_TRY(s, launch_pdl(k_update_cols, dim3(gL), dim3(tpb), 0, s->stream, A));
     CUDA_TRY(s, launch_pdl(k_runs, dim3(A.W), dim3(tpb), 0, s->stream, A, s->pdelta));
     CUDA_TRY(s, launch_pdl(k_row_tree_all<1>, dim3(gR), dim3(256), 0, s->stream, A, nullptr, 1));
     CUDA_TRY(s, launch_pdl(k_step_done, dim3(1), dim3(32), 0, s->stream, A));
     CUDA_TRY(s, cudaGetLastError());
-    s->lead->stats.kernel_launches += 14;
+    s->lead->stats.kernel_launches += 12;
   }
   s->lead->stats.block_steps += 1;
   s->lead->k_pending += 1;
