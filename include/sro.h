@@ -103,7 +103,8 @@ typedef struct {
   int32_t nranks;       /* processes sharing the G shards: 1 = this process holds all G shards and
                            runs them in sequence on its stream (exchanges are in-place device
                            writes), or G = one shard per process exchanged with NCCL all-gathers
-                           on cuda_stream (libnccl.so.2 loaded at run time) or with the host
+                           on cuda_stream (libnccl.so.2 loaded at run time: the one already in the process, else
+                           $SRO_NCCL_LIB, else the loader's default) or with the host
                            all-gather `exchange` */
   int32_t rank;         /* this process's shard when nranks == G */
   const void* nccl_id;  /* 128-byte ncclUniqueId (sro_nccl_unique_id on rank 0, shared by the

@@ -38,6 +38,7 @@ namespace sro {
 
 struct BlockArgs {
   int m, n, cap;
+  int runs_kmax;         // k_runs: chunks with more pairs search the supports instead (<= RUN_KMAX)
   double lambda;
   const double* a;
   const double* b;
@@ -691,7 +692,7 @@ __global__ void __launch_bounds__(256) k_runs(BlockArgs A, const double* __restr
   for (int c = blockIdx.x; c < A.W; c += gridDim.x) {
     const int lo = (int)chunk_lo(c, A.L, A.W), hi = (int)chunk_lo(c + 1, A.L, A.W);
     const int q0 = A.poff[lo], N = A.poff[hi] - q0;
-    if (N > RUN_KMAX || A.m >= (1 << 20) - 1) {
+    if (N > A.runs_kmax || A.m >= (1 << 20) - 1) {
       for (int q = q0 + t; q < q0 + N; q += blockDim.x) run_of_pair(A, val, q);
       continue;
     }

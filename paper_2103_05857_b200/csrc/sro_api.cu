@@ -56,7 +56,12 @@ NcclApi& nccl() {
   static NcclApi api;
   if (api.tried) return api;
   api.tried = true;
-  void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  // the NCCL the process already uses (torch's), else SRO_NCCL_LIB (the Python binding points it at
+  // the wheel torch ships), else the loader's default: loading an older system libnccl.so.2 first
+  // would break a later `import torch` (its libtorch_cuda needs the newer NCCL's symbols)
+  void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+  if (!lib && getenv("SRO_NCCL_LIB")) lib = dlopen(getenv("SRO_NCCL_LIB"), RTLD_NOW | RTLD_GLOBAL);
+  if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
   if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
   if (!lib) { api.err = std::string("cannot load libnccl.so.2: ") + dlerror(); return api; }
   api.get_id = (decltype(api.get_id))dlsym(lib, "ncclGetUniqueId");
@@ -174,6 +179,8 @@ struct Solver {
   bool no_rf = getenv("SRO_NO_RF") != nullptr;      // debug: force the shared-memory kernel
   bool no_tail = getenv("SRO_NO_TAIL") != nullptr;  // debug: force the multi-kernel block step
   bool no_smtail = getenv("SRO_NO_SMTAIL") != nullptr;  // debug: force the global-memory single-CTA tail
+  // debug: chunks with more pairs than this take k_runs' support search instead of its sort (0: all)
+  int runs_kmax = getenv("SRO_RUNS_KMAX") ? std::max(0, std::min(RUN_KMAX, atoi(getenv("SRO_RUNS_KMAX")))) : RUN_KMAX;
   // k_block_coop (one cooperative launch, grid barriers) measured slower than the per-phase
   // kernels replayed from a CUDA graph (FW config [1]: 40 vs 34 ms): opt-in only
   bool no_coop = getenv("SRO_COOP") == nullptr;
@@ -1333,6 +1340,7 @@ BlockArgs block_args(Solver* s, const int* col0_dev, int col0_mul, int L, int st
   A.m = s->m; A.n = s->n; A.cap = s->cap; A.lambda = s->lambda; A.a = s->a; A.b = s->b; A.r = s->r; A.h = s->h;
   A.cnt = s->cnt; A.srow = s->srow; A.sval = s->sval; A.col0_dev = col0_dev; A.col0_mul = col0_mul; A.L = L;
   A.W = 256 / s->G;
+  A.runs_kmax = s->runs_kmax;
   A.j = s->sw_j; A.minval = s->sw_min; A.g = s->sw_g; A.pcount = s->pcount; A.poff = s->poff; A.ptotal = s->ptotal;
   A.prow = s->prow; A.ppos = s->ppos; A.pd = s->pd; A.ptold = s->G > 1 ? s->ptold : nullptr; A.pdelta = s->pdelta;
   A.rowcnt = s->rowcnt; A.rowidx = s->rowidx; A.trows = s->trows; A.ntouch = s->ntouch; A.X = s->X;

@@ -19,6 +19,27 @@ __all__ = [
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SRO_LIB", os.path.join(HERE, "libsro.so"))
 
+
+def _default_nccl_lib():
+    """The libnccl.so.2 of the nvidia-nccl wheel torch is built against (the library dlopens NCCL
+    for sharded handles; an older system copy loaded first would break a later `import torch`)."""
+    import importlib.util
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return None
+    for d in (spec.submodule_search_locations or []) if spec else []:
+        p = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(p):
+            return p
+    return None
+
+
+if "SRO_NCCL_LIB" not in os.environ:
+    _nccl = _default_nccl_lib()
+    if _nccl:
+        os.environ["SRO_NCCL_LIB"] = _nccl
+
 SRO_FW, SRO_BCFW, SRO_BCAFW, SRO_BCPFW, SRO_BATCHED = 0, 1, 2, 3, 4
 STEP_DEC, STEP_ELS = 0, 1
 SAMPLE_U, SAMPLE_P, SAMPLE_GA = 0, 1, 2

@@ -276,14 +276,19 @@ def test_config0_shared_memory_kernel_bitexact(name, ov, gv, kw, monkeypatch):
     assert_same_state(g, o)
 
 
-@pytest.mark.parametrize("coop", [True, False], ids=["cooperative", "per-phase"])
+@pytest.mark.parametrize("coop,runs", [(True, "sort"), (False, "sort"), (False, "search")],
+                         ids=["cooperative", "per-phase", "per-phase-run-search"])
 @pytest.mark.parametrize("variant,B", [(BATCHED, 16), (FW, 0)])
-def test_block_step_multikernel_path_bitexact(variant, B, coop, monkeypatch):
+def test_block_step_multikernel_path_bitexact(variant, B, coop, runs, monkeypatch):
     """The large-U block step (one cooperative launch, or the per-phase kernels) forced on
-    small instances: same bit-exact trajectory as the single-CTA tail path and the oracle."""
+    small instances: same bit-exact trajectory as the single-CTA tail path and the oracle. The
+    per-phase k_runs forms the (row, chunk) runs by a per-chunk key sort, or (SRO_RUNS_KMAX=0, its
+    fallback for chunks of more than 4096 pairs) by searching the earlier columns' supports."""
     monkeypatch.setenv("SRO_NO_TAIL", "1")
     if coop:
         monkeypatch.setenv("SRO_COOP", "1")
+    if runs == "search":
+        monkeypatch.setenv("SRO_RUNS_KMAX", "0")
     d = instance(1, m=300, n=256, seed=8)
     g, o = pair(d, prec="f32")
     kw = dict(block_size=B, sampling=P) if B else {}
