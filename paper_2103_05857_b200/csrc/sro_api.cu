@@ -672,10 +672,10 @@ sro_status sweep_bulk(Solver* s, Src src, const int* col0_dev, int col0_mul, int
   // columns (a batched block) so that every SM still gets several items
   int slab = s->slab_bulk;
   {
-    // about four (slab, column) items per SM: fewer, longer slabs leave fewer partials for a block
-    // step's single-CTA tail (batched config [1], B = 256, with 8-warp CTAs: 35.3 us per block step
-    // at 16 items per SM, 8: 34.5, 4: 33.7, 2.8: 35.3, 2: 37.5; SRO_BULK_ITEMS overrides for A/B)
-    static const double items_per_sm = getenv("SRO_BULK_ITEMS") ? atof(getenv("SRO_BULK_ITEMS")) : 4.0;
+    // about twelve (slab, column) items per SM (batched config [1], B = 256, us per block step at
+    // 4 / 8 / 12 / 16 / 24 items per SM: 33.0 / 31.3 / 30.7 / 32.7 / 33.4 with the round-2 tail, whose
+    // slab merge is no longer the long pole; round 1 had 4 as best; SRO_BULK_ITEMS overrides for A/B)
+    static const double items_per_sm = getenv("SRO_BULK_ITEMS") ? atof(getenv("SRO_BULK_ITEMS")) : 12.0;
     const int64_t target = (int64_t)((double)s->num_sms * items_per_sm);
     const int64_t want = ((int64_t)s->m * L + target - 1) / target;
     if (want < slab) slab = (int)std::max<int64_t>(256, (want + 3) / 4 * 4);
