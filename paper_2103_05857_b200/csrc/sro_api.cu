@@ -764,7 +764,8 @@ sro_status sweep(Solver* s, const int* col0_dev, int col0_mul, int col0_host, in
     const int nslabs = (s->m + slab - 1) / slab;
     { sro_status st = ensure_partials(s, nslabs, L); if (st) return st; }
     const int rows = s->m < slab ? s->m : slab;
-    const size_t smem = sizeof(double) * (size_t)((rows + 1) & ~1) + (size_t)Src::SMEM_PER_ROW * rows;
+    // (+ 16 B: the binary32 colour planes start at even offsets, so one row takes 3 x 2 floats)
+    const size_t smem = sizeof(double) * (size_t)((rows + 1) & ~1) + (size_t)Src::SMEM_PER_ROW * rows + 16;
     const int cols = multi ? Src::COLS : 1;
     // the multi-column colour sweep runs CTAs of 16 warps (twice the warps in flight per SM
     // for the same staged slab)

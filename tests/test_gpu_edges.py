@@ -135,3 +135,47 @@ def test_batched_ga_past_4096_steps_bitexact():
         for f in ("k", "i", "j", "gamma", "num", "den"):
             assert np.array_equal(rg["trace"][f], ro["trace"][f]), f
     assert np.array_equal(g.plan(), o.plan())
+
+
+COLOUR_CASES = [("one_row", 1, 37), ("one_col", 41, 1), ("one_by_one", 1, 1), ("ragged", 257, 35), ("ragged", 5, 3),
+                ("ragged", 1031, 13), ("ragged", 929, 300), ("wide", 33, 9476)]
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("cost", ["sqeuclid", "euclid"])
+@pytest.mark.parametrize("case,m,n", COLOUR_CASES, ids=[f"{c[0]}-{c[1]}x{c[2]}" for c in COLOUR_CASES])
+@pytest.mark.parametrize("name,ov,gv,kw", [RUNS[0], RUNS[5], RUNS[7]], ids=[RUNS[q][0] for q in (0, 5, 7)])
+def test_degenerate_colour_inputs_bitexact(case, m, n, name, ov, gv, kw, cost, prec):
+    """Fused colour costs (the sweeps' packed binary32 paths: row pairs with an odd last row, planar
+    slabs of one row, blocks of one column) on ragged and degenerate shapes: bit-exact trajectories,
+    plans, gaps and objectives against the oracle."""
+    X, _, _ = mixture_colours(m, 4, 0.05, 31)
+    Y, _, _ = mixture_colours(n, 4, 0.05, 32)
+    rng = np.random.default_rng(7)
+    a = rng.random(m) + 0.05
+    b = rng.random(n) + 0.05
+    a /= a.sum()
+    b /= b.sum()
+    kw = dict(kw)
+    if ov == BATCHED:
+        B = next(d for d in (16, 8, 5, 4, 3, 2, 1) if n % d == 0)
+        kw["block_size"] = B
+        iters = 3 * (n // B)
+    elif ov == FW:
+        iters = 6
+    else:
+        iters = 3 * n
+    g = sro.Solver(a, b, 1.0, X=X, Y=Y, cost=cost, prec=prec)
+    o = Oracle(a, b, 1.0, X=X, Y=Y, cost=cost, prec=prec, cap=31)
+    ro = o.solve(ov, iters, seed=5, trace=True, epsilon=-1.0, **kw)
+    rg = g.solve(gv, iters, seed=5, trace=True, epsilon=-1.0, **kw)
+    assert rg["iters_done"] == ro["iters_done"]
+    for f in ("k", "i", "j", "gamma", "num", "den", "minval"):
+        assert np.array_equal(rg["trace"][f], ro["trace"][f]), f
+    assert np.array_equal(g.plan(), o.plan())
+    assert np.array_equal(g.rowsums(), o.r())
+    tg, gg, jg = g.gap()
+    to, go, jo, _ = o.gap()
+    assert tg == to and np.array_equal(gg, go) and np.array_equal(jg, jo)
+    assert g.objective() == o.objective()
+    g.close()
