@@ -54,6 +54,7 @@ struct SrcDense {
   const T* C;
   int64_t ld;
   static constexpr int SMEM_PER_ROW = 0;
+  static constexpr bool WIDE = false;   // 512-thread multi-column sweeps (k_lmo_sweep NT)
   static constexpr bool PLANAR = true;
   static constexpr int COLS = 1;
   template <int NCOL>
@@ -153,6 +154,7 @@ struct SrcColour {
   // binary64: three planes
   static constexpr bool PACKED = sizeof(T) == 4;
   static constexpr int SMEM_PER_ROW = PACKED ? 16 : 3 * sizeof(T);
+  static constexpr bool WIDE = PACKED;   // 512-thread multi-column sweeps (k_lmo_sweep NT)
   static constexpr bool PLANAR = false;
 #ifndef SRO_COLOUR_COLS
 #define SRO_COLOUR_COLS 4
@@ -369,10 +371,11 @@ __device__ __forceinline__ void stage_terms(const Src& src, const SweepOut& out,
 
 // grid = (gx, nslabs). col0 = col0_dev ? col0_dev[cur ? *cur : 0] * col0_mul : col0_host
 // (cur: a device step cursor, so that the launches of consecutive block steps are identical).
-// NT threads per CTA: 256, or 512 for the fused colour sweep over full slabs (two CTAs of 16 warps
-// per SM hide the fp32 -> fp64 add -> compare chains better than two of 8; <= 64 registers)
+// NT threads per CTA: 256, or 512 for the packed binary32 colour sweep over full slabs (two CTAs of
+// 16 warps per SM hide the fp32 -> fp64 add -> compare chains better than two of 8; <= 64 registers,
+// so only the packed source takes it: the binary64 euclid scan would spill)
 template <class Src, int NCOL = Src::COLS, int NT = SWEEP_THREADS>
-__global__ void __launch_bounds__(NT, 1024 / NT) k_lmo_sweep(Src src, int m, int slab_rows, const double* __restrict__ h,
+__global__ void __launch_bounds__(NT, NT > SWEEP_THREADS ? 2 : 1) k_lmo_sweep(Src src, int m, int slab_rows, const double* __restrict__ h,
                                                              const int* __restrict__ col0_dev, const unsigned* __restrict__ cur, int col0_mul,
                                                              int col0_host, int L, const int* __restrict__ cnt,
                                                              const int* __restrict__ srow,

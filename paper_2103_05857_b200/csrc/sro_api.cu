@@ -742,7 +742,7 @@ sro_status sweep(Solver* s, const int* col0_dev, int col0_mul, int col0_host, in
       if (rows_want < 128) rows_want = 128;
       if (rows_want < slab) slab = (int)rows_want;
     }
-    if (multi && sweep_nt_wide() && !getenv_slab_fixed()) {
+    if (Src::WIDE && multi && sweep_nt_wide() && !getenv_slab_fixed()) {
       // a warp's work items are (slab, 4 columns); halve the slab (down to 1024 rows) while that
       // evens out the items per warp (config [2]: 4096-row slabs leave 3.46 items per warp,
       // 2048-row slabs 6.92)
@@ -769,9 +769,11 @@ sro_status sweep(Solver* s, const int* col0_dev, int col0_mul, int col0_host, in
     const int cols = multi ? Src::COLS : 1;
     // the multi-column colour sweep runs CTAs of 16 warps (twice the warps in flight per SM
     // for the same staged slab)
-    const int nt = multi && sweep_nt_wide() ? 2 * SWEEP_THREADS : SWEEP_THREADS;
-    auto kern = multi ? (nt > SWEEP_THREADS ? k_lmo_sweep<Src, Src::COLS, 2 * SWEEP_THREADS> : k_lmo_sweep<Src, Src::COLS>)
-                      : k_lmo_sweep<Src, 1>;
+    constexpr bool wide_ok = Src::WIDE;   // the packed binary32 colour source
+    const int nt = wide_ok && multi && sweep_nt_wide() ? 2 * SWEEP_THREADS : SWEEP_THREADS;
+    auto kern = k_lmo_sweep<Src, 1>;
+    if (multi) kern = k_lmo_sweep<Src, Src::COLS>;
+    if constexpr (wide_ok) { if (nt > SWEEP_THREADS) kern = k_lmo_sweep<Src, Src::COLS, 2 * SWEEP_THREADS>; }
     CUDA_TRY(s, set_dyn_smem((const void*)kern, s->device, (int)smem));
     int per_sm = 0;
     CUDA_TRY(s, occupancy((const void*)kern, s->device, nt, smem, &per_sm));
