@@ -150,8 +150,8 @@ template <typename T, bool EUCLID>
 struct SrcColour {
   const T* x;   // 3m
   const T* y;   // 3n
-  // binary32 colours: one 16-byte (x0, x1, x2, 0) record per row (one LDS.128 per row);
-  // binary64: three planes
+  // staged colours: binary32 multi-column sweeps one 16-byte (x0, x1, x2, 0) record per row (one
+  // LDS.128 per row), everything else three planes (SMEM_PER_ROW covers both layouts)
   static constexpr bool PACKED = sizeof(T) == 4;
   static constexpr int SMEM_PER_ROW = PACKED ? 16 : 3 * sizeof(T);
   static constexpr bool WIDE = PACKED;   // 512-thread multi-column sweeps (k_lmo_sweep NT)
@@ -159,11 +159,14 @@ struct SrcColour {
 #ifndef SRO_COLOUR_COLS
 #define SRO_COLOUR_COLS 4
 #endif
-#ifndef SRO_COLOUR_UNROLL   // rows per unrolled iteration of the 4-column scan: 1 / 2 / 4 / 6 / 8 measured
-#define SRO_COLOUR_UNROLL 4   // 1.26 / 1.36 / 1.46 / 1.48 / 1.48e12 entries/s at config [2]
+// rows per unrolled iteration of the 4-column scan. Unpacked loop, 1 / 2 / 4 / 6 / 8 rows: 1.26 /
+// 1.36 / 1.46 / 1.48 / 1.48e12 entries/s at config [2]; packed loop, 2 / 4 / 8: 1.65 / 1.67 / 1.69e12,
+// but 8 spills the binary64 and euclid instantiations under the 64-register cap
+#ifndef SRO_COLOUR_UNROLL
+#define SRO_COLOUR_UNROLL 4
 #endif
-  static constexpr int COLS = SRO_COLOUR_COLS;
-  static constexpr int UNROLL = SRO_COLOUR_UNROLL;   // rows per unrolled iteration of scan_multi   // columns a warp evaluates per loaded row (registers hold their y)
+  static constexpr int COLS = SRO_COLOUR_COLS;   // columns a warp evaluates per loaded row (registers hold their y)
+  static constexpr int UNROLL = SRO_COLOUR_UNROLL;
   __device__ __forceinline__ static int hidx(int k, int) { return k; }
   // planes (x0 | x1 | x2) of the slab's colours; binary32 planes start at even offsets so that a
   // lane reads two consecutive rows of a coordinate as one packed pair
