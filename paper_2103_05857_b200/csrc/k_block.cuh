@@ -734,13 +734,32 @@ __global__ void __launch_bounds__(256) k_row_tree_small(BlockArgs A, double* slo
   if (!blk_skip(A)) dev_row_tree_small<MODE>(A, slot, clear != 0, pass);
 }
 // Warp per touched row over every touched row (the multi-CTA path: one launch).
+// done_ticket (the unsharded step's last kernel): the last CTA to finish also does k_step_done's
+// work — the step count and the cursor advance (every CTA has read the cursor by then) — behind a
+// threadfence and an arrival counter it resets, one launch fewer per step.
 template <int MODE>
-__global__ void __launch_bounds__(256) k_row_tree_all(BlockArgs A, double* slot, int clear) { pdl_entry();
+__global__ void __launch_bounds__(256) k_row_tree_all(BlockArgs A, double* slot, int clear, unsigned* done_ticket) {
+  pdl_entry();
   __shared__ double wsl[8 * 256];
-  if (blk_skip(A)) return;
-  for (int q = threadIdx.x; q < 8 * 256; q += blockDim.x) wsl[q] = 0.0;
-  __syncthreads();
-  dev_row_tree_big<MODE>(A, slot, clear != 0, 0, wsl, true);
+  const bool skip = blk_skip(A);
+  if (!skip) {
+    for (int q = threadIdx.x; q < 8 * 256; q += blockDim.x) wsl[q] = 0.0;
+    __syncthreads();
+    dev_row_tree_big<MODE>(A, slot, clear != 0, 0, wsl, true);
+  }
+  if (done_ticket) {
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      last = atomicAdd(done_ticket, 1u) == gridDim.x - 1;
+      if (last) {
+        *done_ticket = 0u;
+        if (!skip) atomicAdd(A.dsteps, 1ULL);
+        if (A.cur) *A.cur += 1u;
+      }
+    }
+  }
 }
 template <int MODE>
 __global__ void __launch_bounds__(256) k_row_tree_big(BlockArgs A, double* slot, int clear, int pass) {

@@ -154,6 +154,7 @@ struct Solver {
   cudaGraphExec_t gexec = nullptr;       // captured block steps of the current solve call
   int gexec_steps = 0;
   int last_nslabs = 1;        // slabs of the last sweep
+  unsigned* done_ticket = nullptr;   // k_row_tree_all<1>'s arrival counter (zeroed; its last CTA resets it)
   // block-step workspace
   int64_t blk_L = 0, blk_P = 0;
   int *pcount = nullptr, *poff = nullptr, *ptotal = nullptr, *prow = nullptr, *ppos = nullptr;
@@ -1430,15 +1431,18 @@ sro_status plain_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
     CUDA_TRY(s, launch_pdl(k_pairs_gen, dim3(gL), dim3(tpb), 0, s->stream, A));
     CUDA_TRY(s, launch_pdl(k_touched_scan, dim3(1), dim3(1024), 0, s->stream, A));
     CUDA_TRY(s, launch_pdl(k_runs, dim3(A.W), dim3(tpb), 0, s->stream, A, s->pd));
-    CUDA_TRY(s, launch_pdl(k_row_tree_all<0>, dim3(gR), dim3(256), 0, s->stream, A, nullptr, 0));
+    CUDA_TRY(s, launch_pdl(k_row_tree_all<0>, dim3(gR), dim3(256), 0, s->stream, A, nullptr, 0, (unsigned*)nullptr));
     CUDA_TRY(s, launch_pdl(k_den_gamma, dim3(1), dim3(256), 0, s->stream, A));
     CUDA_TRY(s, launch_pdl(k_cap_check, dim3(gL), dim3(tpb), 0, s->stream, A));
     CUDA_TRY(s, launch_pdl(k_update_cols, dim3(gL), dim3(tpb), 0, s->stream, A));
     CUDA_TRY(s, launch_pdl(k_runs, dim3(A.W), dim3(tpb), 0, s->stream, A, s->pdelta));
-    CUDA_TRY(s, launch_pdl(k_row_tree_all<1>, dim3(gR), dim3(256), 0, s->stream, A, nullptr, 1));
-    CUDA_TRY(s, launch_pdl(k_step_done, dim3(1), dim3(32), 0, s->stream, A));
+    if (!s->done_ticket) {
+      CUDA_TRY(s, salloc(&s->done_ticket, 1, s->stream));
+      CUDA_TRY(s, cudaMemsetAsync(s->done_ticket, 0, sizeof(unsigned), s->stream));
+    }
+    CUDA_TRY(s, launch_pdl(k_row_tree_all<1>, dim3(gR), dim3(256), 0, s->stream, A, nullptr, 1, s->done_ticket));   // + k_step_done
     CUDA_TRY(s, cudaGetLastError());
-    s->lead->stats.kernel_launches += 12;
+    s->lead->stats.kernel_launches += 11;
   }
   s->lead->stats.block_steps += 1;
   s->lead->k_pending += 1;
@@ -1484,7 +1488,7 @@ sro_status shard_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
       k_pairs_gen<<<gL, tpb, 0, s->stream>>>(A);
       k_touched_scan<<<1, 1024, 0, s->stream>>>(A);
       k_runs<<<A.W, tpb, 0, s->stream>>>(A, t->pd);
-      k_row_tree_all<2><<<gR, 256, 0, s->stream>>>(A, s1, 0);
+      k_row_tree_all<2><<<gR, 256, 0, s->stream>>>(A, s1, 0, nullptr);
       k_publish_a<<<1, 32, 0, s->stream>>>(A);
       s->stats.kernel_launches += 9;
     }
@@ -1506,7 +1510,7 @@ sro_status shard_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
       k_zero_slot<<<gR, 256, 0, s->stream>>>(A, s2);
       k_update_cols<<<gL, tpb, 0, s->stream>>>(A);
       k_runs<<<A.W, tpb, 0, s->stream>>>(A, t->pdelta);
-      k_row_tree_all<2><<<gR, 256, 0, s->stream>>>(A, s2, 1);
+      k_row_tree_all<2><<<gR, 256, 0, s->stream>>>(A, s2, 1, nullptr);
       k_publish_b<<<1, 32, 0, s->stream>>>(A);
       s->stats.kernel_launches += 7;
     }
@@ -1598,7 +1602,7 @@ void free_shard(Solver* s) {
   void* aptrs[] = {s->visit, s->trace, s->part_j, s->part_min, s->pcount, s->poff, s->ptotal, s->prow, s->ppos, s->pd,
                    s->ptold, s->pdelta, s->runc, s->runv, s->rowcnt, s->rowidx, s->tstart, s->tcur, s->X,
                    s->trows, s->ntouch, s->capfail, s->bigw, s->nbig, s->st_cnt, s->st_row, s->st_val, s->st_b, s->st_term,
-                   s->ga_blk, s->dsteps, s->cur, s->phase, s->a, s->b, s->b_full, s->r, s->h, s->cnt, s->srow, s->sval, s->G_ga,
+                   s->done_ticket, s->ga_blk, s->dsteps, s->cur, s->phase, s->a, s->b, s->b_full, s->r, s->h, s->cnt, s->srow, s->sval, s->G_ga,
                    s->fen, s->status, s->steps_done, s->stop, s->scal, s->epsd, s->sw_j, s->sw_min, s->sw_g};
   if (s->stream) for (void* p : aptrs) sfree(p, s->stream);
   if (s->stream) stream_wait(s);
@@ -2241,7 +2245,7 @@ sro_status plan_row_sums(Solver* s, const double* y_dev, const int* chans, int n
     CUDA_TRY(s, cudaMemsetAsync(out[c], 0, sizeof(double) * s->m, s->stream));
     k_plan_channel<<<gP, tpb, 0, s->stream>>>(A, y_dev, chans[c], s->pdelta);
     k_runs<<<A.W, tpb, 0, s->stream>>>(A, s->pdelta);
-    k_row_tree_all<2><<<gR, 256, 0, s->stream>>>(A, out[c], c == nch - 1 ? 1 : 0);
+    k_row_tree_all<2><<<gR, 256, 0, s->stream>>>(A, out[c], c == nch - 1 ? 1 : 0, nullptr);
   }
   s->lead->stats.kernel_launches += 5 + 3 * nch;
   CUDA_TRY(s, cudaGetLastError());
