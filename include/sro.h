@@ -286,6 +286,19 @@ sro_status sro_kmeans(const uint8_t* pixels, int64_t npix, int32_t k, const int3
                       int32_t pixels_on_device, void* cuda_stream, double* centroids, int32_t* labels,
                       int64_t* counts, int32_t* iters, int32_t* converged);
 
+/* k-means++ seeding of sro_kmeans' init_idx (R34): k distinct pixel
+ * indices, centre 0 = min(floor(u[0] npix), npix - 1), centre t the first pixel whose inclusive
+ * prefix sum (pixel order) of D2 exceeds min(floor(u[t] * total), total - 1), where D2(p) is the
+ * squared RGB distance from pixel p to its nearest chosen centre (exact integers) and total their
+ * sum; total = 0 (every pixel repeats a chosen colour) takes the lowest index not yet chosen.
+ * pixels: uint8 npix x 3 (host, or device when pixels_on_device; borrowed for the call); u: host
+ * fp64[k], each in [0, 1) (the caller's random draw); init_idx: host int32[k] output. Runs on
+ * cuda_stream (NULL: the default stream) and returns after it has synchronised. Errors:
+ * INVALID_ARG (null pointers, k < 1 or > npix, u outside [0, 1)), DIMENSION (npix > 2^31 - 1),
+ * CUDA. */
+sro_status sro_kmeanspp(const uint8_t* pixels, int64_t npix, int32_t k, const double* u, int32_t pixels_on_device,
+                        void* cuda_stream, int32_t* init_idx);
+
 /* Recolouring: out_pixels[p] = clip(rint(255 * xhat[labels[p]]), 0, 255)
  * per channel. labels: host int32[npix] in [0, k); xhat: host fp64 k x 3 (e.g.
  * sro_barycentric's output); out_pixels: host uint8 npix x 3. Errors:

@@ -18,7 +18,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["kmeans_quantize", "sqdist", "colour_features", "recolour"]
+__all__ = ["kmeans_quantize", "kmeanspp_init", "sqdist", "colour_features", "recolour"]
 
 
 def sqdist(P: np.ndarray, C: np.ndarray) -> np.ndarray:
@@ -74,6 +74,40 @@ def kmeans_quantize(pixels: np.ndarray, k: int, init_idx: np.ndarray, max_iters:
             counts[c] = 1
             repaired = True
     return cen, labels, counts, it, converged
+
+
+def kmeanspp_init(pixels: np.ndarray, k: int, u: np.ndarray) -> np.ndarray:
+    """k-means++ seeding (reading R34 in DESIGN.md) of the k initial centres as pixel
+    indices, from k uniforms u in [0, 1) drawn by the caller:
+      c_0 = min(floor(u_0 N), N - 1);
+      D2(p) = min over the chosen centres c of ||P_p - P_c||^2 (8-bit pixels: exact integers);
+      c_t = the first p whose inclusive prefix sum of D2 (pixel order) exceeds
+            min(floor(u_t * total), total - 1), total = sum_p D2(p) (a D2-weighted draw);
+            if total == 0 (every pixel repeats a chosen colour) c_t = the lowest index not chosen.
+    Integer sums, so no summation order enters."""
+    P = np.asarray(pixels, dtype=np.uint8).astype(np.int64)
+    N = len(P)
+    u = np.asarray(u, dtype=np.float64)
+    out = np.empty(k, dtype=np.int32)
+    chosen = np.zeros(N, dtype=bool)
+    c = min(int(np.float64(u[0]) * np.float64(N)), N - 1)
+    D2 = None
+    for t in range(k):
+        if t > 0:
+            total = int(D2.sum())
+            if total == 0:
+                c = int(np.nonzero(~chosen)[0][0])
+            else:
+                target = int(np.float64(u[t]) * np.float64(total))   # one rounded product, then floor
+                target = min(target, total - 1)
+                prefix = np.cumsum(D2)
+                c = int(np.searchsorted(prefix, target, side="right"))   # first prefix > target
+        out[t] = c
+        chosen[c] = True
+        d = P - P[c]
+        dist = (d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2]
+        D2 = dist if D2 is None else np.minimum(D2, dist)
+    return out
 
 
 def colour_features(cen: np.ndarray, counts: np.ndarray, npix: int):

@@ -174,4 +174,125 @@ __global__ void k_km_recolour(const int32_t* __restrict__ labels, int64_t N, con
   }
 }
 
+// ---------------------------------------------------------------------------
+// k-means++ seeding (R34): D2(p) = min over the chosen centres of the
+// squared RGB distance (8-bit pixels: exact integers <= 3 x 255^2), the next centre the first pixel
+// whose inclusive prefix of D2 exceeds min(floor(u_t * total), total - 1). Integer sums: the
+// parallel order cannot change them.
+// ---------------------------------------------------------------------------
+constexpr int KPP_BLOCK = 4096;   // pixels per partial sum (and per k_kpp_update CTA)
+
+// D2 <- min(D2, d2(., centre)) (first: D2 = d2) over one 4096-pixel block per CTA; block sums.
+__global__ void __launch_bounds__(256) k_kpp_update(const uint8_t* __restrict__ px, int64_t N,
+                                                     const int32_t* __restrict__ centre, int first,
+                                                     int32_t* d2, long long* bsum) {
+  __shared__ long long red[8];
+  const int64_t b0 = (int64_t)blockIdx.x * KPP_BLOCK;
+  const int64_t c = *centre;
+  const int c0 = px[3 * c], c1 = px[3 * c + 1], c2 = px[3 * c + 2];
+  long long acc = 0;
+  for (int64_t p = b0 + threadIdx.x; p < N && p < b0 + KPP_BLOCK; p += 256) {
+    const int e0 = (int)px[3 * p] - c0, e1 = (int)px[3 * p + 1] - c1, e2 = (int)px[3 * p + 2] - c2;
+    int v = (e0 * e0 + e1 * e1) + e2 * e2;
+    if (!first) v = min(v, d2[p]);
+    d2[p] = v;
+    acc += v;
+  }
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long t = 0;
+    for (int w = 0; w < 8; w++) t += red[w];
+    bsum[blockIdx.x] = t;
+  }
+}
+
+// Exclusive prefix over x[0..n) by one CTA of 1024 threads: returns the index q of the element
+// whose [prefix, prefix + x_q) holds target (0 <= target < total), and that prefix in *base.
+__device__ __forceinline__ long long kpp_find(const long long* x, int64_t n, long long target, long long* base,
+                                              long long* sh) {
+  const int t = threadIdx.x;
+  const int64_t per = (n + 1023) / 1024;
+  const int64_t lo = min(n, t * per), hi = min(n, lo + per);
+  long long s = 0;
+  for (int64_t q = lo; q < hi; q++) s += x[q];
+  // inclusive scan of the 1024 thread sums
+  long long incl = s;
+  for (int o = 1; o < 32; o <<= 1) { const long long y = __shfl_up_sync(FULL, incl, o); if ((t & 31) >= o) incl += y; }
+  if ((t & 31) == 31) sh[t >> 5] = incl;
+  __syncthreads();
+  if (t < 32) {
+    long long w = sh[t];
+    for (int o = 1; o < 32; o <<= 1) { const long long y = __shfl_up_sync(FULL, w, o); if (t >= o) w += y; }
+    sh[t] = w;
+  }
+  __syncthreads();
+  const long long start = incl - s + ((t >> 5) ? sh[(t >> 5) - 1] : 0);
+  __shared__ long long res[2];
+  if (s > 0 && start <= target && target < start + s) {   // exactly one thread: its range holds target
+    long long run = start;
+    int64_t q = lo;
+    while (run + x[q] <= target) { run += x[q]; q++; }
+    res[0] = q;
+    res[1] = run;
+  }
+  __syncthreads();
+  *base = res[1];
+  const long long q = res[0];
+  __syncthreads();
+  return q;
+}
+
+// Centre t: from the block sums and D2 (one CTA of 1024 threads); the total-0 case takes the lowest
+// pixel not yet chosen.
+__global__ void __launch_bounds__(1024) k_kpp_pick(const int32_t* __restrict__ d2, int64_t N,
+                                                    const long long* __restrict__ bsum, int64_t nb,
+                                                    const double* __restrict__ u, int t, int32_t* centres,
+                                                    int32_t* centre, uint8_t* chosen) {
+  __shared__ long long sh[32];
+  __shared__ long long stot[1];
+  __shared__ int64_t sfirst;
+  const int tid = threadIdx.x;
+  long long s = 0;
+  for (int64_t q = tid; q < nb; q += 1024) s += bsum[q];
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+  if ((tid & 31) == 0) sh[tid >> 5] = s;
+  __syncthreads();
+  if (tid == 0) {
+    long long tot = 0;
+    for (int w = 0; w < 32; w++) tot += sh[w];
+    stot[0] = tot;
+    sfirst = N;
+  }
+  __syncthreads();
+  const long long total = stot[0];
+  int64_t pick;
+  if (total == 0) {
+    for (int64_t p = tid; p < N; p += 1024)
+      if (!chosen[p]) { atomicMin((unsigned long long*)&sfirst, (unsigned long long)p); break; }
+    __syncthreads();
+    pick = sfirst;
+  } else {
+    long long target = (long long)d_mul(u[t], (double)total);   // one rounded product, then floor
+    if (target > total - 1) target = total - 1;
+    long long base = 0;
+    const long long b = kpp_find(bsum, nb, target, &base, sh);
+    // within block b: the D2 values as long long, found the same way
+    __shared__ long long vals[KPP_BLOCK];
+    const int64_t p0 = b * KPP_BLOCK;
+    const int64_t cnt = min((int64_t)KPP_BLOCK, N - p0);
+    for (int64_t q = tid; q < cnt; q += 1024) vals[q] = d2[p0 + q];
+    __syncthreads();
+    long long base2 = 0;
+    const long long q = kpp_find(vals, cnt, target - base, &base2, sh);
+    pick = p0 + q;
+  }
+  if (tid == 0) {
+    centres[t] = (int32_t)pick;
+    *centre = (int32_t)pick;
+    chosen[pick] = 1;
+  }
+}
+
 }  // namespace sro

@@ -2451,6 +2451,62 @@ const char* sro_kmeans_error(void) { return g_km_err.c_str(); }
     if (e_ != cudaSuccess) { g_km_err = cudaGetErrorString(e_); st = SRO_ERR_CUDA; goto done; } \
   } while (0)
 
+// k-means++ seeding (R34): centre 0 = min(floor(u_0 N), N - 1) on the host, then per centre
+// one k_kpp_update (D2 and its 4096-pixel block sums) and one k_kpp_pick (the D2-weighted draw).
+sro_status sro_kmeanspp(const uint8_t* pixels, int64_t npix, int32_t k, const double* u, int32_t pixels_on_device,
+                        void* cuda_stream, int32_t* init_idx) {
+  g_km_err.clear();
+  if (!pixels || !u || !init_idx || npix < 1 || k < 1 || k > npix) { g_km_err = "bad argument"; return SRO_ERR_INVALID_ARG; }
+  if (npix > INT32_MAX) { g_km_err = "npix exceeds int32 pixel indices"; return SRO_ERR_DIMENSION; }
+  for (int t = 0; t < k; t++)
+    if (!(u[t] >= 0.0 && u[t] < 1.0)) { g_km_err = "u: k uniforms in [0, 1)"; return SRO_ERR_INVALID_ARG; }
+  sro_status st = SRO_OK;
+  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  const int64_t nb = (npix + KPP_BLOCK - 1) / KPP_BLOCK;
+  uint8_t *dpx = nullptr, *dch = nullptr;
+  int32_t *d2 = nullptr, *dcent = nullptr, *dcur = nullptr;
+  long long* bsum = nullptr;
+  double* du = nullptr;
+  int64_t c0 = (int64_t)(u[0] * (double)npix);   // one rounded product, then floor
+  if (c0 > npix - 1) c0 = npix - 1;
+  const int32_t c0i = (int32_t)c0;
+  const uint8_t one = 1;
+  const uint8_t* px = pixels;
+  if (!pixels_on_device) {
+    KM_TRY(cudaMallocAsync(&dpx, (size_t)3 * npix, stream));
+    KM_TRY(cudaMemcpyAsync(dpx, pixels, (size_t)3 * npix, cudaMemcpyHostToDevice, stream));
+    px = dpx;
+  }
+  KM_TRY(cudaMallocAsync(&d2, sizeof(int32_t) * npix, stream));
+  KM_TRY(cudaMallocAsync(&dch, (size_t)npix, stream));
+  KM_TRY(cudaMallocAsync(&bsum, sizeof(long long) * nb, stream));
+  KM_TRY(cudaMallocAsync(&du, sizeof(double) * k, stream));
+  KM_TRY(cudaMallocAsync(&dcent, sizeof(int32_t) * k, stream));
+  KM_TRY(cudaMallocAsync(&dcur, sizeof(int32_t), stream));
+  KM_TRY(cudaMemsetAsync(dch, 0, (size_t)npix, stream));
+  KM_TRY(cudaMemcpyAsync(du, u, sizeof(double) * k, cudaMemcpyHostToDevice, stream));
+  KM_TRY(cudaMemcpyAsync(dcur, &c0i, sizeof(int32_t), cudaMemcpyHostToDevice, stream));
+  KM_TRY(cudaMemcpyAsync(dcent, &c0i, sizeof(int32_t), cudaMemcpyHostToDevice, stream));
+  KM_TRY(cudaMemcpyAsync(dch + c0, &one, 1, cudaMemcpyHostToDevice, stream));
+  k_kpp_update<<<(unsigned)nb, 256, 0, stream>>>(px, npix, dcur, 1, d2, bsum);
+  KM_TRY(cudaGetLastError());
+  for (int t = 1; t < k; t++) {
+    k_kpp_pick<<<1, 1024, 0, stream>>>(d2, npix, bsum, nb, du, t, dcent, dcur, dch);
+    KM_TRY(cudaGetLastError());
+    if (t + 1 < k) {
+      k_kpp_update<<<(unsigned)nb, 256, 0, stream>>>(px, npix, dcur, 0, d2, bsum);
+      KM_TRY(cudaGetLastError());
+    }
+  }
+  KM_TRY(cudaMemcpyAsync(init_idx, dcent, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, stream));
+  KM_TRY(cudaStreamSynchronize(stream));
+done:
+  for (void* q : {(void*)dpx, (void*)d2, (void*)dch, (void*)bsum, (void*)du, (void*)dcent, (void*)dcur})
+    if (q) cudaFreeAsync(q, stream);
+  cudaStreamSynchronize(stream);
+  return st;
+}
+
 sro_status sro_kmeans(const uint8_t* pixels, int64_t npix, int32_t k, const int32_t* init_idx, int32_t max_iters,
                       int32_t pixels_on_device, void* cuda_stream, double* centroids, int32_t* labels,
                       int64_t* counts, int32_t* iters, int32_t* converged) {

@@ -13,7 +13,7 @@ import numpy as np
 __all__ = [
     "load_library", "Solver", "SroError", "SRO_FW", "SRO_BCFW", "SRO_BCAFW", "SRO_BCPFW", "SRO_BATCHED",
     "STEP_DEC", "STEP_ELS", "SAMPLE_U", "SAMPLE_P", "SAMPLE_GA", "TRACE_DTYPE", "EXPORTED_SYMBOLS",
-    "nccl_unique_id", "kmeans_quantize", "kmeans_features", "recolour", "colour_transfer",
+    "nccl_unique_id", "kmeans_quantize", "kmeanspp_init", "kmeans_features", "recolour", "colour_transfer",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -49,7 +49,8 @@ OK, NOT_CONVERGED = 0, 1
 EXPORTED_SYMBOLS = ("sro_create", "sro_solve", "sro_gap", "sro_objective", "sro_get_plan", "sro_get_rowsums",
                     "sro_reset", "sro_destroy", "sro_last_error", "sro_version", "sro_get_stats", "sro_set_timing",
                     "sro_held_columns", "sro_nccl_unique_id", "sro_barycentric", "sro_metrics",
-                    "sro_kmeans", "sro_recolour", "sro_kmeans_error", "sro_lp_metrics", "sro_kmeans_features")
+                    "sro_kmeans", "sro_recolour", "sro_kmeans_error", "sro_lp_metrics", "sro_kmeans_features",
+                    "sro_kmeanspp")
 
 _STATUS = {0: "OK", 1: "NOT_CONVERGED", 2: "ERR_INVALID_ARG", 3: "ERR_DIMENSION", 4: "ERR_MARGINALS",
            5: "ERR_NONFINITE", 6: "ERR_CAPACITY", 7: "ERR_CUDA", 8: "ERR_NCCL", 9: "ERR_OOM", 10: "ERR_STATE"}
@@ -151,6 +152,8 @@ def load_library():
         L.sro_metrics.restype = ct.c_int
         L.sro_kmeans.argtypes = [vp, i64, i32, vp, i32, i32, vp, vp, vp, vp, ct.POINTER(i32), ct.POINTER(i32)]
         L.sro_kmeans.restype = ct.c_int
+        L.sro_kmeanspp.argtypes = [vp, i64, i32, vp, i32, vp, vp]
+        L.sro_kmeanspp.restype = ct.c_int
         L.sro_recolour.argtypes = [vp, i64, vp, i32, vp, vp]
         L.sro_recolour.restype = ct.c_int
         L.sro_lp_metrics.argtypes = [vp, vp, vp, vp, i64, ct.POINTER(d), ct.POINTER(d)]
@@ -390,6 +393,25 @@ def kmeans_quantize(pixels, k: int, init_idx, max_iters: int = 100, stream=None)
     if st != OK:
         raise SroError(st, L.sro_kmeans_error().decode())
     return cen, lab, cnt, int(it.value), bool(conv.value)
+
+
+def kmeanspp_init(pixels, k: int, u, stream=None):
+    """sro_kmeanspp: k-means++ seeding (R34) of k distinct pixel indices from the caller's k uniforms
+    u in [0, 1) (numpy pixels, or a CUDA uint8 tensor, borrowed). Returns int32[k]."""
+    L = load_library()
+    on_dev = 1 if _is_cuda(pixels) else 0
+    if not on_dev:
+        pixels = np.ascontiguousarray(pixels, dtype=np.uint8)
+    npix = int(pixels.shape[0])
+    uu = np.ascontiguousarray(u, dtype=np.float64)
+    k = int(k)
+    if uu.shape[0] < max(k, 0):
+        raise SroError(2, "u needs k uniforms")
+    out = np.empty(max(k, 0), dtype=np.int32)
+    st = L.sro_kmeanspp(_ptr(pixels), npix, k, _ptr(uu), on_dev, ct.c_void_p(stream) if stream else None, _ptr(out))
+    if st != OK:
+        raise SroError(st, L.sro_kmeans_error().decode())
+    return out
 
 
 def kmeans_features(centroids, counts):

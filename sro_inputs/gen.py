@@ -18,7 +18,7 @@ __all__ = [
     "GOLDEN", "splitmix64_mix", "rng_u64", "uniform53", "normals",
     "uniform_colours", "mixture_colours", "density_weights", "uniform_weights",
     "sqeuclid_cost", "hash_uniform_cost", "instance", "CONFIGS",
-    "synthetic_image", "kmeans_init",
+    "synthetic_image", "kmeans_init", "kmeanspp_uniforms",
 ]
 
 GOLDEN = np.uint64(0x9E3779B97F4A7C15)
@@ -185,3 +185,11 @@ def kmeans_init(npix: int, k: int, seed: int) -> np.ndarray:
         perm[t], perm[r] = vr, vt
         out[t] = vr
     return out
+
+
+def kmeanspp_uniforms(k: int, seed: int) -> np.ndarray:
+    """The k uniforms in [0, 1) that k-means++ seeding consumes (one per centre), passed as an
+    input to both the oracle and the GPU (the draw itself is the method's; R34)."""
+    if k < 1:
+        raise ValueError("need k >= 1")
+    return uniform53(rng_u64(seed * 1000003 + 29, k))

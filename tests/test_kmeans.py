@@ -11,8 +11,8 @@ from fractions import Fraction
 import numpy as np
 import pytest
 
-from oracle.kmeans import colour_features, kmeans_quantize, recolour
-from sro_inputs import kmeans_init, synthetic_image
+from oracle.kmeans import colour_features, kmeans_quantize, kmeanspp_init, recolour
+from sro_inputs import kmeans_init, kmeanspp_uniforms, synthetic_image
 
 
 def test_k_distinct_colours_are_recovered_exactly():
@@ -176,3 +176,105 @@ def test_gpu_kmeans_features_match_oracle_and_reject_bad_input():
     for bad in (np.array([3, -1, 2]), np.zeros(3, dtype=np.int64)):
         with pytest.raises(sro.SroError):
             sro.kmeans_features(np.ones((3, 3)), bad)
+
+
+# ---- k-means++ seeding (R34) ----------------------------------------
+
+def _brute_d2(P, centres):
+    """min over the centres of the squared RGB distance, python integers (independent of the oracle)."""
+    out = []
+    for p in P:
+        out.append(min(sum((int(p[q]) - int(P[c][q])) ** 2 for q in range(3)) for c in centres))
+    return out
+
+
+def test_kmeanspp_oracle_draw_is_d2_weighted():
+    """Pin: the second centre is drawn with probability D2(p) / sum D2 — over a uniform grid of G values
+    of u_1 each pixel is chosen G * D2(p) / total times up to one per boundary."""
+    P = np.array([[0, 0, 0], [10, 0, 0], [0, 20, 0], [3, 4, 12], [255, 255, 255], [0, 0, 0], [7, 7, 7]], np.uint8)
+    u0 = 0.0   # first centre: pixel 0
+    d2 = _brute_d2(P, [0])
+    total = sum(d2)
+    G = 20000
+    counts = np.zeros(len(P), dtype=np.int64)
+    for g in range(G):
+        c = kmeanspp_init(P, 2, np.array([u0, (g + 0.5) / G]))
+        assert c[0] == 0
+        counts[c[1]] += 1
+    for p in range(len(P)):
+        assert abs(counts[p] - G * d2[p] / total) <= 1.0 + 1e-9, (p, counts[p], G * d2[p] / total)
+    assert counts[0] == 0 and counts[5] == 0   # D2 = 0: never drawn
+
+
+def test_kmeanspp_oracle_first_centre_and_edges():
+    P = synthetic_image(9, 11, seed=4).reshape(-1, 3)
+    N = len(P)
+    for u0 in (0.0, 0.3, 0.999999999):
+        c = kmeanspp_init(P, 1, np.array([u0]))
+        assert c[0] == min(int(u0 * N), N - 1)
+    # u_t = 0: the first pixel with D2 > 0 (the target 0 is exceeded by the first nonzero prefix)
+    c = kmeanspp_init(P, 3, np.array([0.5, 0.0, 0.0]))
+    d2 = _brute_d2(P, [c[0]])
+    assert c[1] == next(p for p in range(N) if d2[p] > 0)
+    d2 = _brute_d2(P, [c[0], c[1]])
+    assert c[2] == next(p for p in range(N) if d2[p] > 0)
+    # every centre is a pixel index, all distinct, and each later centre had D2 > 0 when drawn
+    u = kmeanspp_uniforms(12, 2)
+    c = kmeanspp_init(P, 12, u)
+    assert len(set(c.tolist())) == 12
+    for t in range(1, 12):
+        assert _brute_d2(P, c[:t].tolist())[c[t]] > 0
+
+
+def test_kmeanspp_oracle_fewer_colours_than_centres():
+    """Every pixel repeats one of three colours, k = 6: three centres of distinct colours, then (total D2
+    = 0) the lowest indices not yet chosen."""
+    base = np.array([[1, 2, 3], [200, 100, 0], [50, 50, 50]], np.uint8)
+    P = base[np.array([0, 1, 0, 2, 1, 1, 0, 2])]
+    c = kmeanspp_init(P, 6, np.array([0.4, 0.9, 0.1, 0.5, 0.5, 0.5]))
+    assert len({tuple(P[i]) for i in c[:3]}) == 3
+    rest = [p for p in range(len(P)) if p not in set(c[:3].tolist())][:3]
+    assert c[3:].tolist() == rest
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("h,w,k,seed", [(1, 1, 1, 0), (7, 13, 5, 1), (100, 100, 64, 2), (333, 517, 257, 3),
+                                        (1000, 1000, 128, 4)])
+def test_gpu_kmeanspp_bitexact(h, w, k, seed):
+    """k-means++ seeding on the GPU (sro_kmeanspp) equals the oracle's centre for centre."""
+    import paper_2103_05857_b200 as sro
+    img = synthetic_image(h, w, seed=seed).reshape(-1, 3)
+    k = min(k, len(img))
+    u = kmeanspp_uniforms(k, seed)
+    ref = kmeanspp_init(img, k, u)
+    got = sro.kmeanspp_init(img, k, u)
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.gpu
+def test_gpu_kmeanspp_degenerate_and_errors():
+    import paper_2103_05857_b200 as sro
+    base = np.array([[1, 2, 3], [200, 100, 0], [50, 50, 50]], np.uint8)
+    rng = np.random.default_rng(5)
+    P = base[rng.integers(0, 3, size=5000)]
+    u = kmeanspp_uniforms(9, 7)
+    assert np.array_equal(sro.kmeanspp_init(P, 9, u), kmeanspp_init(P, 9, u))
+    with pytest.raises(sro.SroError):
+        sro.kmeanspp_init(P, 0, u)
+    with pytest.raises(sro.SroError):
+        sro.kmeanspp_init(P[:4], 9, u)
+    with pytest.raises(sro.SroError):
+        sro.kmeanspp_init(P, 2, np.array([0.5, 1.0]))
+
+
+@pytest.mark.gpu
+def test_gpu_kmeans_from_kmeanspp_seeds_bitexact():
+    """Lloyd from k-means++ seeds: the GPU chain (sro_kmeanspp -> sro_kmeans) equals the oracle chain."""
+    import paper_2103_05857_b200 as sro
+    img = synthetic_image(120, 160, seed=6).reshape(-1, 3)
+    u = kmeanspp_uniforms(32, 6)
+    init = kmeanspp_init(img, 32, u)
+    ref = kmeans_quantize(img, 32, init, 50)
+    g_init = sro.kmeanspp_init(img, 32, u)
+    got = sro.kmeans_quantize(img, 32, g_init, 50)
+    assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1]) and np.array_equal(got[2], ref[2])
