@@ -448,7 +448,8 @@ def colour_transfer(src_pixels, ref_pixels, m: int, n: int, init_src, init_ref, 
     colours x with histogram a and the reference into n colours y with b (sro_kmeans),
     solve the semi-relaxed problem with C = ||x_k - y_i||_2 (or its square), project the
     source colours (Eq. 15, sro_barycentric) and recolour the source pixels (sro_recolour).
-    Returns (recoloured pixels, solve result dict, (x, a, y, b, xhat))."""
+    init_src / init_ref: m / n distinct pixel indices (k-means++ seeds from kmeanspp_init, or any
+    caller's draw). Returns (recoloured pixels, solve result dict, (x, a, y, b, xhat))."""
     cx, lx, ax_cnt, _, _ = kmeans_quantize(src_pixels, m, init_src, kmeans_iters)
     cy, _, by_cnt, _, _ = kmeans_quantize(ref_pixels, n, init_ref, kmeans_iters)
     x, a = kmeans_features(cx, ax_cnt)
