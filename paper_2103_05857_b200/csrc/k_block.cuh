@@ -734,9 +734,9 @@ __global__ void __launch_bounds__(256) k_row_tree_small(BlockArgs A, double* slo
   if (!blk_skip(A)) dev_row_tree_small<MODE>(A, slot, clear != 0, pass);
 }
 // Warp per touched row over every touched row (the multi-CTA path: one launch).
-// done_ticket (the unsharded step's last kernel): the last CTA to finish also does k_step_done's
-// work — the step count and the cursor advance (every CTA has read the cursor by then) — behind a
-// threadfence and an arrival counter it resets, one launch fewer per step.
+// done_ticket (the unsharded step's last kernel): the last CTA to finish also ends the step — the
+// step count and the cursor advance (every CTA has read the cursor by then) — behind a threadfence
+// and an arrival counter it resets, one launch fewer per step.
 template <int MODE>
 __global__ void __launch_bounds__(256) k_row_tree_all(BlockArgs A, double* slot, int clear, unsigned* done_ticket) {
   pdl_entry();
@@ -769,7 +769,6 @@ __global__ void __launch_bounds__(256) k_row_tree_big(BlockArgs A, double* slot,
   __syncthreads();
   dev_row_tree_big<MODE>(A, slot, clear != 0, pass, wsl);
 }
-__global__ void k_gamma(BlockArgs A) { pdl_entry(); if (!blk_skip(A)) dev_gamma(A); }
 // The denominator psum256 of Delta_k^2 over the m rows and gamma in one launch (unsharded multi-CTA
 // step; thread 0 writes scal[1] and reads it back for gamma). One CTA of 256 threads.
 __global__ void __launch_bounds__(256) k_den_gamma(BlockArgs A) { pdl_entry();
@@ -799,10 +798,6 @@ __global__ void __launch_bounds__(256) k_psum256(const double* __restrict__ x, i
   dev_psumW_any(x, L, 256, out, eps, stop_flag);
 }
 
-__global__ void k_step_done(BlockArgs A) { pdl_entry();
-  if (!blk_skip(A) && threadIdx.x == 0) atomicAdd(A.dsteps, 1ULL);
-  if (A.cur && threadIdx.x == 0) *A.cur += 1u;   // the step's last kernel advances the cursor
-}
 
 // Single-CTA kernels: take the cursor's values once, then advance it (every
 // thread has read it before thread 0 writes).

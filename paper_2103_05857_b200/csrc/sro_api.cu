@@ -1440,7 +1440,7 @@ sro_status plain_block_step(Solver* s, const int* col0_dev, int col0_mul, int L,
       CUDA_TRY(s, salloc(&s->done_ticket, 1, s->stream));
       CUDA_TRY(s, cudaMemsetAsync(s->done_ticket, 0, sizeof(unsigned), s->stream));
     }
-    CUDA_TRY(s, launch_pdl(k_row_tree_all<1>, dim3(gR), dim3(256), 0, s->stream, A, nullptr, 1, s->done_ticket));   // + k_step_done
+    CUDA_TRY(s, launch_pdl(k_row_tree_all<1>, dim3(gR), dim3(256), 0, s->stream, A, nullptr, 1, s->done_ticket));   // + the step count and cursor advance
     CUDA_TRY(s, cudaGetLastError());
     s->lead->stats.kernel_launches += 11;
   }
