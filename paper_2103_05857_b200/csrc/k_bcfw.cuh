@@ -55,6 +55,7 @@ struct BcfwArgs {
   int a_smem;            // a staged in shared memory
   int visit_smem;        // the segment's visit list staged in shared memory
   int dbg;               // timing experiments only (SRO_DBG): 1 = skip the serial part, 2 = skip the LMO
+  int spec;              // GA pipe: speculative next column prefetched and pre-scanned; 0 = off (SRO_NO_SPEC)
   const int* halt;       // device flag: set -> the segment is a no-op (it was enqueued ahead of
                          // the host's check of the previous one, which converged or failed)
 };

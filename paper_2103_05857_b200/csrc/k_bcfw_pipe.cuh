@@ -410,18 +410,32 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_pipe(BcfwArgs A, const
 // Per step: draw (warp 0) -> column index to the LMO warps (BAR_COL) -> the
 // support mask (BAR_MASK) -> partials (BAR_PART) -> serial part, gap refresh,
 // Fenwick update (warp 0).
-// ---------------------------------------------------------------------------
+// Speculation (A.spec): while warp 0 runs the merge, serial part, gap refresh
+// and Fenwick update of step s, the LMO warps would idle. Instead one of them
+// draws a candidate next column i' from the tree as it stands (before step s's
+// refresh: the drawn column about two times in three on config [1]), reads its
+// support S' (step s changes no column but i_s; i' = i_s is not pre-scanned)
+// and prefetches its slab lines for warp 0 into L1; all LMO warps load column
+// i' and, once warp 0 has published T_s = supp(t_{i_s}) U {j_s} (the only rows
+// whose h step s changes), pre-scan it over the rows outside S' U T_s, whose h
+// is already final. If the draw gives i', each thread only adds its rows of
+// T_s \ S' with the updated h, ordered by (value, row), which is exactly the
+// first minimum and the second smallest value the ascending scan would find;
+// else the full scan runs as before. Every value is the one without speculation.
 constexpr int BAR_COL = 3;
-// The GA kernel has no slab prefetch to overlap: its column scan is on the
-// critical path, so every warp but warp 0 scans (warp 0 shares its SMSP with
-// three of them; it waits at BAR_PART while they scan).
-constexpr int GA_LMO_WARPS = PIPE_THREADS / 32 - 1;
+constexpr int BAR_SPEC = 4;   // LMO warps only: the speculative next column (misc[4]) and its support mask
+constexpr int BAR_T = 5;      // T of the step published (warp 0 arrives, LMO warps wait; speculation only)
+// The LMO warps are the 12 with w % 4 != 0, as in k_bcfw_pipe: warp 0 has its SM
+// sub-partition to itself, so the speculative pre-scan that runs during its
+// serial part takes none of its issue slots (15 scanning warps, three of them
+// beside warp 0, measured 3.09 us per step against 2.96 without speculation).
+constexpr int GA_LMO_WARPS = PIPE_LMO_WARPS;
 constexpr int GA_LMO = GA_LMO_WARPS * 32;
 constexpr int GA_SYNC = GA_LMO + 32;
 
 struct GaPipeLayout {
   __host__ __device__ static size_t fixed() {
-    return 256 * 8 + 16 * 4 * 8 + 16 * 4 * 4 + 16 * 4 + GA_LMO * 4;   // slots, key partials, row partials, misc, masks
+    return 256 * 8 + 16 * 4 * 8 + 16 * 4 * 4 + 16 * 4 + 3 * GA_LMO * 4;   // slots, key partials, row partials, misc, 3 masks
   }
   // a_smem / gs_smem: a and the stored gaps in shared memory (else read from / written to
   // global memory: a is read for the touched rows only, the stored gap once per step
@@ -456,6 +470,8 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
   int* pj = reinterpret_cast<int*>(p); p += 16 * 4 * 4;                               // [4][16] rows
   volatile int* misc = reinterpret_cast<volatile int*>(p); p += 16 * 4;   // [0] = column, [2] = abort
   unsigned* mflag = reinterpret_cast<unsigned*>(p); p += GA_LMO * 4;
+  unsigned* mflagT = reinterpret_cast<unsigned*>(p); p += GA_LMO * 4;   // T of the step (speculation)
+  unsigned* mflagS = reinterpret_cast<unsigned*>(p); p += GA_LMO * 4;   // support of the speculative column
   double* sh_h = reinterpret_cast<double*>(p); p += rup16((size_t)m * 8);
   double* sh_r = reinterpret_cast<double*>(p); p += rup16((size_t)m * 8);
   double* sh_a = GSM ? reinterpret_cast<double*>(p) : const_cast<double*>(A.a);
@@ -475,39 +491,27 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
   }
   for (int c = tid; c < n; c += PIPE_THREADS) { sh_cnt[c] = A.cnt[c]; if (GSM) Gs[c] = A.G[c]; }
   for (int c = tid; c <= n; c += PIPE_THREADS) fens[c] = A.fen[c];
-  for (int c = tid; c < GA_LMO; c += PIPE_THREADS) mflag[c] = 0;
-  if (tid == 0) { misc[0] = 0; misc[2] = 0; }
+  for (int c = tid; c < GA_LMO; c += PIPE_THREADS) { mflag[c] = 0; mflagT[c] = 0; mflagS[c] = 0; }
+  if (tid == 0) { misc[0] = 0; misc[2] = 0; misc[4] = -1; }
   __syncthreads();
 
-  if (steps > 0 && warp > 0) {
+  if (steps > 0 && warp > 0 && (warp & 3) != 0) {
     // =================== LMO warps ===================
-    const int lw = warp - 1;
-    // logical LMO thread index: the first 64 (which get a third vector when m = 4096)
-    // go to warps 4 and 8, so every SM sub-partition scans the same number of vectors
-    const int rank = lw == 3 ? 0 : (lw == 7 ? 1 : (lw < 3 ? lw + 2 : (lw < 7 ? lw + 1 : lw)));
-    const int lt = rank * 32 + lane;
+    const int lw = warp - 1 - (warp >> 2);   // 0..11; sub-partition lw % 3 + 1
+    const int lt = lw * 32 + lane;
     const int kt = nvec * W + lt;
     PipeCol<T, MAXV, GA_LMO> col;
     col.C = Cg; col.ld = ld; col.m = m; col.nvec = nvec;
-    for (int t = 0; t < steps; t++) {
-      nbar_sync(BAR_COL, GA_SYNC);                   // the drawn column (or abort)
-      if (misc[2]) break;
-      const int i = misc[0];
-      col.fetch(i, lt);
-      col.advance();
-      nbar_sync(BAR_MASK, GA_SYNC);                  // its support as a mask
-      const unsigned mk = mflag[lt];
-      mflag[lt] = 0;
-#ifdef SRO_PHASE_TIMING
-      long long lt0 = clock64() + (long long)(mk & 0u);
-#endif
-      // rows outside the support only: smallest (value, row) with its C, and the
-      // second smallest value (the support rows are warp 0's: it holds their C)
-      // (only warps holding a support row run the variant with the mask tests)
-      double u1 = dinf(), u2 = dinf();
-      T c1 = T(0);
-      int j1 = 0x7fffffff;
-      auto scan = [&](auto masked_tag) {
+    int ispec = -1;     // the column held in col.cur from the speculative prefetch (-1: none)
+    bool pre = false;   // (pu1, pj1, pc1, pu2) hold the pre-scan of column ispec
+    double pu1 = 0.0, pu2 = 0.0;
+    T pc1 = T(0);
+    int pj1 = 0x7fffffff;
+    // two smallest (value, row) of this thread's rows outside the mask, rows ascending;
+    // the second as a value only
+    auto scan = [&](unsigned mk, double& u1, int& j1, T& c1, double& u2) {
+      u1 = dinf(); u2 = dinf(); c1 = T(0); j1 = 0x7fffffff;
+      auto go = [&](auto masked_tag) {
         constexpr bool MASKED = decltype(masked_tag)::value;
         auto visit = [&](T c, double h, int k, bool masked) {
           const double x = d_add((double)c, h);
@@ -536,8 +540,78 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
         }
         if (kt < m) visit(col.ctail, sh_h[kt], kt, mk >> 31);
       };
-      if (__any_sync(FULL, mk != 0u)) scan(std::true_type{});
-      else scan(std::false_type{});
+      if (__any_sync(FULL, mk != 0u)) go(std::true_type{});
+      else go(std::false_type{});
+    };
+#ifdef SRO_PHASE_TIMING
+    long long sp_t = 0;
+#endif
+    for (int t = 0; t < steps; t++) {
+      nbar_sync(BAR_COL, GA_SYNC);                   // the drawn column (or abort)
+      if (misc[2]) break;
+      const int i = misc[0];
+      const bool hit = pre && i == ispec;
+#ifdef SRO_PHASE_TIMING
+      if (lane == 0 && lw == 0 && A.phase && t > 0) {
+        atomicAdd((unsigned long long*)&A.phase[21], (unsigned long long)(clock64() - sp_t));
+        atomicAdd((unsigned long long*)&A.phase[22], (unsigned long long)hit);
+        atomicAdd((unsigned long long*)&A.phase[23], (unsigned long long)pre);
+      }
+#endif
+      if (i != ispec) {
+        col.fetch(i, lt);
+        col.advance();
+      }
+      nbar_sync(BAR_MASK, GA_SYNC);                  // its support as a mask
+      const unsigned mk = mflag[lt];
+      mflag[lt] = 0;
+      const unsigned mkT = mflagT[lt];               // T of the previous step (speculation only)
+      mflagT[lt] = 0;
+#ifdef SRO_PHASE_TIMING
+      long long lt0 = clock64() + (long long)(mk & 0u);
+#endif
+      // rows outside the support only: smallest (value, row) with its C, and the
+      // second smallest value (the support rows are warp 0's: it holds their C)
+      // (only warps holding a support row run the variant with the mask tests)
+      double u1, u2;
+      T c1;
+      int j1;
+      if (hit) {
+        // the pre-scan covered every row outside supp U T_prev with h as it is now;
+        // the rows of T_prev outside the support, with their updated h, join by
+        // (value, row) order, which is what the ascending scan's first minimum is
+        u1 = pu1; u2 = pu2; c1 = pc1; j1 = pj1;
+        const unsigned fx = mkT & ~mk;
+        if (__any_sync(FULL, fx != 0u)) {
+          auto visit = [&](T c, double h, int k, bool on) {
+            if (!on) return;
+            const double x = d_add((double)c, h);
+            if (x < u1 || (x == u1 && k < j1)) { u2 = u1; u1 = x; j1 = k; c1 = c; }
+            else if (x < u2) u2 = x;
+          };
+#pragma unroll
+          for (int u = 0; u < MAXV; u++) {
+            const int q = lt + u * GA_LMO;
+            const unsigned mu = fx >> (u * W);
+            if (q < nvec && (mu & ((1u << W) - 1u))) {
+              double hv[W];
+              pipe_h(hp, nvec, q, col.cur, hv);
+              if constexpr (W == 4) {
+                visit(col.cur[u].x, hv[0], W * q, mu & 1u);
+                visit(col.cur[u].y, hv[1], W * q + 1, mu & 2u);
+                visit(col.cur[u].z, hv[2], W * q + 2, mu & 4u);
+                visit(col.cur[u].w, hv[3], W * q + 3, mu & 8u);
+              } else {
+                visit(col.cur[u].x, hv[0], W * q, mu & 1u);
+                visit(col.cur[u].y, hv[1], W * q + 1, mu & 2u);
+              }
+            }
+          }
+          if (kt < m && (fx >> 31)) visit(col.ctail, sh_h[kt], kt, true);
+        }
+      } else {
+        scan(mk, u1, j1, c1, u2);
+      }
 #ifdef SRO_PHASE_TIMING
       long long lt1 = clock64() + (long long)(j1 & 0);
 #endif
@@ -558,6 +632,59 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
       if (lane == 0 && (lw == 0 || lw == GA_LMO_WARPS - 1) && A.phase) {
         atomicAdd((unsigned long long*)&A.phase[lw == 0 ? 16 : 18], (unsigned long long)(lt1 - lt0));
         atomicAdd((unsigned long long*)&A.phase[lw == 0 ? 17 : 19], (unsigned long long)(lt2 - lt1));
+      }
+#endif
+      pre = false;
+      ispec = -1;
+#ifdef SRO_PHASE_TIMING
+      sp_t = clock64();
+#endif
+      if (A.spec && t + 1 < steps) {
+        // speculative next draw from the tree as it stands (warp 0 may be updating
+        // it: any node value read is an old or a new one; the result only decides
+        // what to prefetch and pre-scan)
+        if (lw == 0) {
+          int ic = 0;
+          if (lane == 0) {
+            ic = ga_draw_sh(fens, Gs, n, uniform53(rng_u64(A.seed, 1, (uint64_t)(A.k0 + t + 1))));
+            misc[4] = ic;
+          }
+          ic = __shfl_sync(FULL, ic, 0);
+          if (ic != i) {
+            // its support (step t does not touch column ic) -> mflagS; its slab lines
+            // (warp 0's first loads after the draw) into L1
+            const int cs = sh_cnt[ic];
+            for (int q = lane; q < cs; q += 32) {
+              int ot;
+              unsigned bit;
+              pipe_owner<W, GA_LMO>(A.srow[(int64_t)ic * cap + q], nvec, ot, bit);
+              atomicOr(&mflagS[ot], bit);
+            }
+            const char* pl = nullptr;
+            if (lane == 0) pl = reinterpret_cast<const char*>(A.srow + (int64_t)ic * cap);
+            else if (lane <= 2 && (lane - 1) * 16 < cs) pl = reinterpret_cast<const char*>(A.sval + (int64_t)ic * cap + (lane - 1) * 16);
+            else if (lane == 3) pl = reinterpret_cast<const char*>(A.b + ic);
+            if (pl) asm volatile("prefetch.global.L1 [%0];" ::"l"(pl));
+          }
+        }
+        nbar_sync(BAR_SPEC, GA_LMO);
+        ispec = misc[4];
+        col.fetch(ispec, lt);
+        const unsigned mkS = mflagS[lt];
+        mflagS[lt] = 0;
+        nbar_sync(BAR_T, GA_SYNC);                    // T_t = supp(t_i) U {j} published by warp 0
+        col.advance();
+        if (ispec != i) {
+          // rows outside supp(t_ispec) U T_t: their h is final for step t+1
+          scan(mkS | mflagT[lt], pu1, pj1, pc1, pu2);
+          pre = true;
+        }
+      }
+#ifdef SRO_PHASE_TIMING
+      if (lane == 0 && lw == 0 && A.phase) {
+        const long long t2 = clock64();
+        atomicAdd((unsigned long long*)&A.phase[20], (unsigned long long)(t2 - sp_t));
+        sp_t = t2;
       }
 #endif
     }
@@ -637,6 +764,17 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bcfw_ga_pipe(BcfwArgs A, co
       double mC = __shfl_sync(FULL, cw, src);
       if (!j_in && lane == ins) { mrow = j; mC = cj; }
       const int M = c0 + (j_in ? 0 : 1);
+      if (A.spec && s + 1 < steps) {
+        // T to the LMO warps: their pre-scan of the speculative next column skips these rows
+        if (lane < M) {
+          int ot;
+          unsigned bit;
+          pipe_owner<W, GA_LMO>(mrow, nvec, ot, bit);
+          atomicOr(&mflagT[ot], bit);
+        }
+        __syncwarp();
+        nbar_arrive(BAR_T, GA_SYNC);
+      }
       // ---- the serial part
       PW_MARK(4);
       const StepOut o = serial_step<VAR, true>(A, kk, i, j, mv, bi, c0, rw, tv, gk, sh_r, sh_h, nullptr, sh_a, sh_cnt,

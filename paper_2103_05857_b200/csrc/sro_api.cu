@@ -1092,6 +1092,7 @@ sro_status bcfw_segment(Solver* s, int variant, const sro_options* o, int steps,
   A.status = s->status; A.steps_done = s->steps_done; A.trace = dtrace;
   A.phase = s->phase;
   A.dbg = getenv("SRO_DBG") ? atoi(getenv("SRO_DBG")) : 0;
+  A.spec = getenv("SRO_NO_SPEC") ? 0 : 1;   // A/B: SRO_NO_SPEC turns the GA pipe's speculative pre-scan off
   const bool ga = o->sampling == SRO_SAMPLE_GA;
   { sro_status st = ensure_cmax(s); if (st) return st; }
   A.cmax = s->cmax;

@@ -23,3 +23,6 @@ steps = 4096 * 4
 print("ga warp0 cycles/step", round(ph[:8].sum() / steps, 1), {n: round(float(v) / steps, 1) for n, v in zip(names, ph[:8])})
 print("LMO warp 1: scan", round(ph[16] / steps, 1), "reduce+arrive", round(ph[17] / steps, 1),
       "| last LMO warp: scan", round(ph[18] / steps, 1), "reduce+arrive", round(ph[19] / steps, 1))
+print("LMO warp 1 speculation: draw + fetch + pre-scan", round(ph[20] / steps, 1), "then waiting for the next column",
+      round(ph[21] / steps, 1), "| pre-scanned", round(ph[23] / steps, 3), "hits", round(ph[22] / steps, 3),
+      "| SRO_NO_SPEC" if os.environ.get("SRO_NO_SPEC") else "")
