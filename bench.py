@@ -426,6 +426,10 @@ def sweep_roofline_config3(local_rank, peaks, sweeps=3):
                           f"{ach / 8000.0:.3f}, against the read-only stream microbenchmark (7.3 TB/s, "
                           f"profiles/r01_microbench.jsonl) {ach / 7300.0:.3f}"),
             "algorithmic_bytes_per_launch": byts, "avg_launch_ms": round(per_ms, 4), "sweeps_timed": sweeps,
+            "traffic": 17181008000.0 + 16534016.0,
+            "traffic_source": ("ncu --set full dram__bytes_read.sum + dram__bytes_write.sum of one k_lmo_sweep_bulk "
+                               "launch on this workload, closing round-2 build "
+                               "(profiles/r02_ncu_sweep3.md): 1.0010 x the algorithmic bytes"),
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, of measured)",
             "fw_els_time_to_gap_ms": round(r["device_ms"], 3), "fw_els_iterations": r["iters_done"],
             "fw_els_converged": bool(r["converged"]), "fw_gap": r["gap"],
